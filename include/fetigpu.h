@@ -1,0 +1,153 @@
+/*
+ * fetigpu.h — C-ABI of the B200-native range-space Schur solve
+ * (two complex-symmetric FETI-DP(H) solves on K -/+ i*phi^-1/2*M).
+ *
+ * Plain C types only (no torch / CUDA types in any signature).  Complex vectors are
+ * interleaved (re, im) doubles, i.e. C99 `double _Complex` / std::complex<double>.
+ * Vector orderings are the reference's: free dofs in ascending mesh-dof order
+ * (fem.cpp:142-150), constrained dofs likewise, multipliers ascending by (node, comp)
+ * (feti.cpp:69-81).
+ *
+ * Each entry point names the reference interface it replaces.
+ */
+#ifndef FETIGPU_H
+#define FETIGPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes.  Mirror the reference's exception taxonomy (csr.hpp:24-36):
+ *   FETIGPU_CONTRACT  <-> ContractError  (std::invalid_argument; python ValueError)
+ *   FETIGPU_NUMERICAL <-> NumericalError (std::runtime_error;    python RuntimeError)
+ * Non-convergence is NOT an error (krylov.hpp:97-100): rc 0 with converged = 0. */
+#define FETIGPU_OK 0
+#define FETIGPU_CONTRACT 1
+#define FETIGPU_NUMERICAL 2
+#define FETIGPU_RUNTIME 3 /* CUDA runtime failure, no device, or extension missing */
+
+typedef struct fetigpu_ctx fetigpu_ctx; /* opaque: owns device memory, stream, factors */
+
+/* Problem + solver description.  Replaces the pieces of ControlProblem
+ * (control.hpp:15-31), Physics (fem.hpp:20-30), FetiConfig (feti.hpp:22-30) and
+ * FactorSolverConfig (control.hpp:99-104) that the FetiDp path consumes. */
+typedef struct {
+  int n_x, n_y;          /* elements per axis, build_rectangle_mesh (mesh.cpp:7) */
+  double len_x, len_y;   /* extents; elements must be square (mesh.cpp:13-15) */
+  int physics;           /* 0 = heat, whole-boundary Dirichlet (fem.cpp:121-122)
+                            1 = plane strain, clamped x = 0 (fem.cpp:124-128) */
+  double young, poisson; /* plane strain material (fem.cpp:46-58) */
+  int s_x, s_y;          /* subdomain grid (FetiConfig::s_x/s_y) */
+  double phi;            /* > 0: operator factor is K + c V, c = -i/sqrt(phi)
+                            (build_complex_factors, control.cpp:113-120) */
+  double mass_coeff_re;  /* used only when phi == 0: c = mass_coeff (feti_solve(),   */
+  double mass_coeff_im;  /*   bindings.cpp:158-185); schur_solve then rejected      */
+  double tol;            /* relative dual residual (FetiConfig::tol, feti.hpp:26) */
+  int max_iter;          /* FetiConfig::max_iter; GMRES is unrestarted (feti.cpp:684) */
+  int augment;           /* edge-RBM augmentation: must be 0 (FETIGPU_CONTRACT otherwise) */
+  int device;            /* CUDA device ordinal */
+} fetigpu_desc;
+
+/* FetiStats (feti.hpp:95-103) + SolveStats (krylov.hpp:14-19). */
+typedef struct {
+  int iterations;
+  int converged;
+  double relative_residual;
+  double primal_residual;
+  double interface_jump;
+  int n_lambda;
+  int coarse_dim;
+  double setup_seconds;
+  double solve_seconds;
+} fetigpu_feti_stats;
+
+/* RangeSpaceResult (control.hpp:140-147). plus = K + cV, minus = K - cV. */
+typedef struct {
+  fetigpu_feti_stats plus;
+  fetigpu_feti_stats minus;
+  double imag_leak;
+  int imag_leak_warning;
+  int converged;
+  double factor_setup_seconds;
+  double solve_seconds;
+} fetigpu_schur_stats;
+
+/* ---- host-only queries (no GPU needed) ------------------------------------------- */
+
+/* info[0..9] = n_free, n_constrained, n_subdomains, n_corner_dofs, n_lambda, n_edges,
+ *              ex, ey, dofs_per_node, band half-width of A_ii.
+ * Replaces partition_structured (feti.cpp:34-169) + assemble_operators sizes. */
+int fetigpu_problem_info(const fetigpu_desc* desc, int* info);
+
+/* Reference thermal target and boundary trace (fem.cpp:194-220): ybar (n_free),
+ * yc (n_constrained). Either pointer may be NULL. */
+int fetigpu_target_thermal(const fetigpu_desc* desc, double* ybar, double* yc);
+
+/* Seeded sine-mode target of BASELINE.json configs 1-3:
+ * ybar(x,y) = sum_k a_k sin(m_k pi x) sin(n_k pi y), mt19937_64(seed), Box-Muller a_k,
+ * m_k, n_k = 1 + rng() % mmax.  Sampled at the free nodes. */
+int fetigpu_target_sine(const fetigpu_desc* desc, unsigned long long seed, int modes, int mmax,
+                        double* ybar);
+
+/* ---- GPU context ----------------------------------------------------------------- */
+
+/* Partition + upload + factor once (K1-K4).  Replaces the two ComplexFactorSolver
+ * constructions of solve_range_space (control.cpp:303-304; feti.cpp:373-480): the
+ * conjugate factor K - cV = conj(K + cV) is never factored (conjugate reuse). */
+int fetigpu_create(const fetigpu_desc* desc, fetigpu_ctx** out);
+void fetigpu_destroy(fetigpu_ctx* ctx);
+
+/* Range-space Schur solve, HOST buffers (control.cpp:297-334; python
+ * solve_range_space, bindings.cpp:93-111).  ybar: n_free; yc: n_constrained or NULL
+ * (y_c = 0); outputs y, u, lambda: n_free each.  Copies in/out are inside the call. */
+int fetigpu_schur_solve(fetigpu_ctx* ctx, const double* ybar, const double* yc, double* y, double* u,
+                        double* lambda, fetigpu_schur_stats* stats);
+
+/* Same, DEVICE pointers (inputs already resident in HBM; results left on device). */
+int fetigpu_schur_solve_device(fetigpu_ctx* ctx, const double* d_ybar, const double* d_yc, double* d_y,
+                               double* d_u, double* d_lambda, fetigpu_schur_stats* stats);
+
+/* Single-factor FETI-DP solve (FetiSolver<Complex>::solve, feti.cpp:630-717; python
+ * feti_solve, bindings.cpp:158-185).  sign = +1: (K + cV) x = rhs; sign = -1:
+ * (K + conj(c) V) x = rhs.  rhs, x: n_free complex (interleaved), host buffers. */
+int fetigpu_feti_solve(fetigpu_ctx* ctx, int sign, const double* rhs_c128, double* x_c128,
+                       fetigpu_feti_stats* stats);
+
+/* Operator-level parity hooks on n_lambda complex vectors (host buffers):
+ * apply_dual_operator (feti.cpp:581-594), apply_dirichlet_preconditioner (597-627). */
+int fetigpu_apply_dual(fetigpu_ctx* ctx, int sign, const double* lam_c128, double* out_c128);
+int fetigpu_apply_precond(fetigpu_ctx* ctx, int sign, const double* r_c128, double* out_c128);
+
+/* ---- instrumentation --------------------------------------------------------------- */
+
+/* The cudaStream_t (as void*) every kernel of this context is launched on. */
+void* fetigpu_stream(fetigpu_ctx* ctx);
+
+/* Number of kernels this context has launched since creation (or the last reset). */
+long long fetigpu_launch_count(fetigpu_ctx* ctx, int reset);
+
+/* Per-kernel-class device time.  enable != 0 brackets every launch of the classes
+ * below with CUDA events on the context stream; read accumulates elapsed ms and
+ * launch counts since the last reset.  class ids: see FETIGPU_K_* below. */
+#define FETIGPU_K_PRECOND_GEMV 0 /* Dirichlet S_bb apply (K6)            */
+#define FETIGPU_K_DUAL_GEMV 1    /* local dual operator apply (K5)       */
+#define FETIGPU_K_COARSE 2       /* coarse gather + solve (K4)           */
+#define FETIGPU_K_LAMBDA 3       /* signed B / B^T gathers (K5/K6 tails) */
+#define FETIGPU_K_ORTHO 4        /* GMRES CGS2 + reductions (K7)         */
+#define FETIGPU_K_BAND 5         /* banded fwd/bwd substitution (K5)     */
+#define FETIGPU_K_GLOBAL 6       /* global stencils, mass solve (K8)     */
+#define FETIGPU_K_OTHER 7
+#define FETIGPU_K_COUNT 8
+int fetigpu_profile(fetigpu_ctx* ctx, int enable);
+int fetigpu_profile_read(fetigpu_ctx* ctx, double* ms, long long* launches, int reset);
+
+/* Algorithmic bytes per launch of a kernel class (the roofline numerator). */
+double fetigpu_class_bytes(fetigpu_ctx* ctx, int klass);
+
+/* Thread-local message of the last failing call. */
+const char* fetigpu_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FETIGPU_H */

@@ -1,0 +1,1051 @@
+// fetigpu.cu — context, setup pipeline, device GMRES driver and the C-ABI of
+// include/fetigpu.h.  Host control flow restates the reference:
+//   FetiSolver ctor       feti.cpp:373-480   -> Ctx::setup()
+//   eliminate             feti.cpp:516-556   -> Ctx::eliminate()
+//   apply_dual_operator   feti.cpp:581-594   -> Ctx::apply_dual()
+//   Dirichlet precond     feti.cpp:597-627   -> Ctx::apply_precond()
+//   FetiSolver::solve     feti.cpp:630-717   -> Ctx::feti_solve()
+//   gmres                 krylov.hpp:102-223 -> Ctx::gmres()
+//   solve_range_space     control.cpp:297-334 -> Ctx::schur_solve()
+// Only the factor K + cV is ever built: the reference's second factor K - cV is its
+// elementwise conjugate, so the second FETI solve is conj(FETI_+(conj(rhs))).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "band.cuh"
+#include "fetigpu.h"
+#include "host_core.hpp"
+#include "kernels.cuh"
+
+namespace fetigpu {
+
+using cd = std::complex<double>;
+static thread_local std::string g_last_error;
+
+#define CU(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      throw RuntimeError(std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call);   \
+  } while (0)
+
+static inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+static inline double2 d2(cd z) { return make_double2(z.real(), z.imag()); }
+
+// supported template band widths
+static int round_band(int w) {
+  const int opts[] = {4, 8, 16, 32, 64};
+  for (int o : opts)
+    if (w <= o) return o;
+  throw ContractError("band half-width " + std::to_string(w) + " exceeds the supported maximum 64");
+}
+
+struct ProfEvent {
+  cudaEvent_t a, b;
+  int klass;
+};
+
+struct Ctx {
+  fetigpu_desc desc{};
+  HostProblem P;
+  HostPartition H;
+  cudaStream_t stream = nullptr;
+  cd mc;       // mass coefficient of the factored operator K + mc V
+  double phi = 0;
+  SubLayout L{};
+  MeshLayout M{};
+  int Wt = 0, WCt = 0, nc = 0, nl = 0, n = 0, m = 0;
+  double setup_seconds = 0;
+  long long launches = 0;
+  std::vector<void*> allocs;
+  // profiling
+  bool prof = false;
+  std::vector<ProfEvent> pool;
+  size_t pool_used = 0;
+  double prof_ms[FETIGPU_K_COUNT] = {};
+  long long prof_n[FETIGPU_K_COUNT] = {};
+
+  // -------- device data
+  int *d_ldof = nullptr, *d_idof = nullptr, *d_bdof = nullptr, *d_blam = nullptr, *d_cglob = nullptr;
+  int *d_corner_dof = nullptr, *d_lam_lo = nullptr, *d_lam_hi = nullptr, *d_corner_slots = nullptr;
+  int *d_xkind = nullptr, *d_xa = nullptr, *d_xb = nullptr, *d_free_dofs = nullptr, *d_free_map = nullptr;
+  int *d_cons_map = nullptr, *d_n_i = nullptr, *d_n_b = nullptr, *d_status = nullptr;
+  double* d_bsign = nullptr;
+  double2 *d_colband = nullptr, *d_rowband = nullptr;
+  int *d_bi_idx = nullptr, *d_ib_idx = nullptr;
+  double2 *d_bi_val = nullptr, *d_ib_val = nullptr;
+  double2 *d_Sbb = nullptr, *d_Sinv = nullptr, *d_Aic = nullptr, *d_Abc = nullptr, *d_Acc = nullptr;
+  double2 *d_cpl_i = nullptr, *d_cpl_b = nullptr;
+  double2 *d_Cinv = nullptr;
+  // workspaces
+  double2 *d_fi = nullptr, *d_fb = nullptr, *d_fc = nullptr, *d_tb = nullptr, *d_yi = nullptr, *d_ri = nullptr;
+  double2 *d_u1b = nullptr, *d_gcp = nullptr, *d_g = nullptr, *d_z = nullptr, *d_wb = nullptr;
+  double2 *d_V = nullptr, *d_w = nullptr, *d_zl = nullptr, *d_t = nullptr, *d_lam = nullptr, *d_r = nullptr;
+  double2 *d_d = nullptr, *d_best = nullptr, *d_part = nullptr, *d_red = nullptr, *d_y = nullptr;
+  double2 *d_rhs = nullptr, *d_x = nullptr, *d_x2 = nullptr, *d_ax = nullptr;
+  double2 *d_api_rhs = nullptr, *d_api_x = nullptr;
+  double *d_in_ybar = nullptr, *d_in_yc = nullptr, *d_out_y = nullptr, *d_out_u = nullptr, *d_out_l = nullptr;
+  double *d_real0 = nullptr, *d_real1 = nullptr, *d_real2 = nullptr, *d_real3 = nullptr, *d_real4 = nullptr;
+  double2* h_pin = nullptr;
+  size_t ldv = 0;
+  int vcap = 0;  // basis vectors allocated
+  int mdot_blocks = 0, mdot_chunk = 0;
+  // mass solve (Kronecker tridiagonal)
+  double *d_mx_cp = nullptr, *d_mx_dinv = nullptr, *d_my_cp = nullptr, *d_my_dinv = nullptr;
+  double moff = 0;
+  int Lx = 0, Ly = 0;
+
+  ~Ctx() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& e : pool) {
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    for (void* p : allocs) cudaFree(p);
+    if (h_pin) cudaFreeHost(h_pin);
+    if (stream) cudaStreamDestroy(stream);
+  }
+
+  template <typename T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    CU(cudaMalloc(&p, count * sizeof(T)));
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <typename T>
+  T* upload(const std::vector<T>& v) {
+    T* p = alloc<T>(v.size());
+    if (!v.empty()) CU(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, stream));
+    return p;
+  }
+  template <typename T>
+  void zero(T* p, size_t count) {
+    CU(cudaMemsetAsync(p, 0, count * sizeof(T), stream));
+  }
+
+  // Every kernel launch goes through here: counts launches, optionally brackets the
+  // launch with CUDA events on the context stream, and surfaces launch errors.
+  template <typename F>
+  void launch(int klass, F&& f) {
+    ProfEvent* ev = nullptr;
+    if (prof) {
+      if (pool_used == pool.size()) {
+        ProfEvent e{};
+        CU(cudaEventCreate(&e.a));
+        CU(cudaEventCreate(&e.b));
+        pool.push_back(e);
+      }
+      ev = &pool[pool_used++];
+      ev->klass = klass;
+      CU(cudaEventRecord(ev->a, stream));
+    }
+    f();
+    CU(cudaGetLastError());
+    if (ev) CU(cudaEventRecord(ev->b, stream));
+    ++launches;
+  }
+  void prof_collect() {
+    if (!prof || pool_used == 0) return;
+    CU(cudaStreamSynchronize(stream));
+    for (size_t i = 0; i < pool_used; ++i) {
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, pool[i].a, pool[i].b));
+      prof_ms[pool[i].klass] += ms;
+      prof_n[pool[i].klass] += 1;
+    }
+    pool_used = 0;
+  }
+  void sync() { CU(cudaStreamSynchronize(stream)); }
+
+  // ------------------------------------------------------------------------ band solve
+  // In-place x = A_ii^-1 x for nrhs right-hand sides per subdomain (or for the coarse).
+  void band_solve(const double2* colband, const double2* rowband, int Wt_, int nmat, int nrow, double2* X,
+                  size_t x_sub_stride, size_t x_rhs_stride, int nrhs) {
+    const size_t bstride = (size_t)nrow * (Wt_ + 1);
+    auto go = [&](auto wtag, auto warps_tag, auto ch_tag, auto st_tag) {
+      constexpr int Wc = decltype(wtag)::value, WARPS = decltype(warps_tag)::value;
+      constexpr int CHc = decltype(ch_tag)::value, STc = decltype(st_tag)::value;
+      const size_t smem = band_solve_smem<Wc, WARPS, CHc, STc>();
+      auto kfn = k_band_solve<Wc, WARPS, CHc, STc>;
+      static bool attr_set = false;
+      if (!attr_set) {
+        CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+      }
+      dim3 grid(nmat, cdiv(nrhs, WARPS));
+      launch(FETIGPU_K_BAND, [&] {
+        kfn<<<grid, WARPS * 32, smem, stream>>>(colband, rowband, bstride, nrow, X, x_sub_stride, x_rhs_stride, nrhs);
+      });
+    };
+    using I = std::integral_constant<int, 0>;
+    (void)sizeof(I);
+#define BAND_CASE(WV)                                                                                  \
+  case WV:                                                                                             \
+    if (nrhs == 1)                                                                                     \
+      go(std::integral_constant<int, WV>{}, std::integral_constant<int, 1>{},                          \
+         std::integral_constant<int, 16>{}, std::integral_constant<int, 3>{});                         \
+    else                                                                                               \
+      go(std::integral_constant<int, WV>{}, std::integral_constant<int, 8>{},                          \
+         std::integral_constant<int, 32>{}, std::integral_constant<int, (WV > 32 ? 2 : 3)>{});         \
+    break;
+    switch (Wt_) {
+      BAND_CASE(4)
+      BAND_CASE(8)
+      BAND_CASE(16)
+      BAND_CASE(32)
+      BAND_CASE(64)
+      default:
+        throw ContractError("unsupported band width");
+    }
+#undef BAND_CASE
+  }
+
+  void band_ldlt(double2* colband, double2* rowband, int Wt_, int nmat, int nrow, int* status) {
+    const size_t stride = (size_t)nrow * (Wt_ + 1);
+    auto go = [&](auto wtag, int threads) {
+      constexpr int Wc = decltype(wtag)::value;
+      const size_t smem = (size_t)(Wc + 2) * (Wc + 1) * sizeof(double2);
+      static bool attr_set = false;
+      if (!attr_set) {
+        CU(cudaFuncSetAttribute(k_band_ldlt<Wc>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+      }
+      launch(FETIGPU_K_OTHER,
+             [&] { k_band_ldlt<Wc><<<nmat, threads, smem, stream>>>(colband, rowband, stride, nrow, status); });
+    };
+    switch (Wt_) {
+      case 4: go(std::integral_constant<int, 4>{}, 64); break;
+      case 8: go(std::integral_constant<int, 8>{}, 64); break;
+      case 16: go(std::integral_constant<int, 16>{}, 256); break;
+      case 32: go(std::integral_constant<int, 32>{}, 256); break;
+      case 64: go(std::integral_constant<int, 64>{}, 256); break;
+      default: throw ContractError("unsupported band width");
+    }
+  }
+
+  void check_status(int count, const char* what) {
+    std::vector<int> st(count);
+    CU(cudaMemcpyAsync(st.data(), d_status, count * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    for (int s = 0; s < count; ++s)
+      if (st[s] != 0) throw NumericalError(std::string("assemble_subdomain_operators: singular ") + what + " in subdomain " + std::to_string(s));
+  }
+
+  // ------------------------------------------------------------------------ setup
+  void setup() {
+    auto t0 = std::chrono::steady_clock::now();
+    CU(cudaSetDevice(desc.device));
+    CU(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    n = P.n();
+    m = P.m();
+    nc = H.n_corner;
+    nl = H.n_lambda;
+    Wt = round_band(std::max(H.W, 1));
+    WCt = round_band(std::max(H.WC, 1));
+    if (H.MAXE_BI > MAXE || H.MAXE_IB > MAXE) throw ContractError("ELL width exceeds kernel capacity");
+    if (H.NC > 8) throw ContractError("more than 8 corner dofs per subdomain");
+    if (H.NB > 4096) throw ContractError("too many interface dofs per subdomain");
+    L = SubLayout{H.n_sub, H.nld, H.ex, H.ey, H.dpn, H.NI, H.NB, H.NC, Wt, H.MAXE_BI, H.MAXE_IB};
+    M = MeshLayout{P.nx, P.ny, P.dpn};
+    const int S = H.n_sub, NI = H.NI, NB = H.NB, NC = H.NC, LD = Wt + 1;
+
+    // element matrices -> constant memory
+    {
+      double2 ae[64];
+      const int ed = P.edofs;
+      for (int q = 0; q < ed * ed; ++q) ae[q] = d2(cd(P.ke[q]) + mc * P.me[q]);
+      CU(cudaMemcpyToSymbolAsync(c_Ae, ae, sizeof(double2) * ed * ed, 0, cudaMemcpyHostToDevice, stream));
+      CU(cudaMemcpyToSymbolAsync(c_Ke, P.ke, sizeof(double) * ed * ed, 0, cudaMemcpyHostToDevice, stream));
+      CU(cudaMemcpyToSymbolAsync(c_Me, P.me, sizeof(double) * ed * ed, 0, cudaMemcpyHostToDevice, stream));
+    }
+    // index tables
+    d_ldof = upload(H.ldof);
+    d_idof = upload(H.idof);
+    d_bdof = upload(H.bdof);
+    d_blam = upload(H.blam);
+    d_bsign = upload(H.bsign);
+    d_cglob = upload(H.cglob);
+    d_corner_dof = upload(H.corner_dof);
+    d_lam_lo = upload(H.lam_lo);
+    d_lam_hi = upload(H.lam_hi);
+    d_corner_slots = upload(H.corner_slots);
+    d_xkind = upload(H.xkind);
+    d_xa = upload(H.xa);
+    d_xb = upload(H.xb);
+    d_free_dofs = upload(P.free_dofs);
+    d_free_map = upload(P.free_map);
+    d_cons_map = upload(P.cons_map);
+    d_n_i = upload(H.n_i);
+    d_n_b = upload(H.n_b);
+    d_status = alloc<int>(std::max(S, 1));
+
+    // K1: block assembly
+    d_colband = alloc<double2>((size_t)S * NI * LD);
+    d_rowband = alloc<double2>((size_t)S * NI * LD);
+    d_bi_idx = alloc<int>((size_t)S * NB * H.MAXE_BI);
+    d_bi_val = alloc<double2>((size_t)S * NB * H.MAXE_BI);
+    d_ib_idx = alloc<int>((size_t)S * NI * H.MAXE_IB);
+    d_ib_val = alloc<double2>((size_t)S * NI * H.MAXE_IB);
+    d_Sbb = alloc<double2>((size_t)S * NB * NB);
+    d_Sinv = alloc<double2>((size_t)S * NB * NB);
+    d_Aic = alloc<double2>((size_t)S * NI * NC);
+    d_Abc = alloc<double2>((size_t)S * NB * NC);
+    d_Acc = alloc<double2>((size_t)S * NC * NC);
+    d_cpl_i = alloc<double2>((size_t)S * NI * NC);
+    d_cpl_b = alloc<double2>((size_t)S * NB * NC);
+    zero(d_colband, (size_t)S * NI * LD);
+    zero(d_rowband, (size_t)S * NI * LD);
+    zero(d_Sbb, (size_t)S * NB * NB);
+    zero(d_Aic, (size_t)S * NI * NC);
+    zero(d_Abc, (size_t)S * NB * NC);
+    zero(d_Acc, (size_t)S * NC * NC);
+    zero(d_bi_val, (size_t)S * NB * H.MAXE_BI);
+    zero(d_ib_val, (size_t)S * NI * H.MAXE_IB);
+    CU(cudaMemsetAsync(d_bi_idx, 0xff, (size_t)S * NB * H.MAXE_BI * sizeof(int), stream));
+    CU(cudaMemsetAsync(d_ib_idx, 0xff, (size_t)S * NI * H.MAXE_IB * sizeof(int), stream));
+    launch(FETIGPU_K_OTHER, [&] {
+      k_assemble<<<cdiv((long long)S * H.nld, 128), 128, 0, stream>>>(L, d_ldof, d_colband, d_bi_idx, d_bi_val,
+                                                                      d_ib_idx, d_ib_val, d_Sbb, d_Aic, d_Abc, d_Acc);
+    });
+    launch(FETIGPU_K_OTHER, [&] { k_pad_identity<<<S, 128, 0, stream>>>(L, d_n_i, d_n_b, d_colband, d_Sbb); });
+
+    // K2: batched band LDL^T of A_ii
+    band_ldlt(d_colband, d_rowband, Wt, S, NI, d_status);
+    check_status(S, "interior block A_ii");
+
+    // S_bb = A_bb - A_bi A_ii^-1 A_ib  (NB right-hand sides per subdomain)
+    {
+      double2* Y = alloc<double2>((size_t)S * NB * NI);
+      double2* Yc = alloc<double2>((size_t)S * NC * NI);
+      zero(Y, (size_t)S * NB * NI);
+      launch(FETIGPU_K_OTHER, [&] {
+        k_build_aib_rhs<<<cdiv((long long)S * NB * H.MAXE_BI, 256), 256, 0, stream>>>(L, d_bi_idx, d_bi_val, Y);
+      });
+      band_solve(d_colband, d_rowband, Wt, S, NI, Y, (size_t)NB * NI, NI, NB);
+      launch(FETIGPU_K_OTHER, [&] {
+        k_schur_bb<<<cdiv((long long)S * NB * NB, 256), 256, 0, stream>>>(L, d_bi_idx, d_bi_val, Y, d_Sbb);
+      });
+      // S_bb^-1 by in-place Gauss-Jordan on a copy
+      CU(cudaMemcpyAsync(d_Sinv, d_Sbb, (size_t)S * NB * NB * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+      launch(FETIGPU_K_OTHER, [&] {
+        k_gauss_jordan<<<S, 256, 2 * NB * sizeof(double2), stream>>>(d_Sinv, NB, d_status);
+      });
+      check_status(S, "remaining block A_rr");
+      // coupling = A_rr^-1 A_rc via the block formula
+      launch(FETIGPU_K_OTHER, [&] {
+        k_build_aic_rhs<<<cdiv((long long)S * NI * NC, 256), 256, 0, stream>>>(L, d_Aic, Yc);
+      });
+      band_solve(d_colband, d_rowband, Wt, S, NI, Yc, (size_t)NC * NI, NI, NC);
+      launch(FETIGPU_K_OTHER, [&] {
+        k_coupling_b<<<S, 256, NB * NC * sizeof(double2), stream>>>(L, d_Sinv, d_Abc, d_bi_idx, d_bi_val, Yc,
+                                                                    d_cpl_b);
+      });
+      launch(FETIGPU_K_OTHER, [&] {
+        k_coupling_i<<<cdiv((long long)S * NI, 128), 128, 0, stream>>>(L, Yc, Y, d_cpl_b, d_cpl_i);
+      });
+      double2* contrib = alloc<double2>((size_t)S * NC * NC);
+      launch(FETIGPU_K_OTHER, [&] {
+        k_coarse_contrib<<<S, 256, 0, stream>>>(L, d_Aic, d_Abc, d_cpl_i, d_cpl_b, contrib);
+      });
+      // K4: coarse assembly, equilibration, band LDL^T, explicit inverse
+      if (nc > 0) {
+        const int LDC = WCt + 1;
+        double2* cband = alloc<double2>((size_t)nc * LDC);
+        double2* crow = alloc<double2>((size_t)nc * LDC);
+        double* cscale_d = alloc<double>(nc);
+        zero(cband, (size_t)nc * LDC);
+        zero(crow, (size_t)nc * LDC);
+        launch(FETIGPU_K_OTHER, [&] {
+          k_coarse_assemble<<<cdiv(nc, 128), 128, 0, stream>>>(nc, WCt, NC, d_corner_slots, d_cglob, d_Acc, contrib,
+                                                               cband);
+        });
+        launch(FETIGPU_K_OTHER, [&] { k_coarse_scale<<<cdiv(nc, 128), 128, 0, stream>>>(nc, WCt, cband, cscale_d); });
+        launch(FETIGPU_K_OTHER, [&] { k_coarse_apply_scale<<<nc, 64, 0, stream>>>(nc, WCt, cband, cscale_d); });
+        band_ldlt(cband, crow, WCt, 1, nc, d_status);
+        // pivot check relative to the largest |d| (feti.cpp:469-474)
+        {
+          std::vector<double2> f((size_t)nc * LDC);
+          CU(cudaMemcpyAsync(f.data(), cband, f.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+          int st = 0;
+          CU(cudaMemcpyAsync(&st, d_status, sizeof(int), cudaMemcpyDeviceToHost, stream));
+          sync();
+          if (st != 0) throw NumericalError("feti: coarse problem is singular");
+          double umax = 0;
+          std::vector<double> dabs(nc);
+          for (int i = 0; i < nc; ++i) {
+            const double2 di = f[(size_t)i * LDC];
+            dabs[i] = 1.0 / std::sqrt(di.x * di.x + di.y * di.y);
+            umax = std::max(umax, dabs[i]);
+          }
+          for (int i = 0; i < nc; ++i)
+            if (!(dabs[i] > umax * 1e-13)) throw NumericalError("feti: coarse problem is singular");
+        }
+        d_Cinv = alloc<double2>((size_t)nc * nc);
+        launch(FETIGPU_K_OTHER, [&] { k_identity<<<cdiv((long long)nc * nc, 256), 256, 0, stream>>>(nc, d_Cinv); });
+        band_solve(cband, crow, WCt, 1, nc, d_Cinv, (size_t)nc * nc, nc, nc);
+        launch(FETIGPU_K_OTHER, [&] {
+          k_scale_inverse<<<cdiv((long long)nc * nc, 256), 256, 0, stream>>>(nc, d_Cinv, cscale_d);
+        });
+      }
+      sync();
+      // setup temporaries are released here (Y is S*NB*NI complex)
+      for (void* p : {(void*)Y, (void*)Yc}) {
+        cudaFree(p);
+        allocs.erase(std::find(allocs.begin(), allocs.end(), p));
+      }
+    }
+
+    // workspaces
+    d_fi = alloc<double2>((size_t)S * NI);
+    d_fb = alloc<double2>((size_t)S * NB);
+    d_tb = alloc<double2>((size_t)S * NB);
+    d_yi = alloc<double2>((size_t)S * NI);
+    d_ri = alloc<double2>((size_t)S * NI);
+    d_u1b = alloc<double2>((size_t)S * NB);
+    d_wb = alloc<double2>((size_t)S * NB);
+    d_gcp = alloc<double2>((size_t)S * NC);
+    d_fc = alloc<double2>(std::max(nc, 1));
+    d_g = alloc<double2>(std::max(nc, 1));
+    d_z = alloc<double2>(std::max(nc, 1));
+    zero(d_z, std::max(nc, 1));
+    ldv = ((size_t)nl + 63) / 64 * 64;
+    vcap = std::max(2, desc.max_iter + 1);
+    d_V = alloc<double2>(ldv * vcap);
+    d_w = alloc<double2>(ldv);
+    d_zl = alloc<double2>(ldv);
+    d_t = alloc<double2>(ldv);
+    d_lam = alloc<double2>(ldv);
+    d_r = alloc<double2>(ldv);
+    d_d = alloc<double2>(ldv);
+    d_best = alloc<double2>(ldv);
+    mdot_blocks = std::max(1, std::min(296, cdiv(nl, 64)));
+    mdot_chunk = cdiv(nl, mdot_blocks);
+    d_part = alloc<double2>((size_t)(vcap + 2) * mdot_blocks);
+    d_red = alloc<double2>(3 * (vcap + 2));
+    d_y = alloc<double2>(vcap + 2);
+    d_rhs = alloc<double2>(n);
+    d_x = alloc<double2>(n);
+    d_x2 = alloc<double2>(n);
+    d_ax = alloc<double2>(n);
+    d_real0 = alloc<double>(n);
+    d_real1 = alloc<double>(n);
+    d_real2 = alloc<double>(n);
+    d_real3 = alloc<double>(n);
+    d_real4 = alloc<double>(std::max(m, 1));
+    d_api_rhs = alloc<double2>(n);
+    d_api_x = alloc<double2>(n);
+    d_in_ybar = alloc<double>(n);
+    d_in_yc = alloc<double>(std::max(m, 1));
+    d_out_y = alloc<double>(n);
+    d_out_u = alloc<double>(n);
+    d_out_l = alloc<double>(n);
+    CU(cudaMallocHost(&h_pin, sizeof(double2) * 3 * (vcap + 4)));
+    // coarse gemv may need > 48 KB of dynamic smem
+    CU(cudaFuncSetAttribute(k_coarse_gemv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)std::max<size_t>(nc * sizeof(double2), 1)));
+    CU(cudaFuncSetAttribute(k_mdot<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(mdot_chunk * sizeof(double2))));
+    CU(cudaFuncSetAttribute(k_mupdate<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(mdot_chunk * sizeof(double2))));
+    setup_mass();
+    sync();
+    setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+
+  // V = M_y ⊗ M_x ⊗ I_dpn on the structured mesh: 1-D P1 mass (h/6)[.., 1, 4, 1, ..] with
+  // diagonal 2 at a free end.  Thomas coefficients computed once on the host.
+  void setup_mass() {
+    // free node index ranges along x and y
+    int i0 = P.nx, i1 = -1, j0 = P.ny, j1 = -1;
+    for (int md : P.free_dofs) {
+      const int node = md / P.dpn, i = node % (P.nx + 1), j = node / (P.nx + 1);
+      i0 = std::min(i0, i), i1 = std::max(i1, i), j0 = std::min(j0, j), j1 = std::max(j1, j);
+    }
+    Lx = i1 - i0 + 1;
+    Ly = j1 - j0 + 1;
+    if ((long long)Lx * Ly * P.dpn != n) throw ContractError("mass solve: free dofs do not form a tensor grid");
+    const double hh = P.h / 6.0;
+    moff = hh;
+    auto factor = [&](int lo, int hi, int nmax, std::vector<double>& cp, std::vector<double>& dinv) {
+      const int len = hi - lo + 1;
+      cp.assign(len, 0.0);
+      dinv.assign(len, 0.0);
+      for (int k = 0; k < len; ++k) {
+        const int g = lo + k;
+        const double diag = hh * ((g == 0 || g == nmax) ? 2.0 : 4.0);
+        const double den = k == 0 ? diag : diag - hh * cp[k - 1];
+        dinv[k] = 1.0 / den;
+        cp[k] = hh * dinv[k];
+      }
+    };
+    std::vector<double> cx, dx, cy, dy;
+    factor(i0, i1, P.nx, cx, dx);
+    factor(j0, j1, P.ny, cy, dy);
+    d_mx_cp = upload(cx);
+    d_mx_dinv = upload(dx);
+    d_my_cp = upload(cy);
+    d_my_dinv = upload(dy);
+  }
+
+  void mass_solve(double* v) {  // in place, V^-1 v
+    launch(FETIGPU_K_GLOBAL, [&] {
+      k_tridiag_x<<<cdiv((long long)Ly * P.dpn, 128), 128, 0, stream>>>(Ly, Lx, P.dpn, d_mx_cp, d_mx_dinv, moff, v);
+    });
+    launch(FETIGPU_K_GLOBAL, [&] {
+      k_tridiag_y<<<cdiv((long long)Lx * P.dpn, 128), 128, 0, stream>>>(Ly, Lx * P.dpn, d_my_cp, d_my_dinv, moff, v,
+                                                                        Ly);
+    });
+  }
+
+  template <typename T>
+  void apply_global(const T* x, const double* xc, cd kc, cd mcoef, T* y) {
+    launch(FETIGPU_K_GLOBAL, [&] {
+      k_apply_global<T><<<cdiv(n, 256), 256, 0, stream>>>(M, n, d_free_dofs, d_free_map, d_cons_map, x, xc, d2(kc),
+                                                          d2(mcoef), y);
+    });
+  }
+
+  // ------------------------------------------------------------------------ operators
+  void coarse_solve(const double2* fc) {  // g = fc - sum gcp ; z = C^-1 g
+    if (nc == 0) return;
+    launch(FETIGPU_K_COARSE, [&] {
+      k_coarse_rhs<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_slots, d_gcp, fc, d_g);
+    });
+    launch(FETIGPU_K_COARSE, [&] {
+      k_coarse_gemv<8><<<std::min(cdiv(nc, 8), 296), 256, nc * sizeof(double2), stream>>>(nc, d_Cinv, d_g, d_z);
+    });
+  }
+
+  // F lam (feti.cpp:581-594) -> out
+  void apply_dual(const double2* lam, double2* out) {
+    launch(FETIGPU_K_DUAL_GEMV, [&] {
+      k_bnd_gemv<8><<<H.n_sub, 256, H.NB * sizeof(double2), stream>>>(H.NB, H.NC, d_Sinv, d_blam, d_bsign, lam, -1.0,
+                                                                       d_u1b, d_cpl_b, d_gcp);
+    });
+    coarse_solve(nullptr);
+    launch(FETIGPU_K_LAMBDA, [&] {
+      k_lam_gather_dual<<<cdiv(nl, 256), 256, 0, stream>>>(nl, H.NB, H.NC, d_lam_lo, d_lam_hi, d_u1b, d_cpl_b,
+                                                           d_cglob, d_z, out);
+    });
+  }
+  // Dirichlet preconditioner (feti.cpp:597-627) -> out
+  void apply_precond(const double2* r, double2* out) {
+    launch(FETIGPU_K_PRECOND_GEMV, [&] {
+      k_bnd_gemv<8><<<H.n_sub, 256, H.NB * sizeof(double2), stream>>>(H.NB, H.NC, d_Sbb, d_blam, d_bsign, r, 0.5,
+                                                                       d_wb, nullptr, nullptr);
+    });
+    launch(FETIGPU_K_LAMBDA, [&] {
+      k_lam_gather_pre<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_lam_lo, d_lam_hi, d_wb, out);
+    });
+  }
+
+  // eliminate (feti.cpp:516-556) on (t_i = ti, t_b = tb, f_c = fc); leaves u_i in d_ri,
+  // u_b in d_u1b, z in d_z.
+  void eliminate(const double2* ti, const double2* tb, const double2* fc) {
+    const int S = H.n_sub, NI = H.NI, NB = H.NB;
+    CU(cudaMemcpyAsync(d_yi, ti, (size_t)S * NI * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+    band_solve(d_colband, d_rowband, Wt, S, NI, d_yi, NI, NI, 1);
+    launch(FETIGPU_K_OTHER, [&] {
+      k_elim_b<8><<<S, 256, NB * sizeof(double2), stream>>>(L, d_Sinv, tb, d_bi_idx, d_bi_val, d_yi, d_u1b);
+    });
+    launch(FETIGPU_K_OTHER, [&] {
+      k_ib_apply<<<cdiv((long long)S * NI, 256), 256, 0, stream>>>(L, d_ib_idx, d_ib_val, d_u1b, d_ri);
+    });
+    band_solve(d_colband, d_rowband, Wt, S, NI, d_ri, NI, NI, 1);
+    launch(FETIGPU_K_OTHER, [&] {
+      k_elim_i_gcp<<<S, 256, 0, stream>>>(L, d_yi, d_ri, d_u1b, d_Aic, d_Abc, d_gcp);
+    });
+    coarse_solve(fc);
+    launch(FETIGPU_K_OTHER, [&] {
+      k_elim_final<<<cdiv((long long)S * (NI + NB), 256), 256, 0, stream>>>(L, d_cglob, d_z, d_cpl_i, d_cpl_b, d_ri,
+                                                                            d_u1b);
+    });
+  }
+
+  // |x|^2 and max|x| of a complex vector -> host (synchronizes)
+  std::pair<double, double> norm_max(const double2* x, int len) {
+    const int blocks = std::max(1, std::min(296, cdiv(len, 256)));
+    launch(FETIGPU_K_ORTHO, [&] { k_norm_max_part<<<blocks, 256, 0, stream>>>(len, x, d_part); });
+    launch(FETIGPU_K_ORTHO, [&] { k_norm_max_final<<<1, 32, 0, stream>>>(blocks, d_part, d_red); });
+    CU(cudaMemcpyAsync(h_pin, d_red, sizeof(double2), cudaMemcpyDeviceToHost, stream));
+    sync();
+    return {std::sqrt(h_pin[0].x), h_pin[0].y};
+  }
+
+  // ------------------------------------------------------------------------ GMRES
+  // Right-preconditioned unrestarted GMRES (krylov.hpp:102-223).  The Hermitian MGS of
+  // the reference is replaced by CGS2 (two classical passes, equal in exact arithmetic);
+  // Givens rotations, both stopping tests and the best-iterate fallback are the
+  // reference's, run on the host on the (j+2)-vector of coefficients of each step.
+  fetigpu_feti_stats gmres(const double2* b, double2* x) {
+    fetigpu_feti_stats st{};
+    const double tol = desc.tol;
+    const int max_iter = desc.max_iter;
+    zero(x, nl);
+    const double bnorm = norm_max(b, nl).first;
+    if (bnorm == 0.0) {
+      st.converged = 1;
+      return st;
+    }
+    CU(cudaMemcpyAsync(d_r, b, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+    double best_res = 1.0;  // |b - F 0| / |b|
+    CU(cudaMemcpyAsync(d_best, x, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+    const int mr = std::max(1, max_iter);
+    std::vector<std::vector<cd>> Hc;  // columns of the Hessenberg, column j has j+2 entries
+    std::vector<double> gc(mr + 1);
+    std::vector<cd> gs(mr + 1), g(mr + 2);
+    double relres = 0;
+    bool first = true;
+    while (true) {
+      double rnorm;
+      if (first) {
+        rnorm = bnorm;
+        first = false;
+      } else {
+        rnorm = norm_max(d_r, nl).first;
+      }
+      relres = rnorm / bnorm;
+      if (relres < best_res) {
+        best_res = relres;
+        CU(cudaMemcpyAsync(d_best, x, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+      }
+      if (relres <= tol) {
+        st.converged = 1;
+        break;
+      }
+      if (st.iterations >= max_iter) break;
+      launch(FETIGPU_K_ORTHO, [&] { k_scale_copy<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, 1.0 / rnorm, d_V); });
+      std::fill(g.begin(), g.end(), cd(0));
+      g[0] = rnorm;
+      Hc.clear();
+      int k = 0;
+      for (int j = 0; j < mr && st.iterations < max_iter; ++j) {
+        if (j + 1 >= vcap) throw RuntimeError("gmres: basis capacity exceeded");
+        apply_precond(d_V + (size_t)j * ldv, d_zl);
+        apply_dual(d_zl, d_w);
+        const int nv = j + 1;
+        // pass 1: h1 = V^H w, |w|^2
+        launch(FETIGPU_K_ORTHO, [&] {
+          k_mdot<8><<<mdot_blocks, 256, mdot_chunk * sizeof(double2), stream>>>(nl, mdot_chunk, d_V, ldv, nv, d_w, 1,
+                                                                              d_part);
+        });
+        double2* h1 = d_red;
+        double2* h2 = d_red + (vcap + 2);
+        double2* hn = d_red + 2 * (vcap + 2);
+        launch(FETIGPU_K_ORTHO, [&] { k_reduce_parts<<<nv + 1, 32, 0, stream>>>(nv + 1, mdot_blocks, d_part, h1); });
+        // pass 2: w -= V h1 ; h2 = V^H w
+        launch(FETIGPU_K_ORTHO, [&] {
+          k_mupdate<8><<<mdot_blocks, 256, mdot_chunk * sizeof(double2), stream>>>(nl, mdot_chunk, d_V, ldv, nv, h1,
+                                                                                  d_w, 1, d_part);
+        });
+        launch(FETIGPU_K_ORTHO, [&] { k_reduce_parts<<<nv + 1, 32, 0, stream>>>(nv + 1, mdot_blocks, d_part, h2); });
+        // pass 3: w -= V h2 ; |w|^2
+        launch(FETIGPU_K_ORTHO, [&] {
+          k_mupdate<8><<<mdot_blocks, 256, mdot_chunk * sizeof(double2), stream>>>(nl, mdot_chunk, d_V, ldv, nv, h2,
+                                                                                  d_w, 0, d_part);
+        });
+        launch(FETIGPU_K_ORTHO, [&] { k_reduce_parts<<<1, 32, 0, stream>>>(1, mdot_blocks, d_part, hn); });
+        CU(cudaMemcpyAsync(h_pin, h1, sizeof(double2) * (nv + 1), cudaMemcpyDeviceToHost, stream));
+        CU(cudaMemcpyAsync(h_pin + (nv + 1), h2, sizeof(double2) * nv, cudaMemcpyDeviceToHost, stream));
+        CU(cudaMemcpyAsync(h_pin + (2 * nv + 1), hn, sizeof(double2), cudaMemcpyDeviceToHost, stream));
+        sync();
+        const double wpre = std::sqrt(h_pin[nv].x);
+        std::vector<cd> col(j + 2);
+        bool finite = true;
+        for (int i = 0; i <= j; ++i) {
+          col[i] = cd(h_pin[i].x, h_pin[i].y) + cd(h_pin[nv + 1 + i].x, h_pin[nv + 1 + i].y);
+          finite = finite && std::isfinite(col[i].real()) && std::isfinite(col[i].imag());
+        }
+        const double hnext = std::sqrt(std::max(0.0, h_pin[2 * nv + 1].x));
+        if (!std::isfinite(hnext) || !finite) throw NumericalError("gmres: breakdown (NaN/Inf in Arnoldi)");
+        col[j + 1] = hnext;
+        for (int i = 0; i < j; ++i) {  // previous rotations (krylov.hpp:169-173)
+          const cd t1 = col[i], t2 = col[i + 1];
+          col[i] = gc[i] * t1 + gs[i] * t2;
+          col[i + 1] = -std::conj(gs[i]) * t1 + gc[i] * t2;
+        }
+        {  // make_givens (krylov.hpp:66-83)
+          const cd h1v = col[j], h2v = col[j + 1];
+          const double a1 = std::abs(h1v), a2 = std::abs(h2v);
+          if (a2 == 0.0) {
+            gc[j] = 1.0;
+            gs[j] = 0.0;
+          } else if (a1 == 0.0) {
+            gc[j] = 0.0;
+            gs[j] = 1.0;
+          } else {
+            const double tt = std::hypot(a1, a2);
+            gc[j] = a1 / tt;
+            gs[j] = (h1v / a1) * (std::conj(h2v) / tt);
+          }
+        }
+        col[j] = gc[j] * col[j] + gs[j] * col[j + 1];
+        col[j + 1] = 0.0;
+        g[j + 1] = -std::conj(gs[j]) * g[j];
+        g[j] = gc[j] * g[j];
+        Hc.push_back(col);
+        ++st.iterations;
+        k = j + 1;
+        const double est = std::abs(g[j + 1]);
+        const bool happy = hnext <= 1e-14 * std::max(wpre, 1e-300);
+        if (happy || est <= tol * bnorm) break;
+        launch(FETIGPU_K_ORTHO, [&] {
+          k_scale_copy<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_w, 1.0 / hnext, d_V + (size_t)(j + 1) * ldv);
+        });
+      }
+      // back substitution (krylov.hpp:191-196) and x += P^-1 (Q y)
+      std::vector<cd> y(k);
+      for (int i = k - 1; i >= 0; --i) {
+        cd acc = g[i];
+        for (int j2 = i + 1; j2 < k; ++j2) acc -= Hc[j2][i] * y[j2];
+        y[i] = acc / Hc[i][i];
+      }
+      for (int i = 0; i < k; ++i) h_pin[i] = make_double2(y[i].real(), y[i].imag());
+      CU(cudaMemcpyAsync(d_y, h_pin, sizeof(double2) * k, cudaMemcpyHostToDevice, stream));
+      launch(FETIGPU_K_ORTHO, [&] {
+        k_combine<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_V, ldv, k, d_y, d_t);
+      });
+      apply_precond(d_t, d_zl);
+      launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nl, 256), 256, 0, stream>>>(nl, x, d_zl); });
+      apply_dual(x, d_w);
+      launch(FETIGPU_K_ORTHO, [&] { k_sub<<<cdiv(nl, 256), 256, 0, stream>>>(nl, b, d_w, d_r); });
+      sync();  // h_pin is reused by the next norm
+    }
+    // krylov.hpp:214-220: the final residual equals the last cycle's r; best-iterate fallback
+    if (relres > best_res) {
+      CU(cudaMemcpyAsync(x, d_best, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+      relres = best_res;
+    }
+    st.relative_residual = relres;
+    st.converged = relres <= tol;
+    return st;
+  }
+
+  // ------------------------------------------------------------------------ FETI solve
+  // (K + mc V) x = rhs on device vectors (feti.cpp:630-717)
+  fetigpu_feti_stats feti_solve(const double2* rhs, double2* x) {
+    auto t0 = std::chrono::steady_clock::now();
+    fetigpu_feti_stats st{};
+    st.n_lambda = nl;
+    st.coarse_dim = nc;
+    st.setup_seconds = setup_seconds;
+    const double rn = norm_max(rhs, n).first;
+    if (rn == 0.0) {
+      zero(x, n);
+      st.converged = 1;
+      sync();
+      st.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      return st;
+    }
+    const int S = H.n_sub, NI = H.NI, NB = H.NB;
+    launch(FETIGPU_K_OTHER, [&] {
+      k_split_rhs<<<cdiv((long long)S * (NI + NB), 256), 256, 0, stream>>>(L, d_idof, d_bdof, rhs, d_fi, d_fb);
+    });
+    if (nc > 0)
+      launch(FETIGPU_K_OTHER, [&] { k_gather_corner<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_dof, rhs, d_fc); });
+    eliminate(d_fi, d_fb, d_fc);
+    launch(FETIGPU_K_LAMBDA, [&] { k_jump<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_lam_lo, d_lam_hi, d_u1b, d_d); });
+    const fetigpu_feti_stats gst = gmres(d_d, d_lam);
+    st.iterations = gst.iterations;
+    st.converged = gst.converged;
+    st.relative_residual = gst.relative_residual;
+    launch(FETIGPU_K_OTHER, [&] {
+      k_recover_tb<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(S * NB, d_blam, d_bsign, d_fb, d_lam, d_tb);
+    });
+    eliminate(d_fi, d_tb, d_fc);
+    launch(FETIGPU_K_OTHER, [&] {
+      k_assemble_x<<<cdiv(n, 256), 256, 0, stream>>>(n, d_xkind, d_xa, d_xb, d_ri, d_u1b, d_z, x);
+    });
+    launch(FETIGPU_K_LAMBDA, [&] { k_jump<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_lam_lo, d_lam_hi, d_u1b, d_d); });
+    st.interface_jump = nl > 0 ? norm_max(d_d, nl).second : 0.0;
+    apply_global<double2>(x, nullptr, 1.0, mc, d_ax);
+    launch(FETIGPU_K_GLOBAL, [&] { k_sub<<<cdiv(n, 256), 256, 0, stream>>>(n, d_ax, rhs, d_ax); });
+    st.primal_residual = norm_max(d_ax, n).first / rn;
+    st.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return st;
+  }
+
+  // sign = -1 solves with conj(K + mc V) = K + conj(mc) V
+  fetigpu_feti_stats feti_solve_signed(int sign, const double2* rhs, double2* x) {
+    if (sign == 1) return feti_solve(rhs, x);
+    launch(FETIGPU_K_OTHER, [&] { k_conj<<<cdiv(n, 256), 256, 0, stream>>>(n, rhs, d_x2); });
+    // d_x2 is used as the conjugated rhs; copy to d_rhs workspace to keep d_x2 free
+    CU(cudaMemcpyAsync(d_rhs, d_x2, n * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+    auto st = feti_solve(d_rhs, d_x2);
+    launch(FETIGPU_K_OTHER, [&] { k_conj<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x2, x); });
+    return st;
+  }
+
+  // ------------------------------------------------------------------------ range space
+  // solve_range_space (control.cpp:297-334) on device buffers.
+  void schur_solve(const double* ybar, const double* yc, double* y, double* u, double* lam,
+                   fetigpu_schur_stats* out) {
+    auto t0 = std::chrono::steady_clock::now();
+    // rhs = K ybar + Kc yc  (control.cpp:15)
+    apply_global<double>(ybar, (yc && m > 0) ? yc : nullptr, 1.0, 0.0, d_real0);
+    launch(FETIGPU_K_GLOBAL, [&] { k_real_to_complex<<<cdiv(n, 256), 256, 0, stream>>>(n, d_real0, d_rhs); });
+    // a = (K + cV)^-1 rhs
+    const fetigpu_feti_stats sp = feti_solve(d_rhs, d_x);
+    // second factor: (K - cV) t = V a  <=>  t = conj((K + cV)^-1 conj(V a)) = conj(FETI(V conj(a)))
+    launch(FETIGPU_K_OTHER, [&] { k_conj<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x, d_x2); });
+    apply_global<double2>(d_x2, nullptr, 0.0, 1.0, d_rhs);
+    const fetigpu_feti_stats sm = feti_solve(d_rhs, d_x);
+    // lambda = Re t = Re t'; imag leak = max |Im t'|
+    launch(FETIGPU_K_GLOBAL, [&] { k_realify<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x, lam); });
+    const int blocks = std::max(1, std::min(296, cdiv(n, 256)));
+    launch(FETIGPU_K_GLOBAL, [&] {
+      k_imag_max_part<<<blocks, 256, 0, stream>>>(n, d_x, reinterpret_cast<double*>(d_part));
+    });
+    // y = ybar - V^-1 K lambda ; u = lambda / phi  (control.cpp:323-325)
+    apply_global<double>(lam, nullptr, 1.0, 0.0, d_real1);
+    mass_solve(d_real1);
+    launch(FETIGPU_K_GLOBAL, [&] {
+      k_recover_yu<<<cdiv(n, 256), 256, 0, stream>>>(n, ybar, d_real1, lam, 1.0 / phi, y, u);
+    });
+    std::vector<double> parts(blocks);
+    CU(cudaMemcpyAsync(parts.data(), d_part, blocks * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    // |lambda|_inf for the leak warning
+    launch(FETIGPU_K_GLOBAL, [&] { k_real_to_complex<<<cdiv(n, 256), 256, 0, stream>>>(n, lam, d_ax); });
+    const double lmax = norm_max(d_ax, n).second;  // syncs
+    double leak = 0;
+    for (double v : parts) leak = std::max(leak, v);
+    if (out) {
+      out->plus = sp;
+      out->minus = sm;
+      out->imag_leak = leak;
+      out->imag_leak_warning = leak > 1e-6 * std::max(lmax, 1e-300);
+      out->converged = sp.converged && sm.converged;
+      out->factor_setup_seconds = setup_seconds;
+      out->solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+  }
+
+  double class_bytes(int klass) const {
+    const double S = H.n_sub, NB = H.NB;
+    switch (klass) {
+      case FETIGPU_K_PRECOND_GEMV:  // S_bb streamed once + lambda gather + out_b
+        return 16.0 * (S * NB * NB + 2.0 * S * NB) + 12.0 * S * NB;
+      case FETIGPU_K_DUAL_GEMV:  // S_bb^-1 + coupling_b + vectors
+        return 16.0 * (S * NB * NB + S * NB * H.NC + 2.0 * S * NB + S * H.NC) + 12.0 * S * NB;
+      case FETIGPU_K_BAND:  // one single-RHS solve: both factor sweeps + vector in/out
+        return 16.0 * (2.0 * S * H.NI * (Wt + 1) + 3.0 * S * H.NI);
+      case FETIGPU_K_COARSE:
+        return 16.0 * ((double)nc * nc + 2.0 * nc);
+      default:
+        return 0.0;
+    }
+  }
+};
+
+static int guard(const std::function<void()>& f) {
+  try {
+    f();
+    return FETIGPU_OK;
+  } catch (const ContractError& e) {
+    g_last_error = e.what();
+    return FETIGPU_CONTRACT;
+  } catch (const NumericalError& e) {
+    g_last_error = e.what();
+    return FETIGPU_NUMERICAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return FETIGPU_RUNTIME;
+  }
+}
+
+static void validate_desc(const fetigpu_desc* d) {
+  if (!d) throw ContractError("fetigpu: null descriptor");
+  if (d->augment) throw ContractError("fetigpu: edge-RBM augmentation is not implemented (augment must be 0)");
+  if (!(d->tol > 0.0)) throw ContractError("fetigpu: tol must be positive");
+  if (d->max_iter < 0) throw ContractError("fetigpu: max_iter must be non-negative");
+  if (d->phi < 0.0) throw ContractError("ControlProblem: phi must be positive");
+}
+
+}  // namespace fetigpu
+
+using namespace fetigpu;
+
+struct fetigpu_ctx {
+  std::unique_ptr<Ctx> c;
+};
+
+extern "C" {
+
+const char* fetigpu_last_error(void) { return g_last_error.c_str(); }
+
+int fetigpu_problem_info(const fetigpu_desc* desc, int* info) {
+  return guard([&] {
+    validate_desc(desc);
+    HostProblem P = build_problem(*desc);
+    std::fill(info, info + 10, 0);
+    info[0] = P.n();
+    info[1] = P.m();
+    info[8] = P.dpn;
+    if (desc->s_x == 1 && desc->s_y == 1) return;  // mesh-only query
+    HostPartition H = build_partition(P, desc->s_x, desc->s_y);
+    const int v[10] = {P.n(), P.m(), H.n_sub, H.n_corner, H.n_lambda, H.n_edges, H.ex, H.ey, P.dpn, H.W};
+    std::copy(v, v + 10, info);
+  });
+}
+
+int fetigpu_target_thermal(const fetigpu_desc* desc, double* ybar, double* yc) {
+  return guard([&] {
+    if (!desc) throw ContractError("fetigpu: null descriptor");
+    HostProblem P = build_problem(*desc);
+    target_thermal(P, ybar, yc);
+  });
+}
+
+int fetigpu_target_sine(const fetigpu_desc* desc, unsigned long long seed, int modes, int mmax, double* ybar) {
+  return guard([&] {
+    if (!desc) throw ContractError("fetigpu: null descriptor");
+    HostProblem P = build_problem(*desc);
+    target_sine(P, seed, modes, mmax, ybar);
+  });
+}
+
+int fetigpu_create(const fetigpu_desc* desc, fetigpu_ctx** out) {
+  return guard([&] {
+    validate_desc(desc);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw RuntimeError("fetigpu: no CUDA device");
+    if (desc->device < 0 || desc->device >= ndev) throw ContractError("fetigpu: bad device ordinal");
+    auto c = std::make_unique<Ctx>();
+    c->desc = *desc;
+    c->P = build_problem(*desc);
+    c->H = build_partition(c->P, desc->s_x, desc->s_y);
+    if (desc->phi > 0.0) {
+      c->phi = desc->phi;
+      c->mc = cd(0.0, -1.0 / std::sqrt(desc->phi));  // c = 1/(i sqrt(phi)), control.cpp:116
+    } else {
+      c->phi = 0.0;
+      c->mc = cd(desc->mass_coeff_re, desc->mass_coeff_im);
+    }
+    c->setup();
+    auto* h = new fetigpu_ctx;
+    h->c = std::move(c);
+    *out = h;
+  });
+}
+
+void fetigpu_destroy(fetigpu_ctx* ctx) { delete ctx; }
+
+int fetigpu_schur_solve_device(fetigpu_ctx* ctx, const double* d_ybar, const double* d_yc, double* d_y, double* d_u,
+                               double* d_lambda, fetigpu_schur_stats* stats) {
+  return guard([&] {
+    if (!ctx) throw ContractError("fetigpu: null context");
+    Ctx& c = *ctx->c;
+    if (!(c.phi > 0.0)) throw ContractError("build_complex_factors: phi must be positive");
+    c.schur_solve(d_ybar, d_yc, d_y, d_u, d_lambda, stats);
+    c.prof_collect();
+  });
+}
+
+int fetigpu_schur_solve(fetigpu_ctx* ctx, const double* ybar, const double* yc, double* y, double* u, double* lambda,
+                        fetigpu_schur_stats* stats) {
+  return guard([&] {
+    if (!ctx) throw ContractError("fetigpu: null context");
+    Ctx& c = *ctx->c;
+    if (!(c.phi > 0.0)) throw ContractError("build_complex_factors: phi must be positive");
+    const size_t nb = sizeof(double) * c.n;
+    CU(cudaMemcpyAsync(c.d_in_ybar, ybar, nb, cudaMemcpyHostToDevice, c.stream));
+    const double* dyc = nullptr;
+    if (yc && c.m > 0) {
+      CU(cudaMemcpyAsync(c.d_in_yc, yc, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
+      dyc = c.d_in_yc;
+    }
+    double* dy = c.d_out_y;
+    double* du = c.d_out_u;
+    double* dl = c.d_out_l;
+    c.schur_solve(c.d_in_ybar, dyc, dy, du, dl, stats);
+    CU(cudaMemcpyAsync(y, dy, nb, cudaMemcpyDeviceToHost, c.stream));
+    CU(cudaMemcpyAsync(u, du, nb, cudaMemcpyDeviceToHost, c.stream));
+    CU(cudaMemcpyAsync(lambda, dl, nb, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    c.prof_collect();
+  });
+}
+
+int fetigpu_feti_solve(fetigpu_ctx* ctx, int sign, const double* rhs_c128, double* x_c128, fetigpu_feti_stats* stats) {
+  return guard([&] {
+    if (!ctx) throw ContractError("fetigpu: null context");
+    if (sign != 1 && sign != -1) throw ContractError("fetigpu_feti_solve: sign must be +1 or -1");
+    Ctx& c = *ctx->c;
+    const size_t bytes = sizeof(double2) * c.n;
+    CU(cudaMemcpyAsync(c.d_api_rhs, rhs_c128, bytes, cudaMemcpyHostToDevice, c.stream));
+    auto st = c.feti_solve_signed(sign, c.d_api_rhs, c.d_api_x);
+    CU(cudaMemcpyAsync(x_c128, c.d_api_x, bytes, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (stats) *stats = st;
+    c.prof_collect();
+  });
+}
+
+static int lam_op(fetigpu_ctx* ctx, int sign, const double* in, double* out, bool dual) {
+  return guard([&] {
+    if (!ctx) throw ContractError("fetigpu: null context");
+    if (sign != 1 && sign != -1) throw ContractError("sign must be +1 or -1");
+    Ctx& c = *ctx->c;
+    const size_t bytes = sizeof(double2) * c.nl;
+    CU(cudaMemcpyAsync(c.d_t, in, bytes, cudaMemcpyHostToDevice, c.stream));
+    if (sign == -1) c.launch(FETIGPU_K_OTHER, [&] { k_conj<<<cdiv(c.nl, 256), 256, 0, c.stream>>>(c.nl, c.d_t, c.d_t); });
+    if (dual)
+      c.apply_dual(c.d_t, c.d_w);
+    else
+      c.apply_precond(c.d_t, c.d_w);
+    if (sign == -1) c.launch(FETIGPU_K_OTHER, [&] { k_conj<<<cdiv(c.nl, 256), 256, 0, c.stream>>>(c.nl, c.d_w, c.d_w); });
+    CU(cudaMemcpyAsync(out, c.d_w, bytes, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+  });
+}
+int fetigpu_apply_dual(fetigpu_ctx* ctx, int sign, const double* lam, double* out) {
+  return lam_op(ctx, sign, lam, out, true);
+}
+int fetigpu_apply_precond(fetigpu_ctx* ctx, int sign, const double* r, double* out) {
+  return lam_op(ctx, sign, r, out, false);
+}
+
+void* fetigpu_stream(fetigpu_ctx* ctx) { return ctx ? (void*)ctx->c->stream : nullptr; }
+
+long long fetigpu_launch_count(fetigpu_ctx* ctx, int reset) {
+  if (!ctx) return 0;
+  const long long v = ctx->c->launches;
+  if (reset) ctx->c->launches = 0;
+  return v;
+}
+
+int fetigpu_profile(fetigpu_ctx* ctx, int enable) {
+  return guard([&] {
+    if (!ctx) throw ContractError("fetigpu: null context");
+    ctx->c->prof_collect();
+    ctx->c->prof = enable != 0;
+  });
+}
+
+int fetigpu_profile_read(fetigpu_ctx* ctx, double* ms, long long* launches, int reset) {
+  return guard([&] {
+    if (!ctx) throw ContractError("fetigpu: null context");
+    Ctx& c = *ctx->c;
+    c.prof_collect();
+    for (int k = 0; k < FETIGPU_K_COUNT; ++k) {
+      if (ms) ms[k] = c.prof_ms[k];
+      if (launches) launches[k] = c.prof_n[k];
+      if (reset) c.prof_ms[k] = 0, c.prof_n[k] = 0;
+    }
+  });
+}
+
+double fetigpu_class_bytes(fetigpu_ctx* ctx, int klass) { return ctx ? ctx->c->class_bytes(klass) : 0.0; }
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// host_core.hpp — C++ host side of the B200 FETI-DP(H) path: structured mesh,
+// free-dof numbering, Q1 element matrices, the reference partition rules and the
+// flattened per-subdomain index tables the device kernels consume.
+//
+// Restates (not copies) the reference host logic:
+//   build_rectangle_mesh      mesh.cpp:7-36
+//   element matrices          fem.cpp:62-117
+//   free/constrained numbering fem.cpp:133-150
+//   partition_structured      feti.cpp:34-169  (corner rule, lambda numbering, signs)
+// Everything here is O(n) integer bookkeeping run once per context.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "fetigpu.h"
+
+namespace fetigpu {
+
+struct ContractError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct NumericalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct RuntimeError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+// Local-dof category codes of the per-subdomain table (ldof).
+enum : int { CAT_DIRICHLET = 0, CAT_CORNER = 1, CAT_INTERIOR = 2, CAT_BOUNDARY = 3 };
+inline int ldof_code(int cat, int idx) { return (cat << 24) | idx; }
+inline int ldof_cat(int code) { return code >> 24; }
+inline int ldof_idx(int code) { return code & 0xFFFFFF; }
+
+struct HostProblem {
+  int nx = 0, ny = 0, dpn = 1, physics = 0, edofs = 4;
+  double h = 0, lx = 1, ly = 1, young = 0, poisson = 0;
+  std::vector<int> free_map, cons_map;  // mesh dof -> free / constrained index, -1 otherwise
+  std::vector<int> free_dofs, cons_dofs;
+  double ke[64] = {}, me[64] = {};       // element matrices, row-major edofs x edofs
+  int n() const { return (int)free_dofs.size(); }
+  int m() const { return (int)cons_dofs.size(); }
+  int node_id(int i, int j) const { return j * (nx + 1) + i; }
+};
+
+// Flattened partition in the layout the device wants.  Per-subdomain arrays are
+// padded to the maxima (NI, NB, NC) so subdomain s owns a fixed-stride slab.
+struct HostPartition {
+  int sx = 0, sy = 0, ex = 0, ey = 0, dpn = 1;
+  int n_sub = 0, n_free = 0, n_corner = 0, n_lambda = 0, n_edges = 0;
+  int nld = 0;             // local mesh dofs per subdomain: (ex+1)(ey+1) dpn
+  int NI = 0, NB = 0, NC = 0;
+  int W = 0;               // max half-bandwidth of A_ii in natural order
+  int WC = 0;              // half-bandwidth of the coarse matrix in corner order
+  int MAXE_BI = 0, MAXE_IB = 0;  // ELL widths of A_bi (per b row) and A_ib (per i row)
+  std::vector<int> n_i, n_b, n_c;        // per subdomain counts
+  std::vector<int> ldof;                 // [S][nld] category/index codes
+  std::vector<int> idof;                 // [S][NI] global free dof of interior k (-1 pad)
+  std::vector<int> bdof;                 // [S][NB] global free dof of boundary k
+  std::vector<int> blam;                 // [S][NB] multiplier row of boundary k (-1 pad)
+  std::vector<double> bsign;             // [S][NB] +1 / -1 (0 pad)
+  std::vector<int> cglob;                // [S][NC] global corner id (-1 pad)
+  std::vector<int> corner_dof;           // [n_corner] global free dof of corner c
+  std::vector<int> lam_lo, lam_hi;       // [n_lambda] flat slot s*NB+k of the +1 / -1 owner
+  std::vector<int> corner_slots;         // [n_corner][4] flat slot s*NC+k, ascending s, -1 pad
+  std::vector<int> xkind, xa, xb;        // [n_free] primal assembly map (0 int, 1 bnd, 2 corner)
+  // element-local structure: sub origin (node) for subdomain s
+  std::vector<int> sub_i0, sub_j0;
+};
+
+HostProblem build_problem(const fetigpu_desc& d);
+HostPartition build_partition(const HostProblem& P, int sx, int sy);
+
+void target_thermal(const HostProblem& P, double* ybar, double* yc);
+void target_sine(const HostProblem& P, uint64_t seed, int modes, int mmax, double* ybar);
+
+}  // namespace fetigpu

@@ -1,0 +1,148 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle and dense
+direct solves.  Re-expresses the reference's hot-path tests:
+test_feti.cpp:300-351, test_control.cpp:141-163, verify.cpp:150-191, test_smoke.py:48-58.
+
+Tolerances: north_star parity is relative L2 <= 1e-8 in u, y, lambda at the same Krylov
+tolerance with iteration counts within +-2; operator applications agree to 1e-12.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def dense_kkt_solution(orc_problem, phi, ybar, yc):
+    K, V, Kc = orc_problem.dense(0), orc_problem.dense(1), orc_problem.dense(2)
+    n = orc_problem.n
+    A = np.zeros((3 * n, 3 * n))
+    A[:n, :n] = V
+    A[:n, 2 * n:] = K
+    A[n:2 * n, n:2 * n] = phi * V
+    A[n:2 * n, 2 * n:] = -V
+    A[2 * n:, :n] = K
+    A[2 * n:, n:2 * n] = -V
+    rhs = np.zeros(3 * n)
+    rhs[:n] = V @ ybar
+    if yc is not None and len(yc):
+        rhs[2 * n:] = -(Kc @ yc)
+    x = np.linalg.solve(A, rhs)
+    return x[:n], x[n:2 * n], x[2 * n:]
+
+
+@pytest.mark.parametrize("n,s", [(16, 2), (32, 4), (64, 4)])
+@pytest.mark.parametrize("phi", [2e-8, 1e-4])
+def test_operators_match_oracle(fetigpu, oracle_mod, n, s, phi):
+    """apply_dual_operator / apply_dirichlet_preconditioner (feti.cpp:581-627)."""
+    p = fetigpu.make_seeded_problem(n, phi)
+    c = -1j / np.sqrt(phi)
+    gpu = fetigpu.SchurSolver(p, s, s, tol=1e-10)
+    ref = oracle_mod.Feti(oracle_mod.Problem(n), s, s, c)
+    assert gpu.n_lambda == ref.n_lambda
+    rng = np.random.default_rng(7)
+    lam = rng.uniform(-1, 1, ref.n_lambda) + 1j * rng.uniform(-1, 1, ref.n_lambda)
+    for sign, coeff in ((1, c), (-1, -c)):
+        r = ref if sign == 1 else oracle_mod.Feti(oracle_mod.Problem(n), s, s, coeff)
+        assert rel(gpu.apply_dual_operator(lam, sign), r.apply_dual_operator(lam)) <= 1e-12
+        assert rel(gpu.apply_dirichlet_preconditioner(lam, sign), r.apply_dirichlet_preconditioner(lam)) <= 1e-12
+    gpu.close()
+
+
+def test_feti_complex_factors_match_direct(fetigpu, oracle_mod):
+    """test_feti.cpp:309-332 (augment=false here): n=16, 2x2, phi=2e-8, tol 1e-10, <=1e-8."""
+    n, phi = 16, 2e-8
+    p = fetigpu.make_seeded_problem(n, phi)
+    op = oracle_mod.Problem(n)
+    K, V = op.dense(0), op.dense(1)
+    rng = np.random.default_rng(29)
+    rhs = rng.uniform(-1, 1, op.n).astype(complex)
+    c = -1j / np.sqrt(phi)
+    for coeff in (c, -c):
+        out = fetigpu.feti_solve(p, coeff, rhs, s_x=2, s_y=2, tol=1e-10)
+        assert out["converged"]
+        direct = np.linalg.solve(K + coeff * V, rhs)
+        assert rel(out["x"], direct) <= 1e-8
+        assert out["interface_jump"] <= 1e-8
+        xo, so = oracle_mod.Feti(op, 2, 2, coeff, tol=1e-10).solve(rhs)
+        assert abs(out["iterations"] - so["iterations"]) <= 2
+        assert rel(out["x"], xo) <= 1e-8
+
+
+def test_feti_criterion5_n32(fetigpu, oracle_mod):
+    """verify.cpp:150-191: n=32, 4x4, phi=2e-8, tol 1e-10, FETI vs direct <= 1e-8, jump <= 1e-8."""
+    n, phi = 32, 2e-8
+    p = fetigpu.make_thermal_problem(n, phi)
+    op = oracle_mod.Problem(n)
+    K, V, Kc = op.dense(0), op.dense(1), op.dense(2)
+    rhs = (K @ op.target_thermal() + Kc @ op.boundary_thermal()).astype(complex)
+    c = -1j / np.sqrt(phi)
+    for coeff in (c, -c):
+        out = fetigpu.feti_solve(p, coeff, rhs, s_x=4, s_y=4, tol=1e-10)
+        assert out["converged"]
+        direct = np.linalg.solve(K + coeff * V, rhs)
+        assert rel(out["x"], direct) <= 1e-8
+        assert out["interface_jump"] <= 1e-8 * np.abs(out["x"]).max()
+
+
+def test_conjugate_pair_iterations(fetigpu):
+    """test_feti.cpp:334-351: the two conjugate factors need iteration counts within 2."""
+    n, phi = 16, 2e-6
+    p = fetigpu.make_seeded_problem(n, phi)
+    rng = np.random.default_rng(31)
+    rhs = rng.uniform(-1, 1, p.n).astype(complex)
+    c = -1j / np.sqrt(phi)
+    its = [fetigpu.feti_solve(p, coeff, rhs, tol=1e-10)["iterations"] for coeff in (c, -c)]
+    assert abs(its[0] - its[1]) <= 2
+
+
+def test_feti_zero_rhs(fetigpu):
+    """test_feti.cpp:300-307: zero rhs -> zero solution in zero iterations."""
+    p = fetigpu.make_seeded_problem(8, 1e-4)
+    out = fetigpu.feti_solve(p, -1j * 100.0, np.zeros(p.n, dtype=complex))
+    assert out["iterations"] == 0 and out["converged"]
+    assert np.linalg.norm(out["x"]) == 0.0
+
+
+def test_range_space_matches_dense_kkt_n8(fetigpu, oracle_mod):
+    """test_control.cpp:152-163 / test_smoke.py:25-38: n=8, phi=2e-5, <= 1e-8."""
+    n, phi = 8, 2e-5
+    p = fetigpu.make_thermal_problem(n, phi)
+    out = fetigpu.solve_range_space(p, tol=1e-12)
+    assert out["converged"] and not out["imag_leak_warning"]
+    y, u, lam = dense_kkt_solution(oracle_mod.Problem(n), phi, p.target_state, p.boundary_values)
+    assert rel(out["y"], y) <= 1e-8
+    assert rel(out["u"], u) <= 1e-8
+    assert rel(out["lambda"], lam) <= 1e-8
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_config1_schur_matches_oracle(fetigpu, oracle_mod, seed):
+    """BASELINE config 1: 64x64 Q1, 4x4 subdomains, phi=1e-4, seeded sine target, tol 1e-10."""
+    n, s, phi = 64, 4, 1e-4
+    p = fetigpu.make_seeded_problem(n, phi, seed=seed)
+    op = oracle_mod.Problem(n)
+    ybar = op.target_sine(seed)
+    assert np.array_equal(ybar, p.target_state)
+    ref = op.schur_solve(s, s, phi, ybar, None, tol=1e-10, max_iter=2000, threads=4)
+    solver = fetigpu.SchurSolver(p, s, s, tol=1e-10, max_iter=2000)
+    out = solver.solve()
+    solver.close()
+    assert out["converged"]
+    for k in ("y", "u", "lambda"):
+        assert rel(out[k], ref[k]) <= 1e-8, k
+    assert abs(out["plus_stats"]["iterations"] - ref["plus_stats"]["iterations"]) <= 2
+    assert abs(out["minus_stats"]["iterations"] - ref["minus_stats"]["iterations"]) <= 2
+
+
+def test_schur_solver_reuse_is_deterministic(fetigpu):
+    """Factor once, solve twice: bit-identical results (verify.cpp:354-369 determinism)."""
+    p = fetigpu.make_seeded_problem(64, 1e-4)
+    solver = fetigpu.SchurSolver(p, 4, 4, tol=1e-10)
+    a = solver.solve()
+    b = solver.solve()
+    solver.close()
+    for k in ("y", "u", "lambda"):
+        assert np.array_equal(a[k], b[k])
