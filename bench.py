@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""Benchmark: range-space Schur solves/sec (two complex FETI-DP(H) solves on K -/+ i beta M)
+on BASELINE.json configs[1] (2D heat control, 1024x1024 Q1 grid, 32x32 subdomains of
+32x32 elements, FP64 complex, relative dual residual 1e-10).
+
+One step = one range-space Schur solve (rhs = K ybar, FETI on K + cV, V a, FETI on K - cV,
+primal recovery) for a fresh seeded sine-mode target ybar (seed = step index), factors
+reused across steps (the reference's per_solve_seconds regime, experiments.cpp:265).
+
+  value : solves/s through fetigpu_schur_solve_device (ybar resident in HBM), CUDA events
+          on the library stream, max over ranks
+  e2e   : solves/s through fetigpu_schur_solve (host buffers; H2D of ybar and D2H of y, u,
+          lambda inside the timed region)
+  --impl reference : the CPU restatement of the reference (oracle/) on this host's cores,
+          same workload and metric (rank 0 only under torchrun).
+
+Multi-GPU (N > 1): each rank runs its own config-2 Schur solves (replicas, weak scaling);
+the subdomain-sharded NCCL path is SURVEY.md §8(e) work in progress.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Schur solves/sec (2 complex FETI-DPH solves), 2D Poisson 1M dofs"
+UNIT = "solves/s"
+N_GRID, S_SUB, PHI, TOL, MAX_ITER = 1024, 32, 1e-4, 1e-10, 2000
+PHI_SWEEP = (1e-2, 1e-4, 1e-6, 1e-8)
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons through NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device=0, period=0.1):
+        self.samples, self.reasons, self.period = [], set(), period
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def cpu_sample_oracle(threads, steps, warmup, budget_s=150.0):
+    """The oracle (CPU restatement of the reference) on config 2: setup once, then Schur
+    solves on seeded targets.  Returns (solves/s, iterations, setup s, steps run)."""
+    from oracle import oracle as O
+
+    p = O.Problem(N_GRID)
+    pair = O.SchurPair(p, S_SUB, S_SUB, PHI, tol=TOL, max_iter=MAX_ITER, threads=threads)
+    for w in range(warmup):
+        pair.run(p.target_sine(1000 + w))
+    times, its = [], None
+    t_start = time.perf_counter()
+    for k in range(steps):
+        ybar = p.target_sine(k)
+        t0 = time.perf_counter()
+        r = pair.run(ybar)
+        times.append(time.perf_counter() - t0)
+        its = (r["plus_stats"]["iterations"], r["minus_stats"]["iterations"])
+        if time.perf_counter() - t_start > budget_s:
+            break
+    return len(times) / sum(times), its, pair.setup_seconds, len(times)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    # each step is one full config-2 Schur solve (~10 s on 16 cores); warm-up is capped at
+    # one solve and the timed steps at a 150 s budget so the arm ends within minutes
+    rate, its, setup_s, ran = cpu_sample_oracle(threads, args.steps, min(args.warmup, 1))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 / rate, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded sine-mode ybar, seed = step)",
+        "config": {"workload": "config2: 1024x1024 Q1 heat, 32x32 subdomains, phi=1e-4, tol 1e-10",
+                   "phi": PHI, "steps_run": ran, "iterations_plus_minus": its,
+                   "setup_seconds_both_factors": setup_s},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{ran} config-2 Schur solves after setup (oracle/, std::thread x{threads})"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu(args):
+    rank, world, local = dist_env()
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1312_5653_b200 as F
+
+    steps, warmup = args.steps, max(args.warmup, 3)
+    p = F.make_seeded_problem(N_GRID, PHI, seed=0)
+    t0 = time.perf_counter()
+    solver = F.SchurSolver(p, S_SUB, S_SUB, tol=TOL, max_iter=MAX_ITER, device=local)
+    setup_s = time.perf_counter() - t0
+    n = p.n
+    # seeded targets for every step, resident in HBM before the timed region
+    seeds = [rank * 100000 + k for k in range(warmup + steps)]
+    targets = [F.make_seeded_problem(N_GRID, PHI, seed=s).target_state for s in seeds]
+    d_ybar = [torch.from_numpy(t).cuda() for t in targets]
+    d_y = torch.empty(n, dtype=torch.float64, device="cuda")
+    d_u = torch.empty_like(d_y)
+    d_l = torch.empty_like(d_y)
+    stream = torch.cuda.ExternalStream(solver.stream)
+
+    def device_step(k):
+        return solver.solve_device(d_ybar[k].data_ptr(), 0, d_y.data_ptr(), d_u.data_ptr(), d_l.data_ptr())
+
+    for k in range(warmup):
+        st = device_step(k)
+    torch.cuda.synchronize()
+    its = []
+    # ---------------- timed region: value (inputs resident in HBM) ----------------
+    barrier(world)
+    torch.cuda.synchronize()
+    launches0 = solver.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for k in range(warmup, warmup + steps):
+            st = device_step(k)
+            its.append((st["plus_stats"]["iterations"], st["minus_stats"]["iterations"]))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = solver.launch_count() - launches0
+    t_dev = ev0.elapsed_time(ev1) / 1000.0
+    t_max = max_over_ranks(t_dev, world)
+    total_solves = sum_over_ranks(steps, world)
+    value = total_solves / t_max
+    # ---------------- e2e: host buffers through the public API ----------------
+    host_t = [np.ascontiguousarray(t) for t in targets]
+    barrier(world)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    for k in range(warmup, warmup + steps):
+        r = solver.solve(host_t[k], None)
+    w1 = time.perf_counter()
+    barrier(world)
+    e2e_t = max_over_ranks(w1 - w0, world)
+    e2e = sum_over_ranks(steps, world) / e2e_t
+    # ---------------- per-kernel roofline pass (same K steps, events per launch) ----------------
+    solver.profile(True)
+    solver.profile_read(reset=True)
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev2.record(stream)
+    for k in range(warmup, warmup + steps):
+        device_step(k)
+    ev3.record(stream)
+    torch.cuda.synchronize()
+    prof = solver.profile_read(reset=True)
+    solver.profile(False)
+    t_prof = ev2.elapsed_time(ev3) / steps
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    kclass = max(("dual_gemv", "precond_gemv"), key=lambda c: prof[c]["ms"])
+    kb = solver.class_bytes(kclass)
+    avg_ms = prof[kclass]["ms"] / max(prof[kclass]["launches"], 1)
+    achieved = kb / (avg_ms / 1000.0) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(kclass)
+    except Exception:
+        pass
+    kernel_breakdown = {c: {"ms_per_step": v["ms"] / steps, "launches_per_step": v["launches"] / steps}
+                        for c, v in prof.items() if v["launches"]}
+    # per-solve HBM bytes of the local operators (both GEMV classes) -> effective GB/s
+    iters = np.mean([a + b for a, b in its])
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warmup,
+        "ms_per_step": t_max / steps * 1000.0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (seeded sine-mode ybar, seed = step; factors random-free FEM)",
+        "config": {
+            "workload": "config2: 1024x1024 Q1 heat, 32x32 subdomains of 32x32, phi=1e-4, tol 1e-10, FP64 complex",
+            "phi": PHI, "n_free": n, "n_lambda": solver.n_lambda, "coarse_dim": solver.coarse_dim,
+            "iterations_plus_minus_mean": [float(np.mean([a for a, _ in its])), float(np.mean([b for _, b in its]))],
+            "setup_seconds": setup_s, "l2": "inputs larger than L2 (local operators 0.5 GB streamed per iteration)",
+            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+            "kernel_ms_per_step": kernel_breakdown, "profiled_ms_per_step": t_prof,
+        },
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 3 * 8 * n},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": kclass, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                     "bytes_per_launch": kb, "avg_launch_ms": avg_ms},
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        rate, cits, csetup, ran = cpu_sample_oracle(os.cpu_count() or 1, 1, 0)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
+                                "sample": f"{ran} config-2 Schur solve after setup ({csetup:.1f} s), oracle/ "
+                                          f"std::thread x{os.cpu_count()}, iterations {cits}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    solver.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -74,7 +74,8 @@ typedef struct {
 
 /* ---- host-only queries (no GPU needed) ------------------------------------------- */
 
-/* info[0..9] = n_free, n_constrained, n_subdomains, n_corner_dofs, n_lambda, n_edges,
+/* s_x = s_y = 0: mesh-only query (partition fields 0).
+ * info[0..9] = n_free, n_constrained, n_subdomains, n_corner_dofs, n_lambda, n_edges,
  *              ex, ey, dofs_per_node, band half-width of A_ii.
  * Replaces partition_structured (feti.cpp:34-169) + assemble_operators sizes. */
 int fetigpu_problem_info(const fetigpu_desc* desc, int* info);

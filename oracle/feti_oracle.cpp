@@ -1307,6 +1307,75 @@ int orc_schur_solve(void* p, int sx, int sy, double phi, const double* ybar, con
   });
 }
 
+// Persistent pair of factor solvers (the two ComplexFactorSolver of control.cpp:303-304)
+// so timing can separate setup from per-solve cost (experiments.cpp:264-265).
+struct SchurPair {
+  Problem* P;
+  Feti plus, minus;
+  double phi;
+};
+int orc_schur_create(void* p, int sx, int sy, double phi, double tol, int max_iter, int threads, void** out,
+                     double* setup_seconds) {
+  return guard([&] {
+    auto* P = static_cast<Problem*>(p);
+    if (!(phi > 0.0)) throw ContractError("ControlProblem: phi must be positive");
+    auto sp = std::make_unique<SchurPair>();
+    sp->P = P;
+    sp->phi = phi;
+    const cd c(0.0, -1.0 / std::sqrt(phi));
+    auto t0 = std::chrono::steady_clock::now();
+    for (Feti* F : {&sp->plus, &sp->minus}) {
+      F->P = P;
+      F->part = partition_structured(*P, sx, sy);
+      F->kcoef = 1.0;
+      F->tol = tol;
+      F->max_iter = max_iter;
+      F->threads = threads;
+    }
+    sp->plus.mcoef = c;
+    sp->minus.mcoef = -c;
+    sp->plus.setup();
+    sp->minus.setup();
+    if (setup_seconds) *setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = sp.release();
+  });
+}
+void orc_schur_destroy(void* h) { delete static_cast<SchurPair*>(h); }
+int orc_schur_run(void* h, const double* ybar, const double* yc, double* y, double* u, double* lam, OrcStats* plus,
+                  OrcStats* minus, double* imag_leak) {
+  return guard([&] {
+    auto* sp = static_cast<SchurPair*>(h);
+    Problem* P = sp->P;
+    const int n = P->n(), m = P->m();
+    RVec rhs(n), kc(n, 0.0);
+    P->K.apply(ybar, rhs.data());
+    if (yc && m > 0) {
+      P->Kc.apply(yc, kc.data());
+      for (int i = 0; i < n; ++i) rhs[i] += kc[i];
+    }
+    CVec crhs(rhs.begin(), rhs.end());
+    auto [a, s1] = sp->plus.solve(crhs);
+    CVec va(n);
+    P->V.apply(a.data(), va.data());
+    auto [t, s2] = sp->minus.solve(va);
+    double leak = 0;
+    for (int i = 0; i < n; ++i) {
+      lam[i] = t[i].real();
+      leak = std::max(leak, std::abs(t[i].imag()));
+    }
+    RVec kl(n), vk(n);
+    P->K.apply(lam, kl.data());
+    mass_solve(*P, kl.data(), vk.data());
+    for (int i = 0; i < n; ++i) {
+      y[i] = ybar[i] - vk[i];
+      u[i] = lam[i] / sp->phi;
+    }
+    fill(plus, s1);
+    fill(minus, s2);
+    if (imag_leak) *imag_leak = leak;
+  });
+}
+
 // Dense GMRES harness (krylov.hpp restated) for the reference's Krylov tests.
 int orc_gmres_dense(int n, const double* a, const double* b, double tol, int max_iter, double* x, int* iters,
                     double* relres, int* converged, double* hist, int hist_cap) {

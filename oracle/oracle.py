@@ -82,6 +82,10 @@ def lib():
         L.orc_feti_solve.argtypes = [vp, dp, dp, C.POINTER(OracleStats), dp, C.c_int]
         L.orc_schur_solve.argtypes = [vp, C.c_int, C.c_int, C.c_double, dp, dp, C.c_double, C.c_int, C.c_int,
                                       dp, dp, dp, C.POINTER(OracleStats), C.POINTER(OracleStats), dp, dp]
+        L.orc_schur_create.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                       C.POINTER(vp), dp]
+        L.orc_schur_destroy.argtypes = [vp]
+        L.orc_schur_run.argtypes = [vp, dp, dp, dp, dp, dp, C.POINTER(OracleStats), C.POINTER(OracleStats), dp]
         L.orc_gmres_dense.argtypes = [C.c_int, dp, dp, C.c_double, C.c_int, dp, ip, dp, ip, dp, C.c_int]
         _lib = L
     return _lib
@@ -227,6 +231,38 @@ class Feti:
         if history:
             d["history"] = hist[: d["iterations"]].copy()
         return x, d
+
+
+class SchurPair:
+    """Both reference factor solvers built once (control.cpp:303-304); run() = one Schur solve."""
+
+    def __init__(self, problem: Problem, s_x, s_y, phi, tol=1e-10, max_iter=2000, threads=1):
+        self.problem = problem
+        h = C.c_void_p()
+        t = np.zeros(1)
+        _check(lib().orc_schur_create(problem._h, s_x, s_y, phi, tol, max_iter, threads, C.byref(h), _dp(t)))
+        self._h = h
+        self.setup_seconds = float(t[0])
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.orc_schur_destroy(self._h)
+            self._h = None
+
+    def run(self, ybar, yc=None):
+        n = self.problem.n
+        ybar = np.ascontiguousarray(ybar, dtype=np.float64)
+        ycp = None
+        if yc is not None and self.problem.m > 0:
+            yc = np.ascontiguousarray(yc, dtype=np.float64)
+            ycp = _dp(yc)
+        y, u, lam = np.zeros(n), np.zeros(n), np.zeros(n)
+        sp, sm = OracleStats(), OracleStats()
+        leak = np.zeros(1)
+        _check(lib().orc_schur_run(self._h, _dp(ybar), ycp, _dp(y), _dp(u), _dp(lam), C.byref(sp), C.byref(sm),
+                                   _dp(leak)))
+        return {"y": y, "u": u, "lambda": lam, "imag_leak": float(leak[0]), "plus_stats": sp.as_dict(),
+                "minus_stats": sm.as_dict(), "converged": bool(sp.converged and sm.converged)}
 
 
 def sine_modes(seed, modes=8, mmax=8):

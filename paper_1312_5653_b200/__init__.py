@@ -96,11 +96,11 @@ class ControlProblem:
 
     @property
     def n(self):
-        return int(self._info(1, 1)[0])
+        return int(self._info(0, 0)[0])
 
     @property
     def m(self):
-        return int(self._info(1, 1)[1])
+        return int(self._info(0, 0)[1])
 
     def validate(self):  # control.cpp:7-13
         if not (self.phi > 0.0):
@@ -129,7 +129,7 @@ def make_problem(n_x, n_y=None, phi=1e-4, physics=0, len_x=1.0, len_y=1.0, young
         raise ContractError("build_rectangle_mesh: need at least 2 elements per axis")
     p = ControlProblem(n_x=n_x, n_y=n_y, phi=phi, physics=physics, len_x=len_x, len_y=len_y, young=young,
                        poisson=poisson)
-    info = p._info(1, 1)
+    info = p._info(0, 0)
     n, m = int(info[0]), int(info[1])
     d = _base_desc(n_x, n_y, physics, len_x, len_y, young, poisson)
     ybar = np.zeros(n)
@@ -137,7 +137,7 @@ def make_problem(n_x, n_y=None, phi=1e-4, physics=0, len_x=1.0, len_y=1.0, young
         yc = np.zeros(m)
         _check(_native.lib().fetigpu_target_thermal(C.byref(d), _dp(ybar), _dp(yc) if m else None))
     elif target == "sine":
-        yc = np.zeros(m)
+        yc = None  # homogeneous Dirichlet data, y_c = 0 (BASELINE.json configs)
         _check(_native.lib().fetigpu_target_sine(C.byref(d), seed, modes, mmax, _dp(ybar)))
     else:
         raise ContractError("target must be 'thermal' or 'sine'")

@@ -892,7 +892,7 @@ int fetigpu_problem_info(const fetigpu_desc* desc, int* info) {
     info[0] = P.n();
     info[1] = P.m();
     info[8] = P.dpn;
-    if (desc->s_x == 1 && desc->s_y == 1) return;  // mesh-only query
+    if (desc->s_x == 0 && desc->s_y == 0) return;  // mesh-only query
     HostPartition H = build_partition(P, desc->s_x, desc->s_y);
     const int v[10] = {P.n(), P.m(), H.n_sub, H.n_corner, H.n_lambda, H.n_edges, H.ex, H.ey, P.dpn, H.W};
     std::copy(v, v + 10, info);

@@ -1,0 +1,102 @@
+"""CPU tests of the product's host side: the C-ABI library loads and exports every
+symbol of include/fetigpu.h, and the C++ host core (mesh, partition, targets) agrees
+with the oracle.  No kernel is launched (no GPU in this container)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "fetigpu.h")).read()
+    return sorted(set(re.findall(r"\b(fetigpu_[a-z_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol(fetigpu):
+    import ctypes
+
+    from paper_1312_5653_b200 import _native
+
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 15
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_native.EXPORTED_SYMBOLS)
+
+
+def test_library_is_sm100a(fetigpu):
+    import subprocess
+
+    from paper_1312_5653_b200 import _native
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _native.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+@pytest.mark.parametrize("n,s", [(8, 2), (16, 2), (32, 4), (64, 4), (128, 8), (1024, 32), (2048, 64)])
+def test_partition_matches_oracle(fetigpu, oracle_mod, n, s):
+    p = fetigpu.make_problem(n, n, 1e-4, target="sine")
+    info = fetigpu.partition_info(p, s, s)
+    ref = oracle_mod.Problem(n).partition_info(s, s) if n <= 1024 else None
+    if ref:
+        for k in ("n_subdomains", "n_corner_dofs", "n_lambda", "n_edges", "ex", "ey"):
+            assert info[k] == ref[k], k
+    if n == 2048:
+        assert (info["n_subdomains"], info["n_corner_dofs"], info["n_lambda"], info["n_edges"]) == (
+            4096, 3969, 249984, 8064)
+        assert info["band_halfwidth"] == 32
+
+
+def test_partition_sizes_rectangles(fetigpu, oracle_mod):
+    for nx, ny, sx, sy in ((16, 8, 4, 2), (24, 12, 3, 2), (8, 8, 1, 2), (12, 8, 2, 4)):
+        p = fetigpu.make_problem(nx, ny, 1e-4, len_x=nx / 8.0, len_y=ny / 8.0)
+        info = fetigpu.partition_info(p, sx, sy)
+        ref = oracle_mod.Problem(nx, ny, nx / 8.0, ny / 8.0).partition_info(sx, sy)
+        assert all(info[k] == ref[k] for k in ref), (nx, ny, sx, sy)
+
+
+def test_targets_match_oracle_bitwise(fetigpu, oracle_mod):
+    for n in (8, 64, 256):
+        p = fetigpu.make_thermal_problem(n, 1e-4)
+        o = oracle_mod.Problem(n)
+        assert np.array_equal(p.target_state, o.target_thermal())
+        assert np.array_equal(p.boundary_values, o.boundary_thermal())
+        for seed in (0, 1, 2):
+            q = fetigpu.make_seeded_problem(n, 1e-4, seed=seed)
+            assert np.array_equal(q.target_state, o.target_sine(seed))
+
+
+def test_sine_modes_recipe(oracle_mod):
+    """mt19937_64(seed), Box-Muller amplitudes, modes in 1..8."""
+    a, m, n = oracle_mod.sine_modes(0)
+    assert a.shape == (8,) and np.all((m >= 1) & (m <= 8)) and np.all((n >= 1) & (n <= 8))
+    a1, _, _ = oracle_mod.sine_modes(1)
+    assert not np.array_equal(a, a1)
+
+
+def test_contract_errors(fetigpu):
+    F = fetigpu
+    with pytest.raises(ValueError):
+        F.make_thermal_problem(1, 1e-4)  # test_smoke.py:81-83
+    with pytest.raises(ValueError):
+        F.make_thermal_problem(8, 0.0)
+    p = F.make_thermal_problem(6, 1e-4)
+    for sx, sy in ((4, 2), (6, 6), (1, 1)):  # test_feti.cpp:70-77
+        with pytest.raises(ValueError):
+            F.partition_info(p, sx, sy)
+    with pytest.raises(ValueError):
+        F.SchurSolver(F.make_thermal_problem(8, 1e-4), 2, 2, augment=True)
+    with pytest.raises(ValueError):
+        F.solve_range_space(F.make_thermal_problem(8, 1e-4), method="direct")
+
+
+def test_problem_sizes(fetigpu):
+    p = fetigpu.make_thermal_problem(4, 1e-3)
+    assert (p.n, p.m) == (9, 16)  # test_mesh_fem.cpp:128-133
+    q = fetigpu.make_problem(12, 4, 1e-4, physics=1, len_x=3.0, len_y=1.0, young=20.7e6, poisson=0.45)
+    assert (q.n, q.m) == (2 * 12 * 5, 2 * 5)  # clamped x = 0 edge (fem.cpp:124-128)
