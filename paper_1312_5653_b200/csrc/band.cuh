@@ -154,24 +154,29 @@ __global__ void __launch_bounds__(WARPS * 32)
     const double2* panel = stage + (size_t)st * CH * LD;
     const int rows = min(CH, n - q * CH);
     if (active) {
+#pragma unroll 4
       for (int t = 0; t < rows; ++t) {
         const int j = q * CH + t;
         const double2* col = panel + t * LD;
         const int p = j & (WIN - 1);
         const int pl = p & 31, ps = p >> 5;
+        // shared-memory operands first: only SHFL -> DFMA stays on the per-step chain
+        int k[NS];
+        double2 c[NS];
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
+          k[sl] = (lane + 32 * sl - p) & (WIN - 1);
+          c[sl] = k[sl] <= W ? col[k[sl]] : cz();
+        }
+        const double2 cw = (WIN <= W) ? col[WIN <= W ? WIN : 0] : cz();
+        const double2 nb = myb[t];
         const double2 ysel = (NS == 1 || ps == 0) ? y[0] : y[NS - 1];
         const double2 v = shfl2(ysel, pl);
 #pragma unroll
         for (int sl = 0; sl < NS; ++sl) {
-          const int k = (lane + 32 * sl - p) & (WIN - 1);
-          if (k == 0) {
-            x[j] = cmul(v, col[0]);
-            double2 nb = myb[t];
-            if (WIN <= W) nb = cfms(col[WIN <= W ? WIN : 0], v, nb);
-            y[sl] = nb;
-          } else if (k <= W) {
-            y[sl] = cfms(col[k], v, y[sl]);
-          }
+          const bool piv = k[sl] == 0;
+          y[sl] = cfms(piv ? cw : c[sl], v, piv ? nb : y[sl]);
+          if (piv) x[j] = cmul(v, c[sl]);
         }
       }
     }
@@ -216,24 +221,28 @@ __global__ void __launch_bounds__(WARPS * 32)
     const double2* panel = stage + (size_t)st * CH * LD;
     const int rows = min(CH, n - c * CH);
     if (active) {
+#pragma unroll 4
       for (int t = rows - 1; t >= 0; --t) {
         const int j = c * CH + t;
         const double2* rw = panel + t * LD;
         const int p = j & (WIN - 1);
         const int pl = p & 31, ps = p >> 5;
+        int k[NS];
+        double2 cf[NS];
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
+          k[sl] = (p - (lane + 32 * sl)) & (WIN - 1);
+          cf[sl] = k[sl] <= W ? rw[k[sl]] : cz();
+        }
+        const double2 cw = (WIN <= W) ? rw[WIN <= W ? WIN : 0] : cz();
+        const double2 nb = myb[t];
         const double2 ysel = (NS == 1 || ps == 0) ? y[0] : y[NS - 1];
         const double2 v = shfl2(ysel, pl);
 #pragma unroll
         for (int sl = 0; sl < NS; ++sl) {
-          const int k = (p - (lane + 32 * sl)) & (WIN - 1);
-          if (k == 0) {
-            x[j] = v;
-            double2 nb = myb[t];
-            if (WIN <= W) nb = cfms(rw[WIN <= W ? WIN : 0], v, nb);
-            y[sl] = nb;
-          } else if (k <= W) {
-            y[sl] = cfms(rw[k], v, y[sl]);
-          }
+          const bool piv = k[sl] == 0;
+          y[sl] = cfms(piv ? cw : cf[sl], v, piv ? nb : y[sl]);
+          if (piv) x[j] = v;
         }
       }
     }

@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -86,6 +87,8 @@ struct Ctx {
   double2 *d_Sbb = nullptr, *d_Sinv = nullptr, *d_Aic = nullptr, *d_Abc = nullptr, *d_Acc = nullptr;
   double2 *d_cpl_i = nullptr, *d_cpl_b = nullptr;
   double2 *d_Cinv = nullptr;
+  double2 *d_Sbb_p = nullptr, *d_Sinv_p = nullptr;  // packed symmetric tiles (k_sym_gemv)
+  int NT = 0;
   // workspaces
   double2 *d_fi = nullptr, *d_fb = nullptr, *d_fc = nullptr, *d_tb = nullptr, *d_yi = nullptr, *d_ri = nullptr;
   double2 *d_u1b = nullptr, *d_gcp = nullptr, *d_g = nullptr, *d_z = nullptr, *d_wb = nullptr;
@@ -98,6 +101,16 @@ struct Ctx {
   double2* h_pin = nullptr;
   size_t ldv = 0;
   int vcap = 0;  // basis vectors allocated
+  GmresState* d_gst = nullptr;
+  GmresState* h_gst = nullptr;
+  double2 *d_R = nullptr, *d_gsin = nullptr, *d_gvec = nullptr;
+  double* d_gcos = nullptr;
+  unsigned int* d_counter = nullptr;
+  bool use_graph = true;
+  cudaGraph_t arnoldi_graph = nullptr;
+  cudaGraphExec_t arnoldi_exec = nullptr;
+  cudaGraphConditionalHandle arnoldi_handle{};
+  int arnoldi_body_kernels = 0;
   int mdot_blocks = 0, mdot_chunk = 0;
   // mass solve (Kronecker tridiagonal)
   double *d_mx_cp = nullptr, *d_mx_dinv = nullptr, *d_my_cp = nullptr, *d_my_dinv = nullptr;
@@ -112,6 +125,9 @@ struct Ctx {
     }
     for (void* p : allocs) cudaFree(p);
     if (h_pin) cudaFreeHost(h_pin);
+    if (h_gst) cudaFreeHost(h_gst);
+    if (arnoldi_exec) cudaGraphExecDestroy(arnoldi_exec);
+    if (arnoldi_graph) cudaGraphDestroy(arnoldi_graph);
     if (stream) cudaStreamDestroy(stream);
   }
 
@@ -247,6 +263,9 @@ struct Ctx {
     auto t0 = std::chrono::steady_clock::now();
     CU(cudaSetDevice(desc.device));
     CU(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    // FETIGPU_EAGER=1: launch the Arnoldi steps one by one instead of through the
+    // conditional-node graph (ncu cannot profile kernel nodes of such graphs)
+    if (const char* e = std::getenv("FETIGPU_EAGER")) use_graph = !(e[0] == '1');
     n = P.n();
     m = P.m();
     nc = H.n_corner;
@@ -398,12 +417,25 @@ struct Ctx {
           k_scale_inverse<<<cdiv((long long)nc * nc, 256), 256, 0, stream>>>(nc, d_Cinv, cscale_d);
         });
       }
+      // packed symmetric storage of S_bb and S_bb^-1 for the per-iteration GEMVs
+      NT = (NB + 31) / 32;
+      if (NT > 8) throw ContractError("more than 256 interface dofs per subdomain");
+      const size_t per = (size_t)sym_tile_entries(NT);
+      d_Sbb_p = alloc<double2>((size_t)S * per);
+      d_Sinv_p = alloc<double2>((size_t)S * per);
+      launch(FETIGPU_K_OTHER, [&] {
+        k_pack_sym<<<cdiv((long long)S * per, 256), 256, 0, stream>>>(S, NB, NT, d_Sbb, d_Sbb_p);
+      });
+      launch(FETIGPU_K_OTHER, [&] {
+        k_pack_sym<<<cdiv((long long)S * per, 256), 256, 0, stream>>>(S, NB, NT, d_Sinv, d_Sinv_p);
+      });
       sync();
-      // setup temporaries are released here (Y is S*NB*NI complex)
-      for (void* p : {(void*)Y, (void*)Yc}) {
+      // setup temporaries are released here (Y is S*NB*NI complex; dense S_bb, S_bb^-1)
+      for (void* p : {(void*)Y, (void*)Yc, (void*)d_Sbb, (void*)d_Sinv}) {
         cudaFree(p);
         allocs.erase(std::find(allocs.begin(), allocs.end(), p));
       }
+      d_Sbb = d_Sinv = nullptr;
     }
 
     // workspaces
@@ -434,6 +466,14 @@ struct Ctx {
     d_part = alloc<double2>((size_t)(vcap + 2) * mdot_blocks);
     d_red = alloc<double2>(3 * (vcap + 2));
     d_y = alloc<double2>(vcap + 2);
+    d_gst = alloc<GmresState>(1);
+    d_R = alloc<double2>((size_t)vcap * (vcap + 1) / 2);
+    d_gcos = alloc<double>(vcap + 1);
+    d_gsin = alloc<double2>(vcap + 1);
+    d_gvec = alloc<double2>(vcap + 2);
+    d_counter = alloc<unsigned int>(4);
+    zero(d_counter, 4);
+    CU(cudaMallocHost(&h_gst, sizeof(GmresState)));
     d_rhs = alloc<double2>(n);
     d_x = alloc<double2>(n);
     d_x2 = alloc<double2>(n);
@@ -454,9 +494,7 @@ struct Ctx {
     // coarse gemv may need > 48 KB of dynamic smem
     CU(cudaFuncSetAttribute(k_coarse_gemv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)std::max<size_t>(nc * sizeof(double2), 1)));
-    CU(cudaFuncSetAttribute(k_mdot<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(mdot_chunk * sizeof(double2))));
-    CU(cudaFuncSetAttribute(k_mupdate<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CU(cudaFuncSetAttribute(k_cgs_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(mdot_chunk * sizeof(double2))));
     setup_mass();
     sync();
@@ -499,12 +537,16 @@ struct Ctx {
   }
 
   void mass_solve(double* v) {  // in place, V^-1 v
+    const int dpn = P.dpn;
+    // along x: Ly*dpn lines of Lx entries, stride dpn
     launch(FETIGPU_K_GLOBAL, [&] {
-      k_tridiag_x<<<cdiv((long long)Ly * P.dpn, 128), 128, 0, stream>>>(Ly, Lx, P.dpn, d_mx_cp, d_mx_dinv, moff, v);
+      k_tridiag_lines<8, true><<<cdiv((long long)Ly * dpn, 8), dim3(32, 8), 0, stream>>>(
+          v, Ly * dpn, Lx, dpn, (long long)Lx * dpn, 1, dpn, d_mx_cp, d_mx_dinv, moff);
     });
+    // along y: Lx*dpn lines of Ly entries, stride Lx*dpn
     launch(FETIGPU_K_GLOBAL, [&] {
-      k_tridiag_y<<<cdiv((long long)Lx * P.dpn, 128), 128, 0, stream>>>(Ly, Lx * P.dpn, d_my_cp, d_my_dinv, moff, v,
-                                                                        Ly);
+      k_tridiag_lines<32, false><<<cdiv((long long)Lx * dpn, 32), dim3(32, 32), 0, stream>>>(
+          v, Lx * dpn, Ly, 1, 1, 0, (long long)Lx * dpn, d_my_cp, d_my_dinv, moff);
     });
   }
 
@@ -527,49 +569,114 @@ struct Ctx {
     });
   }
 
-  // F lam (feti.cpp:581-594) -> out
-  void apply_dual(const double2* lam, double2* out) {
-    launch(FETIGPU_K_DUAL_GEMV, [&] {
-      k_bnd_gemv<8><<<H.n_sub, 256, H.NB * sizeof(double2), stream>>>(H.NB, H.NC, d_Sinv, d_blam, d_bsign, lam, -1.0,
-                                                                       d_u1b, d_cpl_b, d_gcp);
-    });
+  size_t sym_smem() const {
+    const int noff = NT * (NT - 1) / 2;
+    return sizeof(double2) * 32 * (NT + (noff + NT) + noff);
+  }
+  SymGemvArgs sym_args(const double2* pack) const {
+    SymGemvArgs g{};
+    g.NB = H.NB;
+    g.NT = NT;
+    g.NC = H.NC;
+    g.NI = H.NI;
+    g.EBI = H.MAXE_BI;
+    g.pack = pack;
+    g.blam = d_blam;
+    g.bsign = d_bsign;
+    g.lam_lo = d_lam_lo;
+    g.lam_hi = d_lam_hi;
+    g.bi_idx = d_bi_idx;
+    g.bi_val = d_bi_val;
+    return g;
+  }
+  // local dual solve u1_b = S_bb^-1 t_b with t_b = -B^T lam, plus gcp = cpl_b^T t_b (K5)
+  void dual_gemv(SymGemvArgs g) {
+    g.alpha = -1.0;
+    g.out = d_u1b;
+    g.cpl_b = d_cpl_b;
+    g.gcp = d_gcp;
+    launch(FETIGPU_K_DUAL_GEMV, [&] { k_sym_gemv<<<H.n_sub, 256, sym_smem(), stream>>>(g); });
+  }
+  void dual_tail(double2* out) {
     coarse_solve(nullptr);
     launch(FETIGPU_K_LAMBDA, [&] {
       k_lam_gather_dual<<<cdiv(nl, 256), 256, 0, stream>>>(nl, H.NB, H.NC, d_lam_lo, d_lam_hi, d_u1b, d_cpl_b,
                                                            d_cglob, d_z, out);
     });
   }
-  // Dirichlet preconditioner (feti.cpp:597-627) -> out
+  // F lam (feti.cpp:581-594) -> out
+  void apply_dual(const double2* lam, double2* out) {
+    SymGemvArgs g = sym_args(d_Sinv_p);
+    g.mode = 0;
+    g.lam = lam;
+    dual_gemv(g);
+    dual_tail(out);
+  }
+  // Dirichlet preconditioner (feti.cpp:597-627): wb = S_bb (sign r / 2) per subdomain
+  void precond_gemv(const double2* r, const int* jsel) {
+    SymGemvArgs g = sym_args(d_Sbb_p);
+    g.mode = 0;
+    g.lam = r;
+    g.jsel = jsel;
+    g.jstride = ldv;
+    g.alpha = 0.5;
+    g.out = d_wb;
+    launch(FETIGPU_K_PRECOND_GEMV, [&] { k_sym_gemv<<<H.n_sub, 256, sym_smem(), stream>>>(g); });
+  }
   void apply_precond(const double2* r, double2* out) {
-    launch(FETIGPU_K_PRECOND_GEMV, [&] {
-      k_bnd_gemv<8><<<H.n_sub, 256, H.NB * sizeof(double2), stream>>>(H.NB, H.NC, d_Sbb, d_blam, d_bsign, r, 0.5,
-                                                                       d_wb, nullptr, nullptr);
-    });
+    precond_gemv(r, nullptr);
     launch(FETIGPU_K_LAMBDA, [&] {
       k_lam_gather_pre<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_lam_lo, d_lam_hi, d_wb, out);
     });
   }
+  // F P v in one pass over the interface: the dual GEMV gathers t_b = -sign (wb_lo - wb_hi)/2
+  // straight from the preconditioner's per-subdomain output (z = P v is never materialised)
+  void apply_dual_precond(const double2* v, const int* jsel, double2* out) {
+    precond_gemv(v, jsel);
+    SymGemvArgs g = sym_args(d_Sinv_p);
+    g.mode = 1;
+    g.wb = d_wb;
+    dual_gemv(g);
+    dual_tail(out);
+  }
 
-  // eliminate (feti.cpp:516-556) on (t_i = ti, t_b = tb, f_c = fc); leaves u_i in d_ri,
-  // u_b in d_u1b, z in d_z.
-  void eliminate(const double2* ti, const double2* tb, const double2* fc) {
+  // eliminate (feti.cpp:516-556), split in two halves.  A_rr is applied through its block
+  // factorization: y_i = A_ii^-1 t_i (banded), u1_b = S_bb^-1 (t_b - A_bi y_i) (dense),
+  // g = f_c - coupling^T t, z = C^-1 g, u_b = u1_b - cpl_b z.  Both eliminations of a FETI
+  // solve share t_i = f_i, so y_i is solved once (new_yi) and reused.
+  void eliminate_boundary(const double2* ti, const double2* tb, const double2* fc, bool new_yi) {
     const int S = H.n_sub, NI = H.NI, NB = H.NB;
-    CU(cudaMemcpyAsync(d_yi, ti, (size_t)S * NI * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
-    band_solve(d_colband, d_rowband, Wt, S, NI, d_yi, NI, NI, 1);
+    if (new_yi) {
+      CU(cudaMemcpyAsync(d_yi, ti, (size_t)S * NI * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+      band_solve(d_colband, d_rowband, Wt, S, NI, d_yi, NI, NI, 1);
+    }
+    {
+      SymGemvArgs g = sym_args(d_Sinv_p);
+      g.mode = 2;
+      g.tb = tb;
+      g.yi = d_yi;
+      g.alpha = 1.0;
+      g.out = d_u1b;
+      launch(FETIGPU_K_OTHER, [&] { k_sym_gemv<<<S, 256, sym_smem(), stream>>>(g); });
+    }
+    (void)NB;
+    launch(FETIGPU_K_OTHER, [&] { k_gcp_full<<<S, 256, 0, stream>>>(L, d_cpl_i, d_cpl_b, ti, tb, d_gcp); });
+    coarse_solve(fc);
     launch(FETIGPU_K_OTHER, [&] {
-      k_elim_b<8><<<S, 256, NB * sizeof(double2), stream>>>(L, d_Sinv, tb, d_bi_idx, d_bi_val, d_yi, d_u1b);
+      k_ub_correct<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(L, d_cglob, d_z, d_cpl_b, d_u1b);
     });
+  }
+  // interior harmonic extension u_i = A_ii^-1 (t_i - A_ib u_b - A_ic z) = y_i - A_ii^-1 (A_ib u_b + A_ic z)
+  // -> d_ri (requires eliminate_boundary first)
+  void eliminate_interior() {
+    const int S = H.n_sub, NI = H.NI;
     launch(FETIGPU_K_OTHER, [&] {
-      k_ib_apply<<<cdiv((long long)S * NI, 256), 256, 0, stream>>>(L, d_ib_idx, d_ib_val, d_u1b, d_ri);
+      k_ri_rhs<<<cdiv((long long)S * NI, 256), 256, 0, stream>>>(L, d_ib_idx, d_ib_val, d_Aic, d_cglob, d_z, d_u1b,
+                                                                 d_ri);
     });
     band_solve(d_colband, d_rowband, Wt, S, NI, d_ri, NI, NI, 1);
     launch(FETIGPU_K_OTHER, [&] {
-      k_elim_i_gcp<<<S, 256, 0, stream>>>(L, d_yi, d_ri, d_u1b, d_Aic, d_Abc, d_gcp);
-    });
-    coarse_solve(fc);
-    launch(FETIGPU_K_OTHER, [&] {
-      k_elim_final<<<cdiv((long long)S * (NI + NB), 256), 256, 0, stream>>>(L, d_cglob, d_z, d_cpl_i, d_cpl_b, d_ri,
-                                                                            d_u1b);
+      k_ui_final<<<cdiv((long long)S * NI, 256), 256, 0, stream>>>((long long)S * NI, d_yi, d_ri);
     });
   }
 
@@ -584,10 +691,59 @@ struct Ctx {
   }
 
   // ------------------------------------------------------------------------ GMRES
-  // Right-preconditioned unrestarted GMRES (krylov.hpp:102-223).  The Hermitian MGS of
-  // the reference is replaced by CGS2 (two classical passes, equal in exact arithmetic);
-  // Givens rotations, both stopping tests and the best-iterate fallback are the
-  // reference's, run on the host on the (j+2)-vector of coefficients of each step.
+  // Right-preconditioned unrestarted GMRES (krylov.hpp:102-223).  One Arnoldi step
+  // (precondition, dual operator, CGS2 orthogonalisation, Givens, both stopping tests,
+  // normalisation) is the fixed kernel sequence arnoldi_step(); j lives in device memory.
+  // Default: the step is captured once into the body of a CUDA-graph conditional WHILE
+  // node, so a whole cycle runs without returning to the host.  Eager mode (profiling)
+  // launches the same sequence step by step.  The reference's Hermitian MGS is replaced
+  // by CGS2 (two classical passes; equal in exact arithmetic).
+  void arnoldi_step(bool in_graph) {
+    double2* h1 = d_red;
+    double2* h2 = d_red + (vcap + 2);
+    double2* hn = d_red + 2 * (vcap + 2);
+    apply_dual_precond(d_V, &d_gst->j, d_w);
+    const size_t sm = mdot_chunk * sizeof(double2);
+    launch(FETIGPU_K_ORTHO, [&] {
+      k_cgs_pass<8><<<mdot_blocks, 256, sm, stream>>>(nl, mdot_chunk, d_V, ldv, d_gst, nullptr, d_w, 0, d_part, h1,
+                                                      d_counter);
+    });
+    launch(FETIGPU_K_ORTHO, [&] {
+      k_cgs_pass<8><<<mdot_blocks, 256, sm, stream>>>(nl, mdot_chunk, d_V, ldv, d_gst, h1, d_w, 0, d_part, h2,
+                                                      d_counter);
+    });
+    launch(FETIGPU_K_ORTHO, [&] {
+      k_givens<<<1, 32, 0, stream>>>(d_gst, h1, h2, hn, d_R, d_gcos, d_gsin, d_gvec, in_graph ? 1 : 0,
+                                     arnoldi_handle);
+    });
+    launch(FETIGPU_K_ORTHO, [&] {
+      k_update_normalize<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_gst, h2, d_w, d_V, ldv);
+    });
+  }
+
+  void build_arnoldi_graph() {
+    CU(cudaGraphCreate(&arnoldi_graph, 0));
+    CU(cudaGraphConditionalHandleCreate(&arnoldi_handle, arnoldi_graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = arnoldi_handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CU(cudaGraphAddNode(&node, arnoldi_graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    const long long before = launches;
+    const bool was_prof = prof;
+    prof = false;
+    CU(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    arnoldi_step(true);
+    CU(cudaStreamEndCapture(stream, &body));
+    prof = was_prof;
+    arnoldi_body_kernels = (int)(launches - before);
+    launches = before;
+    CU(cudaGraphInstantiate(&arnoldi_exec, arnoldi_graph, 0));
+  }
+
   fetigpu_feti_stats gmres(const double2* b, double2* x) {
     fetigpu_feti_stats st{};
     const double tol = desc.tol;
@@ -598,23 +754,17 @@ struct Ctx {
       st.converged = 1;
       return st;
     }
+    const bool graph = use_graph && !prof;
+    if (graph && !arnoldi_exec) build_arnoldi_graph();
     CU(cudaMemcpyAsync(d_r, b, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
     double best_res = 1.0;  // |b - F 0| / |b|
     CU(cudaMemcpyAsync(d_best, x, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
-    const int mr = std::max(1, max_iter);
-    std::vector<std::vector<cd>> Hc;  // columns of the Hessenberg, column j has j+2 entries
-    std::vector<double> gc(mr + 1);
-    std::vector<cd> gs(mr + 1), g(mr + 2);
+    int iterations = 0;
     double relres = 0;
     bool first = true;
     while (true) {
-      double rnorm;
-      if (first) {
-        rnorm = bnorm;
-        first = false;
-      } else {
-        rnorm = norm_max(d_r, nl).first;
-      }
+      const double rnorm = first ? bnorm : norm_max(d_r, nl).first;
+      first = false;
       relres = rnorm / bnorm;
       if (relres < best_res) {
         best_res = relres;
@@ -624,109 +774,48 @@ struct Ctx {
         st.converged = 1;
         break;
       }
-      if (st.iterations >= max_iter) break;
+      if (iterations >= max_iter) break;
+      // new cycle: V_0 = r / |r|, g = |r| e_0
       launch(FETIGPU_K_ORTHO, [&] { k_scale_copy<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, 1.0 / rnorm, d_V); });
-      std::fill(g.begin(), g.end(), cd(0));
-      g[0] = rnorm;
-      Hc.clear();
-      int k = 0;
-      for (int j = 0; j < mr && st.iterations < max_iter; ++j) {
-        if (j + 1 >= vcap) throw RuntimeError("gmres: basis capacity exceeded");
-        apply_precond(d_V + (size_t)j * ldv, d_zl);
-        apply_dual(d_zl, d_w);
-        const int nv = j + 1;
-        // pass 1: h1 = V^H w, |w|^2
-        launch(FETIGPU_K_ORTHO, [&] {
-          k_mdot<8><<<mdot_blocks, 256, mdot_chunk * sizeof(double2), stream>>>(nl, mdot_chunk, d_V, ldv, nv, d_w, 1,
-                                                                              d_part);
-        });
-        double2* h1 = d_red;
-        double2* h2 = d_red + (vcap + 2);
-        double2* hn = d_red + 2 * (vcap + 2);
-        launch(FETIGPU_K_ORTHO, [&] { k_reduce_parts<<<nv + 1, 32, 0, stream>>>(nv + 1, mdot_blocks, d_part, h1); });
-        // pass 2: w -= V h1 ; h2 = V^H w
-        launch(FETIGPU_K_ORTHO, [&] {
-          k_mupdate<8><<<mdot_blocks, 256, mdot_chunk * sizeof(double2), stream>>>(nl, mdot_chunk, d_V, ldv, nv, h1,
-                                                                                  d_w, 1, d_part);
-        });
-        launch(FETIGPU_K_ORTHO, [&] { k_reduce_parts<<<nv + 1, 32, 0, stream>>>(nv + 1, mdot_blocks, d_part, h2); });
-        // pass 3: w -= V h2 ; |w|^2
-        launch(FETIGPU_K_ORTHO, [&] {
-          k_mupdate<8><<<mdot_blocks, 256, mdot_chunk * sizeof(double2), stream>>>(nl, mdot_chunk, d_V, ldv, nv, h2,
-                                                                                  d_w, 0, d_part);
-        });
-        launch(FETIGPU_K_ORTHO, [&] { k_reduce_parts<<<1, 32, 0, stream>>>(1, mdot_blocks, d_part, hn); });
-        CU(cudaMemcpyAsync(h_pin, h1, sizeof(double2) * (nv + 1), cudaMemcpyDeviceToHost, stream));
-        CU(cudaMemcpyAsync(h_pin + (nv + 1), h2, sizeof(double2) * nv, cudaMemcpyDeviceToHost, stream));
-        CU(cudaMemcpyAsync(h_pin + (2 * nv + 1), hn, sizeof(double2), cudaMemcpyDeviceToHost, stream));
+      *h_gst = GmresState{};
+      h_gst->j = 0;
+      h_gst->iterations = iterations;
+      h_gst->cont = 1;
+      h_gst->max_iter = max_iter;
+      h_gst->m = std::max(1, std::min(max_iter, vcap - 1));
+      h_gst->tol = tol;
+      h_gst->bnorm = bnorm;
+      CU(cudaMemcpyAsync(d_gst, h_gst, sizeof(GmresState), cudaMemcpyHostToDevice, stream));
+      h_pin[0] = make_double2(rnorm, 0.0);
+      CU(cudaMemcpyAsync(d_gvec, h_pin, sizeof(double2), cudaMemcpyHostToDevice, stream));
+      if (graph) {
+        CU(cudaGraphLaunch(arnoldi_exec, stream));
+        CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
         sync();
-        const double wpre = std::sqrt(h_pin[nv].x);
-        std::vector<cd> col(j + 2);
-        bool finite = true;
-        for (int i = 0; i <= j; ++i) {
-          col[i] = cd(h_pin[i].x, h_pin[i].y) + cd(h_pin[nv + 1 + i].x, h_pin[nv + 1 + i].y);
-          finite = finite && std::isfinite(col[i].real()) && std::isfinite(col[i].imag());
-        }
-        const double hnext = std::sqrt(std::max(0.0, h_pin[2 * nv + 1].x));
-        if (!std::isfinite(hnext) || !finite) throw NumericalError("gmres: breakdown (NaN/Inf in Arnoldi)");
-        col[j + 1] = hnext;
-        for (int i = 0; i < j; ++i) {  // previous rotations (krylov.hpp:169-173)
-          const cd t1 = col[i], t2 = col[i + 1];
-          col[i] = gc[i] * t1 + gs[i] * t2;
-          col[i + 1] = -std::conj(gs[i]) * t1 + gc[i] * t2;
-        }
-        {  // make_givens (krylov.hpp:66-83)
-          const cd h1v = col[j], h2v = col[j + 1];
-          const double a1 = std::abs(h1v), a2 = std::abs(h2v);
-          if (a2 == 0.0) {
-            gc[j] = 1.0;
-            gs[j] = 0.0;
-          } else if (a1 == 0.0) {
-            gc[j] = 0.0;
-            gs[j] = 1.0;
-          } else {
-            const double tt = std::hypot(a1, a2);
-            gc[j] = a1 / tt;
-            gs[j] = (h1v / a1) * (std::conj(h2v) / tt);
-          }
-        }
-        col[j] = gc[j] * col[j] + gs[j] * col[j + 1];
-        col[j + 1] = 0.0;
-        g[j + 1] = -std::conj(gs[j]) * g[j];
-        g[j] = gc[j] * g[j];
-        Hc.push_back(col);
-        ++st.iterations;
-        k = j + 1;
-        const double est = std::abs(g[j + 1]);
-        const bool happy = hnext <= 1e-14 * std::max(wpre, 1e-300);
-        if (happy || est <= tol * bnorm) break;
-        launch(FETIGPU_K_ORTHO, [&] {
-          k_scale_copy<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_w, 1.0 / hnext, d_V + (size_t)(j + 1) * ldv);
-        });
+        launches += (long long)arnoldi_body_kernels * (h_gst->iterations - iterations);
+      } else {
+        do {
+          arnoldi_step(false);
+          CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
+          sync();
+        } while (h_gst->cont);
       }
-      // back substitution (krylov.hpp:191-196) and x += P^-1 (Q y)
-      std::vector<cd> y(k);
-      for (int i = k - 1; i >= 0; --i) {
-        cd acc = g[i];
-        for (int j2 = i + 1; j2 < k; ++j2) acc -= Hc[j2][i] * y[j2];
-        y[i] = acc / Hc[i][i];
-      }
-      for (int i = 0; i < k; ++i) h_pin[i] = make_double2(y[i].real(), y[i].imag());
-      CU(cudaMemcpyAsync(d_y, h_pin, sizeof(double2) * k, cudaMemcpyHostToDevice, stream));
-      launch(FETIGPU_K_ORTHO, [&] {
-        k_combine<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_V, ldv, k, d_y, d_t);
-      });
+      if (h_gst->status) throw NumericalError("gmres: breakdown (NaN/Inf in Arnoldi)");
+      iterations = h_gst->iterations;
+      // back substitution and x += P^-1 (Q y)  (krylov.hpp:191-209), true residual r = b - F x
+      launch(FETIGPU_K_ORTHO, [&] { k_backsub<<<1, 32, 0, stream>>>(d_gst, d_R, d_gvec, d_y); });
+      launch(FETIGPU_K_ORTHO, [&] { k_combine<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_V, ldv, d_gst, d_y, d_t); });
       apply_precond(d_t, d_zl);
       launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nl, 256), 256, 0, stream>>>(nl, x, d_zl); });
       apply_dual(x, d_w);
       launch(FETIGPU_K_ORTHO, [&] { k_sub<<<cdiv(nl, 256), 256, 0, stream>>>(nl, b, d_w, d_r); });
-      sync();  // h_pin is reused by the next norm
     }
     // krylov.hpp:214-220: the final residual equals the last cycle's r; best-iterate fallback
     if (relres > best_res) {
       CU(cudaMemcpyAsync(x, d_best, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
       relres = best_res;
     }
+    st.iterations = iterations;
     st.relative_residual = relres;
     st.converged = relres <= tol;
     return st;
@@ -754,7 +843,7 @@ struct Ctx {
     });
     if (nc > 0)
       launch(FETIGPU_K_OTHER, [&] { k_gather_corner<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_dof, rhs, d_fc); });
-    eliminate(d_fi, d_fb, d_fc);
+    eliminate_boundary(d_fi, d_fb, d_fc, true);
     launch(FETIGPU_K_LAMBDA, [&] { k_jump<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_lam_lo, d_lam_hi, d_u1b, d_d); });
     const fetigpu_feti_stats gst = gmres(d_d, d_lam);
     st.iterations = gst.iterations;
@@ -763,7 +852,8 @@ struct Ctx {
     launch(FETIGPU_K_OTHER, [&] {
       k_recover_tb<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(S * NB, d_blam, d_bsign, d_fb, d_lam, d_tb);
     });
-    eliminate(d_fi, d_tb, d_fc);
+    eliminate_boundary(d_fi, d_tb, d_fc, false);
+    eliminate_interior();
     launch(FETIGPU_K_OTHER, [&] {
       k_assemble_x<<<cdiv(n, 256), 256, 0, stream>>>(n, d_xkind, d_xa, d_xb, d_ri, d_u1b, d_z, x);
     });
@@ -834,10 +924,10 @@ struct Ctx {
   double class_bytes(int klass) const {
     const double S = H.n_sub, NB = H.NB;
     switch (klass) {
-      case FETIGPU_K_PRECOND_GEMV:  // S_bb streamed once + lambda gather + out_b
-        return 16.0 * (S * NB * NB + 2.0 * S * NB) + 12.0 * S * NB;
-      case FETIGPU_K_DUAL_GEMV:  // S_bb^-1 + coupling_b + vectors
-        return 16.0 * (S * NB * NB + S * NB * H.NC + 2.0 * S * NB + S * H.NC) + 12.0 * S * NB;
+      case FETIGPU_K_PRECOND_GEMV:  // packed S_bb streamed once + interface vectors in/out
+        return 16.0 * (S * sym_tile_entries(NT) + 2.0 * S * NB) + 12.0 * S * NB;
+      case FETIGPU_K_DUAL_GEMV:  // packed S_bb^-1 + coupling_b + vectors
+        return 16.0 * (S * sym_tile_entries(NT) + S * NB * H.NC + 3.0 * S * NB + S * H.NC) + 12.0 * S * NB;
       case FETIGPU_K_BAND:  // one single-RHS solve: both factor sweeps + vector in/out
         return 16.0 * (2.0 * S * H.NI * (Wt + 1) + 3.0 * S * H.NI);
       case FETIGPU_K_COARSE:

@@ -332,9 +332,11 @@ template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
     k_bnd_gemv(int NB, int NC, const double2* __restrict__ M, const int* __restrict__ blam,
                const double* __restrict__ bsign, const double2* __restrict__ lam, double alpha,
-               double2* __restrict__ out_b, const double2* __restrict__ cpl_b, double2* __restrict__ gcp) {
+               double2* __restrict__ out_b, const double2* __restrict__ cpl_b, double2* __restrict__ gcp,
+               const int* __restrict__ jsel = nullptr, size_t jstride = 0) {
   extern __shared__ double2 in_sh[];
   const int s = blockIdx.x;
+  if (jsel != nullptr) lam += (size_t)(*jsel) * jstride;  // GMRES basis column V_j
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int k = threadIdx.x; k < NB; k += blockDim.x) {
     const int r = blam[(size_t)s * NB + k];
@@ -373,6 +375,176 @@ __global__ void __launch_bounds__(WARPS * 32)
       for (int k = lane; k < NB; k += 32) acc = cfma(cpl_b[((size_t)s * NB + k) * NC + c], in_sh[k], acc);
       acc = warp_sum2(acc);
       if (lane == 0) gcp[(size_t)s * NC + c] = acc;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ packed symmetric GEMV
+// S_bb and S_bb^-1 are complex symmetric (A_rr = A_rr^T).  They are stored as the lower
+// triangle of 32x32 tiles (NT = ceil(NB/32) tiles per dimension), "diagonal-major":
+//   off-diagonal tile (I, J), J < I :  O[c][l] = M[32I + l][32J + (l+c) mod 32],  c = 0..31
+//   diagonal tile (I, I)             :  D[c][l] = M[32I + l][32I + (l+c) mod 32],  c = 0..16
+// so at step c lane l streams entry (l, l+c): coalesced 512 B per warp-load, the row
+// product accumulates in the lane, and the transposed product is carried in a register
+// rotated by one lane per step (no per-row reductions).  Bytes per subdomain:
+// NT*17*512 + NT(NT-1)/2*16384 (133 KB at NB = 124 vs 246 KB dense).
+__host__ __device__ constexpr int sym_tile_entries(int NT) { return NT * 17 * 32 + NT * (NT - 1) / 2 * 1024; }
+
+// pack[s] <- full[s] (row-major NB x NB); entries outside NB are zero
+__global__ void k_pack_sym(int S, int NB, int NT, const double2* __restrict__ full, double2* __restrict__ pack) {
+  const int per = sym_tile_entries(NT);
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)S * per) return;
+  const int s = (int)(gid / per);
+  int e = (int)(gid % per);
+  int r, c;
+  const int ndiag = NT * 17 * 32;
+  if (e < ndiag) {
+    const int I = e / (17 * 32);
+    e %= 17 * 32;
+    const int cc = e / 32, l = e % 32;
+    r = 32 * I + l;
+    c = 32 * I + ((l + cc) & 31);
+  } else {
+    e -= ndiag;
+    const int t = e / 1024;
+    e %= 1024;
+    int I = 1;
+    while ((I + 1) * I / 2 <= t) ++I;
+    const int J = t - I * (I - 1) / 2;
+    const int cc = e / 32, l = e % 32;
+    r = 32 * I + l;
+    c = 32 * J + ((l + cc) & 31);
+  }
+  pack[gid] = (r < NB && c < NB) ? full[((size_t)s * NB + r) * NB + c] : cz();
+}
+
+struct SymGemvArgs {
+  int NB, NT, NC, NI, EBI;
+  const double2* pack;  // [S][sym_tile_entries(NT)]
+  // inputs
+  int mode;                       // 0: in = alpha sign lam[blam]; 1: in = alpha sign (wb_lo - wb_hi)/2; 2: in = tb - A_bi yi
+  const int* blam;
+  const double* bsign;
+  const double2* lam;
+  const int* jsel;                // mode 0: lam += (*jsel) * jstride (GMRES basis column)
+  size_t jstride;
+  double alpha;
+  const int* lam_lo;
+  const int* lam_hi;
+  const double2* wb;
+  const double2* tb;
+  const int* bi_idx;
+  const double2* bi_val;
+  const double2* yi;
+  // outputs
+  double2* out;                   // [S][NB]
+  const double2* cpl_b;           // optional: gcp = cpl_b^T in
+  double2* gcp;
+};
+
+__global__ void __launch_bounds__(256) k_sym_gemv(SymGemvArgs a) {
+  constexpr int WARPS = 8;
+  // dynamic smem: x (32 NT) | row partials (ntiles x 32) | column partials (noff x 32)
+  extern __shared__ double2 sg_sh[];
+  const int NB = a.NB, NT = a.NT;
+  const int noff = NT * (NT - 1) / 2, ntiles = noff + NT;
+  double2* x_sh = sg_sh;
+  double2 (*part_row)[32] = reinterpret_cast<double2 (*)[32]>(sg_sh + 32 * NT);
+  double2 (*part_col)[32] = reinterpret_cast<double2 (*)[32]>(sg_sh + 32 * NT + 32 * ntiles);
+  const int s = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // ---- input vector (B^T scatter) ----
+  const double2* lam = a.lam;
+  if (a.mode == 0 && a.jsel != nullptr) lam += (size_t)(*a.jsel) * a.jstride;
+  for (int k = threadIdx.x; k < 32 * NT; k += blockDim.x) {
+    double2 v = cz();
+    if (k < NB) {
+      const size_t sb = (size_t)s * NB + k;
+      if (a.mode == 2) {
+        v = a.tb[sb];
+        for (int e = 0; e < a.EBI; ++e) {
+          const int i = a.bi_idx[sb * a.EBI + e];
+          if (i >= 0) v = cfms(a.bi_val[sb * a.EBI + e], a.yi[(size_t)s * a.NI + i], v);
+        }
+      } else {
+        const int r = a.blam[sb];
+        if (r >= 0) {
+          double2 z;
+          if (a.mode == 0)
+            z = lam[r];
+          else
+            z = cscale(csub(a.wb[a.lam_lo[r]], a.wb[a.lam_hi[r]]), 0.5);
+          v = cscale(z, a.alpha * a.bsign[sb]);
+        }
+      }
+    }
+    x_sh[k] = v;
+  }
+  __syncthreads();
+  // ---- tiles: off-diagonal first (t < noff), then diagonal.  A diagonal tile streams half
+  // the bytes of an off-diagonal one, so when they fit, two diagonal tiles share a warp
+  // (NT = 4: warps 0-5 one off-diagonal tile each, warps 6-7 two diagonal tiles each).
+  const double2* P = a.pack + (size_t)s * sym_tile_entries(NT);
+  const bool paired = noff + (NT + 1) / 2 <= WARPS;
+  for (int item = warp; item < (paired ? noff + (NT + 1) / 2 : ntiles); item += WARPS)
+  for (int half = 0; half < ((paired && item >= noff) ? 2 : 1); ++half) {
+    const int t = (paired && item >= noff) ? noff + 2 * (item - noff) + half : item;
+    if (t >= ntiles) break;
+    double2 yr = cz(), yc = cz();
+    if (t < noff) {
+      int I = 1;
+      while ((I + 1) * I / 2 <= t) ++I;
+      const int J = t - I * (I - 1) / 2;
+      const double2* O = P + NT * 17 * 32 + (size_t)t * 1024;
+      const double2 xi = x_sh[32 * I + lane];
+#pragma unroll 8
+      for (int c = 0; c < 32; ++c) {
+        const double2 m = __ldcs(O + c * 32 + lane);
+        yr = cfma(m, x_sh[32 * J + ((lane + c) & 31)], yr);
+        yc = cfma(m, xi, yc);
+        yc = shfl2(yc, (lane + 1) & 31);  // carry column (l+c+1) into lane l
+      }
+      // after 32 rotations lane l holds column l
+      part_row[t][lane] = yr;
+      part_col[t][lane] = yc;
+    } else {
+      const int I = t - noff;
+      const double2* D = P + (size_t)I * 17 * 32;
+      const double2 xi = x_sh[32 * I + lane];
+      yr = cmul(__ldcs(D + lane), xi);
+      // c = 1..15: row + transposed; carry for the transposed part as above
+#pragma unroll 5
+      for (int c = 1; c < 16; ++c) {
+        const double2 m = __ldcs(D + c * 32 + lane);
+        yr = cfma(m, x_sh[32 * I + ((lane + c) & 31)], yr);
+        yc = shfl2(yc, (lane + 1) & 31);
+        yc = cfma(m, xi, yc);
+      }
+      // yc in lane l now holds column (l + 15); c = 16 covers both (l, l+16) and (l+16, l)
+      {
+        const double2 m = __ldcs(D + 16 * 32 + lane);
+        yr = cfma(m, x_sh[32 * I + ((lane + 16) & 31)], yr);
+      }
+      yc = shfl2(yc, (lane + 17) & 31);  // lane l <- column l
+      part_row[t][lane] = cadd(yr, yc);
+    }
+  }
+  __syncthreads();
+  // ---- deterministic combination: y_I = sum_J<I rows(I,J) + diag(I) + sum_{I'>I} cols(I',I) ----
+  for (int k = threadIdx.x; k < NB; k += blockDim.x) {
+    const int I = k >> 5, l = k & 31;
+    double2 acc = part_row[noff + I][l];
+    for (int J = 0; J < I; ++J) acc = cadd(acc, part_row[I * (I - 1) / 2 + J][l]);
+    for (int I2 = I + 1; I2 < NT; ++I2) acc = cadd(acc, part_col[I2 * (I2 - 1) / 2 + I][l]);
+    a.out[(size_t)s * NB + k] = acc;
+  }
+  if (a.gcp != nullptr) {
+    for (int c = warp; c < a.NC; c += WARPS) {
+      double2 acc = cz();
+      for (int k = lane; k < NB; k += 32) acc = cfma(a.cpl_b[((size_t)s * NB + k) * a.NC + c], x_sh[k], acc);
+      acc = warp_sum2(acc);
+      if (lane == 0) a.gcp[(size_t)s * a.NC + c] = acc;
     }
   }
 }
@@ -469,7 +641,7 @@ __global__ void k_recover_tb(int nsb, const int* __restrict__ blam, const double
   tb[k] = r >= 0 ? cfms(make_double2(bsign[k], 0.0), lam[r], fb[k]) : cz();
 }
 
-// u1_b = S_bb^-1 (t_b - A_bi y_i) and gcp_b[c] = sum_k A_bc(k,c) u1_b[k]; one CTA per subdomain
+// u1_b = S_bb^-1 (t_b - A_bi y_i); one CTA per subdomain
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
     k_elim_b(SubLayout L, const double2* __restrict__ Sinv, const double2* __restrict__ tb,
@@ -496,37 +668,25 @@ __global__ void __launch_bounds__(WARPS * 32)
     if (lane == 0) u1b[(size_t)s * L.NB + row] = a;
   }
 }
-// r_i = A_ib u1_b
-__global__ void k_ib_apply(SubLayout L, const int* __restrict__ ib_idx, const double2* __restrict__ ib_val,
-                           const double2* __restrict__ u1b, double2* __restrict__ ri) {
-  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long long)L.S * L.NI) return;
-  const int s = (int)(gid / L.NI);
-  double2 acc = cz();
-  for (int e = 0; e < L.EIB; ++e) {
-    const int b = ib_idx[gid * L.EIB + e];
-    if (b >= 0) acc = cfma(ib_val[gid * L.EIB + e], u1b[(size_t)s * L.NB + b], acc);
-  }
-  ri[gid] = acc;
-}
-// u1_i = y_i - ri (ri already A_ii^-1 A_ib u1_b); gcp[c] = A_ic^T u1_i + A_bc^T u1_b
-__global__ void k_elim_i_gcp(SubLayout L, const double2* __restrict__ yi, double2* __restrict__ ri,
-                             const double2* __restrict__ u1b, const double2* __restrict__ Aic,
-                             const double2* __restrict__ Abc, double2* __restrict__ gcp) {
+// gcp[s][c] = (A_rc^T A_rr^-1 t)_c = sum_i cpl_i(i,c) t_i + sum_k cpl_b(k,c) t_b   (feti.cpp:530;
+// equal to A_rc^T u1 because A_rr^-1 is symmetric).  One CTA per subdomain.
+__global__ void k_gcp_full(SubLayout L, const double2* __restrict__ cpl_i, const double2* __restrict__ cpl_b,
+                           const double2* __restrict__ ti, const double2* __restrict__ tb, double2* __restrict__ gcp) {
   __shared__ double2 red[8][32];
   const int s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2 acc[8];
+#pragma unroll
   for (int c = 0; c < 8; ++c) acc[c] = cz();
   for (int i = threadIdx.x; i < L.NI; i += blockDim.x) {
     const size_t si = (size_t)s * L.NI + i;
-    const double2 u = csub(yi[si], ri[si]);
-    ri[si] = u;  // ri now holds u1_i
-    for (int c = 0; c < L.NC; ++c) acc[c] = cfma(Aic[si * L.NC + c], u, acc[c]);
+    const double2 t = ti[si];
+    for (int c = 0; c < L.NC; ++c) acc[c] = cfma(cpl_i[si * L.NC + c], t, acc[c]);
   }
   for (int k = threadIdx.x; k < L.NB; k += blockDim.x) {
     const size_t sb = (size_t)s * L.NB + k;
-    for (int c = 0; c < L.NC; ++c) acc[c] = cfma(Abc[sb * L.NC + c], u1b[sb], acc[c]);
+    const double2 t = tb[sb];
+    for (int c = 0; c < L.NC; ++c) acc[c] = cfma(cpl_b[sb * L.NC + c], t, acc[c]);
   }
   for (int c = 0; c < L.NC; ++c) {
     const double2 v = warp_sum2(acc[c]);
@@ -539,24 +699,41 @@ __global__ void k_elim_i_gcp(SubLayout L, const double2* __restrict__ yi, double
     gcp[(size_t)s * L.NC + threadIdx.x] = t;
   }
 }
-// u = u1 - coupling z_loc (feti.cpp:542-555), interior and boundary slabs
-__global__ void k_elim_final(SubLayout L, const int* __restrict__ cglob, const double2* __restrict__ z,
-                             const double2* __restrict__ cpl_i, const double2* __restrict__ cpl_b,
-                             double2* __restrict__ ui, double2* __restrict__ ub) {
-  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long ni = (long long)L.S * L.NI, nb = (long long)L.S * L.NB;
-  if (gid >= ni + nb) return;
-  const bool interior = gid < ni;
-  const long long k = interior ? gid : gid - ni;
-  const int s = (int)(k / (interior ? L.NI : L.NB));
-  const double2* cp = (interior ? cpl_i : cpl_b) + k * L.NC;
+// u_b = u1_b - cpl_b z_loc  (feti.cpp:542-555, boundary rows)
+__global__ void k_ub_correct(SubLayout L, const int* __restrict__ cglob, const double2* __restrict__ z,
+                             const double2* __restrict__ cpl_b, double2* __restrict__ ub) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (long long)L.S * L.NB) return;
+  const int s = (int)(k / L.NB);
   double2 acc = cz();
   for (int c = 0; c < L.NC; ++c) {
     const int cg = cglob[(size_t)s * L.NC + c];
-    if (cg >= 0) acc = cfma(cp[c], z[cg], acc);
+    if (cg >= 0) acc = cfma(cpl_b[k * L.NC + c], z[cg], acc);
   }
-  double2* u = interior ? ui : ub;
-  u[k] = csub(u[k], acc);
+  ub[k] = csub(ub[k], acc);
+}
+// r_i = A_ib u_b + A_ic z_loc  (rhs of the interior harmonic extension)
+__global__ void k_ri_rhs(SubLayout L, const int* __restrict__ ib_idx, const double2* __restrict__ ib_val,
+                         const double2* __restrict__ Aic, const int* __restrict__ cglob, const double2* __restrict__ z,
+                         const double2* __restrict__ ub, double2* __restrict__ ri) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)L.S * L.NI) return;
+  const int s = (int)(gid / L.NI);
+  double2 acc = cz();
+  for (int e = 0; e < L.EIB; ++e) {
+    const int b = ib_idx[gid * L.EIB + e];
+    if (b >= 0) acc = cfma(ib_val[gid * L.EIB + e], ub[(size_t)s * L.NB + b], acc);
+  }
+  for (int c = 0; c < L.NC; ++c) {
+    const int cg = cglob[(size_t)s * L.NC + c];
+    if (cg >= 0) acc = cfma(Aic[gid * L.NC + c], z[cg], acc);
+  }
+  ri[gid] = acc;
+}
+// u_i = y_i - A_ii^-1 r_i   (r_i already solved in place)
+__global__ void k_ui_final(long long cnt, const double2* __restrict__ yi, double2* __restrict__ ri) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < cnt) ri[k] = csub(yi[k], ri[k]);
 }
 // d[r] = u_lo - u_hi (gather_jump, feti.cpp:560-569)
 __global__ void k_jump(int nl, const int* __restrict__ lo, const int* __restrict__ hi, const double2* __restrict__ ub,
@@ -582,53 +759,49 @@ __global__ void k_assemble_x(int n, const int* __restrict__ kind, const int* __r
 }
 
 // ------------------------------------------------------------------ GMRES (K7)
-// Partial Hermitian dots of w against nv basis vectors (+ |w|^2 when with_norm):
-// part[i][blk] = sum_{chunk} conj(V_i) w.  w chunk staged in shared memory.
+// Device-resident Arnoldi state.  One Arnoldi step (krylov.hpp:150-188) is a fixed kernel
+// sequence that reads j from here, so it can run eagerly or inside a CUDA-graph
+// conditional WHILE node with no host round trip per step.
+struct GmresState {
+  int j;           // current column
+  int iterations;  // Arnoldi steps so far (SolveStats::iterations)
+  int k;           // columns completed this cycle
+  int cont;        // 1 while the cycle continues
+  int status;      // 1 = NaN/Inf breakdown (krylov.hpp:165-166)
+  int max_iter;
+  int m;           // restart length (= max_iter: unrestarted, feti.cpp:684)
+  int pad;
+  double tol, bnorm, inv_hnext, est;
+};
+
+// One classical Gram-Schmidt pass on the block's chunk of w:
+//   (optional) w -= sum_i h_in[i] V_i ; then partial sums of conj(V_i) w (dots) and/or |w|^2
+// reduced by the last block to finish (fixed order => deterministic).  nv = *jptr + 1.
+// mode 0: dots + norm (out[0..nv]) ; 1: dots (out[0..nv-1]) ; 2: norm only (out[0]).
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
-    k_mdot(int n, int chunk, const double2* __restrict__ V, size_t ldv, int nv, const double2* __restrict__ w,
-           int with_norm, double2* __restrict__ part) {
+    k_cgs_pass(int n, int chunk, const double2* __restrict__ V, size_t ldv, const GmresState* __restrict__ st,
+               const double2* __restrict__ h_in, double2* __restrict__ w, int mode, double2* __restrict__ part,
+               double2* __restrict__ out, unsigned int* __restrict__ counter) {
   extern __shared__ double2 w_sh[];
-  const int b = blockIdx.x, lo = b * chunk, len = min(chunk, n - lo);
+  __shared__ bool is_last;
+  const int nv = st->j + 1;
+  const int b = blockIdx.x, lo = b * chunk, len = max(0, min(chunk, n - lo));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = threadIdx.x; k < len; k += blockDim.x) w_sh[k] = w[lo + k];
-  __syncthreads();
-  const int nout = nv + (with_norm ? 1 : 0);
-  for (int i = warp; i < nout; i += WARPS) {
-    double2 acc = cz();
-    if (i < nv) {
-      const double2* v = V + (size_t)i * ldv + lo;
-      for (int k = lane; k < len; k += 32) acc = cfma_conj(v[k], w_sh[k], acc);
-    } else {
-      for (int k = lane; k < len; k += 32) acc.x += cabs2(w_sh[k]);
-    }
-    acc = warp_sum2(acc);
-    if (lane == 0) part[(size_t)i * gridDim.x + b] = acc;
-  }
-}
-// w -= sum_i h_i V_i on the block's chunk, then partial dots again (CGS2 second pass)
-// or |w|^2 only (final pass).
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    k_mupdate(int n, int chunk, const double2* __restrict__ V, size_t ldv, int nv, const double2* __restrict__ h,
-              double2* __restrict__ w, int dots, double2* __restrict__ part) {
-  extern __shared__ double2 w_sh[];
-  const int b = blockIdx.x, lo = b * chunk, len = min(chunk, n - lo);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ double2 h_sh[1024];
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) h_sh[i] = h[i];
-  __syncthreads();
   for (int k = threadIdx.x; k < len; k += blockDim.x) {
     double2 acc = w[lo + k];
-    for (int i = 0; i < nv; ++i) acc = cfms(h_sh[i], V[(size_t)i * ldv + lo + k], acc);
-    w[lo + k] = acc;
+    if (h_in != nullptr) {
+      for (int i = 0; i < nv; ++i) acc = cfms(h_in[i], V[(size_t)i * ldv + lo + k], acc);
+      w[lo + k] = acc;
+    }
     w_sh[k] = acc;
   }
   __syncthreads();
-  const int nout = dots ? nv + 1 : 1;
+  const int ndots = (mode == 2) ? 0 : nv;
+  const int nout = ndots + (mode == 1 ? 0 : 1);
   for (int i = warp; i < nout; i += WARPS) {
     double2 acc = cz();
-    if (dots && i < nv) {
+    if (i < ndots) {
       const double2* v = V + (size_t)i * ldv + lo;
       for (int k = lane; k < len; k += 32) acc = cfma_conj(v[k], w_sh[k], acc);
     } else {
@@ -637,38 +810,158 @@ __global__ void __launch_bounds__(WARPS * 32)
     acc = warp_sum2(acc);
     if (lane == 0) part[(size_t)i * gridDim.x + b] = acc;
   }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int i = warp; i < nout; i += WARPS) {
+    double2 acc = cz();
+    for (int bb = lane; bb < (int)gridDim.x; bb += 32) acc = cadd(acc, __ldcg(part + (size_t)i * gridDim.x + bb));
+    acc = warp_sum2(acc);
+    if (lane == 0) out[i] = acc;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
 }
-// out[i] = sum_b part[i][b] (fixed order => deterministic), optional accumulate into acc
-__global__ void k_reduce_parts(int nout, int nblk, const double2* __restrict__ part, double2* __restrict__ out) {
-  const int i = blockIdx.x;
+
+// Hessenberg column update, Givens rotations and both stopping tests of one Arnoldi
+// step (krylov.hpp:164-188).  R is the rotated Hessenberg, packed by columns (column j at
+// R + j(j+1)/2).  One warp: the rotation operands are staged in shared memory, the
+// sequential rotation chain runs on lane 0.  In graph mode it drives the WHILE node.
+__global__ void __launch_bounds__(32) k_givens(GmresState* __restrict__ st, const double2* __restrict__ h1,
+                                               const double2* __restrict__ h2, const double2* __restrict__ hn,
+                                               double2* __restrict__ R, double* __restrict__ gcos,
+                                               double2* __restrict__ gsin, double2* __restrict__ g, int in_graph,
+                                               cudaGraphConditionalHandle handle) {
+  constexpr int CHK = 256;
+  __shared__ double sc[CHK];
+  __shared__ double2 ss[CHK], sh[CHK + 1];
   const int lane = threadIdx.x;
-  double2 acc = cz();
-  for (int b = lane; b < nblk; b += 32) acc = cadd(acc, part[(size_t)i * nblk + b]);
-  acc = warp_sum2(acc);
-  if (lane == 0) out[i] = acc;
+  const int j = st->j;
+  double2* col = R + (size_t)j * (j + 1) / 2;
+  bool finite = true;
+  for (int i = lane; i <= j; i += 32) {
+    const double2 v = cadd(h1[i], h2[i]);
+    finite = finite && isfinite(v.x) && isfinite(v.y);
+  }
+  finite = __all_sync(0xffffffffu, finite);
+  const double wpre = sqrt(h1[j + 1].x);
+  // |w - V h2|^2 = |w|^2 - sum |h2_i|^2 (V orthonormal, h2 = V^H w is the round-off-sized
+  // reorthogonalisation correction: no cancellation)
+  double s2 = 0.0;
+  for (int i = lane; i <= j; i += 32) s2 += cabs2(h2[i]);
+  s2 = warp_sum(s2);
+  const double hnext = sqrt(fmax(0.0, h2[j + 1].x - s2));
+  (void)hn;
+  finite = finite && isfinite(hnext);
+  if (!finite) {
+    if (lane == 0) {
+      st->status = 1;
+      st->cont = 0;
+      if (in_graph) cudaGraphSetConditional(handle, 0u);
+    }
+    return;
+  }
+  // previous rotations (krylov.hpp:169-173): carry = rotated entry i, t2 = original entry i+1
+  double2 carry = cadd(h1[0], h2[0]);
+  for (int base = 0; base < j; base += CHK) {
+    const int cnt = min(CHK, j - base);
+    for (int q = lane; q < cnt; q += 32) {
+      sc[q] = gcos[base + q];
+      ss[q] = gsin[base + q];
+      sh[q] = cadd(h1[base + q + 1], h2[base + q + 1]);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      for (int q = 0; q < cnt; ++q) {
+        const double c = sc[q];
+        const double2 s = ss[q], t1 = carry, t2 = sh[q];
+        col[base + q] = cfma(s, t2, cscale(t1, c));
+        carry = cfms(cconj(s), t1, cscale(t2, c));
+      }
+    }
+    __syncwarp();
+  }
+  if (lane != 0) return;
+  // make_givens (krylov.hpp:66-83) on (carry = rotated col[j], hnext)
+  const double2 a = carry;
+  const double a1 = sqrt(cabs2(a)), a2 = hnext;
+  double c;
+  double2 s;
+  if (a2 == 0.0) {
+    c = 1.0;
+    s = cz();
+  } else if (a1 == 0.0) {
+    c = 0.0;
+    s = make_double2(1.0, 0.0);
+  } else {
+    const double t = hypot(a1, a2);
+    c = a1 / t;
+    s = cscale(make_double2(a.x / a1, a.y / a1), a2 / t);  // (h1/|h1|) conj(h2)/t, h2 real
+  }
+  gcos[j] = c;
+  gsin[j] = s;
+  col[j] = cfma(s, make_double2(hnext, 0.0), cscale(a, c));
+  const double2 gj = g[j];
+  g[j + 1] = cmul(make_double2(-s.x, s.y), gj);  // -conj(s) g_j
+  g[j] = cscale(gj, c);
+  const int iters = st->iterations + 1;
+  st->iterations = iters;
+  st->k = j + 1;
+  const double est = sqrt(cabs2(g[j + 1]));
+  st->est = est;
+  const bool happy = hnext <= 1e-14 * fmax(wpre, 1e-300);
+  const int cont = !(happy || est <= st->tol * st->bnorm) && iters < st->max_iter && (j + 1) < st->m;
+  if (cont) {
+    st->inv_hnext = 1.0 / hnext;
+    st->j = j + 1;
+  }
+  st->cont = cont;
+  if (in_graph) cudaGraphSetConditional(handle, cont ? 1u : 0u);
 }
-// y = alpha * x (complex scalar from device memory: y = x / sqrt(re(*nrm2)))
-__global__ void k_normalize(int n, const double2* __restrict__ x, const double2* __restrict__ nrm2,
-                            double2* __restrict__ y) {
+
+// V_{j+1} = (w - V h2) / h_{j+1,j}: the second CGS update fused with the normalisation
+// (only while the cycle continues; st->j already advanced, so V_0..V_{j-1} are read).
+__global__ void k_update_normalize(int n, const GmresState* __restrict__ st, const double2* __restrict__ h2,
+                                   const double2* __restrict__ w, double2* __restrict__ V, size_t ldv) {
+  if (!st->cont) return;
+  const int nv = st->j;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
-  const double inv = 1.0 / sqrt(nrm2->x);
-  y[k] = cscale(x[k], inv);
+  double2 acc = w[k];
+  for (int i = 0; i < nv; ++i) acc = cfms(__ldg(h2 + i), V[(size_t)i * ldv + k], acc);
+  V[(size_t)nv * ldv + k] = cscale(acc, st->inv_hnext);
 }
+
+// y = R^-1 g (krylov.hpp:191-196), one warp
+__global__ void k_backsub(const GmresState* __restrict__ st, const double2* __restrict__ R,
+                          const double2* __restrict__ g, double2* __restrict__ y) {
+  const int k = st->k, lane = threadIdx.x;
+  for (int i = k - 1; i >= 0; --i) {
+    double2 acc = cz();
+    for (int j2 = i + 1 + lane; j2 < k; j2 += 32) acc = cfma(R[(size_t)j2 * (j2 + 1) / 2 + i], y[j2], acc);
+    acc = warp_sum2(acc);
+    if (lane == 0) {
+      const double2 num = csub(g[i], acc);
+      y[i] = cmul(num, crecip(R[(size_t)i * (i + 1) / 2 + i]));
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void k_scale_copy(int n, const double2* __restrict__ x, double s, double2* __restrict__ y) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) y[k] = cscale(x[k], s);
 }
 // t = sum_i y_i V_i
-__global__ void k_combine(int n, const double2* __restrict__ V, size_t ldv, int nv, const double2* __restrict__ y,
-                          double2* __restrict__ t) {
-  __shared__ double2 y_sh[1024];
-  for (int i = threadIdx.x; i < nv; i += blockDim.x) y_sh[i] = y[i];
-  __syncthreads();
+__global__ void k_combine(int n, const double2* __restrict__ V, size_t ldv, const GmresState* __restrict__ st,
+                          const double2* __restrict__ y, double2* __restrict__ t) {
+  const int nv = st->k;
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   double2 acc = cz();
-  for (int i = 0; i < nv; ++i) acc = cfma(y_sh[i], V[(size_t)i * ldv + k], acc);
+  for (int i = 0; i < nv; ++i) acc = cfma(__ldg(y + i), V[(size_t)i * ldv + k], acc);
   t[k] = acc;
 }
 // y = a - b ;  y = a + b
@@ -778,35 +1071,78 @@ __global__ void k_apply_global(MeshLayout M, int n, const int* __restrict__ free
   store_c<T>(y + f, acc);
 }
 
-// Kronecker mass solve V^-1 = (M_y ⊗ M_x ⊗ I_dpn)^-1 with pre-factored 1-D tridiagonal
-// Thomas coefficients (SPD, no pivoting).  Pass along x (lines = rows), then along y.
-// cp[i] = c'_i, dinv[i] = 1 / (b_i - a_i c'_{i-1}); off-diagonals are the constant 'off'.
-__global__ void k_tridiag_x(int nlines, int len, int dpn, const double* __restrict__ cp,
-                            const double* __restrict__ dinv, double off, double* __restrict__ v) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= nlines * dpn) return;
-  const int line = t / dpn, comp = t % dpn;
-  double* p = v + (size_t)line * len * dpn + comp;
-  double prev = 0.0;
-  for (int i = 0; i < len; ++i) {
-    const double d = (p[(size_t)i * dpn] - off * prev) * dinv[i];
-    p[(size_t)i * dpn] = d;
-    prev = d;
+// Kronecker mass solve V^-1 = (M_y ⊗ M_x ⊗ I_dpn)^-1: batches of identical SPD tridiagonal
+// systems (constant off-diagonal 'off', pre-factored Thomas coefficients cp, dinv).
+// Each line is split into 32 segments; the Thomas recurrences
+//   forward  d'_i = d_i dinv_i - off dinv_i d'_{i-1},   backward x_i = d'_i - cp_i x_{i+1}
+// are affine maps, composed per segment, scanned across segments and re-applied, so the
+// sequential depth is ~4 len/32 instead of 2 len.  Same arithmetic as Thomas up to the
+// order of the affine compositions (|off dinv| < 1/3: forward stable).
+// Element i of line t sits at v[(t / G) * S1 + (t % G) * S2 + i * es].
+// SEG_FAST: block = (32 segments, LPB lines) — for lines contiguous in memory;
+// otherwise block = (LPB lines, 32 segments) so a warp reads 32 adjacent lines (coalesced).
+template <int LPB, bool SEG_FAST>
+__global__ void __launch_bounds__(32 * LPB)
+    k_tridiag_lines(double* __restrict__ v, int nlines, int len, int G, long long S1, long long S2, long long es,
+                    const double* __restrict__ cp, const double* __restrict__ dinv, double off) {
+  __shared__ double sa[LPB][33], sb[LPB][33], sx[LPB][33];
+  const int seg = SEG_FAST ? threadIdx.x : threadIdx.y, ly = SEG_FAST ? threadIdx.y : threadIdx.x;
+  const int line = blockIdx.x * LPB + ly;
+  const bool act = line < nlines;
+  double* p = v + (act ? (long long)(line / G) * S1 + (long long)(line % G) * S2 : 0);
+  const int L = (len + 31) / 32;
+  const int i0 = min(len, seg * L), i1 = min(len, i0 + L);
+  // forward: compose x -> A + B x over the segment
+  double a = 0.0, b = 1.0;
+  if (act)
+    for (int i = i0; i < i1; ++i) {
+      const double di = dinv[i];
+      a = fma(-off * di, a, p[(long long)i * es] * di);
+      b *= -off * di;
+    }
+  sa[ly][seg] = a;
+  sb[ly][seg] = b;
+  __syncthreads();
+  if (seg == 0) {
+    double x = 0.0;
+    for (int q = 0; q < 32; ++q) {
+      sx[ly][q] = x;
+      x = fma(sb[ly][q], x, sa[ly][q]);
+    }
   }
-  for (int i = len - 2; i >= 0; --i) p[(size_t)i * dpn] -= cp[i] * p[(size_t)(i + 1) * dpn];
-}
-__global__ void k_tridiag_y(int nlines_y, int stride, const double* __restrict__ cp, const double* __restrict__ dinv,
-                            double off, double* __restrict__ v, int len) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;  // t indexes (x position, comp)
-  if (t >= stride) return;
-  double prev = 0.0;
-  for (int j = 0; j < len; ++j) {
-    const double d = (v[(size_t)j * stride + t] - off * prev) * dinv[j];
-    v[(size_t)j * stride + t] = d;
-    prev = d;
+  __syncthreads();
+  double x = sx[ly][seg];
+  if (act)
+    for (int i = i0; i < i1; ++i) {
+      x = (p[(long long)i * es] - off * x) * dinv[i];
+      p[(long long)i * es] = x;
+    }
+  // backward: x_i = d'_i - cp_i x_{i+1}
+  a = 0.0;
+  b = 1.0;
+  if (act)
+    for (int i = i1 - 1; i >= i0; --i) {
+      a = fma(-cp[i], a, p[(long long)i * es]);
+      b *= -cp[i];
+    }
+  __syncthreads();
+  sa[ly][seg] = a;
+  sb[ly][seg] = b;
+  __syncthreads();
+  if (seg == 0) {
+    double xx = 0.0;
+    for (int q = 31; q >= 0; --q) {
+      sx[ly][q] = xx;
+      xx = fma(sb[ly][q], xx, sa[ly][q]);
+    }
   }
-  for (int j = len - 2; j >= 0; --j) v[(size_t)j * stride + t] -= cp[j] * v[(size_t)(j + 1) * stride + t];
-  (void)nlines_y;
+  __syncthreads();
+  x = sx[ly][seg];
+  if (act)
+    for (int i = i1 - 1; i >= i0; --i) {
+      x = p[(long long)i * es] - cp[i] * x;
+      p[(long long)i * es] = x;
+    }
 }
 // y = ybar - v ; u = lam / phi ; lam = Re t ; leak partial
 __global__ void k_realify(int n, const double2* __restrict__ t, double* __restrict__ lam) {

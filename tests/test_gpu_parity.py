@@ -146,3 +146,20 @@ def test_schur_solver_reuse_is_deterministic(fetigpu):
     solver.close()
     for k in ("y", "u", "lambda"):
         assert np.array_equal(a[k], b[k])
+
+
+def test_graph_and_eager_gmres_identical(fetigpu):
+    """The CUDA-graph (conditional WHILE) Arnoldi loop and the eager step-by-step loop
+    (profiling mode) launch the same kernels: results must be bit-identical."""
+    p = fetigpu.make_seeded_problem(64, 1e-6, seed=5)
+    solver = fetigpu.SchurSolver(p, 4, 4, tol=1e-10)
+    a = solver.solve()
+    solver.profile(True)
+    b = solver.solve()
+    prof = solver.profile_read()
+    solver.profile(False)
+    solver.close()
+    assert prof["dual_gemv"]["launches"] > 0
+    for k in ("y", "u", "lambda"):
+        assert np.array_equal(a[k], b[k])
+    assert a["plus_stats"]["iterations"] == b["plus_stats"]["iterations"]
