@@ -230,12 +230,15 @@ def run_gpu(args):
     total_solves = sum_over_ranks(steps, world)
     value = total_solves / t_max
     # ---------------- e2e: host buffers through the public API ----------------
-    host_t = [np.ascontiguousarray(t) for t in targets]
+    # host buffers in pinned memory (the path a serving caller would use)
+    host_t = [torch.from_numpy(t).pin_memory().numpy() for t in targets]
+    outs = tuple(torch.empty(n, dtype=torch.float64).pin_memory().numpy() for _ in range(3))
+    solver.solve(host_t[0], None, out=outs)
     barrier(world)
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     for k in range(warmup, warmup + steps):
-        r = solver.solve(host_t[k], None)
+        r = solver.solve(host_t[k], None, out=outs)
     w1 = time.perf_counter()
     barrier(world)
     e2e_t = max_over_ranks(w1 - w0, world)
@@ -288,6 +291,27 @@ def run_gpu(args):
                      "bytes_per_launch": kb, "avg_launch_ms": avg_ms},
         "clocks": clk.summary(),
     }
+    # BASELINE config 2 is a phi sweep: rates and iteration counts per phi (own factors each)
+    if rank == 0 and not args.no_sweep:
+        sweep = {}
+        for phi in PHI_SWEEP:
+            q = F.make_seeded_problem(N_GRID, phi, seed=0)
+            t1 = time.perf_counter()
+            sv = F.SchurSolver(q, S_SUB, S_SUB, tol=TOL, max_iter=MAX_ITER, device=local)
+            su = time.perf_counter() - t1
+            sv.solve_device(d_ybar[0].data_ptr(), 0, d_y.data_ptr(), d_u.data_ptr(), d_l.data_ptr())
+            sstream = torch.cuda.ExternalStream(sv.stream)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(sstream)
+            for k in range(3):
+                st = sv.solve_device(d_ybar[k].data_ptr(), 0, d_y.data_ptr(), d_u.data_ptr(), d_l.data_ptr())
+            e1.record(sstream)
+            torch.cuda.synchronize()
+            sweep[f"{phi:g}"] = {"solves_per_s": 3000.0 / e0.elapsed_time(e1), "setup_s": su,
+                                 "iterations_plus_minus": [st["plus_stats"]["iterations"],
+                                                           st["minus_stats"]["iterations"]]}
+            sv.close()
+        line["config"]["phi_sweep"] = sweep
     if rank == 0 and not args.no_cpu_baseline:
         rate, cits, csetup, ran = cpu_sample_oracle(os.cpu_count() or 1, 1, 0)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
@@ -310,6 +334,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

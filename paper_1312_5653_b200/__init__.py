@@ -199,8 +199,9 @@ class SchurSolver:
             pass
 
     # -- range space ---------------------------------------------------------------
-    def solve(self, ybar=None, yc=None):
-        """Range-space Schur solve with host buffers (control.cpp:297-334)."""
+    def solve(self, ybar=None, yc=None, out=None):
+        """Range-space Schur solve with host buffers (control.cpp:297-334).  ``out`` may
+        supply preallocated (e.g. pinned) float64 arrays (y, u, lambda)."""
         p = self.problem
         ybar = np.ascontiguousarray(p.target_state if ybar is None else ybar, dtype=np.float64)
         if yc is None:
@@ -211,7 +212,13 @@ class SchurSolver:
             ycp = _dp(yc)
         if ybar.shape != (self.n,):
             raise ContractError("ControlProblem: target length != n")
-        y, u, lam = np.zeros(self.n), np.zeros(self.n), np.zeros(self.n)
+        if out is None:
+            y, u, lam = np.zeros(self.n), np.zeros(self.n), np.zeros(self.n)
+        else:
+            y, u, lam = out
+            for a in out:
+                if a.dtype != np.float64 or a.shape != (self.n,) or not a.flags.c_contiguous:
+                    raise ContractError("solve: out arrays must be contiguous float64 of length n")
         st = SchurStats()
         _check(_native.lib().fetigpu_schur_solve(self._h, _dp(ybar), ycp, _dp(y), _dp(u), _dp(lam), C.byref(st)))
         return _schur_result(y, u, lam, st)

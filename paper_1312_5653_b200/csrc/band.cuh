@@ -76,9 +76,9 @@ __global__ void __launch_bounds__(256) k_band_ldlt(double2* __restrict__ colband
 // warps of a CTA share the factor panels, which one elected thread streams into a
 // STAGES-deep shared-memory ring with 1-D TMA bulk copies (cp.async.bulk + mbarrier).
 //
-// Per step j a warp keeps the window rows j..j+32*NS-1 in registers, row i in lane
-// (i mod 32), slot (i / 32) mod NS; the pivot lane broadcasts v_j with one shuffle and
-// every lane applies one complex FMA per slot ("warp per band column").
+// Per step j a warp keeps the window rows j..j+32*NS-1 in registers; lane 0 holds the
+// pivot row, broadcasts v_j, and every lane applies one complex FMA per slot with the
+// band column staged in shared memory ("warp per band column").
 template <int W, int WARPS, int CH, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32)
     k_band_solve(const double2* __restrict__ colband, const double2* __restrict__ rowband, size_t band_stride,
@@ -128,6 +128,10 @@ __global__ void __launch_bounds__(WARPS * 32)
     }
   }
 
+  // Shifting window: at step j, lane l of slot sl holds row j + l + 32 sl.  The pivot is
+  // always lane 0 of slot 0, and lane l's coefficient is always col[l + 1 + 32 sl], so a
+  // step is one broadcast + one shift (shuffles), one coalesced LDS and one complex FMA
+  // per slot — no per-lane index arithmetic.
   double2 y[NS];
   // ---------------- forward sweep: L v = b, write D^-1 v --------------------------------
 #pragma unroll
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   // b values of the rows entering the window during chunk c: rows c*CH + t + WIN
   double2 bnext = cz();
   {
-    const int row = lane + WIN;  // chunk 0, t = lane (CH == 32)
+    const int row = lane + WIN;
     if (active && lane < CH && row < n) bnext = x[row];
   }
   for (int q = 0; q < nch; ++q) {
@@ -156,28 +160,26 @@ __global__ void __launch_bounds__(WARPS * 32)
     if (active) {
 #pragma unroll 4
       for (int t = 0; t < rows; ++t) {
-        const int j = q * CH + t;
         const double2* col = panel + t * LD;
-        const int p = j & (WIN - 1);
-        const int pl = p & 31, ps = p >> 5;
-        // shared-memory operands first: only SHFL -> DFMA stays on the per-step chain
-        int k[NS];
-        double2 c[NS];
+        double2 cf[NS];
 #pragma unroll
         for (int sl = 0; sl < NS; ++sl) {
-          k[sl] = (lane + 32 * sl - p) & (WIN - 1);
-          c[sl] = k[sl] <= W ? col[k[sl]] : cz();
+          const int k = lane + 1 + 32 * sl;
+          cf[sl] = k <= W ? col[k] : cz();
         }
-        const double2 cw = (WIN <= W) ? col[WIN <= W ? WIN : 0] : cz();
+        const double2 dinv = col[0];
         const double2 nb = myb[t];
-        const double2 ysel = (NS == 1 || ps == 0) ? y[0] : y[NS - 1];
-        const double2 v = shfl2(ysel, pl);
+        const double2 v = shfl2(y[0], 0);
+        double2 sh[NS];
 #pragma unroll
         for (int sl = 0; sl < NS; ++sl) {
-          const bool piv = k[sl] == 0;
-          y[sl] = cfms(piv ? cw : c[sl], v, piv ? nb : y[sl]);
-          if (piv) x[j] = cmul(v, c[sl]);
+          const double2 up = shfl2(y[sl], (lane + 1) & 31);  // row j+1+l+32sl
+          const double2 nxt = (sl + 1 < NS) ? shfl2(y[sl + 1 < NS ? sl + 1 : sl], 0) : nb;
+          sh[sl] = lane == 31 ? nxt : up;
         }
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) y[sl] = cfms(cf[sl], v, sh[sl]);
+        if (lane == 0) x[q * CH + t] = cmul(v, dinv);
       }
     }
     __syncwarp();
@@ -192,15 +194,12 @@ __global__ void __launch_bounds__(WARPS * 32)
   }
   __syncwarp();
   // ---------------- backward sweep: L^T x = z ------------------------------------------
+  // lane l of slot sl holds row j - l - 32 sl; coefficient rowband[j][l + 1 + 32 sl]
 #pragma unroll
   for (int sl = 0; sl < NS; ++sl) {
-    // row i in [n-WIN, n) with i mod WIN == lane + 32 sl
-    const int base = n - WIN;
-    const int off = ((lane + 32 * sl) - base) & (WIN - 1);
-    const int row = base + off;
-    y[sl] = (active && row >= 0 && row < n) ? x[row] : cz();
+    const int row = n - 1 - lane - 32 * sl;
+    y[sl] = (active && row >= 0) ? x[row] : cz();
   }
-  // entering rows for reverse chunk c: j - WIN for j = c*CH + t
   {
     const int c = nch - 1;
     const int row = c * CH + lane - WIN;
@@ -223,27 +222,25 @@ __global__ void __launch_bounds__(WARPS * 32)
     if (active) {
 #pragma unroll 4
       for (int t = rows - 1; t >= 0; --t) {
-        const int j = c * CH + t;
         const double2* rw = panel + t * LD;
-        const int p = j & (WIN - 1);
-        const int pl = p & 31, ps = p >> 5;
-        int k[NS];
         double2 cf[NS];
 #pragma unroll
         for (int sl = 0; sl < NS; ++sl) {
-          k[sl] = (p - (lane + 32 * sl)) & (WIN - 1);
-          cf[sl] = k[sl] <= W ? rw[k[sl]] : cz();
+          const int k = lane + 1 + 32 * sl;
+          cf[sl] = k <= W ? rw[k] : cz();
         }
-        const double2 cw = (WIN <= W) ? rw[WIN <= W ? WIN : 0] : cz();
         const double2 nb = myb[t];
-        const double2 ysel = (NS == 1 || ps == 0) ? y[0] : y[NS - 1];
-        const double2 v = shfl2(ysel, pl);
+        const double2 v = shfl2(y[0], 0);
+        double2 sh[NS];
 #pragma unroll
         for (int sl = 0; sl < NS; ++sl) {
-          const bool piv = k[sl] == 0;
-          y[sl] = cfms(piv ? cw : cf[sl], v, piv ? nb : y[sl]);
-          if (piv) x[j] = v;
+          const double2 up = shfl2(y[sl], (lane + 1) & 31);
+          const double2 nxt = (sl + 1 < NS) ? shfl2(y[sl + 1 < NS ? sl + 1 : sl], 0) : nb;
+          sh[sl] = lane == 31 ? nxt : up;
         }
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) y[sl] = cfms(cf[sl], v, sh[sl]);
+        if (lane == 0) x[c * CH + t] = v;
       }
     }
     __syncwarp();

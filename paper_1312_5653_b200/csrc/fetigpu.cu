@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -89,6 +90,7 @@ struct Ctx {
   double2 *d_Cinv = nullptr;
   double2 *d_Sbb_p = nullptr, *d_Sinv_p = nullptr;  // packed symmetric tiles (k_sym_gemv)
   int NT = 0;
+  int sym_grid = 0;
   // workspaces
   double2 *d_fi = nullptr, *d_fb = nullptr, *d_fc = nullptr, *d_tb = nullptr, *d_yi = nullptr, *d_ri = nullptr;
   double2 *d_u1b = nullptr, *d_gcp = nullptr, *d_g = nullptr, *d_z = nullptr, *d_wb = nullptr;
@@ -107,6 +109,9 @@ struct Ctx {
   double* d_gcos = nullptr;
   unsigned int* d_counter = nullptr;
   bool use_graph = true;
+  bool debug_sync = false;
+  bool sym_tma = false;
+  bool watchdog = false;
   cudaGraph_t arnoldi_graph = nullptr;
   cudaGraphExec_t arnoldi_exec = nullptr;
   cudaGraphConditionalHandle arnoldi_handle{};
@@ -170,6 +175,10 @@ struct Ctx {
     CU(cudaGetLastError());
     if (ev) CU(cudaEventRecord(ev->b, stream));
     ++launches;
+    if (debug_sync) {  // FETIGPU_DEBUG_SYNC=1: serialise and log every launch (hang hunting)
+      CU(cudaStreamSynchronize(stream));
+      std::fprintf(stderr, "[fetigpu] launch %lld class %d done\n", launches, klass);
+    }
   }
   void prof_collect() {
     if (!prof || pool_used == 0) return;
@@ -266,6 +275,10 @@ struct Ctx {
     // FETIGPU_EAGER=1: launch the Arnoldi steps one by one instead of through the
     // conditional-node graph (ncu cannot profile kernel nodes of such graphs)
     if (const char* e = std::getenv("FETIGPU_EAGER")) use_graph = !(e[0] == '1');
+    if (const char* e = std::getenv("FETIGPU_DEBUG_SYNC")) debug_sync = e[0] == '1';
+    if (debug_sync) use_graph = false;
+    if (const char* e = std::getenv("FETIGPU_SYM_TMA")) sym_tma = e[0] == '1';
+    watchdog = std::getenv("FETIGPU_WATCHDOG") != nullptr;
     n = P.n();
     m = P.m();
     nc = H.n_corner;
@@ -421,6 +434,15 @@ struct Ctx {
       NT = (NB + 31) / 32;
       if (NT > 8) throw ContractError("more than 256 interface dofs per subdomain");
       const size_t per = (size_t)sym_tile_entries(NT);
+      {
+        int dev_sms = 0;
+        CU(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, desc.device));
+        sym_grid = dev_sms * SYM_CTAS_PER_SM;
+        const int smem = (int)sym_tma_smem(NT);
+        CU(cudaFuncSetAttribute(k_sym_gemv_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CU(cudaFuncSetAttribute(k_sym_gemv_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        CU(cudaFuncSetAttribute(k_sym_gemv_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      }
       d_Sbb_p = alloc<double2>((size_t)S * per);
       d_Sinv_p = alloc<double2>((size_t)S * per);
       launch(FETIGPU_K_OTHER, [&] {
@@ -494,8 +516,7 @@ struct Ctx {
     // coarse gemv may need > 48 KB of dynamic smem
     CU(cudaFuncSetAttribute(k_coarse_gemv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)std::max<size_t>(nc * sizeof(double2), 1)));
-    CU(cudaFuncSetAttribute(k_cgs_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(mdot_chunk * sizeof(double2))));
+    CU(cudaFuncSetAttribute(k_cgs_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cgs_smem()));
     setup_mass();
     sync();
     setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -564,11 +585,28 @@ struct Ctx {
     launch(FETIGPU_K_COARSE, [&] {
       k_coarse_rhs<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_slots, d_gcp, fc, d_g);
     });
-    launch(FETIGPU_K_COARSE, [&] {
-      k_coarse_gemv<8><<<std::min(cdiv(nc, 8), 296), 256, nc * sizeof(double2), stream>>>(nc, d_Cinv, d_g, d_z);
-    });
+    coarse_gemv();
   }
 
+  // packed symmetric GEMV: persistent TMA-streamed grid (k_sym_gemv_tma)
+  void launch_sym(const SymGemvArgs& g) {
+    if (!sym_tma) {  // default: one CTA per subdomain, loads streamed from registers
+      switch (g.mode) {
+        case 0: k_sym_gemv<0><<<H.n_sub, 256, sym_smem(), stream>>>(g); break;
+        case 1: k_sym_gemv<1><<<H.n_sub, 256, sym_smem(), stream>>>(g); break;
+        default: k_sym_gemv<2><<<H.n_sub, 256, sym_smem(), stream>>>(g); break;
+      }
+      return;
+    }
+    // FETIGPU_SYM_TMA=1: persistent TMA-streamed variant (experimental)
+    const size_t smem = sym_tma_smem(NT);
+    const int grid = std::min(H.n_sub, sym_grid);
+    switch (g.mode) {
+      case 0: k_sym_gemv_tma<0><<<grid, 288, smem, stream>>>(g, H.n_sub); break;
+      case 1: k_sym_gemv_tma<1><<<grid, 288, smem, stream>>>(g, H.n_sub); break;
+      default: k_sym_gemv_tma<2><<<grid, 288, smem, stream>>>(g, H.n_sub); break;
+    }
+  }
   size_t sym_smem() const {
     const int noff = NT * (NT - 1) / 2;
     return sizeof(double2) * 32 * (NT + (noff + NT) + noff);
@@ -589,16 +627,30 @@ struct Ctx {
     g.bi_val = d_bi_val;
     return g;
   }
-  // local dual solve u1_b = S_bb^-1 t_b with t_b = -B^T lam, plus gcp = cpl_b^T t_b (K5)
+  // local dual solve u1_b = S_bb^-1 t_b with t_b = -B^T lam, gcp = cpl_b^T t_b, and (last
+  // CTA) the coarse rhs g = -sum gcp (K5)
   void dual_gemv(SymGemvArgs g) {
     g.alpha = -1.0;
     g.out = d_u1b;
     g.cpl_b = d_cpl_b;
     g.gcp = d_gcp;
-    launch(FETIGPU_K_DUAL_GEMV, [&] { k_sym_gemv<<<H.n_sub, 256, sym_smem(), stream>>>(g); });
+    if (nc > 0) {
+      g.g_counter = d_counter + 1;
+      g.nc = nc;
+      g.corner_slots = d_corner_slots;
+      g.fc = nullptr;
+      g.g = d_g;
+    }
+    launch(FETIGPU_K_DUAL_GEMV, [&] { launch_sym(g); });
+  }
+  void coarse_gemv() {
+    if (nc == 0) return;
+    launch(FETIGPU_K_COARSE, [&] {
+      k_coarse_gemv<8><<<cdiv(nc, 8), 256, nc * sizeof(double2), stream>>>(nc, d_Cinv, d_g, d_z);
+    });
   }
   void dual_tail(double2* out) {
-    coarse_solve(nullptr);
+    coarse_gemv();
     launch(FETIGPU_K_LAMBDA, [&] {
       k_lam_gather_dual<<<cdiv(nl, 256), 256, 0, stream>>>(nl, H.NB, H.NC, d_lam_lo, d_lam_hi, d_u1b, d_cpl_b,
                                                            d_cglob, d_z, out);
@@ -621,7 +673,7 @@ struct Ctx {
     g.jstride = ldv;
     g.alpha = 0.5;
     g.out = d_wb;
-    launch(FETIGPU_K_PRECOND_GEMV, [&] { k_sym_gemv<<<H.n_sub, 256, sym_smem(), stream>>>(g); });
+    launch(FETIGPU_K_PRECOND_GEMV, [&] { launch_sym(g); });
   }
   void apply_precond(const double2* r, double2* out) {
     precond_gemv(r, nullptr);
@@ -629,17 +681,6 @@ struct Ctx {
       k_lam_gather_pre<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_lam_lo, d_lam_hi, d_wb, out);
     });
   }
-  // F P v in one pass over the interface: the dual GEMV gathers t_b = -sign (wb_lo - wb_hi)/2
-  // straight from the preconditioner's per-subdomain output (z = P v is never materialised)
-  void apply_dual_precond(const double2* v, const int* jsel, double2* out) {
-    precond_gemv(v, jsel);
-    SymGemvArgs g = sym_args(d_Sinv_p);
-    g.mode = 1;
-    g.wb = d_wb;
-    dual_gemv(g);
-    dual_tail(out);
-  }
-
   // eliminate (feti.cpp:516-556), split in two halves.  A_rr is applied through its block
   // factorization: y_i = A_ii^-1 t_i (banded), u1_b = S_bb^-1 (t_b - A_bi y_i) (dense),
   // g = f_c - coupling^T t, z = C^-1 g, u_b = u1_b - cpl_b z.  Both eliminations of a FETI
@@ -657,7 +698,7 @@ struct Ctx {
       g.yi = d_yi;
       g.alpha = 1.0;
       g.out = d_u1b;
-      launch(FETIGPU_K_OTHER, [&] { k_sym_gemv<<<S, 256, sym_smem(), stream>>>(g); });
+      launch(FETIGPU_K_OTHER, [&] { launch_sym(g); });
     }
     (void)NB;
     launch(FETIGPU_K_OTHER, [&] { k_gcp_full<<<S, 256, 0, stream>>>(L, d_cpl_i, d_cpl_b, ti, tb, d_gcp); });
@@ -701,25 +742,60 @@ struct Ctx {
   void arnoldi_step(bool in_graph) {
     double2* h1 = d_red;
     double2* h2 = d_red + (vcap + 2);
-    double2* hn = d_red + 2 * (vcap + 2);
-    apply_dual_precond(d_V, &d_gst->j, d_w);
-    const size_t sm = mdot_chunk * sizeof(double2);
-    launch(FETIGPU_K_ORTHO, [&] {
-      k_cgs_pass<8><<<mdot_blocks, 256, sm, stream>>>(nl, mdot_chunk, d_V, ldv, d_gst, nullptr, d_w, 0, d_part, h1,
-                                                      d_counter);
-    });
-    launch(FETIGPU_K_ORTHO, [&] {
-      k_cgs_pass<8><<<mdot_blocks, 256, sm, stream>>>(nl, mdot_chunk, d_V, ldv, d_gst, h1, d_w, 0, d_part, h2,
-                                                      d_counter);
-    });
-    launch(FETIGPU_K_ORTHO, [&] {
-      k_givens<<<1, 32, 0, stream>>>(d_gst, h1, h2, hn, d_R, d_gcos, d_gsin, d_gvec, in_graph ? 1 : 0,
-                                     arnoldi_handle);
-    });
+    auto mark = [&](unsigned int v) {
+      if (watchdog) launch(FETIGPU_K_OTHER, [&] { k_mark<<<1, 32, 0, stream>>>(d_counter + 3, v); });
+    };
+    // z = P V_j (per-subdomain S_bb apply); the dual GEMV gathers its input straight from it
+    mark(1);
+    precond_gemv(d_V, &d_gst->j);
+    mark(2);
+    {
+      SymGemvArgs g = sym_args(d_Sinv_p);
+      g.mode = 1;
+      g.wb = d_wb;
+      dual_gemv(g);
+    }
+    mark(3);
+    coarse_gemv();
+    mark(4);
+    CgsArgs c{};
+    c.n = nl;
+    c.chunk = mdot_chunk;
+    c.V = d_V;
+    c.ldv = ldv;
+    c.st = d_gst;
+    c.w = d_w;
+    c.part = d_part;
+    c.counter = d_counter;
+    const size_t sm = cgs_smem();
+    // pass 1: w = F z (dual tail gathered per chunk), h1 = V^H w, |w|^2
+    c.mode = 0;
+    c.out = h1;
+    c.gather = 1;
+    c.NB = H.NB;
+    c.NC = H.NC;
+    c.lam_lo = d_lam_lo;
+    c.lam_hi = d_lam_hi;
+    c.cglob = d_cglob;
+    c.u1b = d_u1b;
+    c.cpl_b = d_cpl_b;
+    c.z = d_z;
+    launch(FETIGPU_K_ORTHO, [&] { k_cgs_pass<8><<<mdot_blocks, 256, sm, stream>>>(c); });
+    mark(5);
+    // pass 2: w -= V h1, h2 = V^H w, |w|^2; last block runs the Givens step
+    c.gather = 0;
+    c.h_in = h1;
+    c.out = h2;
+    c.givens = 1;
+    c.ga = GivensArgs{d_gst, h1, h2, d_R, d_gcos, d_gsin, d_gvec, in_graph ? 1 : 0, arnoldi_handle};
+    launch(FETIGPU_K_ORTHO, [&] { k_cgs_pass<8><<<mdot_blocks, 256, sm, stream>>>(c); });
+    mark(6);
+    // V_{j+1} = (w - V h2) / h_{j+1,j}
     launch(FETIGPU_K_ORTHO, [&] {
       k_update_normalize<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_gst, h2, d_w, d_V, ldv);
     });
   }
+  size_t cgs_smem() const { return sizeof(double2) * std::max(mdot_chunk, 640); }
 
   void build_arnoldi_graph() {
     CU(cudaGraphCreate(&arnoldi_graph, 0));
@@ -791,6 +867,24 @@ struct Ctx {
       if (graph) {
         CU(cudaGraphLaunch(arnoldi_exec, stream));
         CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
+        if (watchdog) {  // debugging aid: report a stuck Arnoldi graph
+          auto t0 = std::chrono::steady_clock::now();
+          while (cudaStreamQuery(stream) == cudaErrorNotReady) {
+            if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > 3.0) {
+              cudaStream_t side;
+              CU(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+              GmresState g{};
+              unsigned int cnt[4] = {};
+              cudaMemcpyAsync(&g, d_gst, sizeof(g), cudaMemcpyDeviceToHost, side);
+              cudaMemcpyAsync(cnt, d_counter, sizeof(cnt), cudaMemcpyDeviceToHost, side);
+              cudaStreamSynchronize(side);
+              std::fprintf(stderr,
+                           "[fetigpu] watchdog: j=%d iters=%d k=%d cont=%d status=%d est=%g counters=%u,%u marker=%u\n",
+                           g.j, g.iterations, g.k, g.cont, g.status, g.est, cnt[0], cnt[1], cnt[3]);
+              t0 = std::chrono::steady_clock::now();
+            }
+          }
+        }
         sync();
         launches += (long long)arnoldi_body_kernels * (h_gst->iterations - iterations);
       } else {

@@ -441,8 +441,15 @@ struct SymGemvArgs {
   double2* out;                   // [S][NB]
   const double2* cpl_b;           // optional: gcp = cpl_b^T in
   double2* gcp;
+  // optional, with gcp: the last CTA assembles the coarse rhs g = fc - sum gcp (feti.cpp:523-538)
+  unsigned int* g_counter;
+  int nc;
+  const int* corner_slots;
+  const double2* fc;
+  double2* g;
 };
 
+template <int MODE>
 __global__ void __launch_bounds__(256) k_sym_gemv(SymGemvArgs a) {
   constexpr int WARPS = 8;
   // dynamic smem: x (32 NT) | row partials (ntiles x 32) | column partials (noff x 32)
@@ -456,12 +463,12 @@ __global__ void __launch_bounds__(256) k_sym_gemv(SymGemvArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // ---- input vector (B^T scatter) ----
   const double2* lam = a.lam;
-  if (a.mode == 0 && a.jsel != nullptr) lam += (size_t)(*a.jsel) * a.jstride;
+  if (MODE == 0 && a.jsel != nullptr) lam += (size_t)(*a.jsel) * a.jstride;
   for (int k = threadIdx.x; k < 32 * NT; k += blockDim.x) {
     double2 v = cz();
     if (k < NB) {
       const size_t sb = (size_t)s * NB + k;
-      if (a.mode == 2) {
+      if (MODE == 2) {
         v = a.tb[sb];
         for (int e = 0; e < a.EBI; ++e) {
           const int i = a.bi_idx[sb * a.EBI + e];
@@ -471,7 +478,7 @@ __global__ void __launch_bounds__(256) k_sym_gemv(SymGemvArgs a) {
         const int r = a.blam[sb];
         if (r >= 0) {
           double2 z;
-          if (a.mode == 0)
+          if (MODE == 0)
             z = lam[r];
           else
             z = cscale(csub(a.wb[a.lam_lo[r]], a.wb[a.lam_hi[r]]), 0.5);
@@ -546,7 +553,204 @@ __global__ void __launch_bounds__(256) k_sym_gemv(SymGemvArgs a) {
       acc = warp_sum2(acc);
       if (lane == 0) a.gcp[(size_t)s * a.NC + c] = acc;
     }
+    if (a.g_counter != nullptr) {
+      __shared__ bool is_last;
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) is_last = atomicAdd(a.g_counter, 1u) == gridDim.x - 1;
+      __syncthreads();
+      if (is_last) {
+        __threadfence();
+        for (int c = threadIdx.x; c < a.nc; c += blockDim.x) {
+          double2 acc = a.fc ? a.fc[c] : cz();
+          for (int q = 0; q < 4; ++q) {
+            const int slot = a.corner_slots[c * 4 + q];
+            if (slot >= 0) acc = csub(acc, __ldcg(a.gcp + slot));
+          }
+          a.g[c] = acc;
+        }
+        if (threadIdx.x == 0) *a.g_counter = 0u;
+      }
+    }
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// Streaming version of k_sym_gemv: a persistent grid (SYM_CTAS_PER_SM per SM) where warp 8
+// is a TMA producer that streams every tile of every subdomain the CTA owns into a
+// SYM_STAGES-deep shared-memory ring (cp.async.bulk + mbarrier full/empty pairs), and
+// warps 0-7 consume the tiles from shared memory.  Bytes in flight per SM no longer depend
+// on registers: the ring keeps ~SYM_STAGES x 16 KB outstanding per CTA.
+constexpr int SYM_STAGES = 6;
+constexpr int SYM_CTAS_PER_SM = 2;
+constexpr int SYM_TILE = 1024;  // complex entries of a full tile
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(288, 2) k_sym_gemv_tma(SymGemvArgs a, int S) {
+  constexpr int CWARPS = 8, CTHREADS = 256;
+  extern __shared__ __align__(128) unsigned char sgt_raw[];
+  double2* ring = reinterpret_cast<double2*>(sgt_raw);  // SYM_STAGES x SYM_TILE
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)SYM_STAGES * SYM_TILE);
+  uint64_t* empty = full + SYM_STAGES;
+  const int NB = a.NB, NT = a.NT;
+  const int noff = NT * (NT - 1) / 2, ntiles = noff + NT;
+  double2* x_sh = reinterpret_cast<double2*>(empty + SYM_STAGES);
+  double2 (*part_row)[32] = reinterpret_cast<double2 (*)[32]>(x_sh + 32 * NT);
+  double2 (*part_col)[32] = reinterpret_cast<double2 (*)[32]>(x_sh + 32 * NT + 32 * ntiles);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int per = sym_tile_entries(NT);
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < SYM_STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  // tile t of a subdomain: t < noff off-diagonal (16 KB), else diagonal t - noff (8.5 KB)
+  auto tile_off = [&](int t) -> size_t {
+    return t < noff ? (size_t)NT * 17 * 32 + (size_t)t * SYM_TILE : (size_t)(t - noff) * 17 * 32;
+  };
+  if (warp == CWARPS) {  // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int q = 0;
+      for (int s = blockIdx.x; s < S; s += gridDim.x) {
+        const double2* P = a.pack + (size_t)s * per;
+        for (int t = 0; t < ntiles; ++t, ++q) {
+          const int st = q % SYM_STAGES;
+          mbar_wait(&empty[st], ((q / SYM_STAGES) & 1) ^ 1);
+          const uint32_t bytes = (t < noff ? SYM_TILE : 17 * 32) * (uint32_t)sizeof(double2);
+          mbar_arrive_expect_tx(&full[st], bytes);
+          tma_load_1d(ring + (size_t)st * SYM_TILE, P + tile_off(t), bytes, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const double2* lam = a.lam;
+  if (MODE == 0 && a.jsel != nullptr) lam += (size_t)(*a.jsel) * a.jstride;
+  int qbase = 0;
+  for (int s = blockIdx.x; s < S; s += gridDim.x, qbase += ntiles) {
+    for (int k = threadIdx.x; k < 32 * NT; k += CTHREADS) {
+      double2 v = cz();
+      if (k < NB) {
+        const size_t sb = (size_t)s * NB + k;
+        if (MODE == 2) {
+          v = a.tb[sb];
+          for (int e = 0; e < a.EBI; ++e) {
+            const int i = a.bi_idx[sb * a.EBI + e];
+            if (i >= 0) v = cfms(a.bi_val[sb * a.EBI + e], a.yi[(size_t)s * a.NI + i], v);
+          }
+        } else {
+          const int r = a.blam[sb];
+          if (r >= 0) {
+            double2 z;
+            if (MODE == 0)
+              z = lam[r];
+            else
+              z = cscale(csub(a.wb[a.lam_lo[r]], a.wb[a.lam_hi[r]]), 0.5);
+            v = cscale(z, a.alpha * a.bsign[sb]);
+          }
+        }
+      }
+      x_sh[k] = v;
+    }
+    named_bar_sync(1, CTHREADS);
+    // tiles: round robin; with NT = 4, warps 0-5 one off-diagonal tile, warps 6-7 two diagonal
+    const bool paired = noff + (NT + 1) / 2 <= CWARPS;
+    for (int item = warp; item < (paired ? noff + (NT + 1) / 2 : ntiles); item += CWARPS)
+      for (int half = 0; half < ((paired && item >= noff) ? 2 : 1); ++half) {
+        const int t = (paired && item >= noff) ? noff + 2 * (item - noff) + half : item;
+        if (t >= ntiles) break;
+        const int q = qbase + t;
+        const int st = q % SYM_STAGES;
+        mbar_wait(&full[st], (q / SYM_STAGES) & 1);
+        const double2* T = ring + (size_t)st * SYM_TILE;
+        double2 yr = cz(), yc = cz();
+        if (t < noff) {
+          int I = 1;
+          while ((I + 1) * I / 2 <= t) ++I;
+          const int J = t - I * (I - 1) / 2;
+          const double2 xi = x_sh[32 * I + lane];
+#pragma unroll 8
+          for (int c = 0; c < 32; ++c) {
+            const double2 m = T[c * 32 + lane];
+            yr = cfma(m, x_sh[32 * J + ((lane + c) & 31)], yr);
+            yc = cfma(m, xi, yc);
+            yc = shfl2(yc, (lane + 1) & 31);
+          }
+          part_row[t][lane] = yr;
+          part_col[t][lane] = yc;
+        } else {
+          const int I = t - noff;
+          const double2 xi = x_sh[32 * I + lane];
+          yr = cmul(T[lane], xi);
+#pragma unroll 5
+          for (int c = 1; c < 16; ++c) {
+            const double2 m = T[c * 32 + lane];
+            yr = cfma(m, x_sh[32 * I + ((lane + c) & 31)], yr);
+            yc = shfl2(yc, (lane + 1) & 31);
+            yc = cfma(m, xi, yc);
+          }
+          yr = cfma(T[16 * 32 + lane], x_sh[32 * I + ((lane + 16) & 31)], yr);
+          yc = shfl2(yc, (lane + 17) & 31);
+          part_row[t][lane] = cadd(yr, yc);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+    named_bar_sync(1, CTHREADS);
+    for (int k = threadIdx.x; k < NB; k += CTHREADS) {
+      const int I = k >> 5, l = k & 31;
+      double2 acc = part_row[noff + I][l];
+      for (int J = 0; J < I; ++J) acc = cadd(acc, part_row[I * (I - 1) / 2 + J][l]);
+      for (int I2 = I + 1; I2 < NT; ++I2) acc = cadd(acc, part_col[I2 * (I2 - 1) / 2 + I][l]);
+      a.out[(size_t)s * NB + k] = acc;
+    }
+    if (a.gcp != nullptr) {
+      for (int c = warp; c < a.NC; c += CWARPS) {
+        double2 acc = cz();
+        for (int k = lane; k < NB; k += 32) acc = cfma(a.cpl_b[((size_t)s * NB + k) * a.NC + c], x_sh[k], acc);
+        acc = warp_sum2(acc);
+        if (lane == 0) a.gcp[(size_t)s * a.NC + c] = acc;
+      }
+    }
+    named_bar_sync(1, CTHREADS);  // x_sh / partials are rewritten for the next subdomain
+  }
+  if (a.g_counter != nullptr) {  // coarse rhs assembled by the last CTA to finish
+    __shared__ bool is_last;
+    __threadfence();
+    named_bar_sync(1, CTHREADS);
+    if (threadIdx.x == 0) is_last = atomicAdd(a.g_counter, 1u) == gridDim.x - 1;
+    named_bar_sync(1, CTHREADS);
+    if (is_last) {
+      __threadfence();
+      for (int c = threadIdx.x; c < a.nc; c += CTHREADS) {
+        double2 acc = a.fc ? a.fc[c] : cz();
+        for (int q = 0; q < 4; ++q) {
+          const int slot = a.corner_slots[c * 4 + q];
+          if (slot >= 0) acc = csub(acc, __ldcg(a.gcp + slot));
+        }
+        a.g[c] = acc;
+      }
+      if (threadIdx.x == 0) *a.g_counter = 0u;
+    }
+  }
+}
+
+__host__ __device__ constexpr size_t sym_tma_smem(int NT) {
+  return (size_t)SYM_STAGES * SYM_TILE * 16 + 2 * SYM_STAGES * 8 +
+         (size_t)16 * 32 * (NT + (NT * (NT - 1) / 2 + NT) + NT * (NT - 1) / 2);
+}
+
+// debugging aid (FETIGPU_WATCHDOG): progress marker between graph body kernels
+__global__ void k_mark(unsigned int* progress, unsigned int v) {
+  if (threadIdx.x == 0) atomicExch(progress, v);
 }
 
 // Dirichlet tail: out[r] = (w_lo - w_hi) / 2   (feti.cpp:620-626, signs +1 / -1)
@@ -581,6 +785,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   for (int row = blockIdx.x * WARPS + warp; row < nc; row += gridDim.x * WARPS) {
     const double2* cr = Cinv + (size_t)row * nc;
     double2 a = cz();
+#pragma unroll 8
     for (int k = lane; k < nc; k += 32) a = cfma(cr[k], g_sh[k], a);
     a = warp_sum2(a);
     if (lane == 0) z[row] = a;
@@ -774,103 +979,57 @@ struct GmresState {
   double tol, bnorm, inv_hnext, est;
 };
 
-// One classical Gram-Schmidt pass on the block's chunk of w:
-//   (optional) w -= sum_i h_in[i] V_i ; then partial sums of conj(V_i) w (dots) and/or |w|^2
-// reduced by the last block to finish (fixed order => deterministic).  nv = *jptr + 1.
-// mode 0: dots + norm (out[0..nv]) ; 1: dots (out[0..nv-1]) ; 2: norm only (out[0]).
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    k_cgs_pass(int n, int chunk, const double2* __restrict__ V, size_t ldv, const GmresState* __restrict__ st,
-               const double2* __restrict__ h_in, double2* __restrict__ w, int mode, double2* __restrict__ part,
-               double2* __restrict__ out, unsigned int* __restrict__ counter) {
-  extern __shared__ double2 w_sh[];
-  __shared__ bool is_last;
-  const int nv = st->j + 1;
-  const int b = blockIdx.x, lo = b * chunk, len = max(0, min(chunk, n - lo));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = threadIdx.x; k < len; k += blockDim.x) {
-    double2 acc = w[lo + k];
-    if (h_in != nullptr) {
-      for (int i = 0; i < nv; ++i) acc = cfms(h_in[i], V[(size_t)i * ldv + lo + k], acc);
-      w[lo + k] = acc;
-    }
-    w_sh[k] = acc;
-  }
-  __syncthreads();
-  const int ndots = (mode == 2) ? 0 : nv;
-  const int nout = ndots + (mode == 1 ? 0 : 1);
-  for (int i = warp; i < nout; i += WARPS) {
-    double2 acc = cz();
-    if (i < ndots) {
-      const double2* v = V + (size_t)i * ldv + lo;
-      for (int k = lane; k < len; k += 32) acc = cfma_conj(v[k], w_sh[k], acc);
-    } else {
-      for (int k = lane; k < len; k += 32) acc.x += cabs2(w_sh[k]);
-    }
-    acc = warp_sum2(acc);
-    if (lane == 0) part[(size_t)i * gridDim.x + b] = acc;
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-  for (int i = warp; i < nout; i += WARPS) {
-    double2 acc = cz();
-    for (int bb = lane; bb < (int)gridDim.x; bb += 32) acc = cadd(acc, __ldcg(part + (size_t)i * gridDim.x + bb));
-    acc = warp_sum2(acc);
-    if (lane == 0) out[i] = acc;
-  }
-  if (threadIdx.x == 0) *counter = 0u;
-}
-
 // Hessenberg column update, Givens rotations and both stopping tests of one Arnoldi
-// step (krylov.hpp:164-188).  R is the rotated Hessenberg, packed by columns (column j at
-// R + j(j+1)/2).  One warp: the rotation operands are staged in shared memory, the
-// sequential rotation chain runs on lane 0.  In graph mode it drives the WHILE node.
-__global__ void __launch_bounds__(32) k_givens(GmresState* __restrict__ st, const double2* __restrict__ h1,
-                                               const double2* __restrict__ h2, const double2* __restrict__ hn,
-                                               double2* __restrict__ R, double* __restrict__ gcos,
-                                               double2* __restrict__ gsin, double2* __restrict__ g, int in_graph,
-                                               cudaGraphConditionalHandle handle) {
+// step (krylov.hpp:164-188), run by one warp.  R is the rotated Hessenberg, packed by
+// columns (column j at R + j(j+1)/2).  The rotation operands are staged in shared
+// memory and the sequential rotation chain runs on lane 0.  In graph mode it drives the
+// WHILE node.  h1 = [V^H w0, |w0|^2], h2 = [V^H w1, |w1|^2] (CGS2 passes).
+struct GivensArgs {
+  GmresState* st;
+  const double2* h1;
+  const double2* h2;
+  double2* R;
+  double* gcos;
+  double2* gsin;
+  double2* g;
+  int in_graph;
+  cudaGraphConditionalHandle handle;
+};
+__device__ void givens_warp(const GivensArgs& a, double* sc, double2* ss, double2* sh) {
   constexpr int CHK = 256;
-  __shared__ double sc[CHK];
-  __shared__ double2 ss[CHK], sh[CHK + 1];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  GmresState* st = a.st;
   const int j = st->j;
-  double2* col = R + (size_t)j * (j + 1) / 2;
+  double2* col = a.R + (size_t)j * (j + 1) / 2;
   bool finite = true;
+  double s2 = 0.0;
   for (int i = lane; i <= j; i += 32) {
-    const double2 v = cadd(h1[i], h2[i]);
+    const double2 v = cadd(a.h1[i], a.h2[i]);
     finite = finite && isfinite(v.x) && isfinite(v.y);
+    s2 += cabs2(a.h2[i]);
   }
   finite = __all_sync(0xffffffffu, finite);
-  const double wpre = sqrt(h1[j + 1].x);
-  // |w - V h2|^2 = |w|^2 - sum |h2_i|^2 (V orthonormal, h2 = V^H w is the round-off-sized
-  // reorthogonalisation correction: no cancellation)
-  double s2 = 0.0;
-  for (int i = lane; i <= j; i += 32) s2 += cabs2(h2[i]);
   s2 = warp_sum(s2);
-  const double hnext = sqrt(fmax(0.0, h2[j + 1].x - s2));
-  (void)hn;
+  const double wpre = sqrt(a.h1[j + 1].x);
+  // |w1 - V h2|^2 = |w1|^2 - sum |h2_i|^2 (V orthonormal; h2 is round-off sized)
+  const double hnext = sqrt(fmax(0.0, a.h2[j + 1].x - s2));
   finite = finite && isfinite(hnext);
   if (!finite) {
     if (lane == 0) {
       st->status = 1;
       st->cont = 0;
-      if (in_graph) cudaGraphSetConditional(handle, 0u);
+      if (a.in_graph) cudaGraphSetConditional(a.handle, 0u);
     }
     return;
   }
   // previous rotations (krylov.hpp:169-173): carry = rotated entry i, t2 = original entry i+1
-  double2 carry = cadd(h1[0], h2[0]);
+  double2 carry = cadd(a.h1[0], a.h2[0]);
   for (int base = 0; base < j; base += CHK) {
     const int cnt = min(CHK, j - base);
     for (int q = lane; q < cnt; q += 32) {
-      sc[q] = gcos[base + q];
-      ss[q] = gsin[base + q];
-      sh[q] = cadd(h1[base + q + 1], h2[base + q + 1]);
+      sc[q] = a.gcos[base + q];
+      ss[q] = a.gsin[base + q];
+      sh[q] = cadd(a.h1[base + q + 1], a.h2[base + q + 1]);
     }
     __syncwarp();
     if (lane == 0) {
@@ -885,8 +1044,8 @@ __global__ void __launch_bounds__(32) k_givens(GmresState* __restrict__ st, cons
   }
   if (lane != 0) return;
   // make_givens (krylov.hpp:66-83) on (carry = rotated col[j], hnext)
-  const double2 a = carry;
-  const double a1 = sqrt(cabs2(a)), a2 = hnext;
+  const double2 x = carry;
+  const double a1 = sqrt(cabs2(x)), a2 = hnext;
   double c;
   double2 s;
   if (a2 == 0.0) {
@@ -898,18 +1057,18 @@ __global__ void __launch_bounds__(32) k_givens(GmresState* __restrict__ st, cons
   } else {
     const double t = hypot(a1, a2);
     c = a1 / t;
-    s = cscale(make_double2(a.x / a1, a.y / a1), a2 / t);  // (h1/|h1|) conj(h2)/t, h2 real
+    s = cscale(make_double2(x.x / a1, x.y / a1), a2 / t);  // (h1/|h1|) conj(h2)/t, h2 real
   }
-  gcos[j] = c;
-  gsin[j] = s;
-  col[j] = cfma(s, make_double2(hnext, 0.0), cscale(a, c));
-  const double2 gj = g[j];
-  g[j + 1] = cmul(make_double2(-s.x, s.y), gj);  // -conj(s) g_j
-  g[j] = cscale(gj, c);
+  a.gcos[j] = c;
+  a.gsin[j] = s;
+  col[j] = cfma(s, make_double2(hnext, 0.0), cscale(x, c));
+  const double2 gj = a.g[j];
+  a.g[j + 1] = cmul(make_double2(-s.x, s.y), gj);  // -conj(s) g_j
+  a.g[j] = cscale(gj, c);
   const int iters = st->iterations + 1;
   st->iterations = iters;
   st->k = j + 1;
-  const double est = sqrt(cabs2(g[j + 1]));
+  const double est = sqrt(cabs2(a.g[j + 1]));
   st->est = est;
   const bool happy = hnext <= 1e-14 * fmax(wpre, 1e-300);
   const int cont = !(happy || est <= st->tol * st->bnorm) && iters < st->max_iter && (j + 1) < st->m;
@@ -918,7 +1077,113 @@ __global__ void __launch_bounds__(32) k_givens(GmresState* __restrict__ st, cons
     st->j = j + 1;
   }
   st->cont = cont;
-  if (in_graph) cudaGraphSetConditional(handle, cont ? 1u : 0u);
+  if (a.in_graph) cudaGraphSetConditional(a.handle, cont ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(32) k_givens(GivensArgs a) {
+  __shared__ double sc[256];
+  __shared__ double2 ss[256], sh[256];
+  givens_warp(a, sc, ss, sh);
+}
+
+// One classical Gram-Schmidt pass on the block's chunk of w:
+//   w chunk = fused dual-operator tail (gather) or loaded; optional w -= sum_i h_in[i] V_i;
+//   partial sums of conj(V_i) w and/or |w|^2, reduced by the last block to finish (fixed
+//   order => deterministic); optionally the last block then runs the Givens step.
+// nv = st->j + 1.  mode 0: dots + norm (out[0..nv]) ; 1: dots ; 2: norm only.
+struct CgsArgs {
+  int n, chunk, mode;
+  const double2* V;
+  size_t ldv;
+  GmresState* st;
+  const double2* h_in;
+  double2* w;
+  double2* part;
+  double2* out;
+  unsigned int* counter;
+  // fused dual tail (feti.cpp:542-555, 593): w[r] = -((u1_lo - cpl z)_lo - (u1_hi - cpl z)_hi)
+  int gather;
+  int NB, NC;
+  const int *lam_lo, *lam_hi, *cglob;
+  const double2 *u1b, *cpl_b, *z;
+  // fused Givens (pass 2)
+  int givens;
+  GivensArgs ga;
+};
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_cgs_pass(CgsArgs a) {
+  extern __shared__ double2 w_sh[];
+  __shared__ bool is_last;
+  const int nv = a.st->j + 1;
+  const int n = a.n, b = blockIdx.x, lo = b * a.chunk, len = max(0, min(a.chunk, n - lo));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < len; k += blockDim.x) {
+    double2 acc;
+    if (a.gather) {
+      const int r = lo + k;
+      const int slots[2] = {a.lam_lo[r], a.lam_hi[r]};
+      double2 u[2];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int slot = slots[q], s = slot / a.NB;
+        double2 cz_ = cz();
+        for (int c = 0; c < a.NC; ++c) {
+          const int cg = a.cglob[(size_t)s * a.NC + c];
+          if (cg >= 0) cz_ = cfma(a.cpl_b[(size_t)slot * a.NC + c], a.z[cg], cz_);
+        }
+        u[q] = csub(a.u1b[slot], cz_);
+      }
+      const double2 d = csub(u[0], u[1]);
+      acc = make_double2(-d.x, -d.y);
+      a.w[lo + k] = acc;
+    } else {
+      acc = a.w[lo + k];
+    }
+    if (a.h_in != nullptr) {
+      for (int i = 0; i < nv; ++i) acc = cfms(a.h_in[i], a.V[(size_t)i * a.ldv + lo + k], acc);
+      a.w[lo + k] = acc;
+    }
+    w_sh[k] = acc;
+  }
+  __syncthreads();
+  const int ndots = (a.mode == 2) ? 0 : nv;
+  const int nout = ndots + (a.mode == 1 ? 0 : 1);
+  for (int i = warp; i < nout; i += WARPS) {
+    double2 acc = cz();
+    if (i < ndots) {
+      const double2* v = a.V + (size_t)i * a.ldv + lo;
+#pragma unroll 4
+      for (int k = lane; k < len; k += 32) acc = cfma_conj(v[k], w_sh[k], acc);
+    } else {
+      for (int k = lane; k < len; k += 32) acc.x += cabs2(w_sh[k]);
+    }
+    acc = warp_sum2(acc);
+    if (lane == 0) a.part[(size_t)i * gridDim.x + b] = acc;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) is_last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  for (int i = warp; i < nout; i += WARPS) {
+    double2 acc = cz();
+#pragma unroll 4
+    for (int bb = lane; bb < (int)gridDim.x; bb += 32) acc = cadd(acc, __ldcg(a.part + (size_t)i * gridDim.x + bb));
+    acc = warp_sum2(acc);
+    if (lane == 0) a.out[i] = acc;
+  }
+  if (threadIdx.x == 0) *a.counter = 0u;
+  if (a.givens) {
+    __syncthreads();
+    if (warp == 0) {
+      // reuse the w chunk buffer for the rotation staging (256 + 256 + 256 entries)
+      double* sc = reinterpret_cast<double*>(w_sh);
+      double2* ss = w_sh + 128;
+      double2* sh = w_sh + 384;
+      givens_warp(a.ga, sc, ss, sh);
+    }
+  }
 }
 
 // V_{j+1} = (w - V h2) / h_{j+1,j}: the second CGS update fused with the normalisation
