@@ -111,6 +111,8 @@ struct Ctx {
   bool use_graph = true;
   bool debug_sync = false;
   bool sym_tma = false;
+  int sym_warps = 4;
+  size_t l2_persist_bytes = 0;
   bool watchdog = false;
   cudaGraph_t arnoldi_graph = nullptr;
   cudaGraphExec_t arnoldi_exec = nullptr;
@@ -278,6 +280,7 @@ struct Ctx {
     if (const char* e = std::getenv("FETIGPU_DEBUG_SYNC")) debug_sync = e[0] == '1';
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FETIGPU_SYM_TMA")) sym_tma = e[0] == '1';
+    if (const char* e = std::getenv("FETIGPU_SYM_WARPS")) sym_warps = std::atoi(e) == 8 ? 8 : 4;
     watchdog = std::getenv("FETIGPU_WATCHDOG") != nullptr;
     n = P.n();
     m = P.m();
@@ -437,7 +440,7 @@ struct Ctx {
       {
         int dev_sms = 0;
         CU(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, desc.device));
-        sym_grid = dev_sms * SYM_CTAS_PER_SM;
+        sym_grid = dev_sms;  // one persistent CTA per SM (k_sym_gemv_tma)
         const int smem = (int)sym_tma_smem(NT);
         CU(cudaFuncSetAttribute(k_sym_gemv_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         CU(cudaFuncSetAttribute(k_sym_gemv_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -518,8 +521,32 @@ struct Ctx {
                             (int)std::max<size_t>(nc * sizeof(double2), 1)));
     CU(cudaFuncSetAttribute(k_cgs_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cgs_smem()));
     setup_mass();
+    setup_l2_persistence();
     sync();
     setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  }
+
+  // The dense coarse inverse is read every Krylov step while the local operators stream
+  // 0.3 GB through L2 with evict-first loads; pin C^-1 in the persisting L2 carve-out
+  // (access-policy window on the context stream, inherited by captured graph nodes).
+  void setup_l2_persistence() {
+    if (nc == 0 || std::getenv("FETIGPU_NO_L2_PERSIST")) return;
+    int max_persist = 0, max_window = 0;
+    CU(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, desc.device));
+    CU(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, desc.device));
+    if (max_persist <= 0 || max_window <= 0) return;
+    const size_t bytes = (size_t)nc * nc * sizeof(double2);
+    const size_t carve = std::min<size_t>(bytes, (size_t)max_persist);
+    CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
+    cudaStreamAttrValue attr{};
+    attr.accessPolicyWindow.base_ptr = d_Cinv;
+    attr.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, (size_t)max_window);
+    attr.accessPolicyWindow.hitRatio =
+        (float)std::min(1.0, (double)carve / (double)attr.accessPolicyWindow.num_bytes);
+    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    CU(cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+    l2_persist_bytes = carve;
   }
 
   // V = M_y ⊗ M_x ⊗ I_dpn on the structured mesh: 1-D P1 mass (h/6)[.., 1, 4, 1, ..] with
@@ -590,11 +617,21 @@ struct Ctx {
 
   // packed symmetric GEMV: persistent TMA-streamed grid (k_sym_gemv_tma)
   void launch_sym(const SymGemvArgs& g) {
-    if (!sym_tma) {  // default: one CTA per subdomain, loads streamed from registers
-      switch (g.mode) {
-        case 0: k_sym_gemv<0><<<H.n_sub, 256, sym_smem(), stream>>>(g); break;
-        case 1: k_sym_gemv<1><<<H.n_sub, 256, sym_smem(), stream>>>(g); break;
-        default: k_sym_gemv<2><<<H.n_sub, 256, sym_smem(), stream>>>(g); break;
+    // the TMA variant keeps one whole subdomain operator in shared memory (NT <= 5)
+    if (!sym_tma || sym_tma_smem(NT) > 220 * 1024) {  // one CTA per subdomain, register streaming
+      const size_t sm = sym_smem();
+      if (sym_warps == 4) {
+        switch (g.mode) {
+          case 0: k_sym_gemv<0, 8, 4><<<H.n_sub, 128, sm, stream>>>(g); break;
+          case 1: k_sym_gemv<1, 8, 4><<<H.n_sub, 128, sm, stream>>>(g); break;
+          default: k_sym_gemv<2, 8, 4><<<H.n_sub, 128, sm, stream>>>(g); break;
+        }
+      } else {
+        switch (g.mode) {
+          case 0: k_sym_gemv<0, 8, 8><<<H.n_sub, 256, sm, stream>>>(g); break;
+          case 1: k_sym_gemv<1, 8, 8><<<H.n_sub, 256, sm, stream>>>(g); break;
+          default: k_sym_gemv<2, 8, 8><<<H.n_sub, 256, sm, stream>>>(g); break;
+        }
       }
       return;
     }

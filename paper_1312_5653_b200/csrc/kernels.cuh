@@ -449,9 +449,8 @@ struct SymGemvArgs {
   double2* g;
 };
 
-template <int MODE>
-__global__ void __launch_bounds__(256) k_sym_gemv(SymGemvArgs a) {
-  constexpr int WARPS = 8;
+template <int MODE, int SYM_BATCH, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(SymGemvArgs a) {
   // dynamic smem: x (32 NT) | row partials (ntiles x 32) | column partials (noff x 32)
   extern __shared__ double2 sg_sh[];
   const int NB = a.NB, NT = a.NT;
@@ -490,10 +489,10 @@ __global__ void __launch_bounds__(256) k_sym_gemv(SymGemvArgs a) {
   }
   __syncthreads();
   // ---- tiles: off-diagonal first (t < noff), then diagonal.  A diagonal tile streams half
-  // the bytes of an off-diagonal one, so when they fit, two diagonal tiles share a warp
-  // (NT = 4: warps 0-5 one off-diagonal tile each, warps 6-7 two diagonal tiles each).
+  // the bytes of an off-diagonal one, so two diagonal tiles form one work item
+  // (NT = 4, 8 warps: one item each; 4 warps: two items each).
   const double2* P = a.pack + (size_t)s * sym_tile_entries(NT);
-  const bool paired = noff + (NT + 1) / 2 <= WARPS;
+  const bool paired = true;
   for (int item = warp; item < (paired ? noff + (NT + 1) / 2 : ntiles); item += WARPS)
   for (int half = 0; half < ((paired && item >= noff) ? 2 : 1); ++half) {
     const int t = (paired && item >= noff) ? noff + 2 * (item - noff) + half : item;
@@ -505,12 +504,19 @@ __global__ void __launch_bounds__(256) k_sym_gemv(SymGemvArgs a) {
       const int J = t - I * (I - 1) / 2;
       const double2* O = P + NT * 17 * 32 + (size_t)t * 1024;
       const double2 xi = x_sh[32 * I + lane];
-#pragma unroll 8
-      for (int c = 0; c < 32; ++c) {
-        const double2 m = __ldcs(O + c * 32 + lane);
-        yr = cfma(m, x_sh[32 * J + ((lane + c) & 31)], yr);
-        yc = cfma(m, xi, yc);
-        yc = shfl2(yc, (lane + 1) & 31);  // carry column (l+c+1) into lane l
+      // explicit SYM_BATCH-row load batches: all loads of a batch are in flight together
+#pragma unroll
+      for (int cb = 0; cb < 32; cb += SYM_BATCH) {
+        double2 m[SYM_BATCH];
+#pragma unroll
+        for (int u = 0; u < SYM_BATCH; ++u) m[u] = __ldcs(O + (cb + u) * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < SYM_BATCH; ++u) {
+          const int c = cb + u;
+          yr = cfma(m[u], x_sh[32 * J + ((lane + c) & 31)], yr);
+          yc = cfma(m[u], xi, yc);
+          yc = shfl2(yc, (lane + 1) & 31);  // carry column (l+c+1) into lane l
+        }
       }
       // after 32 rotations lane l holds column l
       part_row[t][lane] = yr;
@@ -519,14 +525,22 @@ __global__ void __launch_bounds__(256) k_sym_gemv(SymGemvArgs a) {
       const int I = t - noff;
       const double2* D = P + (size_t)I * 17 * 32;
       const double2 xi = x_sh[32 * I + lane];
-      yr = cmul(__ldcs(D + lane), xi);
-      // c = 1..15: row + transposed; carry for the transposed part as above
-#pragma unroll 5
-      for (int c = 1; c < 16; ++c) {
-        const double2 m = __ldcs(D + c * 32 + lane);
-        yr = cfma(m, x_sh[32 * I + ((lane + c) & 31)], yr);
-        yc = shfl2(yc, (lane + 1) & 31);
-        yc = cfma(m, xi, yc);
+#pragma unroll
+      for (int cb = 0; cb < 16; cb += SYM_BATCH) {
+        double2 m[SYM_BATCH];
+#pragma unroll
+        for (int u = 0; u < SYM_BATCH; ++u) m[u] = __ldcs(D + (cb + u) * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < SYM_BATCH; ++u) {
+          const int c = cb + u;
+          if (c == 0) {
+            yr = cmul(m[u], xi);  // diagonal entry
+          } else {  // c = 1..15: row + transposed; carry for the transposed part as above
+            yr = cfma(m[u], x_sh[32 * I + ((lane + c) & 31)], yr);
+            yc = shfl2(yc, (lane + 1) & 31);
+            yc = cfma(m[u], xi, yc);
+          }
+        }
       }
       // yc in lane l now holds column (l + 15); c = 16 covers both (l, l+16) and (l+16, l)
       {
@@ -576,13 +590,15 @@ __global__ void __launch_bounds__(256) k_sym_gemv(SymGemvArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Streaming version of k_sym_gemv: a persistent grid (SYM_CTAS_PER_SM per SM) where warp 8
-// is a TMA producer that streams every tile of every subdomain the CTA owns into a
-// SYM_STAGES-deep shared-memory ring (cp.async.bulk + mbarrier full/empty pairs), and
-// warps 0-7 consume the tiles from shared memory.  Bytes in flight per SM no longer depend
-// on registers: the ring keeps ~SYM_STAGES x 16 KB outstanding per CTA.
-constexpr int SYM_STAGES = 6;
-constexpr int SYM_CTAS_PER_SM = 2;
+// Streaming version of k_sym_gemv: a persistent grid (one CTA per SM) where warp 8 is a TMA
+// producer streaming every tile of every subdomain the CTA owns into shared memory
+// (cp.async.bulk + mbarrier full/empty pairs) and warps 0-7 consume from shared memory.
+// The buffer holds exactly one subdomain's packed operator (133 KB at NB = 124) with one
+// slot per tile: slot t is always consumed by the same warp, so each barrier is waited on
+// strictly in phase order (a warp may never wait on phase k+1 of a slot before phase k has
+// completed — the parity test would alias).  While the consumers finish subdomain k, the
+// producer already refills every released slot with subdomain k+1: bytes in flight are set
+// by the buffer, not by registers.
 constexpr int SYM_TILE = 1024;  // complex entries of a full tile
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
@@ -590,61 +606,59 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(288, 2) k_sym_gemv_tma(SymGemvArgs a, int S) {
+__global__ void __launch_bounds__(288, 1) k_sym_gemv_tma(SymGemvArgs a, int S) {
   constexpr int CWARPS = 8, CTHREADS = 256;
   extern __shared__ __align__(128) unsigned char sgt_raw[];
-  double2* ring = reinterpret_cast<double2*>(sgt_raw);  // SYM_STAGES x SYM_TILE
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)SYM_STAGES * SYM_TILE);
-  uint64_t* empty = full + SYM_STAGES;
   const int NB = a.NB, NT = a.NT;
   const int noff = NT * (NT - 1) / 2, ntiles = noff + NT;
-  double2* x_sh = reinterpret_cast<double2*>(empty + SYM_STAGES);
+  const int per = sym_tile_entries(NT);
+  double2* buf = reinterpret_cast<double2*>(sgt_raw);  // one subdomain, same layout as global
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + per);
+  uint64_t* empty = full + ntiles;
+  double2* x_sh = reinterpret_cast<double2*>(empty + ntiles);
   double2 (*part_row)[32] = reinterpret_cast<double2 (*)[32]>(x_sh + 32 * NT);
   double2 (*part_col)[32] = reinterpret_cast<double2 (*)[32]>(x_sh + 32 * NT + 32 * ntiles);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int per = sym_tile_entries(NT);
+  // tile t: t < noff off-diagonal (16 KB, after the diagonal block), else diagonal t - noff
+  auto tile_off = [&](int t) -> int { return t < noff ? NT * 17 * 32 + t * SYM_TILE : (t - noff) * 17 * 32; };
   if (threadIdx.x == 0) {
-    for (int st = 0; st < SYM_STAGES; ++st) {
-      mbar_init(&full[st], 1);
-      mbar_init(&empty[st], 1);
+    for (int t = 0; t < ntiles; ++t) {
+      mbar_init(&full[t], 1);
+      mbar_init(&empty[t], 1);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  // tile t of a subdomain: t < noff off-diagonal (16 KB), else diagonal t - noff (8.5 KB)
-  auto tile_off = [&](int t) -> size_t {
-    return t < noff ? (size_t)NT * 17 * 32 + (size_t)t * SYM_TILE : (size_t)(t - noff) * 17 * 32;
-  };
   if (warp == CWARPS) {  // ---------------- TMA producer ----------------
     if (lane == 0) {
-      int q = 0;
-      for (int s = blockIdx.x; s < S; s += gridDim.x) {
+      int k = 0;
+      for (int s = blockIdx.x; s < S; s += gridDim.x, ++k) {
         const double2* P = a.pack + (size_t)s * per;
-        for (int t = 0; t < ntiles; ++t, ++q) {
-          const int st = q % SYM_STAGES;
-          mbar_wait(&empty[st], ((q / SYM_STAGES) & 1) ^ 1);
+        for (int t = 0; t < ntiles; ++t) {
+          mbar_wait(&empty[t], (k & 1) ^ 1);
           const uint32_t bytes = (t < noff ? SYM_TILE : 17 * 32) * (uint32_t)sizeof(double2);
-          mbar_arrive_expect_tx(&full[st], bytes);
-          tma_load_1d(ring + (size_t)st * SYM_TILE, P + tile_off(t), bytes, &full[st]);
+          mbar_arrive_expect_tx(&full[t], bytes);
+          tma_load_1d(buf + tile_off(t), P + tile_off(t), bytes, &full[t]);
         }
       }
     }
+    __syncwarp();
     return;
   }
   // ---------------- consumers ----------------
   const double2* lam = a.lam;
   if (MODE == 0 && a.jsel != nullptr) lam += (size_t)(*a.jsel) * a.jstride;
-  int qbase = 0;
-  for (int s = blockIdx.x; s < S; s += gridDim.x, qbase += ntiles) {
-    for (int k = threadIdx.x; k < 32 * NT; k += CTHREADS) {
+  int k = 0;
+  for (int s = blockIdx.x; s < S; s += gridDim.x, ++k) {
+    for (int i = threadIdx.x; i < 32 * NT; i += CTHREADS) {
       double2 v = cz();
-      if (k < NB) {
-        const size_t sb = (size_t)s * NB + k;
+      if (i < NB) {
+        const size_t sb = (size_t)s * NB + i;
         if (MODE == 2) {
           v = a.tb[sb];
           for (int e = 0; e < a.EBI; ++e) {
-            const int i = a.bi_idx[sb * a.EBI + e];
-            if (i >= 0) v = cfms(a.bi_val[sb * a.EBI + e], a.yi[(size_t)s * a.NI + i], v);
+            const int ii = a.bi_idx[sb * a.EBI + e];
+            if (ii >= 0) v = cfms(a.bi_val[sb * a.EBI + e], a.yi[(size_t)s * a.NI + ii], v);
           }
         } else {
           const int r = a.blam[sb];
@@ -658,19 +672,17 @@ __global__ void __launch_bounds__(288, 2) k_sym_gemv_tma(SymGemvArgs a, int S) {
           }
         }
       }
-      x_sh[k] = v;
+      x_sh[i] = v;
     }
     named_bar_sync(1, CTHREADS);
-    // tiles: round robin; with NT = 4, warps 0-5 one off-diagonal tile, warps 6-7 two diagonal
+    // tiles: with NT = 4, warps 0-5 one off-diagonal tile, warps 6-7 two diagonal tiles
     const bool paired = noff + (NT + 1) / 2 <= CWARPS;
     for (int item = warp; item < (paired ? noff + (NT + 1) / 2 : ntiles); item += CWARPS)
       for (int half = 0; half < ((paired && item >= noff) ? 2 : 1); ++half) {
         const int t = (paired && item >= noff) ? noff + 2 * (item - noff) + half : item;
         if (t >= ntiles) break;
-        const int q = qbase + t;
-        const int st = q % SYM_STAGES;
-        mbar_wait(&full[st], (q / SYM_STAGES) & 1);
-        const double2* T = ring + (size_t)st * SYM_TILE;
+        mbar_wait(&full[t], k & 1);
+        const double2* T = buf + tile_off(t);
         double2 yr = cz(), yc = cz();
         if (t < noff) {
           int I = 1;
@@ -701,21 +713,23 @@ __global__ void __launch_bounds__(288, 2) k_sym_gemv_tma(SymGemvArgs a, int S) {
           yc = shfl2(yc, (lane + 17) & 31);
           part_row[t][lane] = cadd(yr, yc);
         }
+        // order this warp's generic-proxy reads of the slot before the async-proxy refill
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+        if (lane == 0) mbar_arrive(&empty[t]);
       }
     named_bar_sync(1, CTHREADS);
-    for (int k = threadIdx.x; k < NB; k += CTHREADS) {
-      const int I = k >> 5, l = k & 31;
+    for (int i = threadIdx.x; i < NB; i += CTHREADS) {
+      const int I = i >> 5, l = i & 31;
       double2 acc = part_row[noff + I][l];
       for (int J = 0; J < I; ++J) acc = cadd(acc, part_row[I * (I - 1) / 2 + J][l]);
       for (int I2 = I + 1; I2 < NT; ++I2) acc = cadd(acc, part_col[I2 * (I2 - 1) / 2 + I][l]);
-      a.out[(size_t)s * NB + k] = acc;
+      a.out[(size_t)s * NB + i] = acc;
     }
     if (a.gcp != nullptr) {
       for (int c = warp; c < a.NC; c += CWARPS) {
         double2 acc = cz();
-        for (int k = lane; k < NB; k += 32) acc = cfma(a.cpl_b[((size_t)s * NB + k) * a.NC + c], x_sh[k], acc);
+        for (int i = lane; i < NB; i += 32) acc = cfma(a.cpl_b[((size_t)s * NB + i) * a.NC + c], x_sh[i], acc);
         acc = warp_sum2(acc);
         if (lane == 0) a.gcp[(size_t)s * a.NC + c] = acc;
       }
@@ -744,7 +758,7 @@ __global__ void __launch_bounds__(288, 2) k_sym_gemv_tma(SymGemvArgs a, int S) {
 }
 
 __host__ __device__ constexpr size_t sym_tma_smem(int NT) {
-  return (size_t)SYM_STAGES * SYM_TILE * 16 + 2 * SYM_STAGES * 8 +
+  return (size_t)sym_tile_entries(NT) * 16 + 2 * (size_t)(NT * (NT - 1) / 2 + NT) * 8 +
          (size_t)16 * 32 * (NT + (NT * (NT - 1) / 2 + NT) + NT * (NT - 1) / 2);
 }
 
