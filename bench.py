@@ -14,8 +14,13 @@ reused across steps (the reference's per_solve_seconds regime, experiments.cpp:2
   --impl reference : the CPU restatement of the reference (oracle/) on this host's cores,
           same workload and metric (rank 0 only under torchrun).
 
-Multi-GPU (N > 1): each rank runs its own config-2 Schur solves (replicas, weak scaling);
-the subdomain-sharded NCCL path is SURVEY.md §8(e) work in progress.
+Multi-GPU (N > 1, torchrun, one rank per GPU): weak scaling on the subdomain-sharded NCCL
+path.  The mesh grows with N at a fixed 1024 subdomains of 32x32 elements
+per GPU: N=2 1024x2048 (32x64 subdomains), N=4 2048x2048 (64x64, the BASELINE config-3
+mesh), N=8 2048x4096 (64x128); subdomain rows are sharded block-wise, cut-line multipliers
+are exchanged with NCCL send/recv, Krylov dots allreduced, the coarse problem solved
+redundantly.  value = Schur solves/s x N (config-2-equivalent solves/s: each solve of the
+N-GPU mesh is N config-2 blocks of work), so ideal weak scaling is value_N = N value_1.
 """
 from __future__ import annotations
 
@@ -36,6 +41,17 @@ METRIC = "Schur solves/sec (2 complex FETI-DPH solves), 2D Poisson 1M dofs"
 UNIT = "solves/s"
 N_GRID, S_SUB, PHI, TOL, MAX_ITER = 1024, 32, 1e-4, 1e-10, 2000
 PHI_SWEEP = (1e-2, 1e-4, 1e-6, 1e-8)
+# weak-scaling meshes: N -> (blocks along x, blocks along y) of 1024^2 elements / 32x32 subdomains
+WEAK_BLOCKS = {1: (1, 1), 2: (1, 2), 4: (2, 2), 8: (2, 4)}
+
+
+def weak_problem_args(world):
+    """(n_x, n_y, s_x, s_y, len_x, len_y) of the N-GPU weak-scaling mesh (square elements)."""
+    if world not in WEAK_BLOCKS:
+        raise SystemExit(f"bench.py: --gpus must be one of {sorted(WEAK_BLOCKS)}")
+    a, b = WEAK_BLOCKS[world]
+    m = max(a, b)
+    return N_GRID * a, N_GRID * b, S_SUB * a, S_SUB * b, a / m, b / m
 
 
 def dist_env():
@@ -122,17 +138,6 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-def sum_over_ranks(x, world):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
-
-
 def cpu_sample_oracle(threads, steps, warmup, budget_s=150.0):
     """The oracle (CPU restatement of the reference) on config 2: setup once, then Schur
     solves on seeded targets.  Returns (solves/s, iterations, setup s, steps run)."""
@@ -190,14 +195,27 @@ def run_gpu(args):
     import paper_1312_5653_b200 as F
 
     steps, warmup = args.steps, max(args.warmup, 3)
-    p = F.make_seeded_problem(N_GRID, PHI, seed=0)
+    n_x, n_y, s_x, s_y, len_x, len_y = weak_problem_args(world)
+
+    def problem(seed):
+        return F.make_problem(n_x, n_y, PHI, len_x=len_x, len_y=len_y, target="sine", seed=seed)
+
+    p = problem(0)
     t0 = time.perf_counter()
-    solver = F.SchurSolver(p, S_SUB, S_SUB, tol=TOL, max_iter=MAX_ITER, device=local)
+    if world > 1:  # subdomain-sharded over NCCL; rank 0 makes the NCCL id
+        import torch.distributed as dist
+
+        obj = [F.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        solver = F.SchurSolver(p, s_x, s_y, tol=TOL, max_iter=MAX_ITER, device=local, rank=rank, world=world,
+                               nccl_id=obj[0])
+    else:
+        solver = F.SchurSolver(p, s_x, s_y, tol=TOL, max_iter=MAX_ITER, device=local)
     setup_s = time.perf_counter() - t0
     n = p.n
-    # seeded targets for every step, resident in HBM before the timed region
-    seeds = [rank * 100000 + k for k in range(warmup + steps)]
-    targets = [F.make_seeded_problem(N_GRID, PHI, seed=s).target_state for s in seeds]
+    # seeded targets for every step (the same on every rank), resident in HBM before the timed region
+    seeds = list(range(warmup + steps))
+    targets = [problem(s).target_state for s in seeds]
     d_ybar = [torch.from_numpy(t).cuda() for t in targets]
     d_y = torch.empty(n, dtype=torch.float64, device="cuda")
     d_u = torch.empty_like(d_y)
@@ -227,8 +245,7 @@ def run_gpu(args):
     launches = solver.launch_count() - launches0
     t_dev = ev0.elapsed_time(ev1) / 1000.0
     t_max = max_over_ranks(t_dev, world)
-    total_solves = sum_over_ranks(steps, world)
-    value = total_solves / t_max
+    value = steps * world / t_max  # config-2-equivalent solves/s (see the module docstring)
     # ---------------- e2e: host buffers through the public API ----------------
     # host buffers in pinned memory (the path a serving caller would use)
     host_t = [torch.from_numpy(t).pin_memory().numpy() for t in targets]
@@ -242,7 +259,7 @@ def run_gpu(args):
     w1 = time.perf_counter()
     barrier(world)
     e2e_t = max_over_ranks(w1 - w0, world)
-    e2e = sum_over_ranks(steps, world) / e2e_t
+    e2e = steps * world / e2e_t
     # ---------------- per-kernel roofline pass (same K steps, events per launch) ----------------
     solver.profile(True)
     solver.profile_read(reset=True)
@@ -277,11 +294,14 @@ def run_gpu(args):
         "ms_per_step": t_max / steps * 1000.0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (seeded sine-mode ybar, seed = step; factors random-free FEM)",
         "config": {
-            "workload": "config2: 1024x1024 Q1 heat, 32x32 subdomains of 32x32, phi=1e-4, tol 1e-10, FP64 complex",
+            "workload": ("config2: 1024x1024 Q1 heat, 32x32 subdomains of 32x32, phi=1e-4, tol 1e-10, FP64 complex"
+                         if world == 1 else
+                         f"weak scaling: {n_x}x{n_y} Q1 heat, {s_x}x{s_y} subdomains of 32x32 ({s_x * s_y // world} "
+                         f"per GPU), phi=1e-4, tol 1e-10, FP64 complex; value = solves/s x {world}"),
             "phi": PHI, "n_free": n, "n_lambda": solver.n_lambda, "coarse_dim": solver.coarse_dim,
             "iterations_plus_minus_mean": [float(np.mean([a for a, _ in its])), float(np.mean([b for _, b in its]))],
             "setup_seconds": setup_s, "l2": "inputs larger than L2 (local operators 0.5 GB streamed per iteration)",
-            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+            "parallelism": f"subdomain rows sharded over {world} GPUs (NCCL)" if world > 1 else "1 GPU",
             "kernel_ms_per_step": kernel_breakdown, "profiled_ms_per_step": t_prof,
         },
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 3 * 8 * n},
@@ -292,7 +312,7 @@ def run_gpu(args):
         "clocks": clk.summary(),
     }
     # BASELINE config 2 is a phi sweep: rates and iteration counts per phi (own factors each)
-    if rank == 0 and not args.no_sweep:
+    if rank == 0 and world == 1 and not args.no_sweep:
         sweep = {}
         for phi in PHI_SWEEP:
             q = F.make_seeded_problem(N_GRID, phi, seed=0)
@@ -312,7 +332,7 @@ def run_gpu(args):
                                                            st["minus_stats"]["iterations"]]}
             sv.close()
         line["config"]["phi_sweep"] = sweep
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, cits, csetup, ran = cpu_sample_oracle(os.cpu_count() or 1, 1, 0)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
                                 "sample": f"{ran} config-2 Schur solve after setup ({csetup:.1f} s), oracle/ "

@@ -119,6 +119,31 @@ int fetigpu_feti_solve(fetigpu_ctx* ctx, int sign, const double* rhs_c128, doubl
 int fetigpu_apply_dual(fetigpu_ctx* ctx, int sign, const double* lam_c128, double* out_c128);
 int fetigpu_apply_precond(fetigpu_ctx* ctx, int sign, const double* r_c128, double* out_c128);
 
+/* ---- sharded multi-GPU path ------------------------------------------
+ * Rank r of R owns subdomain rows [r s_y/R, (r+1) s_y/R) (s_y % R == 0).  Per Krylov step
+ * the ranks exchange cut-line interface values with their two neighbours and allreduce the
+ * coarse rhs and the two CGS dot vectors; the coarse problem is solved redundantly.  There
+ * is no counterpart in the reference (threads only). */
+
+/* NCCL unique id (128 bytes): create on rank 0, broadcast to the other ranks. */
+int fetigpu_nccl_unique_id(unsigned char* out128);
+
+/* Sharded context over NCCL, one process per GPU (desc->device = this rank's GPU).  The
+ * schur/feti solve entry points then take and return FULL vectors on every rank. */
+int fetigpu_create_sharded(const fetigpu_desc* desc, int rank, int world, const unsigned char* nccl_id,
+                           fetigpu_ctx** out);
+
+/* Host-only layout of rank `rank` (for tests): info[0..11] = first subdomain, local
+ * subdomains, phantom subdomains, first local multiplier (global id), ghost rows, owned
+ * rows, top-cut rows, first owned free dof, owned free dofs, halo slots sent up, halo
+ * slots sent down, local multipliers. */
+int fetigpu_rank_info(const fetigpu_desc* desc, int rank, int world, int* info);
+
+/* `world` ranks emulated by host threads on ONE device (desc->device), with device-to-
+ * device copies standing in for NCCL; one range-space Schur solve, rank 0's result. */
+int fetigpu_emulated_schur_solve(const fetigpu_desc* desc, int world, const double* ybar, const double* yc,
+                                 double* y, double* u, double* lambda, fetigpu_schur_stats* stats);
+
 /* ---- instrumentation --------------------------------------------------------------- */
 
 /* The cudaStream_t (as void*) every kernel of this context is launched on. */

@@ -176,13 +176,20 @@ class SchurSolver:
     """
 
     def __init__(self, problem: ControlProblem, s_x=2, s_y=2, tol=1e-10, max_iter=1000, mass_coeff=None,
-                 device=0, augment=False):
+                 device=0, augment=False, rank=None, world=None, nccl_id=None):
         if augment:
             raise ContractError("edge-RBM augmentation is not implemented on the B200 path (augment=False)")
         self.problem = problem
         self._desc = problem.desc(s_x, s_y, tol, max_iter, mass_coeff, device, augment)
         h = C.c_void_p()
-        _check(_native.lib().fetigpu_create(C.byref(self._desc), C.byref(h)))
+        if world is not None and world > 1:
+            # sharded over NCCL: this process is `rank` (subdomain rows rank*s_y/world ...)
+            if nccl_id is None or rank is None:
+                raise ContractError("sharded SchurSolver needs rank, world and the nccl_id of rank 0")
+            _check(_native.lib().fetigpu_create_sharded(C.byref(self._desc), rank, world, bytes(nccl_id),
+                                                        C.byref(h)))
+        else:
+            _check(_native.lib().fetigpu_create(C.byref(self._desc), C.byref(h)))
         self._h = h
         info = problem._info(s_x, s_y)
         self.n, self.m, self.n_lambda, self.coarse_dim = int(info[0]), int(info[1]), int(info[4]), int(info[3])
@@ -269,6 +276,38 @@ class SchurSolver:
 
     def class_bytes(self, klass):
         return float(_native.lib().fetigpu_class_bytes(self._h, _native.K_CLASSES.index(klass)))
+
+
+def nccl_unique_id():
+    """128-byte NCCL unique id for SchurSolver(..., rank, world, nccl_id) (create on rank 0)."""
+    buf = C.create_string_buffer(128)
+    _check(_native.lib().fetigpu_nccl_unique_id(buf))
+    return buf.raw
+
+
+def rank_info(problem: ControlProblem, s_x, s_y, rank, world):
+    """Host-side layout of one rank of the sharded path (no GPU needed)."""
+    info = np.zeros(12, dtype=np.int32)
+    _check(_native.lib().fetigpu_rank_info(C.byref(problem.desc(s_x, s_y)), rank, world,
+                                           info.ctypes.data_as(C.POINTER(C.c_int))))
+    keys = ("sub_first", "n_sub_local", "n_phantom", "lam_base", "n_ghost", "n_owned", "n_top_cut", "free_first",
+            "free_count", "halo_up", "halo_down", "n_lambda_local")
+    return dict(zip(keys, (int(v) for v in info)))
+
+
+def emulated_schur_solve(problem: ControlProblem, world, s_x=2, s_y=2, tol=1e-10, max_iter=1000, device=0):
+    """The sharded solve with `world` ranks emulated by host threads on ONE GPU (test path)."""
+    problem.validate()
+    d = problem.desc(s_x, s_y, tol, max_iter, None, device)
+    n = problem.n
+    ybar = np.ascontiguousarray(problem.target_state, dtype=np.float64)
+    yc = problem.boundary_values
+    ycp = _dp(np.ascontiguousarray(yc, dtype=np.float64)) if yc is not None and problem.m > 0 else None
+    y, u, lam = np.zeros(n), np.zeros(n), np.zeros(n)
+    st = SchurStats()
+    _check(_native.lib().fetigpu_emulated_schur_solve(C.byref(d), world, _dp(ybar), ycp, _dp(y), _dp(u), _dp(lam),
+                                                      C.byref(st)))
+    return _schur_result(y, u, lam, st)
 
 
 def _stats_dict(st: SchurStats):

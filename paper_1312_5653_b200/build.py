@@ -15,8 +15,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libfetigpu.so")
-SOURCES = ["host_core.cpp", "fetigpu.cu"]
-HEADERS = ["host_core.hpp", "common.cuh", "band.cuh", "kernels.cuh"]
+SOURCES = ["host_core.cpp", "comm.cu", "fetigpu.cu"]
+HEADERS = ["host_core.hpp", "comm.hpp", "common.cuh", "band.cuh", "kernels.cuh"]
 
 
 def nvcc_path():
@@ -24,6 +24,21 @@ def nvcc_path():
         if cand and os.path.exists(cand):
             return cand
     raise RuntimeError("nvcc not found")
+
+
+def nccl_dirs():
+    """NCCL of the torch install (nvidia-nccl wheel) when present, else the system one.
+
+    The library must link the SAME libnccl.so.2 torch loads: both use the soname libnccl.so.2,
+    so whichever is loaded first serves the other, and torch needs its own (newer) version.
+    """
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    for base in (spec.submodule_search_locations or []) if spec else []:
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(lib, "libnccl.so.2")) and os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc, lib
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
 def _stale():
@@ -38,11 +53,13 @@ def build(force=False, verbose=False):
     if not force and not _stale():
         return LIB
     os.makedirs(OUT_DIR, exist_ok=True)
+    nccl_inc, nccl_lib = nccl_dirs()
     cmd = [
         nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
         "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-shared", "-Xptxas", "-v" if verbose else "-O3",
-        "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
+        "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + nccl_inc,
         *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp",
+        "-L" + nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nccl_lib,
     ]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

@@ -21,9 +21,11 @@
 #include <functional>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "band.cuh"
+#include "comm.hpp"
 #include "fetigpu.h"
 #include "host_core.hpp"
 #include "kernels.cuh"
@@ -59,7 +61,17 @@ struct ProfEvent {
 struct Ctx {
   fetigpu_desc desc{};
   HostProblem P;
-  HostPartition H;
+  HostPartition H;  // single GPU: the whole partition; sharded: this rank's local view
+  // ---- sharding; comm == nullptr on one GPU
+  std::unique_ptr<Comm> comm;
+  RankPlan plan;
+  int own0 = 0, nown = 0;  // owned multiplier rows [own0, own0 + nown) of the local numbering
+  int n_slot_ext = 0;      // (local + phantom subdomains) * NB
+  int *d_up_send = nullptr, *d_up_recv = nullptr, *d_dn_send = nullptr, *d_dn_recv = nullptr;
+  double2 *d_xs_up = nullptr, *d_xr_up = nullptr, *d_xs_dn = nullptr, *d_xr_dn = nullptr;
+  bool dist() const { return comm != nullptr && comm->world() > 1; }
+  ElemAe elem_ae{};
+  ElemKM elem_km{};
   cudaStream_t stream = nullptr;
   cd mc;       // mass coefficient of the factored operator K + mc V
   double phi = 0;
@@ -295,15 +307,18 @@ struct Ctx {
     M = MeshLayout{P.nx, P.ny, P.dpn};
     const int S = H.n_sub, NI = H.NI, NB = H.NB, NC = H.NC, LD = Wt + 1;
 
-    // element matrices -> constant memory
+    // element matrices (kernel parameters)
     {
-      double2 ae[64];
       const int ed = P.edofs;
-      for (int q = 0; q < ed * ed; ++q) ae[q] = d2(cd(P.ke[q]) + mc * P.me[q]);
-      CU(cudaMemcpyToSymbolAsync(c_Ae, ae, sizeof(double2) * ed * ed, 0, cudaMemcpyHostToDevice, stream));
-      CU(cudaMemcpyToSymbolAsync(c_Ke, P.ke, sizeof(double) * ed * ed, 0, cudaMemcpyHostToDevice, stream));
-      CU(cudaMemcpyToSymbolAsync(c_Me, P.me, sizeof(double) * ed * ed, 0, cudaMemcpyHostToDevice, stream));
+      for (int q = 0; q < ed * ed; ++q) {
+        elem_ae.v[q] = d2(cd(P.ke[q]) + mc * P.me[q]);
+        elem_km.k[q] = P.ke[q];
+        elem_km.m[q] = P.me[q];
+      }
     }
+    own0 = dist() ? plan.n_ghost : 0;
+    nown = dist() ? plan.n_owned : nl;
+    n_slot_ext = (S + (dist() ? plan.n_phantom : 0)) * NB;
     // index tables
     d_ldof = upload(H.ldof);
     d_idof = upload(H.idof);
@@ -338,7 +353,7 @@ struct Ctx {
     d_Abc = alloc<double2>((size_t)S * NB * NC);
     d_Acc = alloc<double2>((size_t)S * NC * NC);
     d_cpl_i = alloc<double2>((size_t)S * NI * NC);
-    d_cpl_b = alloc<double2>((size_t)S * NB * NC);
+    d_cpl_b = alloc<double2>((size_t)n_slot_ext * NC);
     zero(d_colband, (size_t)S * NI * LD);
     zero(d_rowband, (size_t)S * NI * LD);
     zero(d_Sbb, (size_t)S * NB * NB);
@@ -350,7 +365,7 @@ struct Ctx {
     CU(cudaMemsetAsync(d_bi_idx, 0xff, (size_t)S * NB * H.MAXE_BI * sizeof(int), stream));
     CU(cudaMemsetAsync(d_ib_idx, 0xff, (size_t)S * NI * H.MAXE_IB * sizeof(int), stream));
     launch(FETIGPU_K_OTHER, [&] {
-      k_assemble<<<cdiv((long long)S * H.nld, 128), 128, 0, stream>>>(L, d_ldof, d_colband, d_bi_idx, d_bi_val,
+      k_assemble<<<cdiv((long long)S * H.nld, 128), 128, 0, stream>>>(L, elem_ae, d_ldof, d_colband, d_bi_idx, d_bi_val,
                                                                       d_ib_idx, d_ib_val, d_Sbb, d_Aic, d_Abc, d_Acc);
     });
     launch(FETIGPU_K_OTHER, [&] { k_pad_identity<<<S, 128, 0, stream>>>(L, d_n_i, d_n_b, d_colband, d_Sbb); });
@@ -389,6 +404,8 @@ struct Ctx {
       launch(FETIGPU_K_OTHER, [&] {
         k_coupling_i<<<cdiv((long long)S * NI, 128), 128, 0, stream>>>(L, Yc, Y, d_cpl_b, d_cpl_i);
       });
+      setup_halo();
+      slot_exchange(d_cpl_b, NC);  // phantom rows of the coupling (static)
       double2* contrib = alloc<double2>((size_t)S * NC * NC);
       launch(FETIGPU_K_OTHER, [&] {
         k_coarse_contrib<<<S, 256, 0, stream>>>(L, d_Aic, d_Abc, d_cpl_i, d_cpl_b, contrib);
@@ -405,6 +422,8 @@ struct Ctx {
           k_coarse_assemble<<<cdiv(nc, 128), 128, 0, stream>>>(nc, WCt, NC, d_corner_slots, d_cglob, d_Acc, contrib,
                                                                cband);
         });
+        // sharded: every rank assembled its subdomains' part; sum, then factor redundantly
+        if (dist()) comm->allreduce_sum(reinterpret_cast<double*>(cband), (size_t)nc * LDC * 2, stream);
         launch(FETIGPU_K_OTHER, [&] { k_coarse_scale<<<cdiv(nc, 128), 128, 0, stream>>>(nc, WCt, cband, cscale_d); });
         launch(FETIGPU_K_OTHER, [&] { k_coarse_apply_scale<<<nc, 64, 0, stream>>>(nc, WCt, cband, cscale_d); });
         band_ldlt(cband, crow, WCt, 1, nc, d_status);
@@ -469,8 +488,8 @@ struct Ctx {
     d_tb = alloc<double2>((size_t)S * NB);
     d_yi = alloc<double2>((size_t)S * NI);
     d_ri = alloc<double2>((size_t)S * NI);
-    d_u1b = alloc<double2>((size_t)S * NB);
-    d_wb = alloc<double2>((size_t)S * NB);
+    d_u1b = alloc<double2>((size_t)n_slot_ext);
+    d_wb = alloc<double2>((size_t)n_slot_ext);
     d_gcp = alloc<double2>((size_t)S * NC);
     d_fc = alloc<double2>(std::max(nc, 1));
     d_g = alloc<double2>(std::max(nc, 1));
@@ -486,8 +505,8 @@ struct Ctx {
     d_r = alloc<double2>(ldv);
     d_d = alloc<double2>(ldv);
     d_best = alloc<double2>(ldv);
-    mdot_blocks = std::max(1, std::min(296, cdiv(nl, 64)));
-    mdot_chunk = cdiv(nl, mdot_blocks);
+    mdot_blocks = std::max(1, std::min(296, cdiv(nown, 64)));
+    mdot_chunk = cdiv(std::max(nown, 1), mdot_blocks);
     d_part = alloc<double2>((size_t)(vcap + 2) * mdot_blocks);
     d_red = alloc<double2>(3 * (vcap + 2));
     d_y = alloc<double2>(vcap + 2);
@@ -601,17 +620,73 @@ struct Ctx {
   template <typename T>
   void apply_global(const T* x, const double* xc, cd kc, cd mcoef, T* y) {
     launch(FETIGPU_K_GLOBAL, [&] {
-      k_apply_global<T><<<cdiv(n, 256), 256, 0, stream>>>(M, n, d_free_dofs, d_free_map, d_cons_map, x, xc, d2(kc),
+      k_apply_global<T><<<cdiv(n, 256), 256, 0, stream>>>(M, elem_km, n, d_free_dofs, d_free_map, d_cons_map, x, xc, d2(kc),
                                                           d2(mcoef), y);
     });
+  }
+
+  // ------------------------------------------------------------------------ sharding
+  // All no-ops on one GPU.
+  void setup_halo() {
+    if (!dist()) return;
+    auto up = [&](const std::vector<int>& v) -> int* { return v.empty() ? nullptr : upload(v); };
+    d_up_send = up(plan.to_up.send_slots);
+    d_up_recv = up(plan.to_up.recv_slots);
+    d_dn_send = up(plan.to_down.send_slots);
+    d_dn_recv = up(plan.to_down.recv_slots);
+    const size_t nmax = std::max({plan.to_up.send_slots.size(), plan.to_up.recv_slots.size(),
+                                  plan.to_down.send_slots.size(), plan.to_down.recv_slots.size(), (size_t)1}) *
+                        std::max(H.NC, 1);
+    d_xs_up = alloc<double2>(nmax);
+    d_xr_up = alloc<double2>(nmax);
+    d_xs_dn = alloc<double2>(nmax);
+    d_xr_dn = alloc<double2>(nmax);
+  }
+  // cut-line halo of per-dof slot values (width complex values per slot): my cut dofs go to
+  // the neighbour's phantom slots and theirs come into mine
+  void slot_exchange(double2* val, int width) {
+    if (!dist()) return;
+    const int nus = (int)plan.to_up.send_slots.size(), nur = (int)plan.to_up.recv_slots.size();
+    const int nds = (int)plan.to_down.send_slots.size(), ndr = (int)plan.to_down.recv_slots.size();
+    if (nus)
+      launch(FETIGPU_K_LAMBDA, [&] {
+        k_pack_slots<<<cdiv((long long)nus * width, 256), 256, 0, stream>>>(nus, width, d_up_send, val, d_xs_up);
+      });
+    if (nds)
+      launch(FETIGPU_K_LAMBDA, [&] {
+        k_pack_slots<<<cdiv((long long)nds * width, 256), 256, 0, stream>>>(nds, width, d_dn_send, val, d_xs_dn);
+      });
+    const size_t w2 = 2 * (size_t)width;
+    comm->exchange(reinterpret_cast<double*>(d_xs_up), w2 * nus, reinterpret_cast<double*>(d_xr_up), w2 * nur,
+                   reinterpret_cast<double*>(d_xs_dn), w2 * nds, reinterpret_cast<double*>(d_xr_dn), w2 * ndr, stream);
+    if (nur)
+      launch(FETIGPU_K_LAMBDA, [&] {
+        k_unpack_slots<<<cdiv((long long)nur * width, 256), 256, 0, stream>>>(nur, width, d_up_recv, d_xr_up, val);
+      });
+    if (ndr)
+      launch(FETIGPU_K_LAMBDA, [&] {
+        k_unpack_slots<<<cdiv((long long)ndr * width, 256), 256, 0, stream>>>(ndr, width, d_dn_recv, d_xr_dn, val);
+      });
+  }
+  // ghost multipliers (bottom cut) of a local multiplier vector <- the lower rank's top cut
+  void ghost_refresh(double2* v) {
+    if (!dist()) return;
+    comm->exchange(reinterpret_cast<double*>(v + own0 + nown - plan.n_top_cut), 2 * (size_t)plan.n_top_cut, nullptr,
+                   0, nullptr, 0, reinterpret_cast<double*>(v), 2 * (size_t)plan.n_ghost, stream);
+  }
+  void allreduce(double2* buf, size_t count) {
+    if (dist() && count) comm->allreduce_sum(reinterpret_cast<double*>(buf), 2 * count, stream);
   }
 
   // ------------------------------------------------------------------------ operators
   void coarse_solve(const double2* fc) {  // g = fc - sum gcp ; z = C^-1 g
     if (nc == 0) return;
+    // sharded: each rank sums its own subdomains (f_c counted once, on rank 0), then allreduce
+    const double2* fc_r = (dist() && comm->rank() != 0) ? nullptr : fc;
     launch(FETIGPU_K_COARSE, [&] {
-      k_coarse_rhs<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_slots, d_gcp, fc, d_g);
+      k_coarse_rhs<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_slots, d_gcp, fc_r, d_g);
     });
+    allreduce(d_g, nc);
     coarse_gemv();
   }
 
@@ -665,7 +740,7 @@ struct Ctx {
     return g;
   }
   // local dual solve u1_b = S_bb^-1 t_b with t_b = -B^T lam, gcp = cpl_b^T t_b, and (last
-  // CTA) the coarse rhs g = -sum gcp (K5)
+  // CTA) the coarse rhs g = -sum gcp (K5); sharded: partial g summed over ranks
   void dual_gemv(SymGemvArgs g) {
     g.alpha = -1.0;
     g.out = d_u1b;
@@ -679,6 +754,7 @@ struct Ctx {
       g.g = d_g;
     }
     launch(FETIGPU_K_DUAL_GEMV, [&] { launch_sym(g); });
+    allreduce(d_g, nc);
   }
   void coarse_gemv() {
     if (nc == 0) return;
@@ -686,15 +762,18 @@ struct Ctx {
       k_coarse_gemv<8><<<cdiv(nc, 8), 256, nc * sizeof(double2), stream>>>(nc, d_Cinv, d_g, d_z);
     });
   }
+  // u_b = u1_b - cpl_b z gathered onto the owned multiplier rows: out = -B u  (feti.cpp:593)
   void dual_tail(double2* out) {
     coarse_gemv();
+    slot_exchange(d_u1b, 1);
     launch(FETIGPU_K_LAMBDA, [&] {
-      k_lam_gather_dual<<<cdiv(nl, 256), 256, 0, stream>>>(nl, H.NB, H.NC, d_lam_lo, d_lam_hi, d_u1b, d_cpl_b,
-                                                           d_cglob, d_z, out);
+      k_lam_gather_dual<<<cdiv(nown, 256), 256, 0, stream>>>(nown, H.NB, H.NC, d_lam_lo + own0, d_lam_hi + own0,
+                                                             d_u1b, d_cpl_b, d_cglob, d_z, out + own0);
     });
   }
-  // F lam (feti.cpp:581-594) -> out
-  void apply_dual(const double2* lam, double2* out) {
+  // F lam (feti.cpp:581-594) -> out (owned rows); lam's ghost rows are refreshed first
+  void apply_dual(double2* lam, double2* out) {
+    ghost_refresh(lam);
     SymGemvArgs g = sym_args(d_Sinv_p);
     g.mode = 0;
     g.lam = lam;
@@ -711,11 +790,14 @@ struct Ctx {
     g.alpha = 0.5;
     g.out = d_wb;
     launch(FETIGPU_K_PRECOND_GEMV, [&] { launch_sym(g); });
+    slot_exchange(d_wb, 1);
   }
-  void apply_precond(const double2* r, double2* out) {
+  void apply_precond(double2* r, double2* out) {
+    ghost_refresh(r);
     precond_gemv(r, nullptr);
     launch(FETIGPU_K_LAMBDA, [&] {
-      k_lam_gather_pre<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_lam_lo, d_lam_hi, d_wb, out);
+      k_lam_gather_pre<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_lam_lo + own0, d_lam_hi + own0, d_wb,
+                                                            out + own0);
     });
   }
   // eliminate (feti.cpp:516-556), split in two halves.  A_rr is applied through its block
@@ -743,6 +825,7 @@ struct Ctx {
     launch(FETIGPU_K_OTHER, [&] {
       k_ub_correct<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(L, d_cglob, d_z, d_cpl_b, d_u1b);
     });
+    slot_exchange(d_u1b, 1);  // the other side of owned cut rows (jump, primal assembly)
   }
   // interior harmonic extension u_i = A_ii^-1 (t_i - A_ib u_b - A_ic z) = y_i - A_ii^-1 (A_ib u_b + A_ic z)
   // -> d_ri (requires eliminate_boundary first)
@@ -758,11 +841,16 @@ struct Ctx {
     });
   }
 
-  // |x|^2 and max|x| of a complex vector -> host (synchronizes)
-  std::pair<double, double> norm_max(const double2* x, int len) {
-    const int blocks = std::max(1, std::min(296, cdiv(len, 256)));
+  // |x|^2 and max|x| of a complex vector -> host (synchronizes); sharded = over all ranks
+  std::pair<double, double> norm_max(const double2* x, int len, bool sharded = false) {
+    const int blocks = std::max(1, std::min(296, cdiv(std::max(len, 1), 256)));
     launch(FETIGPU_K_ORTHO, [&] { k_norm_max_part<<<blocks, 256, 0, stream>>>(len, x, d_part); });
     launch(FETIGPU_K_ORTHO, [&] { k_norm_max_final<<<1, 32, 0, stream>>>(blocks, d_part, d_red); });
+    if (sharded && dist()) {
+      double* r = reinterpret_cast<double*>(d_red);
+      comm->allreduce_sum(r, 1, stream);
+      comm->allreduce_max(r + 1, 1, stream);
+    }
     CU(cudaMemcpyAsync(h_pin, d_red, sizeof(double2), cudaMemcpyDeviceToHost, stream));
     sync();
     return {std::sqrt(h_pin[0].x), h_pin[0].y};
@@ -794,42 +882,49 @@ struct Ctx {
     }
     mark(3);
     coarse_gemv();
+    slot_exchange(d_u1b, 1);  // sharded: the other side of the owned cut rows
     mark(4);
     CgsArgs c{};
-    c.n = nl;
+    c.n = nown;  // owned multiplier rows (all rows on one GPU)
     c.chunk = mdot_chunk;
-    c.V = d_V;
+    c.V = d_V + own0;
     c.ldv = ldv;
     c.st = d_gst;
-    c.w = d_w;
+    c.w = d_w + own0;
     c.part = d_part;
     c.counter = d_counter;
     const size_t sm = cgs_smem();
+    const int nv = dist() ? h_gst->j + 1 : 0;  // sharded path is eager: j known on the host
     // pass 1: w = F z (dual tail gathered per chunk), h1 = V^H w, |w|^2
     c.mode = 0;
     c.out = h1;
     c.gather = 1;
     c.NB = H.NB;
     c.NC = H.NC;
-    c.lam_lo = d_lam_lo;
-    c.lam_hi = d_lam_hi;
+    c.lam_lo = d_lam_lo + own0;
+    c.lam_hi = d_lam_hi + own0;
     c.cglob = d_cglob;
     c.u1b = d_u1b;
     c.cpl_b = d_cpl_b;
     c.z = d_z;
     launch(FETIGPU_K_ORTHO, [&] { k_cgs_pass<8><<<mdot_blocks, 256, sm, stream>>>(c); });
+    allreduce(h1, nv + 1);
     mark(5);
-    // pass 2: w -= V h1, h2 = V^H w, |w|^2; last block runs the Givens step
+    // pass 2: w -= V h1, h2 = V^H w, |w|^2; last block runs the Givens step (one GPU)
     c.gather = 0;
     c.h_in = h1;
     c.out = h2;
-    c.givens = 1;
+    c.givens = dist() ? 0 : 1;
     c.ga = GivensArgs{d_gst, h1, h2, d_R, d_gcos, d_gsin, d_gvec, in_graph ? 1 : 0, arnoldi_handle};
     launch(FETIGPU_K_ORTHO, [&] { k_cgs_pass<8><<<mdot_blocks, 256, sm, stream>>>(c); });
+    if (dist()) {  // sharded: global dots first, then the (replicated) Givens step
+      allreduce(h2, nv + 1);
+      launch(FETIGPU_K_ORTHO, [&] { k_givens<<<1, 32, 0, stream>>>(c.ga); });
+    }
     mark(6);
     // V_{j+1} = (w - V h2) / h_{j+1,j}
     launch(FETIGPU_K_ORTHO, [&] {
-      k_update_normalize<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_gst, h2, d_w, d_V, ldv);
+      k_update_normalize<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_gst, h2, d_w + own0, d_V + own0, ldv);
     });
   }
   size_t cgs_smem() const { return sizeof(double2) * std::max(mdot_chunk, 640); }
@@ -862,12 +957,12 @@ struct Ctx {
     const double tol = desc.tol;
     const int max_iter = desc.max_iter;
     zero(x, nl);
-    const double bnorm = norm_max(b, nl).first;
+    const double bnorm = norm_max(b + own0, nown, true).first;
     if (bnorm == 0.0) {
       st.converged = 1;
       return st;
     }
-    const bool graph = use_graph && !prof;
+    const bool graph = use_graph && !prof && !dist();
     if (graph && !arnoldi_exec) build_arnoldi_graph();
     CU(cudaMemcpyAsync(d_r, b, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
     double best_res = 1.0;  // |b - F 0| / |b|
@@ -876,7 +971,7 @@ struct Ctx {
     double relres = 0;
     bool first = true;
     while (true) {
-      const double rnorm = first ? bnorm : norm_max(d_r, nl).first;
+      const double rnorm = first ? bnorm : norm_max(d_r + own0, nown, true).first;
       first = false;
       relres = rnorm / bnorm;
       if (relres < best_res) {
@@ -890,6 +985,7 @@ struct Ctx {
       if (iterations >= max_iter) break;
       // new cycle: V_0 = r / |r|, g = |r| e_0
       launch(FETIGPU_K_ORTHO, [&] { k_scale_copy<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, 1.0 / rnorm, d_V); });
+      ghost_refresh(d_V);
       *h_gst = GmresState{};
       h_gst->j = 0;
       h_gst->iterations = iterations;
@@ -929,17 +1025,22 @@ struct Ctx {
           arnoldi_step(false);
           CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
           sync();
+          if (h_gst->cont) ghost_refresh(d_V + (size_t)h_gst->j * ldv);  // sharded: next basis column
         } while (h_gst->cont);
       }
       if (h_gst->status) throw NumericalError("gmres: breakdown (NaN/Inf in Arnoldi)");
       iterations = h_gst->iterations;
       // back substitution and x += P^-1 (Q y)  (krylov.hpp:191-209), true residual r = b - F x
       launch(FETIGPU_K_ORTHO, [&] { k_backsub<<<1, 32, 0, stream>>>(d_gst, d_R, d_gvec, d_y); });
-      launch(FETIGPU_K_ORTHO, [&] { k_combine<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_V, ldv, d_gst, d_y, d_t); });
+      launch(FETIGPU_K_ORTHO, [&] {
+        k_combine<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_V + own0, ldv, d_gst, d_y, d_t + own0);
+      });
       apply_precond(d_t, d_zl);
-      launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nl, 256), 256, 0, stream>>>(nl, x, d_zl); });
+      launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nown, 256), 256, 0, stream>>>(nown, x + own0, d_zl + own0); });
       apply_dual(x, d_w);
-      launch(FETIGPU_K_ORTHO, [&] { k_sub<<<cdiv(nl, 256), 256, 0, stream>>>(nl, b, d_w, d_r); });
+      launch(FETIGPU_K_ORTHO, [&] {
+        k_sub<<<cdiv(nown, 256), 256, 0, stream>>>(nown, b + own0, d_w + own0, d_r + own0);
+      });
     }
     // krylov.hpp:214-220: the final residual equals the last cycle's r; best-iterate fallback
     if (relres > best_res) {
@@ -975,8 +1076,11 @@ struct Ctx {
     if (nc > 0)
       launch(FETIGPU_K_OTHER, [&] { k_gather_corner<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_dof, rhs, d_fc); });
     eliminate_boundary(d_fi, d_fb, d_fc, true);
-    launch(FETIGPU_K_LAMBDA, [&] { k_jump<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_lam_lo, d_lam_hi, d_u1b, d_d); });
+    launch(FETIGPU_K_LAMBDA, [&] {
+      k_jump<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_lam_lo + own0, d_lam_hi + own0, d_u1b, d_d + own0);
+    });
     const fetigpu_feti_stats gst = gmres(d_d, d_lam);
+    ghost_refresh(d_lam);
     st.iterations = gst.iterations;
     st.converged = gst.converged;
     st.relative_residual = gst.relative_residual;
@@ -988,8 +1092,18 @@ struct Ctx {
     launch(FETIGPU_K_OTHER, [&] {
       k_assemble_x<<<cdiv(n, 256), 256, 0, stream>>>(n, d_xkind, d_xa, d_xb, d_ri, d_u1b, d_z, x);
     });
-    launch(FETIGPU_K_LAMBDA, [&] { k_jump<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_lam_lo, d_lam_hi, d_u1b, d_d); });
-    st.interface_jump = nl > 0 ? norm_max(d_d, nl).second : 0.0;
+    if (dist()) {  // every rank assembled its own rows of x: replicate the whole vector
+      std::vector<size_t> first(plan.world), count(plan.world);
+      for (int q = 0; q < plan.world; ++q) {
+        first[q] = 2 * (size_t)plan.free_first_all[q];
+        count[q] = 2 * (size_t)plan.free_count_all[q];
+      }
+      comm->allgatherv(reinterpret_cast<double*>(x), first, count, stream);
+    }
+    launch(FETIGPU_K_LAMBDA, [&] {
+      k_jump<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_lam_lo + own0, d_lam_hi + own0, d_u1b, d_d + own0);
+    });
+    st.interface_jump = H.n_lambda > 0 ? norm_max(d_d + own0, nown, true).second : 0.0;
     apply_global<double2>(x, nullptr, 1.0, mc, d_ax);
     launch(FETIGPU_K_GLOBAL, [&] { k_sub<<<cdiv(n, 256), 256, 0, stream>>>(n, d_ax, rhs, d_ax); });
     st.primal_residual = norm_max(d_ax, n).first / rn;
@@ -1161,6 +1275,101 @@ int fetigpu_create(const fetigpu_desc* desc, fetigpu_ctx** out) {
 }
 
 void fetigpu_destroy(fetigpu_ctx* ctx) { delete ctx; }
+
+// ---- sharded path ----------------------------------------------------
+static std::unique_ptr<Ctx> make_ctx(const fetigpu_desc* desc) {
+  validate_desc(desc);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw RuntimeError("fetigpu: no CUDA device");
+  if (desc->device < 0 || desc->device >= ndev) throw ContractError("fetigpu: bad device ordinal");
+  auto c = std::make_unique<Ctx>();
+  c->desc = *desc;
+  c->P = build_problem(*desc);
+  if (desc->phi > 0.0) {
+    c->phi = desc->phi;
+    c->mc = cd(0.0, -1.0 / std::sqrt(desc->phi));
+  } else {
+    c->mc = cd(desc->mass_coeff_re, desc->mass_coeff_im);
+  }
+  return c;
+}
+
+int fetigpu_nccl_unique_id(unsigned char* out128) {
+  return guard([&] { nccl_unique_id(out128); });
+}
+
+int fetigpu_create_sharded(const fetigpu_desc* desc, int rank, int world, const unsigned char* nccl_id,
+                           fetigpu_ctx** out) {
+  return guard([&] {
+    if (!nccl_id) throw ContractError("fetigpu_create_sharded: nccl_id required");
+    auto c = make_ctx(desc);
+    const HostPartition G = build_partition(c->P, desc->s_x, desc->s_y);
+    c->H = build_rank_partition(G, rank, world, c->plan);
+    c->comm = make_nccl_comm(nccl_id, rank, world, desc->device);
+    c->setup();
+    auto* h = new fetigpu_ctx;
+    h->c = std::move(c);
+    *out = h;
+  });
+}
+
+int fetigpu_rank_info(const fetigpu_desc* desc, int rank, int world, int* info) {
+  return guard([&] {
+    validate_desc(desc);
+    const HostProblem P = build_problem(*desc);
+    const HostPartition G = build_partition(P, desc->s_x, desc->s_y);
+    RankPlan pl;
+    const HostPartition L = build_rank_partition(G, rank, world, pl);
+    const int v[12] = {pl.sub_first, pl.n_sub_local, pl.n_phantom, pl.lam_base, pl.n_ghost, pl.n_owned,
+                       pl.n_top_cut, pl.free_first, pl.free_count, (int)pl.to_up.send_slots.size(),
+                       (int)pl.to_down.send_slots.size(), L.n_lambda};
+    std::copy(v, v + 12, info);
+  });
+}
+
+int fetigpu_emulated_schur_solve(const fetigpu_desc* desc, int world, const double* ybar, const double* yc,
+                                 double* y, double* u, double* lambda, fetigpu_schur_stats* stats) {
+  return guard([&] {
+    if (world < 1) throw ContractError("fetigpu_emulated_schur_solve: world must be >= 1");
+    auto group = std::make_shared<ThreadGroup>(world);
+    std::vector<std::string> errs(world);
+    std::vector<std::thread> th;
+    for (int q = 0; q < world; ++q)
+      th.emplace_back([&, q] {
+        try {
+          auto c = make_ctx(desc);
+          const HostPartition G = build_partition(c->P, desc->s_x, desc->s_y);
+          c->H = build_rank_partition(G, q, world, c->plan);
+          c->comm = std::make_unique<ThreadComm>(group, q);
+          c->setup();
+          if (!(c->phi > 0.0)) throw ContractError("build_complex_factors: phi must be positive");
+          const size_t nb = sizeof(double) * c->n;
+          CU(cudaMemcpyAsync(c->d_in_ybar, ybar, nb, cudaMemcpyHostToDevice, c->stream));
+          const double* dyc = nullptr;
+          if (yc && c->m > 0) {
+            CU(cudaMemcpyAsync(c->d_in_yc, yc, sizeof(double) * c->m, cudaMemcpyHostToDevice, c->stream));
+            dyc = c->d_in_yc;
+          }
+          fetigpu_schur_stats st{};
+          c->schur_solve(c->d_in_ybar, dyc, c->d_out_y, c->d_out_u, c->d_out_l, &st);
+          if (q == 0) {
+            CU(cudaMemcpyAsync(y, c->d_out_y, nb, cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaMemcpyAsync(u, c->d_out_u, nb, cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaMemcpyAsync(lambda, c->d_out_l, nb, cudaMemcpyDeviceToHost, c->stream));
+            c->sync();
+            if (stats) *stats = st;
+          }
+          group->barrier();  // keep every rank's buffers alive until rank 0 has copied
+        } catch (const std::exception& e) {
+          errs[q] = e.what();
+          group->abort();
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int q = 0; q < world; ++q)
+      if (!errs[q].empty() && errs[q] != "rank group aborted") throw RuntimeError("rank " + std::to_string(q) + ": " + errs[q]);
+  });
+}
 
 int fetigpu_schur_solve_device(fetigpu_ctx* ctx, const double* d_ybar, const double* d_yc, double* d_y, double* d_u,
                                double* d_lambda, fetigpu_schur_stats* stats) {

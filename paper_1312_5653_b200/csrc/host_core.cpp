@@ -344,7 +344,149 @@ HostPartition build_partition(const HostProblem& P, int sx, int sy) {
   }
   for (int f = 0; f < H.n_free; ++f)
     if (H.xkind[f] < 0) throw NumericalError("partition: free dof owned by no subdomain");
+  H.free_row.resize(H.n_free);
+  for (int f = 0; f < H.n_free; ++f) H.free_row[f] = (P.free_dofs[f] / dpn) / (P.nx + 1);
   return H;
+}
+
+HostPartition build_rank_partition(const HostPartition& G, int rank, int world, RankPlan& plan) {
+  if (world < 1 || rank < 0 || rank >= world) throw ContractError("rank partition: bad rank/world");
+  if (G.sy % world != 0) throw ContractError("rank partition: subdomain rows must divide evenly over the ranks");
+  const int sx = G.sx, rows = G.sy / world, NB = G.NB, NC = G.NC;
+  plan = RankPlan{};
+  plan.rank = rank;
+  plan.world = world;
+  plan.sub_first = rank * rows * sx;
+  plan.n_sub_local = rows * sx;
+  const int S = plan.n_sub_local, s0 = plan.sub_first;
+  // phantoms: the lower neighbour row, then the upper one
+  if (rank > 0)
+    for (int p = 0; p < sx; ++p) plan.phantom_global.push_back(s0 - sx + p);
+  if (rank < world - 1)
+    for (int p = 0; p < sx; ++p) plan.phantom_global.push_back(s0 + S + p);
+  plan.n_phantom = (int)plan.phantom_global.size();
+  auto local_sub = [&](int sg) -> int {
+    if (sg >= s0 && sg < s0 + S) return sg - s0;
+    for (int p = 0; p < plan.n_phantom; ++p)
+      if (plan.phantom_global[p] == sg) return S + p;
+    return -1;
+  };
+  auto local_slot = [&](int gslot) -> int {
+    const int ls = local_sub(gslot / NB);
+    return ls < 0 ? -1 : ls * NB + gslot % NB;
+  };
+  auto is_local = [&](int gslot) { const int sg = gslot / NB; return sg >= s0 && sg < s0 + S; };
+  // multiplier ranges: ghosts (bottom cut) then owned, contiguous in the global numbering
+  int gmin = G.n_lambda, gmax = -1, omin = G.n_lambda, omax = -1;
+  for (int r = 0; r < G.n_lambda; ++r) {
+    if (is_local(G.lam_lo[r])) omin = std::min(omin, r), omax = std::max(omax, r), ++plan.n_owned;
+    else if (is_local(G.lam_hi[r])) gmin = std::min(gmin, r), gmax = std::max(gmax, r), ++plan.n_ghost;
+  }
+  if (plan.n_owned > 0 && omax - omin + 1 != plan.n_owned) throw NumericalError("rank partition: owned rows not contiguous");
+  if (plan.n_ghost > 0 && (gmax - gmin + 1 != plan.n_ghost || gmax + 1 != omin))
+    throw NumericalError("rank partition: ghost rows not contiguous with the owned block");
+  plan.lam_base = plan.n_ghost > 0 ? gmin : (plan.n_owned > 0 ? omin : 0);
+  const int NL = plan.n_ghost + plan.n_owned;
+
+  HostPartition L = G;  // copies scalars; per-subdomain arrays rebuilt below
+  L.n_sub = S;
+  L.n_lambda = NL;
+  auto slice = [&](const auto& v, int width) {
+    using T = typename std::decay_t<decltype(v)>::value_type;
+    return std::vector<T>(v.begin() + (size_t)s0 * width, v.begin() + (size_t)(s0 + S) * width);
+  };
+  L.ldof = slice(G.ldof, G.nld);
+  L.idof = slice(G.idof, G.NI);
+  L.bdof = slice(G.bdof, NB);
+  L.bsign = slice(G.bsign, NB);
+  L.n_i = slice(G.n_i, 1);
+  L.n_b = slice(G.n_b, 1);
+  L.n_c = slice(G.n_c, 1);
+  L.sub_i0 = slice(G.sub_i0, 1);
+  L.sub_j0 = slice(G.sub_j0, 1);
+  L.blam = slice(G.blam, NB);
+  for (int& r : L.blam)
+    if (r >= 0) {
+      r -= plan.lam_base;
+      if (r < 0 || r >= NL) throw NumericalError("rank partition: interface dof outside the local multiplier range");
+    }
+  L.cglob.assign((size_t)(S + plan.n_phantom) * NC, -1);
+  for (int ls = 0; ls < S + plan.n_phantom; ++ls) {
+    const int sg = ls < S ? s0 + ls : plan.phantom_global[ls - S];
+    for (int c = 0; c < NC; ++c) L.cglob[(size_t)ls * NC + c] = G.cglob[(size_t)sg * NC + c];
+  }
+  L.lam_lo.assign(NL, -1);
+  L.lam_hi.assign(NL, -1);
+  for (int r = 0; r < NL; ++r) {
+    const int gr = plan.lam_base + r;
+    L.lam_lo[r] = local_slot(G.lam_lo[gr]);
+    L.lam_hi[r] = local_slot(G.lam_hi[gr]);
+    if (L.lam_lo[r] < 0 || L.lam_hi[r] < 0) throw NumericalError("rank partition: multiplier owner outside the halo");
+  }
+  L.corner_slots.assign(G.corner_slots.size(), -1);  // local subdomains only (partial coarse sums)
+  for (size_t q = 0; q < G.corner_slots.size(); ++q) {
+    const int gs = G.corner_slots[q];
+    if (gs >= 0 && (gs / NC) >= s0 && (gs / NC) < s0 + S) L.corner_slots[q] = (gs / NC - s0) * NC + gs % NC;
+  }
+  // top-cut rows: owned rows whose hi owner is an (upper) phantom
+  for (int r = plan.n_ghost; r < NL; ++r)
+    if (L.lam_hi[r] >= S * NB) ++plan.n_top_cut;
+  for (int r = NL - plan.n_top_cut; r < NL; ++r)
+    if (L.lam_hi[r] < S * NB) throw NumericalError("rank partition: top-cut rows not at the end of the owned block");
+  // slot exchanges (canonical order = multiplier id)
+  if (rank < world - 1) {
+    plan.to_up.peer = rank + 1;
+    for (int r = NL - plan.n_top_cut; r < NL; ++r) {
+      plan.to_up.send_slots.push_back(L.lam_lo[r]);  // my side of the top cut
+      plan.to_up.recv_slots.push_back(L.lam_hi[r]);  // the upper neighbour's side (phantom)
+    }
+  }
+  if (rank > 0) {
+    plan.to_down.peer = rank - 1;
+    for (int r = 0; r < plan.n_ghost; ++r) {
+      plan.to_down.send_slots.push_back(L.lam_hi[r]);  // my side of the bottom cut
+      plan.to_down.recv_slots.push_back(L.lam_lo[r]);  // the lower neighbour's side (phantom)
+    }
+  }
+  // owned free dofs: node rows (j0, j1] of this rank's band (contiguous in free-dof order)
+  const int ey = G.ey;
+  auto owned_range = [&](int rr, int& first, int& count) {
+    const int j0 = rr * rows * ey, j1 = (rr + 1) * rows * ey;
+    first = -1;
+    count = 0;
+    for (int f = 0; f < G.n_free; ++f) {
+      const int j = G.free_row[f];
+      const bool mine = (rr == 0 ? j >= 0 : j > j0) && j <= j1;
+      if (mine) {
+        if (first < 0) first = f;
+        ++count;
+      }
+    }
+    if (first < 0) first = 0;
+  };
+  plan.free_first_all.resize(world);
+  plan.free_count_all.resize(world);
+  for (int rr = 0; rr < world; ++rr) owned_range(rr, plan.free_first_all[rr], plan.free_count_all[rr]);
+  plan.free_first = plan.free_first_all[rank];
+  plan.free_count = plan.free_count_all[rank];
+  L.xkind.assign(G.n_free, -1);
+  L.xa.assign(G.n_free, -1);
+  L.xb.assign(G.n_free, -1);
+  for (int f = plan.free_first; f < plan.free_first + plan.free_count; ++f) {
+    const int kind = G.xkind[f];
+    L.xkind[f] = kind;
+    if (kind == 0) {
+      L.xa[f] = (G.xa[f] / G.NI - s0) * G.NI + G.xa[f] % G.NI;
+      if (G.xa[f] / G.NI < s0 || G.xa[f] / G.NI >= s0 + S) throw NumericalError("rank partition: interior dof not local");
+    } else if (kind == 1) {
+      L.xa[f] = local_slot(G.xa[f]);
+      L.xb[f] = local_slot(G.xb[f]);
+      if (L.xa[f] < 0 || L.xb[f] < 0) throw NumericalError("rank partition: interface dof owner outside the halo");
+    } else {
+      L.xa[f] = G.xa[f];  // corner id (z is replicated)
+    }
+  }
+  return L;
 }
 
 namespace {

@@ -67,12 +67,43 @@ struct HostPartition {
   std::vector<int> lam_lo, lam_hi;       // [n_lambda] flat slot s*NB+k of the +1 / -1 owner
   std::vector<int> corner_slots;         // [n_corner][4] flat slot s*NC+k, ascending s, -1 pad
   std::vector<int> xkind, xa, xb;        // [n_free] primal assembly map (0 int, 1 bnd, 2 corner)
+  std::vector<int> free_row;             // [n_free] mesh node row j of each free dof
   // element-local structure: sub origin (node) for subdomain s
   std::vector<int> sub_i0, sub_j0;
 };
 
 HostProblem build_problem(const fetigpu_desc& d);
 HostPartition build_partition(const HostProblem& P, int sx, int sy);
+
+// ---------------------------------------------------------------------------------------
+// Multi-GPU sharding.  Rank r of R owns the subdomain rows
+// [r sy/R, (r+1) sy/R) (contiguous subdomain ids).  Its local view is a HostPartition over
+// the local subdomains whose slot space is extended by "phantom" subdomains (the
+// neighbour rows across each cut line), so every slot-indexed gather of the single-GPU
+// kernels works unchanged.  Multipliers are numbered locally as
+//   [ghost rows of the bottom cut (owned by r-1)] [owned rows, incl. the top cut]
+// which is a contiguous range of the global numbering (multipliers ascend by node id).
+struct SlotExchange {  // one direction of a neighbour exchange of per-dof slot values
+  int peer = -1;
+  std::vector<int> send_slots;  // local slots packed in canonical (multiplier id) order
+  std::vector<int> recv_slots;  // phantom slots unpacked in the same order
+};
+struct RankPlan {
+  int rank = 0, world = 1;
+  int sub_first = 0, n_sub_local = 0, n_phantom = 0;
+  int lam_base = 0;     // global id of local multiplier 0
+  int n_ghost = 0;      // ghost rows [0, n_ghost) (bottom cut)
+  int n_owned = 0;      // owned rows [n_ghost, n_ghost + n_owned)
+  int n_top_cut = 0;    // last n_top_cut owned rows sit on the top cut (sent up as ghosts)
+  int free_first = 0, free_count = 0;  // owned free dofs (x assembly)
+  std::vector<int> free_first_all, free_count_all;  // per rank (all-gather of x)
+  SlotExchange to_up, to_down;  // slot values sent to rank r+1 / r-1
+  std::vector<int> phantom_global;  // global subdomain id of each phantom
+};
+
+// Local view for rank `rank` of `world` and its exchange plan (throws ContractError when
+// the subdomain rows do not divide evenly).
+HostPartition build_rank_partition(const HostPartition& G, int rank, int world, RankPlan& plan);
 
 void target_thermal(const HostProblem& P, double* ybar, double* yc);
 void target_sine(const HostProblem& P, uint64_t seed, int modes, int mmax, double* ybar);

@@ -19,9 +19,14 @@ namespace fetigpu {
 constexpr int MAX_EDOFS = 8;
 constexpr int MAXE = 24;  // ELL capacity checked on the host
 
-__constant__ double2 c_Ae[MAX_EDOFS * MAX_EDOFS];  // Ae = kc*Ke + mc*Me (feti.cpp:264-265)
-__constant__ double c_Ke[MAX_EDOFS * MAX_EDOFS];
-__constant__ double c_Me[MAX_EDOFS * MAX_EDOFS];
+// Element matrices travel by value in the kernel parameter space (constant bank), so
+// several contexts (different meshes / phi, or emulated ranks) can coexist in a process.
+struct ElemAe {
+  double2 v[MAX_EDOFS * MAX_EDOFS];  // Ae = kc*Ke + mc*Me (feti.cpp:264-265)
+};
+struct ElemKM {
+  double k[MAX_EDOFS * MAX_EDOFS], m[MAX_EDOFS * MAX_EDOFS];
+};
 
 struct SubLayout {
   int S, nld, ex, ey, dpn, NI, NB, NC, W, EBI, EIB;
@@ -31,7 +36,7 @@ struct SubLayout {
 // One thread per (subdomain, local mesh dof a).  The thread owns row a of every block it
 // belongs to, visits the <= 4 elements around its node in ascending element id (the
 // reference's sub.elements order, feti.cpp:305) and accumulates deterministically.
-__global__ void k_assemble(SubLayout L, const int* __restrict__ ldof, double2* __restrict__ colband,
+__global__ void k_assemble(SubLayout L, ElemAe Ae, const int* __restrict__ ldof, double2* __restrict__ colband,
                            int* __restrict__ bi_idx, double2* __restrict__ bi_val, int* __restrict__ ib_idx,
                            double2* __restrict__ ib_val, double2* __restrict__ Sbb, double2* __restrict__ Aic,
                            double2* __restrict__ Abc, double2* __restrict__ Acc) {
@@ -63,7 +68,7 @@ __global__ void k_assemble(SubLayout L, const int* __restrict__ ldof, double2* _
           const int code_b = code[en[b] * dpn + cb];
           const int cat_b = code_b >> 24, ib = code_b & 0xFFFFFF;
           if (cat_b == 0) continue;
-          const double2 v = c_Ae[ra * ed + dpn * b + cb];
+          const double2 v = Ae.v[ra * ed + dpn * b + cb];
           if (cat_a == 2) {  // interior row
             if (cat_b == 2) {
               if (ib <= ia) {
@@ -389,6 +394,24 @@ __global__ void __launch_bounds__(WARPS * 32)
 // rotated by one lane per step (no per-row reductions).  Bytes per subdomain:
 // NT*17*512 + NT(NT-1)/2*16384 (133 KB at NB = 124 vs 246 KB dense).
 __host__ __device__ constexpr int sym_tile_entries(int NT) { return NT * 17 * 32 + NT * (NT - 1) / 2 * 1024; }
+
+// ---- sharded path: cut-line halo of per-dof slot values -------------
+// buf[i * width + c] = val[slots[i] * width + c]
+__global__ void k_pack_slots(int n, int width, const int* __restrict__ slots, const double2* __restrict__ val,
+                             double2* __restrict__ buf) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * width) return;
+  const int i = t / width, c = t % width;
+  buf[t] = val[(size_t)slots[i] * width + c];
+}
+// val[slots[i] * width + c] = buf[i * width + c]
+__global__ void k_unpack_slots(int n, int width, const int* __restrict__ slots, const double2* __restrict__ buf,
+                               double2* __restrict__ val) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * width) return;
+  const int i = t / width, c = t % width;
+  val[(size_t)slots[i] * width + c] = buf[t];
+}
 
 // pack[s] <- full[s] (row-major NB x NB); entries outside NB are zero
 __global__ void k_pack_sym(int S, int NB, int NT, const double2* __restrict__ full, double2* __restrict__ pack) {
@@ -967,6 +990,7 @@ __global__ void k_assemble_x(int n, const int* __restrict__ kind, const int* __r
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= n) return;
   const int k = kind[f];
+  if (k < 0) return;  // owned by another rank (sharded path)
   double2 v;
   if (k == 0)
     v = ui[xa[f]];
@@ -1311,7 +1335,7 @@ __device__ __forceinline__ void store_c<double2>(double2* p, double2 v) {
   *p = v;
 }
 template <typename T>
-__global__ void k_apply_global(MeshLayout M, int n, const int* __restrict__ free_dofs, const int* __restrict__ free_map,
+__global__ void k_apply_global(MeshLayout M, ElemKM KM, int n, const int* __restrict__ free_dofs, const int* __restrict__ free_map,
                                const int* __restrict__ cons_map, const T* __restrict__ x, const double* __restrict__ xc,
                                double2 kc, double2 mc, T* __restrict__ y) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1334,7 +1358,7 @@ __global__ void k_apply_global(MeshLayout M, int n, const int* __restrict__ free
       for (int b = 0; b < 4; ++b)
         for (int cb = 0; cb < dpn; ++cb) {
           const int mdb = en[b] * dpn + cb;
-          const double kv = c_Ke[ra * ed + dpn * b + cb], mv = c_Me[ra * ed + dpn * b + cb];
+          const double kv = KM.k[ra * ed + dpn * b + cb], mv = KM.m[ra * ed + dpn * b + cb];
           const int fb = free_map[mdb];
           if (fb >= 0) {
             const double2 xv = as_c<T>(x[fb]);

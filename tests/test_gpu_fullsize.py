@@ -60,15 +60,19 @@ def test_config2_matches_oracle(fetigpu, oracle_mod):
 
 # calibrated on the oracle at 1024^2, seed 1 (the GPU reproduces the same values):
 # 1.83e-4 at phi = 1e-2, 6.1e-8 at phi = 1e-8 (K -/+ i beta V conditioning at FETI tol 1e-10)
-SCHUR_RES_BOUND = {1e-2: 1e-3, 1e-4: 1e-6, 1e-6: 5e-7, 1e-8: 5e-7}
+# and on the oracle at 2048^2, 64x64, phi = 1e-6, seed 0: 1.216e-4, 26 / 26 iterations
+# (orc_schur run for 166 s on 16 cores; the bound grows with the mesh, h^-2 conditioning)
+SCHUR_RES_BOUND = {(1024, 1e-2): 1e-3, (1024, 1e-8): 5e-7, (2048, 1e-6): 5e-4}
+CONFIG3_ORACLE_ITERS = 26
 
 
 def check_kkt(out, ybar, phi, n):
     K, V = q1_operators(n)
     r1 = K @ out["y"] - V @ out["u"]
     r2 = V @ (out["y"] - ybar) + K @ out["lambda"]
-    assert np.linalg.norm(r1) <= SCHUR_RES_BOUND[phi] * np.linalg.norm(K @ ybar)
-    assert np.linalg.norm(r2) <= 1e-12 * np.linalg.norm(K @ out["lambda"])
+    assert np.linalg.norm(r1) <= SCHUR_RES_BOUND[(n, phi)] * np.linalg.norm(K @ ybar)
+    # r2 vanishes by construction (primal recovery); bound it by the rounding scale |K||lambda|
+    assert np.linalg.norm(r2) <= 1e-12 * np.linalg.norm(abs(K) @ abs(out["lambda"]))
     assert np.allclose(out["u"] * phi, out["lambda"], rtol=1e-14, atol=0)
 
 
@@ -95,4 +99,5 @@ def test_config3_kkt_residuals_and_determinism(fetigpu):
     for k in ("y", "u", "lambda"):
         assert np.array_equal(a[k], b[k])
     check_kkt(a, p.target_state, phi, n)
-    assert abs(a["plus_stats"]["iterations"] - a["minus_stats"]["iterations"]) <= 2
+    assert abs(a["plus_stats"]["iterations"] - CONFIG3_ORACLE_ITERS) <= 2
+    assert abs(a["minus_stats"]["iterations"] - CONFIG3_ORACLE_ITERS) <= 2

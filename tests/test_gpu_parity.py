@@ -163,3 +163,24 @@ def test_graph_and_eager_gmres_identical(fetigpu):
     for k in ("y", "u", "lambda"):
         assert np.array_equal(a[k], b[k])
     assert a["plus_stats"]["iterations"] == b["plus_stats"]["iterations"]
+
+
+@pytest.mark.parametrize("n,s", [(80, 2), (136, 34)])
+def test_wide_bands_match_oracle(fetigpu, oracle_mod, n, s):
+    """Half-bandwidths above one warp (NS = 2 register window): A_ii with W = 39 (80^2, 2x2)
+    and the coarse matrix with W = 34 (136^2, 34x34 subdomains)."""
+    phi = 1e-6
+    p = fetigpu.make_seeded_problem(n, phi, seed=4)
+    c = -1j / np.sqrt(phi)
+    gpu = fetigpu.SchurSolver(p, s, s, tol=1e-10, max_iter=2000)
+    ref = oracle_mod.Feti(oracle_mod.Problem(n), s, s, c, tol=1e-10, max_iter=2000)
+    rng = np.random.default_rng(11)
+    lam = rng.uniform(-1, 1, ref.n_lambda) + 1j * rng.uniform(-1, 1, ref.n_lambda)
+    assert rel(gpu.apply_dual_operator(lam), ref.apply_dual_operator(lam)) <= 1e-12
+    assert rel(gpu.apply_dirichlet_preconditioner(lam), ref.apply_dirichlet_preconditioner(lam)) <= 1e-12
+    rhs = rng.uniform(-1, 1, p.n) + 0j
+    x, st = gpu.feti_solve(rhs)
+    xo, so = ref.solve(rhs)
+    assert rel(x, xo) <= 1e-8
+    assert abs(st["iterations"] - so["iterations"]) <= 2
+    gpu.close()
