@@ -123,6 +123,12 @@ struct Ctx {
   bool use_graph = true;
   bool debug_sync = false;
   bool sym_tma = false;
+  bool pdl = true;                      // FETIGPU_NO_PDL=1: plain stream serialisation
+  // FETIGPU_L2PF_KB / FETIGPU_L2PF_AT: per-subdomain bytes of the Dirichlet operator pulled
+  // into L2 by a latency-bound Arnoldi kernel (0 coarse GEMV, 1 CGS pass 1, 2 pass 2, 3 update)
+  unsigned int l2pf_bytes = 0;
+  int l2pf_at = 1;
+  bool arnoldi_phase = false;
   int sym_warps = 4;
   size_t l2_persist_bytes = 0;
   bool watchdog = false;
@@ -130,6 +136,7 @@ struct Ctx {
   cudaGraphExec_t arnoldi_exec = nullptr;
   cudaGraphConditionalHandle arnoldi_handle{};
   int arnoldi_body_kernels = 0;
+  static constexpr int kCgsThreads = 512, kCgsRows = 256;  // k_cgs_pass block shape
   int mdot_blocks = 0, mdot_chunk = 0;
   // mass solve (Kronecker tridiagonal)
   double *d_mx_cp = nullptr, *d_mx_dinv = nullptr, *d_my_cp = nullptr, *d_my_dinv = nullptr;
@@ -193,6 +200,21 @@ struct Ctx {
       CU(cudaStreamSynchronize(stream));
       std::fprintf(stderr, "[fetigpu] launch %lld class %d done\n", launches, klass);
     }
+  }
+  // kernel launch with programmatic dependent launch allowed (see pdl_wait in common.cuh)
+  template <typename... KArgs, typename... Args>
+  void kx(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CU(cudaLaunchKernelEx(&cfg, kern, args...));
   }
   void prof_collect() {
     if (!prof || pool_used == 0) return;
@@ -292,6 +314,9 @@ struct Ctx {
     if (const char* e = std::getenv("FETIGPU_DEBUG_SYNC")) debug_sync = e[0] == '1';
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FETIGPU_SYM_TMA")) sym_tma = e[0] == '1';
+    if (const char* e = std::getenv("FETIGPU_NO_PDL")) pdl = !(e[0] == '1');
+    if (const char* e = std::getenv("FETIGPU_L2PF_KB")) l2pf_bytes = 1024u * (unsigned)std::atoi(e);
+    if (const char* e = std::getenv("FETIGPU_L2PF_AT")) l2pf_at = std::atoi(e);
     if (const char* e = std::getenv("FETIGPU_SYM_WARPS")) sym_warps = std::atoi(e) == 8 ? 8 : 4;
     watchdog = std::getenv("FETIGPU_WATCHDOG") != nullptr;
     n = P.n();
@@ -505,8 +530,8 @@ struct Ctx {
     d_r = alloc<double2>(ldv);
     d_d = alloc<double2>(ldv);
     d_best = alloc<double2>(ldv);
-    mdot_blocks = std::max(1, std::min(296, cdiv(nown, 64)));
-    mdot_chunk = cdiv(std::max(nown, 1), mdot_blocks);
+    mdot_blocks = std::max(1, cdiv(nown, kCgsRows));
+    mdot_chunk = kCgsRows;
     d_part = alloc<double2>((size_t)(vcap + 2) * mdot_blocks);
     d_red = alloc<double2>(3 * (vcap + 2));
     d_y = alloc<double2>(vcap + 2);
@@ -535,10 +560,6 @@ struct Ctx {
     d_out_u = alloc<double>(n);
     d_out_l = alloc<double>(n);
     CU(cudaMallocHost(&h_pin, sizeof(double2) * 3 * (vcap + 4)));
-    // coarse gemv may need > 48 KB of dynamic smem
-    CU(cudaFuncSetAttribute(k_coarse_gemv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)std::max<size_t>(nc * sizeof(double2), 1)));
-    CU(cudaFuncSetAttribute(k_cgs_pass<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cgs_smem()));
     setup_mass();
     setup_l2_persistence();
     sync();
@@ -697,15 +718,15 @@ struct Ctx {
       const size_t sm = sym_smem();
       if (sym_warps == 4) {
         switch (g.mode) {
-          case 0: k_sym_gemv<0, 8, 4><<<H.n_sub, 128, sm, stream>>>(g); break;
-          case 1: k_sym_gemv<1, 8, 4><<<H.n_sub, 128, sm, stream>>>(g); break;
-          default: k_sym_gemv<2, 8, 4><<<H.n_sub, 128, sm, stream>>>(g); break;
+          case 0: kx(k_sym_gemv<0, 8, 4>, H.n_sub, 128, sm, g); break;
+          case 1: kx(k_sym_gemv<1, 8, 4>, H.n_sub, 128, sm, g); break;
+          default: kx(k_sym_gemv<2, 8, 4>, H.n_sub, 128, sm, g); break;
         }
       } else {
         switch (g.mode) {
-          case 0: k_sym_gemv<0, 8, 8><<<H.n_sub, 256, sm, stream>>>(g); break;
-          case 1: k_sym_gemv<1, 8, 8><<<H.n_sub, 256, sm, stream>>>(g); break;
-          default: k_sym_gemv<2, 8, 8><<<H.n_sub, 256, sm, stream>>>(g); break;
+          case 0: kx(k_sym_gemv<0, 8, 8>, H.n_sub, 256, sm, g); break;
+          case 1: kx(k_sym_gemv<1, 8, 8>, H.n_sub, 256, sm, g); break;
+          default: kx(k_sym_gemv<2, 8, 8>, H.n_sub, 256, sm, g); break;
         }
       }
       return;
@@ -722,6 +743,17 @@ struct Ctx {
   size_t sym_smem() const {
     const int noff = NT * (NT - 1) / 2;
     return sizeof(double2) * 32 * (NT + (noff + NT) + noff);
+  }
+  // slices of the Dirichlet operator (the next precond GEMV's input stream) for kernel `at`
+  L2Prefetch l2pf(int at) const {
+    L2Prefetch p{};
+    if (l2pf_bytes == 0 || at != l2pf_at || prof) return p;
+    const size_t per = sizeof(double2) * sym_tile_entries(NT);
+    p.base = reinterpret_cast<const char*>(d_Sbb_p);
+    p.stride = per;
+    p.bytes = (unsigned int)std::min<size_t>(l2pf_bytes, per) & ~15u;
+    p.count = H.n_sub;
+    return p;
   }
   SymGemvArgs sym_args(const double2* pack) const {
     SymGemvArgs g{};
@@ -759,7 +791,7 @@ struct Ctx {
   void coarse_gemv() {
     if (nc == 0) return;
     launch(FETIGPU_K_COARSE, [&] {
-      k_coarse_gemv<8><<<cdiv(nc, 8), 256, nc * sizeof(double2), stream>>>(nc, d_Cinv, d_g, d_z);
+      kx(k_coarse_gemv<256>, nc, 256, 0, nc, (const double2*)d_Cinv, (const double2*)d_g, d_z, l2pf(arnoldi_phase ? 0 : -1));
     });
   }
   // u_b = u1_b - cpl_b z gathered onto the owned multiplier rows: out = -B u  (feti.cpp:593)
@@ -881,7 +913,9 @@ struct Ctx {
       dual_gemv(g);
     }
     mark(3);
+    arnoldi_phase = true;
     coarse_gemv();
+    arnoldi_phase = false;
     slot_exchange(d_u1b, 1);  // sharded: the other side of the owned cut rows
     mark(4);
     CgsArgs c{};
@@ -893,12 +927,12 @@ struct Ctx {
     c.w = d_w + own0;
     c.part = d_part;
     c.counter = d_counter;
-    const size_t sm = cgs_smem();
     const int nv = dist() ? h_gst->j + 1 : 0;  // sharded path is eager: j known on the host
     // pass 1: w = F z (dual tail gathered per chunk), h1 = V^H w, |w|^2
     c.mode = 0;
     c.out = h1;
     c.gather = 1;
+    c.pf = l2pf(1);
     c.NB = H.NB;
     c.NC = H.NC;
     c.lam_lo = d_lam_lo + own0;
@@ -907,16 +941,17 @@ struct Ctx {
     c.u1b = d_u1b;
     c.cpl_b = d_cpl_b;
     c.z = d_z;
-    launch(FETIGPU_K_ORTHO, [&] { k_cgs_pass<8><<<mdot_blocks, 256, sm, stream>>>(c); });
+    launch(FETIGPU_K_ORTHO, [&] { kx(k_cgs_pass<kCgsThreads, kCgsRows>, mdot_blocks, kCgsThreads, 0, c); });
     allreduce(h1, nv + 1);
     mark(5);
     // pass 2: w -= V h1, h2 = V^H w, |w|^2; last block runs the Givens step (one GPU)
     c.gather = 0;
+    c.pf = l2pf(2);
     c.h_in = h1;
     c.out = h2;
     c.givens = dist() ? 0 : 1;
     c.ga = GivensArgs{d_gst, h1, h2, d_R, d_gcos, d_gsin, d_gvec, in_graph ? 1 : 0, arnoldi_handle};
-    launch(FETIGPU_K_ORTHO, [&] { k_cgs_pass<8><<<mdot_blocks, 256, sm, stream>>>(c); });
+    launch(FETIGPU_K_ORTHO, [&] { kx(k_cgs_pass<kCgsThreads, kCgsRows>, mdot_blocks, kCgsThreads, 0, c); });
     if (dist()) {  // sharded: global dots first, then the (replicated) Givens step
       allreduce(h2, nv + 1);
       launch(FETIGPU_K_ORTHO, [&] { k_givens<<<1, 32, 0, stream>>>(c.ga); });
@@ -924,10 +959,10 @@ struct Ctx {
     mark(6);
     // V_{j+1} = (w - V h2) / h_{j+1,j}
     launch(FETIGPU_K_ORTHO, [&] {
-      k_update_normalize<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_gst, h2, d_w + own0, d_V + own0, ldv);
+      kx(k_update_normalize<64, 4>, cdiv(nown, 64), 256, 0, nown, (const GmresState*)d_gst, (const double2*)h2,
+         (const double2*)(d_w + own0), d_V + own0, ldv, l2pf(3));
     });
   }
-  size_t cgs_smem() const { return sizeof(double2) * std::max(mdot_chunk, 640); }
 
   void build_arnoldi_graph() {
     CU(cudaGraphCreate(&arnoldi_graph, 0));
@@ -1033,7 +1068,7 @@ struct Ctx {
       // back substitution and x += P^-1 (Q y)  (krylov.hpp:191-209), true residual r = b - F x
       launch(FETIGPU_K_ORTHO, [&] { k_backsub<<<1, 32, 0, stream>>>(d_gst, d_R, d_gvec, d_y); });
       launch(FETIGPU_K_ORTHO, [&] {
-        k_combine<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_V + own0, ldv, d_gst, d_y, d_t + own0);
+        k_combine<64, 4><<<cdiv(nown, 64), 256, 0, stream>>>(nown, d_V + own0, ldv, d_gst, d_y, d_t + own0);
       });
       apply_precond(d_t, d_zl);
       launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nown, 256), 256, 0, stream>>>(nown, x + own0, d_zl + own0); });

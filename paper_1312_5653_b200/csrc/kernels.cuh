@@ -483,6 +483,8 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(S
   double2 (*part_col)[32] = reinterpret_cast<double2 (*)[32]>(sg_sh + 32 * NT + 32 * ntiles);
   const int s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_trigger();
+  pdl_wait();
   // ---- input vector (B^T scatter) ----
   const double2* lam = a.lam;
   if (MODE == 0 && a.jsel != nullptr) lam += (size_t)(*a.jsel) * a.jstride;
@@ -811,21 +813,32 @@ __global__ void k_coarse_rhs(int nc, const int* __restrict__ corner_slots, const
   g[c] = acc;
 }
 
-// z = C^-1 g  (dense explicit coarse inverse, K4), one warp per row, g staged in smem
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    k_coarse_gemv(int nc, const double2* __restrict__ Cinv, const double2* __restrict__ g, double2* __restrict__ z) {
-  extern __shared__ double2 g_sh[];
-  for (int k = threadIdx.x; k < nc; k += blockDim.x) g_sh[k] = g[k];
-  __syncthreads();
+// z = C^-1 g  (dense explicit coarse inverse, K4), one row per block of THREADS threads:
+// each thread takes a strided set of columns (a few loads, all independent), then a block
+// reduction in fixed order.  Latency-bound kernel (C^-1 stays in L2), so the parallelism
+// comes from the number of warps, not from per-thread batching (ptxas serialises those).
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS)
+    k_coarse_gemv(int nc, const double2* __restrict__ Cinv, const double2* __restrict__ g, double2* __restrict__ z,
+                  L2Prefetch pf) {
+  constexpr int WARPS = THREADS / 32;
+  __shared__ double2 red[WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int row = blockIdx.x * WARPS + warp; row < nc; row += gridDim.x * WARPS) {
-    const double2* cr = Cinv + (size_t)row * nc;
-    double2 a = cz();
-#pragma unroll 8
-    for (int k = lane; k < nc; k += 32) a = cfma(cr[k], g_sh[k], a);
-    a = warp_sum2(a);
-    if (lane == 0) z[row] = a;
+  pdl_trigger();
+  l2_prefetch_slices(pf);
+  pdl_wait();
+  const int row = blockIdx.x;
+  const double2* cr = Cinv + (size_t)row * nc;
+  double2 a = cz();
+  for (int k = threadIdx.x; k < nc; k += THREADS) a = cfma(__ldg(cr + k), __ldg(g + k), a);
+  a = warp_sum2(a);
+  if (lane == 0) red[warp] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 t = red[0];
+#pragma unroll
+    for (int q = 1; q < WARPS; ++q) t = cadd(t, red[q]);
+    z[row] = t;
   }
 }
 
@@ -1147,41 +1160,83 @@ struct CgsArgs {
   // fused Givens (pass 2)
   int givens;
   GivensArgs ga;
+  L2Prefetch pf;
 };
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k_cgs_pass(CgsArgs a) {
-  extern __shared__ double2 w_sh[];
-  __shared__ bool is_last;
-  const int nv = a.st->j + 1;
-  const int n = a.n, b = blockIdx.x, lo = b * a.chunk, len = max(0, min(a.chunk, n - lo));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int k = threadIdx.x; k < len; k += blockDim.x) {
-    double2 acc;
-    if (a.gather) {
-      const int r = lo + k;
-      const int slots[2] = {a.lam_lo[r], a.lam_hi[r]};
-      double2 u[2];
+// sum_{lo <= i < hi} h[i] V_i[r], loads issued in batches of 8 (fixed summation order)
+__device__ __forceinline__ double2 sum_vh(const double2* __restrict__ h, const double2* __restrict__ V, size_t ldv,
+                                          int r, int lo, int hi) {
+  constexpr int VB = 8;
+  double2 acc = cz();
+  int i = lo;
+  for (; i + VB <= hi; i += VB) {
+    double2 v[VB];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int slot = slots[q], s = slot / a.NB;
-        double2 cz_ = cz();
-        for (int c = 0; c < a.NC; ++c) {
-          const int cg = a.cglob[(size_t)s * a.NC + c];
-          if (cg >= 0) cz_ = cfma(a.cpl_b[(size_t)slot * a.NC + c], a.z[cg], cz_);
+    for (int u = 0; u < VB; ++u) v[u] = V[(size_t)(i + u) * ldv + r];
+#pragma unroll
+    for (int u = 0; u < VB; ++u) acc = cfma(__ldg(h + i + u), v[u], acc);
+  }
+  for (; i < hi; ++i) acc = cfma(__ldg(h + i), V[(size_t)i * ldv + r], acc);
+  return acc;
+}
+
+// One classical Gram-Schmidt pass over ROWS multiplier rows per block (THREADS / ROWS
+// thread groups):
+//   phase A  w[r] = fused dual-operator tail (gather) or loaded; optional w -= sum_i h_in[i] V_i
+//            (each group sums a contiguous range of basis vectors, combined in fixed order);
+//   phase B  one warp per basis vector: block partials of conj(V_i) w over the block's rows
+//            (and |w|^2), so each lane keeps ROWS/32 independent loads in flight;
+//   the last block reduces the partials in a fixed order (deterministic) and optionally runs
+//   the Givens step.  nv = st->j + 1.  mode 0: dots + norm (out[0..nv]); 1: dots; 2: norm.
+template <int THREADS, int ROWS>
+__global__ void __launch_bounds__(THREADS) k_cgs_pass(CgsArgs a) {
+  constexpr int WARPS = THREADS / 32, GROUPS = THREADS / ROWS, LPR = ROWS / 32;
+  static_assert(THREADS % ROWS == 0 && ROWS % 32 == 0, "block shape");
+  __shared__ double2 w_sh[ROWS];
+  __shared__ double2 acc_sh[GROUPS][ROWS];
+  __shared__ double2 stage[640];  // Givens staging (cos 256 doubles | sin 256 | h 256)
+  __shared__ bool is_last;
+  pdl_trigger();
+  l2_prefetch_slices(a.pf);
+  pdl_wait();
+  const int nv = a.st->j + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lr = threadIdx.x % ROWS, grp = threadIdx.x / ROWS;
+  const int row0 = blockIdx.x * ROWS, r = row0 + lr;
+  const bool act = r < a.n;
+  if (a.h_in != nullptr) {
+    const int per = (nv + GROUPS - 1) / GROUPS;
+    const int lo = min(nv, grp * per), hi = min(nv, lo + per);
+    acc_sh[grp][lr] = act ? sum_vh(a.h_in, a.V, a.ldv, r, lo, hi) : cz();
+    __syncthreads();
+  }
+  if (grp == 0) {
+    double2 w = cz();
+    if (act) {
+      if (a.gather) {
+        const int slots[2] = {a.lam_lo[r], a.lam_hi[r]};
+        double2 u[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int slot = slots[q], s = slot / a.NB;
+          double2 cz_ = cz();
+          for (int c = 0; c < a.NC; ++c) {
+            const int cg = a.cglob[(size_t)s * a.NC + c];
+            if (cg >= 0) cz_ = cfma(a.cpl_b[(size_t)slot * a.NC + c], a.z[cg], cz_);
+          }
+          u[q] = csub(a.u1b[slot], cz_);
         }
-        u[q] = csub(a.u1b[slot], cz_);
+        const double2 d = csub(u[0], u[1]);
+        w = make_double2(-d.x, -d.y);
+      } else {
+        w = a.w[r];
       }
-      const double2 d = csub(u[0], u[1]);
-      acc = make_double2(-d.x, -d.y);
-      a.w[lo + k] = acc;
-    } else {
-      acc = a.w[lo + k];
+      if (a.h_in != nullptr) {
+#pragma unroll
+        for (int g = 0; g < GROUPS; ++g) w = csub(w, acc_sh[g][lr]);
+      }
+      if (a.gather || a.h_in != nullptr) a.w[r] = w;
     }
-    if (a.h_in != nullptr) {
-      for (int i = 0; i < nv; ++i) acc = cfms(a.h_in[i], a.V[(size_t)i * a.ldv + lo + k], acc);
-      a.w[lo + k] = acc;
-    }
-    w_sh[k] = acc;
+    w_sh[lr] = w;
   }
   __syncthreads();
   const int ndots = (a.mode == 2) ? 0 : nv;
@@ -1189,14 +1244,19 @@ __global__ void __launch_bounds__(WARPS * 32) k_cgs_pass(CgsArgs a) {
   for (int i = warp; i < nout; i += WARPS) {
     double2 acc = cz();
     if (i < ndots) {
-      const double2* v = a.V + (size_t)i * a.ldv + lo;
-#pragma unroll 4
-      for (int k = lane; k < len; k += 32) acc = cfma_conj(v[k], w_sh[k], acc);
+      const double2* v = a.V + (size_t)i * a.ldv + row0;
+      double2 x[LPR];
+      // clamped addresses keep the loads unpredicated (all in flight); w_sh is 0 past n
+#pragma unroll
+      for (int u = 0; u < LPR; ++u) x[u] = v[min(lane + 32 * u, a.n - 1 - row0)];
+#pragma unroll
+      for (int u = 0; u < LPR; ++u) acc = cfma_conj(x[u], w_sh[lane + 32 * u], acc);
     } else {
-      for (int k = lane; k < len; k += 32) acc.x += cabs2(w_sh[k]);
+#pragma unroll
+      for (int u = 0; u < LPR; ++u) acc.x += cabs2(w_sh[lane + 32 * u]);
     }
     acc = warp_sum2(acc);
-    if (lane == 0) a.part[(size_t)i * gridDim.x + b] = acc;
+    if (lane == 0) a.part[(size_t)i * gridDim.x + blockIdx.x] = acc;
   }
   __threadfence();
   __syncthreads();
@@ -1204,37 +1264,64 @@ __global__ void __launch_bounds__(WARPS * 32) k_cgs_pass(CgsArgs a) {
   __syncthreads();
   if (!is_last) return;
   __threadfence();
-  for (int i = warp; i < nout; i += WARPS) {
-    double2 acc = cz();
-#pragma unroll 4
-    for (int bb = lane; bb < (int)gridDim.x; bb += 32) acc = cadd(acc, __ldcg(a.part + (size_t)i * gridDim.x + bb));
-    acc = warp_sum2(acc);
-    if (lane == 0) a.out[i] = acc;
+  // grid reduction: SEGS threads per output, strided over the block partials, then shuffles
+  constexpr int SEGS = 16, PER = THREADS / SEGS;
+  const int G = gridDim.x, seg = threadIdx.x % SEGS;
+  for (int i0 = 0; i0 < nout; i0 += PER) {
+    const int i = i0 + threadIdx.x / SEGS;
+    double2 t = cz();
+    if (i < nout) {
+      const double2* pp = a.part + (size_t)i * G;
+#pragma unroll 8
+      for (int bb = seg; bb < G; bb += SEGS) t = cadd(t, __ldcg(pp + bb));
+    }
+#pragma unroll
+    for (int m = SEGS / 2; m > 0; m >>= 1) t = cadd(t, shfl_xor2(t, m));
+    if (seg == 0 && i < nout) a.out[i] = t;
   }
   if (threadIdx.x == 0) *a.counter = 0u;
   if (a.givens) {
+    __threadfence_block();
     __syncthreads();
-    if (warp == 0) {
-      // reuse the w chunk buffer for the rotation staging (256 + 256 + 256 entries)
-      double* sc = reinterpret_cast<double*>(w_sh);
-      double2* ss = w_sh + 128;
-      double2* sh = w_sh + 384;
-      givens_warp(a.ga, sc, ss, sh);
-    }
+    if (warp == 0) givens_warp(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384);
   }
+}
+
+// Row-block x vector-group combination: ROWS rows per block, GROUPS thread groups each
+// summing a contiguous range of the nv basis vectors (all loads of a group in flight at
+// once), combined in fixed order by group 0.  Returns true on group-0 threads of live rows.
+template <int ROWS, int GROUPS>
+__device__ __forceinline__ bool combine_rows(const double2* __restrict__ h, const double2* __restrict__ V, size_t ldv,
+                                             int n, int nv, int& r, double2& sum) {
+  __shared__ double2 acc_sh[GROUPS][ROWS];
+  const int lr = threadIdx.x % ROWS, grp = threadIdx.x / ROWS;
+  r = blockIdx.x * ROWS + lr;
+  const int per = (nv + GROUPS - 1) / GROUPS;
+  const int lo = min(nv, grp * per), hi = min(nv, lo + per);
+  acc_sh[grp][lr] = r < n ? sum_vh(h, V, ldv, r, lo, hi) : cz();
+  __syncthreads();
+  if (grp != 0 || r >= n) return false;
+  sum = acc_sh[0][lr];
+#pragma unroll
+  for (int g = 1; g < GROUPS; ++g) sum = cadd(sum, acc_sh[g][lr]);
+  return true;
 }
 
 // V_{j+1} = (w - V h2) / h_{j+1,j}: the second CGS update fused with the normalisation
 // (only while the cycle continues; st->j already advanced, so V_0..V_{j-1} are read).
-__global__ void k_update_normalize(int n, const GmresState* __restrict__ st, const double2* __restrict__ h2,
-                                   const double2* __restrict__ w, double2* __restrict__ V, size_t ldv) {
+template <int ROWS, int GROUPS>
+__global__ void __launch_bounds__(ROWS* GROUPS)
+    k_update_normalize(int n, const GmresState* __restrict__ st, const double2* __restrict__ h2,
+                       const double2* __restrict__ w, double2* __restrict__ V, size_t ldv, L2Prefetch pf) {
+  pdl_trigger();
+  l2_prefetch_slices(pf);
+  pdl_wait();
   if (!st->cont) return;
   const int nv = st->j;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  double2 acc = w[k];
-  for (int i = 0; i < nv; ++i) acc = cfms(__ldg(h2 + i), V[(size_t)i * ldv + k], acc);
-  V[(size_t)nv * ldv + k] = cscale(acc, st->inv_hnext);
+  int r;
+  double2 sum;
+  if (combine_rows<ROWS, GROUPS>(h2, V, ldv, n, nv, r, sum))
+    V[(size_t)nv * ldv + r] = cscale(csub(w[r], sum), st->inv_hnext);
 }
 
 // y = R^-1 g (krylov.hpp:191-196), one warp
@@ -1258,14 +1345,13 @@ __global__ void k_scale_copy(int n, const double2* __restrict__ x, double s, dou
   if (k < n) y[k] = cscale(x[k], s);
 }
 // t = sum_i y_i V_i
-__global__ void k_combine(int n, const double2* __restrict__ V, size_t ldv, const GmresState* __restrict__ st,
-                          const double2* __restrict__ y, double2* __restrict__ t) {
-  const int nv = st->k;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  double2 acc = cz();
-  for (int i = 0; i < nv; ++i) acc = cfma(__ldg(y + i), V[(size_t)i * ldv + k], acc);
-  t[k] = acc;
+template <int ROWS, int GROUPS>
+__global__ void __launch_bounds__(ROWS* GROUPS) k_combine(int n, const double2* __restrict__ V, size_t ldv,
+                                                          const GmresState* __restrict__ st,
+                                                          const double2* __restrict__ y, double2* __restrict__ t) {
+  int r;
+  double2 sum;
+  if (combine_rows<ROWS, GROUPS>(y, V, ldv, n, st->k, r, sum)) t[r] = sum;
 }
 // y = a - b ;  y = a + b
 __global__ void k_sub(int n, const double2* a, const double2* b, double2* y) {
