@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "band.cuh"
+#include "blockthomas.cuh"
 #include "comm.hpp"
 #include "fetigpu.h"
 #include "host_core.hpp"
@@ -78,6 +79,10 @@ struct Ctx {
   SubLayout L{};
   MeshLayout M{};
   int Wt = 0, WCt = 0, nc = 0, nl = 0, n = 0, m = 0;
+  // block-Thomas interior solve (blockthomas.cuh): records, block count, enabled
+  double2* d_bt = nullptr;
+  int bt_nb = 0;
+  bool use_bt = false;
   double setup_seconds = 0;
   long long launches = 0;
   std::vector<void*> allocs;
@@ -295,6 +300,36 @@ struct Ctx {
     }
   }
 
+  void setup_block_thomas() {
+    const int S = H.n_sub, NI = H.NI;
+    if (Wt > BT_Q || std::getenv("FETIGPU_NO_BT")) return;
+    bt_nb = cdiv(NI, BT_Q);
+    d_bt = alloc<double2>((size_t)S * bt_nb * BT_REC);
+    CU(cudaFuncSetAttribute(k_bt_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bt_factor_smem()));
+    CU(cudaFuncSetAttribute(k_bt_solve<kBtStages>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)bt_solve_smem<kBtStages>()));
+    launch(FETIGPU_K_OTHER, [&] {
+      k_bt_factor<<<S, 256, bt_factor_smem(), stream>>>(d_colband, (size_t)NI * (Wt + 1), Wt, NI, bt_nb, d_bt,
+                                                        d_status);
+    });
+    std::vector<int> st(S);
+    CU(cudaMemcpyAsync(st.data(), d_status, S * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    use_bt = true;
+    for (int v : st) use_bt = use_bt && v == 0;  // else: the banded substitution serves the solves
+  }
+  // x = A_ii^-1 x in place for one right-hand side per subdomain (stride NI)
+  void interior_solve(double2* X) {
+    if (use_bt) {
+      launch(FETIGPU_K_BAND, [&] {
+        k_bt_solve<kBtStages><<<H.n_sub, 32, bt_solve_smem<kBtStages>(), stream>>>(d_bt, bt_nb, H.NI, X,
+                                                                                    (size_t)H.NI);
+      });
+    } else {
+      band_solve(d_colband, d_rowband, Wt, H.n_sub, H.NI, X, H.NI, H.NI, 1);
+    }
+  }
+  static constexpr int kBtStages = 2;
   void check_status(int count, const char* what) {
     std::vector<int> st(count);
     CU(cudaMemcpyAsync(st.data(), d_status, count * sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -395,7 +430,10 @@ struct Ctx {
     });
     launch(FETIGPU_K_OTHER, [&] { k_pad_identity<<<S, 128, 0, stream>>>(L, d_n_i, d_n_b, d_colband, d_Sbb); });
 
-    // K2: batched band LDL^T of A_ii
+    // K2': block-Thomas factors for the per-solve interior solves (reads the band of A_ii,
+    // so it runs before the in-place band factorization)
+    setup_block_thomas();
+    // K2: batched band LDL^T of A_ii (setup multi-RHS solves; per-solve path if W > 32)
     band_ldlt(d_colband, d_rowband, Wt, S, NI, d_status);
     check_status(S, "interior block A_ii");
 
@@ -840,7 +878,7 @@ struct Ctx {
     const int S = H.n_sub, NI = H.NI, NB = H.NB;
     if (new_yi) {
       CU(cudaMemcpyAsync(d_yi, ti, (size_t)S * NI * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
-      band_solve(d_colband, d_rowband, Wt, S, NI, d_yi, NI, NI, 1);
+      interior_solve(d_yi);
     }
     {
       SymGemvArgs g = sym_args(d_Sinv_p);
@@ -867,7 +905,7 @@ struct Ctx {
       k_ri_rhs<<<cdiv((long long)S * NI, 256), 256, 0, stream>>>(L, d_ib_idx, d_ib_val, d_Aic, d_cglob, d_z, d_u1b,
                                                                  d_ri);
     });
-    band_solve(d_colband, d_rowband, Wt, S, NI, d_ri, NI, NI, 1);
+    interior_solve(d_ri);
     launch(FETIGPU_K_OTHER, [&] {
       k_ui_final<<<cdiv((long long)S * NI, 256), 256, 0, stream>>>((long long)S * NI, d_yi, d_ri);
     });
