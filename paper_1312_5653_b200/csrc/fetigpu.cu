@@ -80,6 +80,9 @@ struct Ctx {
   MeshLayout M{};
   int Wt = 0, WCt = 0, nc = 0, nl = 0, n = 0, m = 0;
   // block-Thomas interior solve (blockthomas.cuh): records, block count, enabled
+  int* d_aic_idx = nullptr;  // compact A_ic (eliminate-phase coarse rhs from the GEMV)
+  double2* d_aic_val = nullptr;
+  static constexpr int kAE = 8;
   double2* d_bt = nullptr;
   int bt_nb = 0;
   bool use_bt = false;
@@ -330,6 +333,20 @@ struct Ctx {
     }
   }
   static constexpr int kBtStages = 2;
+  void setup_compact_aic() {
+    const int S = H.n_sub, NC = H.NC;
+    if (NC == 0 || sym_tma || std::getenv("FETIGPU_NO_AIC")) return;  // (the TMA GEMV has no A_ic term)
+    d_aic_idx = alloc<int>((size_t)S * NC * kAE);
+    d_aic_val = alloc<double2>((size_t)S * NC * kAE);
+    CU(cudaMemsetAsync(d_status, 0, sizeof(int), stream));
+    launch(FETIGPU_K_OTHER, [&] {
+      k_compact_aic<<<cdiv((long long)S * NC, 128), 128, 0, stream>>>(L, kAE, d_Aic, d_aic_idx, d_aic_val, d_status);
+    });
+    int bad = 0;
+    CU(cudaMemcpyAsync(&bad, d_status, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    sync();
+    if (bad) d_aic_idx = nullptr;  // dense fallback: k_gcp_full
+  }
   void check_status(int count, const char* what) {
     std::vector<int> st(count);
     CU(cudaMemcpyAsync(st.data(), d_status, count * sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -467,6 +484,7 @@ struct Ctx {
       launch(FETIGPU_K_OTHER, [&] {
         k_coupling_i<<<cdiv((long long)S * NI, 128), 128, 0, stream>>>(L, Yc, Y, d_cpl_b, d_cpl_i);
       });
+      setup_compact_aic();
       setup_halo();
       slot_exchange(d_cpl_b, NC);  // phantom rows of the coupling (static)
       double2* contrib = alloc<double2>((size_t)S * NC * NC);
@@ -599,6 +617,7 @@ struct Ctx {
     d_out_l = alloc<double>(n);
     CU(cudaMallocHost(&h_pin, sizeof(double2) * 3 * (vcap + 4)));
     setup_mass();
+    setup_stencil();
     setup_l2_persistence();
     sync();
     setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -676,8 +695,38 @@ struct Ctx {
     });
   }
 
+  // 9-point stencils of K and M when the free dofs are exactly the interior grid nodes
+  bool stencil_ok = false;
+  double st_k[9] = {}, st_m[9] = {};
+  void setup_stencil() {
+    if (P.dpn != 1 || std::getenv("FETIGPU_NO_STENCIL")) return;
+    const int fx = P.nx - 1, fy = P.ny - 1;
+    if (fx < 1 || fy < 1 || (long long)fx * fy != (long long)P.free_dofs.size()) return;
+    for (int f = 0; f < (int)P.free_dofs.size(); ++f) {
+      const int I = f % fx, J = f / fx;
+      if (P.free_dofs[f] != (J + 1) * (P.nx + 1) + (I + 1)) return;
+    }
+    // element-local corners (0,0) (1,0) (1,1) (0,1): stencil offset of (alpha -> beta)
+    const int dx[4] = {0, 1, 1, 0}, dy[4] = {0, 0, 1, 1};
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) {
+        const int o = (dy[b] - dy[a] + 1) * 3 + (dx[b] - dx[a] + 1);
+        st_k[o] += P.ke[a * 4 + b];
+        st_m[o] += P.me[a * 4 + b];
+      }
+    stencil_ok = true;
+  }
   template <typename T>
   void apply_global(const T* x, const double* xc, cd kc, cd mcoef, T* y) {
+    if (stencil_ok && xc == nullptr) {
+      Stencil9 S9;
+      for (int q = 0; q < 9; ++q) S9.c[q] = d2(kc * st_k[q] + mcoef * st_m[q]);
+      const int fx = P.nx - 1, fy = P.ny - 1;
+      launch(FETIGPU_K_GLOBAL, [&] {
+        k_apply_stencil9<T><<<dim3(cdiv(fx, 128), fy), 128, 0, stream>>>(fx, fy, S9, x, y);
+      });
+      return;
+    }
     launch(FETIGPU_K_GLOBAL, [&] {
       k_apply_global<T><<<cdiv(n, 256), 256, 0, stream>>>(M, elem_km, n, d_free_dofs, d_free_map, d_cons_map, x, xc, d2(kc),
                                                           d2(mcoef), y);
@@ -887,10 +936,19 @@ struct Ctx {
       g.yi = d_yi;
       g.alpha = 1.0;
       g.out = d_u1b;
+      if (d_aic_idx != nullptr) {  // coarse rhs fused: cpl_b^T (t_b - A_bi y_i) + A_ic^T y_i
+        g.gcp = d_gcp;
+        g.cpl_b = d_cpl_b;
+        g.NC = H.NC;
+        g.AE = kAE;
+        g.aic_idx = d_aic_idx;
+        g.aic_val = d_aic_val;
+      }
       launch(FETIGPU_K_OTHER, [&] { launch_sym(g); });
     }
     (void)NB;
-    launch(FETIGPU_K_OTHER, [&] { k_gcp_full<<<S, 256, 0, stream>>>(L, d_cpl_i, d_cpl_b, ti, tb, d_gcp); });
+    if (d_aic_idx == nullptr)
+      launch(FETIGPU_K_OTHER, [&] { k_gcp_full<<<S, 256, 0, stream>>>(L, d_cpl_i, d_cpl_b, ti, tb, d_gcp); });
     coarse_solve(fc);
     launch(FETIGPU_K_OTHER, [&] {
       k_ub_correct<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(L, d_cglob, d_z, d_cpl_b, d_u1b);

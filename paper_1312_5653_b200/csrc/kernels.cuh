@@ -470,6 +470,10 @@ struct SymGemvArgs {
   const int* corner_slots;
   const double2* fc;
   double2* g;
+  // MODE 2 coarse rhs: the nonzeros of A_ic per (subdomain, corner), AE per corner
+  int AE;
+  const int* aic_idx;
+  const double2* aic_val;
 };
 
 template <int MODE, int SYM_BATCH, int WARPS>
@@ -589,6 +593,12 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(S
     for (int c = warp; c < a.NC; c += WARPS) {
       double2 acc = cz();
       for (int k = lane; k < NB; k += 32) acc = cfma(a.cpl_b[((size_t)s * NB + k) * a.NC + c], x_sh[k], acc);
+      // eliminate (MODE 2): coupling^T t = cpl_b^T (t_b - A_bi y_i) + A_ic^T y_i
+      if (MODE == 2 && a.aic_idx != nullptr && lane < a.AE) {
+        const size_t e = ((size_t)s * a.NC + c) * a.AE + lane;
+        const int i = a.aic_idx[e];
+        if (i >= 0) acc = cfma(a.aic_val[e], a.yi[(size_t)s * a.NI + i], acc);
+      }
       acc = warp_sum2(acc);
       if (lane == 0) a.gcp[(size_t)s * a.NC + c] = acc;
     }
@@ -925,6 +935,31 @@ __global__ void __launch_bounds__(WARPS * 32)
 }
 // gcp[s][c] = (A_rc^T A_rr^-1 t)_c = sum_i cpl_i(i,c) t_i + sum_k cpl_b(k,c) t_b   (feti.cpp:530;
 // equal to A_rc^T u1 because A_rr^-1 is symmetric).  One CTA per subdomain.
+// Nonzeros of A_ic column-wise per (subdomain, corner): the sparse term A_ic^T y_i of the
+// eliminate-phase coarse rhs.  status[0] = 1 if a column has more than AE nonzeros.
+__global__ void k_compact_aic(SubLayout L, int AE, const double2* __restrict__ Aic, int* __restrict__ idx,
+                              double2* __restrict__ val, int* __restrict__ status) {
+  const int sc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (sc >= L.S * L.NC) return;
+  const int s = sc / L.NC, c = sc % L.NC;
+  int e = 0;
+  for (int i = 0; i < L.NI; ++i) {
+    const double2 v = Aic[((size_t)s * L.NI + i) * L.NC + c];
+    if (v.x != 0.0 || v.y != 0.0) {
+      if (e < AE) {
+        idx[(size_t)sc * AE + e] = i;
+        val[(size_t)sc * AE + e] = v;
+      }
+      ++e;
+    }
+  }
+  if (e > AE) atomicExch(status, 1);
+  for (; e < AE; ++e) {
+    idx[(size_t)sc * AE + e] = -1;
+    val[(size_t)sc * AE + e] = cz();
+  }
+}
+
 __global__ void k_gcp_full(SubLayout L, const double2* __restrict__ cpl_i, const double2* __restrict__ cpl_b,
                            const double2* __restrict__ ti, const double2* __restrict__ tb, double2* __restrict__ gcp) {
   __shared__ double2 red[8][32];
@@ -1324,10 +1359,29 @@ __global__ void __launch_bounds__(ROWS* GROUPS)
     V[(size_t)nv * ldv + r] = cscale(csub(w[r], sum), st->inv_hnext);
 }
 
-// y = R^-1 g (krylov.hpp:191-196), one warp
-__global__ void k_backsub(const GmresState* __restrict__ st, const double2* __restrict__ R,
-                          const double2* __restrict__ g, double2* __restrict__ y) {
+// y = R^-1 g (krylov.hpp:191-196), one warp.  When the packed triangle fits (k <= BS_KMAX)
+// it is staged in shared memory first (all loads in flight; static 48 KB cap), so the k-row recurrence runs
+// on shared-memory latencies instead of one global round trip per row.
+constexpr int BS_KMAX = 72;
+__global__ void __launch_bounds__(32) k_backsub(const GmresState* __restrict__ st, const double2* __restrict__ R,
+                                                const double2* __restrict__ g, double2* __restrict__ y) {
+  __shared__ double2 rs[BS_KMAX * (BS_KMAX + 1) / 2];
+  __shared__ double2 ys[BS_KMAX];
   const int k = st->k, lane = threadIdx.x;
+  if (k <= BS_KMAX) {
+    const int tot = k * (k + 1) / 2;
+    for (int e = lane; e < tot; e += 32) rs[e] = R[e];
+    __syncwarp();
+    for (int i = k - 1; i >= 0; --i) {
+      double2 acc = cz();
+      for (int j2 = i + 1 + lane; j2 < k; j2 += 32) acc = cfma(rs[j2 * (j2 + 1) / 2 + i], ys[j2], acc);
+      acc = warp_sum2(acc);
+      if (lane == 0) ys[i] = cmul(csub(g[i], acc), crecip(rs[i * (i + 1) / 2 + i]));
+      __syncwarp();
+    }
+    for (int i = lane; i < k; i += 32) y[i] = ys[i];
+    return;
+  }
   for (int i = k - 1; i >= 0; --i) {
     double2 acc = cz();
     for (int j2 = i + 1 + lane; j2 < k; j2 += 32) acc = cfma(R[(size_t)j2 * (j2 + 1) / 2 + i], y[j2], acc);
@@ -1458,6 +1512,32 @@ __global__ void k_apply_global(MeshLayout M, ElemKM KM, int n, const int* __rest
     }
   }
   store_c<T>(y + f, acc);
+}
+
+// Structured fast path of k_apply_global (scalar physics, every boundary node constrained):
+// the free dofs are the (nx-1) x (ny-1) interior nodes in lexicographic order, so the
+// assembled Q1 operator kc K + mc M is one 9-point stencil (coef[dy+1][dx+1], built on the
+// host from the element matrices).  No constrained-value term (xc == nullptr only).
+struct Stencil9 {
+  double2 c[9];
+};
+template <typename T>
+__global__ void k_apply_stencil9(int fx, int fy, Stencil9 S, const T* __restrict__ x, T* __restrict__ y) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x, J = blockIdx.y;
+  if (I >= fx) return;
+  double2 acc = cz();
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+    const int jj = J + dy;
+    if (jj < 0 || jj >= fy) continue;
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int ii = I + dx;
+      if (ii < 0 || ii >= fx) continue;
+      acc = cfma(S.c[(dy + 1) * 3 + dx + 1], as_c<T>(x[(size_t)jj * fx + ii]), acc);
+    }
+  }
+  store_c<T>(y + (size_t)J * fx + I, acc);
 }
 
 // Kronecker mass solve V^-1 = (M_y ⊗ M_x ⊗ I_dpn)^-1: batches of identical SPD tridiagonal
