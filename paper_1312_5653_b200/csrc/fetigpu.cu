@@ -145,6 +145,10 @@ struct Ctx {
   cudaGraphConditionalHandle arnoldi_handle{};
   int arnoldi_body_kernels = 0;
   static constexpr int kCgsThreads = 512, kCgsRows = 256;  // k_cgs_pass block shape
+  // fused Arnoldi tail (k_arnoldi_tail): rows per thread (0 = off), grid, barrier words
+  int tail_rpt = 0, tail_grid = 0, tail_rb = 1;
+  unsigned int* d_bar = nullptr;
+  unsigned long long* d_tstamp = nullptr;  // FETIGPU_TAIL_TIMES=1: per-phase timestamps
   int mdot_blocks = 0, mdot_chunk = 0;
   // mass solve (Kronecker tridiagonal)
   double *d_mx_cp = nullptr, *d_mx_dinv = nullptr, *d_my_cp = nullptr, *d_my_dinv = nullptr;
@@ -346,6 +350,46 @@ struct Ctx {
     CU(cudaMemcpyAsync(&bad, d_status, sizeof(int), cudaMemcpyDeviceToHost, stream));
     sync();
     if (bad) d_aic_idx = nullptr;  // dense fallback: k_gcp_full
+  }
+  // one-launch Arnoldi tail when every block of its grid can be co-resident (one GPU only)
+  static constexpr int kTailThreads = 512;
+  size_t tail_smem() const { return sizeof(double2) * ((size_t)kTailThreads + 2 * (size_t)(vcap_hint() + 2) + 640); }
+  void setup_fused_tail() {
+    if (dist() || H.NC > 4 || nc > kTailThreads + 2 * (vcap_hint() + 2) || std::getenv("FETIGPU_NO_FUSED_TAIL"))
+      return;
+    const size_t smem = tail_smem();
+    if (smem > 200 * 1024) return;
+    int sms = 0, per_sm = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc.device));
+    CU(cudaFuncSetAttribute(k_arnoldi_tail<kTailThreads, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi_tail<kTailThreads, 4>, kTailThreads, smem));
+    const int grid = std::max(1, cdiv(nown, kTailThreads));
+    if (per_sm <= 0 || grid > per_sm * sms) return;
+    tail_rpt = 1;
+    tail_grid = grid;
+    const int rows = cdiv(std::max(nc, 1), tail_grid);
+    tail_rb = rows <= 1 ? 1 : rows <= 2 ? 2 : rows <= 4 ? 4 : rows <= 8 ? 8 : 16;
+    d_bar = alloc<unsigned int>(2);
+    CU(cudaMemsetAsync(d_bar, 0, 2 * sizeof(unsigned int), stream));
+    if (std::getenv("FETIGPU_TAIL_TIMES")) {
+      d_tstamp = alloc<unsigned long long>((size_t)16 * (vcap_hint() + 2));
+      CU(cudaMemsetAsync(d_tstamp, 0, (size_t)16 * (vcap_hint() + 2) * sizeof(unsigned long long), stream));
+    }
+  }
+  int vcap_hint() const { return std::max(2, desc.max_iter + 1); }
+  void report_tail_times(int it0, int it1) {
+    const int cnt = it1 - it0;
+    if (cnt <= 0) return;
+    std::vector<unsigned long long> t((size_t)16 * cnt);
+    CU(cudaMemcpy(t.data(), d_tstamp + (size_t)16 * it0, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    const char* names[] = {"coarse+pre", "barA", "pass1", "barB+red", "sub1", "dots2", "barC+red", "update", "givens"};
+    std::fprintf(stderr, "[fetigpu] tail phases (us, block 0, mean of %d):", cnt);
+    for (int p = 0; p < 9; ++p) {
+      double acc = 0;
+      for (int i = 0; i < cnt; ++i) acc += (double)t[(size_t)i * 16 + p + 1] - (double)t[(size_t)i * 16 + p];
+      std::fprintf(stderr, " %s %.2f", names[p], acc / cnt / 1e3);
+    }
+    std::fprintf(stderr, "\n");
   }
   void check_status(int count, const char* what) {
     std::vector<int> st(count);
@@ -588,7 +632,8 @@ struct Ctx {
     d_best = alloc<double2>(ldv);
     mdot_blocks = std::max(1, cdiv(nown, kCgsRows));
     mdot_chunk = kCgsRows;
-    d_part = alloc<double2>((size_t)(vcap + 2) * mdot_blocks);
+    setup_fused_tail();
+    d_part = alloc<double2>((size_t)(vcap + 2) * std::max(mdot_blocks, 2 * tail_grid));  // tail: 2 halves
     d_red = alloc<double2>(3 * (vcap + 2));
     d_y = alloc<double2>(vcap + 2);
     d_gst = alloc<GmresState>(1);
@@ -860,12 +905,12 @@ struct Ctx {
   }
   // local dual solve u1_b = S_bb^-1 t_b with t_b = -B^T lam, gcp = cpl_b^T t_b, and (last
   // CTA) the coarse rhs g = -sum gcp (K5); sharded: partial g summed over ranks
-  void dual_gemv(SymGemvArgs g) {
+  void dual_gemv(SymGemvArgs g, bool fused_tail = false) {
     g.alpha = -1.0;
     g.out = d_u1b;
     g.cpl_b = d_cpl_b;
     g.gcp = d_gcp;
-    if (nc > 0) {
+    if (nc > 0 && !fused_tail) {  // (the fused Arnoldi tail assembles g itself)
       g.g_counter = d_counter + 1;
       g.nc = nc;
       g.corner_slots = d_corner_slots;
@@ -1006,9 +1051,40 @@ struct Ctx {
       SymGemvArgs g = sym_args(d_Sinv_p);
       g.mode = 1;
       g.wb = d_wb;
-      dual_gemv(g);
+      dual_gemv(g, tail_rpt > 0);
     }
     mark(3);
+    if (tail_rpt > 0) {  // coarse + CGS2 + Givens + normalisation in one launch
+      ArnoldiTailArgs t{};
+      t.n = nown;
+      t.V = d_V;
+      t.ldv = ldv;
+      t.st = d_gst;
+      t.part = d_part;
+      t.h1 = h1;
+      t.h2 = h2;
+      t.bar = d_bar;
+      t.nc = nc;
+      t.coarse_rb = tail_rb;
+      t.Cinv = d_Cinv;
+      t.gcp = d_gcp;
+      t.corner_slots = d_corner_slots;
+      t.z = d_z;
+      t.NB = H.NB;
+      t.NC = H.NC;
+      t.lam_lo = d_lam_lo;
+      t.lam_hi = d_lam_hi;
+      t.cglob = d_cglob;
+      t.u1b = d_u1b;
+      t.cpl_b = d_cpl_b;
+      t.ga = GivensArgs{d_gst, h1, h2, d_R, d_gcos, d_gsin, d_gvec, in_graph ? 1 : 0, arnoldi_handle};
+      t.tstamp = d_tstamp;
+      t.hcap = vcap + 2;
+      t.vcap = vcap;
+      launch(FETIGPU_K_ORTHO, [&] { kx(k_arnoldi_tail<kTailThreads, 4>, tail_grid, kTailThreads, tail_smem(), t); });
+      mark(6);
+      return;
+    }
     arnoldi_phase = true;
     coarse_gemv();
     arnoldi_phase = false;
@@ -1160,6 +1236,7 @@ struct Ctx {
         } while (h_gst->cont);
       }
       if (h_gst->status) throw NumericalError("gmres: breakdown (NaN/Inf in Arnoldi)");
+      if (d_tstamp) report_tail_times(iterations, h_gst->iterations);
       iterations = h_gst->iterations;
       // back substitution and x += P^-1 (Q y)  (krylov.hpp:191-209), true residual r = b - F x
       launch(FETIGPU_K_ORTHO, [&] { k_backsub<<<1, 32, 0, stream>>>(d_gst, d_R, d_gvec, d_y); });

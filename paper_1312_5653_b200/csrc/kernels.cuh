@@ -1081,25 +1081,43 @@ struct GivensArgs {
   int in_graph;
   cudaGraphConditionalHandle handle;
 };
-__device__ void givens_warp(const GivensArgs& a, double* sc, double2* ss, double2* sh) {
+template <bool SMEM>
+__device__ __forceinline__ double2 ldh(const double2* p) {
+  if constexpr (SMEM) return *p;
+  else return __ldcg(p);
+}
+// hnext = |w1 - V h2| = sqrt(|w1|^2 - sum_{i<=j} |h2_i|^2) (V orthonormal; h2 round-off sized)
+// and the finiteness of h1 + h2, one warp; every caller gets bit-identical results.
+template <bool SMEM>
+__device__ __forceinline__ double warp_hnext(const double2* h1, const double2* h2, int j, bool& finite) {
+  const int lane = threadIdx.x & 31;
+  bool fin = true;
+  double s2 = 0.0;
+  for (int i = lane; i <= j; i += 32) {
+    const double2 h2i = ldh<SMEM>(h2 + i);
+    const double2 v = cadd(ldh<SMEM>(h1 + i), h2i);
+    fin = fin && isfinite(v.x) && isfinite(v.y);
+    s2 += cabs2(h2i);
+  }
+  fin = __all_sync(0xffffffffu, fin);
+  s2 = warp_sum(s2);
+  const double hnext = sqrt(fmax(0.0, ldh<SMEM>(h2 + j + 1).x - s2));
+  finite = fin && isfinite(hnext);
+  return hnext;
+}
+template <bool SMEM = false>
+__device__ void givens_warp(const GivensArgs& a, double* sc, double2* ss, double2* sh, const double2* h1 = nullptr,
+                            const double2* h2 = nullptr) {
   constexpr int CHK = 256;
   const int lane = threadIdx.x & 31;
+  if (h1 == nullptr) h1 = a.h1;
+  if (h2 == nullptr) h2 = a.h2;
   GmresState* st = a.st;
   const int j = st->j;
   double2* col = a.R + (size_t)j * (j + 1) / 2;
-  bool finite = true;
-  double s2 = 0.0;
-  for (int i = lane; i <= j; i += 32) {
-    const double2 v = cadd(a.h1[i], a.h2[i]);
-    finite = finite && isfinite(v.x) && isfinite(v.y);
-    s2 += cabs2(a.h2[i]);
-  }
-  finite = __all_sync(0xffffffffu, finite);
-  s2 = warp_sum(s2);
-  const double wpre = sqrt(a.h1[j + 1].x);
-  // |w1 - V h2|^2 = |w1|^2 - sum |h2_i|^2 (V orthonormal; h2 is round-off sized)
-  const double hnext = sqrt(fmax(0.0, a.h2[j + 1].x - s2));
-  finite = finite && isfinite(hnext);
+  bool finite;
+  const double hnext = warp_hnext<SMEM>(h1, h2, j, finite);
+  const double wpre = sqrt(ldh<SMEM>(h1 + j + 1).x);
   if (!finite) {
     if (lane == 0) {
       st->status = 1;
@@ -1109,13 +1127,13 @@ __device__ void givens_warp(const GivensArgs& a, double* sc, double2* ss, double
     return;
   }
   // previous rotations (krylov.hpp:169-173): carry = rotated entry i, t2 = original entry i+1
-  double2 carry = cadd(a.h1[0], a.h2[0]);
+  double2 carry = cadd(ldh<SMEM>(h1), ldh<SMEM>(h2));
   for (int base = 0; base < j; base += CHK) {
     const int cnt = min(CHK, j - base);
     for (int q = lane; q < cnt; q += 32) {
       sc[q] = a.gcos[base + q];
       ss[q] = a.gsin[base + q];
-      sh[q] = cadd(a.h1[base + q + 1], a.h2[base + q + 1]);
+      sh[q] = cadd(ldh<SMEM>(h1 + base + q + 1), ldh<SMEM>(h2 + base + q + 1));
     }
     __syncwarp();
     if (lane == 0) {
@@ -1214,6 +1232,26 @@ __device__ __forceinline__ double2 sum_vh(const double2* __restrict__ h, const d
   return acc;
 }
 
+// w[r] = -(u_lo - u_hi), u_slot = u1_b[slot] - cpl_b[slot] z_loc: the dual-operator tail of
+// multiplier row r (feti.cpp:542-555, 593).  z_l2: read z through L2 (written in this kernel).
+template <typename A>
+__device__ __forceinline__ double2 dual_tail_row(const A& a, int r, bool z_l2) {
+  const int slots[2] = {a.lam_lo[r], a.lam_hi[r]};
+  double2 u[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int slot = slots[q], s = slot / a.NB;
+    double2 cz_ = cz();
+    for (int c = 0; c < a.NC; ++c) {
+      const int cg = a.cglob[(size_t)s * a.NC + c];
+      if (cg >= 0) cz_ = cfma(a.cpl_b[(size_t)slot * a.NC + c], z_l2 ? __ldcg(a.z + cg) : a.z[cg], cz_);
+    }
+    u[q] = csub(a.u1b[slot], cz_);
+  }
+  const double2 d = csub(u[0], u[1]);
+  return make_double2(-d.x, -d.y);
+}
+
 // One classical Gram-Schmidt pass over ROWS multiplier rows per block (THREADS / ROWS
 // thread groups):
 //   phase A  w[r] = fused dual-operator tail (gather) or loaded; optional w -= sum_i h_in[i] V_i
@@ -1248,20 +1286,7 @@ __global__ void __launch_bounds__(THREADS) k_cgs_pass(CgsArgs a) {
     double2 w = cz();
     if (act) {
       if (a.gather) {
-        const int slots[2] = {a.lam_lo[r], a.lam_hi[r]};
-        double2 u[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int slot = slots[q], s = slot / a.NB;
-          double2 cz_ = cz();
-          for (int c = 0; c < a.NC; ++c) {
-            const int cg = a.cglob[(size_t)s * a.NC + c];
-            if (cg >= 0) cz_ = cfma(a.cpl_b[(size_t)slot * a.NC + c], a.z[cg], cz_);
-          }
-          u[q] = csub(a.u1b[slot], cz_);
-        }
-        const double2 d = csub(u[0], u[1]);
-        w = make_double2(-d.x, -d.y);
+        w = dual_tail_row(a, r, false);
       } else {
         w = a.w[r];
       }
@@ -1407,6 +1432,306 @@ __global__ void __launch_bounds__(ROWS* GROUPS) k_combine(int n, const double2* 
   double2 sum;
   if (combine_rows<ROWS, GROUPS>(y, V, ldv, n, st->k, r, sum)) t[r] = sum;
 }
+// ---------------------------------------------------------------------------------------
+// Fused Arnoldi tail (one GPU): coarse solve z = C^-1 g, CGS pass 1 (dual-operator tail
+// gathered per row, h1 = V^H w, |w|^2), CGS pass 2 (w -= V h1, h2 = V^H w, |w|^2), Givens
+// and V_{j+1} = (w - V h2) / h_{j+1,j}, in ONE launch.  The three data dependences are grid
+// barriers whose last arriving block performs the reduction (fixed order: deterministic)
+// before releasing the others.  Each thread keeps its RPT multiplier rows of w in
+// registers across the phases and re-reads its V rows from L1.  All blocks must be
+// co-resident (the host sizes RPT from the occupancy API); a barrier that does not complete
+// within ~2 s traps instead of hanging.
+struct ArnoldiTailArgs {
+  int n;  // multiplier rows
+  double2* V;
+  size_t ldv;
+  GmresState* st;
+  double2* part;
+  double2 *h1, *h2;
+  unsigned int* bar;  // [0] arrivals, [1] generation
+  int hcap, vcap;  // h staging capacity (>= nv + 1), basis columns allocated
+  // coarse
+  int nc, coarse_rb;  // rb: coarse rows per block per round (1, 2, 4 or 8)
+  const double2* Cinv;
+  const double2* gcp;        // per-(subdomain, corner) coarse contributions of the dual GEMV
+  const int* corner_slots;   // [nc][4]
+  double2* z;
+  // dual tail gather
+  int NB, NC;
+  const int *lam_lo, *lam_hi, *cglob;
+  const double2 *u1b, *cpl_b;
+  GivensArgs ga;
+  unsigned long long* tstamp;  // optional phase timestamps (block 0), 8 per Arnoldi step
+};
+
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ unsigned int atom_add_release_u32(unsigned int* p, unsigned int v) {
+  unsigned int old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned int* p, unsigned int v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// grid barrier; the last block to arrive runs `last()` (all its threads) before the release.
+// Arrival is a release atomic (cumulative over the block's writes, ordered by the preceding
+// bar.sync), the wait an acquire load: no full fences.
+template <typename F>
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, F&& last, unsigned long long* ts = nullptr) {
+  __shared__ unsigned int gen_sh;
+  __shared__ bool last_sh;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    gen_sh = ld_acquire_u32(bar + 1);
+    last_sh = atom_add_release_u32(bar, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last_sh) {
+    if (ts && threadIdx.x == 0) ts[0] = gtimer();
+    if (threadIdx.x == 0) (void)ld_acquire_u32(bar);  // acquire the other blocks' writes
+    __syncthreads();
+    last();
+    __syncthreads();
+    if (ts && threadIdx.x == 0) ts[1] = gtimer();
+    if (threadIdx.x == 0) {
+      st_relaxed_u32(bar, 0u);
+      atom_add_release_u32(bar + 1, 1u);
+    }
+  } else if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    while (ld_acquire_u32(bar + 1) == gen_sh) {
+      if (clock64() - t0 > 4000000000LL) __trap();  // ~2 s: never hang the device
+    }
+  }
+  __syncthreads();
+}
+
+// Grid barrier on a monotonically increasing 64-bit arrival counter: barrier k of the
+// kernel's lifetime completes when the counter reaches (k+1) G.  Arrival is one acq_rel
+// atomic (release: the block's writes, ordered by the preceding bar.sync; acquire: for the
+// last arriver); the others poll with acquire loads.  No reset step, no generation word.
+__device__ __forceinline__ void grid_sync_plain(unsigned int* bar) {
+  unsigned long long* ctr = reinterpret_cast<unsigned long long*>(bar);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long ticket;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(ticket) : "l"(ctr) : "memory");
+    const unsigned long long target = (ticket / gridDim.x + 1) * gridDim.x;
+    if (ticket + 1 != target) {
+      const long long t0 = clock64();
+      unsigned long long v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        if (clock64() - t0 > 4000000000LL) __trap();  // ~2 s: never hang the device
+      } while (v < target);
+    }
+  }
+  __syncthreads();
+}
+
+// every block: out[i] = sum_b part[i][b] for i < nout, fixed order (identical in all blocks)
+template <int THREADS>
+__device__ __forceinline__ void block_reduce_parts(const double2* __restrict__ part, int G, int nout,
+                                                   double2* out_sh) {
+  constexpr int SEGS = 16, PER = THREADS / SEGS;
+  const int seg = threadIdx.x % SEGS;
+  for (int i0 = 0; i0 < nout; i0 += PER) {
+    const int i = i0 + threadIdx.x / SEGS;
+    double2 t = cz();
+    if (i < nout) {
+      const double2* pp = part + (size_t)i * G;
+#pragma unroll 8
+      for (int bb = seg; bb < G; bb += SEGS) t = cadd(t, __ldcg(pp + bb));
+    }
+#pragma unroll
+    for (int m = SEGS / 2; m > 0; m >>= 1) t = cadd(t, shfl_xor2(t, m));
+    if (seg == 0 && i < nout) out_sh[i] = t;
+  }
+  __syncthreads();
+}
+
+// Fused tail, one multiplier row per thread, THREADS rows per block, one block per SM.
+// dynamic smem: w_sh[THREADS] | h1[hcap] | h2[hcap] | Givens staging[640]
+template <int THREADS, int NCM>
+__global__ void __launch_bounds__(THREADS, 1) k_arnoldi_tail(ArnoldiTailArgs a) {
+  constexpr int WARPS = THREADS / 32, LPR = THREADS / 32;
+  extern __shared__ double2 tail_sh[];
+  double2* w_sh = tail_sh;
+  double2* hs1 = w_sh + THREADS;
+  double2* hs2 = hs1 + a.hcap;
+  double2* stage = hs2 + a.hcap;
+  __shared__ double2 cred[WARPS];
+  __shared__ double inv_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = blockIdx.x * THREADS, r = row0 + threadIdx.x;
+  const bool act = r < a.n;
+  pdl_trigger();
+  pdl_wait();
+  const int nv = a.st->j + 1, nout = nv + 1, G = gridDim.x;
+  const int it = a.st->iterations;
+  if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 0] = gtimer();
+  // dual-tail operands that do not depend on z (loaded before the barrier)
+  double2 u[2] = {cz(), cz()}, cpv[2][NCM];
+  int cgv[2][NCM];
+  if (act) {
+    const int slots[2] = {a.lam_lo[r], a.lam_hi[r]};
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int slot = slots[q], s = slot / a.NB;
+      u[q] = a.u1b[slot];
+#pragma unroll
+      for (int c = 0; c < NCM; ++c) {
+        cgv[q][c] = c < a.NC ? a.cglob[(size_t)s * a.NC + c] : -1;
+        cpv[q][c] = c < a.NC ? a.cpl_b[(size_t)slot * a.NC + c] : cz();
+      }
+    }
+  }
+  // ---- phase 0: z = C^-1 g.  g staged in smem (reusing the w buffer); each warp takes one
+  // coarse row at a time with all of its lane's loads in one batch (clamped addresses) ----
+  {
+    double2* g_sh = w_sh;  // nc <= hcap + THREADS is checked on the host
+    // coarse rhs g = -sum_s gcp over the (up to 4) subdomains of each corner, assembled
+    // redundantly by every block (same order as k_coarse_rhs)
+    for (int k = threadIdx.x; k < a.nc; k += THREADS) {
+      double2 acc = cz();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int slot = a.corner_slots[k * 4 + q];
+        if (slot >= 0) acc = csub(acc, a.gcp[slot]);
+      }
+      g_sh[k] = acc;
+    }
+    __syncthreads();
+    // two warps per coarse row (column halves interleaved by 32), 16 loads per lane in flight
+    constexpr int CB = 16;
+    const int half = warp & 1;
+    for (int base = blockIdx.x * (WARPS / 2); base < a.nc; base += G * (WARPS / 2)) {
+      const int row = base + (warp >> 1);
+      double2 acc = cz();
+      if (row < a.nc) {
+        const double2* cr = a.Cinv + (size_t)row * a.nc;
+        for (int k0 = half * 32 + lane; k0 < a.nc; k0 += 64 * CB) {
+          double2 v[CB];
+#pragma unroll
+          for (int q = 0; q < CB; ++q) v[q] = __ldg(cr + min(k0 + 64 * q, a.nc - 1));
+#pragma unroll
+          for (int q = 0; q < CB; ++q)
+            if (k0 + 64 * q < a.nc) acc = cfma(v[q], g_sh[k0 + 64 * q], acc);
+        }
+      }
+      acc = warp_sum2(acc);
+      if (lane == 0) cred[warp] = acc;
+      __syncthreads();
+      if ((int)threadIdx.x < WARPS / 2 && base + (int)threadIdx.x < a.nc)
+        a.z[base + threadIdx.x] = cadd(cred[2 * threadIdx.x], cred[2 * threadIdx.x + 1]);
+      __syncthreads();
+    }
+  }
+  if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 1] = gtimer();
+  grid_sync_plain(a.bar);
+  if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 2] = gtimer();
+  // block partials of conj(V_i) w (i < nv) and |w|^2 (i = nv), one warp per vector
+  // pass-1 and pass-2 partials live in separate halves of `part`: every block reduces the
+  // pass-1 partials after barrier B while faster blocks already write pass-2 partials
+  auto dots = [&](double2 w, double2* part) {
+    w_sh[threadIdx.x] = w;
+    __syncthreads();
+    for (int i = warp; i < nout; i += WARPS) {
+      double2 acc = cz();
+      if (i < nv) {
+        const double2* v = a.V + (size_t)i * a.ldv + row0;
+        double2 x[LPR];
+#pragma unroll
+        for (int q = 0; q < LPR; ++q) x[q] = v[min(lane + 32 * q, a.n - 1 - row0)];
+#pragma unroll
+        for (int q = 0; q < LPR; ++q) acc = cfma_conj(x[q], w_sh[lane + 32 * q], acc);
+      } else {
+#pragma unroll
+        for (int q = 0; q < LPR; ++q) acc.x += cabs2(w_sh[lane + 32 * q]);
+      }
+      acc = warp_sum2(acc);
+      if (lane == 0) part[(size_t)i * G + blockIdx.x] = acc;
+    }
+  };
+  double2* part2 = a.part + (size_t)a.hcap * G;
+  auto sub_vh = [&](double2 w, const double2* h) {  // w - sum_i h_i V_i[r], h in smem
+    if (!act) return w;
+    double2 acc = cz();
+    int i = 0;
+    for (; i + 8 <= nv; i += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = a.V[(size_t)(i + q) * a.ldv + r];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc = cfma(h[i + q], v[q], acc);
+    }
+    for (; i < nv; ++i) acc = cfma(h[i], a.V[(size_t)i * a.ldv + r], acc);
+    return csub(w, acc);
+  };
+  // ---- phase 1: w = F z (dual tail), h1 = V^H w, |w|^2 ----
+  double2 w = cz();
+  if (act) {
+    double2 ud[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      double2 cz_ = cz();
+#pragma unroll
+      for (int c = 0; c < NCM; ++c)
+        if (cgv[q][c] >= 0) cz_ = cfma(cpv[q][c], __ldcg(a.z + cgv[q][c]), cz_);
+      ud[q] = csub(u[q], cz_);
+    }
+    const double2 d = csub(ud[0], ud[1]);
+    w = make_double2(-d.x, -d.y);
+  }
+  dots(w, a.part);
+  if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 3] = gtimer();
+  grid_sync_plain(a.bar);
+  block_reduce_parts<THREADS>(a.part, G, nout, hs1);
+  if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 4] = gtimer();
+  // ---- phase 2: w -= V h1, h2 = V^H w, |w|^2 ----
+  w = sub_vh(w, hs1);
+  if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 5] = gtimer();
+  __syncthreads();  // w_sh reuse
+  dots(w, part2);
+  if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 6] = gtimer();
+  grid_sync_plain(a.bar);
+  block_reduce_parts<THREADS>(part2, G, nout, hs2);
+  if (warp == 0) {
+    bool finite;
+    const double hn = warp_hnext<true>(hs1, hs2, nv - 1, finite);
+    if (lane == 0) inv_sh = 1.0 / hn;
+  }
+  __syncthreads();
+  if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 7] = gtimer();
+  // ---- phase 3: V_{j+1} = (w - V h2) / h_{j+1,j} (written even if the cycle stops: unused) ----
+  if (nv < a.vcap) {
+    w = sub_vh(w, hs2);
+    if (act) a.V[(size_t)nv * a.ldv + r] = cscale(w, inv_sh);
+  }
+  if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 8] = gtimer();
+  // block 0: Givens, stopping tests, WHILE-node condition; h1/h2 published for the host side
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < nout; i += THREADS) {
+      a.h1[i] = hs1[i];
+      a.h2[i] = hs2[i];
+    }
+    if (warp == 0) givens_warp<true>(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384, hs1, hs2);
+    if (a.tstamp && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 9] = gtimer();
+  }
+}
+
 // y = a - b ;  y = a + b
 __global__ void k_sub(int n, const double2* a, const double2* b, double2* y) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
