@@ -146,7 +146,7 @@ struct Ctx {
   int arnoldi_body_kernels = 0;
   static constexpr int kCgsThreads = 512, kCgsRows = 256;  // k_cgs_pass block shape
   // fused Arnoldi tail (k_arnoldi_tail): rows per thread (0 = off), grid, barrier words
-  int tail_rpt = 0, tail_grid = 0, tail_rb = 1;
+  int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_minb = 1;
   unsigned int* d_bar = nullptr;
   unsigned long long* d_tstamp = nullptr;  // FETIGPU_TAIL_TIMES=1: per-phase timestamps
   int mdot_blocks = 0, mdot_chunk = 0;
@@ -361,8 +361,10 @@ struct Ctx {
     if (smem > 200 * 1024) return;
     int sms = 0, per_sm = 0;
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc.device));
-    CU(cudaFuncSetAttribute(k_arnoldi_tail<kTailThreads, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_arnoldi_tail<kTailThreads, 4>, kTailThreads, smem));
+    if (const char* e = std::getenv("FETIGPU_TAIL_MINB")) tail_minb = std::atoi(e) == 2 ? 2 : 1;
+    auto kfn = tail_minb == 2 ? k_arnoldi_tail<kTailThreads, 4, 2> : k_arnoldi_tail<kTailThreads, 4, 1>;
+    CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTailThreads, smem));
     const int grid = std::max(1, cdiv(nown, kTailThreads));
     if (per_sm <= 0 || grid > per_sm * sms) return;
     tail_rpt = 1;
@@ -1081,7 +1083,12 @@ struct Ctx {
       t.tstamp = d_tstamp;
       t.hcap = vcap + 2;
       t.vcap = vcap;
-      launch(FETIGPU_K_ORTHO, [&] { kx(k_arnoldi_tail<kTailThreads, 4>, tail_grid, kTailThreads, tail_smem(), t); });
+      launch(FETIGPU_K_ORTHO, [&] {
+        if (tail_minb == 2)
+          kx(k_arnoldi_tail<kTailThreads, 4, 2>, tail_grid, kTailThreads, tail_smem(), t);
+        else
+          kx(k_arnoldi_tail<kTailThreads, 4, 1>, tail_grid, kTailThreads, tail_smem(), t);
+      });
       mark(6);
       return;
     }

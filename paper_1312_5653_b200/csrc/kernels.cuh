@@ -1564,8 +1564,8 @@ __device__ __forceinline__ void block_reduce_parts(const double2* __restrict__ p
 
 // Fused tail, one multiplier row per thread, THREADS rows per block, one block per SM.
 // dynamic smem: w_sh[THREADS] | h1[hcap] | h2[hcap] | Givens staging[640]
-template <int THREADS, int NCM>
-__global__ void __launch_bounds__(THREADS, 1) k_arnoldi_tail(ArnoldiTailArgs a) {
+template <int THREADS, int NCM, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs a) {
   constexpr int WARPS = THREADS / 32, LPR = THREADS / 32;
   extern __shared__ double2 tail_sh[];
   double2* w_sh = tail_sh;
