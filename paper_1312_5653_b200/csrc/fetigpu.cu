@@ -1388,7 +1388,8 @@ struct Ctx {
         return 16.0 * (S * sym_tile_entries(NT) + 2.0 * S * NB) + 12.0 * S * NB;
       case FETIGPU_K_DUAL_GEMV:  // packed S_bb^-1 + coupling_b + vectors
         return 16.0 * (S * sym_tile_entries(NT) + S * NB * H.NC + 3.0 * S * NB + S * H.NC) + 12.0 * S * NB;
-      case FETIGPU_K_BAND:  // one single-RHS solve: both factor sweeps + vector in/out
+      case FETIGPU_K_BAND:  // one single-RHS interior solve: factor records of both sweeps + vector in/out
+        if (use_bt) return 16.0 * (S * (2.0 * bt_nb - 1.0) * BT_HALF + 3.0 * S * H.NI);
         return 16.0 * (2.0 * S * H.NI * (Wt + 1) + 3.0 * S * H.NI);
       case FETIGPU_K_COARSE:
         return 16.0 * ((double)nc * nc + 2.0 * nc);

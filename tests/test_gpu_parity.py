@@ -184,3 +184,28 @@ def test_wide_bands_match_oracle(fetigpu, oracle_mod, n, s):
     assert rel(x, xo) <= 1e-8
     assert abs(st["iterations"] - so["iterations"]) <= 2
     gpu.close()
+
+
+def test_plane_strain_matches_oracle(fetigpu, oracle_mod):
+    """Plane-strain elasticity (dpn = 2, clamped x = 0, fem.cpp:83-128):
+    W = 64 interior bands (banded substitution path), 8 corner dofs per subdomain, free
+    top/bottom/right boundaries (ragged interiors).  Operators to 1e-12, Schur solve to 1e-8."""
+    n_x, n_y, s_x, s_y, phi = 48, 32, 6, 4, 1e-4
+    p = fetigpu.make_problem(n_x, n_y, phi, physics=1, len_x=1.5, len_y=1.0, young=1.0, poisson=0.3)
+    op = oracle_mod.Problem(n_x, n_y, len_x=1.5, len_y=1.0, physics=1, young=1.0, poisson=0.3)
+    assert op.n == p.n
+    rng = np.random.default_rng(3)
+    ybar = rng.standard_normal(p.n)
+    ref = op.schur_solve(s_x, s_y, phi, ybar, None, tol=1e-10, max_iter=2000, threads=4)
+    solver = fetigpu.SchurSolver(p, s_x, s_y, tol=1e-10, max_iter=2000)
+    out = solver.solve(ybar, np.zeros(p.m))  # y_c = 0 (None would take the problem's trace)
+    feti = oracle_mod.Feti(op, s_x, s_y, -1j / np.sqrt(phi), tol=1e-10, max_iter=2000)
+    lam = rng.uniform(-1, 1, feti.n_lambda) + 1j * rng.uniform(-1, 1, feti.n_lambda)
+    assert rel(solver.apply_dual_operator(lam), feti.apply_dual_operator(lam)) <= 1e-12
+    assert rel(solver.apply_dirichlet_preconditioner(lam), feti.apply_dirichlet_preconditioner(lam)) <= 1e-12
+    solver.close()
+    assert out["converged"]
+    for k in ("y", "u", "lambda"):
+        assert rel(out[k], ref[k]) <= 1e-8, k
+    assert abs(out["plus_stats"]["iterations"] - ref["plus_stats"]["iterations"]) <= 2
+    assert abs(out["minus_stats"]["iterations"] - ref["minus_stats"]["iterations"]) <= 2
