@@ -121,6 +121,11 @@ struct Ctx {
   double *d_in_ybar = nullptr, *d_in_yc = nullptr, *d_out_y = nullptr, *d_out_u = nullptr, *d_out_l = nullptr;
   double *d_real0 = nullptr, *d_real1 = nullptr, *d_real2 = nullptr, *d_real3 = nullptr, *d_real4 = nullptr;
   double2* h_pin = nullptr;
+  // asynchronous statistics: (|x|^2, max|x|) slots filled on the stream, read after the
+  // call's single final synchronisation (rhs norms, interface jumps, primal residuals,
+  // imaginary leak, |lambda|_inf)
+  static constexpr int kStatSlots = 16;
+  double2 *d_stat = nullptr, *h_stat = nullptr;
   size_t ldv = 0;
   int vcap = 0;  // basis vectors allocated
   GmresState* d_gst = nullptr;
@@ -163,6 +168,7 @@ struct Ctx {
     }
     for (void* p : allocs) cudaFree(p);
     if (h_pin) cudaFreeHost(h_pin);
+    if (h_stat) cudaFreeHost(h_stat);
     if (h_gst) cudaFreeHost(h_gst);
     if (arnoldi_exec) cudaGraphExecDestroy(arnoldi_exec);
     if (arnoldi_graph) cudaGraphDestroy(arnoldi_graph);
@@ -663,6 +669,8 @@ struct Ctx {
     d_out_u = alloc<double>(n);
     d_out_l = alloc<double>(n);
     CU(cudaMallocHost(&h_pin, sizeof(double2) * 3 * (vcap + 4)));
+    CU(cudaMallocHost(&h_stat, sizeof(double2) * kStatSlots));
+    d_stat = alloc<double2>(kStatSlots);
     setup_mass();
     setup_stencil();
     setup_l2_persistence();
@@ -1016,6 +1024,28 @@ struct Ctx {
     });
   }
 
+  // (|x|^2, max|x|) -> d_stat[slot] on the stream (no synchronisation); sharded = all ranks
+  void norm_async(const double2* x, int len, int slot, bool sharded = false) {
+    const int blocks = std::max(1, std::min(296, cdiv(std::max(len, 1), 256)));
+    launch(FETIGPU_K_OTHER, [&] { k_norm_max_part<<<blocks, 256, 0, stream>>>(len, x, d_part); });
+    launch(FETIGPU_K_OTHER, [&] { k_norm_max_final<<<1, 32, 0, stream>>>(blocks, d_part, d_stat + slot); });
+    if (sharded && dist()) {
+      double* r = reinterpret_cast<double*>(d_stat + slot);
+      comm->allreduce_sum(r, 1, stream);
+      comm->allreduce_max(r + 1, 1, stream);
+    }
+  }
+  // queue the copy of all statistic slots; valid in h_stat after the next sync()
+  void stats_to_host() {
+    CU(cudaMemcpyAsync(h_stat, d_stat, sizeof(double2) * kStatSlots, cudaMemcpyDeviceToHost, stream));
+  }
+  // slots of one FETI solve: base + 0 rhs, + 1 interface jump, + 2 primal residual
+  void finalize_feti_stats(fetigpu_feti_stats& st, int base) const {
+    const double rn = std::sqrt(h_stat[base].x);
+    st.interface_jump = H.n_lambda > 0 ? h_stat[base + 1].y : 0.0;
+    st.primal_residual = rn > 0.0 ? std::sqrt(h_stat[base + 2].x) / rn : 0.0;
+  }
+
   // |x|^2 and max|x| of a complex vector -> host (synchronizes); sharded = over all ranks
   std::pair<double, double> norm_max(const double2* x, int len, bool sharded = false) {
     const int blocks = std::max(1, std::min(296, cdiv(std::max(len, 1), 256)));
@@ -1270,20 +1300,17 @@ struct Ctx {
 
   // ------------------------------------------------------------------------ FETI solve
   // (K + mc V) x = rhs on device vectors (feti.cpp:630-717)
-  fetigpu_feti_stats feti_solve(const double2* rhs, double2* x) {
+  // Statistics that need reductions (primal residual, interface jump) are left in d_stat
+  // slots [sb, sb + 3) and filled by finalize_feti_stats() after the caller's final sync.
+  // A zero rhs needs no special case: the jump d is zero, GMRES returns x = 0 in 0
+  // iterations (feti.cpp:640-644) and the recovery yields x = 0.
+  fetigpu_feti_stats feti_solve(const double2* rhs, double2* x, int sb = 0) {
     auto t0 = std::chrono::steady_clock::now();
     fetigpu_feti_stats st{};
     st.n_lambda = nl;
     st.coarse_dim = nc;
     st.setup_seconds = setup_seconds;
-    const double rn = norm_max(rhs, n).first;
-    if (rn == 0.0) {
-      zero(x, n);
-      st.converged = 1;
-      sync();
-      st.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      return st;
-    }
+    norm_async(rhs, n, sb);
     const int S = H.n_sub, NI = H.NI, NB = H.NB;
     launch(FETIGPU_K_OTHER, [&] {
       k_split_rhs<<<cdiv((long long)S * (NI + NB), 256), 256, 0, stream>>>(L, d_idof, d_bdof, rhs, d_fi, d_fb);
@@ -1318,21 +1345,21 @@ struct Ctx {
     launch(FETIGPU_K_LAMBDA, [&] {
       k_jump<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_lam_lo + own0, d_lam_hi + own0, d_u1b, d_d + own0);
     });
-    st.interface_jump = H.n_lambda > 0 ? norm_max(d_d + own0, nown, true).second : 0.0;
+    if (H.n_lambda > 0) norm_async(d_d + own0, nown, sb + 1, true);
     apply_global<double2>(x, nullptr, 1.0, mc, d_ax);
     launch(FETIGPU_K_GLOBAL, [&] { k_sub<<<cdiv(n, 256), 256, 0, stream>>>(n, d_ax, rhs, d_ax); });
-    st.primal_residual = norm_max(d_ax, n).first / rn;
+    norm_async(d_ax, n, sb + 2);
     st.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return st;
   }
 
   // sign = -1 solves with conj(K + mc V) = K + conj(mc) V
   fetigpu_feti_stats feti_solve_signed(int sign, const double2* rhs, double2* x) {
-    if (sign == 1) return feti_solve(rhs, x);
+    if (sign == 1) return feti_solve(rhs, x, 0);
     launch(FETIGPU_K_OTHER, [&] { k_conj<<<cdiv(n, 256), 256, 0, stream>>>(n, rhs, d_x2); });
     // d_x2 is used as the conjugated rhs; copy to d_rhs workspace to keep d_x2 free
     CU(cudaMemcpyAsync(d_rhs, d_x2, n * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
-    auto st = feti_solve(d_rhs, d_x2);
+    auto st = feti_solve(d_rhs, d_x2, 0);
     launch(FETIGPU_K_OTHER, [&] { k_conj<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x2, x); });
     return st;
   }
@@ -1346,16 +1373,19 @@ struct Ctx {
     apply_global<double>(ybar, (yc && m > 0) ? yc : nullptr, 1.0, 0.0, d_real0);
     launch(FETIGPU_K_GLOBAL, [&] { k_real_to_complex<<<cdiv(n, 256), 256, 0, stream>>>(n, d_real0, d_rhs); });
     // a = (K + cV)^-1 rhs
-    const fetigpu_feti_stats sp = feti_solve(d_rhs, d_x);
+    fetigpu_feti_stats sp = feti_solve(d_rhs, d_x, 0);
     // second factor: (K - cV) t = V a  <=>  t = conj((K + cV)^-1 conj(V a)) = conj(FETI(V conj(a)))
     launch(FETIGPU_K_OTHER, [&] { k_conj<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x, d_x2); });
     apply_global<double2>(d_x2, nullptr, 0.0, 1.0, d_rhs);
-    const fetigpu_feti_stats sm = feti_solve(d_rhs, d_x);
+    fetigpu_feti_stats sm = feti_solve(d_rhs, d_x, 4);
     // lambda = Re t = Re t'; imag leak = max |Im t'|
     launch(FETIGPU_K_GLOBAL, [&] { k_realify<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x, lam); });
     const int blocks = std::max(1, std::min(296, cdiv(n, 256)));
     launch(FETIGPU_K_GLOBAL, [&] {
       k_imag_max_part<<<blocks, 256, 0, stream>>>(n, d_x, reinterpret_cast<double*>(d_part));
+    });
+    launch(FETIGPU_K_GLOBAL, [&] {
+      k_max_final<<<1, 32, 0, stream>>>(blocks, reinterpret_cast<const double*>(d_part), d_stat + 8);
     });
     // y = ybar - V^-1 K lambda ; u = lambda / phi  (control.cpp:323-325)
     apply_global<double>(lam, nullptr, 1.0, 0.0, d_real1);
@@ -1363,13 +1393,14 @@ struct Ctx {
     launch(FETIGPU_K_GLOBAL, [&] {
       k_recover_yu<<<cdiv(n, 256), 256, 0, stream>>>(n, ybar, d_real1, lam, 1.0 / phi, y, u);
     });
-    std::vector<double> parts(blocks);
-    CU(cudaMemcpyAsync(parts.data(), d_part, blocks * sizeof(double), cudaMemcpyDeviceToHost, stream));
     // |lambda|_inf for the leak warning
     launch(FETIGPU_K_GLOBAL, [&] { k_real_to_complex<<<cdiv(n, 256), 256, 0, stream>>>(n, lam, d_ax); });
-    const double lmax = norm_max(d_ax, n).second;  // syncs
-    double leak = 0;
-    for (double v : parts) leak = std::max(leak, v);
+    norm_async(d_ax, n, 9);
+    stats_to_host();
+    sync();  // the call's one final synchronisation
+    finalize_feti_stats(sp, 0);
+    finalize_feti_stats(sm, 4);
+    const double lmax = h_stat[9].y, leak = h_stat[8].y;
     if (out) {
       out->plus = sp;
       out->minus = sm;
@@ -1632,7 +1663,9 @@ int fetigpu_feti_solve(fetigpu_ctx* ctx, int sign, const double* rhs_c128, doubl
     CU(cudaMemcpyAsync(c.d_api_rhs, rhs_c128, bytes, cudaMemcpyHostToDevice, c.stream));
     auto st = c.feti_solve_signed(sign, c.d_api_rhs, c.d_api_x);
     CU(cudaMemcpyAsync(x_c128, c.d_api_x, bytes, cudaMemcpyDeviceToHost, c.stream));
+    c.stats_to_host();
     c.sync();
+    c.finalize_feti_stats(st, 0);
     if (stats) *stats = st;
     c.prof_collect();
   });

@@ -1773,6 +1773,14 @@ __global__ void k_norm_max_final(int nblk, const double2* __restrict__ part, dou
   if (threadIdx.x == 0) *out = make_double2(s, m);
 }
 
+// max over block partials of k_imag_max_part -> out->y (out->x = 0)
+__global__ void k_max_final(int nblk, const double* __restrict__ part, double2* __restrict__ out) {
+  double m = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += 32) m = fmax(m, part[b]);
+  m = warp_max(m);
+  if (threadIdx.x == 0) *out = make_double2(0.0, m);
+}
+
 // ------------------------------------------------------------------ global operators (K8)
 // y = kc K x + mc V x (+ K_c xc) matrix-free over the Q1 elements around each free dof.
 // Real or complex vectors (T = double or double2); coefficients complex.
