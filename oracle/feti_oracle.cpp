@@ -26,8 +26,9 @@
 //   PartialPivLU  -> dense LU with partial pivoting
 //   SimplicialLLT -> banded Cholesky (small n) / Jacobi-PCG to 1e-15 (large n)
 // Any exact solve agrees with Eigen's to rounding.
-// Edge-RBM augmentation (feti.cpp:171-242) is not restated: the north_star path
-// is the corner-only coarse space (augment=false).
+//   augmentation: src/feti.cpp:132-167 (edges), 171-242 (edge-RBM columns), 394-454
+//                 (augmented coupling / coarse), 516-556 (eliminate), 572-578 + 655-662
+//                 (dual-space projection) — the `augment` option.
 // =============================================================================
 #include <algorithm>
 #include <chrono>
@@ -330,10 +331,17 @@ struct Sub {
       lambda_rows;
   RVec lambda_signs, weights;
 };
+struct Edge {  // feti.hpp:59-65: open segment between subdomain-grid vertices
+  int sub_lo = 0, sub_hi = 0;
+  bool vertical = false;
+  std::vector<int> nodes, lambda_rows;  // dpn rows per node
+};
 struct Partition {
   int sx = 0, sy = 0, ex = 0, ey = 0, dpn = 1, n_free = 0, n_corner = 0, n_lambda = 0, n_edges = 0;
+  double h = 0;
   std::vector<Sub> subs;
   std::vector<int> free_mult;
+  std::vector<Edge> edges;
 };
 static std::pair<int, int> owner_range(int i, int e, int ns) {
   const int lo = (i == 0) ? 0 : (i - 1) / e;
@@ -420,22 +428,93 @@ static Partition partition_structured(const Problem& P, int sx, int sy) {
           }
         }
     }
-  // edges (feti.cpp:132-167): count the non-empty open segments
+  // edges (feti.cpp:132-167): vertical cuts first (row q, cut p), then horizontal cuts;
+  // only free nodes strictly inside the segment; empty segments are dropped
+  part.h = P.h;
+  auto add_edge = [&](Edge e) {
+    for (int node : e.nodes)
+      for (int c = 0; c < dpn; ++c) e.lambda_rows.push_back(lambda_of[node * dpn + c]);
+    if (!e.nodes.empty()) part.edges.push_back(std::move(e));
+  };
   for (int q = 0; q < sy; ++q)
     for (int p = 1; p < sx; ++p) {
-      int cnt = 0;
+      Edge e;
+      e.vertical = true;
+      e.sub_lo = q * sx + p - 1;
+      e.sub_hi = q * sx + p;
       for (int j = q * ey + 1; j < (q + 1) * ey; ++j)
-        if (P.free_map[P.node_id(p * ex, j) * dpn] >= 0) ++cnt;
-      if (cnt) ++part.n_edges;
+        if (P.free_map[P.node_id(p * ex, j) * dpn] >= 0) e.nodes.push_back(P.node_id(p * ex, j));
+      add_edge(std::move(e));
     }
   for (int q = 1; q < sy; ++q)
     for (int p = 0; p < sx; ++p) {
-      int cnt = 0;
+      Edge e;
+      e.vertical = false;
+      e.sub_lo = (q - 1) * sx + p;
+      e.sub_hi = q * sx + p;
       for (int i = p * ex + 1; i < (p + 1) * ex; ++i)
-        if (P.free_map[P.node_id(i, q * ey) * dpn] >= 0) ++cnt;
-      if (cnt) ++part.n_edges;
+        if (P.free_map[P.node_id(i, q * ey) * dpn] >= 0) e.nodes.push_back(P.node_id(i, q * ey));
+      add_edge(std::move(e));
     }
+  part.n_edges = (int)part.edges.size();
   return part;
+}
+
+// ------------------------------------------- edge-RBM augmentation (feti.cpp:171-242)
+// One normalised column per edge for scalar physics (the edge mean); for plane strain the
+// two translations and the in-plane rotation about the edge midpoint.
+struct AugColumn {
+  std::vector<int> rows;
+  RVec values;
+};
+static std::vector<AugColumn> edge_rbm_columns(const Partition& part) {
+  std::vector<AugColumn> cols;
+  for (size_t e = 0; e < part.edges.size(); ++e) {
+    const Edge& ed = part.edges[e];
+    const int nn = (int)ed.nodes.size();
+    std::vector<AugColumn> mine;
+    if (part.dpn == 1) {
+      AugColumn c;
+      c.rows = ed.lambda_rows;
+      c.values.assign(nn, 1.0);
+      mine.push_back(std::move(c));
+    } else {
+      AugColumn tx, ty, rot;
+      for (int k = 0; k < nn; ++k) {
+        const int rx = ed.lambda_rows[2 * k], ry = ed.lambda_rows[2 * k + 1];
+        tx.rows.push_back(rx);
+        tx.values.push_back(1.0);
+        ty.rows.push_back(ry);
+        ty.values.push_back(1.0);
+        const double arm = (k - 0.5 * (nn - 1)) * part.h;  // offset from the edge midpoint
+        rot.rows.push_back(ed.vertical ? rx : ry);
+        rot.values.push_back(ed.vertical ? -arm : arm);
+      }
+      mine.push_back(std::move(tx));
+      mine.push_back(std::move(ty));
+      mine.push_back(std::move(rot));
+    }
+    for (auto& c : mine) {
+      double n2 = 0;
+      for (double v : c.values) n2 += v * v;
+      if (!(n2 > 0.0))
+        throw NumericalError("build_edge_rbm_augmentation: dependent (zero) column on edge " + std::to_string(e) +
+                             "; H/h too small for a rotation mode");
+      const double inv = 1.0 / std::sqrt(n2);
+      for (double& v : c.values) v *= inv;
+    }
+    for (size_t a = 0; a < mine.size(); ++a)
+      for (size_t b = a + 1; b < mine.size(); ++b) {
+        double dot = 0;
+        for (size_t i = 0; i < mine[a].rows.size(); ++i)
+          for (size_t j = 0; j < mine[b].rows.size(); ++j)
+            if (mine[a].rows[i] == mine[b].rows[j]) dot += mine[a].values[i] * mine[b].values[j];
+        if (std::abs(dot) > 1e-12)
+          throw NumericalError("build_edge_rbm_augmentation: dependent columns on edge " + std::to_string(e));
+      }
+    for (auto& c : mine) cols.push_back(std::move(c));
+  }
+  return cols;
 }
 
 // --------------------------------------- banded LU with partial pivoting (zgbtf2/zgbtrs)
@@ -682,7 +761,12 @@ struct Block {
   std::vector<std::tuple<int, int, cd>> arc, aib, abb;  // A_rc (n_r x n_c), A_ib, A_bb
   CVec acc;                                             // n_c x n_c row-major
   BandLU arr, aii;
-  CVec coupling;  // n_r x n_c row-major: A_rr^{-1} A_rc
+  // augmentation columns touching this subdomain (feti.cpp:394-412): global column ids and
+  // their (r-position, sign * value) entries C^s = Q^T B^s
+  std::vector<int> active_aug;
+  std::vector<std::vector<std::pair<int, double>>> aug_entries;
+  int nz = 0;     // local coarse unknowns: n_c corners + active augmentation columns
+  CVec coupling;  // n_r x nz row-major: A_rr^{-1} [A_rc | C^T]
 };
 
 struct FetiStats {
@@ -698,6 +782,9 @@ struct Feti {
   double tol = 1e-10;
   int max_iter = 1000, threads = 1;
   std::vector<Block> blk;
+  bool augment = false;
+  std::vector<AugColumn> aug;  // edge-RBM columns (augment = true)
+  int ncg = 0;                 // corner dofs; coarse = [corners | augmentation columns]
   int nc = 0;
   CVec coarse;  // nc x nc row-major
   RVec cscale;
@@ -776,41 +863,79 @@ struct Feti {
       if (!f.empty()) throw NumericalError("assemble_subdomain_operators: " + f);
   }
 
-  void setup() {  // feti.cpp:373-480 with augment=false (n_q = 0)
+  void setup() {  // feti.cpp:373-480
     auto t0 = std::chrono::steady_clock::now();
     assemble();
-    nc = part.n_corner;
+    if (augment) aug = edge_rbm_columns(part);
+    ncg = part.n_corner;
+    const int nq = (int)aug.size();
+    nc = ncg + nq;
     const int ns = (int)part.subs.size();
+    // lambda row -> (r-position, sign) of each subdomain, for C^s = Q^T B^s (feti.cpp:394-406)
     std::vector<CVec> contrib(ns);
     parallel_for(ns, threads, [&](int s) {
       const Sub& sub = part.subs[s];
       Block& B = blk[s];
       const int nr = (int)sub.r_local.size(), nc_ = (int)sub.corner_local.size();
-      B.coupling.assign((size_t)nr * nc_, cd(0));
-      if (nc_ == 0) return;
-      CVec col(nr);
-      for (int c = 0; c < nc_; ++c) {
-        std::fill(col.begin(), col.end(), cd(0));
-        for (auto& [i, j, v] : B.arc)
-          if (j == c) col[i] += v;
-        B.arr.solve(col.data());
-        for (int i = 0; i < nr; ++i) B.coupling[(size_t)i * nc_ + c] = col[i];
+      std::vector<std::pair<int, int>> row_of;  // sorted (lambda row, k)
+      for (size_t k = 0; k < sub.lambda_rows.size(); ++k) row_of.emplace_back(sub.lambda_rows[k], (int)k);
+      std::sort(row_of.begin(), row_of.end());
+      for (int q = 0; q < nq; ++q) {
+        std::vector<std::pair<int, double>> ent;
+        for (size_t k = 0; k < aug[q].rows.size(); ++k) {
+          auto it = std::lower_bound(row_of.begin(), row_of.end(), std::make_pair(aug[q].rows[k], -1));
+          if (it != row_of.end() && it->first == aug[q].rows[k]) {
+            const int kk = it->second;
+            ent.emplace_back(sub.r_boundary[kk], sub.lambda_signs[kk] * aug[q].values[k]);
+          }
+        }
+        if (!ent.empty()) {
+          B.active_aug.push_back(q);
+          B.aug_entries.push_back(std::move(ent));
+        }
       }
-      // contribs = coupling_rhs^T * coupling_solved  (transpose, not adjoint: feti.cpp:433)
-      contrib[s].assign((size_t)nc_ * nc_, cd(0));
-      for (auto& [i, a, v] : B.arc)
-        for (int b = 0; b < nc_; ++b) contrib[s][(size_t)a * nc_ + b] += v * B.coupling[(size_t)i * nc_ + b];
+      const int na = (int)B.active_aug.size();
+      B.nz = nc_ + na;
+      B.coupling.assign((size_t)nr * B.nz, cd(0));
+      if (B.nz == 0) return;
+      // coupling rhs columns [A_rc | C^T] (sparse), solved with A_rr
+      auto rhs_col = [&](int c, CVec& col) {
+        std::fill(col.begin(), col.end(), cd(0));
+        if (c < nc_) {
+          for (auto& [i, j, v] : B.arc)
+            if (j == c) col[i] += v;
+        } else {
+          for (auto& [rp, v] : B.aug_entries[c - nc_]) col[rp] += v;
+        }
+      };
+      CVec col(nr);
+      for (int c = 0; c < B.nz; ++c) {
+        rhs_col(c, col);
+        B.arr.solve(col.data());
+        for (int i = 0; i < nr; ++i) B.coupling[(size_t)i * B.nz + c] = col[i];
+      }
+      // contribs = rhs^T * coupling_solved  (transpose, not adjoint: feti.cpp:433)
+      contrib[s].assign((size_t)B.nz * B.nz, cd(0));
+      for (int a = 0; a < B.nz; ++a) {
+        rhs_col(a, col);
+        for (int i = 0; i < nr; ++i)
+          if (col[i] != cd(0))
+            for (int b = 0; b < B.nz; ++b) contrib[s][(size_t)a * B.nz + b] += col[i] * B.coupling[(size_t)i * B.nz + b];
+      }
     });
     coarse.assign((size_t)nc * nc, cd(0));
     for (int s = 0; s < ns; ++s) {
       const Sub& sub = part.subs[s];
+      const Block& B = blk[s];
       const int nc_ = (int)sub.corner_local.size();
+      std::vector<int> zidx(B.nz);
+      for (int k = 0; k < nc_; ++k) zidx[k] = sub.corner_global[k];
+      for (size_t a = 0; a < B.active_aug.size(); ++a) zidx[nc_ + a] = ncg + B.active_aug[a];
       for (int k = 0; k < nc_; ++k)
         for (int l = 0; l < nc_; ++l)
-          coarse[(size_t)sub.corner_global[k] * nc + sub.corner_global[l]] += blk[s].acc[(size_t)k * nc_ + l];
-      for (int a = 0; a < nc_; ++a)
-        for (int b = 0; b < nc_; ++b)
-          coarse[(size_t)sub.corner_global[a] * nc + sub.corner_global[b]] -= contrib[s][(size_t)a * nc_ + b];
+          coarse[(size_t)sub.corner_global[k] * nc + sub.corner_global[l]] += B.acc[(size_t)k * nc_ + l];
+      for (int a = 0; a < B.nz; ++a)
+        for (int b = 0; b < B.nz; ++b) coarse[(size_t)zidx[a] * nc + zidx[b]] -= contrib[s][(size_t)a * B.nz + b];
     }
     if (nc > 0) {  // feti.cpp:456-475
       cscale.resize(nc);
@@ -830,6 +955,15 @@ struct Feti {
     setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
 
+  // v -= Q Q^T v, column by column (feti.cpp:572-578)
+  void project_out_augmentation(CVec& v) const {
+    for (const auto& c : aug) {
+      cd coef = 0;
+      for (size_t k = 0; k < c.rows.size(); ++k) coef += c.values[k] * v[c.rows[k]];
+      for (size_t k = 0; k < c.rows.size(); ++k) v[c.rows[k]] -= coef * c.values[k];
+    }
+  }
+
   CVec coarse_solve(const CVec& g) const {  // feti.cpp:483-490
     if (nc == 0) return {};
     CVec z = g;
@@ -842,7 +976,7 @@ struct Feti {
   void split_rhs(const CVec& rhs, std::vector<CVec>& fr, CVec& fc) const {  // 493-510
     const int ns = (int)part.subs.size();
     fr.resize(ns);
-    fc.assign(nc, cd(0));
+    fc.assign(ncg, cd(0));
     for (int s = 0; s < ns; ++s) {
       const Sub& sub = part.subs[s];
       fr[s].resize(sub.r_local.size());
@@ -862,28 +996,36 @@ struct Feti {
       blk[s].arr.solve(u1[s].data());
     });
     CVec g(nc, cd(0));
-    for (int i = 0; i < nc; ++i) g[i] = fc[i];
+    for (int i = 0; i < ncg; ++i) g[i] = fc[i];
     for (int s = 0; s < ns; ++s) {
       const Sub& sub = part.subs[s];
+      const Block& B = blk[s];
       const int nc_ = (int)sub.corner_local.size();
       if (nc_ > 0) {
         CVec v(nc_, cd(0));
-        for (auto& [i, c, val] : blk[s].arc) v[c] += val * u1[s][i];
+        for (auto& [i, c, val] : B.arc) v[c] += val * u1[s][i];
         for (int k = 0; k < nc_; ++k) g[sub.corner_global[k]] -= v[k];
+      }
+      for (size_t a = 0; a < B.active_aug.size(); ++a) {
+        cd acc = 0;
+        for (auto& [rp, val] : B.aug_entries[a]) acc += val * u1[s][rp];
+        g[ncg + B.active_aug[a]] -= acc;
       }
     }
     z = coarse_solve(g);
     ur.resize(ns);
     parallel_for(ns, threads, [&](int s) {
       const Sub& sub = part.subs[s];
+      const Block& B = blk[s];
       const int nc_ = (int)sub.corner_local.size(), nr = (int)sub.r_local.size();
       ur[s] = std::move(u1[s]);
-      if (nc_ > 0) {
-        CVec zl(nc_);
+      if (B.nz > 0) {
+        CVec zl(B.nz);
         for (int k = 0; k < nc_; ++k) zl[k] = z[sub.corner_global[k]];
+        for (size_t a = 0; a < B.active_aug.size(); ++a) zl[nc_ + a] = z[ncg + B.active_aug[a]];
         for (int i = 0; i < nr; ++i) {
           cd acc = 0;
-          for (int k = 0; k < nc_; ++k) acc += blk[s].coupling[(size_t)i * nc_ + k] * zl[k];
+          for (int k = 0; k < B.nz; ++k) acc += B.coupling[(size_t)i * B.nz + k] * zl[k];
           ur[s][i] -= acc;
         }
       }
@@ -911,7 +1053,7 @@ struct Feti {
     }
     std::vector<CVec> ur;
     CVec z;
-    eliminate(t, CVec(nc, cd(0)), ur, z);
+    eliminate(t, CVec(ncg, cd(0)), ur, z);
     CVec out = gather_jump(ur);
     for (auto& v : out) v = -v;
     return out;
@@ -974,8 +1116,14 @@ struct Feti {
     CVec z;
     eliminate(fr, fc, ur, z);
     CVec d = gather_jump(ur);
+    // the coarse solve pins the augmented jump components: the dual problem lives in the
+    // orthogonal complement of the columns (feti.cpp:655-662)
+    project_out_augmentation(d);
     const int nl = part.n_lambda;
-    Op A = [this](const CVec& x, CVec& y) { y = apply_dual(x); };
+    Op A = [this](const CVec& x, CVec& y) {
+      y = apply_dual(x);
+      project_out_augmentation(y);
+    };
     Op M = [this](const CVec& x, CVec& y) { y = apply_dirichlet(x); };
     auto [lam, gst] = gmres(nl, A, M, d, tol, max_iter, std::max(1, max_iter), hist);
     st.dual = gst;
@@ -1197,11 +1345,12 @@ int orc_partition_info(void* p, int sx, int sy, int* info) {
 }
 
 int orc_feti_create(void* p, int sx, int sy, double kre, double kim, double mre, double mim, double tol,
-                    int max_iter, int threads, void** out) {
+                    int max_iter, int threads, int augment, void** out) {
   return guard([&] {
     auto F = std::make_unique<Feti>();
     F->P = static_cast<Problem*>(p);
     F->part = partition_structured(*F->P, sx, sy);
+    F->augment = augment != 0;
     F->kcoef = cd(kre, kim);
     F->mcoef = cd(mre, mim);
     F->tol = tol;
@@ -1251,7 +1400,7 @@ int orc_feti_solve(void* f, const double* rhs, double* x, OrcStats* st, double* 
 // in the reference (control.cpp:303-304). times[0] = setup seconds (both factors),
 // times[1] = solve seconds (both FETI solves + recovery).
 int orc_schur_solve(void* p, int sx, int sy, double phi, const double* ybar, const double* yc, double tol,
-                    int max_iter, int threads, double* y, double* u, double* lam, OrcStats* plus,
+                    int max_iter, int threads, int augment, double* y, double* u, double* lam, OrcStats* plus,
                     OrcStats* minus, double* imag_leak, double* times) {
   return guard([&] {
     auto* P = static_cast<Problem*>(p);
@@ -1263,6 +1412,7 @@ int orc_schur_solve(void* p, int sx, int sy, double phi, const double* ybar, con
     for (Feti* F : {&fp, &fm}) {
       F->P = P;
       F->part = partition_structured(*P, sx, sy);
+      F->augment = augment != 0;
       F->kcoef = 1.0;
       F->tol = tol;
       F->max_iter = max_iter;
@@ -1314,8 +1464,8 @@ struct SchurPair {
   Feti plus, minus;
   double phi;
 };
-int orc_schur_create(void* p, int sx, int sy, double phi, double tol, int max_iter, int threads, void** out,
-                     double* setup_seconds) {
+int orc_schur_create(void* p, int sx, int sy, double phi, double tol, int max_iter, int threads, int augment,
+                     void** out, double* setup_seconds) {
   return guard([&] {
     auto* P = static_cast<Problem*>(p);
     if (!(phi > 0.0)) throw ContractError("ControlProblem: phi must be positive");
@@ -1327,6 +1477,7 @@ int orc_schur_create(void* p, int sx, int sy, double phi, double tol, int max_it
     for (Feti* F : {&sp->plus, &sp->minus}) {
       F->P = P;
       F->part = partition_structured(*P, sx, sy);
+      F->augment = augment != 0;
       F->kcoef = 1.0;
       F->tol = tol;
       F->max_iter = max_iter;

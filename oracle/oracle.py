@@ -71,7 +71,7 @@ def lib():
         L.orc_sine_modes.argtypes = [C.c_ulonglong, C.c_int, C.c_int, dp, ip, ip]
         L.orc_partition_info.argtypes = [vp, C.c_int, C.c_int, ip]
         L.orc_feti_create.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
-                                      C.c_double, C.c_int, C.c_int, C.POINTER(vp)]
+                                      C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
         L.orc_feti_destroy.argtypes = [vp]
         L.orc_feti_n_lambda.argtypes = [vp]
         L.orc_feti_coarse_dim.argtypes = [vp]
@@ -81,8 +81,8 @@ def lib():
         L.orc_feti_apply_precond.argtypes = [vp, dp, dp]
         L.orc_feti_solve.argtypes = [vp, dp, dp, C.POINTER(OracleStats), dp, C.c_int]
         L.orc_schur_solve.argtypes = [vp, C.c_int, C.c_int, C.c_double, dp, dp, C.c_double, C.c_int, C.c_int,
-                                      dp, dp, dp, C.POINTER(OracleStats), C.POINTER(OracleStats), dp, dp]
-        L.orc_schur_create.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                      C.c_int, dp, dp, dp, C.POINTER(OracleStats), C.POINTER(OracleStats), dp, dp]
+        L.orc_schur_create.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
                                        C.POINTER(vp), dp]
         L.orc_schur_destroy.argtypes = [vp]
         L.orc_schur_run.argtypes = [vp, dp, dp, dp, dp, dp, C.POINTER(OracleStats), C.POINTER(OracleStats), dp]
@@ -169,7 +169,7 @@ class Problem:
         keys = ("n_subdomains", "n_corner_dofs", "n_lambda", "n_edges", "ex", "ey")
         return dict(zip(keys, (int(v) for v in info)))
 
-    def schur_solve(self, s_x, s_y, phi, ybar, yc=None, tol=1e-10, max_iter=2000, threads=1):
+    def schur_solve(self, s_x, s_y, phi, ybar, yc=None, tol=1e-10, max_iter=2000, threads=1, augment=False):
         n = self.n
         ybar = np.ascontiguousarray(ybar, dtype=np.float64)
         ycp = None
@@ -180,7 +180,7 @@ class Problem:
         sp, sm = OracleStats(), OracleStats()
         leak = np.zeros(1)
         times = np.zeros(2)
-        _check(lib().orc_schur_solve(self._h, s_x, s_y, phi, _dp(ybar), ycp, tol, max_iter, threads, _dp(y),
+        _check(lib().orc_schur_solve(self._h, s_x, s_y, phi, _dp(ybar), ycp, tol, max_iter, threads, int(augment), _dp(y),
                                      _dp(u), _dp(lam), C.byref(sp), C.byref(sm), _dp(leak), _dp(times)))
         return {"y": y, "u": u, "lambda": lam, "imag_leak": float(leak[0]), "plus_stats": sp.as_dict(),
                 "minus_stats": sm.as_dict(), "setup_seconds": float(times[0]), "solve_seconds": float(times[1]),
@@ -188,15 +188,16 @@ class Problem:
 
 
 class Feti:
-    """One FETI-DP(H) solver on A = k*K + c*V (feti.cpp:373-717, augment=false)."""
+    """One FETI-DP(H) solver on A = k*K + c*V (feti.cpp:373-717); augment: edge-RBM
+    augmentation of the coarse space (feti.cpp:171-242, 394-454, 572-578)."""
 
     def __init__(self, problem: Problem, s_x, s_y, mass_coeff, stiffness_coeff=1.0, tol=1e-10, max_iter=1000,
-                 threads=1):
+                 threads=1, augment=False):
         self.problem = problem
         mc, kc = complex(mass_coeff), complex(stiffness_coeff)
         h = C.c_void_p()
         _check(lib().orc_feti_create(problem._h, s_x, s_y, kc.real, kc.imag, mc.real, mc.imag, tol, max_iter,
-                                     threads, C.byref(h)))
+                                     threads, int(augment), C.byref(h)))
         self._h = h
         self.n_lambda = lib().orc_feti_n_lambda(h)
         self.coarse_dim = lib().orc_feti_coarse_dim(h)
@@ -236,11 +237,12 @@ class Feti:
 class SchurPair:
     """Both reference factor solvers built once (control.cpp:303-304); run() = one Schur solve."""
 
-    def __init__(self, problem: Problem, s_x, s_y, phi, tol=1e-10, max_iter=2000, threads=1):
+    def __init__(self, problem: Problem, s_x, s_y, phi, tol=1e-10, max_iter=2000, threads=1, augment=False):
         self.problem = problem
         h = C.c_void_p()
         t = np.zeros(1)
-        _check(lib().orc_schur_create(problem._h, s_x, s_y, phi, tol, max_iter, threads, C.byref(h), _dp(t)))
+        _check(lib().orc_schur_create(problem._h, s_x, s_y, phi, tol, max_iter, threads, int(augment), C.byref(h),
+                                      _dp(t)))
         self._h = h
         self.setup_seconds = float(t[0])
 
