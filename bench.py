@@ -210,7 +210,7 @@ def run_gpu(args):
         solver = F.SchurSolver(p, s_x, s_y, tol=TOL, max_iter=MAX_ITER, device=local, rank=rank, world=world,
                                nccl_id=obj[0])
     else:
-        solver = F.SchurSolver(p, s_x, s_y, tol=TOL, max_iter=MAX_ITER, device=local)
+        solver = F.SchurSolver(p, s_x, s_y, tol=TOL, max_iter=MAX_ITER, device=local, augment=args.augment)
     setup_s = time.perf_counter() - t0
     n = p.n
     # seeded targets for every step (the same on every rank), resident in HBM before the timed region
@@ -299,6 +299,7 @@ def run_gpu(args):
                          f"weak scaling: {n_x}x{n_y} Q1 heat, {s_x}x{s_y} subdomains of 32x32 ({s_x * s_y // world} "
                          f"per GPU), phi=1e-4, tol 1e-10, FP64 complex; value = solves/s x {world}"),
             "phi": PHI, "n_free": n, "n_lambda": solver.n_lambda, "coarse_dim": solver.coarse_dim,
+            "augment": bool(args.augment),
             "iterations_plus_minus_mean": [float(np.mean([a for a, _ in its])), float(np.mean([b for _, b in its]))],
             "setup_seconds": setup_s, "l2": "inputs larger than L2 (local operators 0.5 GB streamed per iteration)",
             "parallelism": f"subdomain rows sharded over {world} GPUs (NCCL)" if world > 1 else "1 GPU",
@@ -355,6 +356,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--augment", action="store_true",
+                    help="edge-RBM augmented coarse space (reference default; BASELINE configs use augment=false)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -177,8 +177,6 @@ class SchurSolver:
 
     def __init__(self, problem: ControlProblem, s_x=2, s_y=2, tol=1e-10, max_iter=1000, mass_coeff=None,
                  device=0, augment=False, rank=None, world=None, nccl_id=None):
-        if augment:
-            raise ContractError("edge-RBM augmentation is not implemented on the B200 path (augment=False)")
         self.problem = problem
         self._desc = problem.desc(s_x, s_y, tol, max_iter, mass_coeff, device, augment)
         h = C.c_void_p()
@@ -193,6 +191,9 @@ class SchurSolver:
         self._h = h
         info = problem._info(s_x, s_y)
         self.n, self.m, self.n_lambda, self.coarse_dim = int(info[0]), int(info[1]), int(info[4]), int(info[3])
+        self.augment = bool(augment)
+        if augment:  # coarse = corners + edge-RBM columns (1 per edge, 3 for plane strain)
+            self.coarse_dim += int(info[5]) * (1 if int(info[8]) == 1 else 3)
 
     def close(self):
         if getattr(self, "_h", None):

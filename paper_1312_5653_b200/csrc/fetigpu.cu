@@ -79,6 +79,11 @@ struct Ctx {
   SubLayout L{};
   MeshLayout M{};
   int Wt = 0, WCt = 0, nc = 0, nl = 0, n = 0, m = 0;
+  int ncg = 0;  // corner dofs (the first ncg coarse unknowns; the rest are augmentation columns)
+  // edge-RBM augmentation (projection v -= Q Q^T v of the dual space)
+  int *d_edge_col0 = nullptr, *d_edge_ncol = nullptr, *d_col_ptr = nullptr, *d_col_rows = nullptr;
+  double* d_col_vals = nullptr;
+  bool edge_gather_ok = false;
   // block-Thomas interior solve (blockthomas.cuh): records, block count, enabled
   int* d_aic_idx = nullptr;  // compact A_ic (eliminate-phase coarse rhs from the GEMV)
   double2* d_aic_val = nullptr;
@@ -343,6 +348,48 @@ struct Ctx {
     }
   }
   static constexpr int kBtStages = 2;
+  // Augmented coarse problem (feti.cpp:440-475): dense assembly in [corners | columns]
+  // order, symmetric equilibration 1/sqrt|C_ii|, in-place Gauss-Jordan inverse with partial
+  // pivoting (pivots = the U_kk of PartialPivLU), the reference's pivot check, unscaling.
+  void setup_dense_coarse(const double2* contrib) {
+    const int NC = H.NC;
+    d_Cinv = alloc<double2>((size_t)nc * nc);
+    zero(d_Cinv, (size_t)nc * nc);
+    double* sc = alloc<double>(nc);
+    int* piv = alloc<int>(nc);
+    double* pivabs = alloc<double>(nc);
+    double2* fcol = alloc<double2>(nc);
+    launch(FETIGPU_K_OTHER, [&] {
+      k_coarse_assemble_dense<<<cdiv(nc, 128), 128, 0, stream>>>(nc, NC, d_corner_slots, d_cglob, d_Acc, contrib,
+                                                                 d_Cinv);
+    });
+    const long long nn = (long long)nc * nc;
+    launch(FETIGPU_K_OTHER, [&] { k_dense_diag_scale<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_Cinv, sc); });
+    launch(FETIGPU_K_OTHER, [&] { k_dense_apply_scale<<<cdiv(nn, 256), 256, 0, stream>>>(nc, d_Cinv, sc); });
+    for (int k = 0; k < nc; ++k) {
+      k_gj_pivot<<<1, 1024, 0, stream>>>(nc, k, d_Cinv, piv, pivabs, fcol);
+      k_gj_update<<<dim3(cdiv(nc, 256), nc), 256, 0, stream>>>(nc, k, d_Cinv, fcol);
+    }
+    CU(cudaGetLastError());
+    launches += 2LL * nc;
+    launch(FETIGPU_K_OTHER, [&] { k_gj_unpermute<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_Cinv, piv); });
+    std::vector<double> pa(nc);
+    CU(cudaMemcpyAsync(pa.data(), pivabs, nc * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    sync();
+    double umax = 0;
+    for (double v : pa) umax = std::max(umax, v);
+    for (double v : pa)
+      if (!(v > umax * 1e-13)) throw NumericalError("feti: coarse problem is singular");
+    launch(FETIGPU_K_OTHER, [&] { k_scale_inverse<<<cdiv(nn, 256), 256, 0, stream>>>(nc, d_Cinv, sc); });
+  }
+  // v -= Q Q^T v on the owned multiplier rows (no-op without augmentation)
+  void project_aug(double2* v) {
+    if (H.n_aug == 0) return;
+    launch(FETIGPU_K_LAMBDA, [&] {
+      k_project_aug<<<cdiv(H.n_edges, 8), 256, 0, stream>>>(H.n_edges, d_edge_col0, d_edge_ncol, d_col_ptr,
+                                                            d_col_rows, d_col_vals, v);
+    });
+  }
   void setup_compact_aic() {
     const int S = H.n_sub, NC = H.NC;
     if (NC == 0 || sym_tma || std::getenv("FETIGPU_NO_AIC")) return;  // (the TMA GEMV has no A_ic term)
@@ -361,7 +408,8 @@ struct Ctx {
   static constexpr int kTailThreads = 512;
   size_t tail_smem() const { return sizeof(double2) * ((size_t)kTailThreads + 2 * (size_t)(vcap_hint() + 2) + 640); }
   void setup_fused_tail() {
-    if (dist() || H.NC > 4 || nc > kTailThreads + 2 * (vcap_hint() + 2) || std::getenv("FETIGPU_NO_FUSED_TAIL"))
+    if (dist() || H.NC > 4 || H.n_aug > 0 || nc > kTailThreads + 2 * (vcap_hint() + 2) ||
+        std::getenv("FETIGPU_NO_FUSED_TAIL"))
       return;
     const size_t smem = tail_smem();
     if (smem > 200 * 1024) return;
@@ -425,12 +473,15 @@ struct Ctx {
     watchdog = std::getenv("FETIGPU_WATCHDOG") != nullptr;
     n = P.n();
     m = P.m();
-    nc = H.n_corner;
+    nc = H.n_coarse;
+    ncg = H.n_corner;
     nl = H.n_lambda;
+    if (H.n_aug > 0 && dist()) throw ContractError("fetigpu: augmentation is not implemented on the sharded path");
     Wt = round_band(std::max(H.W, 1));
     WCt = round_band(std::max(H.WC, 1));
     if (H.MAXE_BI > MAXE || H.MAXE_IB > MAXE) throw ContractError("ELL width exceeds kernel capacity");
-    if (H.NC > 8) throw ContractError("more than 8 corner dofs per subdomain");
+    if (H.NC > 8)
+      throw ContractError("more than 8 local coarse unknowns per subdomain (augmented plane strain is not supported)");
     if (H.NB > 4096) throw ContractError("too many interface dofs per subdomain");
     L = SubLayout{H.n_sub, H.nld, H.ex, H.ey, H.dpn, H.NI, H.NB, H.NC, Wt, H.MAXE_BI, H.MAXE_IB};
     M = MeshLayout{P.nx, P.ny, P.dpn};
@@ -498,6 +549,24 @@ struct Ctx {
                                                                       d_ib_idx, d_ib_val, d_Sbb, d_Aic, d_Abc, d_Acc);
     });
     launch(FETIGPU_K_OTHER, [&] { k_pad_identity<<<S, 128, 0, stream>>>(L, d_n_i, d_n_b, d_colband, d_Sbb); });
+    if (H.n_aug > 0) {  // augmentation columns of the coupling rhs [A_rc | C^T] (A_ic part zero)
+      const int cnt = (int)H.aug_s.size();
+      int* as = upload(H.aug_s);
+      int* akb = upload(H.aug_kb);
+      int* akc = upload(H.aug_kc);
+      double* av = upload(H.aug_val);
+      launch(FETIGPU_K_OTHER, [&] { k_add_aug<<<cdiv(cnt, 256), 256, 0, stream>>>(cnt, NB, NC, as, akb, akc, av, d_Abc); });
+      // one column per edge covering all of its rows (scalar physics): fused gather + projection
+      edge_gather_ok = true;
+      for (int e = 0; e < H.n_edges; ++e)
+        edge_gather_ok = edge_gather_ok && H.edge_ncol[e] == 1 && H.edge_col0[e] == e &&
+                         H.col_ptr[e + 1] - H.col_ptr[e] <= 128;
+      d_edge_col0 = upload(H.edge_col0);
+      d_edge_ncol = upload(H.edge_ncol);
+      d_col_ptr = upload(H.col_ptr);
+      d_col_rows = upload(H.col_rows);
+      d_col_vals = upload(H.col_vals);
+    }
 
     // K2': block-Thomas factors for the per-solve interior solves (reads the band of A_ii,
     // so it runs before the in-place band factorization)
@@ -544,7 +613,9 @@ struct Ctx {
         k_coarse_contrib<<<S, 256, 0, stream>>>(L, d_Aic, d_Abc, d_cpl_i, d_cpl_b, contrib);
       });
       // K4: coarse assembly, equilibration, band LDL^T, explicit inverse
-      if (nc > 0) {
+      if (nc > 0 && H.n_aug > 0) {
+        setup_dense_coarse(contrib);
+      } else if (nc > 0) {
         const int LDC = WCt + 1;
         double2* cband = alloc<double2>((size_t)nc * LDC);
         double2* crow = alloc<double2>((size_t)nc * LDC);
@@ -625,6 +696,7 @@ struct Ctx {
     d_wb = alloc<double2>((size_t)n_slot_ext);
     d_gcp = alloc<double2>((size_t)S * NC);
     d_fc = alloc<double2>(std::max(nc, 1));
+    zero(d_fc, std::max(nc, 1));  // augmentation rows of f_c stay zero (feti.cpp:521-522)
     d_g = alloc<double2>(std::max(nc, 1));
     d_z = alloc<double2>(std::max(nc, 1));
     zero(d_z, std::max(nc, 1));
@@ -1141,6 +1213,20 @@ struct Ctx {
     c.mode = 0;
     c.out = h1;
     c.gather = 1;
+    if (H.n_aug > 0) {  // augmented: w = P F z, gathered and projected before the dots
+      if (edge_gather_ok) {
+        EdgeGatherArgs ea{H.n_edges, H.NB, H.NC, d_col_ptr, d_col_rows, d_col_vals, d_lam_lo, d_lam_hi,
+                          d_cglob, d_u1b, d_cpl_b, d_z, d_w};
+        launch(FETIGPU_K_LAMBDA, [&] { k_gather_project_edges<<<cdiv(H.n_edges, 8), 256, 0, stream>>>(ea); });
+      } else {
+        launch(FETIGPU_K_LAMBDA, [&] {
+          k_lam_gather_dual<<<cdiv(nown, 256), 256, 0, stream>>>(nown, H.NB, H.NC, d_lam_lo + own0, d_lam_hi + own0,
+                                                                 d_u1b, d_cpl_b, d_cglob, d_z, d_w + own0);
+        });
+        project_aug(d_w);
+      }
+      c.gather = 0;
+    }
     c.pf = l2pf(1);
     c.NB = H.NB;
     c.NC = H.NC;
@@ -1283,6 +1369,7 @@ struct Ctx {
       apply_precond(d_t, d_zl);
       launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nown, 256), 256, 0, stream>>>(nown, x + own0, d_zl + own0); });
       apply_dual(x, d_w);
+      project_aug(d_w);  // the GMRES operator is P F (feti.cpp:667-670)
       launch(FETIGPU_K_ORTHO, [&] {
         k_sub<<<cdiv(nown, 256), 256, 0, stream>>>(nown, b + own0, d_w + own0, d_r + own0);
       });
@@ -1316,11 +1403,14 @@ struct Ctx {
       k_split_rhs<<<cdiv((long long)S * (NI + NB), 256), 256, 0, stream>>>(L, d_idof, d_bdof, rhs, d_fi, d_fb);
     });
     if (nc > 0)
-      launch(FETIGPU_K_OTHER, [&] { k_gather_corner<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_dof, rhs, d_fc); });
+      launch(FETIGPU_K_OTHER, [&] { k_gather_corner<<<cdiv(ncg, 128), 128, 0, stream>>>(ncg, d_corner_dof, rhs, d_fc); });
     eliminate_boundary(d_fi, d_fb, d_fc, true);
     launch(FETIGPU_K_LAMBDA, [&] {
       k_jump<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_lam_lo + own0, d_lam_hi + own0, d_u1b, d_d + own0);
     });
+    // augmented: the coarse solve pins the column components; the dual problem lives in
+    // their orthogonal complement (feti.cpp:655-662)
+    project_aug(d_d);
     const fetigpu_feti_stats gst = gmres(d_d, d_lam);
     ghost_refresh(d_lam);
     st.iterations = gst.iterations;
@@ -1448,7 +1538,6 @@ static int guard(const std::function<void()>& f) {
 
 static void validate_desc(const fetigpu_desc* d) {
   if (!d) throw ContractError("fetigpu: null descriptor");
-  if (d->augment) throw ContractError("fetigpu: edge-RBM augmentation is not implemented (augment must be 0)");
   if (!(d->tol > 0.0)) throw ContractError("fetigpu: tol must be positive");
   if (d->max_iter < 0) throw ContractError("fetigpu: max_iter must be non-negative");
   if (d->phi < 0.0) throw ContractError("ControlProblem: phi must be positive");
@@ -1506,7 +1595,7 @@ int fetigpu_create(const fetigpu_desc* desc, fetigpu_ctx** out) {
     auto c = std::make_unique<Ctx>();
     c->desc = *desc;
     c->P = build_problem(*desc);
-    c->H = build_partition(c->P, desc->s_x, desc->s_y);
+    c->H = build_partition(c->P, desc->s_x, desc->s_y, desc->augment != 0);
     if (desc->phi > 0.0) {
       c->phi = desc->phi;
       c->mc = cd(0.0, -1.0 / std::sqrt(desc->phi));  // c = 1/(i sqrt(phi)), control.cpp:116

@@ -132,7 +132,7 @@ HostProblem build_problem(const fetigpu_desc& d) {
   return P;
 }
 
-HostPartition build_partition(const HostProblem& P, int sx, int sy) {
+HostPartition build_partition(const HostProblem& P, int sx, int sy, bool augment) {
   // contract checks of feti.cpp:36-41
   if (sx < 1 || sy < 1 || sx * sy < 2) throw ContractError("partition_structured: need at least two subdomains");
   if (P.nx % sx != 0 || P.ny % sy != 0)
@@ -214,19 +214,84 @@ HostPartition build_partition(const HostProblem& P, int sx, int sy) {
           }
         }
     }
-  // edges (feti.cpp:132-167), counted for the bookkeeping queries
+  // interface edges (feti.cpp:132-167): vertical cuts (row q, cut p) then horizontal cuts;
+  // free nodes strictly inside the segment, dpn multiplier rows per node
+  struct EdgeRec {
+    int lo, hi;
+    bool vertical;
+    std::vector<int> rows;
+  };
+  std::vector<EdgeRec> edges;
+  auto add_edge = [&](int lo, int hi, bool vertical, const std::vector<int>& nodes) {
+    if (nodes.empty()) return;
+    EdgeRec e{lo, hi, vertical, {}};
+    for (int node : nodes)
+      for (int c = 0; c < dpn; ++c) e.rows.push_back(lambda_of[node * dpn + c]);
+    edges.push_back(std::move(e));
+  };
   for (int q = 0; q < sy; ++q)
     for (int p = 1; p < sx; ++p) {
-      int cnt = 0;
-      for (int j = q * ey + 1; j < (q + 1) * ey; ++j) cnt += P.free_map[P.node_id(p * ex, j) * dpn] >= 0;
-      H.n_edges += cnt > 0;
+      std::vector<int> nodes;
+      for (int j = q * ey + 1; j < (q + 1) * ey; ++j)
+        if (P.free_map[P.node_id(p * ex, j) * dpn] >= 0) nodes.push_back(P.node_id(p * ex, j));
+      add_edge(q * sx + p - 1, q * sx + p, true, nodes);
     }
   for (int q = 1; q < sy; ++q)
     for (int p = 0; p < sx; ++p) {
-      int cnt = 0;
-      for (int i = p * ex + 1; i < (p + 1) * ex; ++i) cnt += P.free_map[P.node_id(i, q * ey) * dpn] >= 0;
-      H.n_edges += cnt > 0;
+      std::vector<int> nodes;
+      for (int i = p * ex + 1; i < (p + 1) * ex; ++i)
+        if (P.free_map[P.node_id(i, q * ey) * dpn] >= 0) nodes.push_back(P.node_id(i, q * ey));
+      add_edge((q - 1) * sx + p, q * sx + p, false, nodes);
     }
+  H.n_edges = (int)edges.size();
+  // edge-RBM columns: the edge mean (scalar physics) or the two translations and the
+  // in-plane rotation about the edge midpoint (plane strain), each normalised
+  std::vector<std::vector<int>> sub_cols(H.n_sub);  // augmentation columns per subdomain
+  if (augment) {
+    H.col_ptr.push_back(0);
+    for (int e = 0; e < (int)edges.size(); ++e) {
+      const EdgeRec& ed = edges[e];
+      const int nn = (int)ed.rows.size() / dpn;
+      H.edge_col0.push_back((int)H.col_ptr.size() - 1);
+      std::vector<std::pair<std::vector<int>, std::vector<double>>> cols;
+      if (dpn == 1) {
+        cols.push_back({ed.rows, std::vector<double>(nn, 1.0)});
+      } else {
+        std::vector<int> rx, ry, rr;
+        std::vector<double> vr;
+        for (int k = 0; k < nn; ++k) {
+          rx.push_back(ed.rows[2 * k]);
+          ry.push_back(ed.rows[2 * k + 1]);
+          const double arm = (k - 0.5 * (nn - 1)) * P.h;
+          rr.push_back(ed.vertical ? ed.rows[2 * k] : ed.rows[2 * k + 1]);
+          vr.push_back(ed.vertical ? -arm : arm);
+        }
+        cols.push_back({rx, std::vector<double>(nn, 1.0)});
+        cols.push_back({ry, std::vector<double>(nn, 1.0)});
+        cols.push_back({rr, vr});
+      }
+      for (auto& c : cols) {
+        double n2 = 0;
+        for (double v : c.second) n2 += v * v;
+        if (!(n2 > 0.0))
+          throw NumericalError("build_edge_rbm_augmentation: dependent (zero) column on edge " + std::to_string(e) +
+                               "; H/h too small for a rotation mode");
+        const double inv = 1.0 / std::sqrt(n2);
+        const int q = (int)H.col_ptr.size() - 1;
+        for (size_t k = 0; k < c.first.size(); ++k) {
+          H.col_rows.push_back(c.first[k]);
+          H.col_vals.push_back(c.second[k] * inv);
+        }
+        H.col_ptr.push_back((int)H.col_rows.size());
+        sub_cols[ed.lo].push_back(q);
+        sub_cols[ed.hi].push_back(q);
+      }
+      H.edge_ncol.push_back((int)cols.size());
+    }
+    H.n_aug = (int)H.col_ptr.size() - 1;
+    for (auto& v : sub_cols) std::sort(v.begin(), v.end());
+  }
+  H.n_coarse = H.n_corner + H.n_aug;
 
   const int S = H.n_sub;
   H.n_i.resize(S);
@@ -238,7 +303,7 @@ HostPartition build_partition(const HostProblem& P, int sx, int sy) {
     H.n_c[s] = (int)L[s].cglob.size();
     H.NI = std::max(H.NI, H.n_i[s]);
     H.NB = std::max(H.NB, H.n_b[s]);
-    H.NC = std::max(H.NC, H.n_c[s]);
+    H.NC = std::max(H.NC, H.n_c[s] + (int)sub_cols[s].size());
   }
   H.NI = std::max(H.NI, 1);
   H.NB = std::max(H.NB, 1);
@@ -252,10 +317,10 @@ HostPartition build_partition(const HostProblem& P, int sx, int sy) {
   H.corner_dof.assign(H.n_corner, -1);
   H.lam_lo.assign(H.n_lambda, -1);
   H.lam_hi.assign(H.n_lambda, -1);
-  H.corner_slots.assign((size_t)H.n_corner * 4, -1);
+  H.corner_slots.assign((size_t)H.n_coarse * 4, -1);
   H.sub_i0.resize(S);
   H.sub_j0.resize(S);
-  std::vector<int> ccount(H.n_corner, 0);
+  std::vector<int> ccount(H.n_coarse, 0);
   for (int s = 0; s < S; ++s) {
     const Loc& l = L[s];
     H.sub_i0[s] = (s % sx) * ex;
@@ -276,6 +341,24 @@ HostPartition build_partition(const HostProblem& P, int sx, int sy) {
       H.corner_dof[cg] = l.cdof[k];
       if (ccount[cg] >= 4) throw NumericalError("partition: corner shared by more than 4 subdomains");
       H.corner_slots[(size_t)cg * 4 + ccount[cg]++] = s * H.NC + k;
+    }
+    // augmentation columns of the subdomain's edges after its corners; C^s^T entries on
+    // the boundary rows with the subdomain's multiplier sign (feti.cpp:394-412)
+    for (size_t a = 0; a < sub_cols[s].size(); ++a) {
+      const int q = sub_cols[s][a], kc = H.n_c[s] + (int)a, cg = H.n_corner + q;
+      H.cglob[(size_t)s * H.NC + kc] = cg;
+      H.corner_slots[(size_t)cg * 4 + ccount[cg]++] = s * H.NC + kc;
+      for (int e = H.col_ptr[q]; e < H.col_ptr[q + 1]; ++e) {
+        const int row = H.col_rows[e];
+        int kb = -1;
+        for (int k = 0; k < H.n_b[s]; ++k)
+          if (l.blam[k] == row) kb = k;
+        if (kb < 0) throw NumericalError("augmentation: edge row not on the subdomain interface");
+        H.aug_s.push_back(s);
+        H.aug_kb.push_back(kb);
+        H.aug_kc.push_back(kc);
+        H.aug_val.push_back(l.bsign[kb] * H.col_vals[e]);
+      }
     }
   }
   for (int r = 0; r < H.n_lambda; ++r)

@@ -65,7 +65,16 @@ struct HostPartition {
   std::vector<int> cglob;                // [S][NC] global corner id (-1 pad)
   std::vector<int> corner_dof;           // [n_corner] global free dof of corner c
   std::vector<int> lam_lo, lam_hi;       // [n_lambda] flat slot s*NB+k of the +1 / -1 owner
-  std::vector<int> corner_slots;         // [n_corner][4] flat slot s*NC+k, ascending s, -1 pad
+  std::vector<int> corner_slots;         // [n_coarse][4] flat slot s*NC+k, ascending s, -1 pad
+  // edge-RBM augmentation (augment = true; feti.cpp:171-242, 394-454).  The coarse unknowns
+  // are [corner dofs | augmentation columns]; a subdomain's local coarse list is its corners
+  // followed by the columns of its edges (ascending column id), so NC counts both.
+  int n_coarse = 0, n_aug = 0;
+  std::vector<int> aug_s, aug_kb, aug_kc;   // entries of C^s^T: subdomain, boundary index, local col
+  std::vector<double> aug_val;              //   value sign * q (A_bc-like, A_ic part zero)
+  std::vector<int> col_ptr, col_rows;       // [n_aug+1] / rows of column q (ascending by column)
+  std::vector<double> col_vals;
+  std::vector<int> edge_col0, edge_ncol;    // columns of edge e: [edge_col0[e], + edge_ncol[e])
   std::vector<int> xkind, xa, xb;        // [n_free] primal assembly map (0 int, 1 bnd, 2 corner)
   std::vector<int> free_row;             // [n_free] mesh node row j of each free dof
   // element-local structure: sub origin (node) for subdomain s
@@ -73,7 +82,7 @@ struct HostPartition {
 };
 
 HostProblem build_problem(const fetigpu_desc& d);
-HostPartition build_partition(const HostProblem& P, int sx, int sy);
+HostPartition build_partition(const HostProblem& P, int sx, int sy, bool augment = false);
 
 // ---------------------------------------------------------------------------------------
 // Multi-GPU sharding.  Rank r of R owns the subdomain rows

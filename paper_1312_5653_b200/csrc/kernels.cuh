@@ -245,13 +245,16 @@ __global__ void k_coupling_i(SubLayout L, const double2* __restrict__ Yc, const 
   const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= (long long)L.S * L.NI) return;
   const int s = (int)(gid / L.NI), i = (int)(gid % L.NI);
-  double2 acc[8];
-  for (int c = 0; c < L.NC; ++c) acc[c] = Yc[((size_t)s * L.NC + c) * L.NI + i];
-  for (int b = 0; b < L.NB; ++b) {
-    const double2 y = Y[((size_t)s * L.NB + b) * L.NI + i];
-    for (int c = 0; c < L.NC; ++c) acc[c] = cfms(y, cpl_b[((size_t)s * L.NB + b) * L.NC + c], acc[c]);
+  for (int c0 = 0; c0 < L.NC; c0 += 8) {  // columns in chunks of 8
+    const int nc = min(8, L.NC - c0);
+    double2 acc[8];
+    for (int c = 0; c < nc; ++c) acc[c] = Yc[((size_t)s * L.NC + c0 + c) * L.NI + i];
+    for (int b = 0; b < L.NB; ++b) {
+      const double2 y = Y[((size_t)s * L.NB + b) * L.NI + i];
+      for (int c = 0; c < nc; ++c) acc[c] = cfms(y, cpl_b[((size_t)s * L.NB + b) * L.NC + c0 + c], acc[c]);
+    }
+    for (int c = 0; c < nc; ++c) cpl_i[((size_t)s * L.NI + i) * L.NC + c0 + c] = acc[c];
   }
-  for (int c = 0; c < L.NC; ++c) cpl_i[((size_t)s * L.NI + i) * L.NC + c] = acc[c];
 }
 
 // contrib[s] = A_rc^T coupling (transpose, not adjoint: feti.cpp:433). One warp per entry.
@@ -296,6 +299,136 @@ __global__ void k_coarse_assemble(int nc, int WC, int NC, const int* __restrict_
       double2& t = cband[(size_t)col * LDC + (r - col)];
       t = csub(t, contrib[((size_t)s * NC + ka) * NC + kb]);
     }
+  }
+}
+
+// ---- dense coarse path (edge-RBM augmentation: the coarse matrix is indefinite and not
+// banded in corner order).  Assembly, equilibration and an in-place Gauss-Jordan inverse
+// with partial pivoting (the pivot sequence of the reference's PartialPivLU, feti.cpp:468).
+__global__ void k_coarse_assemble_dense(int nc, int NC, const int* __restrict__ slots, const int* __restrict__ cglob,
+                                        const double2* __restrict__ Acc, const double2* __restrict__ contrib,
+                                        double2* __restrict__ C) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nc) return;
+  for (int q = 0; q < 4; ++q) {
+    const int slot = slots[r * 4 + q];
+    if (slot < 0) continue;
+    const int s = slot / NC, ka = slot % NC;
+    for (int kb = 0; kb < NC; ++kb) {
+      const int col = cglob[(size_t)s * NC + kb];
+      if (col >= 0) C[(size_t)r * nc + col] = cadd(C[(size_t)r * nc + col], Acc[((size_t)s * NC + ka) * NC + kb]);
+    }
+    for (int kb = 0; kb < NC; ++kb) {
+      const int col = cglob[(size_t)s * NC + kb];
+      if (col >= 0) C[(size_t)r * nc + col] = csub(C[(size_t)r * nc + col], contrib[((size_t)s * NC + ka) * NC + kb]);
+    }
+  }
+}
+__global__ void k_dense_diag_scale(int nc, const double2* __restrict__ C, double* __restrict__ scale) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  const double d = sqrt(cabs2(C[(size_t)i * nc + i]));
+  scale[i] = d > 0.0 ? 1.0 / sqrt(d) : 1.0;
+}
+__global__ void k_dense_apply_scale(int nc, double2* __restrict__ C, const double* __restrict__ scale) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long long)nc * nc) return;
+  C[e] = cscale(C[e], scale[e / nc] * scale[e % nc]);
+}
+// Gauss-Jordan step k, part 1 (one block): pivot row p = argmax_{i>=k} |A(i,k)| (smallest
+// index on ties), swap rows k and p, scale row k by 1/A(k,k) (A(k,k) <- 1/A(k,k)), stash
+// column k for the update.  pivabs[k] = |pivot| (the reference's U_kk check).
+__global__ void __launch_bounds__(1024) k_gj_pivot(int n, int k, double2* __restrict__ A, int* __restrict__ piv,
+                                                   double* __restrict__ pivabs, double2* __restrict__ fcol) {
+  __shared__ double wb[32];
+  __shared__ int wi[32];
+  __shared__ int p_sh;
+  __shared__ double2 dinv_sh;
+  double best = -1.0;
+  int bidx = n;
+  for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+    const double a = cabs2(A[(size_t)i * n + k]);
+    if (a > best) best = a, bidx = i;
+  }
+  for (int m = 16; m > 0; m >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, m);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, m);
+    if (ob > best || (ob == best && oi < bidx)) best = ob, bidx = oi;
+  }
+  if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = best, wi[threadIdx.x >> 5] = bidx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = -1.0;
+    int bi = n;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+      if (wb[w] > b || (wb[w] == b && wi[w] < bi)) b = wb[w], bi = wi[w];
+    p_sh = bi < n ? bi : k;
+    piv[k] = p_sh;
+  }
+  __syncthreads();
+  const int p = p_sh;
+  if (p != k)
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const double2 t = A[(size_t)k * n + j];
+      A[(size_t)k * n + j] = A[(size_t)p * n + j];
+      A[(size_t)p * n + j] = t;
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double2 d = A[(size_t)k * n + k];
+    pivabs[k] = sqrt(cabs2(d));
+    dinv_sh = crecip(d);
+  }
+  __syncthreads();
+  const double2 dinv = dinv_sh;
+  for (int j = threadIdx.x; j < n; j += blockDim.x)
+    A[(size_t)k * n + j] = j == k ? dinv : cmul(A[(size_t)k * n + j], dinv);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) fcol[i] = i == k ? cz() : A[(size_t)i * n + k];
+}
+// part 2: rows i != k: A(i,j) -= f_i A(k,j) (j != k), A(i,k) = -f_i / pivot
+__global__ void k_gj_update(int n, int k, double2* __restrict__ A, const double2* __restrict__ fcol) {
+  const int i = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n || i == k) return;
+  const double2 f = fcol[i], pk = A[(size_t)k * n + j];
+  double2& a = A[(size_t)i * n + j];
+  a = j == k ? make_double2(-(f.x * pk.x - f.y * pk.y), -(f.x * pk.y + f.y * pk.x)) : cfms(f, pk, a);
+}
+// undo the row interchanges as column interchanges, last pivot first (one thread per row)
+__global__ void k_gj_unpermute(int n, double2* __restrict__ A, const int* __restrict__ piv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double2* row = A + (size_t)i * n;
+  for (int k = n - 1; k >= 0; --k) {
+    const int p = piv[k];
+    if (p != k) {
+      const double2 t = row[k];
+      row[k] = row[p];
+      row[p] = t;
+    }
+  }
+}
+// signed C^s^T entries of the augmentation columns into the A_bc-like coupling rhs
+__global__ void k_add_aug(int cnt, int NB, int NC, const int* __restrict__ s_, const int* __restrict__ kb,
+                          const int* __restrict__ kc, const double* __restrict__ val, double2* __restrict__ Abc) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cnt) return;
+  double2& t = Abc[((size_t)s_[e] * NB + kb[e]) * NC + kc[e]];
+  t.x += val[e];
+}
+// v -= Q Q^T v edge by edge (feti.cpp:572-578): one warp per edge, its columns in order
+// (plane strain: tx, ty, rot — rot overlaps one translation), edges are disjoint.
+__global__ void k_project_aug(int n_edges, const int* __restrict__ edge_col0, const int* __restrict__ edge_ncol,
+                              const int* __restrict__ col_ptr, const int* __restrict__ rows,
+                              const double* __restrict__ vals, double2* __restrict__ v) {
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (e >= n_edges) return;
+  for (int c = edge_col0[e]; c < edge_col0[e] + edge_ncol[e]; ++c) {
+    double2 coef = cz();
+    for (int q = col_ptr[c] + lane; q < col_ptr[c + 1]; q += 32) coef = cadd(coef, cscale(v[rows[q]], vals[q]));
+    coef = warp_sum2(coef);
+    __syncwarp();
+    for (int q = col_ptr[c] + lane; q < col_ptr[c + 1]; q += 32) v[rows[q]] = csub(v[rows[q]], cscale(coef, vals[q]));
+    __syncwarp();
   }
 }
 
@@ -1344,6 +1477,44 @@ __global__ void __launch_bounds__(THREADS) k_cgs_pass(CgsArgs a) {
     __threadfence_block();
     __syncthreads();
     if (warp == 0) givens_warp(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384);
+  }
+}
+
+// Augmented Arnoldi step, scalar physics (one column per edge, rows = the edge's multiplier
+// rows): w = P F z in one pass, one warp per edge — the dual-operator tail gathered per row
+// (dual_tail_row), the edge coefficient q^T w reduced in the warp, w -= coef q, stored.
+struct EdgeGatherArgs {
+  int n_edges, NB, NC;
+  const int *col_ptr, *col_rows;
+  const double* col_vals;
+  const int *lam_lo, *lam_hi, *cglob;
+  const double2 *u1b, *cpl_b, *z;
+  double2* w;
+};
+__global__ void k_gather_project_edges(EdgeGatherArgs a) {
+  constexpr int MAXR = 4;  // up to 128 rows per edge
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (e >= a.n_edges) return;
+  const int q0 = a.col_ptr[e], len = a.col_ptr[e + 1] - q0;
+  double2 w[MAXR];
+  double qv[MAXR];
+  double2 coef = cz();
+#pragma unroll
+  for (int t = 0; t < MAXR; ++t) {
+    const int k = lane + 32 * t;
+    w[t] = cz();
+    qv[t] = 0.0;
+    if (k < len) {
+      qv[t] = a.col_vals[q0 + k];
+      w[t] = dual_tail_row(a, a.col_rows[q0 + k], false);
+      coef = cadd(coef, cscale(w[t], qv[t]));
+    }
+  }
+  coef = warp_sum2(coef);
+#pragma unroll
+  for (int t = 0; t < MAXR; ++t) {
+    const int k = lane + 32 * t;
+    if (k < len) a.w[a.col_rows[q0 + k]] = csub(w[t], cscale(coef, qv[t]));
   }
 }
 

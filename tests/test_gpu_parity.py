@@ -209,3 +209,53 @@ def test_plane_strain_matches_oracle(fetigpu, oracle_mod):
         assert rel(out[k], ref[k]) <= 1e-8, k
     assert abs(out["plus_stats"]["iterations"] - ref["plus_stats"]["iterations"]) <= 2
     assert abs(out["minus_stats"]["iterations"] - ref["minus_stats"]["iterations"]) <= 2
+
+
+@pytest.mark.parametrize("n,s,phi", [(16, 2, 2e-8), (64, 4, 1e-4), (128, 8, 1e-6)])
+def test_augmented_feti_matches_oracle(fetigpu, oracle_mod, n, s, phi):
+    """Edge-RBM augmentation: augmented coupling/coarse (dense, pivoted),
+    projected dual space.  Operators, FETI solves and iteration counts vs the oracle."""
+    p = fetigpu.make_seeded_problem(n, phi, seed=2)
+    c = -1j / np.sqrt(phi)
+    gpu = fetigpu.SchurSolver(p, s, s, tol=1e-10, max_iter=2000, augment=True)
+    ref = oracle_mod.Feti(oracle_mod.Problem(n), s, s, c, tol=1e-10, max_iter=2000, augment=True)
+    rng = np.random.default_rng(17)
+    lam = rng.uniform(-1, 1, ref.n_lambda) + 1j * rng.uniform(-1, 1, ref.n_lambda)
+    assert rel(gpu.apply_dual_operator(lam), ref.apply_dual_operator(lam)) <= 1e-11
+    assert rel(gpu.apply_dirichlet_preconditioner(lam), ref.apply_dirichlet_preconditioner(lam)) <= 1e-12
+    rhs = rng.uniform(-1, 1, p.n) + 0j
+    x, st = gpu.feti_solve(rhs)
+    xo, so = ref.solve(rhs)
+    gpu.close()
+    assert st["converged"] and so["converged"]
+    assert rel(x, xo) <= 1e-8
+    assert abs(st["iterations"] - so["iterations"]) <= 2
+
+
+def test_augmented_spans_interface_zero_iterations(fetigpu, oracle_mod):
+    """test_feti.cpp:407-425: H/h = 2, the edge modes span the whole interface."""
+    p = fetigpu.make_seeded_problem(16, 1e-4, seed=0)
+    gpu = fetigpu.SchurSolver(p, 8, 8, tol=1e-10, max_iter=100, augment=True)
+    rhs = np.random.default_rng(53).standard_normal(p.n) + 0j
+    x, st = gpu.feti_solve(rhs)
+    gpu.close()
+    ref = oracle_mod.Feti(oracle_mod.Problem(16), 8, 8, -1j / np.sqrt(1e-4), tol=1e-10, augment=True)
+    xo, so = ref.solve(rhs)
+    assert st["converged"] and st["iterations"] == 0 == so["iterations"]
+    assert rel(x, xo) <= 1e-9
+
+
+def test_augmented_schur_matches_oracle(fetigpu, oracle_mod):
+    """Range-space Schur solve with augmentation, config-1 mesh, vs the oracle."""
+    n, s, phi = 64, 4, 1e-4
+    p = fetigpu.make_seeded_problem(n, phi, seed=1)
+    ref = oracle_mod.Problem(n).schur_solve(s, s, phi, p.target_state, None, tol=1e-10, max_iter=2000, threads=4,
+                                            augment=True)
+    solver = fetigpu.SchurSolver(p, s, s, tol=1e-10, max_iter=2000, augment=True)
+    out = solver.solve()
+    solver.close()
+    assert out["converged"]
+    for k in ("y", "u", "lambda"):
+        assert rel(out[k], ref[k]) <= 1e-8, k
+    assert abs(out["plus_stats"]["iterations"] - ref["plus_stats"]["iterations"]) <= 2
+    assert abs(out["minus_stats"]["iterations"] - ref["minus_stats"]["iterations"]) <= 2
