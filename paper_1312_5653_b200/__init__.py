@@ -329,7 +329,7 @@ def _schur_result(y, u, lam, st):
     return d
 
 
-def solve_range_space(problem: ControlProblem, method="feti", tol=1e-12, s_x=2, s_y=2, augment=False,
+def solve_range_space(problem: ControlProblem, method="feti", tol=1e-12, s_x=2, s_y=2, augment=True,
                       max_iter=1000):
     """Dual solve through the two complex-conjugate factors, then primal recovery
     (bindings.cpp:93-111).  Only the FETI-DP method runs on the B200 path."""
@@ -343,7 +343,7 @@ def solve_range_space(problem: ControlProblem, method="feti", tol=1e-12, s_x=2, 
         solver.close()
 
 
-def feti_solve(problem: ControlProblem, mass_coeff, rhs, s_x=2, s_y=2, augment=False, tol=1e-10, max_iter=1000):
+def feti_solve(problem: ControlProblem, mass_coeff, rhs, s_x=2, s_y=2, augment=True, tol=1e-10, max_iter=1000):
     """FETI-DP solve of (K + mass_coeff V) x = rhs (bindings.cpp:158-185)."""
     solver = SchurSolver(problem, s_x, s_y, tol, max_iter, mass_coeff=mass_coeff, augment=augment)
     try:

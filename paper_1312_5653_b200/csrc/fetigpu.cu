@@ -1589,13 +1589,13 @@ int fetigpu_target_sine(const fetigpu_desc* desc, unsigned long long seed, int m
 int fetigpu_create(const fetigpu_desc* desc, fetigpu_ctx** out) {
   return guard([&] {
     validate_desc(desc);
+    auto c = std::make_unique<Ctx>();
+    c->desc = *desc;
+    c->P = build_problem(*desc);  // host-side contract / numerical checks first
+    c->H = build_partition(c->P, desc->s_x, desc->s_y, desc->augment != 0);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw RuntimeError("fetigpu: no CUDA device");
     if (desc->device < 0 || desc->device >= ndev) throw ContractError("fetigpu: bad device ordinal");
-    auto c = std::make_unique<Ctx>();
-    c->desc = *desc;
-    c->P = build_problem(*desc);
-    c->H = build_partition(c->P, desc->s_x, desc->s_y, desc->augment != 0);
     if (desc->phi > 0.0) {
       c->phi = desc->phi;
       c->mc = cd(0.0, -1.0 / std::sqrt(desc->phi));  // c = 1/(i sqrt(phi)), control.cpp:116

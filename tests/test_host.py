@@ -89,8 +89,11 @@ def test_contract_errors(fetigpu):
     for sx, sy in ((4, 2), (6, 6), (1, 1)):  # test_feti.cpp:70-77
         with pytest.raises(ValueError):
             F.partition_info(p, sx, sy)
-    with pytest.raises(ValueError):
-        F.SchurSolver(F.make_thermal_problem(8, 1e-4), 2, 2, augment=True)
+    # augmentation: a one-node edge has no rotation mode (feti.cpp:219-222) -> NumericalError,
+    # raised by the host partition before any device work
+    q = F.make_problem(12, 4, 1e-4, physics=1, len_x=3.0, len_y=1.0, young=20.7e6, poisson=0.45)
+    with pytest.raises(RuntimeError, match="rotation"):
+        F.SchurSolver(q, 2, 2, augment=True)
     with pytest.raises(ValueError):
         F.solve_range_space(F.make_thermal_problem(8, 1e-4), method="direct")
 
