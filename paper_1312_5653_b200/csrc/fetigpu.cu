@@ -157,8 +157,13 @@ struct Ctx {
   static constexpr int kCgsThreads = 512, kCgsRows = 256;  // k_cgs_pass block shape
   // fused Arnoldi tail (k_arnoldi_tail): rows per thread (0 = off), grid, barrier words
   int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_minb = 1;
+  static constexpr int kBodyUnroll = 4;
+  int body_unroll = 1;
   unsigned int* d_bar = nullptr;
   unsigned long long* d_tstamp = nullptr;  // FETIGPU_TAIL_TIMES=1: per-phase timestamps
+  unsigned long long* d_span = nullptr;    // FETIGPU_STEP_TIMES=1: kernel spans per Arnoldi step
+  bool span_on = false;
+  bool in_arnoldi = false;  // sym_args: Arnoldi-step GEMVs (skip check of the unrolled body)
   int mdot_blocks = 0, mdot_chunk = 0;
   // mass solve (Kronecker tridiagonal)
   double *d_mx_cp = nullptr, *d_mx_dinv = nullptr, *d_my_cp = nullptr, *d_my_dinv = nullptr;
@@ -433,6 +438,31 @@ struct Ctx {
     }
   }
   int vcap_hint() const { return std::max(2, desc.max_iter + 1); }
+  void report_step_spans(int it0, int it1) {
+    const int cnt = it1 - it0;
+    if (cnt <= 1) return;
+    std::vector<unsigned long long> t((size_t)6 * cnt);
+    CU(cudaMemcpy(t.data(), d_span + (size_t)6 * it0, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    double acc[6] = {};
+    int used = 0;
+    for (int i = 0; i + 1 < cnt; ++i) {  // precond, gap, dual, gap, tail, gap to the next precond
+      const unsigned long long* a = &t[(size_t)i * 6];
+      const unsigned long long* b = &t[(size_t)(i + 1) * 6];
+      acc[0] += (double)(a[1] - a[0]);
+      acc[1] += (double)a[2] - (double)a[1];
+      acc[2] += (double)(a[3] - a[2]);
+      acc[3] += (double)a[4] - (double)a[3];
+      acc[4] += (double)(a[5] - a[4]);
+      acc[5] += (double)b[0] - (double)a[5];
+      ++used;
+    }
+    std::fprintf(stderr, "[fetigpu] step spans (us, mean of %d): precond %.2f | gap %.2f | dual %.2f | gap %.2f | "
+                 "tail %.2f | gap %.2f\n", used, acc[0] / used / 1e3, acc[1] / used / 1e3, acc[2] / used / 1e3,
+                 acc[3] / used / 1e3, acc[4] / used / 1e3, acc[5] / used / 1e3);
+    std::vector<unsigned long long> init((size_t)6 * cnt);
+    for (size_t q = 0; q < init.size(); q += 2) init[q] = ~0ULL, init[q + 1] = 0ULL;
+    CU(cudaMemcpy(d_span + (size_t)6 * it0, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  }
   void report_tail_times(int it0, int it1) {
     const int cnt = it1 - it0;
     if (cnt <= 0) return;
@@ -713,6 +743,13 @@ struct Ctx {
     mdot_blocks = std::max(1, cdiv(nown, kCgsRows));
     mdot_chunk = kCgsRows;
     setup_fused_tail();
+    if (std::getenv("FETIGPU_STEP_TIMES")) {
+      const size_t ns = (size_t)6 * (vcap_hint() + 2);
+      d_span = alloc<unsigned long long>(ns);
+      std::vector<unsigned long long> init(ns);
+      for (size_t q = 0; q < ns; q += 2) init[q] = ~0ULL, init[q + 1] = 0ULL;
+      CU(cudaMemcpy(d_span, init.data(), ns * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    }
     d_part = alloc<double2>((size_t)(vcap + 2) * std::max(mdot_blocks, 2 * tail_grid));  // tail: 2 halves
     d_red = alloc<double2>(3 * (vcap + 2));
     d_y = alloc<double2>(vcap + 2);
@@ -983,6 +1020,11 @@ struct Ctx {
     g.lam_hi = d_lam_hi;
     g.bi_idx = d_bi_idx;
     g.bi_val = d_bi_val;
+    if (span_on) {
+      g.span = d_span;
+      g.it_ptr = &d_gst->iterations;
+    }
+    if (in_arnoldi && tail_rpt > 0) g.cont_ptr = &d_gst->cont;
     return g;
   }
   // local dual solve u1_b = S_bb^-1 t_b with t_b = -B^T lam, gcp = cpl_b^T t_b, and (last
@@ -1149,6 +1191,8 @@ struct Ctx {
     };
     // z = P V_j (per-subdomain S_bb apply); the dual GEMV gathers its input straight from it
     mark(1);
+    span_on = d_span != nullptr;
+    in_arnoldi = true;
     precond_gemv(d_V, &d_gst->j);
     mark(2);
     {
@@ -1157,6 +1201,8 @@ struct Ctx {
       g.wb = d_wb;
       dual_gemv(g, tail_rpt > 0);
     }
+    span_on = false;
+    in_arnoldi = false;
     mark(3);
     if (tail_rpt > 0) {  // coarse + CGS2 + Givens + normalisation in one launch
       ArnoldiTailArgs t{};
@@ -1183,6 +1229,7 @@ struct Ctx {
       t.cpl_b = d_cpl_b;
       t.ga = GivensArgs{d_gst, h1, h2, d_R, d_gcos, d_gsin, d_gvec, in_graph ? 1 : 0, arnoldi_handle};
       t.tstamp = d_tstamp;
+      t.span = d_span;
       t.hcap = vcap + 2;
       t.vcap = vcap;
       launch(FETIGPU_K_ORTHO, [&] {
@@ -1273,11 +1320,15 @@ struct Ctx {
     const long long before = launches;
     const bool was_prof = prof;
     prof = false;
+    // the fused-tail step is three kernels that each return at once when the cycle has
+    // stopped, so the body holds `body_unroll` steps (fewer WHILE-node round trips)
+    body_unroll = tail_rpt > 0 ? kBodyUnroll : 1;
+    if (const char* e = std::getenv("FETIGPU_UNROLL")) body_unroll = tail_rpt > 0 ? std::max(1, std::atoi(e)) : 1;
     CU(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    arnoldi_step(true);
+    for (int u = 0; u < body_unroll; ++u) arnoldi_step(true);
     CU(cudaStreamEndCapture(stream, &body));
     prof = was_prof;
-    arnoldi_body_kernels = (int)(launches - before);
+    arnoldi_body_kernels = (int)(launches - before) / body_unroll;
     launches = before;
     CU(cudaGraphInstantiate(&arnoldi_exec, arnoldi_graph, 0));
   }
@@ -1349,7 +1400,10 @@ struct Ctx {
           }
         }
         sync();
-        launches += (long long)arnoldi_body_kernels * (h_gst->iterations - iterations);
+        {
+          const int steps = h_gst->iterations - iterations;
+          launches += (long long)arnoldi_body_kernels * body_unroll * ((steps + body_unroll - 1) / body_unroll);
+        }
       } else {
         do {
           arnoldi_step(false);
@@ -1360,6 +1414,7 @@ struct Ctx {
       }
       if (h_gst->status) throw NumericalError("gmres: breakdown (NaN/Inf in Arnoldi)");
       if (d_tstamp) report_tail_times(iterations, h_gst->iterations);
+      if (d_span) report_step_spans(iterations, h_gst->iterations);
       iterations = h_gst->iterations;
       // back substitution and x += P^-1 (Q y)  (krylov.hpp:191-209), true residual r = b - F x
       launch(FETIGPU_K_ORTHO, [&] { k_backsub<<<1, 32, 0, stream>>>(d_gst, d_R, d_gvec, d_y); });

@@ -575,6 +575,21 @@ __global__ void k_pack_sym(int S, int NB, int NT, const double2* __restrict__ fu
   pack[gid] = (r < NB && c < NB) ? full[((size_t)s * NB + r) * NB + c] : cz();
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// optional kernel-span instrumentation (FETIGPU_STEP_TIMES=1): span[(it * 3 + kid) * 2 + {0,1}]
+// = earliest CTA start / latest CTA end of kernel kid (0 precond, 1 dual, 2 tail) of Arnoldi
+// step `it` (read from the GMRES state)
+__device__ __forceinline__ void span_mark(unsigned long long* span, const int* it_ptr, int kid, int end) {
+  if (span == nullptr || threadIdx.x != 0) return;
+  unsigned long long* p = span + ((size_t)(*it_ptr) * 3 + kid) * 2 + end;
+  if (end) atomicMax(p, gtimer());
+  else atomicMin(p, gtimer());
+}
+
 struct SymGemvArgs {
   int NB, NT, NC, NI, EBI;
   const double2* pack;  // [S][sym_tile_entries(NT)]
@@ -603,6 +618,10 @@ struct SymGemvArgs {
   const int* corner_slots;
   const double2* fc;
   double2* g;
+  unsigned long long* span;  // FETIGPU_STEP_TIMES (Arnoldi-step GEMVs only)
+  const int* it_ptr;
+  // unrolled WHILE body: a step after the cycle stopped (cont == 0) returns at once
+  const int* cont_ptr;
   // MODE 2 coarse rhs: the nonzeros of A_ic per (subdomain, corner), AE per corner
   int AE;
   const int* aic_idx;
@@ -622,6 +641,8 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(S
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
   pdl_wait();
+  if (a.cont_ptr != nullptr && *a.cont_ptr == 0) return;
+  span_mark(a.span, a.it_ptr, MODE, 0);
   // ---- input vector (B^T scatter) ----
   const double2* lam = a.lam;
   if (MODE == 0 && a.jsel != nullptr) lam += (size_t)(*a.jsel) * a.jstride;
@@ -754,6 +775,10 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(S
         if (threadIdx.x == 0) *a.g_counter = 0u;
       }
     }
+  }
+  if (a.span != nullptr) {
+    __syncthreads();
+    span_mark(a.span, a.it_ptr, MODE, 1);
   }
 }
 
@@ -1633,14 +1658,11 @@ struct ArnoldiTailArgs {
   const double2 *u1b, *cpl_b;
   GivensArgs ga;
   unsigned long long* tstamp;  // optional phase timestamps (block 0), 8 per Arnoldi step
+  unsigned long long* span;    // FETIGPU_STEP_TIMES
 };
 
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
+
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1750,9 +1772,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   const bool act = r < a.n;
   pdl_trigger();
   pdl_wait();
+  if (a.st->cont == 0) return;  // unrolled WHILE body: the cycle already stopped
   const int nv = a.st->j + 1, nout = nv + 1, G = gridDim.x;
   const int it = a.st->iterations;
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 0] = gtimer();
+  span_mark(a.span, &it, 2, 0);
   // dual-tail operands that do not depend on z (loaded before the barrier)
   double2 u[2] = {cz(), cz()}, cpv[2][NCM];
   int cgv[2][NCM];
@@ -1900,6 +1924,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
     }
     if (warp == 0) givens_warp<true>(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384, hs1, hs2);
     if (a.tstamp && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 9] = gtimer();
+  }
+  if (a.span != nullptr) {
+    __syncthreads();
+    span_mark(a.span, &it, 2, 1);
   }
 }
 
