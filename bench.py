@@ -287,6 +287,18 @@ def run_gpu(args):
         pass
     kernel_breakdown = {c: {"ms_per_step": v["ms"] / steps, "launches_per_step": v["launches"] / steps}
                         for c, v in prof.items() if v["launches"]}
+    # in-graph kernel spans (first CTA start .. last CTA end, %globaltimer) of the last
+    # FETI solve of the timed device run above: the GEMVs' streaming rate without the
+    # per-launch event brackets of the profiling pass
+    device_step(warmup)
+    torch.cuda.synchronize()
+    spans = solver.step_spans()
+    in_graph = None
+    if spans:
+        in_graph = {"spans_us": {k: round(v, 3) for k, v in spans.items() if k != "steps"}, "steps": spans["steps"]}
+        for cls, key in (("precond_gemv", "precond"), ("dual_gemv", "dual")):
+            gbs = solver.class_bytes(cls) / (spans[key] * 1e-6) / 1e9
+            in_graph[cls] = {"achieved_gbs": gbs, "frac": gbs / hbm_peak}
     # per-solve HBM bytes of the local operators (both GEMV classes) -> effective GB/s
     iters = np.mean([a + b for a, b in its])
     line = {
@@ -309,7 +321,7 @@ def run_gpu(args):
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": kclass, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
-                     "bytes_per_launch": kb, "avg_launch_ms": avg_ms},
+                     "bytes_per_launch": kb, "avg_launch_ms": avg_ms, "in_graph": in_graph},
         "clocks": clk.summary(),
     }
     # BASELINE config 2 is a phi sweep: rates and iteration counts per phi (own factors each)

@@ -167,6 +167,12 @@ long long fetigpu_launch_count(fetigpu_ctx* ctx, int reset);
 int fetigpu_profile(fetigpu_ctx* ctx, int enable);
 int fetigpu_profile_read(fetigpu_ctx* ctx, double* ms, long long* launches, int reset);
 
+/* Mean in-graph kernel spans (us, first CTA start to last CTA end, %globaltimer) over the
+ * Arnoldi steps of the context's last FETI solve: out6 = {precond GEMV, gap, dual GEMV,
+ * gap, Arnoldi tail, gap to the next step}.  Returns the number of steps averaged (0 if
+ * none were recorded, e.g. on the sharded path). */
+int fetigpu_step_spans(fetigpu_ctx* ctx, double* out6);
+
 /* Algorithmic bytes per launch of a kernel class (the roofline numerator). */
 double fetigpu_class_bytes(fetigpu_ctx* ctx, int klass);
 

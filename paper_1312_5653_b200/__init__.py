@@ -275,6 +275,18 @@ class SchurSolver:
         _check(_native.lib().fetigpu_profile_read(self._h, _dp(ms), n, int(reset)))
         return {k: {"ms": float(ms[i]), "launches": int(n[i])} for i, k in enumerate(_native.K_CLASSES)}
 
+    def step_spans(self):
+        """Mean in-graph kernel spans (us) of the last FETI solve's Arnoldi steps:
+        dict(precond, gap_pd, dual, gap_dt, tail, gap_tp, steps) or None."""
+        out = np.zeros(6)
+        k = _native.lib().fetigpu_step_spans(self._h, _dp(out))
+        if k <= 0:
+            return None
+        keys = ("precond", "gap_pd", "dual", "gap_dt", "tail", "gap_tp")
+        d = dict(zip(keys, (float(v) for v in out)))
+        d["steps"] = int(k)
+        return d
+
     def class_bytes(self, klass):
         return float(_native.lib().fetigpu_class_bytes(self._h, _native.K_CLASSES.index(klass)))
 

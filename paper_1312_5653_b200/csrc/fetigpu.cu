@@ -74,6 +74,8 @@ struct Ctx {
   ElemAe elem_ae{};
   ElemKM elem_km{};
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host-API result copies (created on first use)
+  cudaEvent_t ev_out = nullptr;
   cd mc;       // mass coefficient of the factored operator K + mc V
   double phi = 0;
   SubLayout L{};
@@ -161,7 +163,12 @@ struct Ctx {
   int body_unroll = 1;
   unsigned int* d_bar = nullptr;
   unsigned long long* d_tstamp = nullptr;  // FETIGPU_TAIL_TIMES=1: per-phase timestamps
-  unsigned long long* d_span = nullptr;    // FETIGPU_STEP_TIMES=1: kernel spans per Arnoldi step
+  // kernel spans per Arnoldi step (earliest CTA start / latest CTA end, %globaltimer) of the
+  // last FETI solve: always recorded on one GPU (two atomics per CTA); FETIGPU_STEP_TIMES=1
+  // prints them per cycle, fetigpu_step_spans() returns their means
+  unsigned long long* d_span = nullptr;
+  bool print_spans = false;
+  int last_gmres_steps = 0;
   bool span_on = false;
   bool in_arnoldi = false;  // sym_args: Arnoldi-step GEMVs (skip check of the unrolled body)
   int mdot_blocks = 0, mdot_chunk = 0;
@@ -183,6 +190,8 @@ struct Ctx {
     if (arnoldi_exec) cudaGraphExecDestroy(arnoldi_exec);
     if (arnoldi_graph) cudaGraphDestroy(arnoldi_graph);
     if (stream) cudaStreamDestroy(stream);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (ev_out) cudaEventDestroy(ev_out);
   }
 
   template <typename T>
@@ -459,9 +468,27 @@ struct Ctx {
     std::fprintf(stderr, "[fetigpu] step spans (us, mean of %d): precond %.2f | gap %.2f | dual %.2f | gap %.2f | "
                  "tail %.2f | gap %.2f\n", used, acc[0] / used / 1e3, acc[1] / used / 1e3, acc[2] / used / 1e3,
                  acc[3] / used / 1e3, acc[4] / used / 1e3, acc[5] / used / 1e3);
-    std::vector<unsigned long long> init((size_t)6 * cnt);
-    for (size_t q = 0; q < init.size(); q += 2) init[q] = ~0ULL, init[q + 1] = 0ULL;
-    CU(cudaMemcpy(d_span + (size_t)6 * it0, init.data(), init.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+  }
+  // mean kernel spans (us) over the Arnoldi steps of the last FETI solve: precond, gap,
+  // dual, gap, tail, gap; returns the number of steps averaged
+  int step_spans(double* out6) {
+    if (!d_span || last_gmres_steps < 2) return 0;
+    const int cnt = last_gmres_steps;
+    std::vector<unsigned long long> t((size_t)6 * cnt);
+    CU(cudaMemcpy(t.data(), d_span, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    double acc[6] = {};
+    for (int i = 0; i + 1 < cnt; ++i) {
+      const unsigned long long* a = &t[(size_t)i * 6];
+      const unsigned long long* b = &t[(size_t)(i + 1) * 6];
+      acc[0] += (double)(a[1] - a[0]);
+      acc[1] += (double)a[2] - (double)a[1];
+      acc[2] += (double)(a[3] - a[2]);
+      acc[3] += (double)a[4] - (double)a[3];
+      acc[4] += (double)(a[5] - a[4]);
+      acc[5] += (double)b[0] - (double)a[5];
+    }
+    for (int q = 0; q < 6; ++q) out6[q] = acc[q] / (cnt - 1) / 1e3;
+    return cnt - 1;
   }
   void report_tail_times(int it0, int it1) {
     const int cnt = it1 - it0;
@@ -743,12 +770,9 @@ struct Ctx {
     mdot_blocks = std::max(1, cdiv(nown, kCgsRows));
     mdot_chunk = kCgsRows;
     setup_fused_tail();
-    if (std::getenv("FETIGPU_STEP_TIMES")) {
-      const size_t ns = (size_t)6 * (vcap_hint() + 2);
-      d_span = alloc<unsigned long long>(ns);
-      std::vector<unsigned long long> init(ns);
-      for (size_t q = 0; q < ns; q += 2) init[q] = ~0ULL, init[q + 1] = 0ULL;
-      CU(cudaMemcpy(d_span, init.data(), ns * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    if (!dist()) {
+      d_span = alloc<unsigned long long>((size_t)6 * (vcap_hint() + 2));
+      print_spans = std::getenv("FETIGPU_STEP_TIMES") != nullptr;
     }
     d_part = alloc<double2>((size_t)(vcap + 2) * std::max(mdot_blocks, 2 * tail_grid));  // tail: 2 halves
     d_red = alloc<double2>(3 * (vcap + 2));
@@ -1191,7 +1215,7 @@ struct Ctx {
     };
     // z = P V_j (per-subdomain S_bb apply); the dual GEMV gathers its input straight from it
     mark(1);
-    span_on = d_span != nullptr;
+    span_on = d_span != nullptr;  // (one GPU only)
     in_arnoldi = true;
     precond_gemv(d_V, &d_gst->j);
     mark(2);
@@ -1344,6 +1368,11 @@ struct Ctx {
       return st;
     }
     const bool graph = use_graph && !prof && !dist();
+    if (d_span) {
+      const int cnt = 6 * (vcap_hint() + 2);
+      k_span_init<<<cdiv(cnt, 256), 256, 0, stream>>>(cnt, d_span);
+      ++launches;
+    }
     if (graph && !arnoldi_exec) build_arnoldi_graph();
     CU(cudaMemcpyAsync(d_r, b, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
     double best_res = 1.0;  // |b - F 0| / |b|
@@ -1414,7 +1443,7 @@ struct Ctx {
       }
       if (h_gst->status) throw NumericalError("gmres: breakdown (NaN/Inf in Arnoldi)");
       if (d_tstamp) report_tail_times(iterations, h_gst->iterations);
-      if (d_span) report_step_spans(iterations, h_gst->iterations);
+      if (print_spans) report_step_spans(iterations, h_gst->iterations);
       iterations = h_gst->iterations;
       // back substitution and x += P^-1 (Q y)  (krylov.hpp:191-209), true residual r = b - F x
       launch(FETIGPU_K_ORTHO, [&] { k_backsub<<<1, 32, 0, stream>>>(d_gst, d_R, d_gvec, d_y); });
@@ -1437,6 +1466,7 @@ struct Ctx {
     st.iterations = iterations;
     st.relative_residual = relres;
     st.converged = relres <= tol;
+    last_gmres_steps = iterations;
     return st;
   }
 
@@ -1511,8 +1541,11 @@ struct Ctx {
 
   // ------------------------------------------------------------------------ range space
   // solve_range_space (control.cpp:297-334) on device buffers.
+  // host_y/u/lam (host API): results are copied out inside the call — lambda and u on the
+  // copy stream as soon as they are final, overlapping the recovery of y
   void schur_solve(const double* ybar, const double* yc, double* y, double* u, double* lam,
-                   fetigpu_schur_stats* out) {
+                   fetigpu_schur_stats* out, double* host_y = nullptr, double* host_u = nullptr,
+                   double* host_lam = nullptr) {
     auto t0 = std::chrono::steady_clock::now();
     // rhs = K ybar + Kc yc  (control.cpp:15)
     apply_global<double>(ybar, (yc && m > 0) ? yc : nullptr, 1.0, 0.0, d_real0);
@@ -1523,8 +1556,19 @@ struct Ctx {
     launch(FETIGPU_K_OTHER, [&] { k_conj<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x, d_x2); });
     apply_global<double2>(d_x2, nullptr, 0.0, 1.0, d_rhs);
     fetigpu_feti_stats sm = feti_solve(d_rhs, d_x, 4);
-    // lambda = Re t = Re t'; imag leak = max |Im t'|
-    launch(FETIGPU_K_GLOBAL, [&] { k_realify<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x, lam); });
+    // lambda = Re t = Re t', u = lambda / phi; imag leak = max |Im t'|
+    launch(FETIGPU_K_GLOBAL, [&] { k_realify_u<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x, 1.0 / phi, lam, u); });
+    const size_t nbytes = sizeof(double) * n;
+    if (host_lam != nullptr) {
+      if (!copy_stream) {
+        CU(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+      }
+      CU(cudaEventRecord(ev_out, stream));
+      CU(cudaStreamWaitEvent(copy_stream, ev_out, 0));
+      CU(cudaMemcpyAsync(host_lam, lam, nbytes, cudaMemcpyDeviceToHost, copy_stream));
+      CU(cudaMemcpyAsync(host_u, u, nbytes, cudaMemcpyDeviceToHost, copy_stream));
+    }
     const int blocks = std::max(1, std::min(296, cdiv(n, 256)));
     launch(FETIGPU_K_GLOBAL, [&] {
       k_imag_max_part<<<blocks, 256, 0, stream>>>(n, d_x, reinterpret_cast<double*>(d_part));
@@ -1535,14 +1579,14 @@ struct Ctx {
     // y = ybar - V^-1 K lambda ; u = lambda / phi  (control.cpp:323-325)
     apply_global<double>(lam, nullptr, 1.0, 0.0, d_real1);
     mass_solve(d_real1);
-    launch(FETIGPU_K_GLOBAL, [&] {
-      k_recover_yu<<<cdiv(n, 256), 256, 0, stream>>>(n, ybar, d_real1, lam, 1.0 / phi, y, u);
-    });
+    launch(FETIGPU_K_GLOBAL, [&] { k_recover_y<<<cdiv(n, 256), 256, 0, stream>>>(n, ybar, d_real1, y); });
+    if (host_y != nullptr) CU(cudaMemcpyAsync(host_y, y, nbytes, cudaMemcpyDeviceToHost, stream));
     // |lambda|_inf for the leak warning
     launch(FETIGPU_K_GLOBAL, [&] { k_real_to_complex<<<cdiv(n, 256), 256, 0, stream>>>(n, lam, d_ax); });
     norm_async(d_ax, n, 9);
     stats_to_host();
     sync();  // the call's one final synchronisation
+    if (host_lam != nullptr) CU(cudaStreamSynchronize(copy_stream));
     finalize_feti_stats(sp, 0);
     finalize_feti_stats(sm, 4);
     const double lmax = h_stat[9].y, leak = h_stat[8].y;
@@ -1789,11 +1833,7 @@ int fetigpu_schur_solve(fetigpu_ctx* ctx, const double* ybar, const double* yc, 
     double* dy = c.d_out_y;
     double* du = c.d_out_u;
     double* dl = c.d_out_l;
-    c.schur_solve(c.d_in_ybar, dyc, dy, du, dl, stats);
-    CU(cudaMemcpyAsync(y, dy, nb, cudaMemcpyDeviceToHost, c.stream));
-    CU(cudaMemcpyAsync(u, du, nb, cudaMemcpyDeviceToHost, c.stream));
-    CU(cudaMemcpyAsync(lambda, dl, nb, cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    c.schur_solve(c.d_in_ybar, dyc, dy, du, dl, stats, y, u, lambda);  // copies y, u, lambda out
     c.prof_collect();
   });
 }
@@ -1867,6 +1907,15 @@ int fetigpu_profile_read(fetigpu_ctx* ctx, double* ms, long long* launches, int 
       if (reset) c.prof_ms[k] = 0, c.prof_n[k] = 0;
     }
   });
+}
+
+int fetigpu_step_spans(fetigpu_ctx* ctx, double* out6) {
+  if (!ctx || !out6) return 0;
+  try {
+    return ctx->c->step_spans(out6);
+  } catch (...) {
+    return 0;
+  }
 }
 
 double fetigpu_class_bytes(fetigpu_ctx* ctx, int klass) { return ctx ? ctx->c->class_bytes(klass) : 0.0; }

@@ -590,6 +590,11 @@ __device__ __forceinline__ void span_mark(unsigned long long* span, const int* i
   else atomicMin(p, gtimer());
 }
 
+__global__ void k_span_init(int count, unsigned long long* span) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) span[i] = (i & 1) ? 0ULL : ~0ULL;
+}
+
 struct SymGemvArgs {
   int NB, NT, NC, NI, EBI;
   const double2* pack;  // [S][sym_tile_entries(NT)]
@@ -2149,6 +2154,20 @@ __global__ void __launch_bounds__(32 * LPB)
 __global__ void k_realify(int n, const double2* __restrict__ t, double* __restrict__ lam) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) lam[k] = t[k].x;
+}
+// lambda = Re t and u = lambda / phi (control.cpp:325) in one pass
+__global__ void k_realify_u(int n, const double2* __restrict__ t, double inv_phi, double* __restrict__ lam,
+                            double* __restrict__ u) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double l = t[k].x;
+  lam[k] = l;
+  u[k] = l * inv_phi;
+}
+__global__ void k_recover_y(int n, const double* __restrict__ ybar, const double* __restrict__ vk,
+                            double* __restrict__ y) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) y[k] = ybar[k] - vk[k];
 }
 __global__ void k_recover_yu(int n, const double* __restrict__ ybar, const double* __restrict__ vk,
                              const double* __restrict__ lam, double inv_phi, double* __restrict__ y,
