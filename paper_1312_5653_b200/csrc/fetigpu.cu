@@ -159,6 +159,8 @@ struct Ctx {
   static constexpr int kCgsThreads = 512, kCgsRows = 256;  // k_cgs_pass block shape
   // fused Arnoldi tail (k_arnoldi_tail): rows per thread (0 = off), grid, barrier words
   int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_minb = 1;
+  bool cgs_gram = false;       // FETIGPU_CGS=gram: one-reduction CGS2 via the Gram matrix
+  double2* d_gram = nullptr;
   static constexpr int kBodyUnroll = 4;
   int body_unroll = 1;
   unsigned int* d_bar = nullptr;
@@ -420,8 +422,11 @@ struct Ctx {
   }
   // one-launch Arnoldi tail when every block of its grid can be co-resident (one GPU only)
   static constexpr int kTailThreads = 512;
-  size_t tail_smem() const { return sizeof(double2) * ((size_t)kTailThreads + 2 * (size_t)(vcap_hint() + 2) + 640); }
+  size_t tail_smem() const {
+    return sizeof(double2) * (2 * (size_t)kTailThreads + 3 * (size_t)(vcap_hint() + 2) + 640 + (cgs_gram ? TAIL_GSM : 0));
+  }
   void setup_fused_tail() {
+    if (const char* e = std::getenv("FETIGPU_CGS")) cgs_gram = std::string(e) == "gram";
     if (dist() || H.NC > 4 || H.n_aug > 0 || nc > kTailThreads + 2 * (vcap_hint() + 2) ||
         std::getenv("FETIGPU_NO_FUSED_TAIL"))
       return;
@@ -432,11 +437,14 @@ struct Ctx {
     if (const char* e = std::getenv("FETIGPU_TAIL_MINB")) tail_minb = std::atoi(e) == 2 ? 2 : 1;
     auto kfn = tail_minb == 2 ? k_arnoldi_tail<kTailThreads, 4, 2> : k_arnoldi_tail<kTailThreads, 4, 1>;
     CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaFuncSetAttribute(k_arnoldi_tail<kTailThreads, 4, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTailThreads, smem));
     const int grid = std::max(1, cdiv(nown, kTailThreads));
     if (per_sm <= 0 || grid > per_sm * sms) return;
     tail_rpt = 1;
     tail_grid = grid;
+    if (cgs_gram) d_gram = alloc<double2>((size_t)vcap_hint() * (vcap_hint() + 1) / 2 + 1);
     const int rows = cdiv(std::max(nc, 1), tail_grid);
     tail_rb = rows <= 1 ? 1 : rows <= 2 ? 2 : rows <= 4 ? 4 : rows <= 8 ? 8 : 16;
     d_bar = alloc<unsigned int>(2);
@@ -1256,8 +1264,11 @@ struct Ctx {
       t.span = d_span;
       t.hcap = vcap + 2;
       t.vcap = vcap;
+      t.gram = d_gram;
       launch(FETIGPU_K_ORTHO, [&] {
-        if (tail_minb == 2)
+        if (cgs_gram)
+          kx(k_arnoldi_tail<kTailThreads, 4, 1, true>, tail_grid, kTailThreads, tail_smem(), t);
+        else if (tail_minb == 2)
           kx(k_arnoldi_tail<kTailThreads, 4, 2>, tail_grid, kTailThreads, tail_smem(), t);
         else
           kx(k_arnoldi_tail<kTailThreads, 4, 1>, tail_grid, kTailThreads, tail_smem(), t);
@@ -1434,10 +1445,20 @@ struct Ctx {
           launches += (long long)arnoldi_body_kernels * body_unroll * ((steps + body_unroll - 1) / body_unroll);
         }
       } else {
+        static const bool cgs_ratio = std::getenv("FETIGPU_CGS_RATIO") != nullptr;
         do {
+          const int nv_before = h_gst->j + 1;
           arnoldi_step(false);
           CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
           sync();
+          if (cgs_ratio) {  // diagnostics: |w - V h1| / |w| after CGS pass 1
+            std::vector<double2> h(nv_before + 1);
+            CU(cudaMemcpy(h.data(), d_red, h.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+            double s2 = 0;
+            for (int i = 0; i < nv_before; ++i) s2 += h[i].x * h[i].x + h[i].y * h[i].y;
+            const double w2 = h[nv_before].x;
+            std::fprintf(stderr, "[fetigpu] step %d ratio %.4f\n", h_gst->iterations, std::sqrt(std::max(0.0, 1.0 - s2 / w2)));
+          }
           if (h_gst->cont) ghost_refresh(d_V + (size_t)h_gst->j * ldv);  // sharded: next basis column
         } while (h_gst->cont);
       }

@@ -1651,6 +1651,8 @@ struct ArnoldiTailArgs {
   double2 *h1, *h2;
   unsigned int* bar;  // [0] arrivals, [1] generation
   int hcap, vcap;  // h staging capacity (>= nv + 1), basis columns allocated
+  // GRAM mode: packed columns of G = V^H V (column k at k(k+1)/2, entries v_i^H v_k, i <= k)
+  double2* gram;
   // coarse
   int nc, coarse_rb;  // rb: coarse rows per block per round (1, 2, 4 or 8)
   const double2* Cinv;
@@ -1762,14 +1764,25 @@ __device__ __forceinline__ void block_reduce_parts(const double2* __restrict__ p
 
 // Fused tail, one multiplier row per thread, THREADS rows per block, one block per SM.
 // dynamic smem: w_sh[THREADS] | h1[hcap] | h2[hcap] | Givens staging[640]
-template <int THREADS, int NCM, int MINB>
+// GRAM = true: CGS2 with ONE reduction per step.  Pass 1 reduces h1 = V^H w, |w|^2 and the
+// new Gram column g = V^H v_j together; the second CGS pass is then evaluated exactly in
+// algebra, h2 = V^H (w - V h1) = h1 - G h1 and |w - V h1|^2 = |w|^2 - |h1|^2 - Re h1^H h2,
+// and the new basis vector is (w - V (h1 + h2)) / h_{j+1,j} with the Pythagorean
+// h_{j+1,j} of the two-pass scheme.  G = V^H V carries the basis' actual loss of
+// orthogonality; what the algebra drops is the rounding of forming w - V h1, of relative
+// size eps |h1| / |w - V h1| (measured |w - V h1| / |w| >= 0.05 on the FETI operators).
+// dynamic smem: w_sh | vj_sh | hs1 | hs2 | gs | Givens staging | Gram staging (TAIL_GSM)
+constexpr int TAIL_GSM = 4096;
+template <int THREADS, int NCM, int MINB, bool GRAM = false>
 __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs a) {
   constexpr int WARPS = THREADS / 32, LPR = THREADS / 32;
   extern __shared__ double2 tail_sh[];
   double2* w_sh = tail_sh;
-  double2* hs1 = w_sh + THREADS;
+  double2* vj_sh = w_sh + THREADS;
+  double2* hs1 = vj_sh + THREADS;
   double2* hs2 = hs1 + a.hcap;
-  double2* stage = hs2 + a.hcap;
+  double2* gs = hs2 + a.hcap;
+  double2* stage = gs + a.hcap;
   __shared__ double2 cred[WARPS];
   __shared__ double inv_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1847,6 +1860,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   // pass-1 partials after barrier B while faster blocks already write pass-2 partials
   auto dots = [&](double2 w, double2* part) {
     w_sh[threadIdx.x] = w;
+    if (GRAM) vj_sh[threadIdx.x] = act ? a.V[(size_t)(nv - 1) * a.ldv + r] : cz();
     __syncthreads();
     for (int i = warp; i < nout; i += WARPS) {
       double2 acc = cz();
@@ -1857,6 +1871,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
         for (int q = 0; q < LPR; ++q) x[q] = v[min(lane + 32 * q, a.n - 1 - row0)];
 #pragma unroll
         for (int q = 0; q < LPR; ++q) acc = cfma_conj(x[q], w_sh[lane + 32 * q], acc);
+        if (GRAM) {  // Gram column entry v_i^H v_j from the same loads
+          double2 g = cz();
+#pragma unroll
+          for (int q = 0; q < LPR; ++q) g = cfma_conj(x[q], vj_sh[lane + 32 * q], g);
+          g = warp_sum2(g);
+          if (lane == 0) (part + (size_t)a.hcap * G)[(size_t)i * G + blockIdx.x] = g;
+        }
       } else {
 #pragma unroll
         for (int q = 0; q < LPR; ++q) acc.x += cabs2(w_sh[lane + 32 * q]);
@@ -1900,6 +1921,67 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   grid_sync_plain(a.bar);
   block_reduce_parts<THREADS>(a.part, G, nout, hs1);
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 4] = gtimer();
+  if constexpr (GRAM) {
+    block_reduce_parts<THREADS>(part2, G, nv, gs);  // gs[i] = v_i^H v_j (part2 = the Gram partials)
+    const int j = nv - 1;
+    if (blockIdx.x == 0)
+      for (int i = threadIdx.x; i < nv; i += THREADS) a.gram[(size_t)j * (j + 1) / 2 + i] = gs[i];
+    // h2 = h1 - G h1, one thread per row i, k ascending; the previous Gram columns are
+    // staged in shared memory first (all loads in flight) when they fit
+    const int cnt_old = j * (j + 1) / 2;
+    const bool staged = cnt_old <= TAIL_GSM;
+    double2* gsm = stage + 640;
+    if (staged) {
+      for (int e = threadIdx.x; e < cnt_old; e += THREADS) gsm[e] = __ldcg(a.gram + e);
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < nv; i += THREADS) {
+      double2 acc = cz();
+      for (int k = 0; k < nv; ++k) {
+        double2 gik;
+        if (k == j) gik = gs[i];
+        else if (i == j) gik = cconj(gs[k]);
+        else if (k >= i) gik = staged ? gsm[k * (k + 1) / 2 + i] : __ldcg(a.gram + (size_t)k * (k + 1) / 2 + i);
+        else gik = cconj(staged ? gsm[i * (i + 1) / 2 + k] : __ldcg(a.gram + (size_t)i * (i + 1) / 2 + k));
+        acc = cfma(gik, hs1[k], acc);
+      }
+      hs2[i] = csub(hs1[i], acc);
+    }
+    __syncthreads();
+    if (warp == 0) {  // |w - V h1|^2 = |w|^2 - |h1|^2 - Re h1^H h2  (fixed order)
+      double t = 0.0;
+      for (int i = lane; i < nv; i += 32) t += cabs2(hs1[i]) + (hs1[i].x * hs2[i].x + hs1[i].y * hs2[i].y);
+      t = warp_sum(t);
+      if (lane == 0) hs2[nv] = make_double2(hs1[nv].x - t, 0.0);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      bool finite;
+      const double hn = warp_hnext<true>(hs1, hs2, nv - 1, finite);
+      if (lane == 0) inv_sh = 1.0 / hn;
+    }
+    for (int i = threadIdx.x; i < nv; i += THREADS) gs[i] = cadd(hs1[i], hs2[i]);  // h = h1 + h2
+    __syncthreads();
+    if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 7] = gtimer();
+    if (nv < a.vcap) {
+      w = sub_vh(w, gs);
+      if (act) a.V[(size_t)nv * a.ldv + r] = cscale(w, inv_sh);
+    }
+    if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 8] = gtimer();
+    if (blockIdx.x == 0) {
+      for (int i = threadIdx.x; i < nout; i += THREADS) {
+        a.h1[i] = hs1[i];
+        a.h2[i] = hs2[i];
+      }
+      if (warp == 0) givens_warp<true>(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384, hs1, hs2);
+      if (a.tstamp && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 9] = gtimer();
+    }
+    if (a.span != nullptr) {
+      __syncthreads();
+      span_mark(a.span, &it, 2, 1);
+    }
+    return;
+  }
   // ---- phase 2: w -= V h1, h2 = V^H w, |w|^2 ----
   w = sub_vh(w, hs1);
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 5] = gtimer();
