@@ -119,6 +119,19 @@ int fetigpu_feti_solve(fetigpu_ctx* ctx, int sign, const double* rhs_c128, doubl
 int fetigpu_apply_dual(fetigpu_ctx* ctx, int sign, const double* lam_c128, double* out_c128);
 int fetigpu_apply_precond(fetigpu_ctx* ctx, int sign, const double* r_c128, double* out_c128);
 
+/* Full-space KKT method (solve_full_space, control.cpp:418-476; python solve_full_space,
+ * bindings.cpp:113-145): outer Krylov on [V 0 K; 0 phi V -V; K -V 0] with the Murphy-Golub-
+ * Wathen preconditioner.  precond 0 none, 1 "sp" (Pearson-Wathen K + V/sqrt(phi) through a
+ * second FETI factor), 2 "sc" (exact Schur through the context's complex FETI factor;
+ * requires outer = 1).  outer 0 MINRES, 1 GMRES (flexible when preconditioned).  The
+ * context's FETI tolerance is the inner tolerance.  stats: iterations / relative_residual /
+ * converged of the OUTER solve, n_lambda = 3n, coarse_dim = total inner FETI iterations,
+ * setup_seconds = preconditioner setup.  imag_leak (may be NULL): max |Im| of the last
+ * "sc" application. */
+int fetigpu_full_space(fetigpu_ctx* ctx, int precond, int outer, double tol, int max_iter, const double* ybar,
+                       const double* yc, double* y, double* u, double* lambda, fetigpu_feti_stats* stats,
+                       double* imag_leak);
+
 /* ---- sharded multi-GPU path ------------------------------------------
  * Rank r of R owns subdomain rows [r s_y/R, (r+1) s_y/R) (s_y % R == 0).  Per Krylov step
  * the ranks exchange cut-line interface values with their two neighbours and allreduce the

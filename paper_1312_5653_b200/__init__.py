@@ -6,6 +6,8 @@ Mirrors the ``pdeopt`` python package of the reference (python/bindings.cpp):
     make_thermal_problem(n, phi)                          bindings.cpp:87-88
     solve_range_space(problem, method, tol, s_x, s_y, augment)   bindings.cpp:93-111
     feti_solve(problem, mass_coeff, rhs, s_x, s_y, augment, tol) bindings.cpp:158-185
+    solve_full_space(problem, precond, outer, tol, inner_method, inner_tol, s_x, s_y)
+                                                          bindings.cpp:113-145
     diagnostics(problem, y, u, lambda)                    bindings.cpp:147-156
     ContractError -> ValueError, NumericalError -> RuntimeError (bindings.cpp:60-61)
 
@@ -29,7 +31,8 @@ from ._native import Desc, FetiStats, SchurStats
 
 __all__ = [
     "ContractError", "NumericalError", "ControlProblem", "make_thermal_problem", "make_seeded_problem",
-    "make_problem", "partition_info", "SchurSolver", "solve_range_space", "feti_solve", "diagnostics",
+    "make_problem", "partition_info", "SchurSolver", "solve_range_space", "feti_solve", "solve_full_space",
+    "diagnostics", "nccl_unique_id", "rank_info", "emulated_schur_solve",
 ]
 
 
@@ -365,6 +368,42 @@ def feti_solve(problem: ControlProblem, mass_coeff, rhs, s_x=2, s_y=2, augment=T
     return {"x": x, "iterations": st["iterations"], "converged": st["converged"],
             "interface_jump": st["interface_jump"], "primal_residual": st["primal_residual"],
             "n_lambda": st["n_lambda"], "coarse_dim": st["coarse_dim"]}
+
+
+def solve_full_space(problem: ControlProblem, precond="none", outer="minres", tol=1e-10, inner_method="feti",
+                     inner_tol=1e-12, s_x=2, s_y=2, augment=True, max_iter=5000):
+    """Simultaneous KKT solve, optionally with the block-diagonal Murphy-Golub-Wathen
+    preconditioner (bindings.cpp:113-145, control.cpp:418-476).  precond: "none", "sp"
+    (Pearson-Wathen approximate Schur complement) or "sc" (exact Schur through the complex
+    FETI factors, GMRES only); outer: "minres" or "gmres".  The inner factor solves run on
+    the B200 FETI-DP path (inner_method "feti"; the reference's "direct"/"gmres" inner
+    backends are CPU-only and not provided)."""
+    pc = {"none": 0, "sp": 1, "sc": 2}.get(precond)
+    if pc is None:
+        raise ContractError("precond must be none, sp or sc")
+    oc = {"minres": 0, "gmres": 1}.get(outer)
+    if oc is None:
+        raise ContractError("outer must be minres or gmres")
+    if inner_method != "feti":
+        raise ContractError("solve_full_space: the B200 path's inner factor solves are FETI-DP (inner_method='feti')")
+    problem.validate()
+    solver = SchurSolver(problem, s_x, s_y, inner_tol, 2000, augment=augment)
+    n = problem.n
+    ybar = np.ascontiguousarray(problem.target_state, dtype=np.float64)
+    yc = problem.boundary_values
+    ycp = _dp(np.ascontiguousarray(yc, dtype=np.float64)) if yc is not None and problem.m > 0 else None
+    y, u, lam = np.zeros(n), np.zeros(n), np.zeros(n)
+    st = FetiStats()
+    leak = np.zeros(1)
+    try:
+        _check(_native.lib().fetigpu_full_space(solver._h, pc, oc, tol, max_iter, _dp(ybar), ycp, _dp(y), _dp(u),
+                                                _dp(lam), C.byref(st), _dp(leak)))
+    finally:
+        solver.close()
+    stats = {"iterations": st.iterations, "relative_residual": st.relative_residual, "converged": bool(st.converged),
+             "wall_time": st.solve_seconds}
+    return {"y": y, "u": u, "lambda": lam, "stats": stats, "imag_leak": float(leak[0]),
+            "inner_iterations": st.coarse_dim, "precond_setup_seconds": st.setup_seconds}
 
 
 def diagnostics(problem: ControlProblem, y, u, lam, K=None, V=None, Kc=None):

@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libfetigpu.so")
 SOURCES = ["host_core.cpp", "comm.cu", "fetigpu.cu"]
-HEADERS = ["host_core.hpp", "comm.hpp", "common.cuh", "band.cuh", "blockthomas.cuh", "kernels.cuh"]
+HEADERS = ["host_core.hpp", "comm.hpp", "common.cuh", "band.cuh", "blockthomas.cuh", "kernels.cuh", "fullspace.hpp"]
 
 
 def nvcc_path():

@@ -1750,6 +1750,66 @@ static std::unique_ptr<Ctx> make_ctx(const fetigpu_desc* desc) {
   return c;
 }
 
+}  // extern "C" (the full-space solver is C++)
+#include "fullspace.hpp"
+namespace fetigpu {
+
+// solve_full_space (control.cpp:418-476) on one GPU context; the context's FETI factor
+// (K + cV) serves the "sc" preconditioner, "sp" builds a K + V/sqrt(phi) context
+static void full_space(Ctx& c, int precond, int outer, double tol, int max_iter, const double* ybar,
+                       const double* yc, double* y, double* u, double* lam, fetigpu_feti_stats* stats,
+                       double* imag_leak) {
+  if (!(c.phi > 0.0)) throw ContractError("solve_full_space: phi must be positive");
+  if (c.dist()) throw ContractError("solve_full_space: not available on the sharded path");
+  if (precond == FS_SC && outer == FS_MINRES)
+    throw ContractError("solve_full_space: the complex-factor backend preconditioner requires GMRES");
+  if (precond < FS_NONE || precond > FS_SC || outer < FS_MINRES || outer > FS_GMRES)
+    throw ContractError("solve_full_space: bad precond / outer");
+  auto t0 = std::chrono::steady_clock::now();
+  FullSpace fs(c, precond);
+  if (precond == FS_SP) {
+    fetigpu_desc d = c.desc;
+    d.phi = 0.0;
+    d.mass_coeff_re = 1.0 / std::sqrt(c.phi);
+    d.mass_coeff_im = 0.0;
+    fs.spc = make_ctx(&d);
+    fs.spc->H = build_partition(fs.spc->P, d.s_x, d.s_y, d.augment != 0);
+    fs.spc->setup();
+  }
+  const double setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  const int n = c.n;
+  const size_t nb = sizeof(double) * n;
+  double* b = fs.vec();
+  double* x = fs.vec();
+  CU(cudaMemcpyAsync(c.d_in_ybar, ybar, nb, cudaMemcpyHostToDevice, c.stream));
+  c.apply_global<double>(c.d_in_ybar, nullptr, 0.0, 1.0, b);  // V ybar (control.cpp:19)
+  CU(cudaMemsetAsync(b + n, 0, 2 * nb, c.stream));
+  if (yc && c.m > 0) {  // -K_c y_c (control.cpp:20)
+    CU(cudaMemcpyAsync(c.d_in_yc, yc, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
+    c.apply_global<double>(b + n, c.d_in_yc, 0.0, 0.0, b + 2LL * n);
+    fs.axpby(0.0, b + n, -1.0, b + 2LL * n, n);
+  }
+  CU(cudaMemsetAsync(c.d_stat + 15, 0, sizeof(double2), c.stream));
+  const fetigpu_feti_stats st = outer == FS_GMRES ? fs.gmres(b, x, tol, max_iter) : fs.minres(b, x, tol, max_iter);
+  CU(cudaMemcpyAsync(y, x, nb, cudaMemcpyDeviceToHost, c.stream));
+  CU(cudaMemcpyAsync(u, x + n, nb, cudaMemcpyDeviceToHost, c.stream));
+  CU(cudaMemcpyAsync(lam, x + 2LL * n, nb, cudaMemcpyDeviceToHost, c.stream));
+  double2 leak{};
+  CU(cudaMemcpyAsync(&leak, c.d_stat + 15, sizeof(double2), cudaMemcpyDeviceToHost, c.stream));
+  c.sync();
+  if (stats) {
+    *stats = st;
+    stats->n_lambda = 3 * n;
+    stats->coarse_dim = (int)std::min<long long>(fs.inner_iters, 1LL << 30);  // inner FETI iterations
+    stats->setup_seconds = setup_s;
+    stats->solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() - setup_s;
+  }
+  if (imag_leak) *imag_leak = leak.y;
+}
+
+}  // namespace fetigpu
+extern "C" {
+
 int fetigpu_nccl_unique_id(unsigned char* out128) {
   return guard([&] { nccl_unique_id(out128); });
 }
@@ -1927,6 +1987,16 @@ int fetigpu_profile_read(fetigpu_ctx* ctx, double* ms, long long* launches, int 
       if (launches) launches[k] = c.prof_n[k];
       if (reset) c.prof_ms[k] = 0, c.prof_n[k] = 0;
     }
+  });
+}
+
+int fetigpu_full_space(fetigpu_ctx* ctx, int precond, int outer, double tol, int max_iter, const double* ybar,
+                       const double* yc, double* y, double* u, double* lambda, fetigpu_feti_stats* stats,
+                       double* imag_leak) {
+  return guard([&] {
+    if (!ctx) throw ContractError("fetigpu: null context");
+    if (!(tol > 0.0) || max_iter < 0) throw ContractError("solve_full_space: bad tol / max_iter");
+    full_space(*ctx->c, precond, outer, tol, max_iter, ybar, yc, y, u, lambda, stats, imag_leak);
   });
 }
 

@@ -2067,6 +2067,34 @@ __global__ void k_max_final(int nblk, const double* __restrict__ part, double2* 
   if (threadIdx.x == 0) *out = make_double2(0.0, m);
 }
 
+// ---- real vector helpers of the full-space method (3n-vectors) --------------------------
+__global__ void k_rdot_part(long long n, const double* __restrict__ x, const double* __restrict__ y,
+                            double* __restrict__ part) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+    s = fma(x[k], y[k], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sm[w];
+    part[blockIdx.x] = t;
+  }
+}
+__global__ void k_rdot_final(int nb, const double* __restrict__ part, double* __restrict__ out) {
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nb; b += 32) s += part[b];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) *out = s;
+}
+// y = a x + b y
+__global__ void k_axpby(long long n, double a, const double* __restrict__ x, double b, double* __restrict__ y) {
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) y[k] = b == 0.0 ? a * x[k] : fma(a, x[k], b * y[k]);
+}
+
 // ------------------------------------------------------------------ global operators (K8)
 // y = kc K x + mc V x (+ K_c xc) matrix-free over the Q1 elements around each free dof.
 // Real or complex vectors (T = double or double2); coefficients complex.
