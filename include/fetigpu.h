@@ -90,6 +90,16 @@ int fetigpu_target_thermal(const fetigpu_desc* desc, double* ybar, double* yc);
 int fetigpu_target_sine(const fetigpu_desc* desc, unsigned long long seed, int modes, int mmax,
                         double* ybar);
 
+/* Bottom-edge pressure load of the plane-strain cantilever (fem.cpp:222-238): f (n_free). */
+int fetigpu_pressure_load(const fetigpu_desc* desc, double pressure, double* f);
+
+/* Optimality diagnostics (diagnostics, control.cpp:122-141; python diagnostics,
+ * bindings.cpp:147-156) evaluated with the operators applied on the device.  y, u, ybar:
+ * n_free; yc: n_constrained or NULL.  out5 = {constraint_violation, target_mismatch,
+ * control_norm, objective, violation_defined (0/1)}. */
+int fetigpu_diagnostics(const fetigpu_desc* desc, const double* y, const double* u, const double* ybar,
+                        const double* yc, double* out5);
+
 /* ---- GPU context ----------------------------------------------------------------- */
 
 /* Partition + upload + factor once (K1-K4).  Replaces the two ComplexFactorSolver

@@ -31,7 +31,8 @@ from ._native import Desc, FetiStats, SchurStats
 
 __all__ = [
     "ContractError", "NumericalError", "ControlProblem", "make_thermal_problem", "make_seeded_problem",
-    "make_problem", "partition_info", "SchurSolver", "solve_range_space", "feti_solve", "solve_full_space",
+    "make_problem", "make_cantilever_problem", "partition_info", "SchurSolver", "solve_range_space", "feti_solve",
+    "solve_full_space",
     "diagnostics", "nccl_unique_id", "rank_info", "emulated_schur_solve",
 ]
 
@@ -406,11 +407,42 @@ def solve_full_space(problem: ControlProblem, precond="none", outer="minres", to
             "inner_iterations": st.coarse_dim, "precond_setup_seconds": st.setup_seconds}
 
 
+def make_cantilever_problem(n, phi, pressure=100e3, tol=1e-13):
+    """Plane-strain 3:1 rubber cantilever clamped at x = 0 (control.cpp:36-46): 3n x n Q1
+    mesh on [0,3]x[0,1], E = 20.7e6, nu = 0.45; the target is the displacement under a
+    bottom-edge pressure, K ybar = f (fem.cpp:222-260), solved here by the GPU FETI-DP path
+    with mass coefficient 0 (the reference uses a refined sparse Cholesky)."""
+    if not (phi > 0.0):
+        raise ContractError("ControlProblem: phi must be positive")
+    p = make_problem(3 * n, n, phi, physics=1, len_x=3.0, len_y=1.0, young=20.7e6, poisson=0.45)
+    f = np.zeros(p.n)
+    _check(_native.lib().fetigpu_pressure_load(C.byref(_base_desc(3 * n, n, 1, 3.0, 1.0, 20.7e6, 0.45)),
+                                               float(pressure), _dp(f)))
+    p.boundary_values = np.zeros(p.m)  # clamped edge
+    if np.linalg.norm(f) == 0.0:
+        p.target_state = np.zeros(p.n)
+        return p
+    q = next(d for d in range(1, n + 1) if n % d == 0 and n // d <= 24)  # square subdomains <= 24 h
+    out = feti_solve(p, 0.0, f.astype(complex), s_x=3 * q, s_y=q, augment=False, tol=tol, max_iter=2000)
+    p.target_state = np.ascontiguousarray(out["x"].real)
+    return p
+
+
 def diagnostics(problem: ControlProblem, y, u, lam, K=None, V=None, Kc=None):
-    """Optimality diagnostics (control.cpp:122-141).  Needs K, V (and Kc) as scipy/numpy
-    operators supplied by the caller; the product never materialises them on the host."""
+    """Optimality diagnostics (control.cpp:122-141; bindings.cpp:147-156).  Without operator
+    arguments K, V, Kc are applied on the device (fetigpu_diagnostics); scipy/numpy
+    operators may be passed instead (host evaluation, for tests)."""
     if K is None or V is None:
-        raise ContractError("diagnostics: pass K and V operators (the B200 path keeps them on the device)")
+        yv = np.ascontiguousarray(y, dtype=np.float64)
+        uv = np.ascontiguousarray(u, dtype=np.float64)
+        yb = np.ascontiguousarray(problem.target_state, dtype=np.float64)
+        yc = problem.boundary_values
+        ycp = _dp(np.ascontiguousarray(yc, dtype=np.float64)) if yc is not None and problem.m > 0 else None
+        out = np.zeros(5)
+        _check(_native.lib().fetigpu_diagnostics(C.byref(problem.desc()), _dp(yv), _dp(uv), _dp(yb), ycp,
+                                                 _dp(out)))
+        return {"violation_defined": bool(out[4]), "constraint_violation": float(out[0]),
+                "target_mismatch": float(out[1]), "control_norm": float(out[2]), "objective": float(out[3])}
     yc = problem.boundary_values
     ky = K @ y
     res = ky - V @ u

@@ -81,6 +81,8 @@ def lib():
     L.fetigpu_rank_info.argtypes = [pdesc, C.c_int, C.c_int, ip]
     L.fetigpu_emulated_schur_solve.argtypes = [pdesc, C.c_int, dp, dp, dp, dp, dp, C.POINTER(SchurStats)]
     L.fetigpu_step_spans.argtypes = [vp, dp]
+    L.fetigpu_pressure_load.argtypes = [pdesc, C.c_double, dp]
+    L.fetigpu_diagnostics.argtypes = [pdesc, dp, dp, dp, dp, dp]
     L.fetigpu_full_space.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_int, dp, dp, dp, dp, dp,
                                      C.POINTER(FetiStats), dp]
     L.fetigpu_class_bytes.argtypes = [vp, C.c_int]
@@ -95,5 +97,5 @@ EXPORTED_SYMBOLS = (
     "fetigpu_apply_dual", "fetigpu_apply_precond", "fetigpu_stream", "fetigpu_launch_count",
     "fetigpu_profile", "fetigpu_profile_read", "fetigpu_class_bytes", "fetigpu_last_error",
     "fetigpu_nccl_unique_id", "fetigpu_create_sharded", "fetigpu_rank_info", "fetigpu_emulated_schur_solve",
-    "fetigpu_step_spans", "fetigpu_full_space",
+    "fetigpu_step_spans", "fetigpu_full_space", "fetigpu_pressure_load", "fetigpu_diagnostics",
 )

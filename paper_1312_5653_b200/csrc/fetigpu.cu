@@ -1706,6 +1706,94 @@ int fetigpu_target_sine(const fetigpu_desc* desc, unsigned long long seed, int m
   });
 }
 
+int fetigpu_pressure_load(const fetigpu_desc* desc, double pressure, double* f) {
+  return guard([&] {
+    if (!desc) throw ContractError("fetigpu: null descriptor");
+    HostProblem P = build_problem(*desc);
+    bottom_pressure_load(P, pressure, f);
+  });
+}
+
+// Optimality diagnostics (control.cpp:122-141) with the operators applied on the device:
+// out = {constraint_violation, target_mismatch, control_norm, objective, violation_defined}
+int fetigpu_diagnostics(const fetigpu_desc* desc, const double* y, const double* u, const double* ybar,
+                        const double* yc, double* out5) {
+  return guard([&] {
+    if (!desc) throw ContractError("fetigpu: null descriptor");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw RuntimeError("fetigpu: no CUDA device");
+    CU(cudaSetDevice(desc->device));
+    const HostProblem P = build_problem(*desc);
+    const int n = P.n(), m = P.m();
+    std::vector<void*> mem;
+    auto up = [&](const void* src, size_t bytes) -> void* {
+      void* d = nullptr;
+      CU(cudaMalloc(&d, std::max<size_t>(bytes, 8)));
+      mem.push_back(d);
+      if (src) CU(cudaMemcpy(d, src, bytes, cudaMemcpyHostToDevice));
+      return d;
+    };
+    try {
+      auto* dfd = static_cast<int*>(up(P.free_dofs.data(), sizeof(int) * n));
+      auto* dfm = static_cast<int*>(up(P.free_map.data(), sizeof(int) * P.free_map.size()));
+      auto* dcm = static_cast<int*>(up(P.cons_map.data(), sizeof(int) * P.cons_map.size()));
+      auto* dy = static_cast<double*>(up(y, sizeof(double) * n));
+      auto* du = static_cast<double*>(up(u, sizeof(double) * n));
+      auto* db = static_cast<double*>(up(ybar, sizeof(double) * n));
+      double* dyc = (yc && m > 0) ? static_cast<double*>(up(yc, sizeof(double) * m)) : nullptr;
+      auto* t1 = static_cast<double*>(up(nullptr, sizeof(double) * n));
+      auto* t2 = static_cast<double*>(up(nullptr, sizeof(double) * n));
+      auto* zero = static_cast<double*>(up(nullptr, sizeof(double) * n));
+      auto* part = static_cast<double*>(up(nullptr, sizeof(double) * 296));
+      auto* red = static_cast<double*>(up(nullptr, sizeof(double) * 2));
+      CU(cudaMemset(zero, 0, sizeof(double) * n));
+      ElemKM km{};
+      for (int q = 0; q < P.edofs * P.edofs; ++q) km.k[q] = P.ke[q], km.m[q] = P.me[q];
+      const MeshLayout M{P.nx, P.ny, P.dpn};
+      const int g = (n + 255) / 256;
+      auto apply = [&](const double* x, const double* xc, double kc, double mcoef, double* out) {
+        k_apply_global<double><<<g, 256>>>(M, km, n, dfd, dfm, dcm, x, xc, make_double2(kc, 0.0),
+                                           make_double2(mcoef, 0.0), out);
+        CU(cudaGetLastError());
+      };
+      auto dot = [&](const double* a, const double* b) {
+        const int nb = std::max(1, std::min(296, g));
+        k_rdot_part<<<nb, 256>>>(n, a, b, part);
+        k_rdot_final<<<1, 32>>>(nb, part, red);
+        double h = 0;
+        CU(cudaMemcpy(&h, red, sizeof(double), cudaMemcpyDeviceToHost));
+        return h;
+      };
+      apply(dy, nullptr, 1.0, 0.0, t1);  // K y
+      const double kyn = std::sqrt(dot(t1, t1));
+      if (dyc) {  // + K_c y_c
+        apply(zero, dyc, 0.0, 0.0, t2);
+        k_axpby<<<g, 256>>>(n, 1.0, t2, 1.0, t1);
+      }
+      apply(du, nullptr, 0.0, 1.0, t2);  // - V u
+      k_axpby<<<g, 256>>>(n, -1.0, t2, 1.0, t1);
+      const double resn = std::sqrt(dot(t1, t1));
+      const double cu2 = dot(du, t2);      // u' V u
+      k_axpby<<<g, 256>>>(n, 1.0, dy, 0.0, t1);
+      k_axpby<<<g, 256>>>(n, -1.0, db, 1.0, t1);  // dy = y - ybar
+      apply(t1, nullptr, 0.0, 1.0, t2);
+      const double dyv = std::sqrt(std::max(0.0, dot(t1, t2)));
+      apply(db, nullptr, 0.0, 1.0, t2);
+      const double ybv = std::sqrt(std::max(0.0, dot(db, t2)));
+      const double cn = std::sqrt(std::max(0.0, cu2));
+      out5[0] = kyn == 0.0 ? 0.0 : resn / kyn;
+      out5[1] = ybv > 0.0 ? dyv / ybv : dyv;
+      out5[2] = cn;
+      out5[3] = 0.5 * dyv * dyv + 0.5 * desc->phi * cn * cn;
+      out5[4] = kyn == 0.0 ? 0.0 : 1.0;
+    } catch (...) {
+      for (void* q : mem) cudaFree(q);
+      throw;
+    }
+    for (void* q : mem) cudaFree(q);
+  });
+}
+
 int fetigpu_create(const fetigpu_desc* desc, fetigpu_ctx** out) {
   return guard([&] {
     validate_desc(desc);

@@ -597,6 +597,17 @@ void target_thermal(const HostProblem& P, double* ybar, double* yc) {
 
 // BASELINE.json seeded target, recipe of SURVEY.md §8(d).  Independently restated in
 // oracle/feti_oracle.cpp; tests/test_host.py checks the two agree bit for bit.
+void bottom_pressure_load(const HostProblem& P, double pressure, double* f) {
+  if (P.physics != 1) throw ContractError("bottom_pressure_load: elasticity physics required");
+  std::fill(f, f + P.n(), 0.0);
+  const double nodal = -pressure * P.h / 2.0;  // h/2 per end node of each bottom edge
+  for (int i = 0; i < P.nx; ++i)
+    for (int node : {P.node_id(i, 0), P.node_id(i + 1, 0)}) {
+      const int fi = P.free_map[2 * node + 1];
+      if (fi >= 0) f[fi] += nodal;
+    }
+}
+
 void target_sine(const HostProblem& P, uint64_t seed, int modes, int mmax, double* ybar) {
   if (modes < 0 || mmax < 1) throw ContractError("target_sine: need modes >= 0 and mmax >= 1");
   std::mt19937_64 rng(seed);

@@ -115,6 +115,8 @@ struct RankPlan {
 HostPartition build_rank_partition(const HostPartition& G, int rank, int world, RankPlan& plan);
 
 void target_thermal(const HostProblem& P, double* ybar, double* yc);
+// consistent traction of a constant downward pressure on the bottom edge (fem.cpp:222-238)
+void bottom_pressure_load(const HostProblem& P, double pressure, double* f);
 void target_sine(const HostProblem& P, uint64_t seed, int modes, int mmax, double* ybar);
 
 }  // namespace fetigpu
