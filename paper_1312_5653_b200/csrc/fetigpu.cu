@@ -721,6 +721,7 @@ struct Ctx {
           k_scale_inverse<<<cdiv((long long)nc * nc, 256), 256, 0, stream>>>(nc, d_Cinv, cscale_d);
         });
       }
+      setup_big_coarse();
       // packed symmetric storage of S_bb and S_bb^-1 for the per-iteration GEMVs
       NT = (NB + 31) / 32;
       if (NT > 8) throw ContractError("more than 256 interface dofs per subdomain");
@@ -1066,7 +1067,11 @@ struct Ctx {
     g.out = d_u1b;
     g.cpl_b = d_cpl_b;
     g.gcp = d_gcp;
-    if (nc > 0 && !fused_tail) {  // (the fused Arnoldi tail assembles g itself)
+    // coarse rhs g = -sum gcp: by the GEMV's last CTA for small coarse spaces, by a parallel
+    // kernel for large ones (one CTA would serialise 4 nc loads); the fused Arnoldi tail
+    // assembles g itself
+    const bool last_cta = nc > 0 && !fused_tail && nc <= 2048;
+    if (last_cta) {
       g.g_counter = d_counter + 1;
       g.nc = nc;
       g.corner_slots = d_corner_slots;
@@ -1074,10 +1079,41 @@ struct Ctx {
       g.g = d_g;
     }
     launch(FETIGPU_K_DUAL_GEMV, [&] { launch_sym(g); });
+    if (nc > 0 && !fused_tail && !last_cta)
+      launch(FETIGPU_K_COARSE, [&] {
+        k_coarse_rhs<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_slots, d_gcp, nullptr, d_g);
+      });
     allreduce(d_g, nc);
+  }
+  // packed symmetric C^-1 for large coarse spaces (k_big_sym_gemv), built at setup
+  static constexpr int kBigCoarse = 1536;
+  int NTc = 0;
+  double2 *d_Cinv_p = nullptr, *d_cpart_row = nullptr, *d_cpart_col = nullptr;
+  void setup_big_coarse() {
+    if (nc < kBigCoarse || std::getenv("FETIGPU_DENSE_COARSE")) return;
+    NTc = (nc + 31) / 32;
+    const size_t per = (size_t)NTc * 17 * 32 + (size_t)NTc * (NTc - 1) / 2 * 1024;
+    d_Cinv_p = alloc<double2>(per);
+    launch(FETIGPU_K_OTHER, [&] {
+      k_pack_sym<<<cdiv((long long)per, 256), 256, 0, stream>>>(1, nc, NTc, d_Cinv, d_Cinv_p);
+    });
+    const size_t items = (size_t)NTc * (NTc - 1) / 2 + NTc;
+    d_cpart_row = alloc<double2>(items * 32);
+    d_cpart_col = alloc<double2>(items * 32);
   }
   void coarse_gemv() {
     if (nc == 0) return;
+    if (d_Cinv_p != nullptr) {
+      const int items = NTc * (NTc - 1) / 2 + NTc;
+      launch(FETIGPU_K_COARSE, [&] {
+        kx(k_big_sym_gemv, cdiv(items, 4), 128, 0, nc, NTc, (const double2*)d_Cinv_p, (const double2*)d_g,
+           d_cpart_row, d_cpart_col);
+      });
+      launch(FETIGPU_K_COARSE, [&] {
+        kx(k_big_sym_reduce, NTc, 256, 0, nc, NTc, (const double2*)d_cpart_row, (const double2*)d_cpart_col, d_z);
+      });
+      return;
+    }
     launch(FETIGPU_K_COARSE, [&] {
       kx(k_coarse_gemv<256>, nc, 256, 0, nc, (const double2*)d_Cinv, (const double2*)d_g, d_z, l2pf(arnoldi_phase ? 0 : -1));
     });

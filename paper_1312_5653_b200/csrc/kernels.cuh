@@ -1015,6 +1015,98 @@ __global__ void __launch_bounds__(THREADS)
   }
 }
 
+// ---- large coarse spaces: z = C^-1 g with C^-1 complex symmetric, packed in the 32 x 32
+// tile format of k_pack_sym (4 diagonal tiles' 17 rows + lower off-diagonal tiles): half the
+// bytes of the dense row-major GEMV.  Kernel 1: one warp per tile (row and transposed
+// partials, as k_sym_gemv); kernel 2: fixed-order combination per 32-row block.
+__global__ void __launch_bounds__(128) k_big_sym_gemv(int nc, int NT, const double2* __restrict__ pack,
+                                                      const double2* __restrict__ x, double2* __restrict__ part_row,
+                                                      double2* __restrict__ part_col) {
+  __shared__ double2 xs[4][2][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int noff = NT * (NT - 1) / 2, items = noff + NT;
+  const int t = blockIdx.x * 4 + warp;
+  pdl_trigger();
+  pdl_wait();
+  if (t >= items) return;
+  double2* xI = xs[warp][0];
+  double2* xJ = xs[warp][1];
+  if (t < noff) {
+    int I = 1;
+    while ((I + 1) * I / 2 <= t) ++I;
+    const int J = t - I * (I - 1) / 2;
+    xI[lane] = 32 * I + lane < nc ? x[32 * I + lane] : cz();
+    xJ[lane] = 32 * J + lane < nc ? x[32 * J + lane] : cz();
+    __syncwarp();
+    const double2* O = pack + (size_t)NT * 17 * 32 + (size_t)t * 1024;
+    const double2 xi = xI[lane];
+    double2 yr = cz(), yc = cz();
+#pragma unroll
+    for (int cb = 0; cb < 32; cb += 8) {
+      double2 m[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m[u] = __ldcs(O + (cb + u) * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = cb + u;
+        yr = cfma(m[u], xJ[(lane + c) & 31], yr);
+        yc = cfma(m[u], xi, yc);
+        yc = shfl2(yc, (lane + 1) & 31);
+      }
+    }
+    part_row[(size_t)t * 32 + lane] = yr;
+    part_col[(size_t)t * 32 + lane] = yc;
+  } else {
+    const int I = t - noff;
+    xI[lane] = 32 * I + lane < nc ? x[32 * I + lane] : cz();
+    __syncwarp();
+    const double2* D = pack + (size_t)I * 17 * 32;
+    const double2 xi = xI[lane];
+    double2 yr = cz(), yc = cz();
+#pragma unroll
+    for (int cb = 0; cb < 16; cb += 8) {
+      double2 m[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) m[u] = __ldcs(D + (cb + u) * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = cb + u;
+        if (c == 0) {
+          yr = cmul(m[u], xi);
+        } else {
+          yr = cfma(m[u], xI[(lane + c) & 31], yr);
+          yc = shfl2(yc, (lane + 1) & 31);
+          yc = cfma(m[u], xi, yc);
+        }
+      }
+    }
+    yr = cfma(__ldcs(D + 16 * 32 + lane), xI[(lane + 16) & 31], yr);
+    yc = shfl2(yc, (lane + 17) & 31);
+    part_row[(size_t)t * 32 + lane] = cadd(yr, yc);
+  }
+}
+// y_I = diag(I) + sum_{J<I} rows(I,J) + sum_{I'>I} cols(I',I): one CTA per row block I, 8
+// warps over the partial tiles (fixed assignment and order), then the 8 sums in order
+__global__ void __launch_bounds__(256) k_big_sym_reduce(int nc, int NT, const double2* __restrict__ part_row,
+                                                        const double2* __restrict__ part_col, double2* __restrict__ z) {
+  __shared__ double2 red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, I = blockIdx.x;
+  const int noff = NT * (NT - 1) / 2;
+  pdl_trigger();
+  pdl_wait();
+  double2 acc = cz();
+  for (int J = warp; J < I; J += 8) acc = cadd(acc, part_row[((size_t)I * (I - 1) / 2 + J) * 32 + lane]);
+  for (int I2 = I + 1 + warp; I2 < NT; I2 += 8) acc = cadd(acc, part_col[((size_t)I2 * (I2 - 1) / 2 + I) * 32 + lane]);
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    double2 t = part_row[((size_t)noff + I) * 32 + lane];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) t = cadd(t, red[q][lane]);
+    if (32 * I + lane < nc) z[32 * I + lane] = t;
+  }
+}
+
 // Dual tail: u_b = u1_b - cpl_b z_loc ; out[r] = -(u_lo - u_hi)   (feti.cpp:542-555, 593)
 __global__ void k_lam_gather_dual(int nl, int NB, int NC, const int* __restrict__ lo, const int* __restrict__ hi,
                                   const double2* __restrict__ u1b, const double2* __restrict__ cpl_b,
