@@ -196,9 +196,17 @@ def run_gpu(args):
 
     steps, warmup = args.steps, max(args.warmup, 3)
     n_x, n_y, s_x, s_y, len_x, len_y = weak_problem_args(world)
+    phi = PHI
+    if args.config == 3:  # BASELINE config 3 on one GPU: 2048^2, 64x64 subdomains, phi 1e-6
+        if world != 1:
+            raise SystemExit("bench.py --config 3 is the single-GPU config-3 line (--gpus N runs weak scaling)")
+        n_x = n_y = 2 * N_GRID
+        s_x = s_y = 2 * S_SUB
+        len_x = len_y = 1.0
+        phi = 1e-6
 
     def problem(seed):
-        return F.make_problem(n_x, n_y, PHI, len_x=len_x, len_y=len_y, target="sine", seed=seed)
+        return F.make_problem(n_x, n_y, phi, len_x=len_x, len_y=len_y, target="sine", seed=seed)
 
     p = problem(0)
     t0 = time.perf_counter()
@@ -307,10 +315,12 @@ def run_gpu(args):
         "dtype": "c128", "data": "synthetic (seeded sine-mode ybar, seed = step; factors random-free FEM)",
         "config": {
             "workload": ("config2: 1024x1024 Q1 heat, 32x32 subdomains of 32x32, phi=1e-4, tol 1e-10, FP64 complex"
-                         if world == 1 else
+                         if world == 1 and args.config == 2 else
+                         "config3 (one GPU): 2048x2048 Q1 heat, 64x64 subdomains of 32x32, phi=1e-6, tol 1e-10, "
+                         "FP64 complex; value = config-3 solves/s" if world == 1 else
                          f"weak scaling: {n_x}x{n_y} Q1 heat, {s_x}x{s_y} subdomains of 32x32 ({s_x * s_y // world} "
                          f"per GPU), phi=1e-4, tol 1e-10, FP64 complex; value = solves/s x {world}"),
-            "phi": PHI, "n_free": n, "n_lambda": solver.n_lambda, "coarse_dim": solver.coarse_dim,
+            "phi": phi, "n_free": n, "n_lambda": solver.n_lambda, "coarse_dim": solver.coarse_dim,
             "augment": bool(args.augment),
             "iterations_plus_minus_mean": [float(np.mean([a for a, _ in its])), float(np.mean([b for _, b in its]))],
             "setup_seconds": setup_s, "l2": "inputs larger than L2 (local operators 0.5 GB streamed per iteration)",
@@ -325,7 +335,7 @@ def run_gpu(args):
         "clocks": clk.summary(),
     }
     # BASELINE config 2 is a phi sweep: rates and iteration counts per phi (own factors each)
-    if rank == 0 and world == 1 and not args.no_sweep:
+    if rank == 0 and world == 1 and args.config == 2 and not args.no_sweep:
         sweep = {}
         for phi in PHI_SWEEP:
             q = F.make_seeded_problem(N_GRID, phi, seed=0)
@@ -345,7 +355,7 @@ def run_gpu(args):
                                                            st["minus_stats"]["iterations"]]}
             sv.close()
         line["config"]["phi_sweep"] = sweep
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and args.config == 2 and not args.no_cpu_baseline:
         rate, cits, csetup, ran = cpu_sample_oracle(os.cpu_count() or 1, 1, 0)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
                                 "sample": f"{ran} config-2 Schur solve after setup ({csetup:.1f} s), oracle/ "
@@ -368,6 +378,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
+                    help="2: the headline config (default); 3: BASELINE config 3 on one GPU")
     ap.add_argument("--augment", action="store_true",
                     help="edge-RBM augmented coarse space (reference default; BASELINE configs use augment=false)")
     args = ap.parse_args()

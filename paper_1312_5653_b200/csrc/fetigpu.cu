@@ -158,7 +158,7 @@ struct Ctx {
   int arnoldi_body_kernels = 0;
   static constexpr int kCgsThreads = 512, kCgsRows = 256;  // k_cgs_pass block shape
   // fused Arnoldi tail (k_arnoldi_tail): rows per thread (0 = off), grid, barrier words
-  int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_minb = 1;
+  int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_minb = 1, tail_rows = 512;
   bool cgs_gram = false;       // FETIGPU_CGS=gram: one-reduction CGS2 via the Gram matrix
   double2* d_gram = nullptr;
   static constexpr int kBodyUnroll = 4;
@@ -440,7 +440,10 @@ struct Ctx {
     CU(cudaFuncSetAttribute(k_arnoldi_tail<kTailThreads, 4, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTailThreads, smem));
-    const int grid = std::max(1, cdiv(nown, kTailThreads));
+    // rows per block: spread the rows over every SM (multiple of 32, at most one per thread)
+    tail_rows = std::min(kTailThreads, 32 * cdiv(cdiv(std::max(nown, 1), sms), 32));
+    if (const char* e = std::getenv("FETIGPU_TAIL_ROWS")) tail_rows = std::min(kTailThreads, std::max(32, std::atoi(e)));
+    const int grid = std::max(1, cdiv(nown, tail_rows));
     if (per_sm <= 0 || grid > per_sm * sms) return;
     tail_rpt = 1;
     tail_grid = grid;
@@ -1275,6 +1278,7 @@ struct Ctx {
     if (tail_rpt > 0) {  // coarse + CGS2 + Givens + normalisation in one launch
       ArnoldiTailArgs t{};
       t.n = nown;
+      t.rows_pb = tail_rows;
       t.V = d_V;
       t.ldv = ldv;
       t.st = d_gst;

@@ -1735,7 +1735,8 @@ __global__ void __launch_bounds__(ROWS* GROUPS) k_combine(int n, const double2* 
 // co-resident (the host sizes RPT from the occupancy API); a barrier that does not complete
 // within ~2 s traps instead of hanging.
 struct ArnoldiTailArgs {
-  int n;  // multiplier rows
+  int n;        // multiplier rows
+  int rows_pb;  // rows per block (<= THREADS)
   double2* V;
   size_t ldv;
   GmresState* st;
@@ -1878,8 +1879,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   __shared__ double2 cred[WARPS];
   __shared__ double inv_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = blockIdx.x * THREADS, r = row0 + threadIdx.x;
-  const bool act = r < a.n;
+  // rows_pb (<= THREADS) rows per block so that the grid can fill every SM
+  const int row0 = blockIdx.x * a.rows_pb, r = row0 + threadIdx.x;
+  const bool act = (int)threadIdx.x < a.rows_pb && r < a.n;
+  const int row_end = min(a.n, row0 + a.rows_pb);  // exclusive
   pdl_trigger();
   pdl_wait();
   if (a.st->cont == 0) return;  // unrolled WHILE body: the cycle already stopped
@@ -1960,7 +1963,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
         const double2* v = a.V + (size_t)i * a.ldv + row0;
         double2 x[LPR];
 #pragma unroll
-        for (int q = 0; q < LPR; ++q) x[q] = v[min(lane + 32 * q, a.n - 1 - row0)];
+        for (int q = 0; q < LPR; ++q) x[q] = v[min(lane + 32 * q, row_end - 1 - row0)];
 #pragma unroll
         for (int q = 0; q < LPR; ++q) acc = cfma_conj(x[q], w_sh[lane + 32 * q], acc);
         if (GRAM) {  // Gram column entry v_i^H v_j from the same loads
