@@ -267,6 +267,35 @@ struct Ctx {
     pool_used = 0;
   }
   void sync() { CU(cudaStreamSynchronize(stream)); }
+  // FETIGPU_PHASE_TIMES=1: CUDA events at named points of the Schur solve, printed per solve
+  std::vector<std::pair<const char*, cudaEvent_t>> phase_marks;
+  bool phase_times = false;
+  size_t phase_used = 0;
+  std::vector<cudaEvent_t> phase_pool;
+  void phase(const char* name) {
+    if (!phase_times) return;
+    if (phase_used == phase_pool.size()) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      phase_pool.push_back(e);
+    }
+    cudaEvent_t e = phase_pool[phase_used++];
+    CU(cudaEventRecord(e, stream));
+    phase_marks.emplace_back(name, e);
+  }
+  void phase_report() {
+    if (!phase_times || phase_marks.size() < 2) return;
+    CU(cudaEventSynchronize(phase_marks.back().second));
+    std::fprintf(stderr, "[fetigpu] phases (us):");
+    for (size_t i = 1; i < phase_marks.size(); ++i) {
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, phase_marks[i - 1].second, phase_marks[i].second));
+      std::fprintf(stderr, " %s %.1f", phase_marks[i].first, 1000.0 * ms);
+    }
+    std::fprintf(stderr, "\n");
+    phase_marks.clear();
+    phase_used = 0;
+  }
 
   // ------------------------------------------------------------------------ band solve
   // In-place x = A_ii^-1 x for nrhs right-hand sides per subdomain (or for the coarse).
@@ -535,6 +564,7 @@ struct Ctx {
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FETIGPU_SYM_TMA")) sym_tma = e[0] == '1';
     if (const char* e = std::getenv("FETIGPU_NO_PDL")) pdl = !(e[0] == '1');
+    phase_times = std::getenv("FETIGPU_PHASE_TIMES") != nullptr;
     if (const char* e = std::getenv("FETIGPU_L2PF_KB")) l2pf_bytes = 1024u * (unsigned)std::atoi(e);
     if (const char* e = std::getenv("FETIGPU_L2PF_AT")) l2pf_at = std::atoi(e);
     if (const char* e = std::getenv("FETIGPU_SYM_WARPS")) sym_warps = std::atoi(e) == 8 ? 8 : 4;
@@ -1413,12 +1443,22 @@ struct Ctx {
     const double tol = desc.tol;
     const int max_iter = desc.max_iter;
     zero(x, nl);
-    const double bnorm = norm_max(b + own0, nown, true).first;
-    if (bnorm == 0.0) {
-      st.converged = 1;
-      return st;
-    }
     const bool graph = use_graph && !prof && !dist();
+    // with the fused step (each kernel returns once the cycle stopped) the first cycle starts
+    // from a device-side |b| (statistics slot 14): no host round trip before the graph
+    const bool dev_start = graph && tail_rpt > 0;
+    double bnorm = 0.0;
+    if (dev_start) {
+      const int blocks = std::max(1, std::min(296, cdiv(std::max(nown, 1), 256)));
+      launch(FETIGPU_K_ORTHO, [&] { k_norm_max_part<<<blocks, 256, 0, stream>>>(nown, b + own0, d_part); });
+      launch(FETIGPU_K_ORTHO, [&] { k_norm_max_final<<<1, 32, 0, stream>>>(blocks, d_part, d_stat + 14); });
+    } else {
+      bnorm = norm_max(b + own0, nown, true).first;
+      if (bnorm == 0.0) {
+        st.converged = 1;
+        return st;
+      }
+    }
     if (d_span) {
       const int cnt = 6 * (vcap_hint() + 2);
       k_span_init<<<cdiv(cnt, 256), 256, 0, stream>>>(cnt, d_span);
@@ -1432,9 +1472,10 @@ struct Ctx {
     double relres = 0;
     bool first = true;
     while (true) {
+      const bool dev_cycle = dev_start && first;
       const double rnorm = first ? bnorm : norm_max(d_r + own0, nown, true).first;
       first = false;
-      relres = rnorm / bnorm;
+      relres = dev_cycle ? 1.0 : rnorm / bnorm;
       if (relres < best_res) {
         best_res = relres;
         CU(cudaMemcpyAsync(d_best, x, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
@@ -1445,7 +1486,10 @@ struct Ctx {
       }
       if (iterations >= max_iter) break;
       // new cycle: V_0 = r / |r|, g = |r| e_0
-      launch(FETIGPU_K_ORTHO, [&] { k_scale_copy<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, 1.0 / rnorm, d_V); });
+      if (dev_cycle)
+        launch(FETIGPU_K_ORTHO, [&] { k_scale_by_norm<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, d_stat + 14, d_V); });
+      else
+        launch(FETIGPU_K_ORTHO, [&] { k_scale_copy<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, 1.0 / rnorm, d_V); });
       ghost_refresh(d_V);
       *h_gst = GmresState{};
       h_gst->j = 0;
@@ -1456,11 +1500,16 @@ struct Ctx {
       h_gst->tol = tol;
       h_gst->bnorm = bnorm;
       CU(cudaMemcpyAsync(d_gst, h_gst, sizeof(GmresState), cudaMemcpyHostToDevice, stream));
-      h_pin[0] = make_double2(rnorm, 0.0);
-      CU(cudaMemcpyAsync(d_gvec, h_pin, sizeof(double2), cudaMemcpyHostToDevice, stream));
+      if (dev_cycle) {
+        launch(FETIGPU_K_ORTHO, [&] { k_gmres_init<<<1, 32, 0, stream>>>(d_gst, d_stat + 14, d_gvec); });
+      } else {
+        h_pin[0] = make_double2(rnorm, 0.0);
+        CU(cudaMemcpyAsync(d_gvec, h_pin, sizeof(double2), cudaMemcpyHostToDevice, stream));
+      }
       if (graph) {
         CU(cudaGraphLaunch(arnoldi_exec, stream));
         CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
+        if (dev_cycle) CU(cudaMemcpyAsync(h_pin + 1, d_stat + 14, sizeof(double2), cudaMemcpyDeviceToHost, stream));
         if (watchdog) {  // debugging aid: report a stuck Arnoldi graph
           auto t0 = std::chrono::steady_clock::now();
           while (cudaStreamQuery(stream) == cudaErrorNotReady) {
@@ -1482,7 +1531,15 @@ struct Ctx {
         sync();
         {
           const int steps = h_gst->iterations - iterations;
-          launches += (long long)arnoldi_body_kernels * body_unroll * ((steps + body_unroll - 1) / body_unroll);
+          launches += (long long)arnoldi_body_kernels * body_unroll * std::max(1, (steps + body_unroll - 1) / body_unroll);
+        }
+        if (dev_cycle) {
+          bnorm = std::sqrt(h_pin[1].x);
+          if (bnorm == 0.0) {  // zero rhs: zero solution in 0 iterations (feti.cpp:640-644)
+            st.converged = 1;
+            last_gmres_steps = 0;
+            return st;
+          }
         }
       } else {
         static const bool cgs_ratio = std::getenv("FETIGPU_CGS_RATIO") != nullptr;
@@ -1502,6 +1559,7 @@ struct Ctx {
           if (h_gst->cont) ghost_refresh(d_V + (size_t)h_gst->j * ldv);  // sharded: next basis column
         } while (h_gst->cont);
       }
+      phase("cycle");
       if (h_gst->status) throw NumericalError("gmres: breakdown (NaN/Inf in Arnoldi)");
       if (d_tstamp) report_tail_times(iterations, h_gst->iterations);
       if (print_spans) report_step_spans(iterations, h_gst->iterations);
@@ -1543,6 +1601,7 @@ struct Ctx {
     st.n_lambda = nl;
     st.coarse_dim = nc;
     st.setup_seconds = setup_seconds;
+    phase("start");
     norm_async(rhs, n, sb);
     const int S = H.n_sub, NI = H.NI, NB = H.NB;
     launch(FETIGPU_K_OTHER, [&] {
@@ -1551,13 +1610,16 @@ struct Ctx {
     if (nc > 0)
       launch(FETIGPU_K_OTHER, [&] { k_gather_corner<<<cdiv(ncg, 128), 128, 0, stream>>>(ncg, d_corner_dof, rhs, d_fc); });
     eliminate_boundary(d_fi, d_fb, d_fc, true);
+    phase("elim1");
     launch(FETIGPU_K_LAMBDA, [&] {
       k_jump<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_lam_lo + own0, d_lam_hi + own0, d_u1b, d_d + own0);
     });
     // augmented: the coarse solve pins the column components; the dual problem lives in
     // their orthogonal complement (feti.cpp:655-662)
     project_aug(d_d);
+    phase("jump");
     const fetigpu_feti_stats gst = gmres(d_d, d_lam);
+    phase("gmres");
     ghost_refresh(d_lam);
     st.iterations = gst.iterations;
     st.converged = gst.converged;
@@ -1566,7 +1628,9 @@ struct Ctx {
       k_recover_tb<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(S * NB, d_blam, d_bsign, d_fb, d_lam, d_tb);
     });
     eliminate_boundary(d_fi, d_tb, d_fc, false);
+    phase("elim2b");
     eliminate_interior();
+    phase("elim2i");
     launch(FETIGPU_K_OTHER, [&] {
       k_assemble_x<<<cdiv(n, 256), 256, 0, stream>>>(n, d_xkind, d_xa, d_xb, d_ri, d_u1b, d_z, x);
     });
@@ -1578,13 +1642,34 @@ struct Ctx {
       }
       comm->allgatherv(reinterpret_cast<double*>(x), first, count, stream);
     }
-    launch(FETIGPU_K_LAMBDA, [&] {
-      k_jump<<<cdiv(nown, 256), 256, 0, stream>>>(nown, d_lam_lo + own0, d_lam_hi + own0, d_u1b, d_d + own0);
-    });
-    if (H.n_lambda > 0) norm_async(d_d + own0, nown, sb + 1, true);
-    apply_global<double2>(x, nullptr, 1.0, mc, d_ax);
-    launch(FETIGPU_K_GLOBAL, [&] { k_sub<<<cdiv(n, 256), 256, 0, stream>>>(n, d_ax, rhs, d_ax); });
-    norm_async(d_ax, n, sb + 2);
+    // statistics: |jump|_inf (feti.cpp:708-709) and the primal residual (711-713), reduced
+    // straight from u1_b / x without materialising the vectors
+    if (H.n_lambda > 0) {
+      const int blocks = std::max(1, std::min(296, cdiv(std::max(nown, 1), 256)));
+      launch(FETIGPU_K_OTHER, [&] {
+        k_jump_norm_part<<<blocks, 256, 0, stream>>>(nown, d_lam_lo + own0, d_lam_hi + own0, d_u1b, d_part);
+      });
+      launch(FETIGPU_K_OTHER, [&] { k_norm_max_final<<<1, 32, 0, stream>>>(blocks, d_part, d_stat + sb + 1); });
+      if (dist()) {
+        double* r = reinterpret_cast<double*>(d_stat + sb + 1);
+        comm->allreduce_sum(r, 1, stream);
+        comm->allreduce_max(r + 1, 1, stream);
+      }
+    }
+    if (stencil_ok) {
+      Stencil9 S9;
+      for (int q = 0; q < 9; ++q) S9.c[q] = d2(cd(1.0) * st_k[q] + mc * st_m[q]);
+      const int blocks = std::max(1, std::min(296, cdiv(n, 256)));
+      launch(FETIGPU_K_OTHER, [&] {
+        k_stencil_residual_part<<<blocks, 256, 0, stream>>>(P.nx - 1, P.ny - 1, S9, x, rhs, d_part);
+      });
+      launch(FETIGPU_K_OTHER, [&] { k_norm_max_final<<<1, 32, 0, stream>>>(blocks, d_part, d_stat + sb + 2); });
+    } else {
+      apply_global<double2>(x, nullptr, 1.0, mc, d_ax);
+      launch(FETIGPU_K_GLOBAL, [&] { k_sub<<<cdiv(n, 256), 256, 0, stream>>>(n, d_ax, rhs, d_ax); });
+      norm_async(d_ax, n, sb + 2);
+    }
+    phase("stats");
     st.solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return st;
   }
@@ -1645,8 +1730,10 @@ struct Ctx {
     // |lambda|_inf for the leak warning
     launch(FETIGPU_K_GLOBAL, [&] { k_real_to_complex<<<cdiv(n, 256), 256, 0, stream>>>(n, lam, d_ax); });
     norm_async(d_ax, n, 9);
+    phase("recovery");
     stats_to_host();
     sync();  // the call's one final synchronisation
+    phase_report();
     if (host_lam != nullptr) CU(cudaStreamSynchronize(copy_stream));
     finalize_feti_stats(sp, 0);
     finalize_feti_stats(sm, 4);

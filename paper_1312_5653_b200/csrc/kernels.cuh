@@ -1712,6 +1712,20 @@ __global__ void __launch_bounds__(32) k_backsub(const GmresState* __restrict__ s
   }
 }
 
+// first GMRES cycle without a host round trip: |b| from the statistics slot (sum of squares)
+__global__ void k_scale_by_norm(int n, const double2* __restrict__ x, const double2* __restrict__ nrm2,
+                                double2* __restrict__ y) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const double s2 = nrm2->x;
+  if (k < n) y[k] = s2 > 0.0 ? cscale(x[k], 1.0 / sqrt(s2)) : cz();
+}
+__global__ void k_gmres_init(GmresState* __restrict__ st, const double2* __restrict__ nrm2, double2* __restrict__ g) {
+  if (threadIdx.x != 0) return;
+  const double bn = sqrt(nrm2->x);
+  st->bnorm = bn;
+  st->cont = bn > 0.0 ? 1 : 0;  // zero rhs: the (fused) step kernels all return at once
+  g[0] = make_double2(bn, 0.0);
+}
 __global__ void k_scale_copy(int n, const double2* __restrict__ x, double s, double2* __restrict__ y) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) y[k] = cscale(x[k], s);
@@ -1885,7 +1899,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   const int row_end = min(a.n, row0 + a.rows_pb);  // exclusive
   pdl_trigger();
   pdl_wait();
-  if (a.st->cont == 0) return;  // unrolled WHILE body: the cycle already stopped
+  if (a.st->cont == 0) {  // unrolled WHILE body: the cycle already stopped (or never started:
+    // zero rhs) -- make sure the WHILE node exits
+    if (a.ga.in_graph && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.ga.handle, 0u);
+    return;
+  }
   const int nv = a.st->j + 1, nout = nv + 1, G = gridDim.x;
   const int it = a.st->iterations;
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 0] = gtimer();
@@ -2280,6 +2298,57 @@ __global__ void k_apply_stencil9(int fx, int fy, Stencil9 S, const T* __restrict
     }
   }
   store_c<T>(y + (size_t)J * fx + I, acc);
+}
+
+// Statistics without materialising the vectors: block partials (|v|^2, max|v|) of the
+// interface jump v_r = u_lo - u_hi (feti.cpp:708-709) and of the primal residual
+// v = (kc K + mc V) x - rhs on the structured stencil (feti.cpp:711-713).
+__device__ __forceinline__ void block_sum_max(double s, double m, double2* part) {
+  __shared__ double ss[32], sm_[32];
+  s = warp_sum(s);
+  m = warp_max(m);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) ss[warp] = s, sm_[warp] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ts = 0.0, tm = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) ts += ss[w], tm = fmax(tm, sm_[w]);
+    part[blockIdx.x] = make_double2(ts, tm);
+  }
+}
+__global__ void k_jump_norm_part(int nl, const int* __restrict__ lo, const int* __restrict__ hi,
+                                 const double2* __restrict__ u1b, double2* __restrict__ part) {
+  double s = 0.0, m = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < nl; r += gridDim.x * blockDim.x) {
+    const double a2 = cabs2(csub(u1b[lo[r]], u1b[hi[r]]));
+    s += a2;
+    m = fmax(m, sqrt(a2));
+  }
+  block_sum_max(s, m, part);
+}
+__global__ void k_stencil_residual_part(int fx, int fy, Stencil9 S, const double2* __restrict__ x,
+                                        const double2* __restrict__ rhs, double2* __restrict__ part) {
+  double s = 0.0, m = 0.0;
+  const long long total = (long long)fx * fy;
+  for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += (long long)gridDim.x * blockDim.x) {
+    const int I = (int)(f % fx), J = (int)(f / fx);
+    double2 acc = cz();
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int jj = J + dy;
+      if (jj < 0 || jj >= fy) continue;
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int ii = I + dx;
+        if (ii < 0 || ii >= fx) continue;
+        acc = cfma(S.c[(dy + 1) * 3 + dx + 1], x[(size_t)jj * fx + ii], acc);
+      }
+    }
+    const double a2 = cabs2(csub(acc, rhs[f]));
+    s += a2;
+    m = fmax(m, sqrt(a2));
+  }
+  block_sum_max(s, m, part);
 }
 
 // Kronecker mass solve V^-1 = (M_y ⊗ M_x ⊗ I_dpn)^-1: batches of identical SPD tridiagonal
