@@ -194,69 +194,163 @@ static void element_stiffness_plane_strain(double e, double nu, double h, double
   }
 }
 
+// ---- 3D extension (BASELINE.json configs 4-5; the reference is 2D only, SURVEY.md §0 F5,
+// §7 step 7).  Trilinear Q1 hexahedra, 2x2x2 Gauss (exact for the Q1 mass and stiffness),
+// local nodes counterclockwise in the bottom face then the top face (the 2D order of
+// mesh.cpp:31-34 extruded), 3 interleaved dofs per node for elasticity (fem.cpp:171).
+constexpr double kXi3[8] = {-1, 1, 1, -1, -1, 1, 1, -1};
+constexpr double kEta3[8] = {-1, -1, 1, 1, -1, -1, 1, 1};
+constexpr double kZeta3[8] = {-1, -1, -1, -1, 1, 1, 1, 1};
+static void shape3(int a, double x, double y, double z, double& n, double& dx, double& dy, double& dz) {
+  const double fx = 1.0 + kXi3[a] * x, fy = 1.0 + kEta3[a] * y, fz = 1.0 + kZeta3[a] * z;
+  n = 0.125 * fx * fy * fz;
+  dx = 0.125 * kXi3[a] * fy * fz;
+  dy = 0.125 * kEta3[a] * fx * fz;
+  dz = 0.125 * kZeta3[a] * fx * fy;
+}
+static void element_heat3d(double h, double k[64], double m[64]) {
+  const double g = 1.0 / std::sqrt(3.0), pts[2] = {-g, g};
+  const double detj = h * h * h / 8.0, gs = 2.0 / h;
+  std::fill(k, k + 64, 0.0);
+  std::fill(m, m + 64, 0.0);
+  for (double z : pts)
+    for (double y : pts)
+      for (double x : pts) {
+        double n[8], dx[8], dy[8], dz[8];
+        for (int a = 0; a < 8; ++a) shape3(a, x, y, z, n[a], dx[a], dy[a], dz[a]);
+        for (int a = 0; a < 8; ++a)
+          for (int b = 0; b < 8; ++b) {
+            m[a * 8 + b] += n[a] * n[b] * detj;
+            k[a * 8 + b] += (dx[a] * dx[b] + dy[a] * dy[b] + dz[a] * dz[b]) * gs * gs * detj;
+          }
+      }
+}
+static void element_elastic3d(double e, double nu, double h, double k[576], double m[576]) {
+  const double f = e / ((1.0 + nu) * (1.0 - 2.0 * nu));
+  double d[6][6] = {};
+  for (int p = 0; p < 3; ++p)
+    for (int q = 0; q < 3; ++q) d[p][q] = f * (p == q ? 1.0 - nu : nu);
+  for (int p = 3; p < 6; ++p) d[p][p] = f * (1.0 - 2.0 * nu) / 2.0;
+  const double g = 1.0 / std::sqrt(3.0), pts[2] = {-g, g};
+  const double detj = h * h * h / 8.0, gs = 2.0 / h;
+  std::fill(k, k + 576, 0.0);
+  for (double z : pts)
+    for (double y : pts)
+      for (double x : pts) {
+        double b[6][24] = {};
+        for (int a = 0; a < 8; ++a) {
+          double n, dx, dy, dz;
+          shape3(a, x, y, z, n, dx, dy, dz);
+          dx *= gs, dy *= gs, dz *= gs;
+          b[0][3 * a] = dx;
+          b[1][3 * a + 1] = dy;
+          b[2][3 * a + 2] = dz;
+          b[3][3 * a] = dy, b[3][3 * a + 1] = dx;
+          b[4][3 * a + 1] = dz, b[4][3 * a + 2] = dy;
+          b[5][3 * a] = dz, b[5][3 * a + 2] = dx;
+        }
+        for (int i = 0; i < 24; ++i)
+          for (int j = i; j < 24; ++j) {
+            double acc = 0.0;
+            for (int p = 0; p < 6; ++p)
+              for (int q = 0; q < 6; ++q) acc += b[p][i] * d[p][q] * b[q][j];
+            k[i * 24 + j] += detj * acc;
+          }
+      }
+  for (int i = 0; i < 24; ++i)  // exactly symmetric
+    for (int j = 0; j < i; ++j) k[i * 24 + j] = k[j * 24 + i];
+  double kh[64], mh[64];
+  element_heat3d(h, kh, mh);
+  std::fill(m, m + 576, 0.0);
+  for (int a = 0; a < 8; ++a)
+    for (int b2 = 0; b2 < 8; ++b2)
+      for (int c = 0; c < 3; ++c) m[(3 * a + c) * 24 + 3 * b2 + c] = mh[a * 8 + b2];
+}
+
 struct Problem {
-  int nx = 0, ny = 0, dpn = 1, physics = 0;  // physics 0 = heat, 1 = plane strain
-  double h = 0, lx = 1, ly = 1, E = 0, nu = 0;
+  int nx = 0, ny = 0, nz = 0, dpn = 1, physics = 0;  // physics 0 = heat, 1 = plane strain / 3D elasticity
+  double h = 0, lx = 1, ly = 1, lz = 0, E = 0, nu = 0;  // nz = 0: 2D (the reference), nz > 0: 3D
   std::vector<int> free_map, cons_map, free_dofs, cons_dofs;
   Csr K, V, Kc;
   double mass_sum = 0;
-  double ke[64], me[64];
+  double ke[576], me[576];
   int edofs = 4;
   int n() const { return K.nr; }
   int m() const { return Kc.nc; }
-  int node_id(int i, int j) const { return j * (nx + 1) + i; }
+  bool is3d() const { return nz > 0; }
+  int npe() const { return nz > 0 ? 8 : 4; }
+  int node_id(int i, int j, int k = 0) const { return (k * (ny + 1) + j) * (nx + 1) + i; }
   double node_x(int id) const { return (id % (nx + 1)) * h; }
-  double node_y(int id) const { return (id / (nx + 1)) * h; }
-  void elem_nodes(int e, int out[4]) const {
-    const int i = e % nx, j = e / nx;  // mesh.cpp:31-34, counterclockwise
-    out[0] = node_id(i, j);
-    out[1] = node_id(i + 1, j);
-    out[2] = node_id(i + 1, j + 1);
-    out[3] = node_id(i, j + 1);
+  double node_y(int id) const { return ((id / (nx + 1)) % (ny + 1)) * h; }
+  double node_z(int id) const { return (id / ((nx + 1) * (ny + 1))) * h; }
+  void elem_nodes(int e, int out[8]) const {
+    const int i = e % nx, j = (e / nx) % ny, k = nz > 0 ? e / (nx * ny) : 0;  // mesh.cpp:31-34, counterclockwise
+    out[0] = node_id(i, j, k);
+    out[1] = node_id(i + 1, j, k);
+    out[2] = node_id(i + 1, j + 1, k);
+    out[3] = node_id(i, j + 1, k);
+    if (nz > 0) {
+      out[4] = node_id(i, j, k + 1);
+      out[5] = node_id(i + 1, j, k + 1);
+      out[6] = node_id(i + 1, j + 1, k + 1);
+      out[7] = node_id(i, j + 1, k + 1);
+    }
   }
+  int n_elems() const { return nx * ny * (nz > 0 ? nz : 1); }
 };
 
-// mesh.cpp:7-36 + fem.cpp:119-192
-static Problem* build_problem(int nx, int ny, double lx, double ly, int physics, double E, double nu) {
-  if (nx < 2 || ny < 2) throw ContractError("build_rectangle_mesh: need at least 2 elements per axis");
-  if (lx <= 0 || ly <= 0) throw ContractError("build_rectangle_mesh: non-positive extent");
-  const double hx = lx / nx, hy = ly / ny;
-  if (std::abs(hx - hy) > 1e-12 * std::max(hx, hy))
+// mesh.cpp:7-36 + fem.cpp:119-192 (nz = 0); the 3D extension with nz > 0: whole-boundary
+// Dirichlet for heat, clamped face x = 0 for elasticity (BASELINE.json configs 4-5)
+static Problem* build_problem_any(int nx, int ny, int nz, double lx, double ly, double lz, int physics, double E,
+                                  double nu) {
+  const bool d3 = nz > 0;
+  if (nx < 2 || ny < 2 || (d3 && nz < 2)) throw ContractError("build_rectangle_mesh: need at least 2 elements per axis");
+  if (lx <= 0 || ly <= 0 || (d3 && lz <= 0)) throw ContractError("build_rectangle_mesh: non-positive extent");
+  const double hx = lx / nx, hy = ly / ny, hz = d3 ? lz / nz : hx;
+  if (std::abs(hx - hy) > 1e-12 * std::max(hx, hy) || std::abs(hx - hz) > 1e-12 * std::max(hx, hz))
     throw ContractError("build_rectangle_mesh: elements must be square");
   auto p = std::make_unique<Problem>();
   p->nx = nx;
   p->ny = ny;
+  p->nz = d3 ? nz : 0;
   p->lx = lx;
   p->ly = ly;
+  p->lz = d3 ? lz : 0.0;
   p->h = hx;
   p->physics = physics;
   p->E = E;
   p->nu = nu;
-  p->dpn = physics == 0 ? 1 : 2;
+  p->dpn = physics == 0 ? 1 : (d3 ? 3 : 2);
   const int dpn = p->dpn;
-  if (physics == 0) {
-    element_stiffness_heat(p->ke);
-    element_mass_heat(p->h, p->me);
-    p->edofs = 4;
-  } else {
+  if (physics != 0) {
     if (!(nu > 0.0 && nu < 0.5)) throw ContractError("Physics: poisson_ratio must lie strictly in (0, 0.5)");
     if (E <= 0.0) throw ContractError("Physics: young_modulus must be positive");
+  }
+  if (!d3 && physics == 0) {
+    element_stiffness_heat(p->ke);
+    element_mass_heat(p->h, p->me);
+  } else if (!d3) {
     element_stiffness_plane_strain(E, nu, p->h, p->ke);
     element_mass_elastic(p->h, p->me);
-    p->edofs = 8;
+  } else if (physics == 0) {
+    element_heat3d(p->h, p->ke, p->me);
+  } else {
+    element_elastic3d(E, nu, p->h, p->ke, p->me);
   }
-  const int nn = (nx + 1) * (ny + 1), nmd = nn * dpn;
+  p->edofs = p->npe() * dpn;
+  const int nzz = d3 ? nz : 0;
+  const int nn = (nx + 1) * (ny + 1) * (nzz + 1), nmd = nn * dpn;
   std::vector<char> cons(nmd, 0);
-  if (physics == 0) {  // whole boundary (fem.cpp:121-122)
+  for (int k = 0; k <= nzz; ++k)
     for (int j = 0; j <= ny; ++j)
-      for (int i = 0; i <= nx; ++i)
-        if (i == 0 || i == nx || j == 0 || j == ny) cons[p->node_id(i, j)] = 1;
-  } else {  // clamped x = 0 (fem.cpp:124-128)
-    for (int j = 0; j <= ny; ++j) {
-      cons[2 * p->node_id(0, j)] = 1;
-      cons[2 * p->node_id(0, j) + 1] = 1;
-    }
-  }
+      for (int i = 0; i <= nx; ++i) {
+        const int node = p->node_id(i, j, k);
+        if (physics == 0) {  // whole boundary (fem.cpp:121-122)
+          if (i == 0 || i == nx || j == 0 || j == ny || (d3 && (k == 0 || k == nz))) cons[node] = 1;
+        } else if (i == 0) {  // clamped x = 0 (fem.cpp:124-128)
+          for (int c = 0; c < dpn; ++c) cons[dpn * node + c] = 1;
+        }
+      }
   p->free_map.assign(nmd, -1);
   p->cons_map.assign(nmd, -1);
   for (int d = 0; d < nmd; ++d) {
@@ -269,14 +363,14 @@ static Problem* build_problem(int nx, int ny, double lx, double ly, int physics,
     }
   }
   const int n = (int)p->free_dofs.size(), m = (int)p->cons_dofs.size();
-  const int ed = p->edofs;
+  const int ed = p->edofs, npe = p->npe();
   std::vector<Trip> tk, tv, tkc;
-  tk.reserve((size_t)nx * ny * ed * ed);
+  tk.reserve((size_t)p->n_elems() * ed * ed);
   tv.reserve(tk.capacity());
-  int gd[8], en[4];
-  for (int e = 0; e < nx * ny; ++e) {
+  int gd[24], en[8];
+  for (int e = 0; e < p->n_elems(); ++e) {
     p->elem_nodes(e, en);
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < npe; ++a)
       for (int c = 0; c < dpn; ++c) gd[dpn * a + c] = dpn * en[a] + c;
     for (int a = 0; a < ed; ++a) {
       const int fa = p->free_map[gd[a]];
@@ -297,6 +391,9 @@ static Problem* build_problem(int nx, int ny, double lx, double ly, int physics,
   p->V = csr_from_triplets(n, n, std::move(tv));
   p->Kc = csr_from_triplets(n, m, std::move(tkc));
   return p.release();
+}
+static Problem* build_problem(int nx, int ny, double lx, double ly, int physics, double E, double nu) {
+  return build_problem_any(nx, ny, 0, lx, ly, 0.0, physics, E, nu);
 }
 
 // fem.cpp:194-202
@@ -327,8 +424,12 @@ static void sine_modes(uint64_t seed, int modes, int mmax, double* a, int* m, in
 
 // ------------------------------------------------------------ partition (feti.cpp:34-169)
 struct Sub {
-  std::vector<int> elements, dofs, corner_local, corner_global, r_local, r_interior, r_boundary,
-      lambda_rows;
+  std::vector<int> elements, dofs, corner_local, corner_global, r_local, r_interior, r_boundary;
+  // signed Boolean jump entries B^s(row, rpos) = sign.  In 2D every interface dof has exactly
+  // one multiplier row, so entry k is boundary dof k (feti.cpp:98-121).  In 3D a dof on a
+  // subdomain edge (multiplicity 4) is in 3 rows of this subdomain: lambda_bidx[k] is the
+  // boundary index and lambda_rpos[k] the r-position of entry k.
+  std::vector<int> lambda_rows, lambda_rpos, lambda_bidx;
   RVec lambda_signs, weights;
 };
 struct Edge {  // feti.hpp:59-65: open segment between subdomain-grid vertices
@@ -338,7 +439,11 @@ struct Edge {  // feti.hpp:59-65: open segment between subdomain-grid vertices
 };
 struct Partition {
   int sx = 0, sy = 0, ex = 0, ey = 0, dpn = 1, n_free = 0, n_corner = 0, n_lambda = 0, n_edges = 0;
+  int sz = 1, ez = 0;  // 3D extension (sz = 1, ez = 0 in 2D)
   double h = 0;
+  // Dirichlet-preconditioner scaling W of each multiplier row: 1/multiplicity of its node
+  // (the reference hard-codes W = 1/2, feti.cpp:602, 626, which is 1/mult in 2D)
+  RVec lam_weight;
   std::vector<Sub> subs;
   std::vector<int> free_mult;
   std::vector<Edge> edges;
@@ -414,6 +519,8 @@ static Partition partition_structured(const Problem& P, int sx, int sy) {
               const int rpos = (int)s.r_local.size();
               s.r_local.push_back(local);
               if (lambda_of[md] >= 0) {
+                s.lambda_bidx.push_back((int)s.r_boundary.size());
+                s.lambda_rpos.push_back(rpos);
                 s.r_boundary.push_back(rpos);
                 s.lambda_rows.push_back(lambda_of[md]);
                 auto [plo2, phi2] = owner_range(i, ex, sx);
@@ -457,7 +564,127 @@ static Partition partition_structured(const Problem& P, int sx, int sy) {
       add_edge(std::move(e));
     }
   part.n_edges = (int)part.edges.size();
+  part.lam_weight.assign(part.n_lambda, 0.5);
   return part;
+}
+
+// 3D extension of partition_structured (new: the reference rejects multiplicity 4,
+// feti.cpp:76-78).  Same corner rule (subdomain-grid vertices that are free with
+// multiplicity >= 2), same +1-for-the-lower-subdomain sign rule, applied pairwise: a
+// non-corner interface dof shared by subdomains s_1 < ... < s_m gets one row per pair
+// (s_a, s_b), a < b (fully redundant multipliers; m = 2 on faces, 4 on subdomain edges).
+// Rows ascend by (node, component, pair); the Dirichlet scaling is W = 1/m per row.
+static Partition partition_structured3d(const Problem& P, int sx, int sy, int sz) {
+  if (!P.is3d()) throw ContractError("partition_structured3d: 2D problem");
+  if (sx < 1 || sy < 1 || sz < 1 || sx * sy * sz < 2) throw ContractError("partition_structured: need at least two subdomains");
+  if (P.nx % sx != 0 || P.ny % sy != 0 || P.nz % sz != 0)
+    throw ContractError("partition_structured: subdomain grid must divide the element grid");
+  const int ex = P.nx / sx, ey = P.ny / sy, ez = P.nz / sz;
+  if (ex < 2 || ey < 2 || ez < 2) throw ContractError("partition_structured: H/h must be at least 2");
+  const int dpn = P.dpn;
+  Partition part;
+  part.sx = sx, part.sy = sy, part.sz = sz;
+  part.ex = ex, part.ey = ey, part.ez = ez;
+  part.dpn = dpn;
+  part.n_free = P.n();
+  part.h = P.h;
+  const int nn = (P.nx + 1) * (P.ny + 1) * (P.nz + 1);
+  std::vector<int> mult(nn, 0);
+  std::vector<char> corner(nn, 0);
+  auto owners = [&](int node) {
+    const int i = node % (P.nx + 1), j = (node / (P.nx + 1)) % (P.ny + 1), k = node / ((P.nx + 1) * (P.ny + 1));
+    auto [plo, phi] = owner_range(i, ex, sx);
+    auto [qlo, qhi] = owner_range(j, ey, sy);
+    auto [rlo, rhi] = owner_range(k, ez, sz);
+    std::vector<int> o;
+    for (int r = rlo; r <= rhi; ++r)
+      for (int q = qlo; q <= qhi; ++q)
+        for (int p = plo; p <= phi; ++p) o.push_back((r * sy + q) * sx + p);  // ascending
+    return o;
+  };
+  for (int k = 0; k <= P.nz; ++k)
+    for (int j = 0; j <= P.ny; ++j)
+      for (int i = 0; i <= P.nx; ++i) {
+        const int node = P.node_id(i, j, k);
+        auto [plo, phi] = owner_range(i, ex, sx);
+        auto [qlo, qhi] = owner_range(j, ey, sy);
+        auto [rlo, rhi] = owner_range(k, ez, sz);
+        mult[node] = (phi - plo + 1) * (qhi - qlo + 1) * (rhi - rlo + 1);
+        const bool fr = P.free_map[node * dpn] >= 0;
+        corner[node] = (i % ex == 0) && (j % ey == 0) && (k % ez == 0) && mult[node] >= 2 && fr;
+      }
+  // rows of node*dpn+c: first row id and the owner list (pairs in lexicographic order)
+  std::vector<int> corner_of(nn * dpn, -1), lambda0(nn * dpn, -1);
+  for (int node = 0; node < nn; ++node) {
+    if (P.free_map[node * dpn] < 0) continue;
+    if (corner[node]) {
+      for (int c = 0; c < dpn; ++c) corner_of[node * dpn + c] = part.n_corner++;
+    } else if (mult[node] >= 2) {
+      const int m = mult[node], pairs = m * (m - 1) / 2;
+      for (int c = 0; c < dpn; ++c) {
+        lambda0[node * dpn + c] = part.n_lambda;
+        part.n_lambda += pairs;
+        for (int q = 0; q < pairs; ++q) part.lam_weight.push_back(1.0 / m);
+      }
+    }
+  }
+  part.free_mult.assign(part.n_free, 1);
+  for (int node = 0; node < nn; ++node)
+    for (int c = 0; c < dpn; ++c) {
+      const int f = P.free_map[node * dpn + c];
+      if (f >= 0) part.free_mult[f] = mult[node];
+    }
+  part.subs.resize(sx * sy * sz);
+  for (int r = 0; r < sz; ++r)
+    for (int q = 0; q < sy; ++q)
+      for (int p = 0; p < sx; ++p) {
+        const int sid = (r * sy + q) * sx + p;
+        Sub& s = part.subs[sid];
+        for (int k = r * ez; k < (r + 1) * ez; ++k)
+          for (int j = q * ey; j < (q + 1) * ey; ++j)
+            for (int i = p * ex; i < (p + 1) * ex; ++i) s.elements.push_back((k * P.ny + j) * P.nx + i);
+        for (int k = r * ez; k <= (r + 1) * ez; ++k)
+          for (int j = q * ey; j <= (q + 1) * ey; ++j)
+            for (int i = p * ex; i <= (p + 1) * ex; ++i) {
+              const int node = P.node_id(i, j, k);
+              std::vector<int> own;
+              if (mult[node] >= 2 && !corner[node]) own = owners(node);
+              for (int c = 0; c < dpn; ++c) {
+                const int md = node * dpn + c, f = P.free_map[md];
+                if (f < 0) continue;
+                const int local = (int)s.dofs.size();
+                s.dofs.push_back(f);
+                s.weights.push_back(1.0 / mult[node]);
+                if (corner[node]) {
+                  s.corner_local.push_back(local);
+                  s.corner_global.push_back(corner_of[md]);
+                  continue;
+                }
+                const int rpos = (int)s.r_local.size();
+                s.r_local.push_back(local);
+                if (lambda0[md] < 0) {
+                  s.r_interior.push_back(rpos);
+                  continue;
+                }
+                const int bidx = (int)s.r_boundary.size();
+                s.r_boundary.push_back(rpos);
+                int row = lambda0[md];
+                for (size_t a = 0; a < own.size(); ++a)
+                  for (size_t b = a + 1; b < own.size(); ++b, ++row) {
+                    if (own[a] != sid && own[b] != sid) continue;
+                    s.lambda_rows.push_back(row);
+                    s.lambda_rpos.push_back(rpos);
+                    s.lambda_bidx.push_back(bidx);
+                    s.lambda_signs.push_back(own[a] == sid ? 1.0 : -1.0);
+                  }
+              }
+            }
+      }
+  part.n_edges = 0;  // edge-RBM augmentation is 2D only
+  return part;
+}
+static Partition partition_any(const Problem& P, int sx, int sy, int sz) {
+  return P.is3d() ? partition_structured3d(P, sx, sy, sz) : partition_structured(P, sx, sy);
 }
 
 // ------------------------------------------- edge-RBM augmentation (feti.cpp:171-242)
@@ -800,7 +1027,7 @@ struct Feti {
   // feti.cpp:244-364 (assembly + local factorizations; serial as in the reference)
   void assemble() {
     const int dpn = P->dpn, ed = P->edofs;
-    cd ae[64];
+    cd ae[576];
     for (int q = 0; q < ed * ed; ++q) ae[q] = kcoef * cd(P->ke[q]) + mcoef * cd(P->me[q]);
     const int ns = (int)part.subs.size();
     blk.resize(ns);
@@ -819,10 +1046,11 @@ struct Feti {
       for (int l = 0; l < nl; ++l) local_of_free[sub.dofs[l]] = l;
       std::vector<std::tuple<int, int, cd>> trr, tii;
       B.acc.assign((size_t)nc_ * nc_, cd(0));
-      int gd[8], en[4];
+      int gd[24], en[8];
+      const int npe = P->npe();
       for (int e : sub.elements) {
         P->elem_nodes(e, en);
-        for (int a = 0; a < 4; ++a)
+        for (int a = 0; a < npe; ++a)
           for (int c = 0; c < dpn; ++c) gd[dpn * a + c] = dpn * en[a] + c;
         for (int a = 0; a < ed; ++a) {
           const int fa = P->free_map[gd[a]];
@@ -886,7 +1114,7 @@ struct Feti {
           auto it = std::lower_bound(row_of.begin(), row_of.end(), std::make_pair(aug[q].rows[k], -1));
           if (it != row_of.end() && it->first == aug[q].rows[k]) {
             const int kk = it->second;
-            ent.emplace_back(sub.r_boundary[kk], sub.lambda_signs[kk] * aug[q].values[k]);
+            ent.emplace_back(sub.lambda_rpos[kk], sub.lambda_signs[kk] * aug[q].values[k]);
           }
         }
         if (!ent.empty()) {
@@ -1037,7 +1265,7 @@ struct Feti {
     for (size_t s = 0; s < part.subs.size(); ++s) {
       const Sub& sub = part.subs[s];
       for (size_t k = 0; k < sub.lambda_rows.size(); ++k)
-        out[sub.lambda_rows[k]] += sub.lambda_signs[k] * ur[s][sub.r_boundary[k]];
+        out[sub.lambda_rows[k]] += sub.lambda_signs[k] * ur[s][sub.lambda_rpos[k]];
     }
     return out;
   }
@@ -1049,7 +1277,7 @@ struct Feti {
       const Sub& sub = part.subs[s];
       t[s].assign(sub.r_local.size(), cd(0));
       for (size_t k = 0; k < sub.lambda_rows.size(); ++k)
-        t[s][sub.r_boundary[k]] = -sub.lambda_signs[k] * lam[sub.lambda_rows[k]];
+        t[s][sub.lambda_rpos[k]] -= sub.lambda_signs[k] * lam[sub.lambda_rows[k]];
     }
     std::vector<CVec> ur;
     CVec z;
@@ -1059,17 +1287,18 @@ struct Feti {
     return out;
   }
 
-  CVec apply_dirichlet(const CVec& res) const {  // 597-627
+  CVec apply_dirichlet(const CVec& res) const {  // 597-627; W = 1/2 there, 1/mult per row here
     const int ns = (int)part.subs.size();
     CVec wr(res.size());
-    for (size_t i = 0; i < res.size(); ++i) wr[i] = res[i] / 2.0;
+    for (size_t i = 0; i < res.size(); ++i) wr[i] = res[i] * part.lam_weight[i];
     std::vector<CVec> contrib(ns);
     parallel_for(ns, threads, [&](int s) {
       const Sub& sub = part.subs[s];
       const Block& B = blk[s];
       const int nb = (int)sub.r_boundary.size(), ni = (int)sub.r_interior.size();
-      CVec vb(nb);
-      for (size_t k = 0; k < sub.lambda_rows.size(); ++k) vb[k] = sub.lambda_signs[k] * wr[sub.lambda_rows[k]];
+      CVec vb(nb, cd(0));
+      for (size_t k = 0; k < sub.lambda_rows.size(); ++k)
+        vb[sub.lambda_bidx[k]] += sub.lambda_signs[k] * wr[sub.lambda_rows[k]];
       CVec wb(nb, cd(0));
       for (auto& [i, j, v] : B.abb) wb[i] += v * vb[j];
       if (ni > 0) {
@@ -1083,9 +1312,10 @@ struct Feti {
     CVec out(part.n_lambda, cd(0));
     for (int s = 0; s < ns; ++s) {
       const Sub& sub = part.subs[s];
-      for (size_t k = 0; k < sub.lambda_rows.size(); ++k) out[sub.lambda_rows[k]] += sub.lambda_signs[k] * contrib[s][k];
+      for (size_t k = 0; k < sub.lambda_rows.size(); ++k)
+        out[sub.lambda_rows[k]] += sub.lambda_signs[k] * contrib[s][sub.lambda_bidx[k]];
     }
-    for (auto& v : out) v /= 2.0;
+    for (size_t i = 0; i < out.size(); ++i) out[i] *= part.lam_weight[i];
     return out;
   }
 
@@ -1133,7 +1363,7 @@ struct Feti {
       const Sub& sub = part.subs[s];
       t[s] = fr[s];
       for (size_t k = 0; k < sub.lambda_rows.size(); ++k)
-        t[s][sub.r_boundary[k]] -= sub.lambda_signs[k] * lam[sub.lambda_rows[k]];
+        t[s][sub.lambda_rpos[k]] -= sub.lambda_signs[k] * lam[sub.lambda_rows[k]];
     }
     eliminate(t, fc, ur, z);
     CVec x(part.n_free, cd(0));
@@ -1276,6 +1506,10 @@ void fill(OrcStats* o, const FetiStats& s) {
 extern "C" {
 const char* orc_last_error() { return g_err.c_str(); }
 
+int orc_problem_create3(int nx, int ny, int nz, double lx, double ly, double lz, int physics, double E, double nu,
+                        void** out) {
+  return guard([&] { *out = build_problem_any(nx, ny, nz, lx, ly, lz, physics, E, nu); });
+}
 int orc_problem_create(int nx, int ny, double lx, double ly, int physics, double E, double nu, void** out) {
   return guard([&] { *out = build_problem(nx, ny, lx, ly, physics, E, nu); });
 }
@@ -1328,13 +1562,36 @@ void orc_target_sine(void* p, unsigned long long seed, int modes, int mmax, doub
     out[f] = v;
   }
 }
+// 3D seeded target: per mode a_k (Box-Muller), then l_k, m_k, n_k = 1 + rng() % M
+void orc_target_sine3(void* p, unsigned long long seed, int modes, int mmax, double* out) {
+  auto* P = static_cast<Problem*>(p);
+  std::mt19937_64 g(seed);
+  std::vector<double> a(modes);
+  std::vector<int> l(modes), m(modes), nn(modes);
+  for (int k = 0; k < modes; ++k) {
+    const double u1 = u01(g), u2 = u01(g);
+    a[k] = std::sqrt(-2.0 * std::log(1.0 - u1)) * std::cos(2.0 * M_PI * u2);
+    l[k] = 1 + (int)(g() % (uint64_t)mmax);
+    m[k] = 1 + (int)(g() % (uint64_t)mmax);
+    nn[k] = 1 + (int)(g() % (uint64_t)mmax);
+  }
+  for (int f = 0; f < P->n(); ++f) {
+    const int node = P->free_dofs[f] / P->dpn;
+    const double x = P->node_x(node), y = P->node_y(node), z = P->node_z(node);
+    double v = 0.0;
+    for (int k = 0; k < modes; ++k)
+      v += a[k] * std::sin(l[k] * M_PI * x) * std::sin(m[k] * M_PI * y) * std::sin(nn[k] * M_PI * z);
+    out[f] = v;
+  }
+}
 void orc_sine_modes(unsigned long long seed, int modes, int mmax, double* a, int* m, int* n) {
   sine_modes(seed, modes, mmax, a, m, n);
 }
-// info: [n_sub, n_corner, n_lambda, n_edges, ex, ey]
-int orc_partition_info(void* p, int sx, int sy, int* info) {
+// info: [n_sub, n_corner, n_lambda, n_edges, ex, ey, ez]
+int orc_partition_info3(void* p, int sx, int sy, int sz, int* info) {
   return guard([&] {
-    Partition part = partition_structured(*static_cast<Problem*>(p), sx, sy);
+    Partition part = partition_any(*static_cast<Problem*>(p), sx, sy, sz);
+    info[6] = part.ez;
     info[0] = (int)part.subs.size();
     info[1] = part.n_corner;
     info[2] = part.n_lambda;
@@ -1344,12 +1601,33 @@ int orc_partition_info(void* p, int sx, int sy, int* info) {
   });
 }
 
-int orc_feti_create(void* p, int sx, int sy, double kre, double kim, double mre, double mim, double tol,
-                    int max_iter, int threads, int augment, void** out) {
+int orc_partition_info(void* p, int sx, int sy, int* info) {
+  int tmp[7];
+  const int rc = orc_partition_info3(p, sx, sy, 1, tmp);
+  if (rc == 0) std::copy(tmp, tmp + 6, info);
+  return rc;
+}
+// per-subdomain sizes of a partition: out[s*5 + {0..4}] = n_r, n_i, n_b, n_c, jump entries
+int orc_partition_sizes(void* p, int sx, int sy, int sz, int* out) {
+  return guard([&] {
+    Partition part = partition_any(*static_cast<Problem*>(p), sx, sy, sz);
+    for (size_t s = 0; s < part.subs.size(); ++s) {
+      const Sub& b = part.subs[s];
+      out[s * 5 + 0] = (int)b.r_local.size();
+      out[s * 5 + 1] = (int)b.r_interior.size();
+      out[s * 5 + 2] = (int)b.r_boundary.size();
+      out[s * 5 + 3] = (int)b.corner_local.size();
+      out[s * 5 + 4] = (int)b.lambda_rows.size();
+    }
+  });
+}
+int orc_feti_create3(void* p, int sx, int sy, int sz, double kre, double kim, double mre, double mim, double tol,
+                     int max_iter, int threads, int augment, void** out) {
   return guard([&] {
     auto F = std::make_unique<Feti>();
     F->P = static_cast<Problem*>(p);
-    F->part = partition_structured(*F->P, sx, sy);
+    if (augment && F->P->is3d()) throw ContractError("feti: edge-RBM augmentation is 2D only");
+    F->part = partition_any(*F->P, sx, sy, sz);
     F->augment = augment != 0;
     F->kcoef = cd(kre, kim);
     F->mcoef = cd(mre, mim);
@@ -1359,6 +1637,10 @@ int orc_feti_create(void* p, int sx, int sy, double kre, double kim, double mre,
     F->setup();
     *out = F.release();
   });
+}
+int orc_feti_create(void* p, int sx, int sy, double kre, double kim, double mre, double mim, double tol,
+                    int max_iter, int threads, int augment, void** out) {
+  return orc_feti_create3(p, sx, sy, 1, kre, kim, mre, mim, tol, max_iter, threads, augment, out);
 }
 void orc_feti_destroy(void* f) { delete static_cast<Feti*>(f); }
 int orc_feti_n_lambda(void* f) { return static_cast<Feti*>(f)->part.n_lambda; }
@@ -1399,9 +1681,9 @@ int orc_feti_solve(void* f, const double* rhs, double* x, OrcStats* st, double* 
 // Range-space Schur solve (control.cpp:297-334). Two independent FETI setups, as
 // in the reference (control.cpp:303-304). times[0] = setup seconds (both factors),
 // times[1] = solve seconds (both FETI solves + recovery).
-int orc_schur_solve(void* p, int sx, int sy, double phi, const double* ybar, const double* yc, double tol,
-                    int max_iter, int threads, int augment, double* y, double* u, double* lam, OrcStats* plus,
-                    OrcStats* minus, double* imag_leak, double* times) {
+int orc_schur_solve3(void* p, int sx, int sy, int sz, double phi, const double* ybar, const double* yc, double tol,
+                     int max_iter, int threads, int augment, double* y, double* u, double* lam, OrcStats* plus,
+                     OrcStats* minus, double* imag_leak, double* times) {
   return guard([&] {
     auto* P = static_cast<Problem*>(p);
     if (!(phi > 0.0)) throw ContractError("ControlProblem: phi must be positive");
@@ -1411,7 +1693,7 @@ int orc_schur_solve(void* p, int sx, int sy, double phi, const double* ybar, con
     Feti fp, fm;
     for (Feti* F : {&fp, &fm}) {
       F->P = P;
-      F->part = partition_structured(*P, sx, sy);
+      F->part = partition_any(*P, sx, sy, sz);
       F->augment = augment != 0;
       F->kcoef = 1.0;
       F->tol = tol;
@@ -1457,6 +1739,13 @@ int orc_schur_solve(void* p, int sx, int sy, double phi, const double* ybar, con
   });
 }
 
+int orc_schur_solve(void* p, int sx, int sy, double phi, const double* ybar, const double* yc, double tol,
+                    int max_iter, int threads, int augment, double* y, double* u, double* lam, OrcStats* plus,
+                    OrcStats* minus, double* imag_leak, double* times) {
+  return orc_schur_solve3(p, sx, sy, 1, phi, ybar, yc, tol, max_iter, threads, augment, y, u, lam, plus, minus,
+                          imag_leak, times);
+}
+
 // Persistent pair of factor solvers (the two ComplexFactorSolver of control.cpp:303-304)
 // so timing can separate setup from per-solve cost (experiments.cpp:264-265).
 struct SchurPair {
@@ -1464,8 +1753,8 @@ struct SchurPair {
   Feti plus, minus;
   double phi;
 };
-int orc_schur_create(void* p, int sx, int sy, double phi, double tol, int max_iter, int threads, int augment,
-                     void** out, double* setup_seconds) {
+int orc_schur_create3(void* p, int sx, int sy, int sz, double phi, double tol, int max_iter, int threads,
+                      int augment, void** out, double* setup_seconds) {
   return guard([&] {
     auto* P = static_cast<Problem*>(p);
     if (!(phi > 0.0)) throw ContractError("ControlProblem: phi must be positive");
@@ -1476,7 +1765,7 @@ int orc_schur_create(void* p, int sx, int sy, double phi, double tol, int max_it
     auto t0 = std::chrono::steady_clock::now();
     for (Feti* F : {&sp->plus, &sp->minus}) {
       F->P = P;
-      F->part = partition_structured(*P, sx, sy);
+      F->part = partition_any(*P, sx, sy, sz);
       F->augment = augment != 0;
       F->kcoef = 1.0;
       F->tol = tol;
@@ -1490,6 +1779,10 @@ int orc_schur_create(void* p, int sx, int sy, double phi, double tol, int max_it
     if (setup_seconds) *setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = sp.release();
   });
+}
+int orc_schur_create(void* p, int sx, int sy, double phi, double tol, int max_iter, int threads, int augment,
+                     void** out, double* setup_seconds) {
+  return orc_schur_create3(p, sx, sy, 1, phi, tol, max_iter, threads, augment, out, setup_seconds);
 }
 void orc_schur_destroy(void* h) { delete static_cast<SchurPair*>(h); }
 int orc_schur_run(void* h, const double* ybar, const double* yc, double* y, double* u, double* lam, OrcStats* plus,

@@ -57,6 +57,8 @@ def lib():
         L.orc_last_error.restype = C.c_char_p
         L.orc_problem_create.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_double,
                                          C.c_double, C.POINTER(vp)]
+        L.orc_problem_create3.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,
+                                          C.c_double, C.c_double, C.POINTER(vp)]
         L.orc_problem_destroy.argtypes = [vp]
         for f in ("orc_problem_n", "orc_problem_m"):
             getattr(L, f).argtypes = [vp]
@@ -70,6 +72,16 @@ def lib():
         L.orc_target_sine.argtypes = [vp, C.c_ulonglong, C.c_int, C.c_int, dp]
         L.orc_sine_modes.argtypes = [C.c_ulonglong, C.c_int, C.c_int, dp, ip, ip]
         L.orc_partition_info.argtypes = [vp, C.c_int, C.c_int, ip]
+        L.orc_partition_info3.argtypes = [vp, C.c_int, C.c_int, C.c_int, ip]
+        L.orc_partition_sizes.argtypes = [vp, C.c_int, C.c_int, C.c_int, ip]
+        L.orc_target_sine3.argtypes = [vp, C.c_ulonglong, C.c_int, C.c_int, dp]
+        L.orc_feti_create3.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                       C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+        L.orc_schur_solve3.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_double, dp, dp, C.c_double, C.c_int,
+                                       C.c_int, C.c_int, dp, dp, dp, C.POINTER(OracleStats),
+                                       C.POINTER(OracleStats), dp, dp]
+        L.orc_schur_create3.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                        C.c_int, C.POINTER(vp), dp]
         L.orc_feti_create.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                       C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
         L.orc_feti_destroy.argtypes = [vp]
@@ -109,14 +121,17 @@ def _ip(a):
 
 
 class Problem:
-    """Mesh + Q1 assembly (mesh.cpp:7-36, fem.cpp:133-192). physics 0=heat, 1=plane strain."""
+    """Mesh + Q1 assembly (mesh.cpp:7-36, fem.cpp:133-192). physics 0=heat, 1=plane strain
+    (2D) / linear elasticity (3D).  n_z > 0: the 3D extension (trilinear hexahedra; BASELINE
+    configs 4-5), whole-boundary Dirichlet for heat, clamped face x = 0 for elasticity."""
 
-    def __init__(self, n_x, n_y=None, len_x=1.0, len_y=1.0, physics=0, young=0.0, poisson=0.0):
+    def __init__(self, n_x, n_y=None, len_x=1.0, len_y=1.0, physics=0, young=0.0, poisson=0.0, n_z=0, len_z=1.0):
         n_y = n_x if n_y is None else n_y
         h = C.c_void_p()
-        _check(lib().orc_problem_create(n_x, n_y, len_x, len_y, physics, young, poisson, C.byref(h)))
+        _check(lib().orc_problem_create3(n_x, n_y, n_z, len_x, len_y, len_z, physics, young, poisson, C.byref(h)))
         self._h = h
-        self.n_x, self.n_y, self.physics = n_x, n_y, physics
+        self.n_x, self.n_y, self.n_z, self.physics = n_x, n_y, n_z, physics
+        self.dim = 3 if n_z > 0 else 2
         self.n = lib().orc_problem_n(h)
         self.m = lib().orc_problem_m(h)
 
@@ -130,7 +145,8 @@ class Problem:
         return lib().orc_problem_mass_sum(self._h)
 
     def element_matrices(self):
-        ed = 4 if self.physics == 0 else 8
+        npe = 8 if self.dim == 3 else 4
+        ed = npe * (1 if self.physics == 0 else self.dim)
         ke = np.zeros((ed, ed))
         me = np.zeros((ed, ed))
         lib().orc_element_matrices(self._h, _dp(ke), _dp(me))
@@ -160,16 +176,29 @@ class Problem:
 
     def target_sine(self, seed, modes=8, mmax=8):
         out = np.zeros(self.n)
-        lib().orc_target_sine(self._h, seed, modes, mmax, _dp(out))
+        if self.dim == 3:
+            lib().orc_target_sine3(self._h, seed, modes, mmax, _dp(out))
+        else:
+            lib().orc_target_sine(self._h, seed, modes, mmax, _dp(out))
         return out
 
-    def partition_info(self, s_x, s_y):
-        info = np.zeros(6, dtype=np.int32)
-        _check(lib().orc_partition_info(self._h, s_x, s_y, _ip(info)))
-        keys = ("n_subdomains", "n_corner_dofs", "n_lambda", "n_edges", "ex", "ey")
-        return dict(zip(keys, (int(v) for v in info)))
+    def partition_info(self, s_x, s_y, s_z=1):
+        info = np.zeros(7, dtype=np.int32)
+        _check(lib().orc_partition_info3(self._h, s_x, s_y, s_z, _ip(info)))
+        keys = ("n_subdomains", "n_corner_dofs", "n_lambda", "n_edges", "ex", "ey", "ez")
+        d = dict(zip(keys, (int(v) for v in info)))
+        if self.dim == 2:
+            d.pop("ez")
+        return d
 
-    def schur_solve(self, s_x, s_y, phi, ybar, yc=None, tol=1e-10, max_iter=2000, threads=1, augment=False):
+    def partition_sizes(self, s_x, s_y, s_z=1):
+        """Per subdomain (n_r, n_i, n_b, n_c, jump entries)."""
+        ns = s_x * s_y * s_z
+        out = np.zeros((ns, 5), dtype=np.int32)
+        _check(lib().orc_partition_sizes(self._h, s_x, s_y, s_z, _ip(out)))
+        return out
+
+    def schur_solve(self, s_x, s_y, phi, ybar, yc=None, tol=1e-10, max_iter=2000, threads=1, augment=False, s_z=1):
         n = self.n
         ybar = np.ascontiguousarray(ybar, dtype=np.float64)
         ycp = None
@@ -180,8 +209,8 @@ class Problem:
         sp, sm = OracleStats(), OracleStats()
         leak = np.zeros(1)
         times = np.zeros(2)
-        _check(lib().orc_schur_solve(self._h, s_x, s_y, phi, _dp(ybar), ycp, tol, max_iter, threads, int(augment), _dp(y),
-                                     _dp(u), _dp(lam), C.byref(sp), C.byref(sm), _dp(leak), _dp(times)))
+        _check(lib().orc_schur_solve3(self._h, s_x, s_y, s_z, phi, _dp(ybar), ycp, tol, max_iter, threads, int(augment),
+                                      _dp(y), _dp(u), _dp(lam), C.byref(sp), C.byref(sm), _dp(leak), _dp(times)))
         return {"y": y, "u": u, "lambda": lam, "imag_leak": float(leak[0]), "plus_stats": sp.as_dict(),
                 "minus_stats": sm.as_dict(), "setup_seconds": float(times[0]), "solve_seconds": float(times[1]),
                 "converged": bool(sp.converged and sm.converged)}
@@ -192,12 +221,12 @@ class Feti:
     augmentation of the coarse space (feti.cpp:171-242, 394-454, 572-578)."""
 
     def __init__(self, problem: Problem, s_x, s_y, mass_coeff, stiffness_coeff=1.0, tol=1e-10, max_iter=1000,
-                 threads=1, augment=False):
+                 threads=1, augment=False, s_z=1):
         self.problem = problem
         mc, kc = complex(mass_coeff), complex(stiffness_coeff)
         h = C.c_void_p()
-        _check(lib().orc_feti_create(problem._h, s_x, s_y, kc.real, kc.imag, mc.real, mc.imag, tol, max_iter,
-                                     threads, int(augment), C.byref(h)))
+        _check(lib().orc_feti_create3(problem._h, s_x, s_y, s_z, kc.real, kc.imag, mc.real, mc.imag, tol, max_iter,
+                                      threads, int(augment), C.byref(h)))
         self._h = h
         self.n_lambda = lib().orc_feti_n_lambda(h)
         self.coarse_dim = lib().orc_feti_coarse_dim(h)
@@ -237,12 +266,12 @@ class Feti:
 class SchurPair:
     """Both reference factor solvers built once (control.cpp:303-304); run() = one Schur solve."""
 
-    def __init__(self, problem: Problem, s_x, s_y, phi, tol=1e-10, max_iter=2000, threads=1, augment=False):
+    def __init__(self, problem: Problem, s_x, s_y, phi, tol=1e-10, max_iter=2000, threads=1, augment=False, s_z=1):
         self.problem = problem
         h = C.c_void_p()
         t = np.zeros(1)
-        _check(lib().orc_schur_create(problem._h, s_x, s_y, phi, tol, max_iter, threads, int(augment), C.byref(h),
-                                      _dp(t)))
+        _check(lib().orc_schur_create3(problem._h, s_x, s_y, s_z, phi, tol, max_iter, threads, int(augment),
+                                       C.byref(h), _dp(t)))
         self._h = h
         self.setup_seconds = float(t[0])
 
