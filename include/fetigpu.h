@@ -202,6 +202,53 @@ double fetigpu_class_bytes(fetigpu_ctx* ctx, int klass);
 /* Thread-local message of the last failing call. */
 const char* fetigpu_last_error(void);
 
+/* ---- 3D extension (BASELINE.json configs 4-5) -----------------------------------------
+ * The reference is 2D only.  This is the same FETI-DP(H) range-space
+ * Schur solve on trilinear Q1 hexahedra: heat with whole-boundary Dirichlet, or linear
+ * elasticity (3 dofs/node interleaved) clamped on the face x = 0; corners = free subdomain-
+ * grid vertices; pairwise multipliers on multiplicity-4 subdomain edges with Dirichlet
+ * scaling W = 1/multiplicity (the natural extension of feti.cpp:34-169, 597-627).  Vector
+ * orders: free dofs ascending by mesh dof (x fastest, then y, then z; dof = dpn node + comp);
+ * multipliers ascending by (node, comp, pair).  Return codes / stats as above. */
+typedef struct fetigpu3d_ctx fetigpu3d_ctx;
+typedef struct {
+  int n_x, n_y, n_z;          /* elements per axis (cube elements) */
+  double len_x, len_y, len_z;
+  int physics;                /* 0 heat, 1 linear elasticity (E = young, nu = poisson) */
+  double young, poisson;
+  int s_x, s_y, s_z;          /* subdomain grid */
+  double phi;                 /* > 0: factor K + cV, c = -i/sqrt(phi) */
+  double mass_coeff_re;       /* phi == 0: c = mass_coeff (feti_solve only) */
+  double mass_coeff_im;
+  double tol;                 /* relative dual residual */
+  int max_iter;
+  int device;
+} fetigpu3d_desc;
+
+/* info[0..15] = n_free, n_constrained, subdomains, corner dofs, n_lambda, NI (padded), NB,
+ * NC, MR, block half-bandwidth P, dofs per node, ex, ey, ez, MAXE_BI, MAXE_IB (host only). */
+int fetigpu3d_problem_info(const fetigpu3d_desc* desc, long long* info16);
+/* Seeded sine-mode target ybar = sum_k a_k sin(l_k pi x) sin(m_k pi y) sin(n_k pi z). */
+int fetigpu3d_target_sine(const fetigpu3d_desc* desc, unsigned long long seed, int modes, int mmax, double* ybar);
+int fetigpu3d_create(const fetigpu3d_desc* desc, fetigpu3d_ctx** out);
+void fetigpu3d_destroy(fetigpu3d_ctx* ctx);
+int fetigpu3d_schur_solve(fetigpu3d_ctx* ctx, const double* ybar, const double* yc, double* y, double* u,
+                          double* lambda, fetigpu_schur_stats* stats);
+int fetigpu3d_schur_solve_device(fetigpu3d_ctx* ctx, const double* d_ybar, const double* d_yc, double* d_y,
+                                 double* d_u, double* d_lambda, fetigpu_schur_stats* stats);
+int fetigpu3d_feti_solve(fetigpu3d_ctx* ctx, int sign, const double* rhs_c128, double* x_c128,
+                         fetigpu_feti_stats* stats);
+int fetigpu3d_apply_dual(fetigpu3d_ctx* ctx, int sign, const double* lam_c128, double* out_c128);
+int fetigpu3d_apply_precond(fetigpu3d_ctx* ctx, int sign, const double* r_c128, double* out_c128);
+void* fetigpu3d_stream(fetigpu3d_ctx* ctx);
+long long fetigpu3d_launch_count(fetigpu3d_ctx* ctx, int reset);
+int fetigpu3d_profile(fetigpu3d_ctx* ctx, int enable);
+int fetigpu3d_profile_read(fetigpu3d_ctx* ctx, double* ms, long long* launches, int reset);
+/* Algorithmic bytes per launch of a kernel class; setup phase times (s): out8 = {assembly,
+ * A_ii factor, multi-RHS solves, S_bb build, S_bb inverse, coupling + coarse, pack, total}. */
+double fetigpu3d_class_bytes(fetigpu3d_ctx* ctx, int klass);
+int fetigpu3d_setup_times(fetigpu3d_ctx* ctx, double* out8);
+
 #ifdef __cplusplus
 }
 #endif

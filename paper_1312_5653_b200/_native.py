@@ -45,6 +45,18 @@ class SchurStats(C.Structure):
     ]
 
 
+class Desc3(C.Structure):
+    """fetigpu3d_desc (include/fetigpu.h, 3D extension)."""
+    _fields_ = [
+        ("n_x", C.c_int), ("n_y", C.c_int), ("n_z", C.c_int),
+        ("len_x", C.c_double), ("len_y", C.c_double), ("len_z", C.c_double),
+        ("physics", C.c_int), ("young", C.c_double), ("poisson", C.c_double),
+        ("s_x", C.c_int), ("s_y", C.c_int), ("s_z", C.c_int), ("phi", C.c_double),
+        ("mass_coeff_re", C.c_double), ("mass_coeff_im", C.c_double),
+        ("tol", C.c_double), ("max_iter", C.c_int), ("device", C.c_int),
+    ]
+
+
 _lib = None
 
 
@@ -87,6 +99,25 @@ def lib():
                                      C.POINTER(FetiStats), dp]
     L.fetigpu_class_bytes.argtypes = [vp, C.c_int]
     L.fetigpu_class_bytes.restype = C.c_double
+    pd3, lp = C.POINTER(Desc3), C.POINTER(C.c_longlong)
+    L.fetigpu3d_problem_info.argtypes = [pd3, lp]
+    L.fetigpu3d_target_sine.argtypes = [pd3, C.c_ulonglong, C.c_int, C.c_int, dp]
+    L.fetigpu3d_create.argtypes = [pd3, C.POINTER(vp)]
+    L.fetigpu3d_destroy.argtypes = [vp]
+    L.fetigpu3d_schur_solve.argtypes = [vp, dp, dp, dp, dp, dp, C.POINTER(SchurStats)]
+    L.fetigpu3d_schur_solve_device.argtypes = [vp, vp, vp, vp, vp, vp, C.POINTER(SchurStats)]
+    L.fetigpu3d_feti_solve.argtypes = [vp, C.c_int, dp, dp, C.POINTER(FetiStats)]
+    L.fetigpu3d_apply_dual.argtypes = [vp, C.c_int, dp, dp]
+    L.fetigpu3d_apply_precond.argtypes = [vp, C.c_int, dp, dp]
+    L.fetigpu3d_stream.argtypes = [vp]
+    L.fetigpu3d_stream.restype = vp
+    L.fetigpu3d_launch_count.argtypes = [vp, C.c_int]
+    L.fetigpu3d_launch_count.restype = C.c_longlong
+    L.fetigpu3d_profile.argtypes = [vp, C.c_int]
+    L.fetigpu3d_profile_read.argtypes = [vp, dp, C.POINTER(C.c_longlong), C.c_int]
+    L.fetigpu3d_class_bytes.argtypes = [vp, C.c_int]
+    L.fetigpu3d_class_bytes.restype = C.c_double
+    L.fetigpu3d_setup_times.argtypes = [vp, dp]
     _lib = L
     return L
 
@@ -98,4 +129,8 @@ EXPORTED_SYMBOLS = (
     "fetigpu_profile", "fetigpu_profile_read", "fetigpu_class_bytes", "fetigpu_last_error",
     "fetigpu_nccl_unique_id", "fetigpu_create_sharded", "fetigpu_rank_info", "fetigpu_emulated_schur_solve",
     "fetigpu_step_spans", "fetigpu_full_space", "fetigpu_pressure_load", "fetigpu_diagnostics",
+    "fetigpu3d_problem_info", "fetigpu3d_target_sine", "fetigpu3d_create", "fetigpu3d_destroy",
+    "fetigpu3d_schur_solve", "fetigpu3d_schur_solve_device", "fetigpu3d_feti_solve", "fetigpu3d_apply_dual",
+    "fetigpu3d_apply_precond", "fetigpu3d_stream", "fetigpu3d_launch_count", "fetigpu3d_profile",
+    "fetigpu3d_profile_read", "fetigpu3d_class_bytes", "fetigpu3d_setup_times",
 )

@@ -15,8 +15,9 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libfetigpu.so")
-SOURCES = ["host_core.cpp", "comm.cu", "fetigpu.cu"]
-HEADERS = ["host_core.hpp", "comm.hpp", "common.cuh", "band.cuh", "blockthomas.cuh", "kernels.cuh", "fullspace.hpp"]
+SOURCES = ["host_core.cpp", "host3d.cpp", "comm.cu", "fetigpu.cu", "fetigpu3d.cu"]
+HEADERS = ["host_core.hpp", "comm.hpp", "common.cuh", "band.cuh", "blockthomas.cuh", "kernels.cuh", "fullspace.hpp", "host3d.hpp",
+           "kernels3d.cuh"]
 
 
 def nvcc_path():

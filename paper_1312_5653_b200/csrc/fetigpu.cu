@@ -35,6 +35,7 @@ namespace fetigpu {
 
 using cd = std::complex<double>;
 static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
 
 #define CU(call)                                                                                   \
   do {                                                                                             \

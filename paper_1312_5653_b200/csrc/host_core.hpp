@@ -81,6 +81,9 @@ struct HostPartition {
   std::vector<int> sub_i0, sub_j0;
 };
 
+// thread-local message returned by fetigpu_last_error (fetigpu.cu)
+void set_last_error(const std::string& msg);
+
 HostProblem build_problem(const fetigpu_desc& d);
 HostPartition build_partition(const HostProblem& P, int sx, int sy, bool augment = false);
 

@@ -1,0 +1,1180 @@
+// kernels3d.cuh — sm_100a kernels of the 3D FETI-DP(H) path (fetigpu3d.cu).
+//
+// Per-subdomain operators (natural local order, SURVEY.md §8a a4 restated for hexahedra):
+//   A_ii  block-banded in 32x32 blocks: block (K, K-d), d = 0..P, at bb[s][K][d]; after the
+//         block LDL^T (k3_bb_factor) bb[s][K][0] = D_K^-1 and bb[s][K][d] = L_{K,K-d}
+//   A_bi / A_ib  ELL rows;  A_ic, A_bc, A_cc dense (<= 24 corner dofs per subdomain)
+//   S_bb = A_bb - A_bi A_ii^-1 A_ib and S_bb^-1, dense at setup (chunks of subdomains),
+//         then packed symmetric in 32x32 tiles for the per-iteration GEMVs
+// Every 32x32 tile is stored "diagonal-major": entry (r, c) at ((c - r) & 31) * 32 + r, so a
+// warp's load of one 512 B row of storage gives lane l the element (l, l + cc): the row
+// product sum_c T[l][c] x[c] and the transposed product (rotating shuffle carry) are both
+// coalesced.  Diagonal tiles of the symmetric packs keep only cc = 0..16 (17 x 32).
+#pragma once
+
+#include "common.cuh"
+
+namespace fetigpu {
+namespace k3 {
+
+__device__ __forceinline__ int tpos(int r, int c) { return (((c - r) & 31) << 5) | r; }
+
+// ---------------------------------------------------------------------------------------
+// Assembly (K1): one thread per (subdomain, local mesh dof) row; the row owner adds every
+// element contribution of its row into the block it belongs to (deterministic, no atomics).
+struct Asm3 {
+  int S, nld, ex, ey, ez, dpn, ed;
+  int NI, NB, NC, P, EBI, EIB;
+  const int* ldof;        // [S][nld]
+  const double2* ae;      // [ed][ed] element matrix K_e + c M_e
+  double2* bb;            // [S][NI/32][P+1][1024]
+  int* bi_idx;            // [S][NB][EBI]
+  double2* bi_val;
+  int* ib_idx;            // [S][NI][EIB]
+  double2* ib_val;
+  double2* aic;           // [S][NI][NC]
+  double2* abc;           // [S][NB][NC]
+  double2* acc;           // [S][NC][NC]
+  // mode 1: only A_bb of subdomains [s0, s0 + cnt) into dense [s - s0][NBP][NBP]
+  int mode, s0, cnt, NBP;
+  double2* dense;
+};
+
+__device__ __forceinline__ void ell_add(int* idx, double2* val, int width, int key, double2 v) {
+  for (int e = 0; e < width; ++e) {
+    const int k = idx[e];
+    if (k == key) {
+      val[e] = cadd(val[e], v);
+      return;
+    }
+    if (k < 0) {
+      idx[e] = key;
+      val[e] = v;
+      return;
+    }
+  }
+}
+
+__global__ void k3_assemble(Asm3 a) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nsub = a.mode == 0 ? a.S : a.cnt;
+  if (gid >= (long long)nsub * a.nld) return;
+  const int s = (a.mode == 0 ? 0 : a.s0) + (int)(gid / a.nld);
+  const int l = (int)(gid % a.nld);
+  const int* ld = a.ldof + (size_t)s * a.nld;
+  const int code = ld[l], cat = code >> 24, row = code & 0xFFFFFF;
+  if (cat == 0) return;
+  if (a.mode == 1 && cat != 3) return;
+  const int dpn = a.dpn, lx = a.ex + 1, ly = a.ey + 1;
+  const int c = l % dpn, node = l / dpn;
+  const int li = node % lx, lj = (node / lx) % ly, lk = node / (lx * ly);
+  const int hx[8] = {0, 1, 1, 0, 0, 1, 1, 0}, hy[8] = {0, 0, 1, 1, 0, 0, 1, 1};
+  for (int ek = max(lk - 1, 0); ek <= min(lk, a.ez - 1); ++ek)
+    for (int ej = max(lj - 1, 0); ej <= min(lj, a.ey - 1); ++ej)
+      for (int ei = max(li - 1, 0); ei <= min(li, a.ex - 1); ++ei) {
+        const int dx = li - ei, dy = lj - ej, dz = lk - ek;
+        const int an = dz * 4 + (dy == 0 ? dx : 3 - dx);  // local node of this dof in the element
+        for (int b = 0; b < 8; ++b) {
+          const int nb = ((ek + (b >> 2)) * ly + (ej + hy[b])) * lx + (ei + hx[b]);
+          for (int c2 = 0; c2 < dpn; ++c2) {
+            const int code2 = ld[nb * dpn + c2], cat2 = code2 >> 24, col = code2 & 0xFFFFFF;
+            if (cat2 == 0) continue;
+            const double2 v = a.ae[(an * dpn + c) * a.ed + b * dpn + c2];
+            if (a.mode == 1) {
+              if (cat2 == 3) {
+                double2* d = a.dense + ((size_t)(s - a.s0) * a.NBP + row) * a.NBP + col;
+                *d = cadd(*d, v);
+              }
+              continue;
+            }
+            if (cat == 1) {  // corner row
+              if (cat2 == 1) {
+                double2* d = a.acc + ((size_t)s * a.NC + row) * a.NC + col;
+                *d = cadd(*d, v);
+              }
+            } else if (cat == 2) {  // interior row
+              if (cat2 == 2) {
+                const int K = row >> 5, d = K - (col >> 5);
+                if (d >= 0 && d <= a.P) {
+                  double2* t = a.bb + (((size_t)s * (a.NI >> 5) + K) * (a.P + 1) + d) * 1024 + tpos(row & 31, col & 31);
+                  *t = cadd(*t, v);
+                }
+              } else if (cat2 == 3) {
+                const size_t r0 = ((size_t)s * a.NI + row) * a.EIB;
+                ell_add(a.ib_idx + r0, a.ib_val + r0, a.EIB, col, v);
+              } else {
+                double2* d = a.aic + ((size_t)s * a.NI + row) * a.NC + col;
+                *d = cadd(*d, v);
+              }
+            } else {  // interface row
+              if (cat2 == 2) {
+                const size_t r0 = ((size_t)s * a.NB + row) * a.EBI;
+                ell_add(a.bi_idx + r0, a.bi_val + r0, a.EBI, col, v);
+              } else if (cat2 == 1) {
+                double2* d = a.abc + ((size_t)s * a.NB + row) * a.NC + col;
+                *d = cadd(*d, v);
+              }
+            }
+          }
+        }
+      }
+}
+
+// identity on the padded interior rows (n_i <= i < NI) so every block row is regular
+__global__ void k3_pad_identity(int S, int NI, int P, const int* __restrict__ n_i, double2* bb) {
+  const int s = blockIdx.x;
+  for (int i = n_i[s] + threadIdx.x; i < NI; i += blockDim.x)
+    bb[(((size_t)s * (NI >> 5) + (i >> 5)) * (P + 1)) * 1024 + tpos(i & 31, i & 31)] = make_double2(1.0, 0.0);
+}
+
+// ---------------------------------------------------------------------------------------
+// 32x32 complex block helpers for 256-thread CTAs.  Shared tiles are row-major [32][33].
+typedef double2 Tile[32][33];
+
+__device__ __forceinline__ void tile_load(Tile& t, const double2* __restrict__ g) {  // g in tpos layout
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+    const int cc = e >> 5, r = e & 31;
+    t[r][(r + cc) & 31] = g[e];
+  }
+}
+__device__ __forceinline__ void tile_store(double2* __restrict__ g, const Tile& t) {
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+    const int cc = e >> 5, r = e & 31;
+    g[e] = t[r][(r + cc) & 31];
+  }
+}
+// dense row-major block (leading dimension ld) <-> shared tile
+__device__ __forceinline__ void tile_load_rm(Tile& t, const double2* __restrict__ g, size_t ld) {
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) t[e >> 5][e & 31] = g[(size_t)(e >> 5) * ld + (e & 31)];
+}
+__device__ __forceinline__ void tile_store_rm(double2* __restrict__ g, size_t ld, const Tile& t) {
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) g[(size_t)(e >> 5) * ld + (e & 31)] = t[e >> 5][e & 31];
+}
+// acc[q] (rows r, cols c0..c0+3 of the owning thread) of A B (TB = false) or A B^T (TB = true)
+template <bool TB>
+__device__ __forceinline__ void tile_mma(const Tile& A, const Tile& B, double2 acc[4]) {
+  const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {
+    const double2 a = A[r][k];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = cfma(a, TB ? B[c0 + q][k] : B[k][c0 + q], acc[q]);
+  }
+}
+// in-place inverse of a shared 32x32 tile by Gauss-Jordan without pivoting (complex
+// symmetric with positive definite real part: every leading pivot is nonzero); returns the
+// smallest |pivot| relative to the largest in *pivrat (thread 0)
+__device__ void tile_invert(Tile& t, double* pivrat) {
+  __shared__ double2 prow[32], pcol[32];
+  __shared__ double pmin, pmax;
+  if (threadIdx.x == 0) pmin = 1e300, pmax = 0.0;
+  __syncthreads();
+  for (int p = 0; p < 32; ++p) {
+    const double2 piv = t[p][p];
+    const double2 pinv = crecip(piv);
+    if (threadIdx.x < 32) {
+      const int c = threadIdx.x;
+      prow[c] = c == p ? pinv : cmul(t[p][c], pinv);
+      pcol[c] = c == p ? cz() : t[c][p];
+    }
+    if (threadIdx.x == 0) {
+      const double a = sqrt(cabs2(piv));
+      pmin = fmin(pmin, a);
+      pmax = fmax(pmax, a);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+      const int r = e >> 5, c = e & 31;
+      if (r == p) {
+        t[r][c] = prow[c];
+      } else {
+        const double2 base = c == p ? cz() : t[r][c];
+        t[r][c] = cfms(pcol[r], prow[c], base);
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *pivrat = pmax > 0.0 ? pmin / pmax : 0.0;
+}
+
+// ---------------------------------------------------------------------------------------
+// K2: block LDL^T of A_ii (right-looking, one CTA of 256 threads per subdomain).  For each
+// block column K: D_K^-1 (in-tile Gauss-Jordan), L_IK = Abar_IK D_K^-1, trailing update
+// A_IJ -= Abar_IK L_JK^T (K < J <= I <= K+P), then L replaces Abar.  Scratch: [S][P][1024].
+__global__ void __launch_bounds__(256) k3_bb_factor(int NBK, int P, double2* __restrict__ bb,
+                                                    double2* __restrict__ scratch, int* __restrict__ status) {
+  extern __shared__ __align__(16) unsigned char k3f_raw[];
+  Tile& A = *reinterpret_cast<Tile*>(k3f_raw);
+  Tile& B = *reinterpret_cast<Tile*>(k3f_raw + sizeof(Tile));
+  const int s = blockIdx.x;
+  double2* band = bb + (size_t)s * NBK * (P + 1) * 1024;
+  double2* Lc = scratch + (size_t)s * P * 1024;
+  __shared__ double rat;
+  double worst = 1.0;
+  for (int K = 0; K < NBK; ++K) {
+    double2* blkKK = band + ((size_t)K * (P + 1)) * 1024;
+    tile_load(A, blkKK);
+    __syncthreads();
+    tile_invert(A, &rat);
+    __syncthreads();
+    worst = fmin(worst, rat);
+    tile_store(blkKK, A);  // D_K^-1
+    const int nd = min(P, NBK - 1 - K);
+    // L_dI = Abar_dI D^-1
+    for (int dI = 1; dI <= nd; ++dI) {
+      __syncthreads();
+      tile_load(B, band + ((size_t)(K + dI) * (P + 1) + dI) * 1024);
+      __syncthreads();
+      double2 acc[4] = {cz(), cz(), cz(), cz()};
+      tile_mma<false>(B, A, acc);
+      const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Lc[(size_t)(dI - 1) * 1024 + tpos(r, c0 + q)] = acc[q];
+    }
+    __syncthreads();
+    // trailing update: block (K+dI, K+dJ) -= Abar_dI L_dJ^T
+    for (int dI = 1; dI <= nd; ++dI) {
+      __syncthreads();
+      tile_load(A, band + ((size_t)(K + dI) * (P + 1) + dI) * 1024);  // Abar (still unscaled)
+      for (int dJ = 1; dJ <= dI; ++dJ) {
+        __syncthreads();
+        tile_load(B, Lc + (size_t)(dJ - 1) * 1024);
+        __syncthreads();
+        double2 acc[4] = {cz(), cz(), cz(), cz()};
+        tile_mma<true>(A, B, acc);
+        double2* tgt = band + ((size_t)(K + dI) * (P + 1) + (dI - dJ)) * 1024;
+        const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int p = tpos(r, c0 + q);
+          tgt[p] = csub(tgt[p], acc[q]);
+        }
+      }
+    }
+    __syncthreads();
+    for (int dI = 1; dI <= nd; ++dI)
+      for (int e = threadIdx.x; e < 1024; e += blockDim.x)
+        band[((size_t)(K + dI) * (P + 1) + dI) * 1024 + e] = Lc[(size_t)(dI - 1) * 1024 + e];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) status[s] = (worst > 1e-14) ? 0 : 1;
+}
+
+// ---------------------------------------------------------------------------------------
+// Per-solve interior substitution x = A_ii^-1 x, one CTA (8 warps) per subdomain (K5).
+// Forward y_K = b_K - sum_d L_{K,K-d} y_{K-d}; diagonal z_K = D_K^-1 y_K; backward
+// x_K = z_K - sum_d L_{K+d,K}^T x_{K+d}.  Warp w takes the blocks d = w+1, w+9, ...; the
+// other warps' partials are summed in a fixed order (deterministic).
+template <int RING>
+__global__ void __launch_bounds__(256) k3_bb_solve1(int NBK, int P, const double2* __restrict__ bb, int NI,
+                                                    double2* __restrict__ X) {
+  __shared__ double2 ring[RING][32];
+  __shared__ double2 part[8][32];
+  const int s = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double2* band = bb + (size_t)s * NBK * (P + 1) * 1024;
+  double2* x = X + (size_t)s * NI;
+  // forward + diagonal (z_K is written over b_K; the ring keeps the forward values y)
+  for (int K = 0; K < NBK; ++K) {
+    double2 acc = cz();
+    for (int d = warp + 1; d <= P; d += 8) {
+      if (K - d < 0) break;
+      const double2* T = band + ((size_t)K * (P + 1) + d) * 1024;
+      const double2* y = ring[(K - d) % RING];
+#pragma unroll 8
+      for (int cc = 0; cc < 32; ++cc) acc = cfma(__ldg(T + cc * 32 + lane), y[(lane + cc) & 31], acc);
+    }
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+      double2 v = x[(size_t)K * 32 + lane];
+      for (int w = 0; w < 8; ++w) v = csub(v, part[w][lane]);
+      ring[K % RING][lane] = v;
+    }
+    __syncthreads();
+    if (warp == 1) {  // z_K = D_K^-1 y_K
+      const double2* D = band + ((size_t)K * (P + 1)) * 1024;
+      const double2* y = ring[K % RING];
+      double2 z = cz();
+#pragma unroll 8
+      for (int cc = 0; cc < 32; ++cc) z = cfma(__ldg(D + cc * 32 + lane), y[(lane + cc) & 31], z);
+      x[(size_t)K * 32 + lane] = z;
+    }
+  }
+  __syncthreads();
+  // backward
+  for (int K = NBK - 1; K >= 0; --K) {
+    double2 acc = cz();
+    for (int d = warp + 1; d <= P; d += 8) {
+      if (K + d >= NBK) break;
+      const double2* T = band + ((size_t)(K + d) * (P + 1) + d) * 1024;
+      const double2 xr = ring[(K + d) % RING][lane];
+      double2 yc = cz();
+#pragma unroll 8
+      for (int cc = 0; cc < 32; ++cc) {
+        yc = cfma(__ldg(T + cc * 32 + lane), xr, yc);
+        yc = shfl2(yc, (lane + 1) & 31);
+      }
+      acc = cadd(acc, yc);
+    }
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+      double2 v = x[(size_t)K * 32 + lane];
+      for (int w = 0; w < 8; ++w) v = csub(v, part[w][lane]);
+      ring[K % RING][lane] = v;
+      x[(size_t)K * 32 + lane] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Setup multi-RHS substitution (K3): Y = A_ii^-1 Y for tiles of 32 right-hand sides
+// ([sub][tile][NI][32]); CTA = (column group, tile, subdomain), each warp owns 4 columns and
+// keeps its columns of the last P+1 blocks in a shared ring (warp-private: no CTA barriers).
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k3_bb_msolve(int NBK, int P, const double2* __restrict__ bb,
+                                                           int NI, int ntile, int s0, double2* __restrict__ Y) {
+  constexpr int CPB = 4 * WARPS;
+  extern __shared__ __align__(16) double2 k3m_ring[];  // [P+1][32][CPB]
+  const int RING = P + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cg = blockIdx.x, tile = blockIdx.y, sc = blockIdx.z, s = s0 + sc;
+  const double2* band = bb + (size_t)s * NBK * (P + 1) * 1024;
+  double2* y = Y + ((size_t)sc * ntile + tile) * NI * 32 + cg * CPB + warp * 4;
+  double2* rg = k3m_ring + warp * 4;
+  auto R = [&](int blk, int row) -> double2* { return rg + ((size_t)(blk % RING) * 32 + row) * CPB; };
+  for (int K = 0; K < NBK; ++K) {
+    double2 acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = y[(size_t)(K * 32 + lane) * 32 + q];
+    for (int d = 1; d <= P && K - d >= 0; ++d) {
+      const double2* T = band + ((size_t)K * (P + 1) + d) * 1024;
+#pragma unroll 4
+      for (int cc = 0; cc < 32; ++cc) {
+        const double2 t = __ldg(T + cc * 32 + lane);
+        const double2* yr = R(K - d, (lane + cc) & 31);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] = cfms(t, yr[q], acc[q]);
+      }
+    }
+    double2* w = R(K, lane);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) w[q] = acc[q];
+    __syncwarp();
+    const double2* D = band + ((size_t)K * (P + 1)) * 1024;
+    double2 z[4] = {cz(), cz(), cz(), cz()};
+#pragma unroll 4
+    for (int cc = 0; cc < 32; ++cc) {
+      const double2 t = __ldg(D + cc * 32 + lane);
+      const double2* yr = R(K, (lane + cc) & 31);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) z[q] = cfma(t, yr[q], z[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) y[(size_t)(K * 32 + lane) * 32 + q] = z[q];
+    __syncwarp();
+  }
+  for (int K = NBK - 1; K >= 0; --K) {
+    double2 acc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = y[(size_t)(K * 32 + lane) * 32 + q];
+    for (int d = 1; d <= P && K + d < NBK; ++d) {
+      const double2* T = band + ((size_t)(K + d) * (P + 1) + d) * 1024;
+      const double2* xr = R(K + d, lane);
+      double2 xv[4], yc[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) xv[q] = xr[q], yc[q] = cz();
+#pragma unroll 4
+      for (int cc = 0; cc < 32; ++cc) {
+        const double2 t = __ldg(T + cc * 32 + lane);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          yc[q] = cfma(t, xv[q], yc[q]);
+          yc[q] = shfl2(yc[q], (lane + 1) & 31);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] = csub(acc[q], yc[q]);
+    }
+    __syncwarp();
+    double2* w = R(K, lane);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      w[q] = acc[q];
+      y[(size_t)(K * 32 + lane) * 32 + q] = acc[q];
+    }
+    __syncwarp();
+  }
+}
+
+// RHS tiles of the setup solves: tile T < NTB holds columns 32T.. of A_ib (column k = the
+// interior entries of interface dof k), tile NTB holds A_ic.
+__global__ void k3_build_rhs(int cnt, int s0, int NI, int NB, int NC, int EBI, int ntile, int NTB,
+                             const int* __restrict__ bi_idx, const double2* __restrict__ bi_val,
+                             const double2* __restrict__ aic, double2* __restrict__ Y) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per = (long long)NTB * 32 + 32;  // columns per subdomain
+  if (gid >= (long long)cnt * per) return;
+  const int sc = (int)(gid / per), col = (int)(gid % per), s = s0 + sc;
+  const int tile = col >> 5, c = col & 31;
+  double2* y = Y + ((size_t)sc * ntile + tile) * NI * 32 + c;
+  if (tile < NTB) {
+    const int k = col;
+    if (k >= NB) return;
+    for (int e = 0; e < EBI; ++e) {
+      const int i = bi_idx[((size_t)s * NB + k) * EBI + e];
+      if (i >= 0) y[(size_t)i * 32] = bi_val[((size_t)s * NB + k) * EBI + e];  // A_ib(i,k) = A_bi(k,i)
+    }
+  } else if (c < NC) {
+    for (int i = 0; i < NI; ++i) y[(size_t)i * 32] = aic[((size_t)s * NI + i) * NC + c];
+  }
+}
+
+// S_bb = A_bb - A_bi X in the dense chunk buffer (A_bb assembled there by k3_assemble mode 1);
+// padding: identity rows/columns beyond n_b
+__global__ void k3_schur_build(int cnt, int s0, int NI, int NB, int NBP, int EBI, int ntile,
+                               const int* __restrict__ n_b, const int* __restrict__ bi_idx,
+                               const double2* __restrict__ bi_val, const double2* __restrict__ X,
+                               double2* __restrict__ dense) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)cnt * NBP * NBP) return;
+  const int sc = (int)(gid / ((long long)NBP * NBP));
+  const int r = (int)((gid / NBP) % NBP), c = (int)(gid % NBP), s = s0 + sc;
+  const int nb = n_b[s];
+  double2* d = dense + gid;
+  if (r >= nb || c >= nb) {
+    *d = (r == c) ? make_double2(1.0, 0.0) : cz();
+    return;
+  }
+  double2 v = *d;
+  const double2* x = X + ((size_t)sc * ntile + (c >> 5)) * NI * 32 + (c & 31);
+  for (int e = 0; e < EBI; ++e) {
+    const int i = bi_idx[((size_t)s * NB + r) * EBI + e];
+    if (i >= 0) v = cfms(bi_val[((size_t)s * NB + r) * EBI + e], x[(size_t)i * 32], v);
+  }
+  *d = v;
+}
+
+// ---------------------------------------------------------------------------------------
+// Blocked Gauss-Jordan inverse of the dense S_bb chunk (no pivoting, see tile_invert),
+// NT x NT blocks of 32.  Step K: (1) P = A_KK^-1; (2) row panel A_KJ <- P A_KJ and saved
+// column panel C_I = A_IK; (3) A_IJ -= C_I A_KJ, A_IK = -C_I P.
+__global__ void __launch_bounds__(256) k3_gj_pivot(int NBP, int K, double2* __restrict__ dense,
+                                                   double2* __restrict__ pbuf, double* __restrict__ prat) {
+  __shared__ Tile A;
+  __shared__ double rat;
+  const int sc = blockIdx.x;
+  double2* M = dense + (size_t)sc * NBP * NBP;
+  tile_load_rm(A, M + (size_t)(K * 32) * NBP + K * 32, NBP);
+  __syncthreads();
+  tile_invert(A, &rat);
+  __syncthreads();
+  tile_store_rm(pbuf + (size_t)sc * 1024, 32, A);
+  if (threadIdx.x == 0) prat[sc] = fmin(prat[sc], rat);
+}
+__global__ void __launch_bounds__(256) k3_gj_panel(int NBP, int NT, int K, double2* __restrict__ dense,
+                                                   const double2* __restrict__ pbuf, double2* __restrict__ cbuf) {
+  __shared__ Tile A, B;
+  const int J = blockIdx.x, sc = blockIdx.y;
+  double2* M = dense + (size_t)sc * NBP * NBP;
+  // save the old column block (J, K)
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x)
+    cbuf[((size_t)sc * NT + J) * 1024 + e] = M[(size_t)(J * 32 + (e >> 5)) * NBP + K * 32 + (e & 31)];
+  if (J == K) return;
+  tile_load_rm(A, pbuf + (size_t)sc * 1024, 32);
+  tile_load_rm(B, M + (size_t)(K * 32) * NBP + J * 32, NBP);
+  __syncthreads();
+  double2 acc[4] = {cz(), cz(), cz(), cz()};
+  tile_mma<false>(A, B, acc);
+  const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) M[(size_t)(K * 32 + r) * NBP + J * 32 + c0 + q] = acc[q];
+}
+__global__ void __launch_bounds__(256) k3_gj_update(int NBP, int NT, int K, double2* __restrict__ dense,
+                                                    const double2* __restrict__ pbuf, const double2* __restrict__ cbuf) {
+  __shared__ Tile A, B;
+  const int J = blockIdx.x, I = blockIdx.y, sc = blockIdx.z;
+  double2* M = dense + (size_t)sc * NBP * NBP;
+  const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
+  if (I == K) {
+    if (J == K) {  // the pivot block itself becomes P
+      for (int e = threadIdx.x; e < 1024; e += blockDim.x)
+        M[(size_t)(K * 32 + (e >> 5)) * NBP + K * 32 + (e & 31)] = pbuf[(size_t)sc * 1024 + e];
+    }
+    return;
+  }
+  tile_load_rm(A, cbuf + ((size_t)sc * NT + I) * 1024, 32);
+  if (J == K) tile_load_rm(B, pbuf + (size_t)sc * 1024, 32);
+  else tile_load_rm(B, M + (size_t)(K * 32) * NBP + J * 32, NBP);
+  __syncthreads();
+  double2 acc[4] = {cz(), cz(), cz(), cz()};
+  tile_mma<false>(A, B, acc);
+  double2* out = M + (size_t)(I * 32 + r) * NBP + J * 32 + c0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) out[q] = (J == K) ? make_double2(-acc[q].x, -acc[q].y) : csub(out[q], acc[q]);
+}
+
+// ---------------------------------------------------------------------------------------
+// Packed symmetric storage of a dense chunk (subdomain s = s0 + sc, NT_s tiles):
+// row I = [off-diagonal tiles J < I (1024 each) | diagonal tile (17 x 32)]
+__device__ __forceinline__ long long sym_row_off(int I) { return 1024LL * I * (I - 1) / 2 + 544LL * I; }
+__device__ __forceinline__ long long sym_size(int NT) { return sym_row_off(NT); }
+
+__global__ void k3_pack_sym(int cnt, int s0, int NBP, const int* __restrict__ nt, const long long* __restrict__ off,
+                            const double2* __restrict__ dense, double2* __restrict__ pack) {
+  const int sc = blockIdx.y, s = s0 + sc;
+  const long long sz = sym_size(nt[s]);
+  const double2* M = dense + (size_t)sc * NBP * NBP;
+  double2* out = pack + off[s];
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < sz; e += (long long)gridDim.x * blockDim.x) {
+    // row I: largest I with sym_row_off(I) <= e
+    int I = (int)sqrt((double)e / 512.0);
+    while (I > 0 && sym_row_off(I) > e) --I;
+    while (sym_row_off(I + 1) <= e) ++I;
+    const long long w = e - sym_row_off(I);
+    int r, c;
+    if (w < 1024LL * I) {
+      const int J = (int)(w >> 10), q = (int)(w & 1023);
+      r = 32 * I + (q & 31);
+      c = 32 * J + (((q >> 5) + (q & 31)) & 31);
+    } else {
+      const int q = (int)(w - 1024LL * I);
+      r = 32 * I + (q & 31);
+      c = 32 * I + (((q >> 5) + (q & 31)) & 31);
+    }
+    out[e] = M[(size_t)r * NBP + c];
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Per-iteration packed symmetric GEMV y = S x (K5/K6), one CTA (4 warps) per tile row
+// (s, I): y_I (rows) is complete in the CTA; the transposed contributions of the
+// off-diagonal tiles go to colpart[s][t = I(I-1)/2 + J] and k3_sym_reduce adds them.
+struct SymArgs {
+  const int2* work;          // (s, I) per CTA
+  const int* nt;             // tiles per subdomain
+  const long long* off;      // packed offset per subdomain
+  const long long* coff;     // column-partial offset per subdomain (units of 32 entries)
+  const double2* pack;
+  const double2* xin;        // [S][NB]
+  int NB;
+  double2* rowsum;           // [S][NB]
+  double2* colpart;          // [sum_s NT_s (NT_s - 1) / 2][32]
+};
+template <int BATCH>
+__global__ void __launch_bounds__(128) k3_sym_rows(SymArgs a) {
+  extern __shared__ double2 k3s_x[];  // x_0 .. x_I (32 (I + 1))
+  __shared__ double2 red[4][32];
+  const int2 wk = a.work[blockIdx.x];
+  const int s = wk.x, I = wk.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double2* x = a.xin + (size_t)s * a.NB;
+  for (int k = threadIdx.x; k < 32 * (I + 1); k += blockDim.x) k3s_x[k] = k < a.NB ? x[k] : cz();
+  __syncthreads();
+  const double2* row = a.pack + a.off[s] + sym_row_off(I);
+  double2* cp = a.colpart + (a.coff[s] + (long long)I * (I - 1) / 2) * 32;
+  const double2 xi = k3s_x[32 * I + lane];
+  double2 yr = cz();
+  for (int J = warp; J < I; J += 4) {
+    const double2* T = row + (size_t)J * 1024;
+    double2 yc = cz();
+#pragma unroll
+    for (int cb = 0; cb < 32; cb += BATCH) {
+      double2 m[BATCH];
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) m[u] = __ldcs(T + (cb + u) * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) {
+        yr = cfma(m[u], k3s_x[32 * J + ((lane + cb + u) & 31)], yr);
+        yc = cfma(m[u], xi, yc);
+        yc = shfl2(yc, (lane + 1) & 31);
+      }
+    }
+    cp[(size_t)J * 32 + lane] = yc;
+  }
+  if (warp == (I & 3)) {  // diagonal tile: cc = 0 diagonal, 1..15 both halves, 16 both (l, l+16)
+    const double2* D = row + (size_t)I * 1024;
+    double2 yc = cz();
+#pragma unroll
+    for (int cb = 0; cb < 16; cb += BATCH) {
+      double2 m[BATCH];
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) m[u] = __ldcs(D + (cb + u) * 32 + lane);
+#pragma unroll
+      for (int u = 0; u < BATCH; ++u) {
+        const int c = cb + u;
+        if (c == 0) {
+          yr = cfma(m[u], xi, yr);
+        } else {
+          yr = cfma(m[u], k3s_x[32 * I + ((lane + c) & 31)], yr);
+          yc = shfl2(yc, (lane + 1) & 31);
+          yc = cfma(m[u], xi, yc);
+        }
+      }
+    }
+    const double2 m16 = __ldcs(D + 16 * 32 + lane);
+    yr = cfma(m16, k3s_x[32 * I + ((lane + 16) & 31)], yr);
+    yc = shfl2(yc, (lane + 17) & 31);
+    yr = cadd(yr, yc);
+  }
+  red[warp][lane] = yr;
+  __syncthreads();
+  if (warp == 0) {
+    const double2 v = cadd(cadd(red[0][lane], red[1][lane]), cadd(red[2][lane], red[3][lane]));
+    const int k = 32 * I + lane;
+    if (k < a.NB) a.rowsum[(size_t)s * a.NB + k] = v;
+  }
+}
+// y[s][32J + l] = rowsum + sum_{I > J} colpart[s][I(I-1)/2 + J][l]   (one warp per (s, J))
+__global__ void k3_sym_reduce(int nwork, const int2* __restrict__ work, const int* __restrict__ nt,
+                              const long long* __restrict__ coff, int NB, const double2* __restrict__ rowsum,
+                              const double2* __restrict__ colpart, double2* __restrict__ y) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= nwork) return;
+  const int2 wk = work[w];
+  const int s = wk.x, J = wk.y, k = 32 * J + lane;
+  if (k >= NB) return;
+  double2 v = rowsum[(size_t)s * NB + k];
+  const double2* cp = colpart + coff[s] * 32;
+  for (int I = J + 1; I < nt[s]; ++I) v = cadd(v, cp[((size_t)I * (I - 1) / 2 + J) * 32 + lane]);
+  y[(size_t)s * NB + k] = v;
+}
+
+// ---------------------------------------------------------------------------------------
+// Jump operators (K5/K6): B^T gathers onto interface slots and B gathers onto multipliers.
+// mode 0: xin = alpha sum_e sign_e w_row lam[row]   (Dirichlet: alpha = 1, weights W)
+// mode 1: xin = -sum_e sign_e lam[row]               (dual operator input t_b = -B^T lam)
+// mode 2: xin = fb - sum_e sign_e lam[row]           (t_b = f_b - B^T lam, final eliminate)
+__global__ void k3_gather_in(int S, int NB, int MR, int mode, const int* __restrict__ n_b,
+                             const int* __restrict__ brow, const double* __restrict__ bsgn,
+                             const double* __restrict__ lam_w, const double2* __restrict__ lam,
+                             const double2* __restrict__ fb, double2* __restrict__ xin) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)S * NB) return;
+  const int s = (int)(gid / NB), k = (int)(gid % NB);
+  double2 v = mode == 2 ? fb[gid] : cz();
+  if (k < n_b[s]) {
+    for (int e = 0; e < MR; ++e) {
+      const int r = brow[gid * MR + e];
+      if (r < 0) break;
+      const double sg = bsgn[gid * MR + e];
+      if (mode == 0) v = cadd(v, cscale(lam[r], sg * lam_w[r]));
+      else v = csub(v, cscale(lam[r], sg));
+    }
+  }
+  xin[gid] = v;
+}
+// Dirichlet output: out[row] = w_row (wb[lo] - wb[hi])
+__global__ void k3_lam_pre(int nl, const int* __restrict__ lo, const int* __restrict__ hi,
+                           const double* __restrict__ lam_w, const double2* __restrict__ wb, double2* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nl) return;
+  out[r] = cscale(csub(wb[lo[r]], wb[hi[r]]), lam_w[r]);
+}
+// jump of u_b = u1_b - cpl_b z: out[row] = sign (u_b[lo] - u_b[hi])  (sign -1: F lam)
+__global__ void k3_lam_jump(int nl, int NB, int NC, double sign, const int* __restrict__ lo, const int* __restrict__ hi,
+                            const double2* __restrict__ u1, const double2* __restrict__ cpl_b,
+                            const int* __restrict__ cglob, const double2* __restrict__ z, double2* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nl) return;
+  double2 u[2];
+  const int sl[2] = {lo[r], hi[r]};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int slot = sl[q], s = slot / NB;
+    double2 v = u1[slot];
+    if (z != nullptr)
+      for (int c = 0; c < NC; ++c) {
+        const int g = cglob[(size_t)s * NC + c];
+        if (g >= 0) v = cfms(cpl_b[(size_t)slot * NC + c], z[g], v);
+      }
+    u[q] = v;
+  }
+  out[r] = cscale(csub(u[0], u[1]), sign);
+}
+// u_b = u1_b - cpl_b z (in place)
+__global__ void k3_ub_correct(int S, int NB, int NC, const int* __restrict__ cglob, const double2* __restrict__ z,
+                              const double2* __restrict__ cpl_b, double2* __restrict__ u) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)S * NB) return;
+  const int s = (int)(gid / NB);
+  double2 v = u[gid];
+  for (int c = 0; c < NC; ++c) {
+    const int g = cglob[(size_t)s * NC + c];
+    if (g >= 0) v = cfms(cpl_b[gid * NC + c], z[g], v);
+  }
+  u[gid] = v;
+}
+
+// ---------------------------------------------------------------------------------------
+// Coarse problem (K4).  gcp[s][c] = cpl_b^T xin (+ cpl_i^T fi): one CTA per subdomain,
+// one warp per local corner dof; g = fc - sum_slots gcp; z = C^-1 g (dense, row per warp).
+__global__ void k3_gcp(int NB, int NC, int NI, const double2* __restrict__ cpl_b, const double2* __restrict__ xin,
+                       const double2* __restrict__ cpl_i, const double2* __restrict__ fi, double2* __restrict__ gcp) {
+  const int s = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = warp; c < NC; c += nw) {
+    double2 acc = cz();
+    for (int k = lane; k < NB; k += 32)
+      acc = cfma(cpl_b[((size_t)s * NB + k) * NC + c], xin[(size_t)s * NB + k], acc);
+    if (cpl_i != nullptr)
+      for (int i = lane; i < NI; i += 32)
+        acc = cfma(cpl_i[((size_t)s * NI + i) * NC + c], fi[(size_t)s * NI + i], acc);
+    acc = warp_sum2(acc);
+    if (lane == 0) gcp[(size_t)s * NC + c] = acc;
+  }
+}
+__global__ void k3_coarse_rhs(int nc, const int* __restrict__ slots, const double2* __restrict__ gcp,
+                              const double2* __restrict__ fc, double2* __restrict__ g) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  double2 acc = fc ? fc[c] : cz();
+  for (int q = 0; q < 8; ++q) {
+    const int sl = slots[c * 8 + q];
+    if (sl >= 0) acc = csub(acc, gcp[sl]);
+  }
+  g[c] = acc;
+}
+__global__ void k3_dense_gemv(int n, const double2* __restrict__ A, const double2* __restrict__ x,
+                              double2* __restrict__ y) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (r >= n) return;
+  double2 acc = cz();
+  for (int c = lane; c < n; c += 32) acc = cfma(A[(size_t)r * n + c], x[c], acc);
+  acc = warp_sum2(acc);
+  if (lane == 0) y[r] = acc;
+}
+
+// coupling pieces at setup (chunk): R = A_bc - A_bi Yc (Yc = tile NTB of X)
+__global__ void k3_cpl_rhs(int cnt, int s0, int NI, int NB, int NC, int EBI, int ntile, int NTB,
+                           const int* __restrict__ bi_idx, const double2* __restrict__ bi_val,
+                           const double2* __restrict__ abc, const double2* __restrict__ X, double2* __restrict__ R) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)cnt * NB * NC) return;
+  const int sc = (int)(gid / ((long long)NB * NC)), k = (int)((gid / NC) % NB), c = (int)(gid % NC), s = s0 + sc;
+  double2 v = abc[((size_t)s * NB + k) * NC + c];
+  const double2* yc = X + ((size_t)sc * ntile + NTB) * NI * 32 + c;
+  for (int e = 0; e < EBI; ++e) {
+    const int i = bi_idx[((size_t)s * NB + k) * EBI + e];
+    if (i >= 0) v = cfms(bi_val[((size_t)s * NB + k) * EBI + e], yc[(size_t)i * 32], v);
+  }
+  R[gid] = v;
+}
+// cpl_b[s][k][:] = Sinv[k][:] R  (one warp per (sc, k); NC <= 32 accumulators in lanes' loop)
+__global__ void k3_cpl_b(int cnt, int s0, int NB, int NBP, int NC, const int* __restrict__ n_b,
+                         const double2* __restrict__ sinv, const double2* __restrict__ R, double2* __restrict__ cpl_b) {
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (w >= (long long)cnt * NB) return;
+  const int sc = (int)(w / NB), k = (int)(w % NB), s = s0 + sc;
+  const int nb = n_b[s];
+  double2* out = cpl_b + ((size_t)s * NB + k) * NC;
+  if (k >= nb) {
+    if (lane < NC) out[lane] = cz();
+    return;
+  }
+  const double2* row = sinv + ((size_t)sc * NBP + k) * NBP;
+  const double2* Rs = R + (size_t)sc * NB * NC;
+  for (int c = 0; c < NC; ++c) {
+    double2 acc = cz();
+    for (int k2 = lane; k2 < nb; k2 += 32) acc = cfma(row[k2], Rs[(size_t)k2 * NC + c], acc);
+    acc = warp_sum2(acc);
+    if (lane == 0) out[c] = acc;
+  }
+}
+// second coupling rhs A_ic - A_ib cpl_b into tile NTB of X
+__global__ void k3_cpl_i_rhs(int cnt, int s0, int NI, int NB, int NC, int EIB, int ntile, int NTB,
+                             const int* __restrict__ ib_idx, const double2* __restrict__ ib_val,
+                             const double2* __restrict__ aic, const double2* __restrict__ cpl_b, double2* __restrict__ X) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)cnt * NI * 32) return;
+  const int sc = (int)(gid / ((long long)NI * 32)), i = (int)((gid / 32) % NI), c = (int)(gid % 32), s = s0 + sc;
+  double2 v = cz();
+  if (c < NC) {
+    v = aic[((size_t)s * NI + i) * NC + c];
+    for (int e = 0; e < EIB; ++e) {
+      const int k = ib_idx[((size_t)s * NI + i) * EIB + e];
+      if (k >= 0) v = cfms(ib_val[((size_t)s * NI + i) * EIB + e], cpl_b[((size_t)s * NB + k) * NC + c], v);
+    }
+  }
+  X[(((size_t)sc * ntile + NTB) * NI + i) * 32 + c] = v;
+}
+// cpl_i = tile NTB; contrib = A_cc - A_ic^T cpl_i - A_bc^T cpl_b (transpose, feti.cpp:433)
+__global__ void k3_coarse_contrib(int cnt, int s0, int NI, int NB, int NC, int ntile, int NTB,
+                                  const double2* __restrict__ X, const double2* __restrict__ aic,
+                                  const double2* __restrict__ abc, const double2* __restrict__ acc,
+                                  const double2* __restrict__ cpl_b, double2* __restrict__ cpl_i,
+                                  double2* __restrict__ contrib) {
+  const int sc = blockIdx.x, s = s0 + sc;
+  const double2* Xc = X + ((size_t)sc * ntile + NTB) * NI * 32;
+  for (long long e = threadIdx.x; e < (long long)NI * NC; e += blockDim.x) {
+    const int i = (int)(e / NC), c = (int)(e % NC);
+    cpl_i[((size_t)s * NI + i) * NC + c] = Xc[(size_t)i * 32 + c];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int p = warp; p < NC * NC; p += nw) {
+    const int c1 = p / NC, c2 = p % NC;
+    double2 v = cz();
+    for (int i = lane; i < NI; i += 32)
+      v = cfma(aic[((size_t)s * NI + i) * NC + c1], Xc[(size_t)i * 32 + c2], v);
+    for (int k = lane; k < NB; k += 32)
+      v = cfma(abc[((size_t)s * NB + k) * NC + c1], cpl_b[((size_t)s * NB + k) * NC + c2], v);
+    v = warp_sum2(v);
+    if (lane == 0) contrib[((size_t)s * NC + c1) * NC + c2] = csub(acc[((size_t)s * NC + c1) * NC + c2], v);
+  }
+}
+// dense coarse matrix sum_s (A_cc - contrib) over the corner slots (feti.cpp:440-454)
+__global__ void k3_coarse_assemble(int nc, int NC, const int* __restrict__ slots, const double2* __restrict__ contrib,
+                                   double2* __restrict__ C) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)nc * nc) return;
+  const int a = (int)(gid / nc), b = (int)(gid % nc);
+  double2 v = cz();
+  for (int qa = 0; qa < 8; ++qa) {
+    const int sa = slots[a * 8 + qa];
+    if (sa < 0) continue;
+    for (int qb = 0; qb < 8; ++qb) {
+      const int sb = slots[b * 8 + qb];
+      if (sb < 0 || sb / NC != sa / NC) continue;
+      const int s = sa / NC;
+      v = cadd(v, contrib[((size_t)s * NC + sa % NC) * NC + sb % NC]);
+    }
+  }
+  C[gid] = v;
+}
+// Gauss-Jordan with partial pivoting on the equilibrated coarse matrix (PartialPivLU's
+// pivots; the 1e-13 singularity check of feti.cpp:469-474 is applied on the host)
+__global__ void k3_cgj_pivot(int n, int k, double2* __restrict__ A, int* __restrict__ piv, double* __restrict__ pabs,
+                             double2* __restrict__ col) {
+  __shared__ double bv[1024];
+  __shared__ int bi[1024];
+  double best = -1.0;
+  int arg = k;
+  for (int r = k + threadIdx.x; r < n; r += blockDim.x) {
+    const double v = cabs2(A[(size_t)r * n + k]);
+    if (v > best) best = v, arg = r;
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = arg;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double v = bv[threadIdx.x + o];
+      const int j = bi[threadIdx.x + o];
+      if (v > bv[threadIdx.x] || (v == bv[threadIdx.x] && j < bi[threadIdx.x])) bv[threadIdx.x] = v, bi[threadIdx.x] = j;
+    }
+    __syncthreads();
+  }
+  const int p = bi[0];
+  if (p != k)
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      const double2 t = A[(size_t)k * n + c];
+      A[(size_t)k * n + c] = A[(size_t)p * n + c];
+      A[(size_t)p * n + c] = t;
+    }
+  __syncthreads();
+  const double2 pv = A[(size_t)k * n + k];
+  if (threadIdx.x == 0) {
+    piv[k] = p;
+    pabs[k] = sqrt(cabs2(pv));
+  }
+  const double2 inv = crecip(pv);
+  __syncthreads();
+  for (int c = threadIdx.x; c < n; c += blockDim.x) A[(size_t)k * n + c] = c == k ? inv : cmul(A[(size_t)k * n + c], inv);
+  for (int r = threadIdx.x; r < n; r += blockDim.x) col[r] = r == k ? cz() : A[(size_t)r * n + k];
+}
+__global__ void k3_cgj_update(int n, int k, double2* __restrict__ A, const double2* __restrict__ col) {
+  const int r = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r == k || c >= n) return;
+  const double2 f = col[r];
+  const double2 pk = A[(size_t)k * n + c];
+  A[(size_t)r * n + c] = c == k ? make_double2(-(f.x * pk.x - f.y * pk.y), -(f.x * pk.y + f.y * pk.x))
+                                : cfms(f, pk, A[(size_t)r * n + c]);
+}
+// undo the row exchanges of Gauss-Jordan: columns swapped in reverse order
+__global__ void k3_cgj_unpermute(int n, double2* __restrict__ A, const int* __restrict__ piv) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  for (int k = n - 1; k >= 0; --k) {
+    const int p = piv[k];
+    if (p != k) {
+      const double2 t = A[(size_t)r * n + k];
+      A[(size_t)r * n + k] = A[(size_t)r * n + p];
+      A[(size_t)r * n + p] = t;
+    }
+  }
+}
+__global__ void k3_scale_sym(int n, double2* __restrict__ A, const double* __restrict__ sc) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)n * n) return;
+  A[gid] = cscale(A[gid], sc[gid / n] * sc[gid % n]);
+}
+__global__ void k3_diag_scale(int n, const double2* __restrict__ A, double* __restrict__ sc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double d = sqrt(cabs2(A[(size_t)i * n + i]));
+  sc[i] = d > 0.0 ? 1.0 / sqrt(d) : 1.0;
+}
+
+// ---------------------------------------------------------------------------------------
+// Eliminate pieces (feti.cpp:493-556)
+// split_rhs: f_i = rhs[idof], f_b = w rhs[bdof], f_c = rhs[corner dof]
+__global__ void k3_split(int S, int NI, int NB, const int* __restrict__ idof, const int* __restrict__ bdof,
+                         const double* __restrict__ bw, const double2* __restrict__ rhs, double2* __restrict__ fi,
+                         double2* __restrict__ fb) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long ni = (long long)S * NI;
+  if (gid < ni) {
+    const int f = idof[gid];
+    fi[gid] = f >= 0 ? rhs[f] : cz();
+  } else if (gid < ni + (long long)S * NB) {
+    const long long k = gid - ni;
+    const int f = bdof[k];
+    fb[k] = f >= 0 ? cscale(rhs[f], bw[k]) : cz();
+  }
+}
+__global__ void k3_gather_corner(int nc, const int* __restrict__ cdof, const double2* __restrict__ rhs,
+                                 double2* __restrict__ fc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < nc) fc[c] = rhs[cdof[c]];
+}
+// tb' = tb - A_bi yi
+__global__ void k3_tb_minus(int S, int NB, int NI, int EBI, const int* __restrict__ bi_idx,
+                            const double2* __restrict__ bi_val, const double2* __restrict__ yi,
+                            const double2* __restrict__ tb, double2* __restrict__ out) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)S * NB) return;
+  const int s = (int)(gid / NB);
+  double2 v = tb[gid];
+  for (int e = 0; e < EBI; ++e) {
+    const int i = bi_idx[gid * EBI + e];
+    if (i >= 0) v = cfms(bi_val[gid * EBI + e], yi[(size_t)s * NI + i], v);
+  }
+  out[gid] = v;
+}
+// r_i = f_i - A_ib u_b - A_ic z
+__global__ void k3_ri_rhs(int S, int NI, int NB, int NC, int EIB, const int* __restrict__ ib_idx,
+                          const double2* __restrict__ ib_val, const double2* __restrict__ aic,
+                          const int* __restrict__ cglob, const double2* __restrict__ z, const double2* __restrict__ ub,
+                          const double2* __restrict__ fi, double2* __restrict__ ri) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)S * NI) return;
+  const int s = (int)(gid / NI);
+  double2 v = fi[gid];
+  for (int e = 0; e < EIB; ++e) {
+    const int k = ib_idx[gid * EIB + e];
+    if (k >= 0) v = cfms(ib_val[gid * EIB + e], ub[(size_t)s * NB + k], v);
+  }
+  for (int c = 0; c < NC; ++c) {
+    const int g = cglob[(size_t)s * NC + c];
+    if (g >= 0) v = cfms(aic[gid * NC + c], z[g], v);
+  }
+  ri[gid] = v;
+}
+// primal assembly x[f] (feti.cpp:700-708): interior u_i, weighted interface slots, corner z
+__global__ void k3_assemble_x(int n, const int* __restrict__ kind, const int* __restrict__ ref,
+                              const double* __restrict__ xw, const double2* __restrict__ ui,
+                              const double2* __restrict__ ub, const double2* __restrict__ z, double2* __restrict__ x) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= n) return;
+  const int k = kind[f];
+  const int* r = ref + (size_t)f * 4;
+  double2 v = cz();
+  if (k == 0) {
+    v = ui[r[0]];
+  } else if (k == 2) {
+    v = z[r[0]];
+  } else {
+    for (int q = 0; q < 4 && r[q] >= 0; ++q) v = cadd(v, cscale(ub[r[q]], xw[f]));
+  }
+  x[f] = v;
+}
+
+// ---------------------------------------------------------------------------------------
+// Global operators on the structured mesh (K8): y = (kc K + mc M) x (+ Kc xc), one thread
+// per free dof gathering its <= 8 elements (element-by-element, exact like the CSR apply).
+struct Glob3 {
+  int nx, ny, nz, dpn, ed, n;
+  const int* free_dofs;
+  const int* free_map;
+  const int* cons_map;
+  const double* ke;
+  const double* me;
+};
+template <typename T>
+__device__ __forceinline__ double2 to_c(T v);
+template <>
+__device__ __forceinline__ double2 to_c<double>(double v) { return make_double2(v, 0.0); }
+template <>
+__device__ __forceinline__ double2 to_c<double2>(double2 v) { return v; }
+template <typename T>
+__device__ __forceinline__ void from_c(T* p, double2 v);
+template <>
+__device__ __forceinline__ void from_c<double>(double* p, double2 v) { *p = v.x; }
+template <>
+__device__ __forceinline__ void from_c<double2>(double2* p, double2 v) { *p = v; }
+
+template <typename T>
+__global__ void k3_apply_global(Glob3 g, const T* __restrict__ x, const double* __restrict__ xc, double2 kc,
+                                double2 mc, T* __restrict__ y) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= g.n) return;
+  const int md = g.free_dofs[f], dpn = g.dpn, c = md % dpn, node = md / dpn;
+  const int nnx = g.nx + 1, nny = g.ny + 1;
+  const int i = node % nnx, j = (node / nnx) % nny, k = node / (nnx * nny);
+  const int hx[8] = {0, 1, 1, 0, 0, 1, 1, 0}, hy[8] = {0, 0, 1, 1, 0, 0, 1, 1};
+  double2 acc = cz();
+  for (int ek = max(k - 1, 0); ek <= min(k, g.nz - 1); ++ek)
+    for (int ej = max(j - 1, 0); ej <= min(j, g.ny - 1); ++ej)
+      for (int ei = max(i - 1, 0); ei <= min(i, g.nx - 1); ++ei) {
+        const int dx = i - ei, dy = j - ej, dz = k - ek;
+        const int an = dz * 4 + (dy == 0 ? dx : 3 - dx);
+        for (int b = 0; b < 8; ++b) {
+          const int nb = ((ek + (b >> 2)) * nny + (ej + hy[b])) * nnx + (ei + hx[b]);
+          for (int c2 = 0; c2 < dpn; ++c2) {
+            const int md2 = nb * dpn + c2, q = (an * dpn + c) * g.ed + b * dpn + c2;
+            const double2 coef = cadd(cscale(kc, g.ke[q]), cscale(mc, g.me[q]));
+            const int f2 = g.free_map[md2];
+            if (f2 >= 0) acc = cfma(coef, to_c<T>(x[f2]), acc);
+            else if (xc != nullptr) acc = cfma(make_double2(g.ke[q], 0.0), make_double2(xc[g.cons_map[md2]], 0.0), acc);
+          }
+        }
+      }
+  from_c<T>(y + f, acc);
+}
+
+// V^-1 v in place for V = M_z (x) M_y (x) M_x (x) I_dpn: Thomas along lines, one thread per
+// line; line l starts at (l / G) * S1 + (l % G) * S2, element stride es
+__global__ void k3_tridiag(double* __restrict__ v, int nlines, int len, int G, long long S1, long long S2,
+                           long long es, const double* __restrict__ cp, const double* __restrict__ dinv, double off) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= nlines) return;
+  double* p = v + (long long)(l / G) * S1 + (long long)(l % G) * S2;
+  double x = 0.0;
+  for (int i = 0; i < len; ++i) {
+    x = (p[(long long)i * es] - off * x) * dinv[i];
+    p[(long long)i * es] = x;
+  }
+  for (int i = len - 2; i >= 0; --i) {
+    x = p[(long long)i * es] - cp[i] * x;
+    p[(long long)i * es] = x;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Krylov vector kernels (K7)
+// part[b][j] = sum_{rows of block b} conj(V_j) w  (j < nv), plus |w|^2 in slot nv
+__global__ void __launch_bounds__(256) k3_mdot_part(int n, int nv, const double2* __restrict__ V, size_t ldv,
+                                                    const double2* __restrict__ w, double2* __restrict__ part, int rows_pb) {
+  __shared__ double2 red[8];
+  const int r0 = blockIdx.x * rows_pb, r1 = min(n, r0 + rows_pb);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = 0; j <= nv; ++j) {
+    double2 acc = cz();
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+      const double2 wv = w[r];
+      acc = j < nv ? cfma_conj(V[(size_t)j * ldv + r], wv, acc) : make_double2(acc.x + cabs2(wv), 0.0);
+    }
+    acc = warp_sum2(acc);
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double2 t = cz();
+      for (int q = 0; q < 8; ++q) t = cadd(t, red[q]);
+      part[(size_t)blockIdx.x * (nv + 1) + j] = t;
+    }
+    __syncthreads();
+  }
+}
+__global__ void k3_mdot_final(int nblk, int nv, const double2* __restrict__ part, double2* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j > nv) return;
+  double2 t = cz();
+  for (int b = 0; b < nblk; ++b) t = cadd(t, part[(size_t)b * (nv + 1) + j]);
+  out[j] = t;
+}
+// w -= sum_j V_j h_j
+__global__ void k3_mupdate(int n, int nv, const double2* __restrict__ V, size_t ldv, const double2* __restrict__ h,
+                           double2* __restrict__ w) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double2 v = w[r];
+  for (int j = 0; j < nv; ++j) v = cfms(V[(size_t)j * ldv + r], h[j], v);
+  w[r] = v;
+}
+// y += sum_j V_j c_j
+__global__ void k3_mcombine(int n, int nv, const double2* __restrict__ V, size_t ldv, const double2* __restrict__ c,
+                            double2* __restrict__ y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double2 v = y[r];
+  for (int j = 0; j < nv; ++j) v = cfma(V[(size_t)j * ldv + r], c[j], v);
+  y[r] = v;
+}
+__global__ void k3_scale_to(int n, double2 a, const double2* __restrict__ x, double2* __restrict__ y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) y[r] = cmul(a, x[r]);
+}
+// y = a x + b y
+__global__ void k3_axpby(int n, double2 a, const double2* __restrict__ x, double2 b, double2* __restrict__ y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) y[r] = cadd(cmul(a, x[r]), cmul(b, y[r]));
+}
+// (|x|^2 sum, max |x|) partials and final
+__global__ void k3_norm_part(int n, const double2* __restrict__ x, double2* __restrict__ part) {
+  __shared__ double ss[8], sm[8];
+  double s = 0.0, m = 0.0;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    const double a = cabs2(x[r]);
+    s += a;
+    m = fmax(m, a);
+  }
+  s = warp_sum(s);
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) ss[threadIdx.x >> 5] = s, sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) a += ss[q], b = fmax(b, sm[q]);
+    part[blockIdx.x] = make_double2(a, b);
+  }
+}
+__global__ void k3_norm_final(int nblk, const double2* __restrict__ part, double2* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double a = 0.0, b = 0.0;
+  for (int q = 0; q < nblk; ++q) a += part[q].x, b = fmax(b, part[q].y);
+  *out = make_double2(a, sqrt(b));
+}
+__global__ void k3_real_to_complex(int n, const double* __restrict__ x, double2* __restrict__ y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) y[r] = make_double2(x[r], 0.0);
+}
+__global__ void k3_conj(int n, const double2* x, double2* y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) y[r] = cconj(x[r]);
+}
+__global__ void k3_sub(int n, const double2* a, const double2* b, double2* y) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) y[r] = csub(a[r], b[r]);
+}
+// lambda = Re t, leak partial = max |Im t| (as |.|^2 in the max slot)
+__global__ void k3_realify(int n, const double2* __restrict__ t, double* __restrict__ lam) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) lam[r] = t[r].x;
+}
+__global__ void k3_imag(int n, const double2* __restrict__ t, double2* __restrict__ out) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < n) out[r] = make_double2(0.0, t[r].y);
+}
+// y = ybar - w, u = lam / phi
+__global__ void k3_recover(int n, const double* __restrict__ ybar, const double* __restrict__ w,
+                           const double* __restrict__ lam, double phi, double* __restrict__ y, double* __restrict__ u) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  y[r] = ybar[r] - w[r];
+  u[r] = lam[r] / phi;
+}
+
+}  // namespace k3
+}  // namespace fetigpu

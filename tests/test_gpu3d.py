@@ -1,0 +1,114 @@
+"""3D extension (BASELINE.json configs 4-5): the sm_100a path against the CPU oracle.
+
+CPU part: the C++ host core's 3D partition and seeded target agree with the oracle's
+restatement (oracle/feti_oracle.cpp partition_structured3d, orc_target_sine3).
+GPU part (-m gpu): FETI-DP solves, operator applications and range-space Schur solves on
+the device equal the oracle's on the same seeded inputs (relative L2 <= 1e-8, iteration
+counts within +-2 — the north_star bar), for heat and linear elasticity.
+"""
+import numpy as np
+import pytest
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+CASES = [  # physics, n, s
+    (0, 8, 2),
+    (0, 12, 3),
+    (0, 16, 2),
+    (1, 8, 2),
+    (1, 12, 3),
+]
+
+
+@pytest.mark.parametrize("physics,n,s", CASES + [(0, 48, 3), (1, 24, 2)])
+def test_host_partition3d_matches_oracle(fetigpu, oracle_mod, physics, n, s):
+    from paper_1312_5653_b200 import box
+
+    p = box.make_box_problem(n, phi=1e-4, physics=physics, young=1.0, poisson=0.3, seed=3)
+    info = box.box_partition_info(p, s)
+    q = oracle_mod.Problem(n, n, n_z=n, physics=physics, young=1.0, poisson=0.3)
+    ref = q.partition_info(s, s, s)
+    assert (info["n"], info["m"]) == (q.n, q.m)
+    for k in ("n_subdomains", "n_corner_dofs", "n_lambda", "ex", "ey", "ez"):
+        assert info[k] == ref[k], k
+    sizes = q.partition_sizes(s, s, s)
+    assert info["NB"] == sizes[:, 2].max() and info["NC"] == max(sizes[:, 3].max(), 1)
+    assert info["NI"] == max(32, -(-sizes[:, 1].max() // 32) * 32)
+    assert np.array_equal(p.target_state, q.target_sine(3, mmax=6))
+
+
+def test_config4_config5_sizes(fetigpu):
+    from paper_1312_5653_b200 import box
+
+    i4 = box.box_partition_info(box.BoxProblem(128, 128, 128, 1e-6), 8)
+    assert (i4["n"], i4["n_subdomains"], i4["n_corner_dofs"], i4["NB"], i4["NC"]) == (127 ** 3, 512, 343, 1530, 8)
+    i5 = box.box_partition_info(box.BoxProblem(64, 64, 64, 1e-4, physics=1, young=1.0, poisson=0.3), 4)
+    assert (i5["n"], i5["n_subdomains"], i5["n_corner_dofs"]) == (3 * 64 * 65 * 65, 64, 288)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("physics,n,s", CASES)
+def test_gpu3d_feti_solve_matches_oracle(fetigpu, oracle_mod, physics, n, s):
+    from paper_1312_5653_b200 import box
+
+    phi = 1e-4
+    c = -1j / np.sqrt(phi)
+    p = box.make_box_problem(n, phi=phi, physics=physics, young=1.0, poisson=0.3, seed=1)
+    q = oracle_mod.Problem(n, n, n_z=n, physics=physics, young=1.0, poisson=0.3)
+    rng = np.random.default_rng(n + 10 * physics)
+    rhs = rng.standard_normal(p.n) + 1j * rng.standard_normal(p.n)
+    solver = box.BoxSchurSolver(p, s, tol=1e-10, max_iter=500)
+    try:
+        x, st = solver.feti_solve(rhs)
+        F = oracle_mod.Feti(q, s, s, c, s_z=s, tol=1e-10, max_iter=500)
+        xr, sr = F.solve(rhs)
+        assert st["converged"] and sr["converged"]
+        assert rel(x, xr) <= 1e-8
+        assert abs(st["iterations"] - sr["iterations"]) <= 2
+        assert st["primal_residual"] <= 1e-8
+        # conjugate factor through conjugate reuse
+        xm, stm = solver.feti_solve(np.conj(rhs), sign=-1)
+        assert rel(xm, np.conj(x)) <= 1e-12 and stm["iterations"] == st["iterations"]
+        # operator parity (apply_dual_operator / apply_dirichlet_preconditioner)
+        lam = rng.standard_normal(F.n_lambda) + 1j * rng.standard_normal(F.n_lambda)
+        assert rel(solver.apply_dual_operator(lam), F.apply_dual_operator(lam)) <= 1e-11
+        assert rel(solver.apply_dirichlet_preconditioner(lam), F.apply_dirichlet_preconditioner(lam)) <= 1e-11
+    finally:
+        solver.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("physics,n,s,phi", [(0, 12, 3, 1e-6), (0, 16, 2, 1e-4), (1, 8, 2, 1e-4), (1, 12, 3, 1e-2)])
+def test_gpu3d_schur_solve_matches_oracle(fetigpu, oracle_mod, physics, n, s, phi):
+    from paper_1312_5653_b200 import box
+
+    p = box.make_box_problem(n, phi=phi, physics=physics, young=1.0, poisson=0.3, seed=2)
+    q = oracle_mod.Problem(n, n, n_z=n, physics=physics, young=1.0, poisson=0.3)
+    r = box.solve_range_space_3d(p, s, tol=1e-10, max_iter=500)
+    o = q.schur_solve(s, s, phi, p.target_state, s_z=s, tol=1e-10, max_iter=500)
+    assert r["converged"] and o["converged"]
+    for k in ("y", "u", "lambda"):
+        assert rel(r[k], o[k]) <= 1e-8, k
+    assert abs(r["plus_stats"]["iterations"] - o["plus_stats"]["iterations"]) <= 2
+    assert abs(r["minus_stats"]["iterations"] - o["minus_stats"]["iterations"]) <= 2
+    assert r["imag_leak"] <= 1e-6
+
+
+@pytest.mark.gpu
+def test_gpu3d_zero_rhs_and_contracts(fetigpu):
+    from paper_1312_5653_b200 import ContractError, box
+
+    p = box.make_box_problem(8, phi=1e-4)
+    solver = box.BoxSchurSolver(p, 2)
+    try:
+        x, st = solver.feti_solve(np.zeros(p.n, dtype=complex))
+        assert st["iterations"] == 0 and st["converged"] and not np.any(x)
+        with pytest.raises(ContractError):
+            solver.solve(np.zeros(p.n + 1))
+    finally:
+        solver.close()
+    with pytest.raises(ContractError):
+        box.BoxSchurSolver(box.make_box_problem(8, phi=1e-4), 3)  # 3 does not divide 8

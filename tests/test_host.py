@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     text = open(os.path.join(ROOT, "include", "fetigpu.h")).read()
-    return sorted(set(re.findall(r"\b(fetigpu_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(fetigpu(?:3d)?_[a-z_0-9]+)\s*\(", text)))
 
 
 def test_library_exports_every_header_symbol(fetigpu):
