@@ -370,6 +370,141 @@ def run_gpu(args):
     return 0
 
 
+CONFIG3D = {  # BASELINE.json configs 4-5 (the 3D extension; one GPU)
+    4: dict(n=128, s=8, phi=1e-6, physics=0, mmax=6,
+            workload="config4: 128^3 Q1 hexahedra heat, 8x8x8 subdomains of 16^3, phi=1e-6, tol 1e-10, FP64 complex"),
+    5: dict(n=64, s=4, phi=1e-4, physics=1, mmax=6,
+            workload="config5: 64^3 Q1 hexahedra linear elasticity (E=1, nu=0.3, clamped x=0), 4x4x4 subdomains of "
+                     "16^3, phi=1e-4, tol 1e-10, FP64 complex"),
+}
+
+
+def cpu_sample_oracle3d(cfg, threads, its_gpu):
+    """Oracle (3D restatement) on a bounded sample with the config's subdomain size: the
+    2x2x2-subdomain cube of 16^3-element subdomains (32^3 mesh), setup once, one Schur solve.
+    Scaled to the config by subdomain count and iteration count (work per Krylov step is
+    per-subdomain), i.e. rate = 1 / (t_sample * (S_config / 8) * (its_gpu / its_sample))."""
+    from oracle import oracle as O
+
+    e = cfg["n"] // cfg["s"]
+    p = O.Problem(2 * e, 2 * e, n_z=2 * e, physics=cfg["physics"], young=1.0, poisson=0.3)
+    pair = O.SchurPair(p, 2, 2, cfg["phi"], tol=TOL, max_iter=MAX_ITER, threads=threads, s_z=2, setup_threads=threads)
+    t0 = time.perf_counter()
+    r = pair.run(p.target_sine(0, mmax=cfg["mmax"]))
+    t = time.perf_counter() - t0
+    its = r["plus_stats"]["iterations"] + r["minus_stats"]["iterations"]
+    scale = (cfg["s"] ** 3 / 8.0) * (its_gpu / max(its, 1))
+    return 1.0 / (t * scale), t, its, pair.setup_seconds, 2 * e
+
+
+def run_gpu3d(args):
+    rank, world, local = dist_env()
+    if world != 1:
+        raise SystemExit("bench.py --config 4/5: the 3D path runs on one GPU (replicas only)")
+    import torch
+
+    torch.cuda.set_device(local)
+    from paper_1312_5653_b200 import box
+
+    cfg = CONFIG3D[args.config]
+    steps, warmup = args.steps, max(args.warmup, 3)
+
+    def problem(seed):
+        return box.make_box_problem(cfg["n"], phi=cfg["phi"], physics=cfg["physics"], young=1.0, poisson=0.3,
+                                    seed=seed, mmax=cfg["mmax"])
+
+    p = problem(0)
+    t0 = time.perf_counter()
+    solver = box.BoxSchurSolver(p, cfg["s"], tol=TOL, max_iter=MAX_ITER, device=local)
+    setup_s = time.perf_counter() - t0
+    n = p.n
+    seeds = list(range(warmup + steps))
+    targets = [problem(sd).target_state for sd in seeds]
+    d_ybar = [torch.from_numpy(t).cuda() for t in targets]
+    d_y = torch.empty(n, dtype=torch.float64, device="cuda")
+    d_u, d_l = torch.empty_like(d_y), torch.empty_like(d_y)
+    stream = torch.cuda.ExternalStream(solver.stream)
+
+    def device_step(k):
+        return solver.solve_device(d_ybar[k].data_ptr(), 0, d_y.data_ptr(), d_u.data_ptr(), d_l.data_ptr())
+
+    for k in range(warmup):
+        device_step(k)
+    torch.cuda.synchronize()
+    its = []
+    launches0 = solver.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for k in range(warmup, warmup + steps):
+            st = device_step(k)
+            its.append((st["plus_stats"]["iterations"], st["minus_stats"]["iterations"]))
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = solver.launch_count() - launches0
+    t_dev = ev0.elapsed_time(ev1) / 1000.0
+    value = steps / t_dev
+    host_t = [torch.from_numpy(t).pin_memory().numpy() for t in targets]
+    outs = tuple(torch.empty(n, dtype=torch.float64).pin_memory().numpy() for _ in range(3))
+    solver.solve(host_t[0], None, out=outs)
+    torch.cuda.synchronize()
+    w0 = time.perf_counter()
+    for k in range(warmup, warmup + steps):
+        solver.solve(host_t[k], None, out=outs)
+    e2e = steps / (time.perf_counter() - w0)
+    solver.profile(True)
+    solver.profile_read(reset=True)
+    for k in range(warmup, warmup + steps):
+        device_step(k)
+    torch.cuda.synchronize()
+    prof = solver.profile_read(reset=True)
+    solver.profile(False)
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    kclass = max(("dual_gemv", "precond_gemv"), key=lambda c: prof[c]["ms"])
+    kb = solver.class_bytes(kclass)
+    avg_ms = prof[kclass]["ms"] / max(prof[kclass]["launches"], 1)
+    achieved = kb / (avg_ms / 1000.0) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(f"config{args.config}_{kclass}")
+    except Exception:
+        pass
+    iters = [float(np.mean([a for a, _ in its])), float(np.mean([b for _, b in its]))]
+    line = {
+        "metric": METRIC.replace("2D Poisson 1M dofs", "3D config %d" % args.config), "value": value, "unit": UNIT,
+        "n_gpus": 1, "steps": steps, "warmup": warmup, "ms_per_step": t_dev / steps * 1000.0,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (seeded sine-mode ybar on the cube, seed = step)",
+        "config": {"workload": cfg["workload"], "phi": cfg["phi"], "n_free": n, "n_lambda": solver.n_lambda,
+                   "coarse_dim": solver.coarse_dim, "iterations_plus_minus_mean": iters, "setup_seconds": setup_s,
+                   "setup_phases_s": solver.setup_times(),
+                   "l2": "inputs larger than L2 (packed S_bb, S_bb^-1: %.1f GB each)" % (kb / 1e9),
+                   "parallelism": "1 GPU",
+                   "kernel_ms_per_step": {c: {"ms_per_step": v["ms"] / steps, "launches_per_step": v["launches"] / steps}
+                                          for c, v in prof.items() if v["launches"]}},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 3 * 8 * n},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": kclass, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "peak_source": "measured" if "hbm_gbs" in peaks else "fallback",
+                     "bytes_per_launch": kb, "avg_launch_ms": avg_ms},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, ts, its_s, su, m = cpu_sample_oracle3d(cfg, threads, sum(iters))
+        line["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"oracle/ ({threads} threads) on the {m}^3 mesh with 2x2x2 subdomains of the config's size: "
+                      f"setup {su:.1f} s, one Schur solve {ts:.2f} s with {its_s} iterations, scaled by "
+                      f"{cfg['s'] ** 3}/8 subdomains and {sum(iters):.0f}/{its_s} iterations"}
+    print(json.dumps(line), flush=True)
+    solver.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -378,13 +513,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
-    ap.add_argument("--config", type=int, default=2, choices=[2, 3],
-                    help="2: the headline config (default); 3: BASELINE config 3 on one GPU")
+    ap.add_argument("--config", type=int, default=2, choices=[2, 3, 4, 5],
+                    help="2: the headline config (default); 3: BASELINE config 3 on one GPU; 4/5: the 3D configs")
     ap.add_argument("--augment", action="store_true",
                     help="edge-RBM augmented coarse space (reference default; BASELINE configs use augment=false)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config in CONFIG3D:
+        return run_gpu3d(args)
     return run_gpu(args)
 
 

@@ -1007,7 +1007,7 @@ struct Feti {
   Partition part;
   cd kcoef = 1.0, mcoef = 0.0;
   double tol = 1e-10;
-  int max_iter = 1000, threads = 1;
+  int max_iter = 1000, threads = 1, setup_threads = 1;
   std::vector<Block> blk;
   bool augment = false;
   std::vector<AugColumn> aug;  // edge-RBM columns (augment = true)
@@ -1032,8 +1032,12 @@ struct Feti {
     const int ns = (int)part.subs.size();
     blk.resize(ns);
     std::vector<std::string> fail(ns);
-    std::vector<int> local_of_free(P->n(), -1);
-    for (int s = 0; s < ns; ++s) {
+    // The reference assembles and factors serially (feti.cpp:271).  setup_threads > 1 runs
+    // independent subdomains on worker threads (identical results; used only to keep the
+    // 3D CPU-baseline samples of bench.py within minutes).
+    const int nt = std::max(1, std::min(setup_threads, ns));
+    std::vector<std::vector<int>> lof_pool(nt, std::vector<int>(P->n(), -1));
+    auto body = [&](int s, std::vector<int>& local_of_free) {
       const Sub& sub = part.subs[s];
       Block& B = blk[s];
       const int nl = (int)sub.dofs.size(), nc_ = (int)sub.corner_local.size(), nr = (int)sub.r_local.size();
@@ -1086,6 +1090,16 @@ struct Feti {
       for (auto& [i, j, v] : tii) B.aii.at(i, j) += v;
       if (!B.arr.factor()) fail[s] = "singular remaining block A_rr in subdomain " + std::to_string(s);
       if (!B.aii.factor()) fail[s] = "singular interior block A_ii in subdomain " + std::to_string(s);
+    };
+    if (nt == 1) {
+      for (int s = 0; s < ns; ++s) body(s, lof_pool[0]);
+    } else {
+      std::vector<std::thread> workers;
+      for (int t = 0; t < nt; ++t)
+        workers.emplace_back([&, t] {
+          for (int s = t; s < ns; s += nt) body(s, lof_pool[t]);
+        });
+      for (auto& w : workers) w.join();
     }
     for (auto& f : fail)
       if (!f.empty()) throw NumericalError("assemble_subdomain_operators: " + f);
@@ -1753,8 +1767,14 @@ struct SchurPair {
   Feti plus, minus;
   double phi;
 };
+int orc_schur_create4(void* p, int sx, int sy, int sz, double phi, double tol, int max_iter, int threads,
+                      int augment, int setup_threads, void** out, double* setup_seconds);
 int orc_schur_create3(void* p, int sx, int sy, int sz, double phi, double tol, int max_iter, int threads,
                       int augment, void** out, double* setup_seconds) {
+  return orc_schur_create4(p, sx, sy, sz, phi, tol, max_iter, threads, augment, 1, out, setup_seconds);
+}
+int orc_schur_create4(void* p, int sx, int sy, int sz, double phi, double tol, int max_iter, int threads,
+                      int augment, int setup_threads, void** out, double* setup_seconds) {
   return guard([&] {
     auto* P = static_cast<Problem*>(p);
     if (!(phi > 0.0)) throw ContractError("ControlProblem: phi must be positive");
@@ -1771,6 +1791,7 @@ int orc_schur_create3(void* p, int sx, int sy, int sz, double phi, double tol, i
       F->tol = tol;
       F->max_iter = max_iter;
       F->threads = threads;
+      F->setup_threads = setup_threads;
     }
     sp->plus.mcoef = c;
     sp->minus.mcoef = -c;

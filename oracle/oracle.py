@@ -82,6 +82,8 @@ def lib():
                                        C.POINTER(OracleStats), dp, dp]
         L.orc_schur_create3.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
                                         C.c_int, C.POINTER(vp), dp]
+        L.orc_schur_create4.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                        C.c_int, C.c_int, C.POINTER(vp), dp]
         L.orc_feti_create.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_double,
                                       C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
         L.orc_feti_destroy.argtypes = [vp]
@@ -266,12 +268,13 @@ class Feti:
 class SchurPair:
     """Both reference factor solvers built once (control.cpp:303-304); run() = one Schur solve."""
 
-    def __init__(self, problem: Problem, s_x, s_y, phi, tol=1e-10, max_iter=2000, threads=1, augment=False, s_z=1):
+    def __init__(self, problem: Problem, s_x, s_y, phi, tol=1e-10, max_iter=2000, threads=1, augment=False, s_z=1,
+                 setup_threads=1):
         self.problem = problem
         h = C.c_void_p()
         t = np.zeros(1)
-        _check(lib().orc_schur_create3(problem._h, s_x, s_y, s_z, phi, tol, max_iter, threads, int(augment),
-                                       C.byref(h), _dp(t)))
+        _check(lib().orc_schur_create4(problem._h, s_x, s_y, s_z, phi, tol, max_iter, threads, int(augment),
+                                       setup_threads, C.byref(h), _dp(t)))
         self._h = h
         self.setup_seconds = float(t[0])
 

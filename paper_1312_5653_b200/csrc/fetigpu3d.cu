@@ -83,8 +83,12 @@ struct Ctx3 {
   int *d_free_dofs = nullptr, *d_free_map = nullptr, *d_cons_map = nullptr, *d_status = nullptr;
   double *d_bsgn = nullptr, *d_bw = nullptr, *d_lam_w = nullptr, *d_xw = nullptr, *d_ke = nullptr, *d_me = nullptr;
   long long *d_off = nullptr, *d_coff = nullptr;
-  int2* d_work = nullptr;
-  int nwork = 0, NTmax = 0;
+  int2* d_work = nullptr;    // tile rows (s, I)
+  int2* d_rowtab = nullptr;  // per tile row: first row-partial slot, count
+  int4* d_items = nullptr;   // GEMV work items (s, I, J0, J1)
+  int* d_rslot = nullptr;    // row-partial slot of each item
+  int nwork = 0, nitems = 0, NTmax = 0, G = 1;
+  static constexpr int kRowChunk = 32;  // tiles per GEMV work item (long rows are split)
   // operators
   double2 *d_ae = nullptr, *d_bb = nullptr, *d_bi_val = nullptr, *d_ib_val = nullptr, *d_aic = nullptr;
   double2 *d_abc = nullptr, *d_acc = nullptr, *d_cpl_b = nullptr, *d_cpl_i = nullptr, *d_Cinv = nullptr;
@@ -222,21 +226,40 @@ struct Ctx3 {
     // ragged packed-symmetric layout of S_bb / S_bb^-1 (per-subdomain tile counts)
     std::vector<int> nt(S);
     std::vector<long long> off(S + 1, 0), coff(S + 1, 0);
-    std::vector<int2> work;
+    std::vector<int2> work, rowtab;
+    std::vector<int4> items;
+    std::vector<int> rslot;
     for (int s = 0; s < S; ++s) {
       nt[s] = std::max(1, (H.n_b[s] + 31) / 32);
       off[s + 1] = off[s] + sym_size_h(nt[s]);
       coff[s + 1] = coff[s] + (long long)nt[s] * (nt[s] - 1) / 2;
-      for (int I = 0; I < nt[s]; ++I) work.push_back(make_int2(s, I));
+      for (int I = 0; I < nt[s]; ++I) {
+        work.push_back(make_int2(s, I));
+        rowtab.push_back(make_int2((int)items.size(), 0));
+        for (int J0 = 0; J0 <= I; J0 += kRowChunk) {
+          rslot.push_back((int)items.size());
+          items.push_back(make_int4(s, I, J0, std::min(J0 + kRowChunk, I + 1)));
+          rowtab.back().y++;
+        }
+      }
       NTmax = std::max(NTmax, nt[s]);
     }
     pack_entries = off[S];
     colpart_rows = coff[S];
     nwork = (int)work.size();
+    nitems = (int)items.size();
     d_nt = upload(nt);
     d_off = upload(off);
     d_coff = upload(coff);
     d_work = upload(work);
+    d_rowtab = upload(rowtab);
+    d_items = upload(items);
+    d_rslot = upload(rslot);
+    {
+      int sms = 0;
+      CU3(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc.device));
+      G = std::max(1, std::min(64, cdiv3(2 * sms, S)));  // coarse-rhs slices per subdomain
+    }
 
     // K1: assembly of the per-subdomain blocks
     const double ta = now();
@@ -408,7 +431,7 @@ struct Ctx3 {
 
     // workspaces
     d_xin = alloc<double2>((size_t)S * NB);
-    d_rows = alloc<double2>((size_t)S * NB);
+    d_rows = alloc<double2>((size_t)nitems * 32);
     d_colp = alloc<double2>((size_t)std::max<long long>(colpart_rows, 1) * 32);
     d_wb = alloc<double2>((size_t)S * NB);
     d_u1 = alloc<double2>((size_t)S * NB);
@@ -417,8 +440,8 @@ struct Ctx3 {
     d_fb = alloc<double2>((size_t)S * NB);
     d_yi = alloc<double2>((size_t)S * NI);
     d_ri = alloc<double2>((size_t)S * NI);
-    d_gcp = alloc<double2>((size_t)S * NC);
-    zero(d_gcp, (size_t)S * NC);
+    d_gcp = alloc<double2>((size_t)S * G * NC);
+    zero(d_gcp, (size_t)S * G * NC);
     d_fc = alloc<double2>(std::max(nc, 1));
     d_g = alloc<double2>(std::max(nc, 1));
     d_z = alloc<double2>(std::max(nc, 1));
@@ -560,17 +583,23 @@ struct Ctx3 {
   // ---------------------------------------------------------------------------- operators
   // y = S x for the packed symmetric operator pk (xin -> y, both [S][NB])
   void sym_gemv(const double2* pk, const double2* xin, double2* y, int klass) {
-    k3::SymArgs a{d_work, d_nt, d_off, d_coff, pk, xin, NB, d_rows, d_colp};
-    const size_t smem = sizeof(double2) * 32 * (size_t)NTmax;
-    launch(klass, [&] { k3::k3_sym_rows<8><<<nwork, 128, smem, stream>>>(a); });
-    launch(klass, [&] {
-      k3::k3_sym_reduce<<<cdiv3(nwork, 8), 256, 0, stream>>>(nwork, d_work, d_nt, d_coff, NB, d_rows, d_colp, y);
+    k3::SymArgs a{d_items, d_rslot, d_nt, d_off, d_coff, pk, xin, NB, d_rows, d_colp};
+    const size_t smem = sizeof(double2) * 32 * (size_t)(kRowChunk + 1);
+    static size_t smem_set = 0;
+    if (smem > 48 * 1024 && smem > smem_set) {
+      CU3(cudaFuncSetAttribute(k3::k3_sym_rows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      smem_set = smem;
+    }
+    launch(klass, [&] { k3::k3_sym_rows<8><<<nitems, 128, smem, stream>>>(a); });
+    launch(FETIGPU_K_LAMBDA, [&] {  // (partial reduction: counted with the gathers)
+      k3::k3_sym_reduce<<<cdiv3(nwork, 8), 256, 0, stream>>>(nwork, d_work, d_rowtab, d_nt, d_coff, NB, d_rows,
+                                                              d_colp, y);
     });
   }
   void coarse_solve(const double2* fc) {  // g = fc - sum gcp, z = C^-1 g
     if (nc == 0) return;
     launch(FETIGPU_K_COARSE, [&] {
-      k3::k3_coarse_rhs<<<cdiv3(nc, 128), 128, 0, stream>>>(nc, d_cslots, d_gcp, fc, d_g);
+      k3::k3_coarse_rhs<<<cdiv3(nc, 128), 128, 0, stream>>>(nc, NC, G, d_cslots, d_gcp, fc, d_g);
     });
     launch(FETIGPU_K_COARSE, [&] { k3::k3_dense_gemv<<<cdiv3(nc, 8), 256, 0, stream>>>(nc, d_Cinv, d_g, d_z); });
   }
@@ -584,7 +613,7 @@ struct Ctx3 {
     sym_gemv(d_Sip, d_xin, d_u1, FETIGPU_K_DUAL_GEMV);
     if (nc > 0) {
       launch(FETIGPU_K_COARSE, [&] {
-        k3::k3_gcp<<<S, 256, 0, stream>>>(NB, NC, NI, d_cpl_b, d_xin, nullptr, nullptr, d_gcp);
+        k3::k3_gcp<<<dim3(S, G), 256, 0, stream>>>(NB, NC, NI, G, d_cpl_b, d_xin, nullptr, nullptr, d_gcp);
       });
       coarse_solve(nullptr);
     }
@@ -615,7 +644,7 @@ struct Ctx3 {
     sym_gemv(d_Sip, d_xin, d_u1, FETIGPU_K_OTHER);
     if (nc > 0) {
       launch(FETIGPU_K_COARSE, [&] {
-        k3::k3_gcp<<<S, 256, 0, stream>>>(NB, NC, NI, d_cpl_b, tb, d_cpl_i, d_fi, d_gcp);
+        k3::k3_gcp<<<dim3(S, G), 256, 0, stream>>>(NB, NC, NI, G, d_cpl_b, tb, d_cpl_i, d_fi, d_gcp);
       });
       coarse_solve(d_fc);
       launch(FETIGPU_K_OTHER, [&] {
@@ -624,7 +653,13 @@ struct Ctx3 {
     }
   }
   void interior_solve(double2* x) {
-    launch(FETIGPU_K_BAND, [&] { k3::k3_bb_solve1<33><<<S, 256, 0, stream>>>(NBK, PB, d_bb, NI, x); });
+    // one warp per off-diagonal block of a block row: 8 warps up to P = 8, else 32
+    launch(FETIGPU_K_BAND, [&] {
+      if (PB <= 8)
+        k3::k3_bb_solve1<33, 8><<<S, 256, 0, stream>>>(NBK, PB, d_bb, NI, x);
+      else
+        k3::k3_bb_solve1<33, 32><<<S, 1024, 0, stream>>>(NBK, PB, d_bb, NI, x);
+    });
   }
   // (|x|^2, max|x|) -> host
   std::pair<double, double> norm_max(const double2* x, int len) {
@@ -640,7 +675,7 @@ struct Ctx3 {
     launch(FETIGPU_K_ORTHO, [&] {
       k3::k3_mdot_part<<<mdot_blocks, 256, 0, stream>>>(nl, nv, d_V, ldv, w, d_part, mdot_rows);
     });
-    launch(FETIGPU_K_ORTHO, [&] { k3::k3_mdot_final<<<cdiv3(nv + 1, 128), 128, 0, stream>>>(mdot_blocks, nv, d_part, h); });
+    launch(FETIGPU_K_ORTHO, [&] { k3::k3_mdot_final<<<cdiv3(nv + 1, 8), 256, 0, stream>>>(mdot_blocks, nv, d_part, h); });
   }
 
   // --------------------------------------------------------------------------------- GMRES
@@ -665,9 +700,16 @@ struct Ctx3 {
     CU3(cudaMemcpyAsync(d_best, x, sizeof(double2) * nl, cudaMemcpyDeviceToDevice, stream));
     double best = 1.0;
     const int mres = std::max(1, max_iter);
-    std::vector<cd> Hm((size_t)(mres + 1) * mres), gs(mres), g(mres + 1);
+    // Hessenberg columns grown on demand (the reference zero-fills (m+1) x m up front,
+    // 64 MB at max_iter = 2000, krylov.hpp:125; every entry read here is written first)
+    std::vector<std::vector<cd>> Hcol;
+    std::vector<cd> gs(mres), g(mres + 1);
     std::vector<double> gc(mres);
-    auto Hij = [&](int i, int j) -> cd& { return Hm[(size_t)j * (mres + 1) + i]; };
+    auto Hij = [&](int i, int j) -> cd& {
+      if ((int)Hcol.size() <= j) Hcol.resize(j + 1);
+      if ((int)Hcol[j].size() < j + 2) Hcol[j].resize(j + 2);
+      return Hcol[j][i];
+    };
     const int nb = cdiv3(nl, 256);
     while (true) {
       const double rnorm = norm_max(d_r, nl).first;
@@ -1032,13 +1074,14 @@ int fetigpu3d_profile_read(fetigpu3d_ctx* ctx, double* ms, long long* cnt, int r
   });
 }
 
-// algorithmic bytes per launch of the two GEMV classes: the packed operator, the gathered
-// input prefix per tile row and the column partials written and read back, the outputs
+// algorithmic bytes per launch of the two GEMV classes (k3_sym_rows): the packed operator
+// (read once), the input vector (once per subdomain), the row sums and the column partials
+// (written once); DESIGN.md §9
 double fetigpu3d_class_bytes(fetigpu3d_ctx* ctx, int klass) {
   Ctx3& c = ctx->c;
   if (klass != FETIGPU_K_PRECOND_GEMV && klass != FETIGPU_K_DUAL_GEMV) return 0.0;
   const double vec = 16.0 * (double)c.S * c.NB;
-  return 16.0 * (double)c.pack_entries + 2.0 * 512.0 * (double)c.colpart_rows + 3.0 * vec;
+  return 16.0 * (double)c.pack_entries + 512.0 * (double)(c.colpart_rows + c.nitems) + vec;
 }
 
 int fetigpu3d_setup_times(fetigpu3d_ctx* ctx, double* out8) {

@@ -265,18 +265,18 @@ __global__ void __launch_bounds__(256) k3_bb_factor(int NBK, int P, double2* __r
 // Forward y_K = b_K - sum_d L_{K,K-d} y_{K-d}; diagonal z_K = D_K^-1 y_K; backward
 // x_K = z_K - sum_d L_{K+d,K}^T x_{K+d}.  Warp w takes the blocks d = w+1, w+9, ...; the
 // other warps' partials are summed in a fixed order (deterministic).
-template <int RING>
-__global__ void __launch_bounds__(256) k3_bb_solve1(int NBK, int P, const double2* __restrict__ bb, int NI,
-                                                    double2* __restrict__ X) {
+template <int RING, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k3_bb_solve1(int NBK, int P, const double2* __restrict__ bb, int NI,
+                                                           double2* __restrict__ X) {
   __shared__ double2 ring[RING][32];
-  __shared__ double2 part[8][32];
+  __shared__ double2 part[WARPS][32];
   const int s = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double2* band = bb + (size_t)s * NBK * (P + 1) * 1024;
   double2* x = X + (size_t)s * NI;
   // forward + diagonal (z_K is written over b_K; the ring keeps the forward values y)
   for (int K = 0; K < NBK; ++K) {
     double2 acc = cz();
-    for (int d = warp + 1; d <= P; d += 8) {
+    for (int d = warp + 1; d <= P; d += WARPS) {
       if (K - d < 0) break;
       const double2* T = band + ((size_t)K * (P + 1) + d) * 1024;
       const double2* y = ring[(K - d) % RING];
@@ -287,11 +287,11 @@ __global__ void __launch_bounds__(256) k3_bb_solve1(int NBK, int P, const double
     __syncthreads();
     if (warp == 0) {
       double2 v = x[(size_t)K * 32 + lane];
-      for (int w = 0; w < 8; ++w) v = csub(v, part[w][lane]);
+      for (int w = 0; w < WARPS; ++w) v = csub(v, part[w][lane]);
       ring[K % RING][lane] = v;
     }
     __syncthreads();
-    if (warp == 1) {  // z_K = D_K^-1 y_K
+    if (warp == (WARPS > 8 ? WARPS - 1 : 1)) {  // z_K = D_K^-1 y_K (a warp idle in the next step)
       const double2* D = band + ((size_t)K * (P + 1)) * 1024;
       const double2* y = ring[K % RING];
       double2 z = cz();
@@ -304,7 +304,7 @@ __global__ void __launch_bounds__(256) k3_bb_solve1(int NBK, int P, const double
   // backward
   for (int K = NBK - 1; K >= 0; --K) {
     double2 acc = cz();
-    for (int d = warp + 1; d <= P; d += 8) {
+    for (int d = warp + 1; d <= P; d += WARPS) {
       if (K + d >= NBK) break;
       const double2* T = band + ((size_t)(K + d) * (P + 1) + d) * 1024;
       const double2 xr = ring[(K + d) % RING][lane];
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256) k3_bb_solve1(int NBK, int P, const double
     __syncthreads();
     if (warp == 0) {
       double2 v = x[(size_t)K * 32 + lane];
-      for (int w = 0; w < 8; ++w) v = csub(v, part[w][lane]);
+      for (int w = 0; w < WARPS; ++w) v = csub(v, part[w][lane]);
       ring[K % RING][lane] = v;
       x[(size_t)K * 32 + lane] = v;
     }
@@ -552,31 +552,37 @@ __global__ void k3_pack_sym(int cnt, int s0, int NBP, const int* __restrict__ nt
 // (s, I): y_I (rows) is complete in the CTA; the transposed contributions of the
 // off-diagonal tiles go to colpart[s][t = I(I-1)/2 + J] and k3_sym_reduce adds them.
 struct SymArgs {
-  const int2* work;          // (s, I) per CTA
+  const int4* work;          // (s, I, J0, J1) per CTA: tiles J0 <= J < J1 of row I (J1 = I + 1: + diagonal)
+  const int* rslot;          // row-partial slot of each work item
   const int* nt;             // tiles per subdomain
   const long long* off;      // packed offset per subdomain
   const long long* coff;     // column-partial offset per subdomain (units of 32 entries)
   const double2* pack;
   const double2* xin;        // [S][NB]
   int NB;
-  double2* rowsum;           // [S][NB]
+  double2* rowpart;          // [items][32]
   double2* colpart;          // [sum_s NT_s (NT_s - 1) / 2][32]
 };
 template <int BATCH>
 __global__ void __launch_bounds__(128) k3_sym_rows(SymArgs a) {
-  extern __shared__ double2 k3s_x[];  // x_0 .. x_I (32 (I + 1))
+  extern __shared__ double2 k3s_x[];  // x_J0 .. x_{J1-1}, then x_I
   __shared__ double2 red[4][32];
-  const int2 wk = a.work[blockIdx.x];
-  const int s = wk.x, I = wk.y;
+  const int4 wk = a.work[blockIdx.x];
+  const int s = wk.x, I = wk.y, J0 = wk.z, J1 = wk.w;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const double2* x = a.xin + (size_t)s * a.NB;
-  for (int k = threadIdx.x; k < 32 * (I + 1); k += blockDim.x) k3s_x[k] = k < a.NB ? x[k] : cz();
+  const int nx = 32 * (J1 - J0);
+  for (int k = threadIdx.x; k < nx + 32; k += blockDim.x) {
+    const int g = k < nx ? 32 * J0 + k : 32 * I + (k - nx);
+    k3s_x[k] = g < a.NB ? x[g] : cz();
+  }
   __syncthreads();
   const double2* row = a.pack + a.off[s] + sym_row_off(I);
   double2* cp = a.colpart + (a.coff[s] + (long long)I * (I - 1) / 2) * 32;
-  const double2 xi = k3s_x[32 * I + lane];
+  const double2 xi = k3s_x[nx + lane];
   double2 yr = cz();
-  for (int J = warp; J < I; J += 4) {
+  const int Jend = min(J1, I);
+  for (int J = J0 + warp; J < Jend; J += 4) {
     const double2* T = row + (size_t)J * 1024;
     double2 yc = cz();
 #pragma unroll
@@ -586,14 +592,14 @@ __global__ void __launch_bounds__(128) k3_sym_rows(SymArgs a) {
       for (int u = 0; u < BATCH; ++u) m[u] = __ldcs(T + (cb + u) * 32 + lane);
 #pragma unroll
       for (int u = 0; u < BATCH; ++u) {
-        yr = cfma(m[u], k3s_x[32 * J + ((lane + cb + u) & 31)], yr);
+        yr = cfma(m[u], k3s_x[32 * (J - J0) + ((lane + cb + u) & 31)], yr);
         yc = cfma(m[u], xi, yc);
         yc = shfl2(yc, (lane + 1) & 31);
       }
     }
     cp[(size_t)J * 32 + lane] = yc;
   }
-  if (warp == (I & 3)) {  // diagonal tile: cc = 0 diagonal, 1..15 both halves, 16 both (l, l+16)
+  if (J1 == I + 1 && warp == (I & 3)) {  // diagonal tile: cc = 0 diagonal, 1..15 both halves, 16 both (l, l+16)
     const double2* D = row + (size_t)I * 1024;
     double2 yc = cz();
 #pragma unroll
@@ -607,14 +613,14 @@ __global__ void __launch_bounds__(128) k3_sym_rows(SymArgs a) {
         if (c == 0) {
           yr = cfma(m[u], xi, yr);
         } else {
-          yr = cfma(m[u], k3s_x[32 * I + ((lane + c) & 31)], yr);
+          yr = cfma(m[u], k3s_x[nx + ((lane + c) & 31)], yr);
           yc = shfl2(yc, (lane + 1) & 31);
           yc = cfma(m[u], xi, yc);
         }
       }
     }
     const double2 m16 = __ldcs(D + 16 * 32 + lane);
-    yr = cfma(m16, k3s_x[32 * I + ((lane + 16) & 31)], yr);
+    yr = cfma(m16, k3s_x[nx + ((lane + 16) & 31)], yr);
     yc = shfl2(yc, (lane + 17) & 31);
     yr = cadd(yr, yc);
   }
@@ -622,20 +628,23 @@ __global__ void __launch_bounds__(128) k3_sym_rows(SymArgs a) {
   __syncthreads();
   if (warp == 0) {
     const double2 v = cadd(cadd(red[0][lane], red[1][lane]), cadd(red[2][lane], red[3][lane]));
-    const int k = 32 * I + lane;
-    if (k < a.NB) a.rowsum[(size_t)s * a.NB + k] = v;
+    a.rowpart[(size_t)a.rslot[blockIdx.x] * 32 + lane] = v;
   }
 }
-// y[s][32J + l] = rowsum + sum_{I > J} colpart[s][I(I-1)/2 + J][l]   (one warp per (s, J))
-__global__ void k3_sym_reduce(int nwork, const int2* __restrict__ work, const int* __restrict__ nt,
-                              const long long* __restrict__ coff, int NB, const double2* __restrict__ rowsum,
-                              const double2* __restrict__ colpart, double2* __restrict__ y) {
+// y[s][32J + l] = sum of the row partials of tile row J + sum_{I > J} colpart[s][I(I-1)/2 + J][l]
+// (one warp per tile row (s, J); rows: first row-partial slot and count per tile row)
+__global__ void k3_sym_reduce(int nwork, const int2* __restrict__ work, const int2* __restrict__ rows,
+                              const int* __restrict__ nt, const long long* __restrict__ coff, int NB,
+                              const double2* __restrict__ rowpart, const double2* __restrict__ colpart,
+                              double2* __restrict__ y) {
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (w >= nwork) return;
   const int2 wk = work[w];
   const int s = wk.x, J = wk.y, k = 32 * J + lane;
   if (k >= NB) return;
-  double2 v = rowsum[(size_t)s * NB + k];
+  const int2 rr = rows[w];
+  double2 v = rowpart[(size_t)rr.x * 32 + lane];
+  for (int q = 1; q < rr.y; ++q) v = cadd(v, rowpart[(size_t)(rr.x + q) * 32 + lane]);
   const double2* cp = colpart + coff[s] * 32;
   for (int I = J + 1; I < nt[s]; ++I) v = cadd(v, cp[((size_t)I * (I - 1) / 2 + J) * 32 + lane]);
   y[(size_t)s * NB + k] = v;
@@ -710,28 +719,54 @@ __global__ void k3_ub_correct(int S, int NB, int NC, const int* __restrict__ cgl
 // ---------------------------------------------------------------------------------------
 // Coarse problem (K4).  gcp[s][c] = cpl_b^T xin (+ cpl_i^T fi): one CTA per subdomain,
 // one warp per local corner dof; g = fc - sum_slots gcp; z = C^-1 g (dense, row per warp).
-__global__ void k3_gcp(int NB, int NC, int NI, const double2* __restrict__ cpl_b, const double2* __restrict__ xin,
-                       const double2* __restrict__ cpl_i, const double2* __restrict__ fi, double2* __restrict__ gcp) {
-  const int s = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int c = warp; c < NC; c += nw) {
-    double2 acc = cz();
-    for (int k = lane; k < NB; k += 32)
-      acc = cfma(cpl_b[((size_t)s * NB + k) * NC + c], xin[(size_t)s * NB + k], acc);
-    if (cpl_i != nullptr)
-      for (int i = lane; i < NI; i += 32)
-        acc = cfma(cpl_i[((size_t)s * NI + i) * NC + c], fi[(size_t)s * NI + i], acc);
-    acc = warp_sum2(acc);
-    if (lane == 0) gcp[(size_t)s * NC + c] = acc;
+// gcp partials: CTA (s, g) covers the slice g of the row-major [k][c] entries of cpl_b (and
+// of cpl_i); thread t reads entries t, t + 256, .. of its slice (coalesced) with c fixed
+// (256 % NC == 0 is not required: threads t >= per idle); per-c partials in fixed order.
+// Output part[s][g][c]; k3_coarse_rhs sums the G slices of a slot in order.
+__global__ void __launch_bounds__(256) k3_gcp(int NB, int NC, int NI, int G, const double2* __restrict__ cpl_b,
+                                              const double2* __restrict__ xin, const double2* __restrict__ cpl_i,
+                                              const double2* __restrict__ fi, double2* __restrict__ part) {
+  __shared__ double2 red[256];
+  const int s = blockIdx.x, g = blockIdx.y, t = threadIdx.x;
+  const int per = 256 / NC * NC;
+  double2 acc = cz();
+  if (t < per) {
+    const long long nb = (long long)NB * NC, ni = cpl_i != nullptr ? (long long)NI * NC : 0;
+    const long long tot = nb + ni, len = (tot + G - 1) / G;
+    const long long e0 = g * len, e1 = min(tot, e0 + len);
+    // align the slice start to a multiple of NC so that thread t keeps c = t % NC
+    long long e = e0 - e0 % NC + t;
+    if (e < e0) e += per;
+    const double2* cb = cpl_b + (size_t)s * NB * NC;
+    const double2* x = xin + (size_t)s * NB;
+    const double2* ci = cpl_i != nullptr ? cpl_i + (size_t)s * NI * NC : nullptr;
+    const double2* f = fi != nullptr ? fi + (size_t)s * NI : nullptr;
+    for (; e < e1; e += per) {
+      if (e < nb) acc = cfma(cb[e], x[e / NC], acc);
+      else acc = cfma(ci[e - nb], f[(e - nb) / NC], acc);
+    }
+  }
+  red[t] = acc;
+  __syncthreads();
+  if (t < NC) {
+    double2 v = cz();
+    for (int q = t; q < per; q += NC) v = cadd(v, red[q]);
+    part[((size_t)s * G + g) * NC + t] = v;
   }
 }
-__global__ void k3_coarse_rhs(int nc, const int* __restrict__ slots, const double2* __restrict__ gcp,
+// g = fc - sum_slots gcp, gcp of slot (s, k) = sum of its G partials part[s][g][k]
+__global__ void k3_coarse_rhs(int nc, int NC, int G, const int* __restrict__ slots, const double2* __restrict__ part,
                               const double2* __restrict__ fc, double2* __restrict__ g) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nc) return;
   double2 acc = fc ? fc[c] : cz();
   for (int q = 0; q < 8; ++q) {
     const int sl = slots[c * 8 + q];
-    if (sl >= 0) acc = csub(acc, gcp[sl]);
+    if (sl < 0) continue;
+    const int s = sl / NC, k = sl % NC;
+    double2 v = cz();
+    for (int gg = 0; gg < G; ++gg) v = cadd(v, part[((size_t)s * G + gg) * NC + k]);
+    acc = csub(acc, v);
   }
   g[c] = acc;
 }
@@ -1087,12 +1122,14 @@ __global__ void __launch_bounds__(256) k3_mdot_part(int n, int nv, const double2
     __syncthreads();
   }
 }
+// one warp per dot: lanes stride over the block partials, fixed-order butterfly
 __global__ void k3_mdot_final(int nblk, int nv, const double2* __restrict__ part, double2* __restrict__ out) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (j > nv) return;
   double2 t = cz();
-  for (int b = 0; b < nblk; ++b) t = cadd(t, part[(size_t)b * (nv + 1) + j]);
-  out[j] = t;
+  for (int b = lane; b < nblk; b += 32) t = cadd(t, part[(size_t)b * (nv + 1) + j]);
+  t = warp_sum2(t);
+  if (lane == 0) out[j] = t;
 }
 // w -= sum_j V_j h_j
 __global__ void k3_mupdate(int n, int nv, const double2* __restrict__ V, size_t ldv, const double2* __restrict__ h,
@@ -1141,10 +1178,13 @@ __global__ void k3_norm_part(int n, const double2* __restrict__ x, double2* __re
   }
 }
 __global__ void k3_norm_final(int nblk, const double2* __restrict__ part, double2* __restrict__ out) {
-  if (threadIdx.x != 0) return;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
   double a = 0.0, b = 0.0;
-  for (int q = 0; q < nblk; ++q) a += part[q].x, b = fmax(b, part[q].y);
-  *out = make_double2(a, sqrt(b));
+  for (int q = lane; q < nblk; q += 32) a += part[q].x, b = fmax(b, part[q].y);
+  a = warp_sum(a);
+  b = warp_max(b);
+  if (lane == 0) *out = make_double2(a, sqrt(b));
 }
 __global__ void k3_real_to_complex(int n, const double* __restrict__ x, double2* __restrict__ y) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
