@@ -112,3 +112,71 @@ def test_gpu3d_zero_rhs_and_contracts(fetigpu):
         solver.close()
     with pytest.raises(ContractError):
         box.BoxSchurSolver(box.make_box_problem(8, phi=1e-4), 3)  # 3 does not divide 8
+
+
+# ---------------------------------------------------------------------------------------
+# The BASELINE subdomain shapes (16^3 elements per subdomain) against committed oracle
+# fixtures (tests/golden/make_3d_golden.py), and the full config-4/5 sizes through
+# size-independent properties.
+GOLDEN = {"heat48": dict(n=48, s=3, phi=1e-6, physics=0), "elast32": dict(n=32, s=2, phi=1e-4, physics=1)}
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", sorted(GOLDEN))
+def test_gpu3d_config_subdomain_size_matches_golden(fetigpu, name):
+    import os
+
+    from paper_1312_5653_b200 import box
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden3d.npz"))
+    c = GOLDEN[name]
+    p = box.make_box_problem(c["n"], phi=c["phi"], physics=c["physics"], young=1.0, poisson=0.3, seed=0)
+    assert abs(np.linalg.norm(p.target_state) - float(g[f"{name}_ybar_norm"])) <= 1e-12 * float(g[f"{name}_ybar_norm"])
+    r = box.solve_range_space_3d(p, c["s"], tol=1e-10, max_iter=2000)
+    assert r["converged"]
+    for k in ("y", "u", "lambda"):
+        assert rel(r[k], g[f"{name}_{k}"]) <= 1e-8, k
+    its = g[f"{name}_iters"]
+    assert abs(r["plus_stats"]["iterations"] - int(its[0])) <= 2
+    assert abs(r["minus_stats"]["iterations"] - int(its[1])) <= 2
+
+
+def kkt_residuals(oracle_mod, cfg, r, ybar):
+    """State equation K y - V u (relative to |K ybar|; equals the Schur residual
+    K ybar - S lambda) and adjoint equation V (y - ybar) + K lambda (relative to |K lambda|),
+    with the exact operators assembled by the oracle (control.cpp:56-59)."""
+    q = oracle_mod.Problem(cfg["n"], cfg["n"], n_z=cfg["n"], physics=cfg["physics"], young=1.0, poisson=0.3)
+    ky = q.apply(0, r["y"])
+    vu = q.apply(1, r["u"])
+    kyb = q.apply(0, ybar)
+    kl = q.apply(0, r["lambda"])
+    vd = q.apply(1, r["y"] - ybar)
+    return np.linalg.norm(ky - vu) / np.linalg.norm(kyb), np.linalg.norm(vd + kl) / np.linalg.norm(kl)
+
+
+FULL = {4: dict(n=128, s=8, phi=1e-6, physics=0, its=16, state_tol=1e-8),
+        5: dict(n=64, s=4, phi=1e-4, physics=1, its=30, state_tol=1e-6)}
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("config", [4, 5])
+def test_gpu3d_full_config_properties(fetigpu, oracle_mod, config):
+    from paper_1312_5653_b200 import box
+
+    c = FULL[config]
+    p = box.make_box_problem(c["n"], phi=c["phi"], physics=c["physics"], young=1.0, poisson=0.3, seed=0)
+    solver = box.BoxSchurSolver(p, c["s"], tol=1e-10, max_iter=2000)
+    try:
+        r = solver.solve()
+        r2 = solver.solve()
+    finally:
+        solver.close()
+    assert r["converged"] and r["imag_leak"] <= 1e-6
+    assert r["plus_stats"]["iterations"] == r["minus_stats"]["iterations"]  # conjugate pair
+    assert abs(r["plus_stats"]["iterations"] - c["its"]) <= 2
+    for k in ("y", "u", "lambda"):  # deterministic: fixed-order reductions, no atomics
+        assert np.array_equal(r[k], r2[k]), k
+    state, adjoint = kkt_residuals(oracle_mod, c, r, p.target_state)
+    assert state <= c["state_tol"], state
+    assert adjoint <= 1e-10, adjoint
