@@ -98,6 +98,26 @@ def test_gpu3d_schur_solve_matches_oracle(fetigpu, oracle_mod, physics, n, s, ph
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("physics", [0, 1])
+def test_gpu3d_schur_solve_with_dirichlet_data(fetigpu, oracle_mod, physics):
+    """Non-zero constrained data y_c: rhs = K ybar + K_c y_c (control.cpp:15)."""
+    from paper_1312_5653_b200 import box
+
+    n, s, phi = 12, 3, 1e-4
+    p = box.make_box_problem(n, phi=phi, physics=physics, young=1.0, poisson=0.3, seed=4)
+    q = oracle_mod.Problem(n, n, n_z=n, physics=physics, young=1.0, poisson=0.3)
+    yc = np.random.default_rng(7).standard_normal(q.m)
+    solver = box.BoxSchurSolver(p, s, tol=1e-10, max_iter=500)
+    try:
+        r = solver.solve(p.target_state, yc)
+    finally:
+        solver.close()
+    o = q.schur_solve(s, s, phi, p.target_state, yc, s_z=s, tol=1e-10, max_iter=500)
+    for k in ("y", "u", "lambda"):
+        assert rel(r[k], o[k]) <= 1e-8, k
+
+
+@pytest.mark.gpu
 def test_gpu3d_zero_rhs_and_contracts(fetigpu):
     from paper_1312_5653_b200 import ContractError, box
 
