@@ -160,6 +160,18 @@ def cpu_sample_oracle(threads, steps, warmup, budget_s=150.0):
     return len(times) / sum(times), its, pair.setup_seconds, len(times)
 
 
+def solve_roofline(solver, prof, steps, ms_per_step, hbm_peak):
+    """Schur-solve roofline: the operator bytes streamed per solve (both GEMV
+    classes and the interior solves, algorithmic bytes x launches) over the HBM peak, as a
+    fraction of the measured time per solve."""
+    b = 0.0
+    for c in ("precond_gemv", "dual_gemv", "band"):
+        b += solver.class_bytes(c) * prof[c]["launches"] / steps
+    t_roof = b / (hbm_peak * 1e9) * 1e3
+    return {"bytes_per_solve": b, "t_roof_ms": t_roof, "ms_per_solve": ms_per_step, "frac": t_roof / ms_per_step,
+            "classes": ["precond_gemv", "dual_gemv", "band"]}
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -334,6 +346,7 @@ def run_gpu(args):
                      "bytes_per_launch": kb, "avg_launch_ms": avg_ms, "in_graph": in_graph},
         "clocks": clk.summary(),
     }
+    line["solve_roofline"] = solve_roofline(solver, prof, steps, t_max / steps * 1000.0, hbm_peak)
     # BASELINE config 2 is a phi sweep: rates and iteration counts per phi (own factors each)
     if rank == 0 and world == 1 and args.config == 2 and not args.no_sweep:
         sweep = {}
@@ -398,12 +411,17 @@ def cpu_sample_oracle3d(cfg, threads, its_gpu):
 
 
 def run_gpu3d(args):
+    """BASELINE configs 4-5.  N > 1 (torchrun): strong scaling of the same mesh, subdomain
+    z-layers sharded over the ranks (NCCL allreduce of the jump partials per operator
+    application, coarse problem assembled by allreduce and solved redundantly)."""
     rank, world, local = dist_env()
-    if world != 1:
-        raise SystemExit("bench.py --config 4/5: the 3D path runs on one GPU (replicas only)")
     import torch
 
     torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1312_5653_b200 import box
 
     cfg = CONFIG3D[args.config]
@@ -415,7 +433,16 @@ def run_gpu3d(args):
 
     p = problem(0)
     t0 = time.perf_counter()
-    solver = box.BoxSchurSolver(p, cfg["s"], tol=TOL, max_iter=MAX_ITER, device=local)
+    if world > 1:
+        import paper_1312_5653_b200 as F
+        import torch.distributed as dist
+
+        obj = [F.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        solver = box.BoxSchurSolver(p, cfg["s"], tol=TOL, max_iter=MAX_ITER, device=local, rank=rank, world=world,
+                                    nccl_id=obj[0])
+    else:
+        solver = box.BoxSchurSolver(p, cfg["s"], tol=TOL, max_iter=MAX_ITER, device=local)
     setup_s = time.perf_counter() - t0
     n = p.n
     seeds = list(range(warmup + steps))
@@ -432,6 +459,8 @@ def run_gpu3d(args):
         device_step(k)
     torch.cuda.synchronize()
     its = []
+    barrier(world)
+    torch.cuda.synchronize()
     launches0 = solver.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -441,17 +470,21 @@ def run_gpu3d(args):
             its.append((st["plus_stats"]["iterations"], st["minus_stats"]["iterations"]))
         ev1.record(stream)
         torch.cuda.synchronize()
+    barrier(world)
     launches = solver.launch_count() - launches0
-    t_dev = ev0.elapsed_time(ev1) / 1000.0
-    value = steps / t_dev
+    t_dev = max_over_ranks(ev0.elapsed_time(ev1) / 1000.0, world)
+    value = steps / t_dev  # strong scaling: the same config solved by all ranks together
     host_t = [torch.from_numpy(t).pin_memory().numpy() for t in targets]
     outs = tuple(torch.empty(n, dtype=torch.float64).pin_memory().numpy() for _ in range(3))
     solver.solve(host_t[0], None, out=outs)
+    barrier(world)
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     for k in range(warmup, warmup + steps):
         solver.solve(host_t[k], None, out=outs)
-    e2e = steps / (time.perf_counter() - w0)
+    w1 = time.perf_counter()
+    barrier(world)
+    e2e = steps / max_over_ranks(w1 - w0, world)
     solver.profile(True)
     solver.profile_read(reset=True)
     for k in range(warmup, warmup + steps):
@@ -474,14 +507,15 @@ def run_gpu3d(args):
     iters = [float(np.mean([a for a, _ in its])), float(np.mean([b for _, b in its]))]
     line = {
         "metric": METRIC.replace("2D Poisson 1M dofs", "3D config %d" % args.config), "value": value, "unit": UNIT,
-        "n_gpus": 1, "steps": steps, "warmup": warmup, "ms_per_step": t_dev / steps * 1000.0,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": t_dev / steps * 1000.0,
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (seeded sine-mode ybar on the cube, seed = step)",
         "config": {"workload": cfg["workload"], "phi": cfg["phi"], "n_free": n, "n_lambda": solver.n_lambda,
                    "coarse_dim": solver.coarse_dim, "iterations_plus_minus_mean": iters, "setup_seconds": setup_s,
                    "setup_phases_s": solver.setup_times(),
                    "l2": "inputs larger than L2 (packed S_bb, S_bb^-1: %.1f GB each)" % (kb / 1e9),
-                   "parallelism": "1 GPU",
+                   "parallelism": (f"subdomain z-layers sharded over {world} GPUs (NCCL allreduce of jump partials)"
+                                   if world > 1 else "1 GPU"),
                    "kernel_ms_per_step": {c: {"ms_per_step": v["ms"] / steps, "launches_per_step": v["launches"] / steps}
                                           for c, v in prof.items() if v["launches"]}},
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 3 * 8 * n},
@@ -492,7 +526,8 @@ def run_gpu3d(args):
                      "bytes_per_launch": kb, "avg_launch_ms": avg_ms},
         "clocks": clk.summary(),
     }
-    if not args.no_cpu_baseline:
+    line["solve_roofline"] = solve_roofline(solver, prof, steps, t_dev / steps * 1000.0, hbm_peak)
+    if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         rate, ts, its_s, su, m = cpu_sample_oracle3d(cfg, threads, sum(iters))
         line["cpu_baseline"] = {
@@ -500,8 +535,13 @@ def run_gpu3d(args):
             "sample": f"oracle/ ({threads} threads) on the {m}^3 mesh with 2x2x2 subdomains of the config's size: "
                       f"setup {su:.1f} s, one Schur solve {ts:.2f} s with {its_s} iterations, scaled by "
                       f"{cfg['s'] ** 3}/8 subdomains and {sum(iters):.0f}/{its_s} iterations"}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     solver.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
     return 0
 
 

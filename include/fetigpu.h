@@ -244,6 +244,20 @@ void* fetigpu3d_stream(fetigpu3d_ctx* ctx);
 long long fetigpu3d_launch_count(fetigpu3d_ctx* ctx, int reset);
 int fetigpu3d_profile(fetigpu3d_ctx* ctx, int enable);
 int fetigpu3d_profile_read(fetigpu3d_ctx* ctx, double* ms, long long* launches, int reset);
+/* Sharded 3D path: rank r of R owns the subdomain z-layers
+ * [r s_z/R, (r+1) s_z/R) (s_z % R == 0); dual (multiplier) and primal vectors are replicated,
+ * each rank applies its subdomains and one allreduce per operator application completes the
+ * jump gathers (two owners per row: the sum is exact); the coarse problem is assembled by an
+ * allreduce and solved redundantly.  NCCL, one process per GPU (nccl_id from
+ * fetigpu_nccl_unique_id on rank 0); solves take and return FULL vectors on every rank. */
+int fetigpu3d_create_sharded(const fetigpu3d_desc* desc, int rank, int world, const unsigned char* nccl_id,
+                             fetigpu3d_ctx** out);
+/* `world` ranks emulated by host threads on ONE device; one Schur solve, rank 0's result. */
+int fetigpu3d_emulated_schur_solve(const fetigpu3d_desc* desc, int world, const double* ybar, const double* yc,
+                                   double* y, double* u, double* lambda, fetigpu_schur_stats* stats);
+/* Host-only layout of a rank: info6 = first subdomain, local subdomains, local row owners,
+ * rows with both owners local, local corner slots, n_lambda. */
+int fetigpu3d_rank_info(const fetigpu3d_desc* desc, int rank, int world, long long* info6);
 /* Algorithmic bytes per launch of a kernel class; setup phase times (s): out8 = {assembly,
  * A_ii factor, multi-RHS solves, S_bb build, S_bb inverse, coupling + coarse, pack, total}. */
 double fetigpu3d_class_bytes(fetigpu3d_ctx* ctx, int klass);

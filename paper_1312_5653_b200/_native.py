@@ -118,6 +118,9 @@ def lib():
     L.fetigpu3d_class_bytes.argtypes = [vp, C.c_int]
     L.fetigpu3d_class_bytes.restype = C.c_double
     L.fetigpu3d_setup_times.argtypes = [vp, dp]
+    L.fetigpu3d_create_sharded.argtypes = [pd3, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]
+    L.fetigpu3d_emulated_schur_solve.argtypes = [pd3, C.c_int, dp, dp, dp, dp, dp, C.POINTER(SchurStats)]
+    L.fetigpu3d_rank_info.argtypes = [pd3, C.c_int, C.c_int, lp]
     _lib = L
     return L
 
@@ -132,5 +135,6 @@ EXPORTED_SYMBOLS = (
     "fetigpu3d_problem_info", "fetigpu3d_target_sine", "fetigpu3d_create", "fetigpu3d_destroy",
     "fetigpu3d_schur_solve", "fetigpu3d_schur_solve_device", "fetigpu3d_feti_solve", "fetigpu3d_apply_dual",
     "fetigpu3d_apply_precond", "fetigpu3d_stream", "fetigpu3d_launch_count", "fetigpu3d_profile",
-    "fetigpu3d_profile_read", "fetigpu3d_class_bytes", "fetigpu3d_setup_times",
+    "fetigpu3d_profile_read", "fetigpu3d_class_bytes", "fetigpu3d_setup_times", "fetigpu3d_create_sharded",
+    "fetigpu3d_emulated_schur_solve", "fetigpu3d_rank_info",
 )

@@ -24,7 +24,7 @@ from . import _native
 from ._native import Desc3, FetiStats, SchurStats
 
 __all__ = ["BoxProblem", "make_box_problem", "box_partition_info", "BoxSchurSolver", "solve_range_space_3d",
-           "feti_solve_3d"]
+           "feti_solve_3d", "emulated_schur_solve_3d", "rank_info_3d"]
 
 INFO_KEYS = ("n", "m", "n_subdomains", "n_corner_dofs", "n_lambda", "NI", "NB", "NC", "MR", "block_halfwidth",
              "dofs_per_node", "ex", "ey", "ez", "maxe_bi", "maxe_ib")
@@ -100,13 +100,19 @@ class BoxSchurSolver:
     factored once through conjugate reuse)."""
 
     def __init__(self, problem: BoxProblem, s_x=2, s_y=None, s_z=None, tol=1e-10, max_iter=1000, mass_coeff=None,
-                 device=0):
+                 device=0, rank=None, world=None, nccl_id=None):
         s_y = s_x if s_y is None else s_y
         s_z = s_x if s_z is None else s_z
         self.problem = problem
         self._desc = problem.desc(s_x, s_y, s_z, tol, max_iter, mass_coeff, device)
         h = C.c_void_p()
-        _check(_native.lib().fetigpu3d_create(C.byref(self._desc), C.byref(h)))
+        if world is not None and world > 1:  # subdomain z-layers sharded over NCCL
+            if nccl_id is None or rank is None:
+                raise ContractError("sharded BoxSchurSolver needs rank, world and the nccl_id of rank 0")
+            _check(_native.lib().fetigpu3d_create_sharded(C.byref(self._desc), rank, world, bytes(nccl_id),
+                                                          C.byref(h)))
+        else:
+            _check(_native.lib().fetigpu3d_create(C.byref(self._desc), C.byref(h)))
         self._h = h
         info = problem.info(s_x, s_y, s_z)
         self.info = info
@@ -205,3 +211,27 @@ def feti_solve_3d(problem: BoxProblem, mass_coeff, rhs, s_x=2, s_y=None, s_z=Non
         return solver.feti_solve(rhs)
     finally:
         solver.close()
+
+
+def emulated_schur_solve_3d(problem: BoxProblem, s_x, world, s_y=None, s_z=None, tol=1e-10, max_iter=1000):
+    """`world` ranks of the sharded path emulated by host threads on one GPU (rank 0's result)."""
+    s_y = s_x if s_y is None else s_y
+    s_z = s_x if s_z is None else s_z
+    d = problem.desc(s_x, s_y, s_z, tol, max_iter)
+    n = problem.n
+    ybar = np.ascontiguousarray(problem.target_state, dtype=np.float64)
+    y, u, lam = np.zeros(n), np.zeros(n), np.zeros(n)
+    st = SchurStats()
+    _check(_native.lib().fetigpu3d_emulated_schur_solve(C.byref(d), world, _dp(ybar), None, _dp(y), _dp(u), _dp(lam),
+                                                        C.byref(st)))
+    return _schur_result(y, u, lam, st)
+
+
+def rank_info_3d(problem: BoxProblem, s_x, rank, world, s_y=None, s_z=None):
+    s_y = s_x if s_y is None else s_y
+    s_z = s_x if s_z is None else s_z
+    out = np.zeros(6, dtype=np.int64)
+    _check(_native.lib().fetigpu3d_rank_info(C.byref(problem.desc(s_x, s_y, s_z)), rank, world,
+                                             out.ctypes.data_as(C.POINTER(C.c_longlong))))
+    keys = ("sub_first", "n_sub_local", "row_owners", "rows_both_local", "corner_slots", "n_lambda")
+    return dict(zip(keys, (int(v) for v in out)))

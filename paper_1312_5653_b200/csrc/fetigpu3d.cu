@@ -27,8 +27,10 @@
 #include <functional>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
+#include "comm.hpp"
 #include "fetigpu.h"
 #include "host3d.hpp"
 #include "kernels3d.cuh"
@@ -60,7 +62,15 @@ struct Ev {
 struct Ctx3 {
   fetigpu3d_desc desc{};
   Host3Problem P;
-  Host3Partition H;
+  Host3Partition H;  // this rank's view (local_partition3d); the whole partition on one GPU
+  // sharding: subdomain z-layers per rank, dual and primal vectors replicated,
+  // one allreduce completes every jump gather (exact: two owners per multiplier row)
+  std::unique_ptr<Comm> comm;
+  bool dist() const { return comm != nullptr && comm->world() > 1; }
+  bool root() const { return !dist() || comm->rank() == 0; }
+  void allreduce(double2* buf, size_t count) {
+    if (dist() && count) comm->allreduce_sum(reinterpret_cast<double*>(buf), 2 * count, stream);
+  }
   cudaStream_t stream = nullptr;
   cd mc;
   double phi = 0;
@@ -493,6 +503,7 @@ struct Ctx3 {
     launch(FETIGPU_K_OTHER, [&] {
       k3::k3_coarse_assemble<<<cdiv3(nn, 256), 256, 0, stream>>>(nc, NC, d_cslots, contrib, d_Cinv);
     });
+    allreduce(d_Cinv, (size_t)nn);  // sharded: every rank assembled its subdomains' part
     double* sc = alloc<double>(nc);
     int* piv = alloc<int>(nc);
     double* pabs = alloc<double>(nc);
@@ -598,9 +609,11 @@ struct Ctx3 {
   }
   void coarse_solve(const double2* fc) {  // g = fc - sum gcp, z = C^-1 g
     if (nc == 0) return;
+    const double2* fc_r = root() ? fc : nullptr;  // f_c counted once
     launch(FETIGPU_K_COARSE, [&] {
-      k3::k3_coarse_rhs<<<cdiv3(nc, 128), 128, 0, stream>>>(nc, NC, G, d_cslots, d_gcp, fc, d_g);
+      k3::k3_coarse_rhs<<<cdiv3(nc, 128), 128, 0, stream>>>(nc, NC, G, d_cslots, d_gcp, fc_r, d_g);
     });
+    allreduce(d_g, nc);
     launch(FETIGPU_K_COARSE, [&] { k3::k3_dense_gemv<<<cdiv3(nc, 8), 256, 0, stream>>>(nc, d_Cinv, d_g, d_z); });
   }
   // F lam (feti.cpp:581-594): t_b = -B^T lam, u1 = S^-1 t_b, g = -sum cpl_b^T t_b,
@@ -621,6 +634,7 @@ struct Ctx3 {
       k3::k3_lam_jump<<<cdiv3(nl, 256), 256, 0, stream>>>(nl, NB, NC, -1.0, d_lam_lo, d_lam_hi, d_u1, d_cpl_b, d_cglob,
                                                          nc > 0 ? d_z : nullptr, out);
     });
+    allreduce(out, nl);
   }
   // Dirichlet preconditioner (feti.cpp:597-627): out = W B S_bb B^T W r
   void apply_precond(const double2* r, double2* out) {
@@ -632,6 +646,7 @@ struct Ctx3 {
     launch(FETIGPU_K_LAMBDA, [&] {
       k3::k3_lam_pre<<<cdiv3(nl, 256), 256, 0, stream>>>(nl, d_lam_lo, d_lam_hi, d_lam_w, d_wb, out);
     });
+    allreduce(out, nl);
   }
   // eliminate (feti.cpp:516-556) for t = [f_i ; tb]: u1_b = S^-1 (tb - A_bi y_i) with y_i =
   // A_ii^-1 f_i (computed once per FETI solve), g = f_c - (cpl_i^T f_i + cpl_b^T tb),
@@ -847,6 +862,7 @@ struct Ctx3 {
       k3::k3_lam_jump<<<cdiv3(nl, 256), 256, 0, stream>>>(nl, NB, NC, 1.0, d_lam_lo, d_lam_hi, d_u1, d_cpl_b, d_cglob,
                                                          nullptr, d_d);
     });
+    allreduce(d_d, nl);
     const Stats gs = gmres(d_d, d_lam, desc.max_iter, desc.tol);
     st.iterations = gs.iterations;
     st.converged = gs.converged ? 1 : 0;
@@ -865,11 +881,13 @@ struct Ctx3 {
     launch(FETIGPU_K_OTHER, [&] {
       k3::k3_assemble_x<<<cdiv3(n, 256), 256, 0, stream>>>(n, d_xkind, d_xref, d_xw, d_ri, d_u1, d_z, x);
     });
+    allreduce(x, n);
     // interface jump max |B u_r| and primal residual |A x - rhs| / |rhs|
     launch(FETIGPU_K_LAMBDA, [&] {
       k3::k3_lam_jump<<<cdiv3(nl, 256), 256, 0, stream>>>(nl, NB, NC, 1.0, d_lam_lo, d_lam_hi, d_u1, d_cpl_b, d_cglob,
                                                          nullptr, d_w);
     });
+    allreduce(d_w, nl);
     st.interface_jump = nl > 0 ? norm_max(d_w, nl).second : 0.0;
     apply_global<double2>(x, nullptr, cd(1.0), mc, d_ax);
     launch(FETIGPU_K_GLOBAL, [&] { k3::k3_sub<<<cdiv3(n, 256), 256, 0, stream>>>(n, d_ax, rhs, d_ax); });
@@ -941,6 +959,19 @@ struct fetigpu3d_ctx {
   Ctx3 c;
 };
 
+static void init_ctx3(Ctx3& c, const fetigpu3d_desc* desc) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw RuntimeError("fetigpu3d: no CUDA device");
+  c.desc = *desc;
+  c.P = build_problem3d(*desc);
+  if (desc->phi > 0.0) {
+    c.phi = desc->phi;
+    c.mc = std::complex<double>(0.0, -1.0 / std::sqrt(desc->phi));  // control.cpp:113-120
+  } else {
+    c.mc = std::complex<double>(desc->mass_coeff_re, desc->mass_coeff_im);
+  }
+}
+
 extern "C" {
 
 int fetigpu3d_problem_info(const fetigpu3d_desc* desc, long long* info) {
@@ -972,25 +1003,103 @@ int fetigpu3d_create(const fetigpu3d_desc* desc, fetigpu3d_ctx** out) {
   return guard3([&] {
     validate3(desc);
     *out = nullptr;
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) throw RuntimeError("fetigpu3d: no CUDA device");
     auto ctx = std::make_unique<fetigpu3d_ctx>();
     Ctx3& c = ctx->c;
-    c.desc = *desc;
-    c.P = build_problem3d(*desc);
+    init_ctx3(c, desc);
     c.H = build_partition3d(c.P, desc->s_x, desc->s_y, desc->s_z);
-    if (desc->phi > 0.0) {
-      c.phi = desc->phi;
-      c.mc = std::complex<double>(0.0, -1.0 / std::sqrt(desc->phi));  // control.cpp:113-120
-    } else {
-      c.mc = std::complex<double>(desc->mass_coeff_re, desc->mass_coeff_im);
-    }
     c.setup();
     *out = ctx.release();
   });
 }
 
 void fetigpu3d_destroy(fetigpu3d_ctx* ctx) { delete ctx; }
+
+// sharded context: this process is rank `rank` of `world` (one GPU each, NCCL); subdomain
+// z-layers [rank s_z/world, (rank+1) s_z/world); schur/feti solves take and return FULL vectors
+int fetigpu3d_create_sharded(const fetigpu3d_desc* desc, int rank, int world, const unsigned char* nccl_id,
+                             fetigpu3d_ctx** out) {
+  return guard3([&] {
+    validate3(desc);
+    if (!nccl_id) throw ContractError("fetigpu3d_create_sharded: nccl_id required");
+    auto ctx = std::make_unique<fetigpu3d_ctx>();
+    Ctx3& c = ctx->c;
+    init_ctx3(c, desc);
+    c.H = local_partition3d(build_partition3d(c.P, desc->s_x, desc->s_y, desc->s_z), rank, world);
+    c.comm = make_nccl_comm(nccl_id, rank, world, desc->device);
+    c.setup();
+    *out = ctx.release();
+  });
+}
+
+// `world` ranks emulated by host threads on ONE device (ThreadComm, device-to-device
+// copies for the allreduces); one range-space Schur solve, rank 0's result.  Tests the
+// sharded logic on a single GPU.
+int fetigpu3d_emulated_schur_solve(const fetigpu3d_desc* desc, int world, const double* ybar, const double* yc,
+                                   double* y, double* u, double* lambda, fetigpu_schur_stats* stats) {
+  return guard3([&] {
+    validate3(desc);
+    if (world < 1) throw ContractError("fetigpu3d_emulated_schur_solve: world must be >= 1");
+    const Host3Problem P0 = build_problem3d(*desc);
+    const Host3Partition G = build_partition3d(P0, desc->s_x, desc->s_y, desc->s_z);
+    auto group = std::make_shared<ThreadGroup>(world);
+    std::vector<std::string> errs(world);
+    std::vector<std::thread> th;
+    for (int q = 0; q < world; ++q)
+      th.emplace_back([&, q] {
+        try {
+          auto ctx = std::make_unique<fetigpu3d_ctx>();
+          Ctx3& c = ctx->c;
+          init_ctx3(c, desc);
+          c.H = local_partition3d(G, q, world);
+          c.comm = std::make_unique<ThreadComm>(group, q);
+          c.setup();
+          if (!(c.phi > 0.0)) throw ContractError("build_complex_factors: phi must be positive");
+          const size_t nb = sizeof(double) * c.n;
+          CU3(cudaMemcpyAsync(c.d_in_ybar, ybar, nb, cudaMemcpyHostToDevice, c.stream));
+          const double* dyc = nullptr;
+          if (yc && c.m > 0) {
+            CU3(cudaMemcpyAsync(c.d_in_yc, yc, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
+            dyc = c.d_in_yc;
+          }
+          fetigpu_schur_stats st{};
+          c.schur_solve(c.d_in_ybar, dyc, c.d_out_y, c.d_out_u, c.d_out_l, &st);
+          if (q == 0) {
+            CU3(cudaMemcpyAsync(y, c.d_out_y, nb, cudaMemcpyDeviceToHost, c.stream));
+            CU3(cudaMemcpyAsync(u, c.d_out_u, nb, cudaMemcpyDeviceToHost, c.stream));
+            CU3(cudaMemcpyAsync(lambda, c.d_out_l, nb, cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            if (stats) *stats = st;
+          }
+          group->barrier();  // keep every rank's buffers alive until rank 0 has copied
+        } catch (const std::exception& e) {
+          errs[q] = e.what();
+          group->abort();
+        }
+      });
+    for (auto& t : th) t.join();
+    for (int q = 0; q < world; ++q)
+      if (!errs[q].empty() && errs[q] != "rank group aborted")
+        throw RuntimeError("rank " + std::to_string(q) + ": " + errs[q]);
+  });
+}
+
+// host-only layout of rank `rank`: info[0..5] = first subdomain, local subdomains, local
+// multiplier-row owners (slots), rows with both owners local, local corner slots, n_lambda
+int fetigpu3d_rank_info(const fetigpu3d_desc* desc, int rank, int world, long long* info6) {
+  return guard3([&] {
+    validate3(desc);
+    const Host3Problem P0 = build_problem3d(*desc);
+    const Host3Partition L = local_partition3d(build_partition3d(P0, desc->s_x, desc->s_y, desc->s_z), rank, world);
+    long long owners = 0, both = 0, cs = 0;
+    for (int r = 0; r < L.n_lambda; ++r) {
+      owners += (L.lam_lo[r] >= 0) + (L.lam_hi[r] >= 0);
+      both += (L.lam_lo[r] >= 0 && L.lam_hi[r] >= 0);
+    }
+    for (int v : L.corner_slots) cs += v >= 0;
+    const long long v[6] = {L.s_first, L.S, owners, both, cs, L.n_lambda};
+    std::copy(v, v + 6, info6);
+  });
+}
 
 int fetigpu3d_schur_solve_device(fetigpu3d_ctx* ctx, const double* d_ybar, const double* d_yc, double* d_y, double* d_u,
                                  double* d_lambda, fetigpu_schur_stats* stats) {
@@ -1079,6 +1188,8 @@ int fetigpu3d_profile_read(fetigpu3d_ctx* ctx, double* ms, long long* cnt, int r
 // (written once); DESIGN.md §9
 double fetigpu3d_class_bytes(fetigpu3d_ctx* ctx, int klass) {
   Ctx3& c = ctx->c;
+  if (klass == FETIGPU_K_BAND)  // one interior solve: all blocks forward, off-diagonal ones backward
+    return 16.0 * 1024.0 * (double)c.S * c.NBK * (2.0 * c.PB + 1.0) + 3.0 * 16.0 * (double)c.S * c.NI;
   if (klass != FETIGPU_K_PRECOND_GEMV && klass != FETIGPU_K_DUAL_GEMV) return 0.0;
   const double vec = 16.0 * (double)c.S * c.NB;
   return 16.0 * (double)c.pack_entries + 512.0 * (double)(c.colpart_rows + c.nitems) + vec;

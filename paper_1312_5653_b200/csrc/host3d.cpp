@@ -330,6 +330,57 @@ Host3Partition build_partition3d(const Host3Problem& P, int sx, int sy, int sz) 
   return H;
 }
 
+Host3Partition local_partition3d(const Host3Partition& G, int rank, int world) {
+  if (world < 1 || rank < 0 || rank >= world) throw ContractError("partition3d: bad rank/world");
+  if (G.sz % world != 0) throw ContractError("partition3d: the subdomain layers (s_z) must divide evenly over the ranks");
+  const int per = G.sz / world * G.sx * G.sy, s0 = rank * per, s1 = s0 + per;
+  Host3Partition L = G;
+  L.S = per, L.s_first = s0, L.rank = rank, L.world = world;
+  auto slice = [&](auto& v, const auto& src, size_t width) {
+    v.assign(src.begin() + (size_t)s0 * width, src.begin() + (size_t)s1 * width);
+  };
+  slice(L.n_i, G.n_i, 1);
+  slice(L.n_b, G.n_b, 1);
+  slice(L.n_c, G.n_c, 1);
+  slice(L.ldof, G.ldof, G.nld);
+  slice(L.idof, G.idof, G.NI);
+  slice(L.bdof, G.bdof, G.NB);
+  slice(L.cglob, G.cglob, G.NC);
+  slice(L.brow, G.brow, (size_t)G.NB * G.MR);
+  slice(L.bsgn, G.bsgn, (size_t)G.NB * G.MR);
+  slice(L.bw, G.bw, G.NB);
+  slice(L.sub_i0, G.sub_i0, 1);
+  slice(L.sub_j0, G.sub_j0, 1);
+  slice(L.sub_k0, G.sub_k0, 1);
+  const long long b0 = (long long)s0 * G.NB, b1 = (long long)s1 * G.NB;
+  auto bslot = [&](int slot) { return (slot >= b0 && slot < b1) ? (int)(slot - b0) : -1; };
+  for (int r = 0; r < G.n_lambda; ++r) L.lam_lo[r] = bslot(G.lam_lo[r]), L.lam_hi[r] = bslot(G.lam_hi[r]);
+  const long long c0 = (long long)s0 * G.NC, c1 = (long long)s1 * G.NC;
+  for (size_t q = 0; q < G.corner_slots.size(); ++q) {
+    const int sl = G.corner_slots[q];
+    L.corner_slots[q] = (sl >= c0 && sl < c1) ? (int)(sl - c0) : -1;
+  }
+  const long long i0 = (long long)s0 * G.NI, i1 = (long long)s1 * G.NI;
+  for (int f = 0; f < G.n_free; ++f) {
+    int* xr = &L.xref[(size_t)f * 4];
+    const int* gr = &G.xref[(size_t)f * 4];
+    if (G.xkind[f] == 0) {
+      const bool mine = gr[0] >= i0 && gr[0] < i1;
+      L.xkind[f] = mine ? 0 : -1;
+      xr[0] = mine ? (int)(gr[0] - i0) : -1;
+    } else if (G.xkind[f] == 1) {
+      int q2 = 0;
+      for (int q = 0; q < 4; ++q) xr[q] = -1;
+      for (int q = 0; q < 4 && gr[q] >= 0; ++q)
+        if (bslot(gr[q]) >= 0) xr[q2++] = bslot(gr[q]);
+      L.xkind[f] = q2 > 0 ? 1 : -1;
+    } else {
+      L.xkind[f] = rank == 0 ? 2 : -1;  // corner values are replicated: one rank contributes
+    }
+  }
+  return L;
+}
+
 void target_sine3d(const Host3Problem& P, uint64_t seed, int modes, int mmax, double* ybar) {
   if (modes < 0 || mmax < 1) throw ContractError("target_sine: need modes >= 0 and mmax >= 1");
   std::mt19937_64 rng(seed);

@@ -59,10 +59,19 @@ struct Host3Partition {
                                     // slots s*NB+k, -1 pad), 2 corner (xref[0] = corner id)
   std::vector<double> xw;           // [n_free] weight of interface slots (1/mult)
   std::vector<int> sub_i0, sub_j0, sub_k0;  // element origin of each subdomain
+  // sharded view (local_partition3d): global id of local subdomain 0, rank, world
+  int s_first = 0, rank = 0, world = 1;
 };
 
 Host3Problem build_problem3d(const fetigpu3d_desc& d);
 Host3Partition build_partition3d(const Host3Problem& P, int sx, int sy, int sz);
+// Multi-GPU view: rank r of R owns the subdomain z-layers
+// [r sz/R, (r+1) sz/R) — a contiguous range of subdomain ids.  Per-subdomain tables are
+// sliced; multiplier rows stay global (dual vectors are replicated on every rank) with the
+// slot of a non-local owner set to -1, so every jump gather yields this rank's partial sum
+// and one allreduce completes it (each row has exactly two owners: the sum is exact).
+// Corner slots / primal refs keep local slots only; corner values are assembled by rank 0.
+Host3Partition local_partition3d(const Host3Partition& G, int rank, int world);
 // seeded sine-mode target of configs 4-5: a_k (Box-Muller), l_k, m_k, n_k =
 // 1 + rng() % mmax; the same scalar field for every component (2D plane strain convention)
 void target_sine3d(const Host3Problem& P, uint64_t seed, int modes, int mmax, double* ybar);

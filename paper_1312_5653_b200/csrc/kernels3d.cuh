@@ -679,7 +679,8 @@ __global__ void k3_lam_pre(int nl, const int* __restrict__ lo, const int* __rest
                            const double* __restrict__ lam_w, const double2* __restrict__ wb, double2* __restrict__ out) {
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= nl) return;
-  out[r] = cscale(csub(wb[lo[r]], wb[hi[r]]), lam_w[r]);
+  const int a = lo[r], b = hi[r];  // -1: owner on another rank (sharded: partial sum)
+  out[r] = cscale(csub(a >= 0 ? wb[a] : cz(), b >= 0 ? wb[b] : cz()), lam_w[r]);
 }
 // jump of u_b = u1_b - cpl_b z: out[row] = sign (u_b[lo] - u_b[hi])  (sign -1: F lam)
 __global__ void k3_lam_jump(int nl, int NB, int NC, double sign, const int* __restrict__ lo, const int* __restrict__ hi,
@@ -692,6 +693,10 @@ __global__ void k3_lam_jump(int nl, int NB, int NC, double sign, const int* __re
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int slot = sl[q], s = slot / NB;
+    if (slot < 0) {  // owner on another rank (sharded: partial sum)
+      u[q] = cz();
+      continue;
+    }
     double2 v = u1[slot];
     if (z != nullptr)
       for (int c = 0; c < NC; ++c) {
@@ -1016,7 +1021,8 @@ __global__ void k3_assemble_x(int n, const int* __restrict__ kind, const int* __
   const int k = kind[f];
   const int* r = ref + (size_t)f * 4;
   double2 v = cz();
-  if (k == 0) {
+  if (k < 0) {  // sharded: owned by other ranks
+  } else if (k == 0) {
     v = ui[r[0]];
   } else if (k == 2) {
     v = z[r[0]];
