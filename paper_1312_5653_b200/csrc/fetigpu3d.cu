@@ -75,7 +75,7 @@ struct Ctx3 {
   cd mc;
   double phi = 0;
   int S = 0, NI = 0, NB = 0, NC = 0, MR = 1, PB = 0, NBK = 0, nl = 0, n = 0, m = 0, nc = 0;
-  int NTB = 0, NBP = 0;  // interface tiles (max) and padded dense size
+  int NTB = 0, NTD = 0, NBP = 0;  // interface tiles (max), dense tiles (even), padded dense size
   std::vector<void*> allocs;
   long long launches = 0;
   double setup_seconds = 0;
@@ -203,7 +203,8 @@ struct Ctx3 {
     if (PB > 32) throw ContractError("fetigpu3d: block half-bandwidth " + std::to_string(PB) + " exceeds 32 blocks");
     if (NC > 32) throw ContractError("fetigpu3d: more than 32 corner dofs per subdomain");
     NTB = (NB + 31) / 32;
-    NBP = NTB * 32;
+    NTD = NTB + (NTB & 1);  // the blocked inverse works on 64-wide tiles
+    NBP = NTD * 32;
     const int ed = P.edofs;
     {
       std::vector<double2> ae((size_t)ed * ed);
@@ -317,7 +318,7 @@ struct Ctx3 {
     // K3: S_bb, S_bb^-1, coupling and coarse contributions, in chunks of subdomains
     const int ntile = NTB + 1;  // A_ib tiles + the A_ic / coupling tile
     const size_t per_sub = sizeof(double2) * ((size_t)ntile * NI * 32 + (size_t)NBP * NBP + (size_t)NB * NC) +
-                           sizeof(double2) * (size_t)(NTB + 1) * 1024;
+                           sizeof(double2) * (size_t)(NTD + 1) * 1024;
     size_t free_b = 0, total_b = 0;
     CU3(cudaMemGetInfo(&free_b, &total_b));
     const size_t persist = sizeof(double2) * (2 * (size_t)pack_entries + (size_t)S * NB * NC + (size_t)S * NI * NC);
@@ -333,7 +334,7 @@ struct Ctx3 {
     double2* dense = alloc<double2>((size_t)chunk * NBP * NBP);
     double2* R = alloc<double2>((size_t)chunk * NB * NC);
     double2* pbuf = alloc<double2>((size_t)chunk * 1024);
-    double2* cbuf = alloc<double2>((size_t)chunk * NTB * 1024);
+    double2* cbuf = alloc<double2>((size_t)chunk * NTD * 1024);
     double* prat = alloc<double>(chunk);
     const int msw = PB <= 12 ? 8 : 4;  // warps of the multi-RHS solve (ring = (P+1) x 32 x 4 warps x 16 B)
     const size_t msmem = (size_t)(PB + 1) * 32 * 4 * msw * sizeof(double2);
@@ -386,12 +387,19 @@ struct Ctx3 {
       {
         std::vector<double> one(cnt, 1.0);
         CU3(cudaMemcpyAsync(prat, one.data(), cnt * sizeof(double), cudaMemcpyHostToDevice, stream));
-        for (int K = 0; K < NTB; ++K) {
+        const size_t gsm = sizeof(double2) * (64 * 33 + 32 * 65);
+        static bool gattr = false;
+        if (!gattr) {
+          CU3(cudaFuncSetAttribute(k3::k3_gj_update64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+          gattr = true;
+        }
+        for (int K = 0; K < NTD; ++K) {
           k3::k3_gj_pivot<<<cnt, 256, 0, stream>>>(NBP, K, dense, pbuf, prat);
-          k3::k3_gj_panel<<<dim3(NTB, cnt), 256, 0, stream>>>(NBP, NTB, K, dense, pbuf, cbuf);
-          k3::k3_gj_update<<<dim3(NTB, NTB, cnt), 256, 0, stream>>>(NBP, NTB, K, dense, pbuf, cbuf);
+          k3::k3_gj_panel<<<dim3(NTD, cnt), 256, 0, stream>>>(NBP, NTD, K, dense, pbuf, cbuf);
+          k3::k3_gj_update64<<<dim3(NTD / 2, NTD / 2, cnt), 256, gsm, stream>>>(NBP, NTD, K, dense, pbuf, cbuf);
+          k3::k3_gj_setpivot<<<cnt, 256, 0, stream>>>(NBP, K, dense, pbuf);
           CU3(cudaGetLastError());
-          launches += 3;
+          launches += 4;
         }
         std::vector<double> pr(cnt);
         CU3(cudaMemcpyAsync(pr.data(), prat, cnt * sizeof(double), cudaMemcpyDeviceToHost, stream));

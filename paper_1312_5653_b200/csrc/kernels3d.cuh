@@ -515,6 +515,72 @@ __global__ void __launch_bounds__(256) k3_gj_update(int NBP, int NT, int K, doub
   for (int q = 0; q < 4; ++q) out[q] = (J == K) ? make_double2(-acc[q].x, -acc[q].y) : csub(out[q], acc[q]);
 }
 
+// Trailing update of step K as a register-blocked rank-32 GEMM on 64x64 tiles of C (the
+// dense chunk; NBP % 64 == 0): C[r][c] -= Cpanel[r][:] R[:][c] with R = the new row panel
+// (A_KJ) for columns outside block K and R = P for the columns of block K (which become
+// -Cpanel P, the new column panel).  Rows of block K (the row panel) are left alone.
+// 256 threads = 16 x 16, each owning a 4 x 4 patch (16 complex accumulators); per k step a
+// thread reads 4 + 4 operands from shared memory for 16 complex FMAs.
+__global__ void __launch_bounds__(256) k3_gj_update64(int NBP, int NT, int K, double2* __restrict__ dense,
+                                                      const double2* __restrict__ pbuf,
+                                                      const double2* __restrict__ cbuf) {
+  extern __shared__ __align__(16) double2 k3g_sm[];
+  double2 (*As)[33] = reinterpret_cast<double2 (*)[33]>(k3g_sm);             // [64][33]  rows x k
+  double2 (*Bs)[65] = reinterpret_cast<double2 (*)[65]>(k3g_sm + 64 * 33);   // [32][65]  k x cols
+  const int J0 = blockIdx.x * 64, I0 = blockIdx.y * 64, sc = blockIdx.z;
+  const int kr = K * 32;
+  if (I0 == kr && I0 + 64 <= kr + 32) return;  // (never: tiles are 64 wide)
+  double2* M = dense + (size_t)sc * NBP * NBP;
+  const double2* P = pbuf + (size_t)sc * 1024;
+  // A: old column panel of rows I0..I0+63 (cbuf holds block rows of 32)
+  for (int e = threadIdx.x; e < 64 * 32; e += 256) {
+    const int r = e >> 5, k = e & 31, I = (I0 + r) >> 5;
+    As[r][k] = cbuf[((size_t)sc * NT + I) * 1024 + ((I0 + r) & 31) * 32 + k];
+  }
+  for (int e = threadIdx.x; e < 32 * 64; e += 256) {
+    const int k = e >> 6, c = e & 63, gc = J0 + c;
+    Bs[k][c] = (gc >= kr && gc < kr + 32) ? P[k * 32 + (gc - kr)] : M[(size_t)(kr + k) * NBP + gc];
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = cz();
+#pragma unroll 2
+  for (int k = 0; k < 32; ++k) {
+    double2 a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = As[ty * 4 + i][k];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx + 16 * j];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = cfma(a[i], b[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gr = I0 + ty * 4 + i;
+    if (gr >= kr && gr < kr + 32) continue;  // row panel: already final
+    double2* row = M + (size_t)gr * NBP;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gc = J0 + tx + 16 * j;
+      if (gc >= kr && gc < kr + 32) row[gc] = make_double2(-acc[i][j].x, -acc[i][j].y);
+      else row[gc] = csub(row[gc], acc[i][j]);
+    }
+  }
+}
+// the pivot block of step K becomes P (after the update kernel has read the row panel)
+__global__ void k3_gj_setpivot(int NBP, int K, double2* __restrict__ dense, const double2* __restrict__ pbuf) {
+  const int sc = blockIdx.x;
+  double2* M = dense + (size_t)sc * NBP * NBP;
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x)
+    M[(size_t)(K * 32 + (e >> 5)) * NBP + K * 32 + (e & 31)] = pbuf[(size_t)sc * 1024 + e];
+}
+
 // ---------------------------------------------------------------------------------------
 // Packed symmetric storage of a dense chunk (subdomain s = s0 + sc, NT_s tiles):
 // row I = [off-diagonal tiles J < I (1024 each) | diagonal tile (17 x 32)]
