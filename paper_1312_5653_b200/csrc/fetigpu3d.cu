@@ -306,10 +306,27 @@ struct Ctx3 {
     const double tb = now();
     {
       double2* scratch = alloc<double2>((size_t)S * std::max(PB, 1) * 1024);
-      const size_t smem = 2 * sizeof(k3::Tile);
-      CU3(cudaFuncSetAttribute(k3::k3_bb_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      launch(FETIGPU_K_OTHER,
-             [&] { k3::k3_bb_factor<<<S, 256, smem, stream>>>(NBK, PB, d_bb, scratch, d_status); });
+      int sms = 0;
+      CU3(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc.device));
+      if (S >= 2 * sms || PB <= 2) {  // one CTA per subdomain fills the GPU
+        const size_t smem = 2 * sizeof(k3::Tile);
+        CU3(cudaFuncSetAttribute(k3::k3_bb_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        launch(FETIGPU_K_OTHER,
+               [&] { k3::k3_bb_factor<<<S, 256, smem, stream>>>(NBK, PB, d_bb, scratch, d_status); });
+      } else {  // few subdomains: every block column over the whole grid
+        zero(d_status, S);
+        for (int K = 0; K < NBK; ++K) {
+          const int nd = std::min(PB, NBK - 1 - K);
+          k3::k3_bbf_pivot<<<S, 256, 0, stream>>>(NBK, PB, K, d_bb, d_status);
+          if (nd > 0) {
+            k3::k3_bbf_lcol<<<dim3(nd, S), 256, 0, stream>>>(NBK, PB, K, d_bb, scratch);
+            k3::k3_bbf_update<<<dim3(nd * (nd + 1) / 2, S), 256, 0, stream>>>(NBK, PB, K, d_bb, scratch);
+            k3::k3_bbf_store<<<dim3(nd, S), 256, 0, stream>>>(NBK, PB, K, d_bb, scratch);
+          }
+          CU3(cudaGetLastError());
+          launches += nd > 0 ? 4 : 1;
+        }
+      }
       check_status(S, "interior block A_ii");
       release(scratch);
     }
@@ -342,7 +359,17 @@ struct Ctx3 {
       CU3(cudaFuncSetAttribute(k3::k3_bb_msolve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
     else
       CU3(cudaFuncSetAttribute(k3::k3_bb_msolve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
+    const size_t m2smem = sizeof(double2) * (32 * 33 + 32 * 65);
+    CU3(cudaFuncSetAttribute(k3::k3_bb_msolve2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m2smem));
+    const bool msolve_ring = std::getenv("FETIGPU3D_MSOLVE_RING") != nullptr;  // the first (ring) kernel
     auto msolve = [&](int cnt, int s0, int t0_, int tiles) {
+      if (!msolve_ring) {
+        launch(FETIGPU_K_OTHER, [&] {
+          k3::k3_bb_msolve2<<<dim3((tiles + 1) / 2, cnt), 256, m2smem, stream>>>(NBK, PB, d_bb, NI, ntile, t0_,
+                                                                               tiles, s0, X);
+        });
+        return;
+      }
       const int cpb = 4 * msw;
       dim3 grid(32 / cpb, tiles, cnt);
       double2* Yb = X + (size_t)t0_ * NI * 32;

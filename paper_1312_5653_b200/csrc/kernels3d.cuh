@@ -260,6 +260,68 @@ __global__ void __launch_bounds__(256) k3_bb_factor(int NBK, int P, double2* __r
   if (threadIdx.x == 0) status[s] = (worst > 1e-14) ? 0 : 1;
 }
 
+// The same block LDL^T with every block column K spread over the whole grid (4 launches per
+// K, all subdomains at once): pivot inverse (CTA per subdomain), L blocks (CTA per (d, s)),
+// trailing update (CTA per (dI, dJ, s)), write-back of L.  Used when the subdomains are
+// too few to fill the GPU one CTA each (config 5: 64 subdomains, P = 26).
+__global__ void __launch_bounds__(256) k3_bbf_pivot(int NBK, int P, int K, double2* __restrict__ bb,
+                                                    int* __restrict__ status) {
+  __shared__ Tile A;
+  __shared__ double rat;
+  const int s = blockIdx.x;
+  double2* blk = bb + (((size_t)s * NBK + K) * (P + 1)) * 1024;
+  tile_load(A, blk);
+  __syncthreads();
+  tile_invert(A, &rat);
+  __syncthreads();
+  tile_store(blk, A);
+  if (threadIdx.x == 0 && !(rat > 1e-14)) status[s] = 1;
+}
+__global__ void __launch_bounds__(256) k3_bbf_lcol(int NBK, int P, int K, const double2* __restrict__ bb,
+                                                   double2* __restrict__ scratch) {
+  __shared__ Tile A, D;
+  const int dI = blockIdx.x + 1, s = blockIdx.y;
+  const double2* band = bb + (size_t)s * NBK * (P + 1) * 1024;
+  tile_load(D, band + ((size_t)K * (P + 1)) * 1024);
+  tile_load(A, band + ((size_t)(K + dI) * (P + 1) + dI) * 1024);
+  __syncthreads();
+  double2 acc[4] = {cz(), cz(), cz(), cz()};
+  tile_mma<false>(A, D, acc);
+  const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
+  double2* L = scratch + ((size_t)s * P + (dI - 1)) * 1024;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) L[tpos(r, c0 + q)] = acc[q];
+}
+__global__ void __launch_bounds__(256) k3_bbf_update(int NBK, int P, int K, double2* __restrict__ bb,
+                                                     const double2* __restrict__ scratch) {
+  __shared__ Tile A, B;
+  // pair index -> (dI, dJ), 1 <= dJ <= dI
+  const int t = blockIdx.x, s = blockIdx.y;
+  int dI = (int)((sqrt(8.0 * t + 1.0) - 1.0) / 2.0) + 1;
+  while (dI * (dI - 1) / 2 > t) --dI;
+  while ((dI + 1) * dI / 2 <= t) ++dI;
+  const int dJ = t - dI * (dI - 1) / 2 + 1;
+  double2* band = bb + (size_t)s * NBK * (P + 1) * 1024;
+  tile_load(A, band + ((size_t)(K + dI) * (P + 1) + dI) * 1024);
+  tile_load(B, scratch + ((size_t)s * P + (dJ - 1)) * 1024);
+  __syncthreads();
+  double2 acc[4] = {cz(), cz(), cz(), cz()};
+  tile_mma<true>(A, B, acc);
+  double2* tgt = band + ((size_t)(K + dI) * (P + 1) + (dI - dJ)) * 1024;
+  const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int p = tpos(r, c0 + q);
+    tgt[p] = csub(tgt[p], acc[q]);
+  }
+}
+__global__ void k3_bbf_store(int NBK, int P, int K, double2* __restrict__ bb, const double2* __restrict__ scratch) {
+  const int dI = blockIdx.x + 1, s = blockIdx.y;
+  double2* dst = bb + (((size_t)s * NBK + K + dI) * (P + 1) + dI) * 1024;
+  const double2* src = scratch + ((size_t)s * P + (dI - 1)) * 1024;
+  for (int e = threadIdx.x; e < 1024; e += blockDim.x) dst[e] = src[e];
+}
+
 // ---------------------------------------------------------------------------------------
 // Per-solve interior substitution x = A_ii^-1 x, one CTA (8 warps) per subdomain (K5).
 // Forward y_K = b_K - sum_d L_{K,K-d} y_{K-d}; diagonal z_K = D_K^-1 y_K; backward
@@ -405,6 +467,108 @@ __global__ void __launch_bounds__(WARPS * 32) k3_bb_msolve(int NBK, int P, const
       y[(size_t)(K * 32 + lane) * 32 + q] = acc[q];
     }
     __syncwarp();
+  }
+}
+
+// Setup multi-RHS substitution, register-blocked (K3): a CTA solves 64 right-hand sides
+// (RHS tiles 2t, 2t+1 of [sub][tile][NI][32]) of one subdomain.  Every block product is a
+// 32 x 64 x 32 complex GEMM on shared-memory tiles, 256 threads each owning 2 rows x 4
+// columns.  Forward values y_K stay in Y until the backward sweep, which forms
+// z_K = D_K^-1 y_K and x_K = z_K - sum_d L_{K+d,K}^T x_{K+d} block row by block row.
+__device__ __forceinline__ void msv_stage(double2 (*Ls)[33], double2 (*Ys)[65], const double2* __restrict__ T,
+                                          const double2* __restrict__ y0, const double2* __restrict__ y1, int two) {
+  for (int e = threadIdx.x; e < 1024; e += 256) {
+    const int cc = e >> 5, r = e & 31;
+    Ls[r][(r + cc) & 31] = T[e];
+  }
+  for (int e = threadIdx.x; e < 32 * 64; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    Ys[r][c] = c < 32 ? y0[(size_t)r * 32 + c] : (two ? y1[(size_t)r * 32 + c - 32] : cz());
+  }
+}
+template <bool TRANS>
+__device__ __forceinline__ void msv_mma(const double2 (*Ls)[33], const double2 (*Ys)[65], double2 acc[2][4],
+                                        bool sub) {
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {
+    double2 a[2], b[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = TRANS ? Ls[k][ty * 2 + i] : Ls[ty * 2 + i][k];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = Ys[k][tx + 16 * j];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = sub ? cfms(a[i], b[j], acc[i][j]) : cfma(a[i], b[j], acc[i][j]);
+  }
+}
+__global__ void __launch_bounds__(256) k3_bb_msolve2(int NBK, int P, const double2* __restrict__ bb, int NI,
+                                                     int ntile, int tile0, int ntiles, int s0,
+                                                     double2* __restrict__ Y) {
+  extern __shared__ __align__(16) double2 k3v_sm[];
+  double2 (*Ls)[33] = reinterpret_cast<double2 (*)[33]>(k3v_sm);
+  double2 (*Ys)[65] = reinterpret_cast<double2 (*)[65]>(k3v_sm + 32 * 33);
+  const int t2 = blockIdx.x, sc = blockIdx.y, s = s0 + sc;
+  const int ta = tile0 + 2 * t2, two = (2 * t2 + 1 < ntiles) ? 1 : 0;
+  const double2* band = bb + (size_t)s * NBK * (P + 1) * 1024;
+  double2* ya = Y + ((size_t)sc * ntile + ta) * NI * 32;
+  double2* yb = two ? ya + (size_t)NI * 32 : ya;
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  auto load_acc = [&](int K, double2 acc[2][4]) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = K * 32 + ty * 2 + i, c = tx + 16 * j;
+        acc[i][j] = c < 32 ? ya[(size_t)r * 32 + c] : (two ? yb[(size_t)r * 32 + c - 32] : cz());
+      }
+  };
+  auto store_acc = [&](int K, double2 acc[2][4]) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = K * 32 + ty * 2 + i, c = tx + 16 * j;
+        if (c < 32) ya[(size_t)r * 32 + c] = acc[i][j];
+        else if (two) yb[(size_t)r * 32 + c - 32] = acc[i][j];
+      }
+  };
+  // forward: y_K = b_K - sum_d L_{K,K-d} y_{K-d}
+  for (int K = 0; K < NBK; ++K) {
+    double2 acc[2][4];
+    load_acc(K, acc);
+    for (int d = 1; d <= P && K - d >= 0; ++d) {
+      __syncthreads();
+      msv_stage(Ls, Ys, band + ((size_t)K * (P + 1) + d) * 1024, ya + (size_t)(K - d) * 1024,
+                yb + (size_t)(K - d) * 1024, two);
+      __syncthreads();
+      msv_mma<false>(Ls, Ys, acc, true);
+    }
+    __syncthreads();
+    store_acc(K, acc);
+  }
+  __syncthreads();
+  // backward: x_K = D_K^-1 y_K - sum_d L_{K+d,K}^T x_{K+d}
+  for (int K = NBK - 1; K >= 0; --K) {
+    double2 acc[2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = cz();
+    __syncthreads();
+    msv_stage(Ls, Ys, band + ((size_t)K * (P + 1)) * 1024, ya + (size_t)K * 1024, yb + (size_t)K * 1024, two);
+    __syncthreads();
+    msv_mma<false>(Ls, Ys, acc, false);
+    for (int d = 1; d <= P && K + d < NBK; ++d) {
+      __syncthreads();
+      msv_stage(Ls, Ys, band + ((size_t)(K + d) * (P + 1) + d) * 1024, ya + (size_t)(K + d) * 1024,
+                yb + (size_t)(K + d) * 1024, two);
+      __syncthreads();
+      msv_mma<true>(Ls, Ys, acc, true);
+    }
+    __syncthreads();
+    store_acc(K, acc);
   }
 }
 
