@@ -702,13 +702,26 @@ struct Ctx3 {
       });
     }
   }
+  // interior solves: the TMA-streamed kernel (default), or the direct-load one
+  // (FETIGPU3D_SOLVE=direct: one warp per off-diagonal block, 8 warps up to P = 8, else 32)
+  int solve_kind = -1;
   void interior_solve(double2* x) {
-    // one warp per off-diagonal block of a block row: 8 warps up to P = 8, else 32
+    if (solve_kind < 0) {
+      const char* e = std::getenv("FETIGPU3D_SOLVE");
+      solve_kind = (e && std::string(e) == "direct") ? 0 : 1;
+      if (solve_kind == 1) {
+        CU3(cudaFuncSetAttribute(k3::k3_bb_solve_tma<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)k3::bb_solve_tma_smem<8, 8>()));
+      }
+    }
     launch(FETIGPU_K_BAND, [&] {
-      if (PB <= 8)
+      if (solve_kind == 1) {
+        k3::k3_bb_solve_tma<8, 8><<<S, 288, k3::bb_solve_tma_smem<8, 8>(), stream>>>(NBK, PB, d_bb, NI, x);
+      } else if (PB <= 8) {
         k3::k3_bb_solve1<33, 8><<<S, 256, 0, stream>>>(NBK, PB, d_bb, NI, x);
-      else
+      } else {
         k3::k3_bb_solve1<33, 32><<<S, 1024, 0, stream>>>(NBK, PB, d_bb, NI, x);
+      }
     });
   }
   // (|x|^2, max|x|) -> host

@@ -18,6 +18,9 @@ namespace fetigpu {
 namespace k3 {
 
 __device__ __forceinline__ int tpos(int r, int c) { return (((c - r) & 31) << 5) | r; }
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // ---------------------------------------------------------------------------------------
 // Assembly (K1): one thread per (subdomain, local mesh dof) row; the row owner adds every
@@ -388,6 +391,131 @@ __global__ void __launch_bounds__(WARPS * 32) k3_bb_solve1(int NBK, int P, const
     }
     __syncthreads();
   }
+}
+
+// TMA-streamed variant of k3_bb_solve1: a producer warp streams every 16 KB block of the
+// substitution, in consumption order, through a STAGES-deep shared-memory ring (1-D bulk
+// copies, full/empty mbarrier pairs), so the block loads run ahead of the recurrence and the
+// bytes in flight no longer depend on the consumers' progress.  Item order: forward
+// K = 0..: the blocks (K, K-d), d = 1..min(P,K), then D_K^-1; backward K = NBK-1..0: the
+// blocks (K+d, K), d = 1..min(P, NBK-1-K).  Item j always goes to consumer warp j % W
+// (W divides STAGES), so every ring slot is waited on by one warp in phase order (a warp
+// never waits on round r+1 of a slot before round r completed — the parity would alias).
+// Each warp keeps a partial of the step; the warp that owns D_K^-1 closes the step.
+template <int STAGES, int W>
+__global__ void __launch_bounds__((W + 1) * 32, 1) k3_bb_solve_tma(int NBK, int P, const double2* __restrict__ bb,
+                                                                   int NI, double2* __restrict__ X) {
+  static_assert(STAGES % W == 0, "slot -> warp must be fixed");
+  extern __shared__ __align__(128) unsigned char k3t_raw[];
+  double2* ring = reinterpret_cast<double2*>(k3t_raw);                                    // [STAGES][1024]
+  double2 (*yr)[32] = reinterpret_cast<double2 (*)[32]>(ring + (size_t)STAGES * 1024);     // [33][32]
+  double2 (*part)[32] = yr + 33;                                                          // [W][32]
+  uint64_t* full = reinterpret_cast<uint64_t*>(part + W);
+  uint64_t* empty = full + STAGES;
+  const int s = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double2* band = bb + (size_t)s * NBK * (P + 1) * 1024;
+  double2* x = X + (size_t)s * NI;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < STAGES; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  constexpr uint32_t BYTES = 1024 * sizeof(double2);
+  if (warp == W) {  // ---- producer ----
+    if (lane == 0) {
+      long long i = 0;
+      auto issue = [&](const double2* src) {
+        const int st = (int)(i % STAGES);
+        const uint32_t round = (uint32_t)(i / STAGES);
+        if (round > 0) mbar_wait(&empty[st], (round - 1) & 1u);
+        mbar_arrive_expect_tx(&full[st], BYTES);
+        tma_load_1d(ring + (size_t)st * 1024, src, BYTES, &full[st]);
+        ++i;
+      };
+      for (int K = 0; K < NBK; ++K) {
+        for (int d = 1; d <= P && K - d >= 0; ++d) issue(band + ((size_t)K * (P + 1) + d) * 1024);
+        issue(band + ((size_t)K * (P + 1)) * 1024);
+      }
+      for (int K = NBK - 1; K >= 0; --K)
+        for (int d = 1; d <= P && K + d < NBK; ++d) issue(band + ((size_t)(K + d) * (P + 1) + d) * 1024);
+    }
+    return;
+  }
+  // ---- consumers ----
+  auto consume = [&](long long item) -> const double2* {
+    mbar_wait(&full[item % STAGES], (uint32_t)(item / STAGES) & 1u);
+    return ring + (size_t)(item % STAGES) * 1024;
+  };
+  auto release = [&](long long item) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[item % STAGES]);
+  };
+  // first item of this warp at or after `base`
+  auto first_mine = [&](long long base) { return base + (((long long)warp - base % W) % W + W) % W; };
+  long long base = 0;
+  for (int K = 0; K < NBK; ++K) {
+    const int nd = min(P, K);
+    double2 acc = cz();
+    for (long long it = first_mine(base); it < base + nd; it += W) {
+      const int d = (int)(it - base) + 1;
+      const double2* T = consume(it);
+      const double2* y = yr[(K - d) % 33];
+#pragma unroll 8
+      for (int cc = 0; cc < 32; ++cc) acc = cfma(T[cc * 32 + lane], y[(lane + cc) & 31], acc);
+      release(it);
+    }
+    part[warp][lane] = acc;
+    named_bar_sync(1, W * 32);
+    const long long itd = base + nd;  // D_K^-1: its warp closes the step
+    if (warp == (int)(itd % W)) {
+      double2 v = x[(size_t)K * 32 + lane];
+      for (int w = 0; w < W; ++w) v = csub(v, part[w][lane]);
+      yr[K % 33][lane] = v;
+      __syncwarp();
+      const double2* D = consume(itd);
+      double2 z = cz();
+#pragma unroll 8
+      for (int cc = 0; cc < 32; ++cc) z = cfma(D[cc * 32 + lane], yr[K % 33][(lane + cc) & 31], z);
+      release(itd);
+      x[(size_t)K * 32 + lane] = z;
+    }
+    named_bar_sync(1, W * 32);
+    base += nd + 1;
+  }
+  for (int K = NBK - 1; K >= 0; --K) {
+    const int nd = min(P, NBK - 1 - K);
+    double2 acc = cz();
+    for (long long it = first_mine(base); it < base + nd; it += W) {
+      const int d = (int)(it - base) + 1;
+      const double2* T = consume(it);
+      const double2 xr = yr[(K + d) % 33][lane];
+      double2 yc = cz();
+#pragma unroll 8
+      for (int cc = 0; cc < 32; ++cc) {
+        yc = cfma(T[cc * 32 + lane], xr, yc);
+        yc = shfl2(yc, (lane + 1) & 31);
+      }
+      acc = cadd(acc, yc);
+      release(it);
+    }
+    part[warp][lane] = acc;
+    named_bar_sync(1, W * 32);
+    if (warp == 0) {
+      double2 v = x[(size_t)K * 32 + lane];
+      for (int w = 0; w < W; ++w) v = csub(v, part[w][lane]);
+      yr[K % 33][lane] = v;
+      x[(size_t)K * 32 + lane] = v;
+    }
+    named_bar_sync(1, W * 32);
+    base += nd;
+  }
+}
+template <int STAGES, int W>
+constexpr size_t bb_solve_tma_smem() {
+  return sizeof(double2) * ((size_t)STAGES * 1024 + 33 * 32 + W * 32) + sizeof(uint64_t) * 2 * STAGES;
 }
 
 // ---------------------------------------------------------------------------------------
