@@ -138,6 +138,18 @@ struct Ctx {
   int vcap = 0;  // basis vectors allocated
   GmresState* d_gst = nullptr;
   GmresState* h_gst = nullptr;
+  // deferred completion (schur_solve on the one-GPU graph path): each FETI solve's GMRES
+  // cycle, solution update and true residual are only enqueued; the state and the norms
+  // are read after the Schur solve's single final synchronisation (pending[i], i = sb / 4),
+  // and a solve that would need a restart or the best-iterate fallback is re-run
+  // synchronously (never the case on the BASELINE configs)
+  bool async_ok = false;
+  GmresState* h_gst_async = nullptr;  // [2] pinned
+  struct Pending {
+    bool active = false;
+    int max_iter = 0;
+    double tol = 0;
+  } pending[2];
   double2 *d_R = nullptr, *d_gsin = nullptr, *d_gvec = nullptr;
   double* d_gcos = nullptr;
   unsigned int* d_counter = nullptr;
@@ -190,6 +202,7 @@ struct Ctx {
     if (h_pin) cudaFreeHost(h_pin);
     if (h_stat) cudaFreeHost(h_stat);
     if (h_gst) cudaFreeHost(h_gst);
+    if (h_gst_async) cudaFreeHost(h_gst_async);
     if (arnoldi_exec) cudaGraphExecDestroy(arnoldi_exec);
     if (arnoldi_graph) cudaGraphDestroy(arnoldi_graph);
     if (stream) cudaStreamDestroy(stream);
@@ -828,6 +841,7 @@ struct Ctx {
     d_counter = alloc<unsigned int>(4);
     zero(d_counter, 4);
     CU(cudaMallocHost(&h_gst, sizeof(GmresState)));
+    CU(cudaMallocHost(&h_gst_async, 4 * sizeof(GmresState)));  // [0,1] results, [2,3] initial states
     d_rhs = alloc<double2>(n);
     d_x = alloc<double2>(n);
     d_x2 = alloc<double2>(n);
@@ -1439,20 +1453,22 @@ struct Ctx {
     CU(cudaGraphInstantiate(&arnoldi_exec, arnoldi_graph, 0));
   }
 
-  fetigpu_feti_stats gmres(const double2* b, double2* x) {
+  fetigpu_feti_stats gmres(const double2* b, double2* x, int sb = 0) {
     fetigpu_feti_stats st{};
     const double tol = desc.tol;
     const int max_iter = desc.max_iter;
     zero(x, nl);
     const bool graph = use_graph && !prof && !dist();
     // with the fused step (each kernel returns once the cycle stopped) the first cycle starts
-    // from a device-side |b| (statistics slot 14): no host round trip before the graph
+    // from a device-side |b| (statistics slot bslot): no host round trip before the graph
     const bool dev_start = graph && tail_rpt > 0;
+    const bool deferred = dev_start && async_ok;
+    const int bslot = deferred ? 10 + sb / 4 : 14;
     double bnorm = 0.0;
     if (dev_start) {
       const int blocks = std::max(1, std::min(296, cdiv(std::max(nown, 1), 256)));
       launch(FETIGPU_K_ORTHO, [&] { k_norm_max_part<<<blocks, 256, 0, stream>>>(nown, b + own0, d_part); });
-      launch(FETIGPU_K_ORTHO, [&] { k_norm_max_final<<<1, 32, 0, stream>>>(blocks, d_part, d_stat + 14); });
+      launch(FETIGPU_K_ORTHO, [&] { k_norm_max_final<<<1, 32, 0, stream>>>(blocks, d_part, d_stat + bslot); });
     } else {
       bnorm = norm_max(b + own0, nown, true).first;
       if (bnorm == 0.0) {
@@ -1488,29 +1504,52 @@ struct Ctx {
       if (iterations >= max_iter) break;
       // new cycle: V_0 = r / |r|, g = |r| e_0
       if (dev_cycle)
-        launch(FETIGPU_K_ORTHO, [&] { k_scale_by_norm<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, d_stat + 14, d_V); });
+        launch(FETIGPU_K_ORTHO, [&] { k_scale_by_norm<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, d_stat + bslot, d_V); });
       else
         launch(FETIGPU_K_ORTHO, [&] { k_scale_copy<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, 1.0 / rnorm, d_V); });
       ghost_refresh(d_V);
-      *h_gst = GmresState{};
-      h_gst->j = 0;
-      h_gst->iterations = iterations;
-      h_gst->cont = 1;
-      h_gst->max_iter = max_iter;
-      h_gst->m = std::max(1, std::min(max_iter, vcap - 1));
-      h_gst->tol = tol;
-      h_gst->bnorm = bnorm;
-      CU(cudaMemcpyAsync(d_gst, h_gst, sizeof(GmresState), cudaMemcpyHostToDevice, stream));
+      // (deferred: a pinned staging slot of its own, the copy may run after the host moved on)
+      GmresState* init = deferred ? h_gst_async + 2 + sb / 4 : h_gst;
+      *init = GmresState{};
+      init->j = 0;
+      init->iterations = iterations;
+      init->cont = 1;
+      init->max_iter = max_iter;
+      init->m = std::max(1, std::min(max_iter, vcap - 1));
+      init->tol = tol;
+      init->bnorm = bnorm;
+      if (!deferred) *h_gst = *init;
+      CU(cudaMemcpyAsync(d_gst, init, sizeof(GmresState), cudaMemcpyHostToDevice, stream));
       if (dev_cycle) {
-        launch(FETIGPU_K_ORTHO, [&] { k_gmres_init<<<1, 32, 0, stream>>>(d_gst, d_stat + 14, d_gvec); });
+        launch(FETIGPU_K_ORTHO, [&] { k_gmres_init<<<1, 32, 0, stream>>>(d_gst, d_stat + bslot, d_gvec); });
       } else {
         h_pin[0] = make_double2(rnorm, 0.0);
         CU(cudaMemcpyAsync(d_gvec, h_pin, sizeof(double2), cudaMemcpyHostToDevice, stream));
       }
+      if (deferred) {
+        // the whole first cycle, the update x += P^-1 (Q y) and the true residual are only
+        // enqueued; finish_deferred() reads them after the caller's final synchronisation
+        CU(cudaGraphLaunch(arnoldi_exec, stream));
+        launch(FETIGPU_K_ORTHO, [&] { k_backsub<<<1, 32, 0, stream>>>(d_gst, d_R, d_gvec, d_y); });
+        launch(FETIGPU_K_ORTHO, [&] {
+          k_combine<64, 4><<<cdiv(nown, 64), 256, 0, stream>>>(nown, d_V + own0, ldv, d_gst, d_y, d_t + own0);
+        });
+        apply_precond(d_t, d_zl);
+        launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nown, 256), 256, 0, stream>>>(nown, x + own0, d_zl + own0); });
+        apply_dual(x, d_w);
+        project_aug(d_w);
+        launch(FETIGPU_K_ORTHO, [&] { k_sub<<<cdiv(nown, 256), 256, 0, stream>>>(nown, b + own0, d_w + own0, d_r + own0); });
+        norm_async(d_r + own0, nown, 12 + sb / 4);
+        CU(cudaMemcpyAsync(h_gst_async + sb / 4, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
+        pending[sb / 4].active = true;
+        pending[sb / 4].max_iter = max_iter;
+        pending[sb / 4].tol = tol;
+        return st;  // iterations / residual filled in by finish_deferred
+      }
       if (graph) {
         CU(cudaGraphLaunch(arnoldi_exec, stream));
         CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
-        if (dev_cycle) CU(cudaMemcpyAsync(h_pin + 1, d_stat + 14, sizeof(double2), cudaMemcpyDeviceToHost, stream));
+        if (dev_cycle) CU(cudaMemcpyAsync(h_pin + 1, d_stat + bslot, sizeof(double2), cudaMemcpyDeviceToHost, stream));
         if (watchdog) {  // debugging aid: report a stuck Arnoldi graph
           auto t0 = std::chrono::steady_clock::now();
           while (cudaStreamQuery(stream) == cudaErrorNotReady) {
@@ -1619,7 +1658,7 @@ struct Ctx {
     // their orthogonal complement (feti.cpp:655-662)
     project_aug(d_d);
     phase("jump");
-    const fetigpu_feti_stats gst = gmres(d_d, d_lam);
+    const fetigpu_feti_stats gst = gmres(d_d, d_lam, sb);
     phase("gmres");
     ghost_refresh(d_lam);
     st.iterations = gst.iterations;
@@ -1686,6 +1725,34 @@ struct Ctx {
     return st;
   }
 
+  // After the final synchronisation: the deferred GMRES results of FETI solve i (sb = 4 i).
+  // Returns false when the solve would have needed a restart cycle or the best-iterate
+  // fallback of krylov.hpp:214-220 (then the caller re-runs synchronously).
+  bool finish_deferred(fetigpu_feti_stats& st, int sb) {
+    Pending& pd = pending[sb / 4];
+    if (!pd.active) return true;
+    pd.active = false;
+    const GmresState& g = h_gst_async[sb / 4];
+    if (g.status) throw NumericalError("gmres: breakdown (NaN/Inf in Arnoldi)");
+    const double bnorm = std::sqrt(h_stat[10 + sb / 4].x);
+    if (bnorm == 0.0) {  // zero rhs: zero solution in 0 iterations (feti.cpp:640-644)
+      st.iterations = 0;
+      st.relative_residual = 0.0;
+      st.converged = 1;
+      last_gmres_steps = 0;
+      return true;
+    }
+    const double rel = std::sqrt(h_stat[12 + sb / 4].x) / bnorm;
+    if (rel > 1.0) return false;                                  // best iterate would be x = 0
+    if (rel > pd.tol && g.iterations < pd.max_iter) return false;  // would restart
+    st.iterations = g.iterations;
+    st.relative_residual = rel;
+    st.converged = rel <= pd.tol;
+    last_gmres_steps = g.iterations;
+    launches += (long long)arnoldi_body_kernels * body_unroll * std::max(1, (g.iterations + body_unroll - 1) / body_unroll);
+    return true;
+  }
+
   // ------------------------------------------------------------------------ range space
   // solve_range_space (control.cpp:297-334) on device buffers.
   // host_y/u/lam (host API): results are copied out inside the call — lambda and u on the
@@ -1693,6 +1760,20 @@ struct Ctx {
   void schur_solve(const double* ybar, const double* yc, double* y, double* u, double* lam,
                    fetigpu_schur_stats* out, double* host_y = nullptr, double* host_u = nullptr,
                    double* host_lam = nullptr) {
+    async_ok = !std::getenv("FETIGPU_NO_DEFER");
+    bool ok = false;
+    try {
+      ok = schur_solve_once(ybar, yc, y, u, lam, out, host_y, host_u, host_lam);
+    } catch (...) {
+      async_ok = false;
+      pending[0].active = pending[1].active = false;
+      throw;
+    }
+    async_ok = false;
+    if (!ok) schur_solve_once(ybar, yc, y, u, lam, out, host_y, host_u, host_lam);  // synchronous re-run
+  }
+  bool schur_solve_once(const double* ybar, const double* yc, double* y, double* u, double* lam,
+                        fetigpu_schur_stats* out, double* host_y, double* host_u, double* host_lam) {
     auto t0 = std::chrono::steady_clock::now();
     // rhs = K ybar + Kc yc  (control.cpp:15)
     apply_global<double>(ybar, (yc && m > 0) ? yc : nullptr, 1.0, 0.0, d_real0);
@@ -1736,6 +1817,10 @@ struct Ctx {
     sync();  // the call's one final synchronisation
     phase_report();
     if (host_lam != nullptr) CU(cudaStreamSynchronize(copy_stream));
+    if (!finish_deferred(sp, 0) || !finish_deferred(sm, 4)) {
+      pending[0].active = pending[1].active = false;
+      return false;
+    }
     finalize_feti_stats(sp, 0);
     finalize_feti_stats(sm, 4);
     const double lmax = h_stat[9].y, leak = h_stat[8].y;
@@ -1748,6 +1833,7 @@ struct Ctx {
       out->factor_setup_seconds = setup_seconds;
       out->solve_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
+    return true;
   }
 
   double class_bytes(int klass) const {
