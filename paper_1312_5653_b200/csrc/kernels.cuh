@@ -1360,15 +1360,46 @@ __device__ __forceinline__ double warp_hnext(const double2* h1, const double2* h
   finite = fin && isfinite(hnext);
   return hnext;
 }
+// Operands of a Givens step that are known before the Arnoldi step's reductions (the fused
+// tail loads them at its start, off the critical path): the state scalars, g_j and, when
+// j <= 256, the previous rotations already staged in sc / ss.
+struct GivensPre {
+  int j, iterations, max_iter, m;
+  double tol, bnorm;
+  double2 gj;
+  int staged;
+};
+// block 0, warp 0 of the fused tail: fill GivensPre and the rotation staging
+__device__ __forceinline__ void givens_prefetch(const GivensArgs& a, GivensPre* pre, double* sc, double2* ss) {
+  const int lane = threadIdx.x & 31;
+  const GmresState* st = a.st;
+  const int j = st->j;
+  const bool staged = j <= 256;
+  if (staged)
+    for (int q = lane; q < j; q += 32) {
+      sc[q] = a.gcos[q];
+      ss[q] = a.gsin[q];
+    }
+  if (lane == 0) {
+    pre->j = j;
+    pre->iterations = st->iterations;
+    pre->max_iter = st->max_iter;
+    pre->m = st->m;
+    pre->tol = st->tol;
+    pre->bnorm = st->bnorm;
+    pre->gj = a.g[j];
+    pre->staged = staged ? 1 : 0;
+  }
+}
 template <bool SMEM = false>
 __device__ void givens_warp(const GivensArgs& a, double* sc, double2* ss, double2* sh, const double2* h1 = nullptr,
-                            const double2* h2 = nullptr) {
+                            const double2* h2 = nullptr, const GivensPre* pre = nullptr) {
   constexpr int CHK = 256;
   const int lane = threadIdx.x & 31;
   if (h1 == nullptr) h1 = a.h1;
   if (h2 == nullptr) h2 = a.h2;
   GmresState* st = a.st;
-  const int j = st->j;
+  const int j = pre ? pre->j : st->j;
   double2* col = a.R + (size_t)j * (j + 1) / 2;
   bool finite;
   const double hnext = warp_hnext<SMEM>(h1, h2, j, finite);
@@ -1385,9 +1416,12 @@ __device__ void givens_warp(const GivensArgs& a, double* sc, double2* ss, double
   double2 carry = cadd(ldh<SMEM>(h1), ldh<SMEM>(h2));
   for (int base = 0; base < j; base += CHK) {
     const int cnt = min(CHK, j - base);
+    const bool have = pre != nullptr && pre->staged;  // (staged only when j <= CHK)
     for (int q = lane; q < cnt; q += 32) {
-      sc[q] = a.gcos[base + q];
-      ss[q] = a.gsin[base + q];
+      if (!have) {
+        sc[q] = a.gcos[base + q];
+        ss[q] = a.gsin[base + q];
+      }
       sh[q] = cadd(ldh<SMEM>(h1 + base + q + 1), ldh<SMEM>(h2 + base + q + 1));
     }
     __syncwarp();
@@ -1421,16 +1455,19 @@ __device__ void givens_warp(const GivensArgs& a, double* sc, double2* ss, double
   a.gcos[j] = c;
   a.gsin[j] = s;
   col[j] = cfma(s, make_double2(hnext, 0.0), cscale(x, c));
-  const double2 gj = a.g[j];
-  a.g[j + 1] = cmul(make_double2(-s.x, s.y), gj);  // -conj(s) g_j
+  const double2 gj = pre ? pre->gj : a.g[j];
+  const double2 gj1 = cmul(make_double2(-s.x, s.y), gj);  // -conj(s) g_j
+  a.g[j + 1] = gj1;
   a.g[j] = cscale(gj, c);
-  const int iters = st->iterations + 1;
+  const int iters = (pre ? pre->iterations : st->iterations) + 1;
   st->iterations = iters;
   st->k = j + 1;
-  const double est = sqrt(cabs2(a.g[j + 1]));
+  const double est = sqrt(cabs2(gj1));
   st->est = est;
   const bool happy = hnext <= 1e-14 * fmax(wpre, 1e-300);
-  const int cont = !(happy || est <= st->tol * st->bnorm) && iters < st->max_iter && (j + 1) < st->m;
+  const double tol = pre ? pre->tol : st->tol, bnorm = pre ? pre->bnorm : st->bnorm;
+  const int max_iter = pre ? pre->max_iter : st->max_iter, m = pre ? pre->m : st->m;
+  const int cont = !(happy || est <= tol * bnorm) && iters < max_iter && (j + 1) < m;
   if (cont) {
     st->inv_hnext = 1.0 / hnext;
     st->j = j + 1;
@@ -1907,6 +1944,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   const int nv = a.st->j + 1, nout = nv + 1, G = gridDim.x;
   const int it = a.st->iterations;
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 0] = gtimer();
+  // Givens operands known now (block 0): loaded during the coarse phase, off the critical path
+  __shared__ GivensPre gpre;
+  if (!GRAM && blockIdx.x == 0 && warp == 0)
+    givens_prefetch(a.ga, &gpre, reinterpret_cast<double*>(stage), stage + 128);
   span_mark(a.span, &it, 2, 0);
   // dual-tail operands that do not depend on z (loaded before the barrier)
   double2 u[2] = {cz(), cz()}, cpv[2][NCM];
@@ -2122,7 +2163,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
       a.h1[i] = hs1[i];
       a.h2[i] = hs2[i];
     }
-    if (warp == 0) givens_warp<true>(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384, hs1, hs2);
+    if (warp == 0)
+      givens_warp<true>(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384, hs1, hs2, &gpre);
     if (a.tstamp && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 9] = gtimer();
   }
   if (a.span != nullptr) {

@@ -1,5 +1,5 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_v13.json 2> gpurun_out/bench_v13.err; echo "bench rc=$?" >> gpurun_out/bench_v13.err
-FETIGPU_NO_DEFER=1 timeout 900 python bench.py --no-cpu-baseline --no-sweep --steps 20 > gpurun_out/bench_v13_nodefer.json 2>&1
+timeout 900 python bench.py --no-cpu-baseline --no-sweep > gpurun_out/bench_v14.json 2> gpurun_out/bench_v14.err; echo "bench rc=$?" >> gpurun_out/bench_v14.err
+FETIGPU_TAIL_TIMES=1 timeout 300 python tools/profile_step.py > gpurun_out/tail_times.log 2>&1
