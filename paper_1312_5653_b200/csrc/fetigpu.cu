@@ -830,7 +830,9 @@ struct Ctx {
       d_span = alloc<unsigned long long>((size_t)6 * (vcap_hint() + 2));
       print_spans = std::getenv("FETIGPU_STEP_TIMES") != nullptr;
     }
-    d_part = alloc<double2>((size_t)(vcap + 2) * std::max(mdot_blocks, 2 * tail_grid));  // tail: 2 halves
+    // tail: 2 halves; also the per-block partials of the primal-residual stencil reduction
+    d_part = alloc<double2>(std::max((size_t)(vcap + 2) * std::max(mdot_blocks, 2 * tail_grid),
+                                     (size_t)cdiv(std::max(P.nx - 1, 1), 256) * std::max(P.ny - 1, 1) + 64));
     d_red = alloc<double2>(3 * (vcap + 2));
     d_y = alloc<double2>(vcap + 2);
     d_gst = alloc<GmresState>(1);
@@ -1699,11 +1701,13 @@ struct Ctx {
     if (stencil_ok) {
       Stencil9 S9;
       for (int q = 0; q < 9; ++q) S9.c[q] = d2(cd(1.0) * st_k[q] + mc * st_m[q]);
-      const int blocks = std::max(1, std::min(296, cdiv(n, 256)));
+      const dim3 grid(cdiv(P.nx - 1, 256), P.ny - 1);
       launch(FETIGPU_K_OTHER, [&] {
-        k_stencil_residual_part<<<blocks, 256, 0, stream>>>(P.nx - 1, P.ny - 1, S9, x, rhs, d_part);
+        k_stencil_residual_part<<<grid, 256, 0, stream>>>(P.nx - 1, P.ny - 1, S9, x, rhs, d_part);
       });
-      launch(FETIGPU_K_OTHER, [&] { k_norm_max_final<<<1, 32, 0, stream>>>(blocks, d_part, d_stat + sb + 2); });
+      launch(FETIGPU_K_OTHER, [&] {
+        k_norm_max_final<<<1, 32, 0, stream>>>((int)(grid.x * grid.y), d_part, d_stat + sb + 2);
+      });
     } else {
       apply_global<double2>(x, nullptr, 1.0, mc, d_ax);
       launch(FETIGPU_K_GLOBAL, [&] { k_sub<<<cdiv(n, 256), 256, 0, stream>>>(n, d_ax, rhs, d_ax); });

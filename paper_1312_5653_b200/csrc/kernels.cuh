@@ -2371,9 +2371,10 @@ __global__ void k_jump_norm_part(int nl, const int* __restrict__ lo, const int* 
 __global__ void k_stencil_residual_part(int fx, int fy, Stencil9 S, const double2* __restrict__ x,
                                         const double2* __restrict__ rhs, double2* __restrict__ part) {
   double s = 0.0, m = 0.0;
-  const long long total = (long long)fx * fy;
-  for (long long f = (long long)blockIdx.x * blockDim.x + threadIdx.x; f < total; f += (long long)gridDim.x * blockDim.x) {
-    const int I = (int)(f % fx), J = (int)(f / fx);
+  // one row per blockIdx.y, one column per thread: every load of the launch in flight at once
+  const int J = blockIdx.y, I = blockIdx.x * blockDim.x + threadIdx.x;
+  if (I < fx) {
+    const size_t f = (size_t)J * fx + I;
     double2 acc = cz();
 #pragma unroll
     for (int dy = -1; dy <= 1; ++dy) {
@@ -2390,7 +2391,7 @@ __global__ void k_stencil_residual_part(int fx, int fy, Stencil9 S, const double
     s += a2;
     m = fmax(m, sqrt(a2));
   }
-  block_sum_max(s, m, part);
+  block_sum_max(s, m, part + (size_t)blockIdx.y * gridDim.x);
 }
 
 // Kronecker mass solve V^-1 = (M_y ⊗ M_x ⊗ I_dpn)^-1: batches of identical SPD tridiagonal
