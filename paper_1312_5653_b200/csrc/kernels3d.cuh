@@ -1443,6 +1443,38 @@ __global__ void k3_apply_global(Glob3 g, const T* __restrict__ x, const double* 
   from_c<T>(y + f, acc);
 }
 
+// y = S x with a constant 27-point stencil on the Lx x Ly x Lz grid of interior nodes
+// (free dofs in lexicographic order, zero outside): heat with whole-boundary Dirichlet.
+// The stencil entries are the element sums of the element matrix at an interior node, so
+// this equals the element-by-element apply up to the order of the additions.
+struct Stencil27 {
+  double2 c[27];
+};
+template <typename T>
+__global__ void k3_apply_stencil27(int Lx, int Ly, int Lz, Stencil27 S, const T* __restrict__ x, T* __restrict__ y) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x, j = blockIdx.y, k = blockIdx.z;
+  if (i >= Lx) return;
+  double2 acc = cz();
+#pragma unroll
+  for (int dz = -1; dz <= 1; ++dz) {
+    const int kk = k + dz;
+    if (kk < 0 || kk >= Lz) continue;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int jj = j + dy;
+      if (jj < 0 || jj >= Ly) continue;
+      const T* row = x + ((size_t)kk * Ly + jj) * Lx;
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int ii = i + dx;
+        if (ii < 0 || ii >= Lx) continue;
+        acc = cfma(S.c[((dz + 1) * 3 + (dy + 1)) * 3 + dx + 1], to_c<T>(row[ii]), acc);
+      }
+    }
+  }
+  from_c<T>(y + ((size_t)k * Ly + j) * Lx + i, acc);
+}
+
 // V^-1 v in place for V = M_z (x) M_y (x) M_x (x) I_dpn: Thomas along lines, one thread per
 // line; line l starts at (l / G) * S1 + (l % G) * S2, element stride es
 __global__ void k3_tridiag(double* __restrict__ v, int nlines, int len, int G, long long S1, long long S2,
