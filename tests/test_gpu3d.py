@@ -118,6 +118,24 @@ def test_gpu3d_schur_solve_with_dirichlet_data(fetigpu, oracle_mod, physics):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("physics,mass_coeff", [(0, 100.0), (1, 10.0 + 5.0j)])
+def test_gpu3d_feti_solve_mass_coeff(fetigpu, oracle_mod, physics, mass_coeff):
+    """feti_solve with an explicit mass coefficient (python feti_solve, bindings.cpp:158-185),
+    e.g. the real Pearson-Wathen factor K + V / sqrt(phi)."""
+    from paper_1312_5653_b200 import box
+
+    n, s = 12, 3
+    p = box.make_box_problem(n, phi=1e-4, physics=physics, young=1.0, poisson=0.3, seed=6)
+    q = oracle_mod.Problem(n, n, n_z=n, physics=physics, young=1.0, poisson=0.3)
+    rhs = np.random.default_rng(11).standard_normal(p.n).astype(complex)
+    x, st = box.feti_solve_3d(p, mass_coeff, rhs, s, tol=1e-10, max_iter=500)
+    xr, sr = oracle_mod.Feti(q, s, s, mass_coeff, s_z=s, tol=1e-10, max_iter=500).solve(rhs)
+    assert st["converged"] and sr["converged"]
+    assert rel(x, xr) <= 1e-8
+    assert abs(st["iterations"] - sr["iterations"]) <= 2
+
+
+@pytest.mark.gpu
 def test_gpu3d_zero_rhs_and_contracts(fetigpu):
     from paper_1312_5653_b200 import ContractError, box
 
