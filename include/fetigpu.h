@@ -156,6 +156,10 @@ int fetigpu_nccl_unique_id(unsigned char* out128);
 int fetigpu_create_sharded(const fetigpu_desc* desc, int rank, int world, const unsigned char* nccl_id,
                            fetigpu_ctx** out);
 
+/* NCCL plumbing self-test: communicator init, allreduce sum/max and allgatherv on
+ * [rank+1, 2(rank+1), -(rank+1), 0] -> out4 (every rank of `world` calls it). */
+int fetigpu_nccl_selftest(const unsigned char* nccl_id, int rank, int world, int device, double* out4);
+
 /* Host-only layout of rank `rank` (for tests): info[0..11] = first subdomain, local
  * subdomains, phantom subdomains, first local multiplier (global id), ghost rows, owned
  * rows, top-cut rows, first owned free dof, owned free dofs, halo slots sent up, halo

@@ -91,6 +91,7 @@ def lib():
     L.fetigpu_nccl_unique_id.argtypes = [C.c_char_p]
     L.fetigpu_create_sharded.argtypes = [pdesc, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]
     L.fetigpu_rank_info.argtypes = [pdesc, C.c_int, C.c_int, ip]
+    L.fetigpu_nccl_selftest.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, dp]
     L.fetigpu_emulated_schur_solve.argtypes = [pdesc, C.c_int, dp, dp, dp, dp, dp, C.POINTER(SchurStats)]
     L.fetigpu_step_spans.argtypes = [vp, dp]
     L.fetigpu_pressure_load.argtypes = [pdesc, C.c_double, dp]
@@ -132,6 +133,7 @@ EXPORTED_SYMBOLS = (
     "fetigpu_profile", "fetigpu_profile_read", "fetigpu_class_bytes", "fetigpu_last_error",
     "fetigpu_nccl_unique_id", "fetigpu_create_sharded", "fetigpu_rank_info", "fetigpu_emulated_schur_solve",
     "fetigpu_step_spans", "fetigpu_full_space", "fetigpu_pressure_load", "fetigpu_diagnostics",
+    "fetigpu_nccl_selftest",
     "fetigpu3d_problem_info", "fetigpu3d_target_sine", "fetigpu3d_create", "fetigpu3d_destroy",
     "fetigpu3d_schur_solve", "fetigpu3d_schur_solve_device", "fetigpu3d_feti_solve", "fetigpu3d_apply_dual",
     "fetigpu3d_apply_precond", "fetigpu3d_stream", "fetigpu3d_launch_count", "fetigpu3d_profile",

@@ -2135,6 +2135,32 @@ int fetigpu_create_sharded(const fetigpu_desc* desc, int rank, int world, const 
   });
 }
 
+// NCCL plumbing self-test (no solver): communicator init, allreduce sum / max and the
+// grouped-broadcast allgatherv on a 4-double device buffer [rank+1, 2(rank+1), -(rank+1), 0]
+int fetigpu_nccl_selftest(const unsigned char* nccl_id, int rank, int world, int device, double* out4) {
+  return guard([&] {
+    if (!nccl_id) throw ContractError("fetigpu_nccl_selftest: nccl_id required");
+    auto comm = make_nccl_comm(nccl_id, rank, world, device);
+    cudaStream_t st;
+    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    double* d = nullptr;
+    CU(cudaMalloc(&d, 4 * sizeof(double)));
+    const double r = rank + 1.0;
+    const double h[4] = {r, 2.0 * r, -r, 0.0};
+    CU(cudaMemcpyAsync(d, h, sizeof(h), cudaMemcpyHostToDevice, st));
+    comm->allreduce_sum(d, 2, st);
+    comm->allreduce_max(d + 2, 1, st);
+    std::vector<size_t> first(world), count(world, 0);
+    for (int q = 0; q < world; ++q) first[q] = 3;
+    count[0] = 1;  // rank 0's entry 3 replicated everywhere
+    comm->allgatherv(d, first, count, st);
+    CU(cudaMemcpyAsync(out4, d, 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    cudaFree(d);
+    cudaStreamDestroy(st);
+  });
+}
+
 int fetigpu_rank_info(const fetigpu_desc* desc, int rank, int world, int* info) {
   return guard([&] {
     validate_desc(desc);

@@ -1495,27 +1495,28 @@ __global__ void k3_tridiag(double* __restrict__ v, int nlines, int len, int G, l
 
 // ---------------------------------------------------------------------------------------
 // Krylov vector kernels (K7)
-// part[b][j] = sum_{rows of block b} conj(V_j) w  (j < nv), plus |w|^2 in slot nv
+// part[b][j] = sum_{rows of block b} conj(V_j) w  (j < nv), plus |w|^2 in slot nv.
+// The block's rows of w are staged in shared memory once; warp q then takes the vectors
+// j = q, q + 8, ... (coalesced loads of V_j), so all dots of the block run concurrently.
+// rows_pb <= 2048 (32 KB of staging).
 __global__ void __launch_bounds__(256) k3_mdot_part(int n, int nv, const double2* __restrict__ V, size_t ldv,
                                                     const double2* __restrict__ w, double2* __restrict__ part, int rows_pb) {
-  __shared__ double2 red[8];
-  const int r0 = blockIdx.x * rows_pb, r1 = min(n, r0 + rows_pb);
+  __shared__ double2 ws[2048];
+  const int r0 = blockIdx.x * rows_pb, cnt = min(n, r0 + rows_pb) - r0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = 0; j <= nv; ++j) {
+  for (int q = threadIdx.x; q < cnt; q += blockDim.x) ws[q] = w[r0 + q];
+  __syncthreads();
+  for (int j = warp; j <= nv; j += 8) {
     double2 acc = cz();
-    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-      const double2 wv = w[r];
-      acc = j < nv ? cfma_conj(V[(size_t)j * ldv + r], wv, acc) : make_double2(acc.x + cabs2(wv), 0.0);
+    if (j < nv) {
+      const double2* v = V + (size_t)j * ldv + r0;
+#pragma unroll 4
+      for (int q = lane; q < cnt; q += 32) acc = cfma_conj(v[q], ws[q], acc);
+    } else {
+      for (int q = lane; q < cnt; q += 32) acc.x += cabs2(ws[q]);
     }
     acc = warp_sum2(acc);
-    if (lane == 0) red[warp] = acc;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double2 t = cz();
-      for (int q = 0; q < 8; ++q) t = cadd(t, red[q]);
-      part[(size_t)blockIdx.x * (nv + 1) + j] = t;
-    }
-    __syncthreads();
+    if (lane == 0) part[(size_t)blockIdx.x * (nv + 1) + j] = acc;
   }
 }
 // one warp per dot: lanes stride over the block partials, fixed-order butterfly

@@ -155,3 +155,18 @@ def test_emulated_sharded_solve_matches_single_gpu(fetigpu, case):
         assert rel(out[k], ref[k]) <= 1e-8, k
     for side in ("plus_stats", "minus_stats"):
         assert abs(out[side]["iterations"] - ref[side]["iterations"]) <= 2
+
+
+@pytest.mark.gpu
+def test_nccl_plumbing_one_rank(fetigpu):
+    """The NCCL communicator of the sharded paths initialises and runs its collectives on
+    the box (one rank: the results equal the inputs).  Multi-rank NCCL needs several GPUs."""
+    import ctypes as C
+
+    from paper_1312_5653_b200 import _native
+
+    uid = fetigpu.nccl_unique_id()
+    out = np.zeros(4)
+    rc = _native.lib().fetigpu_nccl_selftest(bytes(uid), 0, 1, 0, out.ctypes.data_as(C.POINTER(C.c_double)))
+    assert rc == 0, _native.lib().fetigpu_last_error()
+    assert out.tolist() == [1.0, 2.0, -1.0, 0.0]
