@@ -136,6 +136,31 @@ def test_gpu3d_feti_solve_mass_coeff(fetigpu, oracle_mod, physics, mass_coeff):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("physics,grid", [(0, (1, 1, 2)), (0, (2, 1, 1)), (1, (2, 1, 1)), (0, (3, 2, 1))])
+def test_gpu3d_anisotropic_subdomain_grids(fetigpu, oracle_mod, physics, grid):
+    """Slab partitions (1 x 1 x 2 heat: no corner at all, the coarse problem is empty) and
+    anisotropic subdomain grids against the oracle."""
+    from paper_1312_5653_b200 import box
+
+    n, phi = 12, 1e-4
+    sx, sy, sz = grid
+    p = box.make_box_problem(n, phi=phi, physics=physics, young=1.0, poisson=0.3, seed=8)
+    q = oracle_mod.Problem(n, n, n_z=n, physics=physics, young=1.0, poisson=0.3)
+    solver = box.BoxSchurSolver(p, sx, sy, sz, tol=1e-10, max_iter=500)
+    try:
+        r = solver.solve()
+        nc = solver.coarse_dim
+    finally:
+        solver.close()
+    o = q.schur_solve(sx, sy, phi, p.target_state, s_z=sz, tol=1e-10, max_iter=500)
+    if grid == (1, 1, 2) and physics == 0:
+        assert nc == 0
+    for k in ("y", "u", "lambda"):
+        assert rel(r[k], o[k]) <= 1e-8, k
+    assert abs(r["plus_stats"]["iterations"] - o["plus_stats"]["iterations"]) <= 2
+
+
+@pytest.mark.gpu
 def test_gpu3d_zero_rhs_and_contracts(fetigpu):
     from paper_1312_5653_b200 import ContractError, box
 
