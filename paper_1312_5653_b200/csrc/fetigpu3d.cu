@@ -110,6 +110,8 @@ struct Ctx3 {
   double2 *d_fi = nullptr, *d_fb = nullptr, *d_fc = nullptr, *d_yi = nullptr, *d_ri = nullptr, *d_gcp = nullptr;
   double2 *d_g = nullptr, *d_z = nullptr, *d_tb = nullptr;
   double2 *d_V = nullptr, *d_w = nullptr, *d_zl = nullptr, *d_r = nullptr, *d_lam = nullptr, *d_best = nullptr;
+  double2* d_Z = nullptr;  // preconditioned basis M V_j (the solution update is Z y)
+  double2 *d_u0 = nullptr, *d_gcp0 = nullptr;  // first elimination's S^-1 (f_b - A_bi y_i) and coarse terms
   double2 *d_d = nullptr, *d_t = nullptr, *d_h = nullptr, *d_part = nullptr, *d_red = nullptr, *d_coef = nullptr;
   double2 *d_rhs = nullptr, *d_x = nullptr, *d_x2 = nullptr, *d_ax = nullptr;
   double *d_real0 = nullptr, *d_real1 = nullptr, *d_in_ybar = nullptr, *d_in_yc = nullptr, *d_out_y = nullptr,
@@ -494,6 +496,9 @@ struct Ctx3 {
     ldv = ((size_t)nl + 63) / 64 * 64;
     vcap = std::max(2, desc.max_iter + 1);
     d_V = alloc<double2>(ldv * vcap);
+    d_Z = alloc<double2>(ldv * vcap);
+    d_u0 = alloc<double2>((size_t)S * NB);
+    d_gcp0 = alloc<double2>((size_t)S * G * NC);
     for (double2** p : {&d_w, &d_zl, &d_r, &d_lam, &d_best, &d_d, &d_t}) *p = alloc<double2>(ldv);
     mdot_rows = 2048;
     mdot_blocks = std::max(1, cdiv3(nl, mdot_rows));
@@ -713,16 +718,18 @@ struct Ctx3 {
   // eliminate (feti.cpp:516-556) for t = [f_i ; tb]: u1_b = S^-1 (tb - A_bi y_i) with y_i =
   // A_ii^-1 f_i (computed once per FETI solve), g = f_c - (cpl_i^T f_i + cpl_b^T tb),
   // z = C^-1 g, u_b = u1_b - cpl_b z  -> d_u1
-  void eliminate_boundary(const double2* tb) {
+  void eliminate_boundary(const double2* tb, bool save = false) {
     launch(FETIGPU_K_OTHER, [&] {
       k3::k3_tb_minus<<<cdiv3((long long)S * NB, 256), 256, 0, stream>>>(S, NB, NI, H.MAXE_BI, d_bi_idx, d_bi_val,
                                                                         d_yi, tb, d_xin);
     });
     sym_gemv(d_Sip, d_xin, d_u1, FETIGPU_K_OTHER);
+    if (save) CU3(cudaMemcpyAsync(d_u0, d_u1, sizeof(double2) * S * NB, cudaMemcpyDeviceToDevice, stream));
     if (nc > 0) {
       launch(FETIGPU_K_COARSE, [&] {
         k3::k3_gcp<<<dim3(S, G), 256, 0, stream>>>(NB, NC, NI, G, d_cpl_b, tb, d_cpl_i, d_fi, d_gcp);
       });
+      if (save) CU3(cudaMemcpyAsync(d_gcp0, d_gcp, sizeof(double2) * S * G * NC, cudaMemcpyDeviceToDevice, stream));
       coarse_solve(d_fc);
       launch(FETIGPU_K_OTHER, [&] {
         k3::k3_ub_correct<<<cdiv3((long long)S * NB, 256), 256, 0, stream>>>(S, NB, NC, d_cglob, d_z, d_cpl_b, d_u1);
@@ -777,6 +784,7 @@ struct Ctx3 {
     int iterations = 0;
     bool converged = false;
     double relres = 0;
+    bool dual_of_x = false;  // d_u1 / d_gcp hold S^-1(-B^T x) / its coarse terms for the returned x
   };
   Stats gmres(const double2* b, double2* x, int max_iter, double tol) {
     Stats st;
@@ -821,8 +829,9 @@ struct Ctx3 {
       int k = 0;
       for (int j = 0; j < mres && st.iterations < max_iter; ++j) {
         double2* vj = d_V + (size_t)j * ldv;
-        apply_precond(vj, d_zl);
-        apply_dual(d_zl, d_w);
+        double2* zj = d_Z + (size_t)j * ldv;
+        apply_precond(vj, zj);
+        apply_dual(zj, d_w);
         // CGS2: h1 = V^H w (+|w|^2), w -= V h1, h2 = V^H w, w -= V h2, |w|
         double2* h1 = d_h;
         double2* h2 = d_h + (vcap + 2);
@@ -887,13 +896,11 @@ struct Ctx3 {
       }
       for (int i = 0; i < k; ++i) h_pin[i] = dd2(y[i]);
       CU3(cudaMemcpyAsync(d_coef, h_pin, sizeof(double2) * std::max(k, 1), cudaMemcpyHostToDevice, stream));
-      zero(d_t, nl);
-      launch(FETIGPU_K_ORTHO, [&] { k3::k3_mcombine<<<nb, 256, 0, stream>>>(nl, k, d_V, ldv, d_coef, d_t); });
-      apply_precond(d_t, d_zl);
-      launch(FETIGPU_K_ORTHO, [&] {
-        k3::k3_axpby<<<nb, 256, 0, stream>>>(nl, make_double2(1.0, 0.0), d_zl, make_double2(1.0, 0.0), x);
-      });
+      // x += P^-1 (V y) = Z y (the preconditioned basis of the cycle; linear, so equal up to
+      // rounding, and one Dirichlet application cheaper), true residual r = b - F x
+      launch(FETIGPU_K_ORTHO, [&] { k3::k3_mcombine<<<nb, 256, 0, stream>>>(nl, k, d_Z, ldv, d_coef, x); });
       apply_dual(x, d_w);
+      st.dual_of_x = true;
       launch(FETIGPU_K_ORTHO, [&] { k3::k3_sub<<<nb, 256, 0, stream>>>(nl, b, d_w, d_r); });
     }
     // final true residual (krylov.hpp:205-215): r already holds b - A x
@@ -901,6 +908,7 @@ struct Ctx3 {
     if (st.relres > best) {
       CU3(cudaMemcpyAsync(x, d_best, sizeof(double2) * nl, cudaMemcpyDeviceToDevice, stream));
       st.relres = best;
+      st.dual_of_x = false;
     }
     st.converged = st.relres <= tol;
     return st;
@@ -932,7 +940,7 @@ struct Ctx3 {
       launch(FETIGPU_K_OTHER, [&] { k3::k3_gather_corner<<<cdiv3(nc, 128), 128, 0, stream>>>(nc, d_cdof, rhs, d_fc); });
     CU3(cudaMemcpyAsync(d_yi, d_fi, sizeof(double2) * S * NI, cudaMemcpyDeviceToDevice, stream));
     interior_solve(d_yi);
-    eliminate_boundary(d_fb);
+    eliminate_boundary(d_fb, true);
     launch(FETIGPU_K_LAMBDA, [&] {  // d = B u_r
       k3::k3_lam_jump<<<cdiv3(nl, 256), 256, 0, stream>>>(nl, NB, NC, 1.0, d_lam_lo, d_lam_hi, d_u1, d_cpl_b, d_cglob,
                                                          nullptr, d_d);
@@ -942,12 +950,32 @@ struct Ctx3 {
     st.iterations = gs.iterations;
     st.converged = gs.converged ? 1 : 0;
     st.relative_residual = gs.relres;
-    // t = f_r - B^T lam, final eliminate, interior recovery, primal assembly
-    launch(FETIGPU_K_LAMBDA, [&] {
-      k3::k3_gather_in<<<cdiv3((long long)S * NB, 256), 256, 0, stream>>>(S, NB, MR, 2, d_n_b, d_brow, d_bsgn,
-                                                                         d_lam_w, d_lam, d_fb, d_tb);
-    });
-    eliminate_boundary(d_tb);
+    // t = f_r - B^T lam, final eliminate, interior recovery, primal assembly.  S^-1 and the
+    // coarse terms are linear in t: when GMRES's last dual application was on the returned
+    // lam, S^-1 (t_b - A_bi y_i) = u0 + S^-1(-B^T lam) and coupling^T t = gcp0 + its part, so
+    // the elimination needs no further GEMV
+    if (gs.dual_of_x) {
+      launch(FETIGPU_K_OTHER, [&] {
+        k3::k3_axpby<<<cdiv3((long long)S * NB, 256), 256, 0, stream>>>(S * NB, make_double2(1.0, 0.0), d_u0,
+                                                                       make_double2(1.0, 0.0), d_u1);
+      });
+      if (nc > 0) {
+        launch(FETIGPU_K_OTHER, [&] {
+          k3::k3_axpby<<<cdiv3((long long)S * G * NC, 256), 256, 0, stream>>>(S * G * NC, make_double2(1.0, 0.0), d_gcp0,
+                                                                             make_double2(1.0, 0.0), d_gcp);
+        });
+        coarse_solve(d_fc);
+        launch(FETIGPU_K_OTHER, [&] {
+          k3::k3_ub_correct<<<cdiv3((long long)S * NB, 256), 256, 0, stream>>>(S, NB, NC, d_cglob, d_z, d_cpl_b, d_u1);
+        });
+      }
+    } else {
+      launch(FETIGPU_K_LAMBDA, [&] {
+        k3::k3_gather_in<<<cdiv3((long long)S * NB, 256), 256, 0, stream>>>(S, NB, MR, 2, d_n_b, d_brow, d_bsgn,
+                                                                           d_lam_w, d_lam, d_fb, d_tb);
+      });
+      eliminate_boundary(d_tb);
+    }
     launch(FETIGPU_K_OTHER, [&] {
       k3::k3_ri_rhs<<<cdiv3((long long)S * NI, 256), 256, 0, stream>>>(S, NI, NB, NC, H.MAXE_IB, d_ib_idx, d_ib_val,
                                                                       d_aic, d_cglob, d_z, d_u1, d_fi, d_ri);
