@@ -420,12 +420,20 @@ struct Ctx3 {
         static bool gattr = false;
         if (!gattr) {
           CU3(cudaFuncSetAttribute(k3::k3_gj_update64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
+          CU3(cudaFuncSetAttribute(k3::k3_gj_update64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
           gattr = true;
         }
+        // FETIGPU3D_GJ=tc: the DMMA (FP64 tensor core) trailing update — measured no faster
+        // (1.01 vs 0.99 s at config 4): the update is bound by its read-modify-write of C
+        const char* gje = std::getenv("FETIGPU3D_GJ");
+        const bool gj_tc = gje && std::string(gje) == "tc";
         for (int K = 0; K < NTD; ++K) {
           k3::k3_gj_pivot<<<cnt, 256, 0, stream>>>(NBP, K, dense, pbuf, prat);
           k3::k3_gj_panel<<<dim3(NTD, cnt), 256, 0, stream>>>(NBP, NTD, K, dense, pbuf, cbuf);
-          k3::k3_gj_update64<<<dim3(NTD / 2, NTD / 2, cnt), 256, gsm, stream>>>(NBP, NTD, K, dense, pbuf, cbuf);
+          if (gj_tc)
+            k3::k3_gj_update64_tc<<<dim3(NTD / 2, NTD / 2, cnt), 256, gsm, stream>>>(NBP, NTD, K, dense, pbuf, cbuf);
+          else
+            k3::k3_gj_update64<<<dim3(NTD / 2, NTD / 2, cnt), 256, gsm, stream>>>(NBP, NTD, K, dense, pbuf, cbuf);
           k3::k3_gj_setpivot<<<cnt, 256, 0, stream>>>(NBP, K, dense, pbuf);
           CU3(cudaGetLastError());
           launches += 4;

@@ -865,6 +865,81 @@ __global__ void __launch_bounds__(256) k3_gj_update64(int NBP, int NT, int K, do
     }
   }
 }
+// The same trailing update on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64): each warp
+// owns a 16 x 32 patch of the 64 x 64 tile as 2 x 4 fragments of 8 x 8; a complex product
+// is four real MMAs (re += Are Bre - Aim Bim, im += Are Bim + Aim Bre).  Operands are the
+// same shared-memory tiles as k3_gj_update64.
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(256) k3_gj_update64_tc(int NBP, int NT, int K, double2* __restrict__ dense,
+                                                         const double2* __restrict__ pbuf,
+                                                         const double2* __restrict__ cbuf) {
+  extern __shared__ __align__(16) double2 k3g_sm[];
+  double2 (*As)[33] = reinterpret_cast<double2 (*)[33]>(k3g_sm);
+  double2 (*Bs)[65] = reinterpret_cast<double2 (*)[65]>(k3g_sm + 64 * 33);
+  const int J0 = blockIdx.x * 64, I0 = blockIdx.y * 64, sc = blockIdx.z;
+  const int kr = K * 32;
+  double2* M = dense + (size_t)sc * NBP * NBP;
+  const double2* P = pbuf + (size_t)sc * 1024;
+  for (int e = threadIdx.x; e < 64 * 32; e += 256) {
+    const int r = e >> 5, k = e & 31, I = (I0 + r) >> 5;
+    As[r][k] = cbuf[((size_t)sc * NT + I) * 1024 + ((I0 + r) & 31) * 32 + k];
+  }
+  for (int e = threadIdx.x; e < 32 * 64; e += 256) {
+    const int k = e >> 6, c = e & 63, gc = J0 + c;
+    Bs[k][c] = (gc >= kr && gc < kr + 32) ? P[k * 32 + (gc - kr)] : M[(size_t)(kr + k) * NBP + gc];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wr = (warp & 3) * 16, wc = (warp >> 2) * 32;
+  const int g = lane >> 2, t = lane & 3;
+  double cre[2][4][2], cim[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cre[i][j][0] = cre[i][j][1] = cim[i][j][0] = cim[i][j][1] = 0.0;
+#pragma unroll 2
+  for (int k0 = 0; k0 < 32; k0 += 4) {
+    double are[2], aim[2], bre[4], bim[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const double2 v = As[wr + 8 * i + g][k0 + t];
+      are[i] = v.x, aim[i] = v.y;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double2 v = Bs[k0 + t][wc + 8 * j + g];
+      bre[j] = v.x, bim[j] = v.y;
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        dmma884(cre[i][j][0], cre[i][j][1], are[i], bre[j]);
+        dmma884(cre[i][j][0], cre[i][j][1], -aim[i], bim[j]);
+        dmma884(cim[i][j][0], cim[i][j][1], are[i], bim[j]);
+        dmma884(cim[i][j][0], cim[i][j][1], aim[i], bre[j]);
+      }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int gr = I0 + wr + 8 * i + g;
+    if (gr >= kr && gr < kr + 32) continue;  // row panel: already final
+    double2* row = M + (size_t)gr * NBP;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int gc = J0 + wc + 8 * j + 2 * t + e;
+        const double2 acc = make_double2(cre[i][j][e], cim[i][j][e]);
+        if (gc >= kr && gc < kr + 32) row[gc] = make_double2(-acc.x, -acc.y);
+        else row[gc] = csub(row[gc], acc);
+      }
+  }
+}
 // the pivot block of step K becomes P (after the update kernel has read the row panel)
 __global__ void k3_gj_setpivot(int NBP, int K, double2* __restrict__ dense, const double2* __restrict__ pbuf) {
   const int sc = blockIdx.x;

@@ -259,3 +259,25 @@ def test_augmented_schur_matches_oracle(fetigpu, oracle_mod):
         assert rel(out[k], ref[k]) <= 1e-8, k
     assert abs(out["plus_stats"]["iterations"] - ref["plus_stats"]["iterations"]) <= 2
     assert abs(out["minus_stats"]["iterations"] - ref["minus_stats"]["iterations"]) <= 2
+
+
+@pytest.mark.gpu
+def test_schur_zero_target_deferred_path(fetigpu):
+    """A zero target through the Schur solve (the deferred-GMRES graph path): zero y, u,
+    lambda, converged in 0 iterations for both factors (feti.cpp:640-644); then a regular
+    solve on the same context is unaffected."""
+    p = fetigpu.make_seeded_problem(64, 1e-4, seed=0)
+    solver = fetigpu.SchurSolver(p, 4, 4, tol=1e-10, max_iter=500)
+    try:
+        z = solver.solve(np.zeros(p.n))
+        assert z["converged"]
+        assert z["plus_stats"]["iterations"] == 0 and z["minus_stats"]["iterations"] == 0
+        for k in ("y", "u", "lambda"):
+            assert not np.any(z[k]), k
+        r1 = solver.solve()
+        r2 = solver.solve()
+        assert r1["converged"] and r1["plus_stats"]["iterations"] > 0
+        for k in ("y", "u", "lambda"):
+            assert np.array_equal(r1[k], r2[k]), k
+    finally:
+        solver.close()
