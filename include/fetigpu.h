@@ -200,6 +200,11 @@ int fetigpu_profile_read(fetigpu_ctx* ctx, double* ms, long long* launches, int 
  * none were recorded, e.g. on the sharded path). */
 int fetigpu_step_spans(fetigpu_ctx* ctx, double* out6);
 
+/* Average launch duration (ms) of the Arnoldi step's two GEMVs: CUDA events around a
+ * captured graph of `reps` consecutive launches of each on the context's operators:
+ * out4 = {precond ms, dual ms, precond bytes, dual bytes}.  One-GPU contexts. */
+int fetigpu_gemv_timing(fetigpu_ctx* ctx, int reps, double* out4);
+
 /* Algorithmic bytes per launch of a kernel class (the roofline numerator). */
 double fetigpu_class_bytes(fetigpu_ctx* ctx, int klass);
 

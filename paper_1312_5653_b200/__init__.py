@@ -279,6 +279,13 @@ class SchurSolver:
         _check(_native.lib().fetigpu_profile_read(self._h, _dp(ms), n, int(reset)))
         return {k: {"ms": float(ms[i]), "launches": int(n[i])} for i, k in enumerate(_native.K_CLASSES)}
 
+    def gemv_timing(self, reps=20):
+        """Per-launch ms of the Arnoldi GEMVs, CUDA events inside a captured graph of
+        back-to-back (precond, dual) pairs: {precond_gemv: ms, dual_gemv: ms}."""
+        out = np.zeros(4)
+        _check(_native.lib().fetigpu_gemv_timing(self._h, reps, _dp(out)))
+        return {"precond_gemv": float(out[0]), "dual_gemv": float(out[1])}
+
     def step_spans(self):
         """Mean in-graph kernel spans (us) of the last FETI solve's Arnoldi steps:
         dict(precond, gap_pd, dual, gap_dt, tail, gap_tp, steps) or None."""

@@ -98,6 +98,7 @@ def lib():
     L.fetigpu_diagnostics.argtypes = [pdesc, dp, dp, dp, dp, dp]
     L.fetigpu_full_space.argtypes = [vp, C.c_int, C.c_int, C.c_double, C.c_int, dp, dp, dp, dp, dp,
                                      C.POINTER(FetiStats), dp]
+    L.fetigpu_gemv_timing.argtypes = [vp, C.c_int, dp]
     L.fetigpu_class_bytes.argtypes = [vp, C.c_int]
     L.fetigpu_class_bytes.restype = C.c_double
     pd3, lp = C.POINTER(Desc3), C.POINTER(C.c_longlong)
@@ -133,7 +134,7 @@ EXPORTED_SYMBOLS = (
     "fetigpu_profile", "fetigpu_profile_read", "fetigpu_class_bytes", "fetigpu_last_error",
     "fetigpu_nccl_unique_id", "fetigpu_create_sharded", "fetigpu_rank_info", "fetigpu_emulated_schur_solve",
     "fetigpu_step_spans", "fetigpu_full_space", "fetigpu_pressure_load", "fetigpu_diagnostics",
-    "fetigpu_nccl_selftest",
+    "fetigpu_nccl_selftest", "fetigpu_gemv_timing",
     "fetigpu3d_problem_info", "fetigpu3d_target_sine", "fetigpu3d_create", "fetigpu3d_destroy",
     "fetigpu3d_schur_solve", "fetigpu3d_schur_solve_device", "fetigpu3d_feti_solve", "fetigpu3d_apply_dual",
     "fetigpu3d_apply_precond", "fetigpu3d_stream", "fetigpu3d_launch_count", "fetigpu3d_profile",

@@ -1840,6 +1840,48 @@ struct Ctx {
     return true;
   }
 
+  // Average launch duration of the two Arnoldi GEMVs, CUDA events on the context stream
+  // around a captured graph of `reps` consecutive launches of each (the preconditioner GEMV
+  // on the basis column j of the last cycle, then the dual GEMV on its output — idempotent
+  // repeats), launched as in the Arnoldi graph (PDL); per-launch event brackets would add
+  // the launch latency of every ~25 us kernel to its interval.
+  void gemv_timing(int reps, double* out4) {
+    reps = std::max(1, std::min(reps, 256));
+    cudaEvent_t ev[3];
+    for (auto& e : ev) CU(cudaEventCreate(&e));
+    sync();
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    const bool was_prof = prof;
+    prof = false;
+    CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    CU(cudaEventRecordWithFlags(ev[0], stream, cudaEventRecordExternal));
+    for (int r = 0; r < reps; ++r) precond_gemv(d_V, &d_gst->j);
+    CU(cudaEventRecordWithFlags(ev[1], stream, cudaEventRecordExternal));
+    for (int r = 0; r < reps; ++r) {
+      SymGemvArgs a = sym_args(d_Sinv_p);
+      a.mode = 1;
+      a.wb = d_wb;
+      dual_gemv(a, tail_rpt > 0);
+    }
+    CU(cudaEventRecordWithFlags(ev[2], stream, cudaEventRecordExternal));
+    CU(cudaStreamEndCapture(stream, &g));
+    prof = was_prof;
+    CU(cudaGraphInstantiate(&ge, g, 0));
+    CU(cudaGraphLaunch(ge, stream));
+    sync();
+    float a = 0, b = 0;
+    CU(cudaEventElapsedTime(&a, ev[0], ev[1]));
+    CU(cudaEventElapsedTime(&b, ev[1], ev[2]));
+    out4[0] = a / reps;
+    out4[1] = b / reps;
+    out4[2] = class_bytes(FETIGPU_K_PRECOND_GEMV);
+    out4[3] = class_bytes(FETIGPU_K_DUAL_GEMV);
+    CU(cudaGraphExecDestroy(ge));
+    CU(cudaGraphDestroy(g));
+    for (auto& e : ev) cudaEventDestroy(e);
+  }
+
   double class_bytes(int klass) const {
     const double S = H.n_sub, NB = H.NB;
     switch (klass) {
@@ -2339,6 +2381,14 @@ int fetigpu_step_spans(fetigpu_ctx* ctx, double* out6) {
   } catch (...) {
     return 0;
   }
+}
+
+int fetigpu_gemv_timing(fetigpu_ctx* ctx, int reps, double* out4) {
+  return guard([&] {
+    if (!ctx) throw ContractError("fetigpu: null context");
+    if (ctx->c->dist()) throw ContractError("fetigpu_gemv_timing: one-GPU contexts only");
+    ctx->c->gemv_timing(reps, out4);
+  });
 }
 
 double fetigpu_class_bytes(fetigpu_ctx* ctx, int klass) { return ctx ? ctx->c->class_bytes(klass) : 0.0; }
