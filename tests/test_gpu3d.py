@@ -243,3 +243,21 @@ def test_gpu3d_full_config_properties(fetigpu, oracle_mod, config):
     state, adjoint = kkt_residuals(oracle_mod, c, r, p.target_state)
     assert state <= c["state_tol"], state
     assert adjoint <= 1e-10, adjoint
+
+
+@pytest.mark.gpu
+def test_gpu3d_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
+    """max_iter reached: converged = false, iterations = max_iter, the same iterate and
+    relative residual as the oracle (krylov.hpp:97-100)."""
+    from paper_1312_5653_b200 import box
+
+    n, s, phi = 12, 3, 1e-4
+    p = box.make_box_problem(n, phi=phi, seed=1)
+    rhs = np.random.default_rng(9).standard_normal(p.n).astype(complex)
+    x, st = box.feti_solve_3d(p, -1j / np.sqrt(phi), rhs, s, tol=1e-12, max_iter=3)
+    xr, sr = oracle_mod.Feti(oracle_mod.Problem(n, n, n_z=n), s, s, -1j / np.sqrt(phi), s_z=s, tol=1e-12,
+                             max_iter=3).solve(rhs)
+    assert not st["converged"] and st["iterations"] == 3
+    assert not sr["converged"] and sr["iterations"] == 3
+    assert abs(st["relative_residual"] - sr["relative_residual"]) <= 1e-6 * sr["relative_residual"]
+    assert rel(x, xr) <= 1e-8

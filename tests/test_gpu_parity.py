@@ -281,3 +281,23 @@ def test_schur_zero_target_deferred_path(fetigpu):
             assert np.array_equal(r1[k], r2[k]), k
     finally:
         solver.close()
+
+
+@pytest.mark.gpu
+def test_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
+    """krylov.hpp:97-100: hitting max_iter returns converged = false with the best iterate
+    (rc 0), iterations = max_iter; the oracle agrees on the count and the relative residual."""
+    n, s, phi = 64, 4, 1e-4
+    p = fetigpu.make_seeded_problem(n, phi, seed=0)
+    rhs = np.random.default_rng(5).standard_normal(p.n).astype(complex)
+    solver = fetigpu.SchurSolver(p, s, s, tol=1e-10, max_iter=4, mass_coeff=-1j / np.sqrt(phi))
+    try:
+        x, st = solver.feti_solve(rhs)
+    finally:
+        solver.close()
+    assert not st["converged"] and st["iterations"] == 4
+    assert np.all(np.isfinite(x))
+    ref_x, ref = oracle_mod.Feti(oracle_mod.Problem(n), s, s, -1j / np.sqrt(phi), tol=1e-10, max_iter=4).solve(rhs)
+    assert not ref["converged"] and ref["iterations"] == 4
+    assert abs(st["relative_residual"] - ref["relative_residual"]) <= 1e-6 * ref["relative_residual"]
+    assert np.linalg.norm(x - ref_x) <= 1e-8 * np.linalg.norm(ref_x)
