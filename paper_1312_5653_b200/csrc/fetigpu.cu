@@ -808,6 +808,11 @@ struct Ctx {
     d_u1b = alloc<double2>((size_t)n_slot_ext);
     d_wb = alloc<double2>((size_t)n_slot_ext);
     d_gcp = alloc<double2>((size_t)S * NC);
+    reuse_elim = !dist() && H.n_aug == 0 && !std::getenv("FETIGPU_NO_ELIM_REUSE");
+    if (reuse_elim) {
+      d_u1b0 = alloc<double2>((size_t)n_slot_ext);
+      d_gcp0 = alloc<double2>((size_t)S * NC);
+    }
     d_fc = alloc<double2>(std::max(nc, 1));
     zero(d_fc, std::max(nc, 1));  // augmentation rows of f_c stay zero (feti.cpp:521-522)
     d_g = alloc<double2>(std::max(nc, 1));
@@ -1210,6 +1215,11 @@ struct Ctx {
   // factorization: y_i = A_ii^-1 t_i (banded), u1_b = S_bb^-1 (t_b - A_bi y_i) (dense),
   // g = f_c - coupling^T t, z = C^-1 g, u_b = u1_b - cpl_b z.  Both eliminations of a FETI
   // solve share t_i = f_i, so y_i is solved once (new_yi) and reused.
+  // first elimination's S^-1 (t_b - A_bi y_i) and coarse terms, kept for the final one
+  // (reuse_elim: one GPU, no augmentation); last_dual_of_x: GMRES's last dual application was
+  // on the returned multipliers (its u1_b / gcp are S^-1(-B^T lam) and cpl_b^T(-B^T lam))
+  double2 *d_u1b0 = nullptr, *d_gcp0 = nullptr;
+  bool reuse_elim = false, last_dual_of_x = false;
   void eliminate_boundary(const double2* ti, const double2* tb, const double2* fc, bool new_yi) {
     const int S = H.n_sub, NI = H.NI, NB = H.NB;
     if (new_yi) {
@@ -1236,6 +1246,10 @@ struct Ctx {
     (void)NB;
     if (d_aic_idx == nullptr)
       launch(FETIGPU_K_OTHER, [&] { k_gcp_full<<<S, 256, 0, stream>>>(L, d_cpl_i, d_cpl_b, ti, tb, d_gcp); });
+    if (new_yi && reuse_elim) {
+      CU(cudaMemcpyAsync(d_u1b0, d_u1b, (size_t)n_slot_ext * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+      CU(cudaMemcpyAsync(d_gcp0, d_gcp, (size_t)S * H.NC * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+    }
     coarse_solve(fc);
     launch(FETIGPU_K_OTHER, [&] {
       k_ub_correct<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(L, d_cglob, d_z, d_cpl_b, d_u1b);
@@ -1457,6 +1471,7 @@ struct Ctx {
 
   fetigpu_feti_stats gmres(const double2* b, double2* x, int sb = 0) {
     fetigpu_feti_stats st{};
+    last_dual_of_x = false;
     const double tol = desc.tol;
     const int max_iter = desc.max_iter;
     zero(x, nl);
@@ -1539,6 +1554,7 @@ struct Ctx {
         apply_precond(d_t, d_zl);
         launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nown, 256), 256, 0, stream>>>(nown, x + own0, d_zl + own0); });
         apply_dual(x, d_w);
+        last_dual_of_x = true;
         project_aug(d_w);
         launch(FETIGPU_K_ORTHO, [&] { k_sub<<<cdiv(nown, 256), 256, 0, stream>>>(nown, b + own0, d_w + own0, d_r + own0); });
         norm_async(d_r + own0, nown, 12 + sb / 4);
@@ -1614,6 +1630,7 @@ struct Ctx {
       apply_precond(d_t, d_zl);
       launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nown, 256), 256, 0, stream>>>(nown, x + own0, d_zl + own0); });
       apply_dual(x, d_w);
+      last_dual_of_x = true;
       project_aug(d_w);  // the GMRES operator is P F (feti.cpp:667-670)
       launch(FETIGPU_K_ORTHO, [&] {
         k_sub<<<cdiv(nown, 256), 256, 0, stream>>>(nown, b + own0, d_w + own0, d_r + own0);
@@ -1623,6 +1640,7 @@ struct Ctx {
     if (relres > best_res) {
       CU(cudaMemcpyAsync(x, d_best, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
       relres = best_res;
+      last_dual_of_x = false;
     }
     st.iterations = iterations;
     st.relative_residual = relres;
@@ -1666,10 +1684,25 @@ struct Ctx {
     st.iterations = gst.iterations;
     st.converged = gst.converged;
     st.relative_residual = gst.relative_residual;
-    launch(FETIGPU_K_OTHER, [&] {
-      k_recover_tb<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(S * NB, d_blam, d_bsign, d_fb, d_lam, d_tb);
-    });
-    eliminate_boundary(d_fi, d_tb, d_fc, false);
+    if (reuse_elim && last_dual_of_x) {
+      // S^-1 and the coarse terms are linear in t = [f_i ; f_b - B^T lam]: the first
+      // elimination plus GMRES's true-residual dual application give them without a GEMV
+      launch(FETIGPU_K_OTHER, [&] {
+        k_add_inplace<<<cdiv((long long)n_slot_ext, 256), 256, 0, stream>>>(n_slot_ext, d_u1b, d_u1b0);
+      });
+      launch(FETIGPU_K_OTHER, [&] {
+        k_add_inplace<<<cdiv((long long)S * H.NC, 256), 256, 0, stream>>>(S * H.NC, d_gcp, d_gcp0);
+      });
+      coarse_solve(d_fc);
+      launch(FETIGPU_K_OTHER, [&] {
+        k_ub_correct<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(L, d_cglob, d_z, d_cpl_b, d_u1b);
+      });
+    } else {
+      launch(FETIGPU_K_OTHER, [&] {
+        k_recover_tb<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(S * NB, d_blam, d_bsign, d_fb, d_lam, d_tb);
+      });
+      eliminate_boundary(d_fi, d_tb, d_fc, false);
+    }
     phase("elim2b");
     eliminate_interior();
     phase("elim2i");
