@@ -154,6 +154,11 @@ struct Ctx {
   double* d_gcos = nullptr;
   unsigned int* d_counter = nullptr;
   bool use_graph = true;
+  // split Givens (graph path with the fused tail): the Givens step of Arnoldi step j runs as
+  // an extra CTA of the preconditioner GEMV of step j+1 (the body's last step: its own small
+  // kernel, it drives the WHILE condition); FETIGPU_NO_SPLIT=1: Givens inside the tail
+  bool split_givens = false;
+  const int* span_it = nullptr;  // split path: the preconditioner GEMV's span slot is st->jcol
   bool debug_sync = false;
   bool sym_tma = false;
   bool pdl = true;                      // FETIGPU_NO_PDL=1: plain stream serialisation
@@ -207,6 +212,7 @@ struct Ctx {
     if (arnoldi_graph) cudaGraphDestroy(arnoldi_graph);
     if (stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
+
     if (ev_out) cudaEventDestroy(ev_out);
   }
 
@@ -1110,7 +1116,7 @@ struct Ctx {
     g.bi_val = d_bi_val;
     if (span_on) {
       g.span = d_span;
-      g.it_ptr = &d_gst->iterations;
+      g.it_ptr = span_it ? span_it : &d_gst->iterations;
     }
     if (in_arnoldi && tail_rpt > 0) g.cont_ptr = &d_gst->cont;
     return g;
@@ -1315,7 +1321,8 @@ struct Ctx {
   // node, so a whole cycle runs without returning to the host.  Eager mode (profiling)
   // launches the same sequence step by step.  The reference's Hermitian MGS is replaced
   // by CGS2 (two classical passes; equal in exact arithmetic).
-  void arnoldi_step(bool in_graph) {
+  void arnoldi_step(bool in_graph, int u = 0) {
+    const bool split = in_graph && split_givens && tail_rpt > 0;
     double2* h1 = d_red;
     double2* h2 = d_red + (vcap + 2);
     auto mark = [&](unsigned int v) {
@@ -1325,7 +1332,26 @@ struct Ctx {
     mark(1);
     span_on = d_span != nullptr;  // (one GPU only)
     in_arnoldi = true;
-    precond_gemv(d_V, &d_gst->j);
+    if (split) {
+      span_it = &d_gst->jcol;  // (st->iterations advances in the Givens CTA of this launch)
+      SymGemvArgs g = sym_args(d_Sbb_p);
+      g.mode = 0;
+      g.lam = d_V;
+      g.jsel = &d_gst->jcol;
+      g.jstride = ldv;
+      g.alpha = 0.5;
+      g.out = d_wb;
+      span_it = nullptr;
+      if (u > 0) {  // fold the previous step's Givens into this launch
+        const GivensArgs ga{d_gst, h1, h2, d_R, d_gcos, d_gsin, d_gvec, 1, arnoldi_handle};
+        const size_t sm = std::max(sym_smem(), (size_t)640 * sizeof(double2));
+        launch(FETIGPU_K_PRECOND_GEMV, [&] { kx(k_sym_gemv_giv<8, 4>, H.n_sub + 1, 128, sm, g, ga); });
+      } else {
+        launch(FETIGPU_K_PRECOND_GEMV, [&] { launch_sym(g); });
+      }
+    } else {
+      precond_gemv(d_V, &d_gst->j);
+    }
     mark(2);
     {
       SymGemvArgs g = sym_args(d_Sinv_p);
@@ -1361,6 +1387,7 @@ struct Ctx {
       t.u1b = d_u1b;
       t.cpl_b = d_cpl_b;
       t.ga = GivensArgs{d_gst, h1, h2, d_R, d_gcos, d_gsin, d_gvec, in_graph ? 1 : 0, arnoldi_handle};
+      t.split_givens = split ? 1 : 0;
       t.tstamp = d_tstamp;
       t.span = d_span;
       t.hcap = vcap + 2;
@@ -1374,6 +1401,8 @@ struct Ctx {
         else
           kx(k_arnoldi_tail<kTailThreads, 4, 1>, tail_grid, kTailThreads, tail_smem(), t);
       });
+      if (split && u == body_unroll - 1)  // the body's last Givens drives the WHILE condition
+        launch(FETIGPU_K_ORTHO, [&] { kx(k_givens_step, 1, 32, 0, t.ga); });
       mark(6);
       return;
     }
@@ -1461,7 +1490,8 @@ struct Ctx {
     body_unroll = tail_rpt > 0 ? kBodyUnroll : 1;
     if (const char* e = std::getenv("FETIGPU_UNROLL")) body_unroll = tail_rpt > 0 ? std::max(1, std::atoi(e)) : 1;
     CU(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    for (int u = 0; u < body_unroll; ++u) arnoldi_step(true);
+    split_givens = tail_rpt > 0 && !cgs_gram && sym_warps == 4 && !sym_tma && !std::getenv("FETIGPU_NO_SPLIT");
+    for (int u = 0; u < body_unroll; ++u) arnoldi_step(true, u);
     CU(cudaStreamEndCapture(stream, &body));
     prof = was_prof;
     arnoldi_body_kernels = (int)(launches - before) / body_unroll;

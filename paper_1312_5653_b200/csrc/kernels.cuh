@@ -633,8 +633,11 @@ struct SymGemvArgs {
   const double2* aic_val;
 };
 
+
+// The per-subdomain packed symmetric GEMV (one CTA = one subdomain), shared by k_sym_gemv
+// and k_sym_gemv_giv (the preconditioner GEMV with the previous step's Givens folded in).
 template <int MODE, int SYM_BATCH, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(SymGemvArgs a) {
+__device__ __forceinline__ void sym_gemv_run(const SymGemvArgs& a) {
   // dynamic smem: x (32 NT) | row partials (ntiles x 32) | column partials (noff x 32)
   extern __shared__ double2 sg_sh[];
   const int NB = a.NB, NT = a.NT;
@@ -644,9 +647,6 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(S
   double2 (*part_col)[32] = reinterpret_cast<double2 (*)[32]>(sg_sh + 32 * NT + 32 * ntiles);
   const int s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pdl_trigger();
-  pdl_wait();
-  if (a.cont_ptr != nullptr && *a.cont_ptr == 0) return;
   span_mark(a.span, a.it_ptr, MODE, 0);
   // ---- input vector (B^T scatter) ----
   const double2* lam = a.lam;
@@ -785,6 +785,14 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(S
     __syncthreads();
     span_mark(a.span, a.it_ptr, MODE, 1);
   }
+}
+
+template <int MODE, int SYM_BATCH, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(SymGemvArgs a) {
+  pdl_trigger();
+  pdl_wait();
+  if (a.cont_ptr != nullptr && *a.cont_ptr == 0) return;
+  sym_gemv_run<MODE, SYM_BATCH, WARPS>(a);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1316,7 +1324,7 @@ struct GmresState {
   int status;      // 1 = NaN/Inf breakdown (krylov.hpp:165-166)
   int max_iter;
   int m;           // restart length (= max_iter: unrestarted, feti.cpp:684)
-  int pad;
+  int jcol;        // basis column of the next preconditioner GEMV (split-Givens graph path)
   double tol, bnorm, inv_hnext, est;
 };
 
@@ -1480,6 +1488,42 @@ __global__ void __launch_bounds__(32) k_givens(GivensArgs a) {
   __shared__ double sc[256];
   __shared__ double2 ss[256], sh[256];
   givens_warp(a, sc, ss, sh);
+}
+// split-Givens graph path: the Givens step of the last step of an unrolled body, skipped
+// once the cycle stopped (the tail of that step returned at once and published nothing)
+__global__ void __launch_bounds__(32) k_givens_step(GivensArgs a) {
+  __shared__ double sc[256];
+  __shared__ double2 ss[256], sh[256];
+  pdl_trigger();
+  pdl_wait();  // (launched with programmatic serialization after the tail)
+  if (a.st->cont == 0) {
+    if (a.in_graph && threadIdx.x == 0) cudaGraphSetConditional(a.handle, 0u);
+    return;
+  }
+  givens_warp(a, sc, ss, sh);
+}
+// Preconditioner GEMV of Arnoldi step j+1 with the Givens step of step j folded in as one
+// extra CTA (blockIdx.x == gridDim.x - 1): the rotation chain runs concurrently with the
+// operator stream instead of ending the previous tail on the critical path.  The GEMV CTAs
+// take their basis column from st->jcol (published by the tail) and may run once past the
+// end of a stopped cycle (harmless: the dual GEMV and tail of that step return at once).
+template <int SYM_BATCH, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv_giv(SymGemvArgs a, GivensArgs ga) {
+  pdl_trigger();
+  pdl_wait();
+  if (blockIdx.x == gridDim.x - 1) {
+    extern __shared__ double2 sg_sh[];  // >= 640 entries (host)
+    if (threadIdx.x < 32) {
+      if (ga.st->cont == 0) {
+        if (ga.in_graph && threadIdx.x == 0) cudaGraphSetConditional(ga.handle, 0u);
+      } else {
+        givens_warp(ga, reinterpret_cast<double*>(sg_sh), sg_sh + 128, sg_sh + 384);
+      }
+    }
+    return;
+  }
+  if (a.cont_ptr != nullptr && *a.cont_ptr == 0) return;
+  sym_gemv_run<0, SYM_BATCH, WARPS>(a);
 }
 
 // One classical Gram-Schmidt pass on the block's chunk of w:
@@ -1808,6 +1852,10 @@ struct ArnoldiTailArgs {
   const int *lam_lo, *lam_hi, *cglob;
   const double2 *u1b, *cpl_b;
   GivensArgs ga;
+  // split_givens: the Givens step runs as its own kernel on a side branch of the graph,
+  // concurrently with the next preconditioner GEMV; the tail only publishes h1/h2 and the
+  // next basis column index (st->jcol)
+  int split_givens;
   unsigned long long* tstamp;  // optional phase timestamps (block 0), 8 per Arnoldi step
   unsigned long long* span;    // FETIGPU_STEP_TIMES
 };
@@ -1946,7 +1994,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 0] = gtimer();
   // Givens operands known now (block 0): loaded during the coarse phase, off the critical path
   __shared__ GivensPre gpre;
-  if (!GRAM && blockIdx.x == 0 && warp == 0)
+  if (!GRAM && !a.split_givens && blockIdx.x == 0 && warp == 0)
     givens_prefetch(a.ga, &gpre, reinterpret_cast<double*>(stage), stage + 128);
   span_mark(a.span, &it, 2, 0);
   // dual-tail operands that do not depend on z (loaded before the barrier)
@@ -2163,8 +2211,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
       a.h1[i] = hs1[i];
       a.h2[i] = hs2[i];
     }
-    if (warp == 0)
+    if (a.split_givens) {
+      if (threadIdx.x == 0) a.st->jcol = nv;  // the next step's basis column (k_givens runs aside)
+    } else if (warp == 0) {
       givens_warp<true>(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384, hs1, hs2, &gpre);
+    }
     if (a.tstamp && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 9] = gtimer();
   }
   if (a.span != nullptr) {
