@@ -63,6 +63,8 @@ __device__ __forceinline__ double warp_max(double v) {
 // pdl_trigger() lets the successor start.  Both are no-ops without the launch attribute.
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// non-binding prefetch of the line holding p into L1
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
 // asynchronous bulk prefetch of [p, p + bytes) into L2 (bytes % 16 == 0)
 __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");

@@ -1983,6 +1983,34 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   const bool act = (int)threadIdx.x < a.rows_pb && r < a.n;
   const int row_end = min(a.n, row0 + a.rows_pb);  // exclusive
   pdl_trigger();
+  // ---- before pdl_wait: solve-constant data only (PDL contract, common.cuh) ----
+  // dual-tail index/coupling operands of this thread's multiplier row
+  int slots[2] = {0, 0};
+  double2 cpv[2][NCM];
+  int cgv[2][NCM];
+  if (act) {
+    slots[0] = a.lam_lo[r];
+    slots[1] = a.lam_hi[r];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int s = slots[q] / a.NB;
+#pragma unroll
+      for (int c = 0; c < NCM; ++c) {
+        cgv[q][c] = c < a.NC ? a.cglob[(size_t)s * a.NC + c] : -1;
+        cpv[q][c] = c < a.NC ? a.cpl_b[(size_t)slots[q] * a.NC + c] : cz();
+      }
+    }
+  }
+  // warm L1 with the coarse phase's constant operands: the corner-slot lists and this
+  // block's first round of C^-1 rows (the L2-persisting inverse)
+  for (int k = threadIdx.x; k < a.nc; k += THREADS) prefetch_l1(a.corner_slots + k * 4);
+  {
+    const int row = blockIdx.x * (WARPS / 2) + (warp >> 1);
+    if (row < a.nc) {
+      const double2* cr = a.Cinv + (size_t)row * a.nc;
+      for (int k0 = (warp & 1) * 32 + lane; k0 < a.nc; k0 += 64) prefetch_l1(cr + k0);
+    }
+  }
   pdl_wait();
   if (a.st->cont == 0) {  // unrolled WHILE body: the cycle already stopped (or never started:
     // zero rhs) -- make sure the WHILE node exits
@@ -1997,21 +2025,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   if (!GRAM && !a.split_givens && blockIdx.x == 0 && warp == 0)
     givens_prefetch(a.ga, &gpre, reinterpret_cast<double*>(stage), stage + 128);
   span_mark(a.span, &it, 2, 0);
-  // dual-tail operands that do not depend on z (loaded before the barrier)
-  double2 u[2] = {cz(), cz()}, cpv[2][NCM];
-  int cgv[2][NCM];
+  // dual-tail operand that does not depend on z (loaded before the barrier)
+  double2 u[2] = {cz(), cz()};
   if (act) {
-    const int slots[2] = {a.lam_lo[r], a.lam_hi[r]};
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int slot = slots[q], s = slot / a.NB;
-      u[q] = a.u1b[slot];
-#pragma unroll
-      for (int c = 0; c < NCM; ++c) {
-        cgv[q][c] = c < a.NC ? a.cglob[(size_t)s * a.NC + c] : -1;
-        cpv[q][c] = c < a.NC ? a.cpl_b[(size_t)slot * a.NC + c] : cz();
-      }
-    }
+    u[0] = a.u1b[slots[0]];
+    u[1] = a.u1b[slots[1]];
   }
   // ---- phase 0: z = C^-1 g.  g staged in smem (reusing the w buffer); each warp takes one
   // coarse row at a time with all of its lane's loads in one batch (clamped addresses) ----
