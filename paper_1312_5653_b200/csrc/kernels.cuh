@@ -1765,17 +1765,18 @@ constexpr int BS_KMAX = 72;
 __global__ void __launch_bounds__(32) k_backsub(const GmresState* __restrict__ st, const double2* __restrict__ R,
                                                 const double2* __restrict__ g, double2* __restrict__ y) {
   __shared__ double2 rs[BS_KMAX * (BS_KMAX + 1) / 2];
-  __shared__ double2 ys[BS_KMAX];
+  __shared__ double2 ys[BS_KMAX], gs[BS_KMAX];
   const int k = st->k, lane = threadIdx.x;
   if (k <= BS_KMAX) {
     const int tot = k * (k + 1) / 2;
     for (int e = lane; e < tot; e += 32) rs[e] = R[e];
+    for (int e = lane; e < k; e += 32) gs[e] = g[e];  // (no global load inside the recurrence)
     __syncwarp();
     for (int i = k - 1; i >= 0; --i) {
       double2 acc = cz();
       for (int j2 = i + 1 + lane; j2 < k; j2 += 32) acc = cfma(rs[j2 * (j2 + 1) / 2 + i], ys[j2], acc);
       acc = warp_sum2(acc);
-      if (lane == 0) ys[i] = cmul(csub(g[i], acc), crecip(rs[i * (i + 1) / 2 + i]));
+      if (lane == 0) ys[i] = cmul(csub(gs[i], acc), crecip(rs[i * (i + 1) / 2 + i]));
       __syncwarp();
     }
     for (int i = lane; i < k; i += 32) y[i] = ys[i];
