@@ -605,6 +605,9 @@ struct SymGemvArgs {
   const double2* lam;
   const int* jsel;                // mode 0: lam += (*jsel) * jstride (GMRES basis column)
   size_t jstride;
+  double2* zout;                  // mode 1, optional: zout[(*jsel) jstride + r] = (wb_lo - wb_hi)/2
+                                  // (the preconditioned basis column Z_j = M^-1 V_j, written
+                                  // by the CTA owning the row's +1 slot)
   double alpha;
   const int* lam_lo;
   const int* lam_hi;
@@ -667,8 +670,11 @@ __device__ __forceinline__ void sym_gemv_run(const SymGemvArgs& a) {
           double2 z;
           if (MODE == 0)
             z = lam[r];
-          else
-            z = cscale(csub(a.wb[a.lam_lo[r]], a.wb[a.lam_hi[r]]), 0.5);
+          else {
+            const int lo = a.lam_lo[r];
+            z = cscale(csub(a.wb[lo], a.wb[a.lam_hi[r]]), 0.5);
+            if (a.zout != nullptr && lo == (int)sb) a.zout[(size_t)(*a.jsel) * a.jstride + r] = z;
+          }
           v = cscale(z, a.alpha * a.bsign[sb]);
         }
       }
