@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libfetigpu.so")
+LIB_PATH = os.environ.get("FETIGPU_LIB") or os.path.join(_HERE, "_lib", "libfetigpu.so")  # (experiment builds)
 
 K_CLASSES = ("precond_gemv", "dual_gemv", "coarse", "lambda", "ortho", "band", "global", "other")
 

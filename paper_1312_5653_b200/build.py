@@ -59,6 +59,7 @@ def build(force=False, verbose=False):
         nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
         "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "-shared", "-Xptxas", "-v" if verbose else "-O3",
         "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + nccl_inc,
+        *os.environ.get("FETIGPU_NVCC_DEFINES", "").split(),  # experiment switches (-DNAME)
         *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp",
         "-L" + nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nccl_lib,
     ]

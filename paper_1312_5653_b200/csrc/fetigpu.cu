@@ -1494,6 +1494,37 @@ struct Ctx {
     });
   }
 
+  // FETIGPU_L2_PERSIST=1: C^-1 (read by every tail's coarse phase) as a persisting L2
+  // access-policy window on the Arnoldi body's kernel nodes, so the GEMV streams between two
+  // tails do not evict it
+  void l2_persist_coarse(cudaGraph_t body) {
+    if (!std::getenv("FETIGPU_L2_PERSIST") || nc == 0 || d_Cinv == nullptr) return;
+    int maxwin = 0, maxpers = 0;
+    CU(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, desc.device));
+    CU(cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, desc.device));
+    const size_t bytes = std::min<size_t>({(size_t)nc * nc * sizeof(double2), (size_t)maxwin, (size_t)maxpers});
+    CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
+    cudaLaunchAttributeValue v{};
+    v.accessPolicyWindow.base_ptr = d_Cinv;
+    v.accessPolicyWindow.num_bytes = bytes;
+    v.accessPolicyWindow.hitRatio = 1.0f;
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    size_t nn = 0;
+    CU(cudaGraphGetNodes(body, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CU(cudaGraphGetNodes(body, nodes.data(), &nn));
+    int set = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType t;
+      CU(cudaGraphNodeGetType(nd, &t));
+      if (t != cudaGraphNodeTypeKernel) continue;
+      CU(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributeAccessPolicyWindow, &v));
+      ++set;
+    }
+    std::fprintf(stderr, "[fetigpu] L2 persisting window: %zu bytes (max window %d, max persisting %d) on %d nodes\n",
+                 bytes, maxwin, maxpers, set);
+  }
   void build_arnoldi_graph() {
     CU(cudaGraphCreate(&arnoldi_graph, 0));
     CU(cudaGraphConditionalHandleCreate(&arnoldi_handle, arnoldi_graph, 1, cudaGraphCondAssignDefault));
@@ -1517,6 +1548,7 @@ struct Ctx {
     for (int u = 0; u < body_unroll; ++u) arnoldi_step(true, u);
     CU(cudaStreamEndCapture(stream, &body));
     prof = was_prof;
+    l2_persist_coarse(body);
     arnoldi_body_kernels = (int)(launches - before) / body_unroll;
     launches = before;
     CU(cudaGraphInstantiate(&arnoldi_exec, arnoldi_graph, 0));

@@ -796,6 +796,22 @@ __device__ __forceinline__ void sym_gemv_run(const SymGemvArgs& a) {
 template <int MODE, int SYM_BATCH, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(SymGemvArgs a) {
   pdl_trigger();
+#ifndef FETIGPU_GEMV_PF_ROWS
+#define FETIGPU_GEMV_PF_ROWS 8
+#endif
+#ifndef FETIGPU_GEMV_PF_MODES
+#define FETIGPU_GEMV_PF_MODES 3
+#endif
+  if ((FETIGPU_GEMV_PF_MODES >> MODE) & 1) {
+    // the operator is solve-constant: warm L1 with the first rows of this warp's first
+    // off-diagonal tile while the producer kernel drains (CTAs that become resident early)
+    const int NT = a.NT, noff = NT * (NT - 1) / 2, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp < noff) {
+      const double2* O = a.pack + (size_t)blockIdx.x * sym_tile_entries(NT) + NT * 17 * 32 + (size_t)warp * 1024;
+#pragma unroll
+      for (int u = 0; u < FETIGPU_GEMV_PF_ROWS; ++u) prefetch_l1(O + u * 32 + lane);
+    }
+  }
   pdl_wait();
   if (a.cont_ptr != nullptr && *a.cont_ptr == 0) return;
   sym_gemv_run<MODE, SYM_BATCH, WARPS>(a);
@@ -2010,7 +2026,16 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   }
   // warm L1 with the coarse phase's constant operands: the corner-slot lists and this
   // block's first round of C^-1 rows (the L2-persisting inverse)
-  for (int k = threadIdx.x; k < a.nc; k += THREADS) prefetch_l1(a.corner_slots + k * 4);
+  // corner-slot lists of this thread's first two coarse rows in registers (the rest, for
+  // large coarse spaces, warmed into L1)
+  int csl[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int k = threadIdx.x + h * THREADS;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) csl[h][q] = k < a.nc ? a.corner_slots[k * 4 + q] : -1;
+  }
+  for (int k = threadIdx.x + 2 * THREADS; k < a.nc; k += THREADS) prefetch_l1(a.corner_slots + k * 4);
   {
     const int row = blockIdx.x * (WARPS / 2) + (warp >> 1);
     if (row < a.nc) {
@@ -2019,6 +2044,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
     }
   }
   pdl_wait();
+  // the dual GEMV's coarse partials, loaded together with the cycle state (one latency)
+  double2 gv[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) gv[h][q] = csl[h][q] >= 0 ? a.gcp[csl[h][q]] : cz();
   if (a.st->cont == 0) {  // unrolled WHILE body: the cycle already stopped (or never started:
     // zero rhs) -- make sure the WHILE node exits
     if (a.ga.in_graph && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.ga.handle, 0u);
@@ -2044,7 +2075,16 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
     double2* g_sh = w_sh;  // nc <= hcap + THREADS is checked on the host
     // coarse rhs g = -sum_s gcp over the (up to 4) subdomains of each corner, assembled
     // redundantly by every block (same order as k_coarse_rhs)
-    for (int k = threadIdx.x; k < a.nc; k += THREADS) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int k = threadIdx.x + h * THREADS;
+      double2 acc = cz();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (csl[h][q] >= 0) acc = csub(acc, gv[h][q]);
+      if (k < a.nc) g_sh[k] = acc;
+    }
+    for (int k = threadIdx.x + 2 * THREADS; k < a.nc; k += THREADS) {
       double2 acc = cz();
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
