@@ -879,6 +879,7 @@ struct Ctx {
     d_stat = alloc<double2>(kStatSlots);
     setup_mass();
     setup_stencil();
+    setup_ri_compact();
     setup_l2_persistence();
     sync();
     setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -1267,16 +1268,62 @@ struct Ctx {
   }
   // interior harmonic extension u_i = A_ii^-1 (t_i - A_ib u_b - A_ic z) = y_i - A_ii^-1 (A_ib u_b + A_ic z)
   // -> d_ri (requires eliminate_boundary first)
+  // (the subtraction u_i = y_i - d_ri is left to k_assemble_x)
   void eliminate_interior() {
     const int S = H.n_sub, NI = H.NI;
-    launch(FETIGPU_K_OTHER, [&] {
-      k_ri_rhs<<<cdiv((long long)S * NI, 256), 256, 0, stream>>>(L, d_ib_idx, d_ib_val, d_Aic, d_cglob, d_z, d_u1b,
-                                                                 d_ri);
-    });
+    if (d_ri_map != nullptr) {
+      launch(FETIGPU_K_OTHER, [&] {
+        k_ri_rhs_compact<<<cdiv((long long)S * NI, 256), 256, 0, stream>>>(
+            (long long)S * NI, H.MAXE_IB, H.NC, NI, H.NB, d_ri_map, d_ri_cidx, d_ri_cval, d_ri_caic, d_cglob, d_z,
+            d_u1b, d_ri);
+      });
+    } else {
+      launch(FETIGPU_K_OTHER, [&] {
+        k_ri_rhs<<<cdiv((long long)S * NI, 256), 256, 0, stream>>>(L, d_ib_idx, d_ib_val, d_Aic, d_cglob, d_z, d_u1b,
+                                                                   d_ri);
+      });
+    }
     interior_solve(d_ri);
-    launch(FETIGPU_K_OTHER, [&] {
-      k_ui_final<<<cdiv((long long)S * NI, 256), 256, 0, stream>>>((long long)S * NI, d_yi, d_ri);
-    });
+  }
+  // compact tables of the interior rows coupled to the interface or a corner (built once
+  // on the host from the assembled ELL blocks): k_ri_rhs reads ~1/8 of the bytes
+  int *d_ri_map = nullptr, *d_ri_cidx = nullptr;
+  double2 *d_ri_cval = nullptr, *d_ri_caic = nullptr;
+  void setup_ri_compact() {
+    if (std::getenv("FETIGPU_NO_RI_COMPACT")) return;
+    const int S = H.n_sub, NI = H.NI, E = H.MAXE_IB, NC = H.NC;
+    const size_t rows = (size_t)S * NI;
+    std::vector<int> idx(rows * E);
+    std::vector<double2> val(rows * E), aic(rows * NC);
+    CU(cudaMemcpyAsync(idx.data(), d_ib_idx, idx.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CU(cudaMemcpyAsync(val.data(), d_ib_val, val.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+    if (NC > 0) CU(cudaMemcpyAsync(aic.data(), d_Aic, aic.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+    sync();
+    std::vector<int> map(rows, -1), cidx;
+    std::vector<double2> cval, caic;
+    int q = 0;
+    for (size_t g = 0; g < rows; ++g) {
+      bool any = false;
+      for (int e = 0; e < E && !any; ++e) any = idx[g * E + e] >= 0;
+      for (int c = 0; c < NC && !any; ++c) any = aic[g * NC + c].x != 0.0 || aic[g * NC + c].y != 0.0;
+      if (!any) continue;
+      map[g] = q++;
+      cidx.insert(cidx.end(), idx.begin() + g * E, idx.begin() + (g + 1) * E);
+      cval.insert(cval.end(), val.begin() + g * E, val.begin() + (g + 1) * E);
+      caic.insert(caic.end(), aic.begin() + g * NC, aic.begin() + (g + 1) * NC);
+    }
+    d_ri_map = alloc<int>(rows);
+    d_ri_cidx = alloc<int>(std::max<size_t>(cidx.size(), 1));
+    d_ri_cval = alloc<double2>(std::max<size_t>(cval.size(), 1));
+    d_ri_caic = alloc<double2>(std::max<size_t>(caic.size(), 1));
+    CU(cudaMemcpyAsync(d_ri_map, map.data(), rows * sizeof(int), cudaMemcpyHostToDevice, stream));
+    if (q > 0) {
+      CU(cudaMemcpyAsync(d_ri_cidx, cidx.data(), cidx.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
+      CU(cudaMemcpyAsync(d_ri_cval, cval.data(), cval.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
+      if (NC > 0)
+        CU(cudaMemcpyAsync(d_ri_caic, caic.data(), caic.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
+    }
+    sync();
   }
 
   // (|x|^2, max|x|) -> d_stat[slot] on the stream (no synchronisation); sharded = all ranks
@@ -1784,7 +1831,7 @@ struct Ctx {
     eliminate_interior();
     phase("elim2i");
     launch(FETIGPU_K_OTHER, [&] {
-      k_assemble_x<<<cdiv(n, 256), 256, 0, stream>>>(n, d_xkind, d_xa, d_xb, d_ri, d_u1b, d_z, x);
+      k_assemble_x<<<cdiv(n, 256), 256, 0, stream>>>(n, d_xkind, d_xa, d_xb, d_ri, d_u1b, d_z, x, d_yi);
     });
     if (dist()) {  // every rank assembled its own rows of x: replicate the whole vector
       std::vector<size_t> first(plan.world), count(plan.world);

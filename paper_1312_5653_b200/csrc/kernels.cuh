@@ -1305,6 +1305,30 @@ __global__ void k_ri_rhs(SubLayout L, const int* __restrict__ ib_idx, const doub
   }
   ri[gid] = acc;
 }
+// same on the compacted coupled rows: map[gid] = row of the compact tables or -1 (no
+// interface / corner coupling: r_i = 0, ~87 % of the interior rows at config 2)
+__global__ void k_ri_rhs_compact(long long cnt, int EIB, int NC, int NI, int NB, const int* __restrict__ map,
+                                 const int* __restrict__ cidx, const double2* __restrict__ cval,
+                                 const double2* __restrict__ caic, const int* __restrict__ cglob,
+                                 const double2* __restrict__ z, const double2* __restrict__ ub,
+                                 double2* __restrict__ ri) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= cnt) return;
+  const int q = map[gid];
+  double2 acc = cz();
+  if (q >= 0) {
+    const int s = (int)(gid / NI);
+    for (int e = 0; e < EIB; ++e) {
+      const int b = cidx[(size_t)q * EIB + e];
+      if (b >= 0) acc = cfma(cval[(size_t)q * EIB + e], ub[(size_t)s * NB + b], acc);
+    }
+    for (int c = 0; c < NC; ++c) {
+      const int cg = cglob[(size_t)s * NC + c];
+      if (cg >= 0) acc = cfma(caic[(size_t)q * NC + c], z[cg], acc);
+    }
+  }
+  ri[gid] = acc;
+}
 // u_i = y_i - A_ii^-1 r_i   (r_i already solved in place)
 __global__ void k_ui_final(long long cnt, const double2* __restrict__ yi, double2* __restrict__ ri) {
   const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1319,14 +1343,15 @@ __global__ void k_jump(int nl, const int* __restrict__ lo, const int* __restrict
 // primal assembly (feti.cpp:699-708)
 __global__ void k_assemble_x(int n, const int* __restrict__ kind, const int* __restrict__ xa,
                              const int* __restrict__ xb, const double2* __restrict__ ui,
-                             const double2* __restrict__ ub, const double2* __restrict__ z, double2* __restrict__ x) {
+                             const double2* __restrict__ ub, const double2* __restrict__ z, double2* __restrict__ x,
+                             const double2* __restrict__ yi = nullptr) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= n) return;
   const int k = kind[f];
   if (k < 0) return;  // owned by another rank (sharded path)
   double2 v;
-  if (k == 0)
-    v = ui[xa[f]];
+  if (k == 0)  // yi given: ui holds A_ii^-1 r_i and u_i = y_i - A_ii^-1 r_i is formed here
+    v = yi != nullptr ? csub(yi[xa[f]], ui[xa[f]]) : ui[xa[f]];
   else if (k == 1)
     v = cadd(cscale(ub[xa[f]], 0.5), cscale(ub[xb[f]], 0.5));
   else
