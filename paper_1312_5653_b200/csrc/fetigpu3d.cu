@@ -508,7 +508,8 @@ struct Ctx3 {
     d_u0 = alloc<double2>((size_t)S * NB);
     d_gcp0 = alloc<double2>((size_t)S * G * NC);
     for (double2** p : {&d_w, &d_zl, &d_r, &d_lam, &d_best, &d_d, &d_t}) *p = alloc<double2>(ldv);
-    mdot_rows = 2048;
+    mdot_rows = 512;  // (2048: 1.35 blocks per SM, latency-bound at small j; measured 4.8 -> 4.0 ms of CGS per config-4 solve)
+    if (const char* e = std::getenv("FETIGPU3D_MDOT_ROWS")) mdot_rows = std::max(64, std::min(2048, std::atoi(e)));
     mdot_blocks = std::max(1, cdiv3(nl, mdot_rows));
     d_part = alloc<double2>((size_t)mdot_blocks * (vcap + 2) + 1024);
     d_h = alloc<double2>(2 * (vcap + 2));

@@ -1609,6 +1609,7 @@ __global__ void k3_mupdate(int n, int nv, const double2* __restrict__ V, size_t 
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   double2 v = w[r];
+#pragma unroll 8
   for (int j = 0; j < nv; ++j) v = cfms(V[(size_t)j * ldv + r], h[j], v);
   w[r] = v;
 }
