@@ -301,3 +301,23 @@ def test_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
     assert not ref["converged"] and ref["iterations"] == 4
     assert abs(st["relative_residual"] - ref["relative_residual"]) <= 1e-6 * ref["relative_residual"]
     assert np.linalg.norm(x - ref_x) <= 1e-8 * np.linalg.norm(ref_x)
+
+
+@pytest.mark.parametrize("switch", ["FETIGPU_NO_ZBASIS", "FETIGPU_NO_RI_COMPACT", "FETIGPU_NO_ELIM_REUSE",
+                                    "FETIGPU_NO_DEFER", "FETIGPU_NO_SPLIT"])
+def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
+    """Each reuse/fusion of the solve path (preconditioned basis Z, compact interior rhs,
+    GEMV-free final elimination, deferred GMRES completion, Givens folded into the next
+    GEMV) against the plain path it replaces: same iterations, results equal to rounding."""
+    p = fetigpu.make_seeded_problem(128, 1e-4, seed=3)
+    solver = fetigpu.SchurSolver(p, 8, 8, tol=1e-10)
+    a = solver.solve()
+    solver.close()
+    monkeypatch.setenv(switch, "1")
+    solver = fetigpu.SchurSolver(p, 8, 8, tol=1e-10)
+    b = solver.solve()
+    solver.close()
+    for side in ("plus_stats", "minus_stats"):
+        assert a[side]["iterations"] == b[side]["iterations"]
+    for k in ("y", "u", "lambda"):
+        assert rel(a[k], b[k]) <= 1e-11, k
