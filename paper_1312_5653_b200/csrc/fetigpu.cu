@@ -937,24 +937,54 @@ struct Ctx {
     std::vector<double> cx, dx, cy, dy;
     factor(i0, i1, P.nx, cx, dx);
     factor(j0, j1, P.ny, cy, dy);
+    if (const char* e = std::getenv("FETIGPU_TRI_X")) tri_x = std::atoi(e);
+    if (const char* e = std::getenv("FETIGPU_TRI_Y")) tri_y = std::atoi(e);
+    if (const char* e = std::getenv("FETIGPU_TRI_ROWS")) tri_rows_lpb = std::atoi(e);
     d_mx_cp = upload(cx);
     d_mx_dinv = upload(dx);
     d_my_cp = upload(cy);
     d_my_dinv = upload(dy);
   }
 
+  // lines per block (FETIGPU_TRI_X / FETIGPU_TRI_Y for experiments): few lines per block so
+  // that the ~1000 lines of config 2 spread over every SM
+  int tri_x = 8, tri_y = 8, tri_rows_lpb = 2;
+  template <int LPB, bool SEG_FAST>
+  void tri_launch(double* v, int nlines, int len, int G, long long S1, long long S2, long long es, const double* cp,
+                  const double* dinv) {
+    const dim3 blk = SEG_FAST ? dim3(32, LPB) : dim3(LPB, 32);
+    launch(FETIGPU_K_GLOBAL, [&] {
+      k_tridiag_lines<LPB, SEG_FAST><<<cdiv((long long)nlines, LPB), blk, 0, stream>>>(v, nlines, len, G, S1, S2, es,
+                                                                                        cp, dinv, moff);
+    });
+  }
   void mass_solve(double* v) {  // in place, V^-1 v
     const int dpn = P.dpn;
     // along x: Ly*dpn lines of Lx entries, stride dpn
-    launch(FETIGPU_K_GLOBAL, [&] {
-      k_tridiag_lines<8, true><<<cdiv((long long)Ly * dpn, 8), dim3(32, 8), 0, stream>>>(
-          v, Ly * dpn, Lx, dpn, (long long)Lx * dpn, 1, dpn, d_mx_cp, d_mx_dinv, moff);
-    });
+    {
+      const int nl = Ly * dpn;
+      const long long S1 = (long long)Lx * dpn;
+      const size_t sm = (size_t)(tri_rows_lpb + 2) * (Lx + Lx / 32 + 1) * sizeof(double);
+      if (dpn == 1 && Lx <= 32 * 32 && tri_rows_lpb > 0 && sm <= 48 * 1024) {  // staged rows (coalesced)
+        launch(FETIGPU_K_GLOBAL, [&] {
+          if (tri_rows_lpb == 4)
+            k_tridiag_rows<4><<<cdiv((long long)nl, 4), dim3(32, 4), sm, stream>>>(v, nl, Lx, d_mx_cp, d_mx_dinv, moff);
+          else
+            k_tridiag_rows<2><<<cdiv((long long)nl, 2), dim3(32, 2), sm, stream>>>(v, nl, Lx, d_mx_cp, d_mx_dinv, moff);
+        });
+      } else if (tri_x == 2) tri_launch<2, true>(v, nl, Lx, dpn, S1, 1, dpn, d_mx_cp, d_mx_dinv);
+      else if (tri_x == 4) tri_launch<4, true>(v, nl, Lx, dpn, S1, 1, dpn, d_mx_cp, d_mx_dinv);
+      else tri_launch<8, true>(v, nl, Lx, dpn, S1, 1, dpn, d_mx_cp, d_mx_dinv);
+    }
     // along y: Lx*dpn lines of Ly entries, stride Lx*dpn
-    launch(FETIGPU_K_GLOBAL, [&] {
-      k_tridiag_lines<32, false><<<cdiv((long long)Lx * dpn, 32), dim3(32, 32), 0, stream>>>(
-          v, Lx * dpn, Ly, 1, 1, 0, (long long)Lx * dpn, d_my_cp, d_my_dinv, moff);
-    });
+    {
+      const int nl = Lx * dpn;
+      const long long es = (long long)Lx * dpn;
+      if (tri_y == 4) tri_launch<4, false>(v, nl, Ly, 1, 1, 0, es, d_my_cp, d_my_dinv);
+      else if (tri_y == 8) tri_launch<8, false>(v, nl, Ly, 1, 1, 0, es, d_my_cp, d_my_dinv);
+      else if (tri_y == 16) tri_launch<16, false>(v, nl, Ly, 1, 1, 0, es, d_my_cp, d_my_dinv);
+      else tri_launch<32, false>(v, nl, Ly, 1, 1, 0, es, d_my_cp, d_my_dinv);
+    }
   }
 
   // 9-point stencils of K and M when the free dofs are exactly the interior grid nodes

@@ -2549,19 +2549,171 @@ template <int LPB, bool SEG_FAST>
 __global__ void __launch_bounds__(32 * LPB)
     k_tridiag_lines(double* __restrict__ v, int nlines, int len, int G, long long S1, long long S2, long long es,
                     const double* __restrict__ cp, const double* __restrict__ dinv, double off) {
+  // segments of up to MAXL entries live in registers: one batch of independent loads, the
+  // four recurrences on registers, one batch of stores (the in-place global version waits
+  // on a load behind every store: 58 us -> see DESIGN §4)
+  constexpr int MAXL = 32;
   __shared__ double sa[LPB][33], sb[LPB][33], sx[LPB][33];
   const int seg = SEG_FAST ? threadIdx.x : threadIdx.y, ly = SEG_FAST ? threadIdx.y : threadIdx.x;
   const int line = blockIdx.x * LPB + ly;
   const bool act = line < nlines;
   double* p = v + (act ? (long long)(line / G) * S1 + (long long)(line % G) * S2 : 0);
   const int L = (len + 31) / 32;
-  const int i0 = min(len, seg * L), i1 = min(len, i0 + L);
+  const int i0 = min(len, seg * L), i1 = min(len, i0 + L), cnt = i1 - i0;
+  const bool reg = L <= MAXL;
+  double r[MAXL];
+  if (reg) {
+#pragma unroll
+    for (int k = 0; k < MAXL; ++k) r[k] = (act && k < cnt) ? p[(long long)(i0 + k) * es] : 0.0;
+  }
   // forward: compose x -> A + B x over the segment
   double a = 0.0, b = 1.0;
-  if (act)
-    for (int i = i0; i < i1; ++i) {
-      const double di = dinv[i];
-      a = fma(-off * di, a, p[(long long)i * es] * di);
+  if (act) {
+    if (reg) {
+#pragma unroll
+      for (int k = 0; k < MAXL; ++k)
+        if (k < cnt) {
+          const double di = dinv[i0 + k];
+          a = fma(-off * di, a, r[k] * di);
+          b *= -off * di;
+        }
+    } else {
+      for (int i = i0; i < i1; ++i) {
+        const double di = dinv[i];
+        a = fma(-off * di, a, p[(long long)i * es] * di);
+        b *= -off * di;
+      }
+    }
+  }
+  sa[ly][seg] = a;
+  sb[ly][seg] = b;
+  __syncthreads();
+  if (seg == 0) {
+    double x = 0.0;
+    for (int q = 0; q < 32; ++q) {
+      sx[ly][q] = x;
+      x = fma(sb[ly][q], x, sa[ly][q]);
+    }
+  }
+  __syncthreads();
+  double x = sx[ly][seg];
+  if (act) {
+    if (reg) {
+#pragma unroll
+      for (int k = 0; k < MAXL; ++k)
+        if (k < cnt) {
+          x = (r[k] - off * x) * dinv[i0 + k];
+          r[k] = x;
+        }
+    } else {
+      for (int i = i0; i < i1; ++i) {
+        x = (p[(long long)i * es] - off * x) * dinv[i];
+        p[(long long)i * es] = x;
+      }
+    }
+  }
+  // backward: x_i = d'_i - cp_i x_{i+1}
+  a = 0.0;
+  b = 1.0;
+  if (act) {
+    if (reg) {
+#pragma unroll
+      for (int k = MAXL - 1; k >= 0; --k)
+        if (k < cnt) {
+          a = fma(-cp[i0 + k], a, r[k]);
+          b *= -cp[i0 + k];
+        }
+    } else {
+      for (int i = i1 - 1; i >= i0; --i) {
+        a = fma(-cp[i], a, p[(long long)i * es]);
+        b *= -cp[i];
+      }
+    }
+  }
+  __syncthreads();
+  sa[ly][seg] = a;
+  sb[ly][seg] = b;
+  __syncthreads();
+  if (seg == 0) {
+    double xx = 0.0;
+    for (int q = 31; q >= 0; --q) {
+      sx[ly][q] = xx;
+      xx = fma(sb[ly][q], xx, sa[ly][q]);
+    }
+  }
+  __syncthreads();
+  x = sx[ly][seg];
+  if (act) {
+    if (reg) {
+#pragma unroll
+      for (int k = MAXL - 1; k >= 0; --k)
+        if (k < cnt) {
+          x = r[k] - cp[i0 + k] * x;
+          r[k] = x;
+        }
+#pragma unroll
+      for (int k = 0; k < MAXL; ++k)
+        if (k < cnt) p[(long long)(i0 + k) * es] = r[k];
+    } else {
+      for (int i = i1 - 1; i >= i0; --i) {
+        x = p[(long long)i * es] - cp[i] * x;
+        p[(long long)i * es] = x;
+      }
+    }
+  }
+}
+// Contiguous lines (x direction, one dof per node): the block's LPB lines (one contiguous
+// range of LPB * len doubles) are staged through shared memory with coalesced loads and
+// stores; segment k of a line is read from a padded layout (one pad per 32 entries: lanes
+// reading entry k of their segments hit 32 different banks), then the same register
+// recurrences as k_tridiag_lines.  len <= 32 * 32.
+template <int LPB>
+__global__ void __launch_bounds__(32 * LPB)
+    k_tridiag_rows(double* __restrict__ v, int nlines, int len, const double* __restrict__ cp,
+                   const double* __restrict__ dinv, double off) {
+  constexpr int MAXL = 32;
+  extern __shared__ double tr_sh[];
+  __shared__ double sa[LPB][33], sb[LPB][33], sx[LPB][33];
+  const int seg = threadIdx.x, ly = threadIdx.y;
+  const int line0 = blockIdx.x * LPB, nb = min(LPB, nlines - line0);
+  const int stride = len + len / 32 + 1;  // padded line length in shared memory
+  double* base = v + (long long)line0 * len;
+  const int tid = threadIdx.y * 32 + threadIdx.x, tot = nb * len;
+  constexpr int NT = 32 * LPB, UB = 16;  // 16 loads in flight per thread
+  for (int e0 = tid; e0 < tot; e0 += UB * NT) {
+    double t[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) t[u] = e0 + u * NT < tot ? base[e0 + u * NT] : 0.0;
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int e = e0 + u * NT;
+      if (e < tot) {
+        const int l = e / len, i = e - l * len;
+        tr_sh[l * stride + i + i / 32] = t[u];
+      }
+    }
+  }
+  // the line-independent Thomas coefficients, same padded layout (conflict-free per lane)
+  double* sdinv = tr_sh + LPB * stride;
+  double* scp = sdinv + stride;
+  for (int i = tid; i < len; i += NT) {
+    sdinv[i + i / 32] = dinv[i];
+    scp[i + i / 32] = cp[i];
+  }
+  __syncthreads();
+  const bool act = ly < nb;
+  const int L = (len + 31) / 32;
+  const int i0 = min(len, seg * L), i1 = min(len, i0 + L), cnt = i1 - i0;
+  double* sl = tr_sh + ly * stride;
+  double r[MAXL];
+#pragma unroll
+  for (int k = 0; k < MAXL; ++k) r[k] = (act && k < cnt) ? sl[i0 + k + (i0 + k) / 32] : 0.0;
+  double a = 0.0, b = 1.0;
+#pragma unroll
+  for (int k = 0; k < MAXL; ++k)
+    if (k < cnt) {
+      const double di = sdinv[i0 + k + (i0 + k) / 32];
+      a = fma(-off * di, a, r[k] * di);
       b *= -off * di;
     }
   sa[ly][seg] = a;
@@ -2576,18 +2728,19 @@ __global__ void __launch_bounds__(32 * LPB)
   }
   __syncthreads();
   double x = sx[ly][seg];
-  if (act)
-    for (int i = i0; i < i1; ++i) {
-      x = (p[(long long)i * es] - off * x) * dinv[i];
-      p[(long long)i * es] = x;
+#pragma unroll
+  for (int k = 0; k < MAXL; ++k)
+    if (k < cnt) {
+      x = (r[k] - off * x) * sdinv[i0 + k + (i0 + k) / 32];
+      r[k] = x;
     }
-  // backward: x_i = d'_i - cp_i x_{i+1}
   a = 0.0;
   b = 1.0;
-  if (act)
-    for (int i = i1 - 1; i >= i0; --i) {
-      a = fma(-cp[i], a, p[(long long)i * es]);
-      b *= -cp[i];
+#pragma unroll
+  for (int k = MAXL - 1; k >= 0; --k)
+    if (k < cnt) {
+      a = fma(-scp[i0 + k + (i0 + k) / 32], a, r[k]);
+      b *= -scp[i0 + k + (i0 + k) / 32];
     }
   __syncthreads();
   sa[ly][seg] = a;
@@ -2602,11 +2755,20 @@ __global__ void __launch_bounds__(32 * LPB)
   }
   __syncthreads();
   x = sx[ly][seg];
-  if (act)
-    for (int i = i1 - 1; i >= i0; --i) {
-      x = p[(long long)i * es] - cp[i] * x;
-      p[(long long)i * es] = x;
+#pragma unroll
+  for (int k = MAXL - 1; k >= 0; --k)
+    if (k < cnt) {
+      x = r[k] - scp[i0 + k + (i0 + k) / 32] * x;
+      r[k] = x;
     }
+#pragma unroll
+  for (int k = 0; k < MAXL; ++k)
+    if (act && k < cnt) sl[i0 + k + (i0 + k) / 32] = r[k];
+  __syncthreads();
+  for (int e = threadIdx.y * 32 + threadIdx.x; e < nb * len; e += 32 * LPB) {
+    const int l = e / len, i = e - l * len;
+    base[e] = tr_sh[l * stride + i + i / 32];
+  }
 }
 // y = ybar - v ; u = lam / phi ; lam = Re t ; leak partial
 __global__ void k_realify(int n, const double2* __restrict__ t, double* __restrict__ lam) {
