@@ -404,7 +404,11 @@ struct Ctx {
   }
   // x = A_ii^-1 x in place for one right-hand side per subdomain (stride NI)
   void interior_solve(double2* X) {
-    if (use_bt) {
+    if (use_fdm) {
+      launch(FETIGPU_K_BAND, [&] {
+        k_fdm_solve<<<H.n_sub, 256, 0, stream>>>(X, (size_t)H.NI, fdm_mx, fdm_my, d_fdm_sx, d_fdm_sy, d_fdm_invd);
+      });
+    } else if (use_bt) {
       launch(FETIGPU_K_BAND, [&] {
         k_bt_solve<kBtStages><<<H.n_sub, 32, bt_solve_smem<kBtStages>(), stream>>>(d_bt, bt_nb, H.NI, X,
                                                                                     (size_t)H.NI);
@@ -414,6 +418,76 @@ struct Ctx {
     }
   }
   static constexpr int kBtStages = 2;
+  // Separable interior solve (k_fdm_solve): heat on the structured mesh, every subdomain
+  // interior the same mx x my grid in x-fastest order and the element matrices exactly the
+  // Kronecker sums of the 1D Q1 matrices (checked here entry by entry; otherwise the
+  // block-Thomas substitution serves).  FETIGPU_NO_FDM=1 disables it.
+  bool use_fdm = false;
+  int fdm_mx = 0, fdm_my = 0;
+  double *d_fdm_sx = nullptr, *d_fdm_sy = nullptr;
+  double2* d_fdm_invd = nullptr;
+  void setup_fdm() {
+    if (std::getenv("FETIGPU_NO_FDM") || P.dpn != 1 || P.physics != 0) return;
+    const int mx = H.ex - 1, my = H.ey - 1;
+    if (mx < 1 || my < 1 || mx > 32 || my > 32 || H.NI != mx * my) return;
+    for (int s = 0; s < H.n_sub; ++s) {
+      if (H.n_i[s] != mx * my) return;
+      for (int k = 0; k < mx * my; ++k) {
+        const int node = P.node_id(H.sub_i0[s] + 1 + k % mx, H.sub_j0[s] + 1 + k / mx);
+        if (P.free_map[node] < 0 || H.idof[(size_t)s * H.NI + k] != P.free_map[node]) return;
+      }
+    }
+    // element stencils of K and M against the Kronecker forms (element corners (0,0) (1,0)
+    // (1,1) (0,1), as setup_stencil)
+    const double h = P.h;
+    const double K1[3] = {-1.0 / h, 2.0 / h, -1.0 / h}, M1[3] = {h / 6.0, 4.0 * h / 6.0, h / 6.0};
+    double sk[9] = {}, sm[9] = {};
+    const int dx[4] = {0, 1, 1, 0}, dy[4] = {0, 0, 1, 1};
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) {
+        const int o = (dy[b] - dy[a] + 1) * 3 + (dx[b] - dx[a] + 1);
+        sk[o] += P.ke[a * 4 + b];
+        sm[o] += P.me[a * 4 + b];
+      }
+    for (int oy = 0; oy < 3; ++oy)
+      for (int ox = 0; ox < 3; ++ox) {
+        const double ek = K1[ox] * M1[oy] + M1[ox] * K1[oy], em = M1[ox] * M1[oy];
+        if (std::abs(sk[oy * 3 + ox] - ek) > 1e-13 * std::abs(K1[1] * M1[1]) ||
+            std::abs(sm[oy * 3 + ox] - em) > 1e-13 * std::abs(M1[1] * M1[1]))
+          return;
+      }
+    auto dst = [](int m, std::vector<double>& S, std::vector<double>& ka, std::vector<double>& nu, double h) {
+      S.assign(32 * 32, 0.0);
+      ka.assign(32, 0.0);
+      nu.assign(32, 0.0);
+      const double c = std::sqrt(2.0 / (m + 1)), pi = std::acos(-1.0);
+      for (int i = 0; i < m; ++i)
+        for (int k = 0; k < m; ++k) S[i * 32 + k] = c * std::sin(pi * (double)(i + 1) * (k + 1) / (m + 1));
+      for (int k = 0; k < m; ++k) {
+        const double cs = std::cos(pi * (k + 1) / (m + 1));
+        ka[k] = (2.0 - 2.0 * cs) / h;
+        nu[k] = h * (4.0 + 2.0 * cs) / 6.0;
+      }
+    };
+    std::vector<double> Sx, Sy, kx, nx, ky, ny;
+    dst(mx, Sx, kx, nx, h);
+    dst(my, Sy, ky, ny, h);
+    std::vector<double2> inv(32 * 32, make_double2(0.0, 0.0));
+    for (int j = 0; j < my; ++j)
+      for (int i = 0; i < mx; ++i) {
+        const cd d = cd(ny[j] * kx[i] + ky[j] * nx[i]) + mc * (ny[j] * nx[i]);
+        const cd r = 1.0 / d;
+        inv[j * 32 + i] = make_double2(r.real(), r.imag());
+      }
+    d_fdm_sx = upload(Sx);
+    d_fdm_sy = upload(Sy);
+    d_fdm_invd = alloc<double2>(32 * 32);
+    CU(cudaMemcpyAsync(d_fdm_invd, inv.data(), inv.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
+    sync();
+    fdm_mx = mx;
+    fdm_my = my;
+    use_fdm = true;
+  }
   // Augmented coarse problem (feti.cpp:440-475): dense assembly in [corners | columns]
   // order, symmetric equilibration 1/sqrt|C_ii|, in-place Gauss-Jordan inverse with partial
   // pivoting (pivots = the U_kk of PartialPivLU), the reference's pivot check, unscaling.
@@ -880,6 +954,7 @@ struct Ctx {
     setup_mass();
     setup_stencil();
     setup_ri_compact();
+    setup_fdm();
     setup_l2_persistence();
     sync();
     setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -2077,6 +2152,7 @@ struct Ctx {
       case FETIGPU_K_DUAL_GEMV:  // packed S_bb^-1 + coupling_b + vectors
         return 16.0 * (S * sym_tile_entries(NT) + S * NB * H.NC + 3.0 * S * NB + S * H.NC) + 12.0 * S * NB;
       case FETIGPU_K_BAND:  // one single-RHS interior solve: factor records of both sweeps + vector in/out
+        if (use_fdm) return 16.0 * 2.0 * S * H.NI;  // separable solve: the vector in and out
         if (use_bt) return 16.0 * (S * (2.0 * bt_nb - 1.0) * BT_HALF + 3.0 * S * H.NI);
         return 16.0 * (2.0 * S * H.NI * (Wt + 1) + 3.0 * S * H.NI);
       case FETIGPU_K_COARSE:

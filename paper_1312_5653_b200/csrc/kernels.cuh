@@ -2770,6 +2770,106 @@ __global__ void __launch_bounds__(32 * LPB)
     base[e] = tr_sh[l * stride + i + i / 32];
   }
 }
+// ------------------------------------------------------------------ separable interior solve
+// Heat on the structured mesh: every subdomain interior is the same mx x my grid and
+//   A_ii = K1x (x) M1y + M1x (x) K1y + mc M1x (x) M1y        (Q1 on squares, exact)
+// with K1 = tridiag(-1, 2, -1)/h, M1 = h tridiag(1, 4, 1)/6 on mx (my) interior nodes.  Both
+// are diagonalised by the orthonormal, symmetric DST-I matrix S (S S = I), so
+//   A_ii^-1 X = Sy ((Sy X Sx) ./ D) Sx,   D[j][i] = nu_y,j ka_x,i + ka_y,j nu_x,i + mc nu_y,j nu_x,i
+// (fast diagonalisation: an exact direct solve).  One CTA per subdomain; the four real
+// 32 x 32 x 32 products per plane run on the FP64 tensor cores (mma.sync m8n8k4): each
+// warp owns one 8-row block and two 8-column blocks of both the real and the imaginary
+// plane, so the division by D happens on the accumulator fragments.
+__device__ __forceinline__ void fdm_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+constexpr int FDM_LD = 36;  // padded row of a 32 x 32 plane in shared memory
+__global__ void __launch_bounds__(256) k_fdm_solve(double2* __restrict__ X, size_t ldx, int mx, int my,
+                                                   const double* __restrict__ Sx, const double* __restrict__ Sy,
+                                                   const double2* __restrict__ invD) {
+  __shared__ double pre[32 * FDM_LD], pim[32 * FDM_LD], qre[32 * FDM_LD], qim[32 * FDM_LD];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double2* x = X + (size_t)blockIdx.x * ldx;
+  const int n = mx * my;
+  pdl_trigger();
+  pdl_wait();
+  for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+    const int j = e >> 5, i = e & 31;
+    double2 v = make_double2(0.0, 0.0);
+    if (j < my && i < mx) v = x[j * mx + i];
+    pre[j * FDM_LD + i] = v.x;
+    pim[j * FDM_LD + i] = v.y;
+  }
+  __syncthreads();
+  const int rb = (warp & 3) * 8, cb = (warp >> 2) * 16;  // rows rb..rb+7, columns cb..cb+15
+  double cr[2][2], ci[2][2];
+  // left product: C = Sy P (A = Sy, B = P)
+  auto left = [&](const double* Pr, const double* Pi) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) cr[q][0] = cr[q][1] = ci[q][0] = ci[q][1] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < 32; k0 += 4) {
+      const double a = __ldg(Sy + (rb + g) * 32 + k0 + t);  // (8 KB, L1-resident)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        fdm_dmma(cr[q][0], cr[q][1], a, Pr[(k0 + t) * FDM_LD + cb + 8 * q + g]);
+        fdm_dmma(ci[q][0], ci[q][1], a, Pi[(k0 + t) * FDM_LD + cb + 8 * q + g]);
+      }
+    }
+  };
+  // right product: C = P Sx (A = P, B = Sx)
+  auto right = [&](const double* Pr, const double* Pi) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) cr[q][0] = cr[q][1] = ci[q][0] = ci[q][1] = 0.0;
+#pragma unroll
+    for (int k0 = 0; k0 < 32; k0 += 4) {
+      const double ar = Pr[(rb + g) * FDM_LD + k0 + t], ai = Pi[(rb + g) * FDM_LD + k0 + t];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const double b = __ldg(Sx + (k0 + t) * 32 + cb + 8 * q + g);
+        fdm_dmma(cr[q][0], cr[q][1], ar, b);
+        fdm_dmma(ci[q][0], ci[q][1], ai, b);
+      }
+    }
+  };
+  auto store = [&](double* Qr, double* Qi) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        Qr[(rb + g) * FDM_LD + cb + 8 * q + 2 * t + e] = cr[q][e];
+        Qi[(rb + g) * FDM_LD + cb + 8 * q + 2 * t + e] = ci[q][e];
+      }
+  };
+  left(pre, pim);
+  store(qre, qim);
+  __syncthreads();
+  right(qre, qim);
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {  // divide by D (zero in the padding)
+      const double2 d = invD[(rb + g) * 32 + cb + 8 * q + 2 * t + e];
+      const double a = cr[q][e], b = ci[q][e];
+      cr[q][e] = a * d.x - b * d.y;
+      ci[q][e] = a * d.y + b * d.x;
+    }
+  store(pre, pim);
+  __syncthreads();
+  left(pre, pim);
+  store(qre, qim);
+  __syncthreads();
+  right(qre, qim);
+  store(pre, pim);
+  __syncthreads();
+  for (int e = threadIdx.x; e < n; e += 256) {
+    const int j = e / mx, i = e - j * mx;
+    x[e] = make_double2(pre[j * FDM_LD + i], pim[j * FDM_LD + i]);
+  }
+}
+
 // y = ybar - v ; u = lam / phi ; lam = Re t ; leak partial
 __global__ void k_realify(int n, const double2* __restrict__ t, double* __restrict__ lam) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;

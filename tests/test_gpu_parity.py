@@ -304,7 +304,7 @@ def test_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
 
 
 @pytest.mark.parametrize("switch", ["FETIGPU_NO_ZBASIS", "FETIGPU_NO_RI_COMPACT", "FETIGPU_NO_ELIM_REUSE",
-                                    "FETIGPU_NO_DEFER", "FETIGPU_NO_SPLIT"])
+                                    "FETIGPU_NO_DEFER", "FETIGPU_NO_SPLIT", "FETIGPU_NO_FDM"])
 def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
     """Each reuse/fusion of the solve path (preconditioned basis Z, compact interior rhs,
     GEMV-free final elimination, deferred GMRES completion, Givens folded into the next
