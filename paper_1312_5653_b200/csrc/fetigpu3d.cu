@@ -529,6 +529,7 @@ struct Ctx3 {
     CU3(cudaMallocHost(&h_pin, sizeof(double2) * 4 * (vcap + 4)));
     setup_mass();
     setup_stencil();
+    setup_fdm();
     sync();
     setup_seconds = now() - t0;
     setup_t[7] = setup_seconds;
@@ -748,7 +749,64 @@ struct Ctx3 {
   // interior solves: the TMA-streamed kernel (default), or the direct-load one
   // (FETIGPU3D_SOLVE=direct: one warp per off-diagonal block, 8 warps up to P = 8, else 32)
   int solve_kind = -1;
+  // separable interior solve (k3_fdm_solve) for heat: FETIGPU3D_NO_FDM=1 disables it
+  bool use_fdm = false;
+  int fdm_m[3] = {0, 0, 0};
+  double *d_fdm_s[3] = {nullptr, nullptr, nullptr};
+  double2* d_fdm_invd = nullptr;
+  void setup_fdm() {
+    if (std::getenv("FETIGPU3D_NO_FDM") || P.dpn != 1 || P.physics != 0) return;
+    const int mx = H.ex - 1, my = H.ey - 1, mz = H.ez - 1, ni = mx * my * mz;
+    if (mx < 1 || my < 1 || mz < 1 || mx > 32 || my > 32 || mz > 32) return;
+    if (k3::fdm3_smem(ni) > 200 * 1024) return;
+    for (int s = 0; s < H.S; ++s) {
+      if (H.n_i[s] != ni) return;
+      for (int e = 0; e < ni; ++e) {
+        const int i = e % mx, j = (e / mx) % my, k = e / (mx * my);
+        const int node = P.node_id(H.sub_i0[s] + 1 + i, H.sub_j0[s] + 1 + j, H.sub_k0[s] + 1 + k);
+        if (P.free_map[node] < 0 || H.idof[(size_t)s * NI + e] != P.free_map[node]) return;
+      }
+    }
+    const double h = P.h, pi = std::acos(-1.0);
+    const int ms[3] = {mx, my, mz};
+    std::vector<double> ka[3], nu[3];
+    for (int a = 0; a < 3; ++a) {
+      const int m = ms[a];
+      std::vector<double> S(1024, 0.0);
+      const double c = std::sqrt(2.0 / (m + 1));
+      for (int i = 0; i < m; ++i)
+        for (int k = 0; k < m; ++k) S[i * 32 + k] = c * std::sin(pi * (double)(i + 1) * (k + 1) / (m + 1));
+      ka[a].assign(m, 0.0);
+      nu[a].assign(m, 0.0);
+      for (int k = 0; k < m; ++k) {
+        const double cs = std::cos(pi * (k + 1) / (m + 1));
+        ka[a][k] = (2.0 - 2.0 * cs) / h;
+        nu[a][k] = h * (4.0 + 2.0 * cs) / 6.0;
+      }
+      d_fdm_s[a] = upload(S);
+      fdm_m[a] = m;
+    }
+    std::vector<double2> inv(ni);
+    for (int e = 0; e < ni; ++e) {
+      const int i = e % mx, j = (e / mx) % my, k = e / (mx * my);
+      const double nx = nu[0][i], ny = nu[1][j], nz = nu[2][k];
+      const cd d = cd(ka[0][i] * ny * nz + nx * ka[1][j] * nz + nx * ny * ka[2][k]) + mc * (nx * ny * nz);
+      const cd r = 1.0 / d;
+      inv[e] = make_double2(r.real(), r.imag());
+    }
+    d_fdm_invd = upload(inv);
+    CU3(cudaFuncSetAttribute(k3::k3_fdm_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k3::fdm3_smem(ni)));
+    sync();
+    use_fdm = true;
+  }
   void interior_solve(double2* x) {
+    if (use_fdm) {
+      launch(FETIGPU_K_BAND, [&] {
+        k3::k3_fdm_solve<<<S, 512, k3::fdm3_smem(fdm_m[0] * fdm_m[1] * fdm_m[2]), stream>>>(
+            x, (size_t)NI, fdm_m[0], fdm_m[1], fdm_m[2], d_fdm_s[0], d_fdm_s[1], d_fdm_s[2], d_fdm_invd);
+      });
+      return;
+    }
     if (solve_kind < 0) {
       const char* e = std::getenv("FETIGPU3D_SOLVE");
       solve_kind = (e && std::string(e) == "direct") ? 0 : 1;
@@ -1300,6 +1358,8 @@ int fetigpu3d_profile_read(fetigpu3d_ctx* ctx, double* ms, long long* cnt, int r
 // (written once); DESIGN.md §9
 double fetigpu3d_class_bytes(fetigpu3d_ctx* ctx, int klass) {
   Ctx3& c = ctx->c;
+  if (klass == FETIGPU_K_BAND && c.use_fdm)  // separable solve: the vector in and out
+    return 2.0 * 16.0 * (double)c.S * c.fdm_m[0] * c.fdm_m[1] * c.fdm_m[2];
   if (klass == FETIGPU_K_BAND)  // one interior solve: all blocks forward, off-diagonal ones backward
     return 16.0 * 1024.0 * (double)c.S * c.NBK * (2.0 * c.PB + 1.0) + 3.0 * 16.0 * (double)c.S * c.NI;
   if (klass != FETIGPU_K_PRECOND_GEMV && klass != FETIGPU_K_DUAL_GEMV) return 0.0;
