@@ -2786,7 +2786,10 @@ __device__ __forceinline__ void fdm_dmma(double& d0, double& d1, double a, doubl
                : "d"(a), "d"(b));
 }
 constexpr int FDM_LD = 36;  // padded row of a 32 x 32 plane in shared memory
-__global__ void __launch_bounds__(256) k_fdm_solve(double2* __restrict__ X, size_t ldx, int mx, int my,
+#ifndef FETIGPU_FDM_MINB
+#define FETIGPU_FDM_MINB 3  // (80 registers: 3 CTAs per SM; measured 32.6 -> 29.6 us)
+#endif
+__global__ void __launch_bounds__(256, FETIGPU_FDM_MINB) k_fdm_solve(double2* __restrict__ X, size_t ldx, int mx, int my,
                                                    const double* __restrict__ Sx, const double* __restrict__ Sy,
                                                    const double2* __restrict__ invD) {
   __shared__ double pre[32 * FDM_LD], pim[32 * FDM_LD], qre[32 * FDM_LD], qim[32 * FDM_LD];
@@ -2795,12 +2798,19 @@ __global__ void __launch_bounds__(256) k_fdm_solve(double2* __restrict__ X, size
   const int n = mx * my;
   pdl_trigger();
   pdl_wait();
-  for (int e = threadIdx.x; e < 32 * 32; e += 256) {
-    const int j = e >> 5, i = e & 31;
-    double2 v = make_double2(0.0, 0.0);
-    if (j < my && i < mx) v = x[j * mx + i];
-    pre[j * FDM_LD + i] = v.x;
-    pim[j * FDM_LD + i] = v.y;
+  {  // all four loads of a thread in flight together
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + 256 * u, j = e >> 5, i = e & 31;
+      v[u] = (j < my && i < mx) ? x[j * mx + i] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = threadIdx.x + 256 * u, j = e >> 5, i = e & 31;
+      pre[j * FDM_LD + i] = v[u].x;
+      pim[j * FDM_LD + i] = v[u].y;
+    }
   }
   __syncthreads();
   const int rb = (warp & 3) * 8, cb = (warp >> 2) * 16;  // rows rb..rb+7, columns cb..cb+15
