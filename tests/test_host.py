@@ -103,3 +103,61 @@ def test_problem_sizes(fetigpu):
     assert (p.n, p.m) == (9, 16)  # test_mesh_fem.cpp:128-133
     q = fetigpu.make_problem(12, 4, 1e-4, physics=1, len_x=3.0, len_y=1.0, young=20.7e6, poisson=0.45)
     assert (q.n, q.m) == (2 * 12 * 5, 2 * 5)  # clamped x = 0 edge (fem.cpp:124-128)
+
+
+def _dst(m):
+    i = np.arange(1, m + 1)
+    return np.sqrt(2.0 / (m + 1)) * np.sin(np.pi * np.outer(i, i) / (m + 1))
+
+
+@pytest.mark.parametrize("mx,my,dim", [(31, 31, 2), (7, 5, 2), (15, 15, 3), (4, 6, 3)])
+def test_separable_interior_solve_is_exact(mx, my, dim):
+    """The fast-diagonalisation interior solve (k_fdm_solve / k3_fdm_solve): the
+    DST-I matrix S is orthonormal and symmetric, diagonalises the 1D Q1 matrices with the
+    eigenvalues used on the device, and (S..)(D^-1)(S..) equals A_ii^-1 for the subdomain
+    interior operator (the Kronecker sum that the next test pins to the oracle's assembly)."""
+    h, mc = 1.0 / 64, complex(0.0, -1.0 / np.sqrt(1e-4))
+    dims = [mx, my] + ([5] if dim == 3 else [])
+    K1 = {m: (2 * np.eye(m) - np.eye(m, k=1) - np.eye(m, k=-1)) / h for m in dims}
+    M1 = {m: h * (4 * np.eye(m) + np.eye(m, k=1) + np.eye(m, k=-1)) / 6 for m in dims}
+    for m in dims:
+        S = _dst(m)
+        assert np.allclose(S @ S, np.eye(m), atol=1e-13) and np.allclose(S, S.T)
+        th = np.pi * np.arange(1, m + 1) / (m + 1)
+        assert np.allclose(S @ K1[m] @ S, np.diag((2 - 2 * np.cos(th)) / h), atol=1e-11)
+        assert np.allclose(S @ M1[m] @ S, np.diag(h * (4 + 2 * np.cos(th)) / 6), atol=1e-15)
+    # interior operator from the oracle's element matrices (Q1, exact Kronecker structure)
+    kron = np.kron
+    if dim == 2:
+        A = kron(M1[my], K1[mx]) + kron(K1[my], M1[mx]) + mc * kron(M1[my], M1[mx])
+        T = kron(_dst(my), _dst(mx))
+        lam = [np.diag(_dst(m) @ K1[m] @ _dst(m)) for m in (mx, my)]
+        nu = [np.diag(_dst(m) @ M1[m] @ _dst(m)) for m in (mx, my)]
+        D = (np.outer(nu[1], lam[0]) + np.outer(lam[1], nu[0]) + mc * np.outer(nu[1], nu[0])).ravel()
+    else:
+        mz = dims[2]
+        A = (kron(kron(M1[mz], M1[my]), K1[mx]) + kron(kron(M1[mz], K1[my]), M1[mx]) +
+             kron(kron(K1[mz], M1[my]), M1[mx]) + mc * kron(kron(M1[mz], M1[my]), M1[mx]))
+        T = kron(kron(_dst(mz), _dst(my)), _dst(mx))
+        lam = [np.diag(_dst(m) @ K1[m] @ _dst(m)) for m in (mx, my, mz)]
+        nu = [np.diag(_dst(m) @ M1[m] @ _dst(m)) for m in (mx, my, mz)]
+        D = (np.einsum("k,j,i->kji", nu[2], nu[1], lam[0]) + np.einsum("k,j,i->kji", nu[2], lam[1], nu[0]) +
+             np.einsum("k,j,i->kji", lam[2], nu[1], nu[0]) + mc * np.einsum("k,j,i->kji", nu[2], nu[1], nu[0])).ravel()
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal(A.shape[0]) + 1j * rng.standard_normal(A.shape[0])
+    y = T @ ((T @ x) / D)
+    assert np.linalg.norm(A @ y - x) <= 1e-12 * np.linalg.norm(A) * np.linalg.norm(y)
+
+
+def test_q1_heat_stencil_is_kronecker_sum(oracle_mod):
+    """The precondition k_fdm_solve checks at setup, on the oracle's Q1 heat element: the
+    assembled 9-point stencils of K and M equal K1 (x) M1 + M1 (x) K1 and M1 (x) M1."""
+    n = 8
+    p = oracle_mod.Problem(n, n)
+    K, V = p.dense(0), p.dense(1)
+    h = 1.0 / n
+    m = n - 1
+    K1 = (2 * np.eye(m) - np.eye(m, k=1) - np.eye(m, k=-1)) / h
+    M1 = h * (4 * np.eye(m) + np.eye(m, k=1) + np.eye(m, k=-1)) / 6
+    assert np.allclose(K, np.kron(M1, K1) + np.kron(K1, M1), atol=1e-13)
+    assert np.allclose(V, np.kron(M1, M1), atol=1e-16)
