@@ -180,7 +180,7 @@ struct Ctx {
   int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_minb = 1, tail_rows = 512;
   bool cgs_gram = false;       // FETIGPU_CGS=gram: one-reduction CGS2 via the Gram matrix
   double2* d_gram = nullptr;
-  static constexpr int kBodyUnroll = 8;  // steps per WHILE-body execution (measured 4: 182.8, 8: 183.5 solves/s)
+  static constexpr int kBodyUnroll = 4;  // steps per WHILE-body execution (measured at config 2: 4 205.6, 8 204.9, 12 203.1 solves/s; earlier code 4: 182.8, 8: 183.5)
   int body_unroll = 1;
   unsigned int* d_bar = nullptr;
   unsigned long long* d_tstamp = nullptr;  // FETIGPU_TAIL_TIMES=1: per-phase timestamps
