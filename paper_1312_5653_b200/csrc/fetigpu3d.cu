@@ -802,7 +802,7 @@ struct Ctx3 {
   void interior_solve(double2* x) {
     if (use_fdm) {
       launch(FETIGPU_K_BAND, [&] {
-        k3::k3_fdm_solve<<<S, 512, k3::fdm3_smem(fdm_m[0] * fdm_m[1] * fdm_m[2]), stream>>>(
+        k3::k3_fdm_solve<<<S, 256, k3::fdm3_smem(fdm_m[0] * fdm_m[1] * fdm_m[2]), stream>>>(
             x, (size_t)NI, fdm_m[0], fdm_m[1], fdm_m[2], d_fdm_s[0], d_fdm_s[1], d_fdm_s[2], d_fdm_invd);
       });
       return;

@@ -1696,7 +1696,7 @@ __global__ void k3_recover(int n, const double* __restrict__ ybar, const double*
 // symmetric DST-I matrices S of each axis: A_ii^-1 X = T (T X ./ D) with T = Sz (x) Sy (x) Sx
 // applied axis by axis (fast diagonalisation, exact).  One CTA per subdomain; the grid
 // lives in shared memory (two ping-pong copies), one thread per output entry and axis pass.
-__global__ void __launch_bounds__(512) k3_fdm_solve(double2* __restrict__ X, size_t ldx, int mx, int my, int mz,
+__global__ void __launch_bounds__(256) k3_fdm_solve(double2* __restrict__ X, size_t ldx, int mx, int my, int mz,
                                                     const double* __restrict__ Sx, const double* __restrict__ Sy,
                                                     const double* __restrict__ Sz, const double2* __restrict__ invD) {
   extern __shared__ double2 f3_sh[];
@@ -1715,51 +1715,46 @@ __global__ void __launch_bounds__(512) k3_fdm_solve(double2* __restrict__ X, siz
   for (int e = threadIdx.x; e < n; e += blockDim.x) A[e] = x[e];
   __syncthreads();
   const int pxy = mx * my;
-  // out[e] = sum_q S[c][q] in[e with coordinate c of the axis replaced by q]
-  auto pass_x = [&](const double2* in, double2* out) {
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-      const int i = e % mx, row = e - i;
-      double2 acc = make_double2(0.0, 0.0);
-      for (int q = 0; q < mx; ++q) {
-        const double c = sx[i * 32 + q];
-        const double2 v = in[row + q];
-        acc.x = fma(c, v.x, acc.x);
-        acc.y = fma(c, v.y, acc.y);
+  // One thread per line of the axis: the line's <= 32 entries are loaded into registers once
+  // and all outputs of the line formed from them (S entries are warp-uniform broadcasts):
+  // out[c] = sum_q S[c][q] in[q] along the line.  FP64 FMA on registers instead of one
+  // shared-memory load per multiply-add.
+  auto pass = [&](const double2* in, double2* out, int len, int lines, int stride, const double* Sa,
+                  const double2* dv) {
+    for (int l = threadIdx.x; l < lines; l += blockDim.x) {
+      int base;
+      if (stride == 1) base = l * mx;                                   // x lines: (k, j)
+      else if (stride == mx) base = (l / mx) * pxy + (l % mx);          // y lines: (k, i)
+      else base = l;                                                    // z lines: (j, i)
+      double vr[32], vi[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const double2 v = q < len ? in[base + q * stride] : make_double2(0.0, 0.0);
+        vr[q] = v.x;
+        vi[q] = v.y;
       }
-      out[e] = acc;
+      for (int c = 0; c < len; ++c) {
+        double ar = 0.0, ai = 0.0;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const double sc = Sa[c * 32 + q];  // zero beyond len
+          ar = fma(sc, vr[q], ar);
+          ai = fma(sc, vi[q], ai);
+        }
+        const int e = base + c * stride;
+        if (dv != nullptr) {
+          const double2 d = dv[e];
+          out[e] = make_double2(ar * d.x - ai * d.y, ar * d.y + ai * d.x);
+        } else {
+          out[e] = make_double2(ar, ai);
+        }
+      }
     }
   };
-  auto pass_y = [&](const double2* in, double2* out) {
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-      const int k = e / pxy, r = e - k * pxy, j = r / mx, i = r - j * mx;
-      const double2* col = in + k * pxy + i;
-      double2 acc = make_double2(0.0, 0.0);
-      for (int q = 0; q < my; ++q) {
-        const double c = sy[j * 32 + q];
-        const double2 v = col[q * mx];
-        acc.x = fma(c, v.x, acc.x);
-        acc.y = fma(c, v.y, acc.y);
-      }
-      out[e] = acc;
-    }
-  };
+  auto pass_x = [&](const double2* in, double2* out) { pass(in, out, mx, my * mz, 1, sx, nullptr); };
+  auto pass_y = [&](const double2* in, double2* out) { pass(in, out, my, mx * mz, mx, sy, nullptr); };
   auto pass_z = [&](const double2* in, double2* out, bool divide) {
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-      const int k = e / pxy, r = e - k * pxy;
-      const double2* col = in + r;
-      double2 acc = make_double2(0.0, 0.0);
-      for (int q = 0; q < mz; ++q) {
-        const double c = sz[k * 32 + q];
-        const double2 v = col[q * pxy];
-        acc.x = fma(c, v.x, acc.x);
-        acc.y = fma(c, v.y, acc.y);
-      }
-      if (divide) {
-        const double2 d = invD[e];
-        acc = make_double2(acc.x * d.x - acc.y * d.y, acc.x * d.y + acc.y * d.x);
-      }
-      out[e] = acc;
-    }
+    pass(in, out, mz, pxy, pxy, sz, divide ? invD : nullptr);
   };
   pass_x(A, B);
   __syncthreads();
