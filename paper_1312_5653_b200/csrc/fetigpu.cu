@@ -1968,7 +1968,7 @@ struct Ctx {
         k_stencil_residual_part<<<grid, 256, 0, stream>>>(P.nx - 1, P.ny - 1, S9, x, rhs, d_part);
       });
       launch(FETIGPU_K_OTHER, [&] {
-        k_norm_max_final<<<1, 32, 0, stream>>>((int)(grid.x * grid.y), d_part, d_stat + sb + 2);
+        k_norm_max_final_big<<<1, 1024, 0, stream>>>((int)(grid.x * grid.y), d_part, d_stat + sb + 2);
       });
     } else {
       apply_global<double2>(x, nullptr, 1.0, mc, d_ax);

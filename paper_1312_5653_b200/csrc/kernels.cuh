@@ -2348,17 +2348,59 @@ __global__ void k_norm_max_part(int n, const double2* __restrict__ x, double2* _
   }
 }
 __global__ void k_norm_max_final(int nblk, const double2* __restrict__ part, double2* __restrict__ out) {
+  // each lane sums its partials b = lane, lane + 32, ... in that order; the loads of 8
+  // consecutive ones are issued together (same sum as the one-at-a-time loop)
   double s = 0.0, m = 0.0;
-  for (int b = threadIdx.x; b < nblk; b += 32) s += part[b].x, m = fmax(m, part[b].y);
+  for (int b0 = threadIdx.x; b0 < nblk; b0 += 32 * 8) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = b0 + 32 * u < nblk ? part[b0 + 32 * u] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (b0 + 32 * u < nblk) s += v[u].x, m = fmax(m, v[u].y);
+  }
   s = warp_sum(s);
   m = warp_max(m);
   if (threadIdx.x == 0) *out = make_double2(s, m);
 }
 
+// the same over many partials (the stencil residual's one-per-row-segment blocks): 1024
+// threads, each summing partials t, t + 1024, ... in order, then a fixed-order block reduce
+__global__ void __launch_bounds__(1024) k_norm_max_final_big(int nblk, const double2* __restrict__ part,
+                                                             double2* __restrict__ out) {
+  __shared__ double ws[32], wm[32];
+  double s = 0.0, m = 0.0;
+  for (int b0 = threadIdx.x; b0 < nblk; b0 += 1024 * 4) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = b0 + 1024 * u < nblk ? part[b0 + 1024 * u] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (b0 + 1024 * u < nblk) s += v[u].x, m = fmax(m, v[u].y);
+  }
+  s = warp_sum(s);
+  m = warp_max(m);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) ws[warp] = s, wm[warp] = m;
+  __syncthreads();
+  if (warp == 0) {
+    s = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0.0;
+    m = lane < (int)(blockDim.x >> 5) ? wm[lane] : 0.0;
+    s = warp_sum(s);
+    m = warp_max(m);
+    if (lane == 0) *out = make_double2(s, m);
+  }
+}
 // max over block partials of k_imag_max_part -> out->y (out->x = 0)
 __global__ void k_max_final(int nblk, const double* __restrict__ part, double2* __restrict__ out) {
   double m = 0.0;
-  for (int b = threadIdx.x; b < nblk; b += 32) m = fmax(m, part[b]);
+  for (int b0 = threadIdx.x; b0 < nblk; b0 += 32 * 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = b0 + 32 * u < nblk ? part[b0 + 32 * u] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) m = fmax(m, v[u]);
+  }
   m = warp_max(m);
   if (threadIdx.x == 0) *out = make_double2(0.0, m);
 }

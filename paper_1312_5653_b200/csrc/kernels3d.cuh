@@ -1599,7 +1599,14 @@ __global__ void k3_mdot_final(int nblk, int nv, const double2* __restrict__ part
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (j > nv) return;
   double2 t = cz();
-  for (int b = lane; b < nblk; b += 32) t = cadd(t, part[(size_t)b * (nv + 1) + j]);
+  for (int b0 = lane; b0 < nblk; b0 += 32 * 8) {  // 8 loads in flight, same summation order
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = b0 + 32 * u < nblk ? part[(size_t)(b0 + 32 * u) * (nv + 1) + j] : cz();
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (b0 + 32 * u < nblk) t = cadd(t, v[u]);
+  }
   t = warp_sum2(t);
   if (lane == 0) out[j] = t;
 }
@@ -1654,7 +1661,14 @@ __global__ void k3_norm_final(int nblk, const double2* __restrict__ part, double
   const int lane = threadIdx.x & 31;
   if (threadIdx.x >= 32) return;
   double a = 0.0, b = 0.0;
-  for (int q = lane; q < nblk; q += 32) a += part[q].x, b = fmax(b, part[q].y);
+  for (int q0 = lane; q0 < nblk; q0 += 32 * 8) {  // 8 loads in flight, same summation order
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = q0 + 32 * u < nblk ? part[q0 + 32 * u] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (q0 + 32 * u < nblk) a += v[u].x, b = fmax(b, v[u].y);
+  }
   a = warp_sum(a);
   b = warp_max(b);
   if (lane == 0) *out = make_double2(a, sqrt(b));
