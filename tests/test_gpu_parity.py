@@ -321,3 +321,21 @@ def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
         assert a[side]["iterations"] == b[side]["iterations"]
     for k in ("y", "u", "lambda"):
         assert rel(a[k], b[k]) <= 1e-11, k
+
+
+@pytest.mark.parametrize("n,s", [(36, 4), (40, 4), (66, 3)])
+def test_separable_solve_even_odd_grids(fetigpu, monkeypatch, n, s):
+    """Separable interior solve on even and odd interior line lengths (m = n/s - 1 = 8, 9,
+    21) against the block-Thomas path."""
+    p = fetigpu.make_seeded_problem(n, 1e-4, seed=1)
+    solver = fetigpu.SchurSolver(p, s, s, tol=1e-10)
+    a = solver.solve()
+    solver.close()
+    monkeypatch.setenv("FETIGPU_NO_FDM", "1")
+    solver = fetigpu.SchurSolver(p, s, s, tol=1e-10)
+    b = solver.solve()
+    solver.close()
+    for side in ("plus_stats", "minus_stats"):
+        assert a[side]["iterations"] == b[side]["iterations"]
+    for k in ("y", "u", "lambda"):
+        assert rel(a[k], b[k]) <= 1e-11, k
