@@ -315,6 +315,8 @@ def run_gpu(args):
             traffic = json.load(f).get(kclass)
     except Exception:
         pass
+    if traffic and not (0.5 * kb <= traffic <= 4 * kb):
+        traffic = None  # the committed ncu capture is of another config's launch size
     kernel_breakdown = {c: {"ms_per_step": v["ms"] / steps, "launches_per_step": v["launches"] / steps}
                         for c, v in prof.items() if v["launches"]}
     # in-graph kernel spans (first CTA start .. last CTA end, %globaltimer) of the last
@@ -325,7 +327,9 @@ def run_gpu(args):
     spans = solver.step_spans()
     in_graph = None
     if spans:
-        in_graph = {"spans_us": {k: round(v, 3) for k, v in spans.items() if k != "steps"}, "steps": spans["steps"]}
+        # a span whose %globaltimer stamps were not both written reads as garbage: null it
+        in_graph = {"spans_us": {k: (round(v, 3) if 0.0 <= v < 1e6 else None)
+                                 for k, v in spans.items() if k != "steps"}, "steps": spans["steps"]}
         for cls, key in (("precond_gemv", "precond"), ("dual_gemv", "dual")):
             gbs = solver.class_bytes(cls) / (spans[key] * 1e-6) / 1e9
             in_graph[cls] = {"achieved_gbs": gbs, "frac": gbs / hbm_peak}
