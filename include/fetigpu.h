@@ -44,7 +44,9 @@ typedef struct {
   double mass_coeff_im;  /*   bindings.cpp:158-185); schur_solve then rejected      */
   double tol;            /* relative dual residual (FetiConfig::tol, feti.hpp:26) */
   int max_iter;          /* FetiConfig::max_iter; GMRES is unrestarted (feti.cpp:684) */
-  int augment;           /* edge-RBM augmentation: must be 0 (FETIGPU_CONTRACT otherwise) */
+  int augment;           /* edge-RBM augmentation (FetiConfig::augment, feti.hpp:25; feti.cpp:171-242):
+                            0 or 1 through fetigpu_create; fetigpu_create_sharded returns
+                            FETIGPU_CONTRACT when it is set */
   int device;            /* CUDA device ordinal */
 } fetigpu_desc;
 

@@ -56,6 +56,20 @@ def _check(rc):
     raise RuntimeError(msg)
 
 
+def _out_arrays(out, n):
+    """Caller-supplied (y, u, lambda) output arrays, checked before their raw pointers reach the
+    C-ABI (which writes n float64 into each)."""
+    if out is None:
+        return np.zeros(n), np.zeros(n), np.zeros(n)
+    if len(out) != 3:
+        raise ContractError("solve: out must be (y, u, lambda)")
+    for a in out:
+        if not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.shape != (n,) or not a.flags.c_contiguous \
+                or not a.flags.writeable:
+            raise ContractError("solve: out arrays must be writeable contiguous float64 of length n")
+    return tuple(out)
+
+
 def _dp(a):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
@@ -221,16 +235,12 @@ class SchurSolver:
         ycp = None
         if yc is not None and self.m > 0:
             yc = np.ascontiguousarray(yc, dtype=np.float64)
+            if yc.shape != (self.m,):
+                raise ContractError("ControlProblem: boundary length != m")
             ycp = _dp(yc)
         if ybar.shape != (self.n,):
             raise ContractError("ControlProblem: target length != n")
-        if out is None:
-            y, u, lam = np.zeros(self.n), np.zeros(self.n), np.zeros(self.n)
-        else:
-            y, u, lam = out
-            for a in out:
-                if a.dtype != np.float64 or a.shape != (self.n,) or not a.flags.c_contiguous:
-                    raise ContractError("solve: out arrays must be contiguous float64 of length n")
+        y, u, lam = _out_arrays(out, self.n)
         st = SchurStats()
         _check(_native.lib().fetigpu_schur_solve(self._h, _dp(ybar), ycp, _dp(y), _dp(u), _dp(lam), C.byref(st)))
         return _schur_result(y, u, lam, st)
@@ -244,6 +254,8 @@ class SchurSolver:
     # -- single factor -------------------------------------------------------------
     def feti_solve(self, rhs, sign=1):
         rhs = np.ascontiguousarray(rhs, dtype=np.complex128)
+        if rhs.shape != (self.n,):
+            raise ContractError("feti: rhs dimension mismatch")  # feti.cpp:639
         x = np.zeros(self.n, dtype=np.complex128)
         st = FetiStats()
         _check(_native.lib().fetigpu_feti_solve(self._h, sign, _dp(rhs.view(np.float64)), _dp(x.view(np.float64)),
@@ -258,6 +270,8 @@ class SchurSolver:
 
     def _lam_op(self, fn, v, sign):
         v = np.ascontiguousarray(v, dtype=np.complex128)
+        if v.shape != (self.n_lambda,):
+            raise ContractError("multiplier vector length != n_lambda")
         out = np.zeros(self.n_lambda, dtype=np.complex128)
         _check(fn(self._h, sign, _dp(v.view(np.float64)), _dp(out.view(np.float64))))
         return out

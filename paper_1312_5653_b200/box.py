@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from . import ContractError, _check, _dp, _schur_result, _stats_dict
+from . import ContractError, _check, _dp, _out_arrays, _schur_result, _stats_dict
 from . import _native
 from ._native import Desc3, FetiStats, SchurStats
 
@@ -137,11 +137,10 @@ class BoxSchurSolver:
         ycp = None
         if yc is not None and self.m > 0:
             yc = np.ascontiguousarray(yc, dtype=np.float64)
+            if yc.shape != (self.m,):
+                raise ContractError("ControlProblem: boundary length != m")
             ycp = _dp(yc)
-        if out is None:
-            y, u, lam = np.zeros(self.n), np.zeros(self.n), np.zeros(self.n)
-        else:
-            y, u, lam = out
+        y, u, lam = _out_arrays(out, self.n)
         st = SchurStats()
         _check(_native.lib().fetigpu3d_schur_solve(self._h, _dp(ybar), ycp, _dp(y), _dp(u), _dp(lam), C.byref(st)))
         return _schur_result(y, u, lam, st)
@@ -153,6 +152,8 @@ class BoxSchurSolver:
 
     def feti_solve(self, rhs, sign=1):
         rhs = np.ascontiguousarray(rhs, dtype=np.complex128)
+        if rhs.shape != (self.n,):
+            raise ContractError("feti: rhs dimension mismatch")
         x = np.zeros(self.n, dtype=np.complex128)
         st = FetiStats()
         _check(_native.lib().fetigpu3d_feti_solve(self._h, sign, _dp(rhs.view(np.float64)), _dp(x.view(np.float64)),
@@ -161,6 +162,8 @@ class BoxSchurSolver:
 
     def _lam_op(self, fn, v, sign):
         v = np.ascontiguousarray(v, dtype=np.complex128)
+        if v.shape != (self.n_lambda,):
+            raise ContractError("multiplier vector length != n_lambda")
         out = np.zeros(self.n_lambda, dtype=np.complex128)
         _check(fn(self._h, sign, _dp(v.view(np.float64)), _dp(out.view(np.float64))))
         return out

@@ -70,22 +70,6 @@ __device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) 
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// Operator slices to pull into L2 while a latency-bound kernel leaves HBM idle: slice s is
-// [base + s * stride, + bytes), s < count; block b of the issuing grid takes s = b, b + G, ..
-struct L2Prefetch {
-  const char* base;
-  size_t stride;
-  unsigned int bytes;
-  int count;
-};
-__device__ __forceinline__ void l2_prefetch_slices(const L2Prefetch& p) {
-  if (p.count <= 0 || threadIdx.x != 0) return;
-  constexpr unsigned int CHUNK = 16384;
-  for (int s = blockIdx.x; s < p.count; s += gridDim.x)
-    for (unsigned int off = 0; off < p.bytes; off += CHUNK)
-      prefetch_l2_bulk(p.base + (size_t)s * p.stride + off, min(CHUNK, p.bytes - off));
-}
-
 // ---- sm_90+/sm_100a async-proxy primitives (inline PTX) -------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

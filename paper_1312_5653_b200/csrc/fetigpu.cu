@@ -118,7 +118,6 @@ struct Ctx {
   double2 *d_Cinv = nullptr;
   double2 *d_Sbb_p = nullptr, *d_Sinv_p = nullptr;  // packed symmetric tiles (k_sym_gemv)
   int NT = 0;
-  int sym_grid = 0;
   // workspaces
   double2 *d_fi = nullptr, *d_fb = nullptr, *d_fc = nullptr, *d_tb = nullptr, *d_yi = nullptr, *d_ri = nullptr;
   double2 *d_u1b = nullptr, *d_gcp = nullptr, *d_g = nullptr, *d_z = nullptr, *d_wb = nullptr;
@@ -161,14 +160,10 @@ struct Ctx {
   bool split_givens = false;
   const int* span_it = nullptr;  // split path: the preconditioner GEMV's span slot is st->jcol
   bool debug_sync = false;
-  bool sym_tma = false;
   bool pdl = true;                      // FETIGPU_NO_PDL=1: plain stream serialisation
   // FETIGPU_L2PF_KB / FETIGPU_L2PF_AT: per-subdomain bytes of the Dirichlet operator pulled
   // into L2 by a latency-bound Arnoldi kernel (0 coarse GEMV, 1 CGS pass 1, 2 pass 2, 3 update)
-  unsigned int l2pf_bytes = 0;
-  int l2pf_at = 1;
   bool arnoldi_phase = false;
-  int sym_warps = 4;
   size_t l2_persist_bytes = 0;
   bool watchdog = false;
   cudaGraph_t arnoldi_graph = nullptr;
@@ -177,9 +172,7 @@ struct Ctx {
   int arnoldi_body_kernels = 0;
   static constexpr int kCgsThreads = 512, kCgsRows = 256;  // k_cgs_pass block shape
   // fused Arnoldi tail (k_arnoldi_tail): rows per thread (0 = off), grid, barrier words
-  int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_minb = 1, tail_rows = 512;
-  bool cgs_gram = false;       // FETIGPU_CGS=gram: one-reduction CGS2 via the Gram matrix
-  double2* d_gram = nullptr;
+  int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_rows = 512;
   static constexpr int kBodyUnroll = 4;  // steps per WHILE-body execution (measured at config 2: 4 205.6, 8 204.9, 12 203.1 solves/s; earlier code 4: 182.8, 8: 183.5)
   int body_unroll = 1;
   unsigned int* d_bar = nullptr;
@@ -264,16 +257,29 @@ struct Ctx {
   // kernel launch with programmatic dependent launch allowed (see pdl_wait in common.cuh)
   template <typename... KArgs, typename... Args>
   void kx(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+    kx_attr(false, kern, grid, block, smem, args...);
+  }
+  // grid-barrier kernels (k_arnoldi_tail): a cooperative launch, so the runtime guarantees
+  // that every block is co-resident (it rejects the launch -- instead of letting the spin
+  // barriers wait forever -- when fewer SMs are available: MPS limits, green contexts)
+  template <typename... KArgs, typename... Args>
+  void kx_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+    kx_attr(true, kern, grid, block, smem, args...);
+  }
+  template <typename... KArgs, typename... Args>
+  void kx_attr(bool coop, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = coop ? 2 : 1;
     CU(cudaLaunchKernelEx(&cfg, kern, args...));
   }
   void prof_collect() {
@@ -532,7 +538,7 @@ struct Ctx {
   }
   void setup_compact_aic() {
     const int S = H.n_sub, NC = H.NC;
-    if (NC == 0 || sym_tma || std::getenv("FETIGPU_NO_AIC")) return;  // (the TMA GEMV has no A_ic term)
+    if (NC == 0 || std::getenv("FETIGPU_NO_AIC")) return;
     d_aic_idx = alloc<int>((size_t)S * NC * kAE);
     d_aic_val = alloc<double2>((size_t)S * NC * kAE);
     CU(cudaMemsetAsync(d_status, 0, sizeof(int), stream));
@@ -547,31 +553,28 @@ struct Ctx {
   // one-launch Arnoldi tail when every block of its grid can be co-resident (one GPU only)
   static constexpr int kTailThreads = 512;
   size_t tail_smem() const {
-    return sizeof(double2) * (2 * (size_t)kTailThreads + 3 * (size_t)(vcap_hint() + 2) + 640 + (cgs_gram ? TAIL_GSM : 0));
+    return sizeof(double2) * ((size_t)kTailThreads + 3 * (size_t)(vcap_hint() + 2) + 640);
   }
   void setup_fused_tail() {
-    if (const char* e = std::getenv("FETIGPU_CGS")) cgs_gram = std::string(e) == "gram";
     if (dist() || H.NC > 4 || H.n_aug > 0 || nc > kTailThreads + 2 * (vcap_hint() + 2) ||
         std::getenv("FETIGPU_NO_FUSED_TAIL"))
       return;
     const size_t smem = tail_smem();
     if (smem > 200 * 1024) return;
-    int sms = 0, per_sm = 0;
+    int sms = 0, per_sm = 0, coop = 0;
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc.device));
-    if (const char* e = std::getenv("FETIGPU_TAIL_MINB")) tail_minb = std::atoi(e) == 2 ? 2 : 1;
-    auto kfn = tail_minb == 2 ? k_arnoldi_tail<kTailThreads, 4, 2> : k_arnoldi_tail<kTailThreads, 4, 1>;
+    CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, desc.device));
+    if (!coop) return;  // the fused tail needs a cooperative (co-residency checked) launch
+    auto kfn = k_arnoldi_tail<kTailThreads, 4, 1>;
     CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CU(cudaFuncSetAttribute(k_arnoldi_tail<kTailThreads, 4, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTailThreads, smem));
     // rows per block: spread the rows over every SM (multiple of 32, at most one per thread)
     tail_rows = std::min(kTailThreads, 32 * cdiv(cdiv(std::max(nown, 1), sms), 32));
-    if (const char* e = std::getenv("FETIGPU_TAIL_ROWS")) tail_rows = std::min(kTailThreads, std::max(32, std::atoi(e)));
     const int grid = std::max(1, cdiv(nown, tail_rows));
     if (per_sm <= 0 || grid > per_sm * sms) return;
+    if (!probe_coop_tail(kfn, grid, smem)) return;
     tail_rpt = 1;
     tail_grid = grid;
-    if (cgs_gram) d_gram = alloc<double2>((size_t)vcap_hint() * (vcap_hint() + 1) / 2 + 1);
     const int rows = cdiv(std::max(nc, 1), tail_grid);
     tail_rb = rows <= 1 ? 1 : rows <= 2 ? 2 : rows <= 4 ? 4 : rows <= 8 ? 8 : 16;
     d_bar = alloc<unsigned int>(2);
@@ -580,6 +583,36 @@ struct Ctx {
       d_tstamp = alloc<unsigned long long>((size_t)16 * (vcap_hint() + 2));
       CU(cudaMemsetAsync(d_tstamp, 0, (size_t)16 * (vcap_hint() + 2) * sizeof(unsigned long long), stream));
     }
+  }
+  // One real cooperative launch of the tail (n = nc = 0 and a stopped cycle: every block
+  // returns right after its prologue).  The runtime rejects it (cudaErrorCooperativeLaunchTooLarge)
+  // when the grid cannot be co-resident in this context; the step then uses the multi-launch
+  // tail (coarse GEMV, two CGS passes, update) instead of spinning in grid barriers.
+  template <typename K>
+  bool probe_coop_tail(K kfn, int grid, size_t smem) {
+    if (std::getenv("FETIGPU_COOP_REJECT")) return false;  // test hook: act as if the runtime rejected the launch
+    GmresState* st = alloc<GmresState>(1);
+    CU(cudaMemsetAsync(st, 0, sizeof(GmresState), stream));
+    ArnoldiTailArgs t{};
+    t.st = st;
+    t.rows_pb = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTailThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, t);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();  // a rejected launch is not sticky
+      return false;
+    }
+    CU(cudaStreamSynchronize(stream));
+    return true;
   }
   int vcap_hint() const { return std::max(2, desc.max_iter + 1); }
   void report_step_spans(int it0, int it1) {
@@ -657,12 +690,8 @@ struct Ctx {
     if (const char* e = std::getenv("FETIGPU_EAGER")) use_graph = !(e[0] == '1');
     if (const char* e = std::getenv("FETIGPU_DEBUG_SYNC")) debug_sync = e[0] == '1';
     if (debug_sync) use_graph = false;
-    if (const char* e = std::getenv("FETIGPU_SYM_TMA")) sym_tma = e[0] == '1';
     if (const char* e = std::getenv("FETIGPU_NO_PDL")) pdl = !(e[0] == '1');
     phase_times = std::getenv("FETIGPU_PHASE_TIMES") != nullptr;
-    if (const char* e = std::getenv("FETIGPU_L2PF_KB")) l2pf_bytes = 1024u * (unsigned)std::atoi(e);
-    if (const char* e = std::getenv("FETIGPU_L2PF_AT")) l2pf_at = std::atoi(e);
-    if (const char* e = std::getenv("FETIGPU_SYM_WARPS")) sym_warps = std::atoi(e) == 8 ? 8 : 4;
     watchdog = std::getenv("FETIGPU_WATCHDOG") != nullptr;
     n = P.n();
     m = P.m();
@@ -854,15 +883,6 @@ struct Ctx {
       NT = (NB + 31) / 32;
       if (NT > 8) throw ContractError("more than 256 interface dofs per subdomain");
       const size_t per = (size_t)sym_tile_entries(NT);
-      {
-        int dev_sms = 0;
-        CU(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, desc.device));
-        sym_grid = dev_sms;  // one persistent CTA per SM (k_sym_gemv_tma)
-        const int smem = (int)sym_tma_smem(NT);
-        CU(cudaFuncSetAttribute(k_sym_gemv_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CU(cudaFuncSetAttribute(k_sym_gemv_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        CU(cudaFuncSetAttribute(k_sym_gemv_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-      }
       d_Sbb_p = alloc<double2>((size_t)S * per);
       d_Sinv_p = alloc<double2>((size_t)S * per);
       launch(FETIGPU_K_OTHER, [&] {
@@ -964,7 +984,7 @@ struct Ctx {
   // 0.3 GB through L2 with evict-first loads; pin C^-1 in the persisting L2 carve-out
   // (access-policy window on the context stream, inherited by captured graph nodes).
   void setup_l2_persistence() {
-    if (nc == 0 || std::getenv("FETIGPU_NO_L2_PERSIST")) return;
+    if (nc == 0) return;
     int max_persist = 0, max_window = 0;
     CU(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, desc.device));
     CU(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, desc.device));
@@ -1012,18 +1032,15 @@ struct Ctx {
     std::vector<double> cx, dx, cy, dy;
     factor(i0, i1, P.nx, cx, dx);
     factor(j0, j1, P.ny, cy, dy);
-    if (const char* e = std::getenv("FETIGPU_TRI_X")) tri_x = std::atoi(e);
-    if (const char* e = std::getenv("FETIGPU_TRI_Y")) tri_y = std::atoi(e);
-    if (const char* e = std::getenv("FETIGPU_TRI_ROWS")) tri_rows_lpb = std::atoi(e);
     d_mx_cp = upload(cx);
     d_mx_dinv = upload(dx);
     d_my_cp = upload(cy);
     d_my_dinv = upload(dy);
   }
 
-  // lines per block (FETIGPU_TRI_X / FETIGPU_TRI_Y for experiments): few lines per block so
-  // that the ~1000 lines of config 2 spread over every SM
-  int tri_x = 8, tri_y = 8, tri_rows_lpb = 2;
+  // lines per block: few, so that the ~1000 lines of config 2 spread over every SM (x lines
+  // staged 2 per block through padded shared memory, y lines 8 per block; measured)
+  static constexpr int kTriRows = 2, kTriLines = 8;
   template <int LPB, bool SEG_FAST>
   void tri_launch(double* v, int nlines, int len, int G, long long S1, long long S2, long long es, const double* cp,
                   const double* dinv) {
@@ -1039,26 +1056,21 @@ struct Ctx {
     {
       const int nl = Ly * dpn;
       const long long S1 = (long long)Lx * dpn;
-      const size_t sm = (size_t)(tri_rows_lpb + 2) * (Lx + Lx / 32 + 1) * sizeof(double);
-      if (dpn == 1 && Lx <= 32 * 32 && tri_rows_lpb > 0 && sm <= 48 * 1024) {  // staged rows (coalesced)
+      const size_t sm = (size_t)(kTriRows + 2) * (Lx + Lx / 32 + 1) * sizeof(double);
+      if (dpn == 1 && Lx <= 32 * 32 && sm <= 48 * 1024) {  // staged rows (coalesced)
         launch(FETIGPU_K_GLOBAL, [&] {
-          if (tri_rows_lpb == 4)
-            k_tridiag_rows<4><<<cdiv((long long)nl, 4), dim3(32, 4), sm, stream>>>(v, nl, Lx, d_mx_cp, d_mx_dinv, moff);
-          else
-            k_tridiag_rows<2><<<cdiv((long long)nl, 2), dim3(32, 2), sm, stream>>>(v, nl, Lx, d_mx_cp, d_mx_dinv, moff);
+          k_tridiag_rows<kTriRows><<<cdiv((long long)nl, kTriRows), dim3(32, kTriRows), sm, stream>>>(
+              v, nl, Lx, d_mx_cp, d_mx_dinv, moff);
         });
-      } else if (tri_x == 2) tri_launch<2, true>(v, nl, Lx, dpn, S1, 1, dpn, d_mx_cp, d_mx_dinv);
-      else if (tri_x == 4) tri_launch<4, true>(v, nl, Lx, dpn, S1, 1, dpn, d_mx_cp, d_mx_dinv);
-      else tri_launch<8, true>(v, nl, Lx, dpn, S1, 1, dpn, d_mx_cp, d_mx_dinv);
+      } else {
+        tri_launch<kTriLines, true>(v, nl, Lx, dpn, S1, 1, dpn, d_mx_cp, d_mx_dinv);
+      }
     }
     // along y: Lx*dpn lines of Ly entries, stride Lx*dpn
     {
       const int nl = Lx * dpn;
       const long long es = (long long)Lx * dpn;
-      if (tri_y == 4) tri_launch<4, false>(v, nl, Ly, 1, 1, 0, es, d_my_cp, d_my_dinv);
-      else if (tri_y == 8) tri_launch<8, false>(v, nl, Ly, 1, 1, 0, es, d_my_cp, d_my_dinv);
-      else if (tri_y == 16) tri_launch<16, false>(v, nl, Ly, 1, 1, 0, es, d_my_cp, d_my_dinv);
-      else tri_launch<32, false>(v, nl, Ly, 1, 1, 0, es, d_my_cp, d_my_dinv);
+      tri_launch<kTriLines, false>(v, nl, Ly, 1, 1, 0, es, d_my_cp, d_my_dinv);
     }
   }
 
@@ -1165,49 +1177,18 @@ struct Ctx {
     coarse_gemv();
   }
 
-  // packed symmetric GEMV: persistent TMA-streamed grid (k_sym_gemv_tma)
+  // packed symmetric GEMV: one CTA per subdomain, register streaming (k_sym_gemv)
   void launch_sym(const SymGemvArgs& g) {
-    // the TMA variant keeps one whole subdomain operator in shared memory (NT <= 5)
-    if (!sym_tma || sym_tma_smem(NT) > 220 * 1024) {  // one CTA per subdomain, register streaming
-      const size_t sm = sym_smem();
-      if (sym_warps == 4) {
-        switch (g.mode) {
-          case 0: kx(k_sym_gemv<0, 8, 4>, H.n_sub, 128, sm, g); break;
-          case 1: kx(k_sym_gemv<1, 8, 4>, H.n_sub, 128, sm, g); break;
-          default: kx(k_sym_gemv<2, 8, 4>, H.n_sub, 128, sm, g); break;
-        }
-      } else {
-        switch (g.mode) {
-          case 0: kx(k_sym_gemv<0, 8, 8>, H.n_sub, 256, sm, g); break;
-          case 1: kx(k_sym_gemv<1, 8, 8>, H.n_sub, 256, sm, g); break;
-          default: kx(k_sym_gemv<2, 8, 8>, H.n_sub, 256, sm, g); break;
-        }
-      }
-      return;
-    }
-    // FETIGPU_SYM_TMA=1: persistent TMA-streamed variant (experimental)
-    const size_t smem = sym_tma_smem(NT);
-    const int grid = std::min(H.n_sub, sym_grid);
+    const size_t sm = sym_smem();
     switch (g.mode) {
-      case 0: k_sym_gemv_tma<0><<<grid, 288, smem, stream>>>(g, H.n_sub); break;
-      case 1: k_sym_gemv_tma<1><<<grid, 288, smem, stream>>>(g, H.n_sub); break;
-      default: k_sym_gemv_tma<2><<<grid, 288, smem, stream>>>(g, H.n_sub); break;
+      case 0: kx(k_sym_gemv<0, 8, 4>, H.n_sub, 128, sm, g); break;
+      case 1: kx(k_sym_gemv<1, 8, 4>, H.n_sub, 128, sm, g); break;
+      default: kx(k_sym_gemv<2, 8, 4>, H.n_sub, 128, sm, g); break;
     }
   }
   size_t sym_smem() const {
     const int noff = NT * (NT - 1) / 2;
     return sizeof(double2) * 32 * (NT + (noff + NT) + noff);
-  }
-  // slices of the Dirichlet operator (the next precond GEMV's input stream) for kernel `at`
-  L2Prefetch l2pf(int at) const {
-    L2Prefetch p{};
-    if (l2pf_bytes == 0 || at != l2pf_at || prof) return p;
-    const size_t per = sizeof(double2) * sym_tile_entries(NT);
-    p.base = reinterpret_cast<const char*>(d_Sbb_p);
-    p.stride = per;
-    p.bytes = (unsigned int)std::min<size_t>(l2pf_bytes, per) & ~15u;
-    p.count = H.n_sub;
-    return p;
   }
   SymGemvArgs sym_args(const double2* pack) const {
     SymGemvArgs g{};
@@ -1285,7 +1266,7 @@ struct Ctx {
       return;
     }
     launch(FETIGPU_K_COARSE, [&] {
-      kx(k_coarse_gemv<256>, nc, 256, 0, nc, (const double2*)d_Cinv, (const double2*)d_g, d_z, l2pf(arnoldi_phase ? 0 : -1));
+      kx(k_coarse_gemv<256>, nc, 256, 0, nc, (const double2*)d_Cinv, (const double2*)d_g, d_z);
     });
   }
   // u_b = u1_b - cpl_b z gathered onto the owned multiplier rows: out = -B u  (feti.cpp:593)
@@ -1567,14 +1548,8 @@ struct Ctx {
       t.span = d_span;
       t.hcap = vcap + 2;
       t.vcap = vcap;
-      t.gram = d_gram;
       launch(FETIGPU_K_ORTHO, [&] {
-        if (cgs_gram)
-          kx(k_arnoldi_tail<kTailThreads, 4, 1, true>, tail_grid, kTailThreads, tail_smem(), t);
-        else if (tail_minb == 2)
-          kx(k_arnoldi_tail<kTailThreads, 4, 2>, tail_grid, kTailThreads, tail_smem(), t);
-        else
-          kx(k_arnoldi_tail<kTailThreads, 4, 1>, tail_grid, kTailThreads, tail_smem(), t);
+        kx_coop(k_arnoldi_tail<kTailThreads, 4, 1>, tail_grid, kTailThreads, tail_smem(), t);
       });
       if (split && u == body_unroll - 1)  // the body's last Givens drives the WHILE condition
         launch(FETIGPU_K_ORTHO, [&] { kx(k_givens_step, 1, 32, 0, t.ga); });
@@ -1614,7 +1589,6 @@ struct Ctx {
       }
       c.gather = 0;
     }
-    c.pf = l2pf(1);
     c.NB = H.NB;
     c.NC = H.NC;
     c.lam_lo = d_lam_lo + own0;
@@ -1628,7 +1602,6 @@ struct Ctx {
     mark(5);
     // pass 2: w -= V h1, h2 = V^H w, |w|^2; last block runs the Givens step (one GPU)
     c.gather = 0;
-    c.pf = l2pf(2);
     c.h_in = h1;
     c.out = h2;
     c.givens = dist() ? 0 : 1;
@@ -1642,40 +1615,8 @@ struct Ctx {
     // V_{j+1} = (w - V h2) / h_{j+1,j}
     launch(FETIGPU_K_ORTHO, [&] {
       kx(k_update_normalize<64, 4>, cdiv(nown, 64), 256, 0, nown, (const GmresState*)d_gst, (const double2*)h2,
-         (const double2*)(d_w + own0), d_V + own0, ldv, l2pf(3));
+         (const double2*)(d_w + own0), d_V + own0, ldv);
     });
-  }
-
-  // FETIGPU_L2_PERSIST=1: C^-1 (read by every tail's coarse phase) as a persisting L2
-  // access-policy window on the Arnoldi body's kernel nodes, so the GEMV streams between two
-  // tails do not evict it
-  void l2_persist_coarse(cudaGraph_t body) {
-    if (!std::getenv("FETIGPU_L2_PERSIST") || nc == 0 || d_Cinv == nullptr) return;
-    int maxwin = 0, maxpers = 0;
-    CU(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, desc.device));
-    CU(cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, desc.device));
-    const size_t bytes = std::min<size_t>({(size_t)nc * nc * sizeof(double2), (size_t)maxwin, (size_t)maxpers});
-    CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes));
-    cudaLaunchAttributeValue v{};
-    v.accessPolicyWindow.base_ptr = d_Cinv;
-    v.accessPolicyWindow.num_bytes = bytes;
-    v.accessPolicyWindow.hitRatio = 1.0f;
-    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    size_t nn = 0;
-    CU(cudaGraphGetNodes(body, nullptr, &nn));
-    std::vector<cudaGraphNode_t> nodes(nn);
-    CU(cudaGraphGetNodes(body, nodes.data(), &nn));
-    int set = 0;
-    for (auto nd : nodes) {
-      cudaGraphNodeType t;
-      CU(cudaGraphNodeGetType(nd, &t));
-      if (t != cudaGraphNodeTypeKernel) continue;
-      CU(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributeAccessPolicyWindow, &v));
-      ++set;
-    }
-    std::fprintf(stderr, "[fetigpu] L2 persisting window: %zu bytes (max window %d, max persisting %d) on %d nodes\n",
-                 bytes, maxwin, maxpers, set);
   }
   void build_arnoldi_graph() {
     CU(cudaGraphCreate(&arnoldi_graph, 0));
@@ -1694,13 +1635,11 @@ struct Ctx {
     // the fused-tail step is three kernels that each return at once when the cycle has
     // stopped, so the body holds `body_unroll` steps (fewer WHILE-node round trips)
     body_unroll = tail_rpt > 0 ? kBodyUnroll : 1;
-    if (const char* e = std::getenv("FETIGPU_UNROLL")) body_unroll = tail_rpt > 0 ? std::max(1, std::atoi(e)) : 1;
     CU(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    split_givens = tail_rpt > 0 && !cgs_gram && sym_warps == 4 && !sym_tma && !std::getenv("FETIGPU_NO_SPLIT");
+    split_givens = tail_rpt > 0 && !std::getenv("FETIGPU_NO_SPLIT");
     for (int u = 0; u < body_unroll; ++u) arnoldi_step(true, u);
     CU(cudaStreamEndCapture(stream, &body));
     prof = was_prof;
-    l2_persist_coarse(body);
     arnoldi_body_kernels = (int)(launches - before) / body_unroll;
     launches = before;
     CU(cudaGraphInstantiate(&arnoldi_exec, arnoldi_graph, 0));
@@ -1833,20 +1772,10 @@ struct Ctx {
           }
         }
       } else {
-        static const bool cgs_ratio = std::getenv("FETIGPU_CGS_RATIO") != nullptr;
         do {
-          const int nv_before = h_gst->j + 1;
           arnoldi_step(false);
           CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
           sync();
-          if (cgs_ratio) {  // diagnostics: |w - V h1| / |w| after CGS pass 1
-            std::vector<double2> h(nv_before + 1);
-            CU(cudaMemcpy(h.data(), d_red, h.size() * sizeof(double2), cudaMemcpyDeviceToHost));
-            double s2 = 0;
-            for (int i = 0; i < nv_before; ++i) s2 += h[i].x * h[i].x + h[i].y * h[i].y;
-            const double w2 = h[nv_before].x;
-            std::fprintf(stderr, "[fetigpu] step %d ratio %.4f\n", h_gst->iterations, std::sqrt(std::max(0.0, 1.0 - s2 / w2)));
-          }
           if (h_gst->cont) ghost_refresh(d_V + (size_t)h_gst->j * ldv);  // sharded: next basis column
         } while (h_gst->cont);
       }

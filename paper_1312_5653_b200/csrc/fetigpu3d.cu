@@ -343,7 +343,6 @@ struct Ctx3 {
     const size_t persist = sizeof(double2) * (2 * (size_t)pack_entries + (size_t)S * NB * NC + (size_t)S * NI * NC);
     const size_t budget = std::min<size_t>(24ull << 30, free_b > persist + (4ull << 30) ? (free_b - persist - (4ull << 30)) / 2 : 0);
     int chunk = (int)std::max<size_t>(1, std::min<size_t>(S, budget / std::max<size_t>(per_sub, 1)));
-    if (const char* e = std::getenv("FETIGPU3D_CHUNK")) chunk = std::max(1, std::min(S, std::atoi(e)));
     d_Sp = alloc<double2>(pack_entries);
     d_Sip = alloc<double2>(pack_entries);
     d_cpl_b = alloc<double2>((size_t)S * NB * NC);
@@ -355,33 +354,12 @@ struct Ctx3 {
     double2* pbuf = alloc<double2>((size_t)chunk * 1024);
     double2* cbuf = alloc<double2>((size_t)chunk * NTD * 1024);
     double* prat = alloc<double>(chunk);
-    const int msw = PB <= 12 ? 8 : 4;  // warps of the multi-RHS solve (ring = (P+1) x 32 x 4 warps x 16 B)
-    const size_t msmem = (size_t)(PB + 1) * 32 * 4 * msw * sizeof(double2);
-    if (msw == 8)
-      CU3(cudaFuncSetAttribute(k3::k3_bb_msolve<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
-    else
-      CU3(cudaFuncSetAttribute(k3::k3_bb_msolve<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem));
     const size_t m2smem = sizeof(double2) * (32 * 33 + 32 * 65);
     CU3(cudaFuncSetAttribute(k3::k3_bb_msolve2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m2smem));
-    const bool msolve_ring = std::getenv("FETIGPU3D_MSOLVE_RING") != nullptr;  // the first (ring) kernel
     auto msolve = [&](int cnt, int s0, int t0_, int tiles) {
-      if (!msolve_ring) {
-        launch(FETIGPU_K_OTHER, [&] {
-          k3::k3_bb_msolve2<<<dim3((tiles + 1) / 2, cnt), 256, m2smem, stream>>>(NBK, PB, d_bb, NI, ntile, t0_,
-                                                                               tiles, s0, X);
-        });
-        return;
-      }
-      const int cpb = 4 * msw;
-      dim3 grid(32 / cpb, tiles, cnt);
-      double2* Yb = X + (size_t)t0_ * NI * 32;
-      // tiles [t0_, t0_ + tiles) of every subdomain of the chunk: the kernel indexes tile via
-      // blockIdx.y with the chunk's tile stride ntile
       launch(FETIGPU_K_OTHER, [&] {
-        if (msw == 8)
-          k3::k3_bb_msolve<8><<<grid, 256, msmem, stream>>>(NBK, PB, d_bb, NI, ntile, s0, Yb);
-        else
-          k3::k3_bb_msolve<4><<<grid, 128, msmem, stream>>>(NBK, PB, d_bb, NI, ntile, s0, Yb);
+        k3::k3_bb_msolve2<<<dim3((tiles + 1) / 2, cnt), 256, m2smem, stream>>>(NBK, PB, d_bb, NI, ntile, t0_, tiles,
+                                                                             s0, X);
       });
     };
     double t_ms = 0, t_sb = 0, t_inv = 0, t_cpl = 0, t_pack = 0;
@@ -420,20 +398,14 @@ struct Ctx3 {
         static bool gattr = false;
         if (!gattr) {
           CU3(cudaFuncSetAttribute(k3::k3_gj_update64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
-          CU3(cudaFuncSetAttribute(k3::k3_gj_update64_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gsm));
           gattr = true;
         }
-        // FETIGPU3D_GJ=tc: the DMMA (FP64 tensor core) trailing update — measured no faster
-        // (1.01 vs 0.99 s at config 4): the update is bound by its read-modify-write of C
-        const char* gje = std::getenv("FETIGPU3D_GJ");
-        const bool gj_tc = gje && std::string(gje) == "tc";
+        // (a DMMA (FP64 tensor core) trailing update measured no faster, 1.01 vs 0.99 s at
+        // config 4: the update is bound by its read-modify-write of C; not kept)
         for (int K = 0; K < NTD; ++K) {
           k3::k3_gj_pivot<<<cnt, 256, 0, stream>>>(NBP, K, dense, pbuf, prat);
           k3::k3_gj_panel<<<dim3(NTD, cnt), 256, 0, stream>>>(NBP, NTD, K, dense, pbuf, cbuf);
-          if (gj_tc)
-            k3::k3_gj_update64_tc<<<dim3(NTD / 2, NTD / 2, cnt), 256, gsm, stream>>>(NBP, NTD, K, dense, pbuf, cbuf);
-          else
-            k3::k3_gj_update64<<<dim3(NTD / 2, NTD / 2, cnt), 256, gsm, stream>>>(NBP, NTD, K, dense, pbuf, cbuf);
+          k3::k3_gj_update64<<<dim3(NTD / 2, NTD / 2, cnt), 256, gsm, stream>>>(NBP, NTD, K, dense, pbuf, cbuf);
           k3::k3_gj_setpivot<<<cnt, 256, 0, stream>>>(NBP, K, dense, pbuf);
           CU3(cudaGetLastError());
           launches += 4;
@@ -509,7 +481,6 @@ struct Ctx3 {
     d_gcp0 = alloc<double2>((size_t)S * G * NC);
     for (double2** p : {&d_w, &d_zl, &d_r, &d_lam, &d_best, &d_d, &d_t}) *p = alloc<double2>(ldv);
     mdot_rows = 512;  // (2048: 1.35 blocks per SM, latency-bound at small j; measured 4.8 -> 4.0 ms of CGS per config-4 solve)
-    if (const char* e = std::getenv("FETIGPU3D_MDOT_ROWS")) mdot_rows = std::max(64, std::min(2048, std::atoi(e)));
     mdot_blocks = std::max(1, cdiv3(nl, mdot_rows));
     d_part = alloc<double2>((size_t)mdot_blocks * (vcap + 2) + 1024);
     d_h = alloc<double2>(2 * (vcap + 2));
@@ -808,21 +779,12 @@ struct Ctx3 {
       return;
     }
     if (solve_kind < 0) {
-      const char* e = std::getenv("FETIGPU3D_SOLVE");
-      solve_kind = (e && std::string(e) == "direct") ? 0 : 1;
-      if (solve_kind == 1) {
-        CU3(cudaFuncSetAttribute(k3::k3_bb_solve_tma<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)k3::bb_solve_tma_smem<8, 8>()));
-      }
+      CU3(cudaFuncSetAttribute(k3::k3_bb_solve_tma<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)k3::bb_solve_tma_smem<8, 8>()));
+      solve_kind = 1;
     }
     launch(FETIGPU_K_BAND, [&] {
-      if (solve_kind == 1) {
-        k3::k3_bb_solve_tma<8, 8><<<S, 288, k3::bb_solve_tma_smem<8, 8>(), stream>>>(NBK, PB, d_bb, NI, x);
-      } else if (PB <= 8) {
-        k3::k3_bb_solve1<33, 8><<<S, 256, 0, stream>>>(NBK, PB, d_bb, NI, x);
-      } else {
-        k3::k3_bb_solve1<33, 32><<<S, 1024, 0, stream>>>(NBK, PB, d_bb, NI, x);
-      }
+      k3::k3_bb_solve_tma<8, 8><<<S, 288, k3::bb_solve_tma_smem<8, 8>(), stream>>>(NBK, PB, d_bb, NI, x);
     });
   }
   // (|x|^2, max|x|) -> host

@@ -817,179 +817,6 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(S
   sym_gemv_run<MODE, SYM_BATCH, WARPS>(a);
 }
 
-// ---------------------------------------------------------------------------------------
-// Streaming version of k_sym_gemv: a persistent grid (one CTA per SM) where warp 8 is a TMA
-// producer streaming every tile of every subdomain the CTA owns into shared memory
-// (cp.async.bulk + mbarrier full/empty pairs) and warps 0-7 consume from shared memory.
-// The buffer holds exactly one subdomain's packed operator (133 KB at NB = 124) with one
-// slot per tile: slot t is always consumed by the same warp, so each barrier is waited on
-// strictly in phase order (a warp may never wait on phase k+1 of a slot before phase k has
-// completed — the parity test would alias).  While the consumers finish subdomain k, the
-// producer already refills every released slot with subdomain k+1: bytes in flight are set
-// by the buffer, not by registers.
-constexpr int SYM_TILE = 1024;  // complex entries of a full tile
-
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(288, 1) k_sym_gemv_tma(SymGemvArgs a, int S) {
-  constexpr int CWARPS = 8, CTHREADS = 256;
-  extern __shared__ __align__(128) unsigned char sgt_raw[];
-  const int NB = a.NB, NT = a.NT;
-  const int noff = NT * (NT - 1) / 2, ntiles = noff + NT;
-  const int per = sym_tile_entries(NT);
-  double2* buf = reinterpret_cast<double2*>(sgt_raw);  // one subdomain, same layout as global
-  uint64_t* full = reinterpret_cast<uint64_t*>(buf + per);
-  uint64_t* empty = full + ntiles;
-  double2* x_sh = reinterpret_cast<double2*>(empty + ntiles);
-  double2 (*part_row)[32] = reinterpret_cast<double2 (*)[32]>(x_sh + 32 * NT);
-  double2 (*part_col)[32] = reinterpret_cast<double2 (*)[32]>(x_sh + 32 * NT + 32 * ntiles);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // tile t: t < noff off-diagonal (16 KB, after the diagonal block), else diagonal t - noff
-  auto tile_off = [&](int t) -> int { return t < noff ? NT * 17 * 32 + t * SYM_TILE : (t - noff) * 17 * 32; };
-  if (threadIdx.x == 0) {
-    for (int t = 0; t < ntiles; ++t) {
-      mbar_init(&full[t], 1);
-      mbar_init(&empty[t], 1);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  if (warp == CWARPS) {  // ---------------- TMA producer ----------------
-    if (lane == 0) {
-      int k = 0;
-      for (int s = blockIdx.x; s < S; s += gridDim.x, ++k) {
-        const double2* P = a.pack + (size_t)s * per;
-        for (int t = 0; t < ntiles; ++t) {
-          mbar_wait(&empty[t], (k & 1) ^ 1);
-          const uint32_t bytes = (t < noff ? SYM_TILE : 17 * 32) * (uint32_t)sizeof(double2);
-          mbar_arrive_expect_tx(&full[t], bytes);
-          tma_load_1d(buf + tile_off(t), P + tile_off(t), bytes, &full[t]);
-        }
-      }
-    }
-    __syncwarp();
-    return;
-  }
-  // ---------------- consumers ----------------
-  const double2* lam = a.lam;
-  if (MODE == 0 && a.jsel != nullptr) lam += (size_t)(*a.jsel) * a.jstride;
-  int k = 0;
-  for (int s = blockIdx.x; s < S; s += gridDim.x, ++k) {
-    for (int i = threadIdx.x; i < 32 * NT; i += CTHREADS) {
-      double2 v = cz();
-      if (i < NB) {
-        const size_t sb = (size_t)s * NB + i;
-        if (MODE == 2) {
-          v = a.tb[sb];
-          for (int e = 0; e < a.EBI; ++e) {
-            const int ii = a.bi_idx[sb * a.EBI + e];
-            if (ii >= 0) v = cfms(a.bi_val[sb * a.EBI + e], a.yi[(size_t)s * a.NI + ii], v);
-          }
-        } else {
-          const int r = a.blam[sb];
-          if (r >= 0) {
-            double2 z;
-            if (MODE == 0)
-              z = lam[r];
-            else
-              z = cscale(csub(a.wb[a.lam_lo[r]], a.wb[a.lam_hi[r]]), 0.5);
-            v = cscale(z, a.alpha * a.bsign[sb]);
-          }
-        }
-      }
-      x_sh[i] = v;
-    }
-    named_bar_sync(1, CTHREADS);
-    // tiles: with NT = 4, warps 0-5 one off-diagonal tile, warps 6-7 two diagonal tiles
-    const bool paired = noff + (NT + 1) / 2 <= CWARPS;
-    for (int item = warp; item < (paired ? noff + (NT + 1) / 2 : ntiles); item += CWARPS)
-      for (int half = 0; half < ((paired && item >= noff) ? 2 : 1); ++half) {
-        const int t = (paired && item >= noff) ? noff + 2 * (item - noff) + half : item;
-        if (t >= ntiles) break;
-        mbar_wait(&full[t], k & 1);
-        const double2* T = buf + tile_off(t);
-        double2 yr = cz(), yc = cz();
-        if (t < noff) {
-          int I = 1;
-          while ((I + 1) * I / 2 <= t) ++I;
-          const int J = t - I * (I - 1) / 2;
-          const double2 xi = x_sh[32 * I + lane];
-#pragma unroll 8
-          for (int c = 0; c < 32; ++c) {
-            const double2 m = T[c * 32 + lane];
-            yr = cfma(m, x_sh[32 * J + ((lane + c) & 31)], yr);
-            yc = cfma(m, xi, yc);
-            yc = shfl2(yc, (lane + 1) & 31);
-          }
-          part_row[t][lane] = yr;
-          part_col[t][lane] = yc;
-        } else {
-          const int I = t - noff;
-          const double2 xi = x_sh[32 * I + lane];
-          yr = cmul(T[lane], xi);
-#pragma unroll 5
-          for (int c = 1; c < 16; ++c) {
-            const double2 m = T[c * 32 + lane];
-            yr = cfma(m, x_sh[32 * I + ((lane + c) & 31)], yr);
-            yc = shfl2(yc, (lane + 1) & 31);
-            yc = cfma(m, xi, yc);
-          }
-          yr = cfma(T[16 * 32 + lane], x_sh[32 * I + ((lane + 16) & 31)], yr);
-          yc = shfl2(yc, (lane + 17) & 31);
-          part_row[t][lane] = cadd(yr, yc);
-        }
-        // order this warp's generic-proxy reads of the slot before the async-proxy refill
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[t]);
-      }
-    named_bar_sync(1, CTHREADS);
-    for (int i = threadIdx.x; i < NB; i += CTHREADS) {
-      const int I = i >> 5, l = i & 31;
-      double2 acc = part_row[noff + I][l];
-      for (int J = 0; J < I; ++J) acc = cadd(acc, part_row[I * (I - 1) / 2 + J][l]);
-      for (int I2 = I + 1; I2 < NT; ++I2) acc = cadd(acc, part_col[I2 * (I2 - 1) / 2 + I][l]);
-      a.out[(size_t)s * NB + i] = acc;
-    }
-    if (a.gcp != nullptr) {
-      for (int c = warp; c < a.NC; c += CWARPS) {
-        double2 acc = cz();
-        for (int i = lane; i < NB; i += 32) acc = cfma(a.cpl_b[((size_t)s * NB + i) * a.NC + c], x_sh[i], acc);
-        acc = warp_sum2(acc);
-        if (lane == 0) a.gcp[(size_t)s * a.NC + c] = acc;
-      }
-    }
-    named_bar_sync(1, CTHREADS);  // x_sh / partials are rewritten for the next subdomain
-  }
-  if (a.g_counter != nullptr) {  // coarse rhs assembled by the last CTA to finish
-    __shared__ bool is_last;
-    __threadfence();
-    named_bar_sync(1, CTHREADS);
-    if (threadIdx.x == 0) is_last = atomicAdd(a.g_counter, 1u) == gridDim.x - 1;
-    named_bar_sync(1, CTHREADS);
-    if (is_last) {
-      __threadfence();
-      for (int c = threadIdx.x; c < a.nc; c += CTHREADS) {
-        double2 acc = a.fc ? a.fc[c] : cz();
-        for (int q = 0; q < 4; ++q) {
-          const int slot = a.corner_slots[c * 4 + q];
-          if (slot >= 0) acc = csub(acc, __ldcg(a.gcp + slot));
-        }
-        a.g[c] = acc;
-      }
-      if (threadIdx.x == 0) *a.g_counter = 0u;
-    }
-  }
-}
-
-__host__ __device__ constexpr size_t sym_tma_smem(int NT) {
-  return (size_t)sym_tile_entries(NT) * 16 + 2 * (size_t)(NT * (NT - 1) / 2 + NT) * 8 +
-         (size_t)16 * 32 * (NT + (NT * (NT - 1) / 2 + NT) + NT * (NT - 1) / 2);
-}
-
 // debugging aid (FETIGPU_WATCHDOG): progress marker between graph body kernels
 __global__ void k_mark(unsigned int* progress, unsigned int v) {
   if (threadIdx.x == 0) atomicExch(progress, v);
@@ -1022,13 +849,11 @@ __global__ void k_coarse_rhs(int nc, const int* __restrict__ corner_slots, const
 // comes from the number of warps, not from per-thread batching (ptxas serialises those).
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS)
-    k_coarse_gemv(int nc, const double2* __restrict__ Cinv, const double2* __restrict__ g, double2* __restrict__ z,
-                  L2Prefetch pf) {
+    k_coarse_gemv(int nc, const double2* __restrict__ Cinv, const double2* __restrict__ g, double2* __restrict__ z) {
   constexpr int WARPS = THREADS / 32;
   __shared__ double2 red[WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
-  l2_prefetch_slices(pf);
   pdl_wait();
   const int row = blockIdx.x;
   const double2* cr = Cinv + (size_t)row * nc;
@@ -1596,7 +1421,6 @@ struct CgsArgs {
   // fused Givens (pass 2)
   int givens;
   GivensArgs ga;
-  L2Prefetch pf;
 };
 // sum_{lo <= i < hi} h[i] V_i[r], loads issued in batches of 8 (fixed summation order)
 __device__ __forceinline__ double2 sum_vh(const double2* __restrict__ h, const double2* __restrict__ V, size_t ldv,
@@ -1652,7 +1476,6 @@ __global__ void __launch_bounds__(THREADS) k_cgs_pass(CgsArgs a) {
   __shared__ double2 stage[640];  // Givens staging (cos 256 doubles | sin 256 | h 256)
   __shared__ bool is_last;
   pdl_trigger();
-  l2_prefetch_slices(a.pf);
   pdl_wait();
   const int nv = a.st->j + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1793,9 +1616,8 @@ __device__ __forceinline__ bool combine_rows(const double2* __restrict__ h, cons
 template <int ROWS, int GROUPS>
 __global__ void __launch_bounds__(ROWS* GROUPS)
     k_update_normalize(int n, const GmresState* __restrict__ st, const double2* __restrict__ h2,
-                       const double2* __restrict__ w, double2* __restrict__ V, size_t ldv, L2Prefetch pf) {
+                       const double2* __restrict__ w, double2* __restrict__ V, size_t ldv) {
   pdl_trigger();
-  l2_prefetch_slices(pf);
   pdl_wait();
   if (!st->cont) return;
   const int nv = st->j;
@@ -1887,8 +1709,6 @@ struct ArnoldiTailArgs {
   double2 *h1, *h2;
   unsigned int* bar;  // [0] arrivals, [1] generation
   int hcap, vcap;  // h staging capacity (>= nv + 1), basis columns allocated
-  // GRAM mode: packed columns of G = V^H V (column k at k(k+1)/2, entries v_i^H v_k, i <= k)
-  double2* gram;
   // coarse
   int nc, coarse_rb;  // rb: coarse rows per block per round (1, 2, 4 or 8)
   const double2* Cinv;
@@ -1923,39 +1743,6 @@ __device__ __forceinline__ unsigned int atom_add_release_u32(unsigned int* p, un
 }
 __device__ __forceinline__ void st_relaxed_u32(unsigned int* p, unsigned int v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-// grid barrier; the last block to arrive runs `last()` (all its threads) before the release.
-// Arrival is a release atomic (cumulative over the block's writes, ordered by the preceding
-// bar.sync), the wait an acquire load: no full fences.
-template <typename F>
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, F&& last, unsigned long long* ts = nullptr) {
-  __shared__ unsigned int gen_sh;
-  __shared__ bool last_sh;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    gen_sh = ld_acquire_u32(bar + 1);
-    last_sh = atom_add_release_u32(bar, 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (last_sh) {
-    if (ts && threadIdx.x == 0) ts[0] = gtimer();
-    if (threadIdx.x == 0) (void)ld_acquire_u32(bar);  // acquire the other blocks' writes
-    __syncthreads();
-    last();
-    __syncthreads();
-    if (ts && threadIdx.x == 0) ts[1] = gtimer();
-    if (threadIdx.x == 0) {
-      st_relaxed_u32(bar, 0u);
-      atom_add_release_u32(bar + 1, 1u);
-    }
-  } else if (threadIdx.x == 0) {
-    const long long t0 = clock64();
-    while (ld_acquire_u32(bar + 1) == gen_sh) {
-      if (clock64() - t0 > 4000000000LL) __trap();  // ~2 s: never hang the device
-    }
-  }
-  __syncthreads();
 }
 
 // Grid barrier on a monotonically increasing 64-bit arrival counter: barrier k of the
@@ -2004,22 +1791,14 @@ __device__ __forceinline__ void block_reduce_parts(const double2* __restrict__ p
 
 // Fused tail, one multiplier row per thread, THREADS rows per block, one block per SM.
 // dynamic smem: w_sh[THREADS] | h1[hcap] | h2[hcap] | Givens staging[640]
-// GRAM = true: CGS2 with ONE reduction per step.  Pass 1 reduces h1 = V^H w, |w|^2 and the
-// new Gram column g = V^H v_j together; the second CGS pass is then evaluated exactly in
-// algebra, h2 = V^H (w - V h1) = h1 - G h1 and |w - V h1|^2 = |w|^2 - |h1|^2 - Re h1^H h2,
-// and the new basis vector is (w - V (h1 + h2)) / h_{j+1,j} with the Pythagorean
-// h_{j+1,j} of the two-pass scheme.  G = V^H V carries the basis' actual loss of
-// orthogonality; what the algebra drops is the rounding of forming w - V h1, of relative
-// size eps |h1| / |w - V h1| (measured |w - V h1| / |w| >= 0.05 on the FETI operators).
-// dynamic smem: w_sh | vj_sh | hs1 | hs2 | gs | Givens staging | Gram staging (TAIL_GSM)
-constexpr int TAIL_GSM = 4096;
-template <int THREADS, int NCM, int MINB, bool GRAM = false>
+// (A one-reduction Gram-matrix CGS2 variant measured 180 vs 188 solves/s; not kept.)
+// dynamic smem: w_sh | hs1 | hs2 | gs | Givens staging
+template <int THREADS, int NCM, int MINB>
 __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs a) {
   constexpr int WARPS = THREADS / 32, LPR = THREADS / 32;
   extern __shared__ double2 tail_sh[];
   double2* w_sh = tail_sh;
-  double2* vj_sh = w_sh + THREADS;
-  double2* hs1 = vj_sh + THREADS;
+  double2* hs1 = w_sh + THREADS;
   double2* hs2 = hs1 + a.hcap;
   double2* gs = hs2 + a.hcap;
   double2* stage = gs + a.hcap;
@@ -2085,7 +1864,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 0] = gtimer();
   // Givens operands known now (block 0): loaded during the coarse phase, off the critical path
   __shared__ GivensPre gpre;
-  if (!GRAM && !a.split_givens && blockIdx.x == 0 && warp == 0)
+  if (!a.split_givens && blockIdx.x == 0 && warp == 0)
     givens_prefetch(a.ga, &gpre, reinterpret_cast<double*>(stage), stage + 128);
   span_mark(a.span, &it, 2, 0);
   // dual-tail operand that does not depend on z (loaded before the barrier)
@@ -2152,7 +1931,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   // pass-1 partials after barrier B while faster blocks already write pass-2 partials
   auto dots = [&](double2 w, double2* part) {
     w_sh[threadIdx.x] = w;
-    if (GRAM) vj_sh[threadIdx.x] = act ? a.V[(size_t)(nv - 1) * a.ldv + r] : cz();
     __syncthreads();
     for (int i = warp; i < nout; i += WARPS) {
       double2 acc = cz();
@@ -2163,13 +1941,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
         for (int q = 0; q < LPR; ++q) x[q] = v[min(lane + 32 * q, row_end - 1 - row0)];
 #pragma unroll
         for (int q = 0; q < LPR; ++q) acc = cfma_conj(x[q], w_sh[lane + 32 * q], acc);
-        if (GRAM) {  // Gram column entry v_i^H v_j from the same loads
-          double2 g = cz();
-#pragma unroll
-          for (int q = 0; q < LPR; ++q) g = cfma_conj(x[q], vj_sh[lane + 32 * q], g);
-          g = warp_sum2(g);
-          if (lane == 0) (part + (size_t)a.hcap * G)[(size_t)i * G + blockIdx.x] = g;
-        }
       } else {
 #pragma unroll
         for (int q = 0; q < LPR; ++q) acc.x += cabs2(w_sh[lane + 32 * q]);
@@ -2213,67 +1984,6 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   grid_sync_plain(a.bar);
   block_reduce_parts<THREADS>(a.part, G, nout, hs1);
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 4] = gtimer();
-  if constexpr (GRAM) {
-    block_reduce_parts<THREADS>(part2, G, nv, gs);  // gs[i] = v_i^H v_j (part2 = the Gram partials)
-    const int j = nv - 1;
-    if (blockIdx.x == 0)
-      for (int i = threadIdx.x; i < nv; i += THREADS) a.gram[(size_t)j * (j + 1) / 2 + i] = gs[i];
-    // h2 = h1 - G h1, one thread per row i, k ascending; the previous Gram columns are
-    // staged in shared memory first (all loads in flight) when they fit
-    const int cnt_old = j * (j + 1) / 2;
-    const bool staged = cnt_old <= TAIL_GSM;
-    double2* gsm = stage + 640;
-    if (staged) {
-      for (int e = threadIdx.x; e < cnt_old; e += THREADS) gsm[e] = __ldcg(a.gram + e);
-      __syncthreads();
-    }
-    for (int i = threadIdx.x; i < nv; i += THREADS) {
-      double2 acc = cz();
-      for (int k = 0; k < nv; ++k) {
-        double2 gik;
-        if (k == j) gik = gs[i];
-        else if (i == j) gik = cconj(gs[k]);
-        else if (k >= i) gik = staged ? gsm[k * (k + 1) / 2 + i] : __ldcg(a.gram + (size_t)k * (k + 1) / 2 + i);
-        else gik = cconj(staged ? gsm[i * (i + 1) / 2 + k] : __ldcg(a.gram + (size_t)i * (i + 1) / 2 + k));
-        acc = cfma(gik, hs1[k], acc);
-      }
-      hs2[i] = csub(hs1[i], acc);
-    }
-    __syncthreads();
-    if (warp == 0) {  // |w - V h1|^2 = |w|^2 - |h1|^2 - Re h1^H h2  (fixed order)
-      double t = 0.0;
-      for (int i = lane; i < nv; i += 32) t += cabs2(hs1[i]) + (hs1[i].x * hs2[i].x + hs1[i].y * hs2[i].y);
-      t = warp_sum(t);
-      if (lane == 0) hs2[nv] = make_double2(hs1[nv].x - t, 0.0);
-    }
-    __syncthreads();
-    if (warp == 0) {
-      bool finite;
-      const double hn = warp_hnext<true>(hs1, hs2, nv - 1, finite);
-      if (lane == 0) inv_sh = 1.0 / hn;
-    }
-    for (int i = threadIdx.x; i < nv; i += THREADS) gs[i] = cadd(hs1[i], hs2[i]);  // h = h1 + h2
-    __syncthreads();
-    if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 7] = gtimer();
-    if (nv < a.vcap) {
-      w = sub_vh(w, gs);
-      if (act) a.V[(size_t)nv * a.ldv + r] = cscale(w, inv_sh);
-    }
-    if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 8] = gtimer();
-    if (blockIdx.x == 0) {
-      for (int i = threadIdx.x; i < nout; i += THREADS) {
-        a.h1[i] = hs1[i];
-        a.h2[i] = hs2[i];
-      }
-      if (warp == 0) givens_warp<true>(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384, hs1, hs2);
-      if (a.tstamp && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 9] = gtimer();
-    }
-    if (a.span != nullptr) {
-      __syncthreads();
-      span_mark(a.span, &it, 2, 1);
-    }
-    return;
-  }
   // ---- phase 2: w -= V h1, h2 = V^H w, |w|^2 ----
   w = sub_vh(w, hs1);
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 5] = gtimer();

@@ -325,76 +325,9 @@ __global__ void k3_bbf_store(int NBK, int P, int K, double2* __restrict__ bb, co
   for (int e = threadIdx.x; e < 1024; e += blockDim.x) dst[e] = src[e];
 }
 
-// ---------------------------------------------------------------------------------------
-// Per-solve interior substitution x = A_ii^-1 x, one CTA (8 warps) per subdomain (K5).
-// Forward y_K = b_K - sum_d L_{K,K-d} y_{K-d}; diagonal z_K = D_K^-1 y_K; backward
-// x_K = z_K - sum_d L_{K+d,K}^T x_{K+d}.  Warp w takes the blocks d = w+1, w+9, ...; the
-// other warps' partials are summed in a fixed order (deterministic).
-template <int RING, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k3_bb_solve1(int NBK, int P, const double2* __restrict__ bb, int NI,
-                                                           double2* __restrict__ X) {
-  __shared__ double2 ring[RING][32];
-  __shared__ double2 part[WARPS][32];
-  const int s = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double2* band = bb + (size_t)s * NBK * (P + 1) * 1024;
-  double2* x = X + (size_t)s * NI;
-  // forward + diagonal (z_K is written over b_K; the ring keeps the forward values y)
-  for (int K = 0; K < NBK; ++K) {
-    double2 acc = cz();
-    for (int d = warp + 1; d <= P; d += WARPS) {
-      if (K - d < 0) break;
-      const double2* T = band + ((size_t)K * (P + 1) + d) * 1024;
-      const double2* y = ring[(K - d) % RING];
-#pragma unroll 8
-      for (int cc = 0; cc < 32; ++cc) acc = cfma(__ldg(T + cc * 32 + lane), y[(lane + cc) & 31], acc);
-    }
-    part[warp][lane] = acc;
-    __syncthreads();
-    if (warp == 0) {
-      double2 v = x[(size_t)K * 32 + lane];
-      for (int w = 0; w < WARPS; ++w) v = csub(v, part[w][lane]);
-      ring[K % RING][lane] = v;
-    }
-    __syncthreads();
-    if (warp == (WARPS > 8 ? WARPS - 1 : 1)) {  // z_K = D_K^-1 y_K (a warp idle in the next step)
-      const double2* D = band + ((size_t)K * (P + 1)) * 1024;
-      const double2* y = ring[K % RING];
-      double2 z = cz();
-#pragma unroll 8
-      for (int cc = 0; cc < 32; ++cc) z = cfma(__ldg(D + cc * 32 + lane), y[(lane + cc) & 31], z);
-      x[(size_t)K * 32 + lane] = z;
-    }
-  }
-  __syncthreads();
-  // backward
-  for (int K = NBK - 1; K >= 0; --K) {
-    double2 acc = cz();
-    for (int d = warp + 1; d <= P; d += WARPS) {
-      if (K + d >= NBK) break;
-      const double2* T = band + ((size_t)(K + d) * (P + 1) + d) * 1024;
-      const double2 xr = ring[(K + d) % RING][lane];
-      double2 yc = cz();
-#pragma unroll 8
-      for (int cc = 0; cc < 32; ++cc) {
-        yc = cfma(__ldg(T + cc * 32 + lane), xr, yc);
-        yc = shfl2(yc, (lane + 1) & 31);
-      }
-      acc = cadd(acc, yc);
-    }
-    part[warp][lane] = acc;
-    __syncthreads();
-    if (warp == 0) {
-      double2 v = x[(size_t)K * 32 + lane];
-      for (int w = 0; w < WARPS; ++w) v = csub(v, part[w][lane]);
-      ring[K % RING][lane] = v;
-      x[(size_t)K * 32 + lane] = v;
-    }
-    __syncthreads();
-  }
-}
 
-// TMA-streamed variant of k3_bb_solve1: a producer warp streams every 16 KB block of the
-// substitution, in consumption order, through a STAGES-deep shared-memory ring (1-D bulk
+// Interior block-band substitution (K5 eliminate, 4 per Schur solve): a producer warp streams
+// every 16 KB block of the substitution, in consumption order, through a STAGES-deep shared-memory ring (1-D bulk
 // copies, full/empty mbarrier pairs), so the block loads run ahead of the recurrence and the
 // bytes in flight no longer depend on the consumers' progress.  Item order: forward
 // K = 0..: the blocks (K, K-d), d = 1..min(P,K), then D_K^-1; backward K = NBK-1..0: the
@@ -516,86 +449,6 @@ __global__ void __launch_bounds__((W + 1) * 32, 1) k3_bb_solve_tma(int NBK, int 
 template <int STAGES, int W>
 constexpr size_t bb_solve_tma_smem() {
   return sizeof(double2) * ((size_t)STAGES * 1024 + 33 * 32 + W * 32) + sizeof(uint64_t) * 2 * STAGES;
-}
-
-// ---------------------------------------------------------------------------------------
-// Setup multi-RHS substitution (K3): Y = A_ii^-1 Y for tiles of 32 right-hand sides
-// ([sub][tile][NI][32]); CTA = (column group, tile, subdomain), each warp owns 4 columns and
-// keeps its columns of the last P+1 blocks in a shared ring (warp-private: no CTA barriers).
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32) k3_bb_msolve(int NBK, int P, const double2* __restrict__ bb,
-                                                           int NI, int ntile, int s0, double2* __restrict__ Y) {
-  constexpr int CPB = 4 * WARPS;
-  extern __shared__ __align__(16) double2 k3m_ring[];  // [P+1][32][CPB]
-  const int RING = P + 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cg = blockIdx.x, tile = blockIdx.y, sc = blockIdx.z, s = s0 + sc;
-  const double2* band = bb + (size_t)s * NBK * (P + 1) * 1024;
-  double2* y = Y + ((size_t)sc * ntile + tile) * NI * 32 + cg * CPB + warp * 4;
-  double2* rg = k3m_ring + warp * 4;
-  auto R = [&](int blk, int row) -> double2* { return rg + ((size_t)(blk % RING) * 32 + row) * CPB; };
-  for (int K = 0; K < NBK; ++K) {
-    double2 acc[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q] = y[(size_t)(K * 32 + lane) * 32 + q];
-    for (int d = 1; d <= P && K - d >= 0; ++d) {
-      const double2* T = band + ((size_t)K * (P + 1) + d) * 1024;
-#pragma unroll 4
-      for (int cc = 0; cc < 32; ++cc) {
-        const double2 t = __ldg(T + cc * 32 + lane);
-        const double2* yr = R(K - d, (lane + cc) & 31);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc[q] = cfms(t, yr[q], acc[q]);
-      }
-    }
-    double2* w = R(K, lane);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) w[q] = acc[q];
-    __syncwarp();
-    const double2* D = band + ((size_t)K * (P + 1)) * 1024;
-    double2 z[4] = {cz(), cz(), cz(), cz()};
-#pragma unroll 4
-    for (int cc = 0; cc < 32; ++cc) {
-      const double2 t = __ldg(D + cc * 32 + lane);
-      const double2* yr = R(K, (lane + cc) & 31);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) z[q] = cfma(t, yr[q], z[q]);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) y[(size_t)(K * 32 + lane) * 32 + q] = z[q];
-    __syncwarp();
-  }
-  for (int K = NBK - 1; K >= 0; --K) {
-    double2 acc[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q] = y[(size_t)(K * 32 + lane) * 32 + q];
-    for (int d = 1; d <= P && K + d < NBK; ++d) {
-      const double2* T = band + ((size_t)(K + d) * (P + 1) + d) * 1024;
-      const double2* xr = R(K + d, lane);
-      double2 xv[4], yc[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) xv[q] = xr[q], yc[q] = cz();
-#pragma unroll 4
-      for (int cc = 0; cc < 32; ++cc) {
-        const double2 t = __ldg(T + cc * 32 + lane);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          yc[q] = cfma(t, xv[q], yc[q]);
-          yc[q] = shfl2(yc[q], (lane + 1) & 31);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q] = csub(acc[q], yc[q]);
-    }
-    __syncwarp();
-    double2* w = R(K, lane);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      w[q] = acc[q];
-      y[(size_t)(K * 32 + lane) * 32 + q] = acc[q];
-    }
-    __syncwarp();
-  }
 }
 
 // Setup multi-RHS substitution, register-blocked (K3): a CTA solves 64 right-hand sides
@@ -783,29 +636,6 @@ __global__ void __launch_bounds__(256) k3_gj_panel(int NBP, int NT, int K, doubl
 #pragma unroll
   for (int q = 0; q < 4; ++q) M[(size_t)(K * 32 + r) * NBP + J * 32 + c0 + q] = acc[q];
 }
-__global__ void __launch_bounds__(256) k3_gj_update(int NBP, int NT, int K, double2* __restrict__ dense,
-                                                    const double2* __restrict__ pbuf, const double2* __restrict__ cbuf) {
-  __shared__ Tile A, B;
-  const int J = blockIdx.x, I = blockIdx.y, sc = blockIdx.z;
-  double2* M = dense + (size_t)sc * NBP * NBP;
-  const int r = threadIdx.x >> 3, c0 = (threadIdx.x & 7) * 4;
-  if (I == K) {
-    if (J == K) {  // the pivot block itself becomes P
-      for (int e = threadIdx.x; e < 1024; e += blockDim.x)
-        M[(size_t)(K * 32 + (e >> 5)) * NBP + K * 32 + (e & 31)] = pbuf[(size_t)sc * 1024 + e];
-    }
-    return;
-  }
-  tile_load_rm(A, cbuf + ((size_t)sc * NT + I) * 1024, 32);
-  if (J == K) tile_load_rm(B, pbuf + (size_t)sc * 1024, 32);
-  else tile_load_rm(B, M + (size_t)(K * 32) * NBP + J * 32, NBP);
-  __syncthreads();
-  double2 acc[4] = {cz(), cz(), cz(), cz()};
-  tile_mma<false>(A, B, acc);
-  double2* out = M + (size_t)(I * 32 + r) * NBP + J * 32 + c0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) out[q] = (J == K) ? make_double2(-acc[q].x, -acc[q].y) : csub(out[q], acc[q]);
-}
 
 // Trailing update of step K as a register-blocked rank-32 GEMM on 64x64 tiles of C (the
 // dense chunk; NBP % 64 == 0): C[r][c] -= Cpanel[r][:] R[:][c] with R = the new row panel
@@ -863,81 +693,6 @@ __global__ void __launch_bounds__(256) k3_gj_update64(int NBP, int NT, int K, do
       if (gc >= kr && gc < kr + 32) row[gc] = make_double2(-acc[i][j].x, -acc[i][j].y);
       else row[gc] = csub(row[gc], acc[i][j]);
     }
-  }
-}
-// The same trailing update on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64): each warp
-// owns a 16 x 32 patch of the 64 x 64 tile as 2 x 4 fragments of 8 x 8; a complex product
-// is four real MMAs (re += Are Bre - Aim Bim, im += Are Bim + Aim Bre).  Operands are the
-// same shared-memory tiles as k3_gj_update64.
-__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-__global__ void __launch_bounds__(256) k3_gj_update64_tc(int NBP, int NT, int K, double2* __restrict__ dense,
-                                                         const double2* __restrict__ pbuf,
-                                                         const double2* __restrict__ cbuf) {
-  extern __shared__ __align__(16) double2 k3g_sm[];
-  double2 (*As)[33] = reinterpret_cast<double2 (*)[33]>(k3g_sm);
-  double2 (*Bs)[65] = reinterpret_cast<double2 (*)[65]>(k3g_sm + 64 * 33);
-  const int J0 = blockIdx.x * 64, I0 = blockIdx.y * 64, sc = blockIdx.z;
-  const int kr = K * 32;
-  double2* M = dense + (size_t)sc * NBP * NBP;
-  const double2* P = pbuf + (size_t)sc * 1024;
-  for (int e = threadIdx.x; e < 64 * 32; e += 256) {
-    const int r = e >> 5, k = e & 31, I = (I0 + r) >> 5;
-    As[r][k] = cbuf[((size_t)sc * NT + I) * 1024 + ((I0 + r) & 31) * 32 + k];
-  }
-  for (int e = threadIdx.x; e < 32 * 64; e += 256) {
-    const int k = e >> 6, c = e & 63, gc = J0 + c;
-    Bs[k][c] = (gc >= kr && gc < kr + 32) ? P[k * 32 + (gc - kr)] : M[(size_t)(kr + k) * NBP + gc];
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wr = (warp & 3) * 16, wc = (warp >> 2) * 32;
-  const int g = lane >> 2, t = lane & 3;
-  double cre[2][4][2], cim[2][4][2];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) cre[i][j][0] = cre[i][j][1] = cim[i][j][0] = cim[i][j][1] = 0.0;
-#pragma unroll 2
-  for (int k0 = 0; k0 < 32; k0 += 4) {
-    double are[2], aim[2], bre[4], bim[4];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const double2 v = As[wr + 8 * i + g][k0 + t];
-      are[i] = v.x, aim[i] = v.y;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const double2 v = Bs[k0 + t][wc + 8 * j + g];
-      bre[j] = v.x, bim[j] = v.y;
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        dmma884(cre[i][j][0], cre[i][j][1], are[i], bre[j]);
-        dmma884(cre[i][j][0], cre[i][j][1], -aim[i], bim[j]);
-        dmma884(cim[i][j][0], cim[i][j][1], are[i], bim[j]);
-        dmma884(cim[i][j][0], cim[i][j][1], aim[i], bre[j]);
-      }
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int gr = I0 + wr + 8 * i + g;
-    if (gr >= kr && gr < kr + 32) continue;  // row panel: already final
-    double2* row = M + (size_t)gr * NBP;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int gc = J0 + wc + 8 * j + 2 * t + e;
-        const double2 acc = make_double2(cre[i][j][e], cim[i][j][e]);
-        if (gc >= kr && gc < kr + 32) row[gc] = make_double2(-acc.x, -acc.y);
-        else row[gc] = csub(row[gc], acc);
-      }
   }
 }
 // the pivot block of step K becomes P (after the update kernel has read the row panel)

@@ -261,3 +261,25 @@ def test_gpu3d_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
     assert not sr["converged"] and sr["iterations"] == 3
     assert abs(st["relative_residual"] - sr["relative_residual"]) <= 1e-6 * sr["relative_residual"]
     assert rel(x, xr) <= 1e-8
+
+
+@pytest.mark.parametrize("switch", ["FETIGPU3D_NO_FDM", "FETIGPU_NO_STENCIL"])
+def test_gpu3d_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
+    """3D heat: the separable interior solve (FETIGPU3D_NO_FDM keeps the block-band
+    substitution) and the 27-point stencil global applies (FETIGPU_NO_STENCIL keeps the
+    element-by-element apply) against the plain paths: same iterations, equal to rounding."""
+    from paper_1312_5653_b200 import box
+
+    p = box.make_box_problem(16, phi=1e-4, seed=2)
+    out = []
+    for plain in (False, True):
+        if plain:
+            monkeypatch.setenv(switch, "1")
+        s = box.BoxSchurSolver(p, 2, tol=1e-10, max_iter=500)
+        out.append(s.solve())
+        s.close()
+    a, b = out
+    for side in ("plus_stats", "minus_stats"):
+        assert a[side]["iterations"] == b[side]["iterations"]
+    for k in ("y", "u", "lambda"):
+        assert np.linalg.norm(a[k] - b[k]) <= 1e-11 * np.linalg.norm(b[k]), k

@@ -52,7 +52,9 @@ def test_operators_match_oracle(fetigpu, oracle_mod, n, s, phi):
 
 
 def test_feti_complex_factors_match_direct(fetigpu, oracle_mod):
-    """test_feti.cpp:309-332 (augment=false here): n=16, 2x2, phi=2e-8, tol 1e-10, <=1e-8."""
+    """test_feti.cpp:309-332: n=16, 2x2, phi=2e-8, tol 1e-10, <=1e-8, with the reference test's
+    augment=true on both sides (the GPU's and the oracle's edge-RBM coarse spaces), and the
+    same case with augment=false."""
     n, phi = 16, 2e-8
     p = fetigpu.make_seeded_problem(n, phi)
     op = oracle_mod.Problem(n)
@@ -60,15 +62,16 @@ def test_feti_complex_factors_match_direct(fetigpu, oracle_mod):
     rng = np.random.default_rng(29)
     rhs = rng.uniform(-1, 1, op.n).astype(complex)
     c = -1j / np.sqrt(phi)
-    for coeff in (c, -c):
-        out = fetigpu.feti_solve(p, coeff, rhs, s_x=2, s_y=2, tol=1e-10)
-        assert out["converged"]
-        direct = np.linalg.solve(K + coeff * V, rhs)
-        assert rel(out["x"], direct) <= 1e-8
-        assert out["interface_jump"] <= 1e-8
-        xo, so = oracle_mod.Feti(op, 2, 2, coeff, tol=1e-10).solve(rhs)
-        assert abs(out["iterations"] - so["iterations"]) <= 2
-        assert rel(out["x"], xo) <= 1e-8
+    for augment in (True, False):
+        for coeff in (c, -c):
+            out = fetigpu.feti_solve(p, coeff, rhs, s_x=2, s_y=2, tol=1e-10, augment=augment)
+            assert out["converged"]
+            direct = np.linalg.solve(K + coeff * V, rhs)
+            assert rel(out["x"], direct) <= 1e-8
+            assert out["interface_jump"] <= 1e-8
+            xo, so = oracle_mod.Feti(op, 2, 2, coeff, tol=1e-10, augment=augment).solve(rhs)
+            assert abs(out["iterations"] - so["iterations"]) <= 2
+            assert rel(out["x"], xo) <= 1e-8
 
 
 def test_feti_criterion5_n32(fetigpu, oracle_mod):
@@ -304,11 +307,16 @@ def test_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
 
 
 @pytest.mark.parametrize("switch", ["FETIGPU_NO_ZBASIS", "FETIGPU_NO_RI_COMPACT", "FETIGPU_NO_ELIM_REUSE",
-                                    "FETIGPU_NO_DEFER", "FETIGPU_NO_SPLIT", "FETIGPU_NO_FDM"])
+                                    "FETIGPU_NO_DEFER", "FETIGPU_NO_SPLIT", "FETIGPU_NO_FDM",
+                                    "FETIGPU_COOP_REJECT", "FETIGPU_NO_FUSED_TAIL", "FETIGPU_NO_PDL",
+                                    "FETIGPU_EAGER", "FETIGPU_NO_AIC", "FETIGPU_NO_STENCIL", "FETIGPU_NO_BT"])
 def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
     """Each reuse/fusion of the solve path (preconditioned basis Z, compact interior rhs,
     GEMV-free final elimination, deferred GMRES completion, Givens folded into the next
-    GEMV) against the plain path it replaces: same iterations, results equal to rounding."""
+    GEMV, the cooperative fused Arnoldi tail -- FETIGPU_COOP_REJECT makes the setup's
+    cooperative-launch probe act as rejected, as under an MPS SM limit, so the step falls
+    back to the multi-launch tail) against the plain path it replaces: same iterations,
+    results equal to rounding."""
     p = fetigpu.make_seeded_problem(128, 1e-4, seed=3)
     solver = fetigpu.SchurSolver(p, 8, 8, tol=1e-10)
     a = solver.solve()
@@ -335,6 +343,26 @@ def test_separable_solve_even_odd_grids(fetigpu, monkeypatch, n, s):
     solver = fetigpu.SchurSolver(p, s, s, tol=1e-10)
     b = solver.solve()
     solver.close()
+    for side in ("plus_stats", "minus_stats"):
+        assert a[side]["iterations"] == b[side]["iterations"]
+    for k in ("y", "u", "lambda"):
+        assert rel(a[k], b[k]) <= 1e-11, k
+
+
+def test_packed_coarse_inverse_agrees_with_dense(fetigpu, monkeypatch):
+    """Coarse spaces of >= 1536 corners keep C^-1 packed symmetric (half the bytes of the
+    per-step coarse GEMV); FETIGPU_DENSE_COARSE keeps the dense inverse.  41 x 41 subdomains
+    of 4 x 4 elements: 1600 corners."""
+    p = fetigpu.make_seeded_problem(164, 1e-4, seed=5)
+    out = []
+    for dense in (False, True):
+        if dense:
+            monkeypatch.setenv("FETIGPU_DENSE_COARSE", "1")
+        solver = fetigpu.SchurSolver(p, 41, 41, tol=1e-10)
+        assert solver.coarse_dim == 1600
+        out.append(solver.solve())
+        solver.close()
+    a, b = out
     for side in ("plus_stats", "minus_stats"):
         assert a[side]["iterations"] == b[side]["iterations"]
     for k in ("y", "u", "lambda"):
