@@ -17,6 +17,11 @@ Cases (BASELINE.json target: seeded sine modes, y_c = 0, augment = false, tol 1e
   ops_cfg1          dual operator / Dirichlet preconditioner of K +- cV on a seeded lambda
   feti16            FetiSolver<Complex> on K + cV, n = 16, 2x2, phi = 2e-8, seeded rhs,
                     augment = true and false (test_feti.cpp:309-332)
+  crit6_iters       acceptance criterion 6's sweep (verify.cpp:194-226; experiments.cpp:118-127,
+                    244-283): thermal 64^2, 8x8, phi = 2e-2 .. 2e-12, augment false / true:
+                    [phi][augment][plus, minus] iterations
+  crit7_iters       criterion 7 (verify.cpp:228-246; experiments.cpp:285-322): thermal n = 16,
+                    32, 64 at H/h = 8, phi = 2e-8, augment = true: [n][plus, minus]
 """
 import os
 import sys
@@ -90,6 +95,19 @@ def main():
         f.close()
         d[f"feti16_aug{int(aug)}_x"] = x
         d[f"feti16_aug{int(aug)}_iters"] = np.array([st["iterations"]])
+    ybar, yc = R.problem_data(R.HEAT, 64)
+    phis = [2.0 * 10.0 ** -e for e in range(2, 13)]
+    d["crit6_phis"] = np.array(phis)
+    d["crit6_iters"] = np.array([[[r["plus_stats"]["iterations"], r["minus_stats"]["iterations"]]
+                                  for r in (R.schur_solve(64, 8, 8, phi, ybar, yc, tol=TOL, max_iter=MAX_ITER,
+                                                          augment=aug) for aug in (False, True))]
+                                 for phi in phis])
+    crit7 = []
+    for n in (16, 32, 64):
+        ybar, yc = R.problem_data(R.HEAT, n)
+        r = R.schur_solve(n, n // 8, n // 8, 2e-8, ybar, yc, tol=TOL, max_iter=MAX_ITER, augment=True)
+        crit7.append([r["plus_stats"]["iterations"], r["minus_stats"]["iterations"]])
+    d["crit7_iters"] = np.array(crit7)
     np.savez_compressed(OUT, **d)
     print(f"wrote {OUT}: {len(d)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")
 
