@@ -11,8 +11,11 @@ reused across steps (the reference's per_solve_seconds regime, experiments.cpp:2
           on the library stream, max over ranks
   e2e   : solves/s through fetigpu_schur_solve (host buffers; H2D of ybar and D2H of y, u,
           lambda inside the timed region)
-  --impl reference : the CPU restatement of the reference (oracle/) on this host's cores,
-          same workload and metric (rank 0 only under torchrun).
+  --impl reference : the REFERENCE's own CPU implementation (oracle/_ref: the unmodified
+          pdeopt sources built against the Eigen-API shim; its ComplexFactorSolver(FetiDp)
+          pair set up once, rate = 1 / per_solve_seconds, experiments.cpp:265) on this host's
+          cores, same workload string and metric (rank 0 only under torchrun); the C++
+          restatement oracle/ where oracle/_ref is absent (kind "port").
 
 Multi-GPU (N > 1, torchrun, one rank per GPU): weak scaling on the subdomain-sharded NCCL
 path.  The mesh grows with N at a fixed 1024 subdomains of 32x32 elements
@@ -21,6 +24,8 @@ mesh), N=8 2048x4096 (64x128); subdomain rows are sharded block-wise, cut-line m
 are exchanged with NCCL send/recv, Krylov dots allreduced, the coarse problem solved
 redundantly.  value = Schur solves/s x N (config-2-equivalent solves/s: each solve of the
 N-GPU mesh is N config-2 blocks of work), so ideal weak scaling is value_N = N value_1.
+--config 3 --gpus N: BASELINE config 3 exactly (2048^2, 64x64 subdomains, phi = 1e-6) on
+every N, value = config-3 solves/s (strong scaling; N = 1 equals the --config 3 line).
 """
 from __future__ import annotations
 
@@ -138,26 +143,77 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-def cpu_sample_oracle(threads, steps, warmup, budget_s=150.0):
-    """The oracle (CPU restatement of the reference) on config 2: setup once, then Schur
-    solves on seeded targets.  Returns (solves/s, iterations, setup s, steps run)."""
-    from oracle import oracle as O
+WORKLOAD2D = {  # one string per BASELINE config, used by BOTH arms (same_config)
+    2: "config2: 1024x1024 Q1 heat, 32x32 subdomains of 32x32, phi=1e-4, tol 1e-10, FP64 complex",
+    3: "config3: 2048x2048 Q1 heat, 64x64 subdomains of 32x32, phi=1e-6, tol 1e-10, FP64 complex",
+}
+CONFIG2D = {2: (N_GRID, S_SUB, PHI), 3: (2 * N_GRID, 2 * S_SUB, 1e-6)}
 
-    p = O.Problem(N_GRID)
-    pair = O.SchurPair(p, S_SUB, S_SUB, PHI, tol=TOL, max_iter=MAX_ITER, threads=threads)
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_sample_reference(config, threads, steps, warmup, budget_s=150.0):
+    """The REFERENCE on the host cores: its unmodified sources (oracle/_ref, built against the
+    Eigen-API shim) through its own classes -- solve_range_space's two
+    ComplexFactorSolver(FetiDp) set up once (control.cpp:302-304), then per step the dual part
+    of solve_range_space (control.cpp:306-320) on a fresh seeded target.  The rate is
+    1 / per_solve_seconds, the reference's own per-solve time (the wall time of the two
+    factor solves, experiments.cpp:265).  Falls back to the C++ restatement (oracle/) where
+    oracle/_ref was not built.  Returns a dict."""
+    n, s, phi = CONFIG2D[config]
+    import paper_1312_5653_b200 as F
+
+    def target(k):
+        return F.make_seeded_problem(n, phi, seed=k).target_state
+
+    try:
+        from oracle import refbind as R
+
+        R.lib()
+        kind = "reference"
+    except Exception:
+        kind = "port"
+    if kind == "reference":
+        pair = R.FactorPair(n, s, s, phi, tol=TOL, max_iter=MAX_ITER, threads=threads)
+        run = lambda yb: pair.solve(yb)[1]  # noqa: E731
+        what = (f"pdeopt ComplexFactorSolver(FetiDp) x2 (unmodified reference sources, Eigen-API shim), "
+                f"FetiConfig::threads={threads}")
+    else:
+        from oracle import oracle as O
+
+        op = O.Problem(n)
+        pair = O.SchurPair(op, s, s, phi, tol=TOL, max_iter=MAX_ITER, threads=threads)
+
+        def run(yb):
+            t0 = time.perf_counter()
+            r = pair.run(yb)
+            return {"per_solve_seconds": time.perf_counter() - t0,
+                    "iterations": (r["plus_stats"]["iterations"], r["minus_stats"]["iterations"])}
+        what = f"oracle/ (C++ restatement), std::thread x{threads}"
     for w in range(warmup):
-        pair.run(p.target_sine(1000 + w))
+        run(target(1000 + w))
     times, its = [], None
     t_start = time.perf_counter()
     for k in range(steps):
-        ybar = p.target_sine(k)
-        t0 = time.perf_counter()
-        r = pair.run(ybar)
-        times.append(time.perf_counter() - t0)
-        its = (r["plus_stats"]["iterations"], r["minus_stats"]["iterations"])
+        st = run(target(k))
+        times.append(st["per_solve_seconds"])
+        its = st["iterations"]
         if time.perf_counter() - t_start > budget_s:
             break
-    return len(times) / sum(times), its, pair.setup_seconds, len(times)
+    rate = len(times) / sum(times)
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": kind, "cpu_model": cpu_model(),
+            "sample": f"{len(times)} {WORKLOAD2D[config].split(':')[0]} Schur solves with the factors reused, "
+                      f"{what}; setup {pair.setup_seconds:.1f} s; iterations {list(its)}",
+            "setup_seconds": pair.setup_seconds, "iterations": list(its), "steps_run": len(times)}
 
 
 def solve_roofline(solver, prof, steps, ms_per_step, hbm_peak):
@@ -173,22 +229,36 @@ def solve_roofline(solver, prof, steps, ms_per_step, hbm_peak):
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path (oracle/_ref) on
+    this host's cores, rank 0 only, on the same workload / metric as our arm.  The 3D configs
+    (4, 5) have no reference counterpart (the reference is 2D only): the oracle's 3D
+    restatement on a bounded sample stands in."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    # each step is one full config-2 Schur solve (~10 s on 16 cores); warm-up is capped at
-    # one solve and the timed steps at a 150 s budget so the arm ends within minutes
-    rate, its, setup_s, ran = cpu_sample_oracle(threads, args.steps, min(args.warmup, 1))
+    if args.config in CONFIG3D:
+        cfg = CONFIG3D[args.config]
+        rate, ts, its_s, su, m = cpu_sample_oracle3d(cfg, threads, None)
+        cb = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+              "sample": f"oracle/ 3D restatement ({threads} threads) on the {m}^3 mesh with 2x2x2 subdomains of the "
+                        f"config's size, one Schur solve {ts:.2f} s, scaled by {cfg['s'] ** 3}/8 subdomains"}
+        workload = cfg["workload"]
+        metric = METRIC.replace("2D Poisson 1M dofs", "3D config %d" % args.config)
+    else:
+        config = 3 if args.config == 3 else 2
+        # each step is one config-2 Schur solve (~5-15 s on 16 cores); warm-up capped at one
+        # solve and the timed steps at a 150 s budget so the arm ends within minutes
+        cb = cpu_sample_reference(config, threads, args.steps, min(args.warmup, 1))
+        rate = cb["value"]
+        workload = WORKLOAD2D[config]
+        metric = METRIC
     line = {
-        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "impl": "reference", "metric": metric, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 / rate, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded sine-mode ybar, seed = step)",
-        "config": {"workload": "config2: 1024x1024 Q1 heat, 32x32 subdomains, phi=1e-4, tol 1e-10",
-                   "phi": PHI, "steps_run": ran, "iterations_plus_minus": its,
-                   "setup_seconds_both_factors": setup_s},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{ran} config-2 Schur solves after setup (oracle/, std::thread x{threads})"},
+        "config": {"workload": workload},
+        "cpu_baseline": cb,
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -209,9 +279,8 @@ def run_gpu(args):
     steps, warmup = args.steps, max(args.warmup, 3)
     n_x, n_y, s_x, s_y, len_x, len_y = weak_problem_args(world)
     phi = PHI
-    if args.config == 3:  # BASELINE config 3 on one GPU: 2048^2, 64x64 subdomains, phi 1e-6
-        if world != 1:
-            raise SystemExit("bench.py --config 3 is the single-GPU config-3 line (--gpus N runs weak scaling)")
+    if args.config == 3:  # BASELINE config 3: 2048^2, 64x64 subdomains, phi 1e-6 -- the same mesh on
+        # every N (subdomain rows sharded over the ranks: strong scaling of the config)
         n_x = n_y = 2 * N_GRID
         s_x = s_y = 2 * S_SUB
         len_x = len_y = 1.0
@@ -265,7 +334,9 @@ def run_gpu(args):
     launches = solver.launch_count() - launches0
     t_dev = ev0.elapsed_time(ev1) / 1000.0
     t_max = max_over_ranks(t_dev, world)
-    value = steps * world / t_max  # config-2-equivalent solves/s (see the module docstring)
+    # weak ladder: config-2-equivalent solves/s (module docstring); --config 3: config-3 solves/s
+    mult = 1 if args.config == 3 else world
+    value = steps * mult / t_max
     # ---------------- e2e: host buffers through the public API ----------------
     # host buffers in pinned memory (the path a serving caller would use)
     host_t = [torch.from_numpy(t).pin_memory().numpy() for t in targets]
@@ -279,7 +350,7 @@ def run_gpu(args):
     w1 = time.perf_counter()
     barrier(world)
     e2e_t = max_over_ranks(w1 - w0, world)
-    e2e = steps * world / e2e_t
+    e2e = steps * mult / e2e_t
     # ---------------- per-kernel roofline pass (same K steps, events per launch) ----------------
     solver.profile(True)
     solver.profile_read(reset=True)
@@ -331,26 +402,33 @@ def run_gpu(args):
         in_graph = {"spans_us": {k: (round(v, 3) if 0.0 <= v < 1e6 else None)
                                  for k, v in spans.items() if k != "steps"}, "steps": spans["steps"]}
         for cls, key in (("precond_gemv", "precond"), ("dual_gemv", "dual")):
-            gbs = solver.class_bytes(cls) / (spans[key] * 1e-6) / 1e9
-            in_graph[cls] = {"achieved_gbs": gbs, "frac": gbs / hbm_peak}
+            if in_graph["spans_us"].get(key) and in_graph["spans_us"][key] > 0.0:
+                gbs = solver.class_bytes(cls) / (spans[key] * 1e-6) / 1e9
+                in_graph[cls] = {"achieved_gbs": gbs, "frac": gbs / hbm_peak}
+            else:
+                in_graph[cls] = None
     # per-solve HBM bytes of the local operators (both GEMV classes) -> effective GB/s
     iters = np.mean([a + b for a, b in its])
+    ms_solve = t_max / steps * 1000.0 / (1 if args.config == 3 else world)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": warmup,
-        "ms_per_step": t_max / steps * 1000.0, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": t_max / steps * 1000.0, "higher_is_better": True,
+        "scaling": "strong" if (args.config == 3 and world > 1) else "weak", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (seeded sine-mode ybar, seed = step; factors random-free FEM)",
         "config": {
-            "workload": ("config2: 1024x1024 Q1 heat, 32x32 subdomains of 32x32, phi=1e-4, tol 1e-10, FP64 complex"
-                         if world == 1 and args.config == 2 else
-                         "config3 (one GPU): 2048x2048 Q1 heat, 64x64 subdomains of 32x32, phi=1e-6, tol 1e-10, "
-                         "FP64 complex; value = config-3 solves/s" if world == 1 else
+            "workload": (WORKLOAD2D[args.config] if (world == 1 or args.config == 3) else
                          f"weak scaling: {n_x}x{n_y} Q1 heat, {s_x}x{s_y} subdomains of 32x32 ({s_x * s_y // world} "
                          f"per GPU), phi=1e-4, tol 1e-10, FP64 complex; value = solves/s x {world}"),
             "phi": phi, "n_free": n, "n_lambda": solver.n_lambda, "coarse_dim": solver.coarse_dim,
             "augment": bool(args.augment),
             "iterations_plus_minus_mean": [float(np.mean([a for a, _ in its])), float(np.mean([b for _, b in its]))],
-            "setup_seconds": setup_s, "l2": "inputs larger than L2 (local operators 0.5 GB streamed per iteration)",
+            "setup_seconds": setup_s,
+            # SURVEY §8d / experiments.cpp:264-265: solves/s including the setup (factorization)
+            "solves_per_s_including_setup": 1.0 / (setup_s + ms_solve / 1000.0),
+            "l2": "inputs larger than L2 (local operators 0.3 GB streamed per iteration)",
             "parallelism": f"subdomain rows sharded over {world} GPUs (NCCL)" if world > 1 else "1 GPU",
+            "weak_or_strong": ("strong: BASELINE config 3 on every N" if args.config == 3 else
+                               "weak: 1024 subdomains of 32x32 per GPU"),
             "kernel_ms_per_step": kernel_breakdown, "profiled_ms_per_step": t_prof,
         },
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 3 * 8 * n},
@@ -388,10 +466,7 @@ def run_gpu(args):
             sv.close()
         line["config"]["phi_sweep"] = sweep
     if rank == 0 and world == 1 and args.config == 2 and not args.no_cpu_baseline:
-        rate, cits, csetup, ran = cpu_sample_oracle(os.cpu_count() or 1, 1, 0)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port",
-                                "sample": f"{ran} config-2 Schur solve after setup ({csetup:.1f} s), oracle/ "
-                                          f"std::thread x{os.cpu_count()}, iterations {cits}"}
+        line["cpu_baseline"] = cpu_sample_reference(2, os.cpu_count() or 1, 1, 0)
     if rank == 0:
         print(json.dumps(line), flush=True)
     solver.close()

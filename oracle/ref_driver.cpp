@@ -52,6 +52,13 @@ ControlProblem make_problem(int kind, int n, double phi, const double* ybar, con
   return p;
 }
 
+// The two factor solvers of solve_range_space (control.cpp:302-304), set up once and reused:
+// the reference's per_solve_seconds regime (experiments.cpp:264-265).
+struct PairHandle {
+  ControlProblem problem;
+  std::unique_ptr<ComplexFactorSolver> plus, minus;
+};
+
 struct FetiHandle {
   ControlProblem problem;
   std::shared_ptr<const FetiPartition> part;
@@ -115,6 +122,59 @@ int ref_schur_solve(int kind, int n, int s_x, int s_y, double phi, const double*
     stats[7] = r.factor_setup_seconds;
     stats[8] = wall;
     stats[9] = r.imag_leak_warning;
+  });
+}
+
+// Setup of solve_range_space's two ComplexFactorSolver(FetiDp) (control.cpp:297-304), timed.
+int ref_pair_create(int kind, int n, int s_x, int s_y, double phi, double tol, int max_iter, int augment, int threads,
+                    void** out, double* setup_seconds) {
+  return guarded([&] {
+    auto h = std::make_unique<PairHandle>();
+    h->problem = kind == 0 ? make_thermal_problem(n, phi) : make_cantilever_problem(n, phi);
+    FactorSolverConfig cfg;
+    cfg.method = FactorMethod::FetiDp;
+    cfg.tol = tol;
+    cfg.max_iter = max_iter;
+    cfg.feti.s_x = s_x;
+    cfg.feti.s_y = s_y;
+    cfg.feti.augment = augment != 0;
+    cfg.feti.tol = tol;
+    cfg.feti.max_iter = max_iter;
+    cfg.feti.threads = threads;
+    const SchurFactors factors = build_complex_factors(h->problem);
+    detail::WallTimer t;
+    h->plus = std::make_unique<ComplexFactorSolver>(h->problem, factors.c, cfg);
+    h->minus = std::make_unique<ComplexFactorSolver>(h->problem, -factors.c, cfg);
+    *setup_seconds = t.seconds();
+    *out = h.release();
+  });
+}
+
+void ref_pair_destroy(void* h) { delete static_cast<PairHandle*>(h); }
+
+// The dual part of solve_range_space (control.cpp:306-320) for a target ybar (y_c = 0) with
+// the factors reused: rhs = K ybar, a = (K + cV)^-1 rhs, t = (K - cV)^-1 V a, lambda = Re t.
+// stats: [0] its+, [1] its-, [2] converged (both), [3] per_solve_seconds = wall time of the
+// two factor solves (experiments.cpp:265), [4] wall seconds of the whole call.
+int ref_pair_solve(void* hv, const double* ybar, double* lam, double* stats) {
+  return guarded([&] {
+    auto* h = static_cast<PairHandle*>(hv);
+    detail::WallTimer t;
+    ControlProblem& p = h->problem;
+    for (int i = 0; i < p.n(); ++i) p.target_state[i] = ybar[i];
+    p.boundary_values = Vec::Zero(p.m());
+    const Vec rhs = p.schur_rhs();
+    const CVec crhs = rhs.cast<Complex>();
+    auto [a, sp] = h->plus->solve(crhs);
+    CVec va(a.size());
+    p.ops.V.apply(a, va);
+    auto [tv, sm] = h->minus->solve(va);
+    for (int i = 0; i < p.n(); ++i) lam[i] = tv[i].real();
+    stats[0] = sp.iterations;
+    stats[1] = sm.iterations;
+    stats[2] = sp.converged && sm.converged;
+    stats[3] = sp.wall_time + sm.wall_time;
+    stats[4] = t.seconds();
   });
 }
 

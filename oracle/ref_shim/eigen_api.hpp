@@ -706,7 +706,36 @@ template <class S, int Opt, class SI> class SparseMatrix {
   const SI* innerIndexPtr() const { return rowidx_.data(); }
   const S* valuePtr() const { return vals_.data(); }
 
-  SparseMatrix transpose() const {
+  // Lazy transpose (like Eigen's): products A^T x run straight off the CSC arrays; the view
+  // converts to a materialised SparseMatrix where one is needed.
+  class TransposeView {
+   public:
+    explicit TransposeView(const SparseMatrix& a) : a_(a) {}
+    operator SparseMatrix() const { return a_.transposed(); }
+    Index rows() const { return a_.cols(); }
+    Index cols() const { return a_.rows(); }
+    const SparseMatrix& nested() const { return a_; }
+    // y = A^T x with A in CSC: y[c] = the dot of column c of A with x
+    template <class D, std::enable_if_t<is_dense<D>::value, int> = 0>
+    friend auto operator*(const TransposeView& at, const D& x) {
+      const SparseMatrix& a = at.a_;
+      using R = internal::prod_t<S, typename D::Scalar>;
+      if (a.rows() != x.rows()) throw std::invalid_argument("Eigen shim: sparse product dimension mismatch");
+      Matrix<R, Dynamic, D::ColsAtCompileTime> y(a.cols(), x.cols());
+      for (Index j = 0; j < x.cols(); ++j)
+        for (Index c = 0; c < a.cols(); ++c) {
+          R acc = R(0);
+          for (SI k = a.colptr_[c]; k < a.colptr_[c + 1]; ++k) acc += a.vals_[k] * x.coeff(a.rowidx_[k], j);
+          y(c, j) = acc;
+        }
+      return y;
+    }
+
+   private:
+    const SparseMatrix& a_;
+  };
+  TransposeView transpose() const { return TransposeView(*this); }
+  SparseMatrix transposed() const {
     std::vector<Triplet<S, SI>> t;
     t.reserve(vals_.size());
     for (Index c = 0; c < cols_; ++c)
@@ -716,7 +745,7 @@ template <class S, int Opt, class SI> class SparseMatrix {
     return out;
   }
   SparseMatrix adjoint() const {
-    SparseMatrix out = transpose();
+    SparseMatrix out = transposed();
     for (auto& v : out.vals_) v = internal::conj_(v);
     return out;
   }

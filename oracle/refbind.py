@@ -54,6 +54,10 @@ def lib():
         L.ref_problem_data.argtypes = [C.c_int, C.c_int, dp, dp]
         L.ref_schur_solve.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, dp, dp, C.c_double, C.c_int,
                                       C.c_int, C.c_int, dp, dp, dp, dp]
+        L.ref_pair_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int,
+                                      C.c_int, C.POINTER(vp), dp]
+        L.ref_pair_destroy.argtypes = [vp]
+        L.ref_pair_solve.argtypes = [vp, dp, dp, dp]
         L.ref_feti_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                       C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
         L.ref_feti_destroy.argtypes = [vp]
@@ -113,6 +117,35 @@ def schur_solve(n, s_x, s_y, phi, ybar=None, yc=None, tol=1e-10, max_iter=2000, 
         "minus_stats": {"iterations": int(st[1]), "converged": bool(st[3]), "relative_residual": st[5]},
         "imag_leak": st[6], "factor_setup_seconds": st[7], "seconds": st[8], "imag_leak_warning": bool(st[9]),
     }
+
+
+class FactorPair:
+    """solve_range_space's two ComplexFactorSolver(FetiDp) (control.cpp:302-304), set up once;
+    solve() runs the dual part (control.cpp:306-320) with the factors reused and returns
+    lambda plus the reference's per_solve_seconds (experiments.cpp:265)."""
+
+    def __init__(self, n, s_x, s_y, phi, tol=1e-10, max_iter=2000, augment=False, threads=1, kind=HEAT):
+        h, setup = C.c_void_p(), C.c_double()
+        _check(lib().ref_pair_create(kind, n, s_x, s_y, phi, tol, max_iter, int(augment), threads, C.byref(h),
+                                     C.byref(setup)))
+        self._h, self.setup_seconds = h, setup.value
+        self.n = problem_size(kind, n)[0]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().ref_pair_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def solve(self, ybar):
+        yb = np.ascontiguousarray(ybar, dtype=np.float64)
+        if yb.size != self.n:
+            raise ContractError("ybar length != n")
+        lam, st = np.zeros(self.n), np.zeros(5)
+        _check(lib().ref_pair_solve(self._h, _dp(yb), _dp(lam), _dp(st)))
+        return lam, {"iterations": (int(st[0]), int(st[1])), "converged": bool(st[2]), "per_solve_seconds": st[3],
+                     "seconds": st[4]}
 
 
 class Feti:
