@@ -505,8 +505,8 @@ def cpu_sample_oracle3d(cfg, threads, its_gpu):
 
 
 def run_gpu3d(args):
-    """BASELINE configs 4-5.  N > 1 (torchrun): strong scaling of the same mesh, subdomain
-    z-layers sharded over the ranks (NCCL allreduce of the jump partials per operator
+    """BASELINE configs 4-5.  N > 1 (torchrun): strong scaling of the same mesh, contiguous
+    subdomain ranges (z-layers, or y-row blocks of a layer: config 5 on 8 GPUs) per rank (NCCL allreduce of the jump partials per operator
     application, coarse problem assembled by allreduce and solved redundantly)."""
     rank, world, local = dist_env()
     import torch
@@ -608,7 +608,7 @@ def run_gpu3d(args):
                    "coarse_dim": solver.coarse_dim, "iterations_plus_minus_mean": iters, "setup_seconds": setup_s,
                    "setup_phases_s": solver.setup_times(),
                    "l2": "inputs larger than L2 (packed S_bb, S_bb^-1: %.1f GB each)" % (kb / 1e9),
-                   "parallelism": (f"subdomain z-layers sharded over {world} GPUs (NCCL allreduce of jump partials)"
+                   "parallelism": (f"contiguous subdomain ranges (z-layers / y-row blocks) over {world} GPUs (NCCL allreduce of jump partials)"
                                    if world > 1 else "1 GPU"),
                    "kernel_ms_per_step": {c: {"ms_per_step": v["ms"] / steps, "launches_per_step": v["launches"] / steps}
                                           for c, v in prof.items() if v["launches"]}},

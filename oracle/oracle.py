@@ -43,6 +43,12 @@ class NumericalError(RuntimeError):
     pass
 
 
+def set_band_ldlt(on):
+    """Subdomain blocks by symmetric band LDL^T (a third of the pivoted LU's memory; exact,
+    agrees to rounding) -- for the full-size 3D digests (tests/golden/make_3d_digest.py)."""
+    lib().orc_set_band_ldlt(int(bool(on)))
+
+
 def build():
     subprocess.check_call(["make", "-s", "-C", _HERE])
 
@@ -55,6 +61,7 @@ def lib():
         L = C.CDLL(_LIB_PATH)
         vp, dp, ip = C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int)
         L.orc_last_error.restype = C.c_char_p
+        L.orc_set_band_ldlt.argtypes = [C.c_int]
         L.orc_problem_create.argtypes = [C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_double,
                                          C.c_double, C.POINTER(vp)]
         L.orc_problem_create3.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double, C.c_int,

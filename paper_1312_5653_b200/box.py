@@ -106,7 +106,7 @@ class BoxSchurSolver:
         self.problem = problem
         self._desc = problem.desc(s_x, s_y, s_z, tol, max_iter, mass_coeff, device)
         h = C.c_void_p()
-        if world is not None and world > 1:  # subdomain z-layers sharded over NCCL
+        if world is not None and world > 1:  # contiguous subdomain ranges sharded over NCCL
             if nccl_id is None or rank is None:
                 raise ContractError("sharded BoxSchurSolver needs rank, world and the nccl_id of rank 0")
             _check(_native.lib().fetigpu3d_create_sharded(C.byref(self._desc), rank, world, bytes(nccl_id),

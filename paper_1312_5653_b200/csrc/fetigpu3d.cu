@@ -63,7 +63,7 @@ struct Ctx3 {
   fetigpu3d_desc desc{};
   Host3Problem P;
   Host3Partition H;  // this rank's view (local_partition3d); the whole partition on one GPU
-  // sharding: subdomain z-layers per rank, dual and primal vectors replicated,
+  // sharding: contiguous subdomain ranges per rank, dual and primal vectors replicated,
   // one allreduce completes every jump gather (exact: two owners per multiplier row)
   std::unique_ptr<Comm> comm;
   bool dist() const { return comm != nullptr && comm->world() > 1; }
@@ -1147,7 +1147,7 @@ int fetigpu3d_create(const fetigpu3d_desc* desc, fetigpu3d_ctx** out) {
 void fetigpu3d_destroy(fetigpu3d_ctx* ctx) { delete ctx; }
 
 // sharded context: this process is rank `rank` of `world` (one GPU each, NCCL); subdomain
-// z-layers [rank s_z/world, (rank+1) s_z/world); schur/feti solves take and return FULL vectors
+// subdomain ids [rank S/world, (rank+1) S/world); schur/feti solves take and return FULL vectors
 int fetigpu3d_create_sharded(const fetigpu3d_desc* desc, int rank, int world, const unsigned char* nccl_id,
                              fetigpu3d_ctx** out) {
   return guard3([&] {

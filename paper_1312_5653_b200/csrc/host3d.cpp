@@ -332,8 +332,14 @@ Host3Partition build_partition3d(const Host3Problem& P, int sx, int sy, int sz) 
 
 Host3Partition local_partition3d(const Host3Partition& G, int rank, int world) {
   if (world < 1 || rank < 0 || rank >= world) throw ContractError("partition3d: bad rank/world");
-  if (G.sz % world != 0) throw ContractError("partition3d: the subdomain layers (s_z) must divide evenly over the ranks");
-  const int per = G.sz / world * G.sx * G.sy, s0 = rank * per, s1 = s0 + per;
+  // rank r owns the subdomain-index range [r S/R, (r+1) S/R) of the z-outer, y, x ordering:
+  // whole z-layers when R divides s_z, otherwise y-row blocks of a layer (config 5's 4x4x4
+  // grid on 8 ranks: 8 subdomains = 2 y-rows of one z-layer per rank).  Dual vectors are
+  // replicated and every jump is completed by one allreduce, so any split of the
+  // subdomains is exact; contiguous ranges keep each rank's interface small.
+  const int S = G.sx * G.sy * G.sz;
+  if (S % world != 0) throw ContractError("partition3d: the subdomains (s_x s_y s_z) must divide evenly over the ranks");
+  const int per = S / world, s0 = rank * per, s1 = s0 + per;
   Host3Partition L = G;
   L.S = per, L.s_first = s0, L.rank = rank, L.world = world;
   auto slice = [&](auto& v, const auto& src, size_t width) {

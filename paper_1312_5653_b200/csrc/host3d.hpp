@@ -65,8 +65,8 @@ struct Host3Partition {
 
 Host3Problem build_problem3d(const fetigpu3d_desc& d);
 Host3Partition build_partition3d(const Host3Problem& P, int sx, int sy, int sz);
-// Multi-GPU view: rank r of R owns the subdomain z-layers
-// [r sz/R, (r+1) sz/R) — a contiguous range of subdomain ids.  Per-subdomain tables are
+// Multi-GPU view: rank r of R owns the subdomain ids [r S/R, (r+1) S/R) of
+// the z-outer ordering — whole z-layers when R divides s_z, else y-row blocks of a layer.  Per-subdomain tables are
 // sliced; multiplier rows stay global (dual vectors are replicated on every rank) with the
 // slot of a non-local owner set to -1, so every jump gather yields this rank's partial sum
 // and one allreduce completes it (each row has exactly two owners: the sum is exact).

@@ -1,4 +1,6 @@
-"""Sharded 3D path (SURVEY.md §8e for BASELINE configs 4-5): subdomain z-layers per rank,
+"""Sharded 3D path (SURVEY.md §8e for BASELINE configs 4-5): contiguous subdomain ranges per
+rank (whole z-layers when the ranks divide s_z, else y-row blocks of a layer: config 5's
+4x4x4 grid on 8 ranks),
 replicated dual/primal vectors, one allreduce completing every jump gather.
 
 CPU (`not gpu`): the per-rank views built by the C++ host core (fetigpu3d_rank_info) tile the
@@ -26,7 +28,8 @@ LAYOUT_CASES = [  # n, physics, s, worlds
     (12, 0, 3, (3,)),
     (32, 0, 4, (2, 4)),
     (128, 0, 8, (2, 4, 8)),
-    (64, 1, 4, (2, 4)),
+    (64, 1, 4, (2, 4, 8)),    # BASELINE config 5 on 8 ranks: 2 y-rows of one z-layer each
+    (12, 0, 3, (9, 27)),       # ranks not dividing s_z: partial layers
 ]
 
 
@@ -61,7 +64,7 @@ def test_rank_layout3d_rejects_bad_world(fetigpu):
 
     p = box.make_box_problem(12, phi=1e-4)
     with pytest.raises(ContractError):
-        box.rank_info_3d(p, 3, 0, 2)  # 3 subdomain layers over 2 ranks
+        box.rank_info_3d(p, 3, 0, 2)  # 27 subdomains over 2 ranks
 
 
 def _free_port():
@@ -126,6 +129,8 @@ GPU_CASES = [  # n, physics, s, world
     (32, 0, 4, 4),
     (8, 1, 2, 2),
     (16, 1, 4, 2),
+    (16, 1, 4, 8),   # config 5's 4x4x4 grid (at 16^3) on 8 ranks: partial z-layers
+    (16, 0, 2, 4),   # 2x2x2 on 4 ranks: one y-row of a layer per rank
 ]
 
 
