@@ -81,6 +81,8 @@ typedef struct {
  *              ex, ey, dofs_per_node, band half-width of A_ii.
  * Replaces partition_structured (feti.cpp:34-169) + assemble_operators sizes. */
 int fetigpu_problem_info(const fetigpu_desc* desc, int* info);
+/* The same ten fields for a created (one-GPU) context, without rebuilding the partition. */
+int fetigpu_context_info(const fetigpu_ctx* ctx, int* info);
 
 /* Reference thermal target and boundary trace (fem.cpp:194-220): ybar (n_free),
  * yc (n_constrained). Either pointer may be NULL. */

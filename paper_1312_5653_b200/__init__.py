@@ -207,7 +207,11 @@ class SchurSolver:
         else:
             _check(_native.lib().fetigpu_create(C.byref(self._desc), C.byref(h)))
         self._h = h
-        info = problem._info(s_x, s_y)
+        if world is not None and world > 1:
+            info = problem._info(s_x, s_y)
+        else:  # the context's own partition (no second host partition build)
+            info = (C.c_int * 10)()
+            _check(_native.lib().fetigpu_context_info(h, info))
         self.n, self.m, self.n_lambda, self.coarse_dim = int(info[0]), int(info[1]), int(info[4]), int(info[3])
         self.augment = bool(augment)
         if augment:  # coarse = corners + edge-RBM columns (1 per edge, 3 for plane strain)

@@ -73,6 +73,7 @@ def lib():
     pdesc = C.POINTER(Desc)
     L.fetigpu_last_error.restype = C.c_char_p
     L.fetigpu_problem_info.argtypes = [pdesc, ip]
+    L.fetigpu_context_info.argtypes = [C.c_void_p, ip]
     L.fetigpu_target_thermal.argtypes = [pdesc, dp, dp]
     L.fetigpu_target_sine.argtypes = [pdesc, C.c_ulonglong, C.c_int, C.c_int, dp]
     L.fetigpu_create.argtypes = [pdesc, C.POINTER(vp)]
@@ -128,7 +129,7 @@ def lib():
 
 
 EXPORTED_SYMBOLS = (
-    "fetigpu_problem_info", "fetigpu_target_thermal", "fetigpu_target_sine", "fetigpu_create",
+    "fetigpu_problem_info", "fetigpu_context_info", "fetigpu_target_thermal", "fetigpu_target_sine", "fetigpu_create",
     "fetigpu_destroy", "fetigpu_schur_solve", "fetigpu_schur_solve_device", "fetigpu_feti_solve",
     "fetigpu_apply_dual", "fetigpu_apply_precond", "fetigpu_stream", "fetigpu_launch_count",
     "fetigpu_profile", "fetigpu_profile_read", "fetigpu_class_bytes", "fetigpu_last_error",

@@ -94,9 +94,11 @@ __global__ void __launch_bounds__(WARPS * 32)
   uint64_t* empty = full + STAGES;
   double2* bbuf = reinterpret_cast<double2*>(empty + STAGES) + 0;  // [WARPS][CH] new-row values
 
-  const int s = blockIdx.x;
+  // grid (rhs groups, matrices): the CTAs of one matrix are adjacent in launch order, so
+  // they run together and all but the first read the band from L2
+  const int s = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rhs = blockIdx.y * WARPS + warp;
+  const int rhs = blockIdx.x * WARPS + warp;
   const bool active = rhs < nrhs;
   double2* x = X + (size_t)s * x_sub_stride + (size_t)(active ? rhs : 0) * x_rhs_stride;
   double2* myb = bbuf + warp * CH;

@@ -339,7 +339,7 @@ struct Ctx {
         CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = true;
       }
-      dim3 grid(nmat, cdiv(nrhs, WARPS));
+      dim3 grid(cdiv(nrhs, WARPS), nmat);
       launch(FETIGPU_K_BAND, [&] {
         kfn<<<grid, WARPS * 32, smem, stream>>>(colband, rowband, bstride, nrow, X, x_sub_stride, x_rhs_stride, nrhs);
       });
@@ -552,6 +552,10 @@ struct Ctx {
   }
   // one-launch Arnoldi tail when every block of its grid can be co-resident (one GPU only)
   static constexpr int kTailThreads = 512;
+  // register budget (launch_bounds min blocks) 1: 128 registers, the SM's whole register
+  // file.  2 (64 registers, so the next GEMV's CTAs could be resident during the tail)
+  // measured 152 vs 203 solves/s (spills, and the tail's CTAs packed two per SM).
+  static constexpr int kTailMinBlocks = 1;
   size_t tail_smem() const {
     return sizeof(double2) * ((size_t)kTailThreads + 3 * (size_t)(vcap_hint() + 2) + 640);
   }
@@ -565,7 +569,7 @@ struct Ctx {
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc.device));
     CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, desc.device));
     if (!coop) return;  // the fused tail needs a cooperative (co-residency checked) launch
-    auto kfn = k_arnoldi_tail<kTailThreads, 4, 1>;
+    auto kfn = k_arnoldi_tail<kTailThreads, 4, kTailMinBlocks>;
     CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTailThreads, smem));
     // rows per block: spread the rows over every SM (multiple of 32, at most one per thread)
@@ -693,6 +697,15 @@ struct Ctx {
     if (const char* e = std::getenv("FETIGPU_NO_PDL")) pdl = !(e[0] == '1');
     phase_times = std::getenv("FETIGPU_PHASE_TIMES") != nullptr;
     watchdog = std::getenv("FETIGPU_WATCHDOG") != nullptr;
+    // FETIGPU_PHASE_TIMES: host wall time of the setup stages (synchronised), printed
+    auto smark = [&, tp = t0](const char* what) mutable {
+      if (!phase_times) return;
+      sync();
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[fetigpu] setup %-10s %8.2f ms\n", what, std::chrono::duration<double>(now - tp).count() * 1e3);
+      tp = now;
+    };
+    smark("init");
     n = P.n();
     m = P.m();
     nc = H.n_coarse;
@@ -741,6 +754,7 @@ struct Ctx {
     d_n_i = upload(H.n_i);
     d_n_b = upload(H.n_b);
     d_status = alloc<int>(std::max(S, 1));
+    smark("upload");
 
     // K1: block assembly
     d_colband = alloc<double2>((size_t)S * NI * LD);
@@ -790,13 +804,16 @@ struct Ctx {
       d_col_vals = upload(H.col_vals);
     }
 
+    smark("assemble");
     // K2': block-Thomas factors for the per-solve interior solves (reads the band of A_ii,
     // so it runs before the in-place band factorization)
     setup_block_thomas();
+    smark("bt_factor");
     // K2: batched band LDL^T of A_ii (setup multi-RHS solves; per-solve path if W > 32)
     band_ldlt(d_colband, d_rowband, Wt, S, NI, d_status);
     check_status(S, "interior block A_ii");
 
+    smark("band_ldlt");
     // S_bb = A_bb - A_bi A_ii^-1 A_ib  (NB right-hand sides per subdomain)
     {
       double2* Y = alloc<double2>((size_t)S * NB * NI);
@@ -879,6 +896,7 @@ struct Ctx {
         });
       }
       setup_big_coarse();
+    smark("sbb+coarse");
       // packed symmetric storage of S_bb and S_bb^-1 for the per-iteration GEMVs
       NT = (NB + 31) / 32;
       if (NT > 8) throw ContractError("more than 256 interface dofs per subdomain");
@@ -900,6 +918,7 @@ struct Ctx {
       d_Sbb = d_Sinv = nullptr;
     }
 
+    smark("pack+free");
     // workspaces
     d_fi = alloc<double2>((size_t)S * NI);
     d_fb = alloc<double2>((size_t)S * NB);
@@ -971,11 +990,16 @@ struct Ctx {
     CU(cudaMallocHost(&h_pin, sizeof(double2) * 3 * (vcap + 4)));
     CU(cudaMallocHost(&h_stat, sizeof(double2) * kStatSlots));
     d_stat = alloc<double2>(kStatSlots);
+    smark("workspace");
     setup_mass();
     setup_stencil();
+    smark("mass+stencil");
     setup_ri_compact();
+    smark("ri_compact");
     setup_fdm();
+    smark("fdm");
     setup_l2_persistence();
+    smark("l2_window");
     sync();
     setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
@@ -1208,7 +1232,7 @@ struct Ctx {
       g.span = d_span;
       g.it_ptr = span_it ? span_it : &d_gst->iterations;
     }
-    if (in_arnoldi && tail_rpt > 0) g.cont_ptr = &d_gst->cont;
+    if (in_arnoldi && (tail_rpt > 0 || dist())) g.cont_ptr = &d_gst->cont;
     return g;
   }
   // local dual solve u1_b = S_bb^-1 t_b with t_b = -B^T lam, gcp = cpl_b^T t_b, and (last
@@ -1378,37 +1402,22 @@ struct Ctx {
   void setup_ri_compact() {
     if (std::getenv("FETIGPU_NO_RI_COMPACT")) return;
     const int S = H.n_sub, NI = H.NI, E = H.MAXE_IB, NC = H.NC;
-    const size_t rows = (size_t)S * NI;
-    std::vector<int> idx(rows * E);
-    std::vector<double2> val(rows * E), aic(rows * NC);
-    CU(cudaMemcpyAsync(idx.data(), d_ib_idx, idx.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CU(cudaMemcpyAsync(val.data(), d_ib_val, val.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream));
-    if (NC > 0) CU(cudaMemcpyAsync(aic.data(), d_Aic, aic.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+    const long long rows = (long long)S * NI;
+    const int nb = cdiv(rows, 1024);
+    int* bcount = alloc<int>((size_t)nb + 1);
+    launch(FETIGPU_K_OTHER, [&] { k_ri_count<<<nb, 1024, 0, stream>>>(rows, E, NC, d_ib_idx, d_Aic, bcount); });
+    launch(FETIGPU_K_OTHER, [&] { k_ri_scan<<<1, 1024, 0, stream>>>(nb, bcount); });
+    int total = 0;
+    CU(cudaMemcpyAsync(&total, bcount + nb, sizeof(int), cudaMemcpyDeviceToHost, stream));
     sync();
-    std::vector<int> map(rows, -1), cidx;
-    std::vector<double2> cval, caic;
-    int q = 0;
-    for (size_t g = 0; g < rows; ++g) {
-      bool any = false;
-      for (int e = 0; e < E && !any; ++e) any = idx[g * E + e] >= 0;
-      for (int c = 0; c < NC && !any; ++c) any = aic[g * NC + c].x != 0.0 || aic[g * NC + c].y != 0.0;
-      if (!any) continue;
-      map[g] = q++;
-      cidx.insert(cidx.end(), idx.begin() + g * E, idx.begin() + (g + 1) * E);
-      cval.insert(cval.end(), val.begin() + g * E, val.begin() + (g + 1) * E);
-      caic.insert(caic.end(), aic.begin() + g * NC, aic.begin() + (g + 1) * NC);
-    }
-    d_ri_map = alloc<int>(rows);
-    d_ri_cidx = alloc<int>(std::max<size_t>(cidx.size(), 1));
-    d_ri_cval = alloc<double2>(std::max<size_t>(cval.size(), 1));
-    d_ri_caic = alloc<double2>(std::max<size_t>(caic.size(), 1));
-    CU(cudaMemcpyAsync(d_ri_map, map.data(), rows * sizeof(int), cudaMemcpyHostToDevice, stream));
-    if (q > 0) {
-      CU(cudaMemcpyAsync(d_ri_cidx, cidx.data(), cidx.size() * sizeof(int), cudaMemcpyHostToDevice, stream));
-      CU(cudaMemcpyAsync(d_ri_cval, cval.data(), cval.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
-      if (NC > 0)
-        CU(cudaMemcpyAsync(d_ri_caic, caic.data(), caic.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
-    }
+    d_ri_map = alloc<int>((size_t)rows);
+    d_ri_cidx = alloc<int>(std::max<size_t>((size_t)total * E, 1));
+    d_ri_cval = alloc<double2>(std::max<size_t>((size_t)total * E, 1));
+    d_ri_caic = alloc<double2>(std::max<size_t>((size_t)total * NC, 1));
+    launch(FETIGPU_K_OTHER, [&] {
+      k_ri_compact<<<nb, 1024, 0, stream>>>(rows, E, NC, d_ib_idx, d_ib_val, d_Aic, bcount, d_ri_map, d_ri_cidx,
+                                            d_ri_cval, d_ri_caic);
+    });
     sync();
   }
 
@@ -1472,7 +1481,8 @@ struct Ctx {
     }
     launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nown, 256), 256, 0, stream>>>(nown, x + own0, d_zl + own0); });
   }
-  void arnoldi_step(bool in_graph, int u = 0) {
+  static constexpr int kLagSteps = 4;  // sharded cycle: steps per host check of the state
+  void arnoldi_step(bool in_graph, int u = 0, int j_host = -1) {
     const bool split = in_graph && split_givens && tail_rpt > 0;
     double2* h1 = d_red;
     double2* h2 = d_red + (vcap + 2);
@@ -1549,7 +1559,7 @@ struct Ctx {
       t.hcap = vcap + 2;
       t.vcap = vcap;
       launch(FETIGPU_K_ORTHO, [&] {
-        kx_coop(k_arnoldi_tail<kTailThreads, 4, 1>, tail_grid, kTailThreads, tail_smem(), t);
+        kx_coop(k_arnoldi_tail<kTailThreads, 4, kTailMinBlocks>, tail_grid, kTailThreads, tail_smem(), t);
       });
       if (split && u == body_unroll - 1)  // the body's last Givens drives the WHILE condition
         launch(FETIGPU_K_ORTHO, [&] { kx(k_givens_step, 1, 32, 0, t.ga); });
@@ -1570,7 +1580,7 @@ struct Ctx {
     c.w = d_w + own0;
     c.part = d_part;
     c.counter = d_counter;
-    const int nv = dist() ? h_gst->j + 1 : 0;  // sharded path is eager: j known on the host
+    const int nv = dist() ? j_host + 1 : 0;  // sharded path: the host's step index
     // pass 1: w = F z (dual tail gathered per chunk), h1 = V^H w, |w|^2
     c.mode = 0;
     c.out = h1;
@@ -1771,12 +1781,27 @@ struct Ctx {
             return st;
           }
         }
+      } else if (dist()) {
+        // sharded (host-driven) cycle without a host round trip per step: the host knows the
+        // step index j of every launch (the cycle advances one column per step while it
+        // continues), launches kLagSteps steps, then reads the state once.  Steps launched
+        // past the end of the cycle are no-ops on the state (every kernel returns when
+        // cont == 0; the collectives still run, identically on every rank, so the ranks
+        // stay matched).
+        int jh = h_gst->j;
+        do {
+          for (int q = 0; q < kLagSteps && jh + 1 < vcap; ++q, ++jh) {
+            arnoldi_step(false, 0, jh);
+            ghost_refresh(d_V + (size_t)(jh + 1) * ldv);  // next basis column's ghost rows
+          }
+          CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
+          sync();
+        } while (h_gst->cont && jh + 1 < vcap);
       } else {
         do {
           arnoldi_step(false);
           CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
           sync();
-          if (h_gst->cont) ghost_refresh(d_V + (size_t)h_gst->j * ldv);  // sharded: next basis column
         } while (h_gst->cont);
       }
       phase("cycle");
@@ -2138,6 +2163,16 @@ int fetigpu_problem_info(const fetigpu_desc* desc, int* info) {
     if (desc->s_x == 0 && desc->s_y == 0) return;  // mesh-only query
     HostPartition H = build_partition(P, desc->s_x, desc->s_y);
     const int v[10] = {P.n(), P.m(), H.n_sub, H.n_corner, H.n_lambda, H.n_edges, H.ex, H.ey, P.dpn, H.W};
+    std::copy(v, v + 10, info);
+  });
+}
+
+int fetigpu_context_info(const fetigpu_ctx* ctx, int* info) {
+  return guard([&] {
+    if (!ctx) throw ContractError("fetigpu: null context");
+    const Ctx& c = *ctx->c;
+    if (c.dist()) throw ContractError("fetigpu_context_info: sharded context (use fetigpu_problem_info)");
+    const int v[10] = {c.P.n(), c.P.m(), c.H.n_sub, c.H.n_corner, c.H.n_lambda, c.H.n_edges, c.H.ex, c.H.ey, c.P.dpn, c.H.W};
     std::copy(v, v + 10, info);
   });
 }

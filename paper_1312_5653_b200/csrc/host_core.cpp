@@ -2,6 +2,7 @@
 #include "host_core.hpp"
 
 #include <algorithm>
+#include <cstdint>
 #include <cmath>
 #include <random>
 
@@ -366,9 +367,29 @@ HostPartition build_partition(const HostProblem& P, int sx, int sy, bool augment
 
   // band half-width of A_ii (natural order) and the ELL widths, from element adjacency
   const int enl = 4;
+  // per-row distinct-neighbour lists in flat scratch (at most 9 node neighbours x dpn),
+  // reused across subdomains (no per-row allocations)
+  const int KN = 9 * dpn;
+  std::vector<int> bi_buf((size_t)H.NB * KN), ib_buf((size_t)H.NI * KN), bi_cnt(H.NB), ib_cnt(H.NI);
+  auto add_unique = [KN](int* row, int& cnt, int v) {
+    for (int k = 0; k < cnt; ++k)
+      if (row[k] == v) return;
+    if (cnt < KN) row[cnt++] = v;
+  };
+  // the widths depend on the local dof layout only: subdomains with an identical layout
+  // (all interior ones, the edge classes, ...) are scanned once
+  std::vector<std::pair<uint64_t, int>> seen;  // (hash of the layout, subdomain)
   for (int s = 0; s < S; ++s) {
     const int* code = &H.ldof[(size_t)s * H.nld];
-    std::vector<std::vector<int>> bi(H.n_b[s]), ib(H.n_i[s]);
+    uint64_t hsh = 1469598103934665603ull;
+    for (int k = 0; k < H.nld; ++k) hsh = (hsh ^ (uint64_t)(uint32_t)code[k]) * 1099511628211ull;
+    bool dup = false;
+    for (const auto& [h2, s2] : seen)
+      if (h2 == hsh && std::equal(code, code + H.nld, &H.ldof[(size_t)s2 * H.nld])) dup = true;
+    if (dup) continue;
+    seen.push_back({hsh, s});
+    std::fill(bi_cnt.begin(), bi_cnt.begin() + H.n_b[s], 0);
+    std::fill(ib_cnt.begin(), ib_cnt.begin() + H.n_i[s], 0);
     for (int ey_ = 0; ey_ < ey; ++ey_)
       for (int ex_ = 0; ex_ < ex; ++ex_) {
         const int ln[enl] = {ey_ * (ex + 1) + ex_, ey_ * (ex + 1) + ex_ + 1, (ey_ + 1) * (ex + 1) + ex_ + 1,
@@ -381,19 +402,15 @@ HostPartition build_partition(const HostProblem& P, int sx, int sy, bool augment
                 const int B = code[ln[b] * dpn + cb];
                 if (ldof_cat(A) == CAT_INTERIOR && ldof_cat(B) == CAT_INTERIOR)
                   H.W = std::max(H.W, std::abs(ldof_idx(A) - ldof_idx(B)));
-                if (ldof_cat(A) == CAT_BOUNDARY && ldof_cat(B) == CAT_INTERIOR) {
-                  auto& v = bi[ldof_idx(A)];
-                  if (std::find(v.begin(), v.end(), ldof_idx(B)) == v.end()) v.push_back(ldof_idx(B));
-                }
-                if (ldof_cat(A) == CAT_INTERIOR && ldof_cat(B) == CAT_BOUNDARY) {
-                  auto& v = ib[ldof_idx(A)];
-                  if (std::find(v.begin(), v.end(), ldof_idx(B)) == v.end()) v.push_back(ldof_idx(B));
-                }
+                if (ldof_cat(A) == CAT_BOUNDARY && ldof_cat(B) == CAT_INTERIOR)
+                  add_unique(&bi_buf[(size_t)ldof_idx(A) * KN], bi_cnt[ldof_idx(A)], ldof_idx(B));
+                if (ldof_cat(A) == CAT_INTERIOR && ldof_cat(B) == CAT_BOUNDARY)
+                  add_unique(&ib_buf[(size_t)ldof_idx(A) * KN], ib_cnt[ldof_idx(A)], ldof_idx(B));
               }
           }
       }
-    for (auto& v : bi) H.MAXE_BI = std::max(H.MAXE_BI, (int)v.size());
-    for (auto& v : ib) H.MAXE_IB = std::max(H.MAXE_IB, (int)v.size());
+    for (int k = 0; k < H.n_b[s]; ++k) H.MAXE_BI = std::max(H.MAXE_BI, bi_cnt[k]);
+    for (int k = 0; k < H.n_i[s]; ++k) H.MAXE_IB = std::max(H.MAXE_IB, ib_cnt[k]);
   }
   H.MAXE_BI = std::max(H.MAXE_BI, 1);
   H.MAXE_IB = std::max(H.MAXE_IB, 1);

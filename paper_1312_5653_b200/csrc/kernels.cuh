@@ -1070,6 +1070,90 @@ __global__ void k_compact_aic(SubLayout L, int AE, const double2* __restrict__ A
   }
 }
 
+// Compact table of the coupled interior rows (an A_ib entry or a nonzero A_ic entry), built
+// on the device in three passes with a fixed order (ascending row): per-1024-row block
+// counts, one block scanning the counts, then the per-block local scan + row copy.
+__device__ __forceinline__ bool ri_coupled(size_t g, int E, int NC, const int* __restrict__ idx,
+                                           const double2* __restrict__ aic) {
+  bool any = false;
+  for (int e = 0; e < E; ++e) any = any || idx[g * E + e] >= 0;
+  for (int c = 0; c < NC; ++c) any = any || aic[g * NC + c].x != 0.0 || aic[g * NC + c].y != 0.0;
+  return any;
+}
+__global__ void __launch_bounds__(1024) k_ri_count(long long rows, int E, int NC, const int* __restrict__ idx,
+                                                   const double2* __restrict__ aic, int* __restrict__ bcount) {
+  __shared__ int wsum[32];
+  const long long g = (long long)blockIdx.x * 1024 + threadIdx.x;
+  const int f = g < rows && ri_coupled((size_t)g, E, NC, idx, aic) ? 1 : 0;
+  const int c = __popc(__ballot_sync(0xffffffffu, f));
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int v = wsum[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) bcount[blockIdx.x] = v;
+  }
+}
+// exclusive scan of nb block counts (one block, sequential over chunks of 1024); total at [nb]
+__global__ void __launch_bounds__(1024) k_ri_scan(int nb, int* __restrict__ bcount) {
+  __shared__ int sh[1024];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < nb ? bcount[i] : 0;
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
+      const int t = threadIdx.x >= o ? sh[threadIdx.x - o] : 0;
+      __syncthreads();
+      sh[threadIdx.x] += t;
+      __syncthreads();
+    }
+    if (i < nb) bcount[i] = carry + sh[threadIdx.x] - v;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry += sh[1023];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bcount[nb] = carry;
+}
+__global__ void __launch_bounds__(1024) k_ri_compact(long long rows, int E, int NC, const int* __restrict__ idx,
+                                                     const double2* __restrict__ val, const double2* __restrict__ aic,
+                                                     const int* __restrict__ boff, int* __restrict__ map,
+                                                     int* __restrict__ cidx, double2* __restrict__ cval,
+                                                     double2* __restrict__ caic) {
+  __shared__ int wsum[32];
+  const long long g = (long long)blockIdx.x * 1024 + threadIdx.x;
+  const int f = g < rows && ri_coupled((size_t)g, E, NC, idx, aic) ? 1 : 0;
+  const unsigned bal = __ballot_sync(0xffffffffu, f);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) wsum[warp] = __popc(bal);
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the 32 warp counts
+    const int v = wsum[lane];
+    int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    wsum[lane] = x - v;
+  }
+  __syncthreads();
+  if (g >= rows) return;
+  if (!f) {
+    map[g] = -1;
+    return;
+  }
+  const int q = boff[blockIdx.x] + wsum[warp] + __popc(bal & ((1u << lane) - 1u));
+  map[g] = q;
+  for (int e = 0; e < E; ++e) {
+    cidx[(size_t)q * E + e] = idx[(size_t)g * E + e];
+    cval[(size_t)q * E + e] = val[(size_t)g * E + e];
+  }
+  for (int c = 0; c < NC; ++c) caic[(size_t)q * NC + c] = aic[(size_t)g * NC + c];
+}
+
 __global__ void k_gcp_full(SubLayout L, const double2* __restrict__ cpl_i, const double2* __restrict__ cpl_b,
                            const double2* __restrict__ ti, const double2* __restrict__ tb, double2* __restrict__ gcp) {
   __shared__ double2 red[8][32];
@@ -1359,6 +1443,7 @@ __device__ void givens_warp(const GivensArgs& a, double* sc, double2* ss, double
 __global__ void __launch_bounds__(32) k_givens(GivensArgs a) {
   __shared__ double sc[256];
   __shared__ double2 ss[256], sh[256];
+  if (a.st->cont == 0) return;  // a step launched past the end of the cycle (sharded loop)
   givens_warp(a, sc, ss, sh);
 }
 // split-Givens graph path: the Givens step of the last step of an unrolled body, skipped

@@ -287,6 +287,7 @@ def test_gpu3d_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
     assert rel(x, xr) <= 1e-8
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("switch", ["FETIGPU3D_NO_FDM", "FETIGPU_NO_STENCIL"])
 def test_gpu3d_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
     """3D heat: the separable interior solve (FETIGPU3D_NO_FDM keeps the block-band
