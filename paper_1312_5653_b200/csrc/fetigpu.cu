@@ -423,6 +423,18 @@ struct Ctx {
       band_solve(d_colband, d_rowband, Wt, H.n_sub, H.NI, X, H.NI, H.NI, 1);
     }
   }
+  // X = A_ii^-1 X for nrhs right-hand sides per subdomain, X [S][nrhs][NI]
+  void interior_solves(double2* X, int nrhs) {
+    if (nrhs <= 0) return;
+    if (use_fdm) {  // every vector is its own CTA: the interiors are all the same grid
+      launch(FETIGPU_K_OTHER, [&] {
+        k_fdm_solve<<<H.n_sub * nrhs, 256, 0, stream>>>(X, (size_t)H.NI, fdm_mx, fdm_my, d_fdm_sx, d_fdm_sy,
+                                                        d_fdm_invd);
+      });
+    } else {
+      band_solve(d_colband, d_rowband, Wt, H.n_sub, H.NI, X, (size_t)nrhs * H.NI, H.NI, nrhs);
+    }
+  }
   static constexpr int kBtStages = 2;
   // Separable interior solve (k_fdm_solve): heat on the structured mesh, every subdomain
   // interior the same mx x my grid in x-fastest order and the element matrices exactly the
@@ -805,15 +817,19 @@ struct Ctx {
     }
 
     smark("assemble");
-    // K2': block-Thomas factors for the per-solve interior solves (reads the band of A_ii,
-    // so it runs before the in-place band factorization)
-    setup_block_thomas();
-    smark("bt_factor");
-    // K2: batched band LDL^T of A_ii (setup multi-RHS solves; per-solve path if W > 32)
-    band_ldlt(d_colband, d_rowband, Wt, S, NI, d_status);
-    check_status(S, "interior block A_ii");
-
-    smark("band_ldlt");
+    // separable interior solve (heat on the structured mesh): it also serves the setup's
+    // multi-right-hand-side solves below, so no banded factorization of A_ii is needed
+    setup_fdm();
+    if (!use_fdm) {
+      // K2': block-Thomas factors for the per-solve interior solves (reads the band of
+      // A_ii, so it runs before the in-place band factorization)
+      setup_block_thomas();
+      smark("bt_factor");
+      // K2: batched band LDL^T of A_ii (setup multi-RHS solves; per-solve path if W > 32)
+      band_ldlt(d_colband, d_rowband, Wt, S, NI, d_status);
+      check_status(S, "interior block A_ii");
+    }
+    smark("factor");
     // S_bb = A_bb - A_bi A_ii^-1 A_ib  (NB right-hand sides per subdomain)
     {
       double2* Y = alloc<double2>((size_t)S * NB * NI);
@@ -822,21 +838,30 @@ struct Ctx {
       launch(FETIGPU_K_OTHER, [&] {
         k_build_aib_rhs<<<cdiv((long long)S * NB * H.MAXE_BI, 256), 256, 0, stream>>>(L, d_bi_idx, d_bi_val, Y);
       });
-      band_solve(d_colband, d_rowband, Wt, S, NI, Y, (size_t)NB * NI, NI, NB);
+      interior_solves(Y, NB);
       launch(FETIGPU_K_OTHER, [&] {
         k_schur_bb<<<cdiv((long long)S * NB * NB, 256), 256, 0, stream>>>(L, d_bi_idx, d_bi_val, Y, d_Sbb);
       });
-      // S_bb^-1 by in-place Gauss-Jordan on a copy
-      CU(cudaMemcpyAsync(d_Sinv, d_Sbb, (size_t)S * NB * NB * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
-      launch(FETIGPU_K_OTHER, [&] {
-        k_gauss_jordan<<<S, 256, 2 * NB * sizeof(double2), stream>>>(d_Sinv, NB, d_status);
-      });
+      // S_bb^-1: symmetric sweep with the packed triangle in shared memory (NB <= 164);
+      // larger blocks (plane strain) by in-place Gauss-Jordan on a copy in global memory
+      const size_t sweep_smem = sizeof(double2) * ((size_t)NB * (NB + 1) / 2 + NB);
+      if (sweep_smem <= 200 * 1024) {
+        CU(cudaFuncSetAttribute(k_sym_sweep_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sweep_smem));
+        launch(FETIGPU_K_OTHER, [&] {
+          k_sym_sweep_inverse<<<S, 256, sweep_smem, stream>>>(d_Sbb, d_Sinv, NB, d_status);
+        });
+      } else {
+        CU(cudaMemcpyAsync(d_Sinv, d_Sbb, (size_t)S * NB * NB * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+        launch(FETIGPU_K_OTHER, [&] {
+          k_gauss_jordan<<<S, 256, 2 * NB * sizeof(double2), stream>>>(d_Sinv, NB, d_status);
+        });
+      }
       check_status(S, "remaining block A_rr");
       // coupling = A_rr^-1 A_rc via the block formula
       launch(FETIGPU_K_OTHER, [&] {
         k_build_aic_rhs<<<cdiv((long long)S * NI * NC, 256), 256, 0, stream>>>(L, d_Aic, Yc);
       });
-      band_solve(d_colband, d_rowband, Wt, S, NI, Yc, (size_t)NC * NI, NI, NC);
+      interior_solves(Yc, NC);
       launch(FETIGPU_K_OTHER, [&] {
         k_coupling_b<<<S, 256, NB * NC * sizeof(double2), stream>>>(L, d_Sinv, d_Abc, d_bi_idx, d_bi_val, Yc,
                                                                     d_cpl_b);
@@ -996,8 +1021,6 @@ struct Ctx {
     smark("mass+stencil");
     setup_ri_compact();
     smark("ri_compact");
-    setup_fdm();
-    smark("fdm");
     setup_l2_persistence();
     smark("l2_window");
     sync();

@@ -213,6 +213,61 @@ __global__ void __launch_bounds__(256) k_gauss_jordan(double2* __restrict__ A, i
   if (tid == 0) status[s] = bad;
 }
 
+// S_bb^-1 of every subdomain by the symmetric sweep operator, the whole packed lower
+// triangle resident in shared memory (n(n+1)/2 complex: 124 KB at n = 124).  S_bb is
+// complex symmetric (A = A^T; real part SPD), so Gauss-Jordan without pivoting keeps the
+// symmetric form when row and column k are both scaled by 1/d:
+//   d = a_kk;  a_ij -= a_ik a_kj / d (i, j != k);  a_ik = a_ik / d;  a_kk = -1/d
+// and sweeping every k yields -A^-1 (Goodnight 1979).  Reads S (dense [S][n][n]), writes the
+// dense symmetric inverse; status[s] = 1-based index of a zero / non-finite pivot.
+__global__ void __launch_bounds__(256) k_sym_sweep_inverse(const double2* __restrict__ S, double2* __restrict__ Sinv,
+                                                           int n, int* __restrict__ status) {
+  extern __shared__ double2 sw_sh[];
+  double2* a = sw_sh;                               // packed lower: (i, j <= i) at i(i+1)/2 + j
+  double2* col = sw_sh + (size_t)n * (n + 1) / 2;   // column k of the current step
+  __shared__ double2 dinv_sh;
+  const int s = blockIdx.x, tid = threadIdx.x;
+  const int tx = tid & 31, ty = tid >> 5;           // 8 row groups x 32 columns
+  const double2* M = S + (size_t)s * n * n;
+  for (int i = ty; i < n; i += 8)
+    for (int j = tx; j <= i; j += 32) a[i * (i + 1) / 2 + j] = M[(size_t)i * n + j];
+  int bad = 0;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    for (int i = tid; i < n; i += 256) col[i] = i >= k ? a[i * (i + 1) / 2 + k] : a[k * (k + 1) / 2 + i];
+    __syncthreads();
+    const double2 d = col[k];
+    if (tid == 0) {
+      const double a2 = cabs2(d);
+      if (bad == 0 && (!(a2 > 0.0) || !isfinite(a2))) bad = k + 1;
+      dinv_sh = crecip(d);
+    }
+    __syncthreads();
+    const double2 dinv = dinv_sh;
+    for (int i = ty; i < n; i += 8) {
+      const double2 ci = col[i];
+      const double2 cid = cmul(ci, dinv);
+      for (int j = tx; j <= i; j += 32) {
+        double2& e = a[i * (i + 1) / 2 + j];
+        if (i == k && j == k) e = make_double2(-dinv.x, -dinv.y);
+        else if (i == k) e = cmul(col[j], dinv);
+        else if (j == k) e = cid;
+        else e = cfms(cid, col[j], e);
+      }
+    }
+    __syncthreads();
+  }
+  double2* O = Sinv + (size_t)s * n * n;  // A^-1 = -(swept matrix)
+  for (int i = ty; i < n; i += 8)
+    for (int j = tx; j <= i; j += 32) {
+      const double2 v = a[i * (i + 1) / 2 + j];
+      const double2 m = make_double2(-v.x, -v.y);
+      O[(size_t)i * n + j] = m;
+      O[(size_t)j * n + i] = m;
+    }
+  if (tid == 0) status[s] = bad;
+}
+
 // coupling_b = S_bb^-1 (A_bc - A_bi Yc),  Yc = A_ii^-1 A_ic.  One CTA per subdomain.
 __global__ void k_coupling_b(SubLayout L, const double2* __restrict__ Sinv, const double2* __restrict__ Abc,
                              const int* __restrict__ bi_idx, const double2* __restrict__ bi_val,
