@@ -1,4 +1,4 @@
-# A/B of a build-time define: bench with the default build, then with $1 (e.g.
+# A/B of a build-time define (e.g. a launch-bounds experiment): bench with the default build, then with $1 (e.g.
 # "-DFETIGPU_TAIL_MINB=2"), then restore the default build.  Usage: bash tools/gpu_ab_build.sh "<defines>" <tag>
 mkdir -p gpurun_out
 python -c "from paper_1312_5653_b200 import build; build.build(force=True)"
