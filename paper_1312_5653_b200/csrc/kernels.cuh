@@ -1919,8 +1919,17 @@ __device__ __forceinline__ void block_reduce_parts(const double2* __restrict__ p
     double2 t = cz();
     if (i < nout) {
       const double2* pp = part + (size_t)i * G;
+      constexpr int QB = 10;  // G <= 160 (one block per SM): all of a thread's loads in one batch
+      if (G <= SEGS * QB) {
+        double2 v[QB];
+#pragma unroll
+        for (int q = 0; q < QB; ++q) v[q] = (seg + SEGS * q < G) ? __ldcg(pp + seg + SEGS * q) : cz();
+#pragma unroll
+        for (int q = 0; q < QB; ++q) t = cadd(t, v[q]);
+      } else {
 #pragma unroll 8
-      for (int bb = seg; bb < G; bb += SEGS) t = cadd(t, __ldcg(pp + bb));
+        for (int bb = seg; bb < G; bb += SEGS) t = cadd(t, __ldcg(pp + bb));
+      }
     }
 #pragma unroll
     for (int m = SEGS / 2; m > 0; m >>= 1) t = cadd(t, shfl_xor2(t, m));
