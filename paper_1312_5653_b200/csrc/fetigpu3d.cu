@@ -720,6 +720,10 @@ struct Ctx3 {
   // interior solves: the TMA-streamed kernel (default), or the direct-load one
   // (FETIGPU3D_SOLVE=direct: one warp per off-diagonal block, 8 warps up to P = 8, else 32)
   int solve_kind = -1;
+  // interior substitution ring: 12 slots of 16 KB (196 KB in flight per CTA), 6 consumer
+  // warps with 2 slots each (config 5, 4 interior solves per Schur solve: 8 slots / 8 warps
+  // 22.5 ms, 12 / 4 24.4, 12 / 3 29.9, 12 / 6 20.6)
+  static constexpr int kBbsStages = 12, kBbsWarps = 6;
   // separable interior solve (k3_fdm_solve) for heat: FETIGPU3D_NO_FDM=1 disables it
   bool use_fdm = false;
   int fdm_m[3] = {0, 0, 0};
@@ -779,12 +783,13 @@ struct Ctx3 {
       return;
     }
     if (solve_kind < 0) {
-      CU3(cudaFuncSetAttribute(k3::k3_bb_solve_tma<8, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)k3::bb_solve_tma_smem<8, 8>()));
+      CU3(cudaFuncSetAttribute(k3::k3_bb_solve_tma<kBbsStages, kBbsWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)k3::bb_solve_tma_smem<kBbsStages, kBbsWarps>()));
       solve_kind = 1;
     }
     launch(FETIGPU_K_BAND, [&] {
-      k3::k3_bb_solve_tma<8, 8><<<S, 288, k3::bb_solve_tma_smem<8, 8>(), stream>>>(NBK, PB, d_bb, NI, x);
+      k3::k3_bb_solve_tma<kBbsStages, kBbsWarps><<<S, (kBbsWarps + 1) * 32, k3::bb_solve_tma_smem<kBbsStages, kBbsWarps>(), stream>>>(
+          NBK, PB, d_bb, NI, x);
     });
   }
   // (|x|^2, max|x|) -> host
