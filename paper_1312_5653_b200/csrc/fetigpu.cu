@@ -116,6 +116,8 @@ struct Ctx {
   double2 *d_Sbb = nullptr, *d_Sinv = nullptr, *d_Aic = nullptr, *d_Abc = nullptr, *d_Acc = nullptr;
   double2 *d_cpl_i = nullptr, *d_cpl_b = nullptr;
   double2 *d_Cinv = nullptr;
+  int* d_crows = nullptr;  // sharded: the corners whose C^-1 rows this rank keeps (d_Cinv: n_crows x nc)
+  int n_crows = 0;
   double2 *d_Sbb_p = nullptr, *d_Sinv_p = nullptr;  // packed symmetric tiles (k_sym_gemv)
   int NT = 0;
   // workspaces
@@ -913,14 +915,42 @@ struct Ctx {
           for (int i = 0; i < nc; ++i)
             if (!(dabs[i] > umax * 1e-13)) throw NumericalError("feti: coarse problem is singular");
         }
-        d_Cinv = alloc<double2>((size_t)nc * nc);
-        launch(FETIGPU_K_OTHER, [&] { k_identity<<<cdiv((long long)nc * nc, 256), 256, 0, stream>>>(nc, d_Cinv); });
-        band_solve(cband, crow, WCt, 1, nc, d_Cinv, (size_t)nc * nc, nc, nc);
-        launch(FETIGPU_K_OTHER, [&] {
-          k_scale_inverse<<<cdiv((long long)nc * nc, 256), 256, 0, stream>>>(nc, d_Cinv, cscale_d);
-        });
+        // sharded: only the rows of C^-1 at the corners of this rank's subdomains and their
+        // phantom neighbours (the only z entries it reads).  C^-1 is complex symmetric, so
+        // row c is the column C^-1 e_c: solve for those columns alone -- per-step coarse
+        // bytes and setup shrink ~world-fold instead of every rank applying the whole inverse
+        std::vector<int> rows;
+        if (dist() && !std::getenv("FETIGPU_FULL_COARSE")) {
+          std::vector<char> seen(nc, 0);
+          for (int c : H.cglob)
+            if (c >= 0) seen[c] = 1;
+          for (int c = 0; c < nc; ++c)
+            if (seen[c]) rows.push_back(c);
+          if ((int)rows.size() == nc) rows.clear();
+        }
+        if (rows.empty()) {
+          d_Cinv = alloc<double2>((size_t)nc * nc);
+          launch(FETIGPU_K_OTHER, [&] { k_identity<<<cdiv((long long)nc * nc, 256), 256, 0, stream>>>(nc, d_Cinv); });
+          band_solve(cband, crow, WCt, 1, nc, d_Cinv, (size_t)nc * nc, nc, nc);
+          launch(FETIGPU_K_OTHER, [&] {
+            k_scale_inverse<<<cdiv((long long)nc * nc, 256), 256, 0, stream>>>(nc, d_Cinv, cscale_d);
+          });
+        } else {
+          n_crows = (int)rows.size();
+          d_crows = upload(rows);
+          const long long cnt = (long long)n_crows * nc;
+          d_Cinv = alloc<double2>((size_t)cnt);
+          zero(d_Cinv, (size_t)cnt);
+          launch(FETIGPU_K_OTHER, [&] {
+            k_select_identity<<<cdiv(n_crows, 256), 256, 0, stream>>>(n_crows, nc, d_crows, d_Cinv);
+          });
+          band_solve(cband, crow, WCt, 1, nc, d_Cinv, (size_t)cnt, nc, n_crows);
+          launch(FETIGPU_K_OTHER, [&] {
+            k_scale_inverse_rows<<<cdiv(cnt, 256), 256, 0, stream>>>(n_crows, nc, d_crows, d_Cinv, cscale_d);
+          });
+        }
       }
-      setup_big_coarse();
+      if (d_crows == nullptr) setup_big_coarse();
     smark("sbb+coarse");
       // packed symmetric storage of S_bb and S_bb^-1 for the per-iteration GEMVs
       NT = (NB + 31) / 32;
@@ -1036,7 +1066,7 @@ struct Ctx {
     CU(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, desc.device));
     CU(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, desc.device));
     if (max_persist <= 0 || max_window <= 0) return;
-    const size_t bytes = (size_t)nc * nc * sizeof(double2);
+    const size_t bytes = (size_t)(d_crows ? n_crows : nc) * nc * sizeof(double2);
     const size_t carve = std::min<size_t>(bytes, (size_t)max_persist);
     CU(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve));
     cudaStreamAttrValue attr{};
@@ -1313,7 +1343,8 @@ struct Ctx {
       return;
     }
     launch(FETIGPU_K_COARSE, [&] {
-      kx(k_coarse_gemv<256>, nc, 256, 0, nc, (const double2*)d_Cinv, (const double2*)d_g, d_z);
+      kx(k_coarse_gemv<256>, d_crows ? n_crows : nc, 256, 0, nc, (const double2*)d_Cinv, (const double2*)d_g, d_z,
+         (const int*)d_crows);
     });
   }
   // u_b = u1_b - cpl_b z gathered onto the owned multiplier rows: out = -B u  (feti.cpp:593)

@@ -514,6 +514,18 @@ __global__ void k_scale_inverse(int n, double2* __restrict__ X, const double* __
   if (gid >= (long long)n * n) return;
   X[gid] = cscale(X[gid], scale[gid / n] * scale[gid % n]);
 }
+// selected columns of the identity (X[r n + rows[r]] = 1, X zeroed) and the matching
+// rescale X[r][j] *= scale[rows[r]] scale[j]: rows `rows` of the equilibrated C^-1
+__global__ void k_select_identity(int nr, int n, const int* __restrict__ rows, double2* __restrict__ X) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < nr) X[(size_t)r * n + rows[r]] = make_double2(1.0, 0.0);
+}
+__global__ void k_scale_inverse_rows(int nr, int n, const int* __restrict__ rows, double2* __restrict__ X,
+                                     const double* __restrict__ scale) {
+  const long long gid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long long)nr * n) return;
+  X[gid] = cscale(X[gid], scale[rows[gid / n]] * scale[gid % n]);
+}
 
 // --------------------------------------------------------------- per-iteration kernels
 // K5/K6 local operator apply, one CTA per subdomain:
@@ -898,13 +910,16 @@ __global__ void k_coarse_rhs(int nc, const int* __restrict__ corner_slots, const
   g[c] = acc;
 }
 
-// z = C^-1 g  (dense explicit coarse inverse, K4), one row per block of THREADS threads:
+// z = C^-1 g  (dense explicit coarse inverse, K4), one row per block of THREADS threads
+// (rows != nullptr, sharded: Cinv holds only the rows C^-1[rows[b], :] and z is written at
+// rows[b]):
 // each thread takes a strided set of columns (a few loads, all independent), then a block
 // reduction in fixed order.  Latency-bound kernel (C^-1 stays in L2), so the parallelism
 // comes from the number of warps, not from per-thread batching (ptxas serialises those).
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS)
-    k_coarse_gemv(int nc, const double2* __restrict__ Cinv, const double2* __restrict__ g, double2* __restrict__ z) {
+    k_coarse_gemv(int nc, const double2* __restrict__ Cinv, const double2* __restrict__ g, double2* __restrict__ z,
+                  const int* __restrict__ rows = nullptr) {
   constexpr int WARPS = THREADS / 32;
   __shared__ double2 red[WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -921,7 +936,7 @@ __global__ void __launch_bounds__(THREADS)
     double2 t = red[0];
 #pragma unroll
     for (int q = 1; q < WARPS; ++q) t = cadd(t, red[q]);
-    z[row] = t;
+    z[rows != nullptr ? rows[row] : row] = t;
   }
 }
 

@@ -158,6 +158,21 @@ def test_emulated_sharded_solve_matches_single_gpu(fetigpu, case):
 
 
 @pytest.mark.gpu
+def test_emulated_sharded_full_coarse_inverse(fetigpu, monkeypatch):
+    """Each rank keeps only the C^-1 rows of the corners its subdomains (and phantom
+    neighbours) touch; FETIGPU_FULL_COARSE=1 keeps the whole inverse on every rank.  Same
+    iterations, results equal to rounding."""
+    p = _problem(fetigpu, 256, 256, 0)
+    a = fetigpu.emulated_schur_solve(p, 4, 8, 8, tol=1e-10, max_iter=1000)
+    monkeypatch.setenv("FETIGPU_FULL_COARSE", "1")
+    b = fetigpu.emulated_schur_solve(p, 4, 8, 8, tol=1e-10, max_iter=1000)
+    for side in ("plus_stats", "minus_stats"):
+        assert a[side]["iterations"] == b[side]["iterations"]
+    for k in ("y", "u", "lambda"):
+        assert rel(a[k], b[k]) <= 1e-11, k
+
+
+@pytest.mark.gpu
 def test_nccl_plumbing_one_rank(fetigpu):
     """The NCCL communicator of the sharded paths initialises and runs its collectives on
     the box (one rank: the results equal the inputs).  Multi-rank NCCL needs several GPUs."""
