@@ -175,6 +175,12 @@ struct Ctx {
   static constexpr int kCgsThreads = 512, kCgsRows = 256;  // k_cgs_pass block shape
   // fused Arnoldi tail (k_arnoldi_tail): rows per thread (0 = off), grid, barrier words
   int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_rows = 512;
+  // coarse solve beside the dual GEMV (k_sym_gemv_aside): coarse groups of 4 CTAs per launch (0 = off)
+  int aside_nx = 0;
+  bool aside_giveup = false;  // test hook FETIGPU_ASIDE_GIVEUP: the coarse CTAs never see their arrivals
+  unsigned int* d_aside_ctr = nullptr;
+  double2* d_zpart = nullptr;  // [nc][aside_nx] partial coarse solutions
+  int* d_blk_corners = nullptr;  // [tail_grid][kTailCorners]
   static constexpr int kBodyUnroll = 4;  // steps per WHILE-body execution (measured at config 2: 4 205.6, 8 204.9, 12 203.1 solves/s; earlier code 4: 182.8, 8: 183.5)
   int body_unroll = 1;
   unsigned int* d_bar = nullptr;
@@ -571,7 +577,7 @@ struct Ctx {
   // measured 152 vs 203 solves/s (spills, and the tail's CTAs packed two per SM).
   static constexpr int kTailMinBlocks = 1;
   size_t tail_smem() const {
-    return sizeof(double2) * ((size_t)kTailThreads + 3 * (size_t)(vcap_hint() + 2) + 640);
+    return sizeof(double2) * ((size_t)kTailThreads + 3 * (size_t)(vcap_hint() + 2) + 640 + (size_t)std::max(nc, 0));
   }
   void setup_fused_tail() {
     if (dist() || H.NC > 4 || H.n_aug > 0 || nc > kTailThreads + 2 * (vcap_hint() + 2) ||
@@ -583,8 +589,10 @@ struct Ctx {
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, desc.device));
     CU(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, desc.device));
     if (!coop) return;  // the fused tail needs a cooperative (co-residency checked) launch
-    auto kfn = k_arnoldi_tail<kTailThreads, 4, kTailMinBlocks>;
+    auto kfn = k_arnoldi_tail<kTailThreads, 4, kTailMinBlocks, false>;
     CU(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CU(cudaFuncSetAttribute(k_arnoldi_tail<kTailThreads, 4, kTailMinBlocks, true>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTailThreads, smem));
     // rows per block: spread the rows over every SM (multiple of 32, at most one per thread)
     tail_rows = std::min(kTailThreads, 32 * cdiv(cdiv(std::max(nown, 1), sms), 32));
@@ -597,10 +605,42 @@ struct Ctx {
     tail_rb = rows <= 1 ? 1 : rows <= 2 ? 2 : rows <= 4 ? 4 : rows <= 8 ? 8 : 16;
     d_bar = alloc<unsigned int>(2);
     CU(cudaMemsetAsync(d_bar, 0, 2 * sizeof(unsigned int), stream));
+    setup_coarse_aside(sms);
     if (std::getenv("FETIGPU_TAIL_TIMES")) {
       d_tstamp = alloc<unsigned long long>((size_t)16 * (vcap_hint() + 2));
       CU(cudaMemsetAsync(d_tstamp, 0, (size_t)16 * (vcap_hint() + 2) * sizeof(unsigned long long), stream));
     }
+  }
+  // The Arnoldi step's coarse solve z = C^-1 g runs in extra CTAs of the dual GEMV's launch
+  // when the whole launch (n_sub GEMV CTAs + nx coarse CTAs) is resident in one wave, the
+  // interface fits four tiles and g fits the CTA's shared memory at full occupancy.
+  void setup_coarse_aside(int sms) {
+    if (nc <= 0 || NT > 4 || H.NC > 4 || std::getenv("FETIGPU_NO_ASIDE")) return;
+    auto kfn = k_sym_gemv_aside<8, 4>;
+    int per_sm = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, 128, sym_smem()));
+    // coarse CTAs: groups of four, at most one CTA per SM and 40 groups (the tail's batch)
+    const int ng = std::min({(per_sm * sms - H.n_sub) / 4, sms / 4, 40});
+    if (ng < 8 || cdiv(nc, ng) > kAsideCpgMax) return;
+    // the corners each tail block's multiplier rows touch (both owners' subdomains)
+    std::vector<int> bc((size_t)tail_grid * kTailCorners, -1);
+    for (int b = 0; b < tail_grid; ++b) {
+      std::vector<int> seen;
+      for (int r = b * tail_rows; r < std::min(nown, (b + 1) * tail_rows); ++r)
+        for (int slot : {H.lam_lo[r], H.lam_hi[r]})
+          for (int c = 0; c < H.NC; ++c) {
+            const int cg = H.cglob[(size_t)(slot / H.NB) * H.NC + c];
+            if (cg >= 0 && std::find(seen.begin(), seen.end(), cg) == seen.end()) seen.push_back(cg);
+          }
+      if ((int)seen.size() > kTailCorners) return;
+      std::copy(seen.begin(), seen.end(), bc.begin() + (size_t)b * kTailCorners);
+    }
+    d_blk_corners = upload(bc);
+    aside_nx = ng;  // coarse groups; 4 CTAs each
+    aside_giveup = std::getenv("FETIGPU_ASIDE_GIVEUP") != nullptr;
+    d_zpart = alloc<double2>((size_t)nc * aside_nx);
+    d_aside_ctr = alloc<unsigned int>(2);
+    CU(cudaMemsetAsync(d_aside_ctr, 0, 2 * sizeof(unsigned int), stream));
   }
   // One real cooperative launch of the tail (n = nc = 0 and a stopped cycle: every block
   // returns right after its prologue).  The runtime rejects it (cudaErrorCooperativeLaunchTooLarge)
@@ -689,6 +729,19 @@ struct Ctx {
       std::fprintf(stderr, " %s %.2f", names[p], acc / cnt / 1e3);
     }
     std::fprintf(stderr, "\n");
+    if (aside_nx > 0) {  // coarse CTA 0 of the dual GEMV launch, relative to the tail's start
+      const char* an[] = {"prewait", "partials", "-", "rows"};
+      std::fprintf(stderr, "[fetigpu] coarse beside the dual GEMV (us, CTA 0):");
+      for (int p = 0; p < 4; ++p) {
+        if (p == 2) continue;
+        double acc = 0;
+        for (int i = 0; i < cnt; ++i) acc += (double)t[(size_t)i * 16 + 11 + p] - (double)t[(size_t)i * 16 + 10 + p];
+        std::fprintf(stderr, " %s %.2f", an[p], acc / cnt / 1e3);
+      }
+      double acc = 0;
+      for (int i = 0; i < cnt; ++i) acc += (double)t[(size_t)i * 16 + 0] - (double)t[(size_t)i * 16 + 14];
+      std::fprintf(stderr, " | end -> tail start %.2f\n", acc / cnt / 1e3);
+    }
   }
   void check_status(int count, const char* what) {
     std::vector<int> st(count);
@@ -1577,7 +1630,18 @@ struct Ctx {
         g.jsel = split ? &d_gst->jcol : &d_gst->j;
         g.jstride = ldv;
       }
-      dual_gemv(g, tail_rpt > 0);
+      if (tail_rpt > 0 && aside_nx > 0) {
+        g.alpha = -1.0;
+        g.out = d_u1b;
+        g.cpl_b = d_cpl_b;
+        g.gcp = d_gcp;
+        const CoarseAsideArgs ca{H.n_sub, aside_nx, nc, aside_giveup ? 1 : 0, d_Cinv, d_corner_slots,
+                                 d_zpart, d_aside_ctr, d_tstamp, &d_gst->iterations};
+        launch(FETIGPU_K_DUAL_GEMV,
+               [&] { kx(k_sym_gemv_aside<8, 4>, H.n_sub + 4 * aside_nx, 128, sym_smem(), g, ca); });
+      } else {
+        dual_gemv(g, tail_rpt > 0);
+      }
     }
     span_on = false;
     in_arnoldi = false;
@@ -1612,8 +1676,16 @@ struct Ctx {
       t.span = d_span;
       t.hcap = vcap + 2;
       t.vcap = vcap;
+      t.aside_ctr = aside_nx > 0 ? d_aside_ctr : nullptr;
+      t.aside_nx = (unsigned int)aside_nx;
+      t.n_gcp = H.n_sub * H.NC;
+      t.zpart = d_zpart;
+      t.blk_corners = d_blk_corners;
       launch(FETIGPU_K_ORTHO, [&] {
-        kx_coop(k_arnoldi_tail<kTailThreads, 4, kTailMinBlocks>, tail_grid, kTailThreads, tail_smem(), t);
+        if (aside_nx > 0)
+          kx_coop(k_arnoldi_tail<kTailThreads, 4, kTailMinBlocks, true>, tail_grid, kTailThreads, tail_smem(), t);
+        else
+          kx_coop(k_arnoldi_tail<kTailThreads, 4, kTailMinBlocks, false>, tail_grid, kTailThreads, tail_smem(), t);
       });
       if (split && u == body_unroll - 1)  // the body's last Givens drives the WHILE condition
         launch(FETIGPU_K_ORTHO, [&] { kx(k_givens_step, 1, 32, 0, t.ga); });
@@ -1732,6 +1804,10 @@ struct Ctx {
         st.converged = 1;
         return st;
       }
+    }
+    if (d_aside_ctr) {  // coarse beside the dual GEMV: done-counter cleared, partials at the sentinel
+      CU(cudaMemsetAsync(d_aside_ctr, 0, 2 * sizeof(unsigned int), stream));
+      CU(cudaMemsetAsync(d_gcp, 0xFF, (size_t)H.n_sub * H.NC * sizeof(double2), stream));
     }
     if (d_span) {
       const int cnt = 6 * (vcap_hint() + 2);

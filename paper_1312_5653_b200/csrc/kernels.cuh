@@ -706,8 +706,39 @@ struct SymGemvArgs {
 
 // The per-subdomain packed symmetric GEMV (one CTA = one subdomain), shared by k_sym_gemv
 // and k_sym_gemv_giv (the preconditioner GEMV with the previous step's Givens folded in).
-template <int MODE, int SYM_BATCH, int WARPS>
-__device__ __forceinline__ void sym_gemv_run(const SymGemvArgs& a) {
+// Solve-constant index operands of the input-vector gather (B^T scatter) of entry
+// k = threadIdx.x, loaded BEFORE griddepcontrol.wait so that only the data-dependent loads
+// (one round trip) remain after it: multiplier row, its sign, and (mode 1) the row's two slots.
+// Used by k_sym_gemv_aside (+0.4 % there; no gain in the plain GEMVs, whose CTAs only become
+// resident when the producer kernel's CTAs exit, and their register budget is full).
+struct SymPre {
+  int r, lo, hi;
+  double sg;
+};
+template <int MODE>
+__device__ __forceinline__ SymPre sym_pre_load(const SymGemvArgs& a, int s) {
+  SymPre p{-1, 0, 0, 0.0};
+  const int k = threadIdx.x;
+  if (MODE != 2 && k < a.NB) {
+    const size_t sb = (size_t)s * a.NB + k;
+    p.r = a.blam[sb];
+    p.sg = a.bsign[sb];
+    if (MODE == 1 && p.r >= 0) {
+      p.lo = a.lam_lo[p.r];
+      p.hi = a.lam_hi[p.r];
+    }
+  }
+  return p;
+}
+// EARLY (dual GEMV of the Arnoldi step with the coarse solve beside it, k_sym_gemv_aside):
+// gcp = cpl_b^T x is formed right after the input vector -- from coupling entries `cp` the
+// warp loaded before griddepcontrol.wait (warp c = local corner c, lane l = rows l + 32 q) --
+// and stored at once (plain stores over the all-ones sentinel the tail left there: the value
+// is its own ready flag, no fence stalls the warp), so the coarse CTAs of the same launch can
+// start while this CTA streams its operator.  Same summation order as the epilogue form.
+template <int MODE, int SYM_BATCH, int WARPS, bool EARLY = false>
+__device__ __forceinline__ void sym_gemv_run(const SymGemvArgs& a, const SymPre* pre = nullptr,
+                                             const double2* cp = nullptr) {
   // dynamic smem: x (32 NT) | row partials (ntiles x 32) | column partials (noff x 32)
   extern __shared__ double2 sg_sh[];
   const int NB = a.NB, NT = a.NT;
@@ -732,23 +763,46 @@ __device__ __forceinline__ void sym_gemv_run(const SymGemvArgs& a) {
           if (i >= 0) v = cfms(a.bi_val[sb * a.EBI + e], a.yi[(size_t)s * a.NI + i], v);
         }
       } else {
-        const int r = a.blam[sb];
+        int r, lo = 0, hi = 0;
+        double sg;
+        if (pre != nullptr && k == (int)threadIdx.x) {
+          r = pre->r;
+          lo = pre->lo;
+          hi = pre->hi;
+          sg = pre->sg;
+        } else {
+          r = a.blam[sb];
+          sg = a.bsign[sb];
+          if (MODE == 1 && r >= 0) {
+            lo = a.lam_lo[r];
+            hi = a.lam_hi[r];
+          }
+        }
         if (r >= 0) {
           double2 z;
           if (MODE == 0)
             z = lam[r];
           else {
-            const int lo = a.lam_lo[r];
-            z = cscale(csub(a.wb[lo], a.wb[a.lam_hi[r]]), 0.5);
+            z = cscale(csub(a.wb[lo], a.wb[hi]), 0.5);
             if (a.zout != nullptr && lo == (int)sb) a.zout[(size_t)(*a.jsel) * a.jstride + r] = z;
           }
-          v = cscale(z, a.alpha * a.bsign[sb]);
+          v = cscale(z, a.alpha * sg);
         }
       }
     }
     x_sh[k] = v;
   }
   __syncthreads();
+  if (EARLY) {
+    if (warp < a.NC) {
+      double2 acc = cz();
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (lane + 32 * q < NB) acc = cfma(cp[q], x_sh[lane + 32 * q], acc);
+      acc = warp_sum2(acc);
+      if (lane == 0) __stcg(a.gcp + (size_t)s * a.NC + warp, acc);
+    }
+  }
   // ---- tiles: off-diagonal first (t < noff), then diagonal.  A diagonal tile streams half
   // the bytes of an off-diagonal one, so two diagonal tiles form one work item
   // (NT = 4, 8 warps: one item each; 4 warps: two items each).
@@ -821,7 +875,7 @@ __device__ __forceinline__ void sym_gemv_run(const SymGemvArgs& a) {
     for (int I2 = I + 1; I2 < NT; ++I2) acc = cadd(acc, part_col[I2 * (I2 - 1) / 2 + I][l]);
     a.out[(size_t)s * NB + k] = acc;
   }
-  if (a.gcp != nullptr) {
+  if (!EARLY && a.gcp != nullptr) {
     for (int c = warp; c < a.NC; c += WARPS) {
       double2 acc = cz();
       for (int k = lane; k < NB; k += 32) acc = cfma(a.cpl_b[((size_t)s * NB + k) * a.NC + c], x_sh[k], acc);
@@ -1881,8 +1935,15 @@ struct ArnoldiTailArgs {
   int split_givens;
   unsigned long long* tstamp;  // optional phase timestamps (block 0), 8 per Arnoldi step
   unsigned long long* span;    // FETIGPU_STEP_TIMES
+  // coarse solve beside the dual GEMV (k_sym_gemv_aside): ctr[1] == aside_nx when z is
+  // already there; the tail resets both counters for the next step.  nullptr: off.
+  unsigned int* aside_ctr;
+  unsigned int aside_nx;
+  int n_gcp;                // entries of gcp (n_sub * NC)
+  const double2* zpart;     // [nc][aside_nx] partial coarse solutions
+  const int* blk_corners;   // [grid][kTailCorners] corners the block's rows touch (-1 pad)
 };
-
+constexpr int kTailCorners = 128;  // corners a tail block's rows may touch (4 threads each)
 
 
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
@@ -1898,6 +1959,133 @@ __device__ __forceinline__ unsigned int atom_add_release_u32(unsigned int* p, un
 }
 __device__ __forceinline__ void st_relaxed_u32(unsigned int* p, unsigned int v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------------------
+// Dual GEMV of the Arnoldi step with the coarse solve beside it.  The launch is the dual
+// GEMV's n_sub CTAs plus 4 ca.ng coarse CTAs (blockIdx >= n_sub), all resident in one wave
+// (the host sizes ng from the occupancy of this kernel).  Every GEMV CTA stores its coarse
+// partials gcp = cpl_b^T t right after forming its input vector (sym_gemv_run EARLY) over
+// the all-ones sentinel the tail left there; a value whose two words both differ from the
+// sentinel is complete, so the value is its own ready flag and no fence stalls the GEMV.
+// The coarse CTAs work in groups of four: group q owns the corners c in [q cpg, (q+1) cpg),
+// each of its CTAs polls the (up to 4) partials of those corners, forms g_c = -sum gcp
+// (feti.cpp:523-538, the order of k_coarse_rhs) and writes one quarter of the columns of the
+// group's share of the coarse solve z = C^-1 g (feti.cpp:483-490),
+//   zpart[j][q] = sum_{c in slice q} C^-1[c][j] g_c        (C^-1 symmetric: row c = column c)
+// while the GEMV CTAs stream S_bb^-1 -- no coarse CTA waits for another one -- then counts
+// itself on ctr[1].  The fused tail finds ctr[1] == 4 ng, sums the ng partials of the corners
+// its rows touch (fixed order) and skips its own coarse phase and the grid barrier after it.
+// The poll is one-directional (GEMV CTAs never wait) and bounded: a coarse CTA that does not
+// see its partials within ~200 us gives up, ctr[1] stays short, and the tail computes z
+// itself -- no spin can hang, whatever the residency.
+struct CoarseAsideArgs {
+  int n_sub, ng, nc;
+  int giveup;  // test hook: act as if the partials never arrived
+  const double2* Cinv;
+  const int* corner_slots;  // [nc][4]
+  double2* zpart;           // [nc][ng]
+  unsigned int* ctr;        // [1] coarse CTAs done (reset by the tail)
+  unsigned long long* tstamp;  // FETIGPU_TAIL_TIMES: slots 10..14 of the step (coarse CTA 0)
+  const int* it_ptr;
+};
+constexpr int kAsideCpgMax = 32;  // corners per coarse group (4 poll threads each: one CTA)
+template <int SYM_BATCH, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv_aside(SymGemvArgs a, CoarseAsideArgs ca) {
+  static_assert(WARPS * 32 >= 4 * kAsideCpgMax, "one poll thread per (corner, partial)");
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if ((int)blockIdx.x < ca.n_sub) {
+    const int NT = a.NT, noff = NT * (NT - 1) / 2;
+    if (warp < noff) {
+      const double2* O = a.pack + (size_t)blockIdx.x * sym_tile_entries(NT) + NT * 17 * 32 + (size_t)warp * 1024;
+#pragma unroll
+      for (int u = 0; u < FETIGPU_GEMV_PF_ROWS; ++u) prefetch_l1(O + u * 32 + lane);
+    }
+    // solve-constant coupling entries of this warp's corner (NB <= 128: four rows per lane)
+    double2 cp[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = lane + 32 * q;
+      cp[q] = (warp < a.NC && k < a.NB) ? a.cpl_b[((size_t)blockIdx.x * a.NB + k) * a.NC + warp] : cz();
+    }
+    const SymPre pre = sym_pre_load<1>(a, blockIdx.x);
+    pdl_wait();
+    if (a.cont_ptr != nullptr && *a.cont_ptr == 0) return;
+    sym_gemv_run<1, SYM_BATCH, WARPS, true>(a, &pre, cp);
+    return;
+  }
+  // ---- coarse CTA: quarter `qd` of the columns of group `gq` ----
+  __shared__ double2 gs[kAsideCpgMax];
+  const int x = blockIdx.x - ca.n_sub, gq = x >> 2, qd = x & 3, nc = ca.nc;
+  const int cpg = (nc + ca.ng - 1) / ca.ng;
+  const int c0 = gq * cpg, ncs = max(0, min(cpg, nc - c0));  // the group's corners [c0, c0 + ncs)
+  // thread t < 4 ncs polls partial t & 3 of corner c0 + t / 4; its slot is solve-constant
+  const int my_slot = (int)threadIdx.x < 4 * ncs ? ca.corner_slots[(size_t)c0 * 4 + threadIdx.x] : -1;
+  // columns of this CTA: [j_lo, j_hi), thread t takes j_lo + t + 128 m
+  const int jq = (nc + 3) / 4, j_lo = qd * jq, j_hi = min(nc, j_lo + jq);
+  const bool stamp = ca.tstamp != nullptr && x == 0 && threadIdx.x == 0;
+  unsigned long long ts0 = 0;
+  if (stamp) ts0 = gtimer();
+  pdl_wait();
+  if (a.cont_ptr != nullptr && *a.cont_ptr == 0) return;
+  unsigned long long* ts = stamp ? ca.tstamp + (size_t)(*ca.it_ptr) * 16 : nullptr;
+  if (stamp) {
+    ts[10] = ts0;
+    ts[11] = gtimer();
+  }
+  bool ok = ca.giveup == 0;
+  {
+    double2 p = cz();
+    if (my_slot >= 0 && ok) {
+      const unsigned long long t0 = gtimer();
+      for (;;) {
+        asm volatile("ld.relaxed.gpu.global.v2.f64 {%0, %1}, [%2];" : "=d"(p.x), "=d"(p.y) : "l"(a.gcp + my_slot) : "memory");
+        if (__double_as_longlong(p.x) != -1LL && __double_as_longlong(p.y) != -1LL) break;
+        if (gtimer() - t0 > 200000ULL) {
+          ok = false;
+          break;
+        }
+      }
+    }
+    // g_c = ((0 - p0) - p1) - p2 - p3 on the corner's first lane
+    const double2 p1 = shfl2(p, (lane & ~3) + 1), p2 = shfl2(p, (lane & ~3) + 2), p3 = shfl2(p, (lane & ~3) + 3);
+    if ((threadIdx.x & 3) == 0 && (int)threadIdx.x < 4 * ncs)
+      gs[threadIdx.x >> 2] = csub(csub(csub(csub(cz(), p), p1), p2), p3);
+  }
+  if (!__syncthreads_and(ok ? 1 : 0)) return;
+  if (stamp) ts[12] = ts[13] = gtimer();
+  // zpart[j][gq] = sum_i g_i C^-1[c0 + i][j] for this CTA's columns, rows in ascending order,
+  // RB rows (RB x 2 loads per thread) in flight
+  constexpr int TPB = WARPS * 32, RB = 4;
+  for (int j0 = j_lo; j0 < j_hi; j0 += 2 * TPB) {
+    const int ja = min(j0 + (int)threadIdx.x, nc - 1), jb = min(j0 + (int)threadIdx.x + TPB, nc - 1);
+    double2 acc_a = cz(), acc_b = cz();
+    for (int i0 = 0; i0 < ncs; i0 += RB) {
+      double2 va[RB], vb[RB];
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        const double2* cr = ca.Cinv + (size_t)(c0 + min(i0 + u, ncs - 1)) * nc;
+        va[u] = __ldg(cr + ja);
+        vb[u] = __ldg(cr + jb);
+      }
+#pragma unroll
+      for (int u = 0; u < RB; ++u)
+        if (i0 + u < ncs) {
+          const double2 g = gs[i0 + u];
+          acc_a = cfma(va[u], g, acc_a);
+          acc_b = cfma(vb[u], g, acc_b);
+        }
+    }
+    if (j0 + (int)threadIdx.x < j_hi) __stcg(ca.zpart + (size_t)(j0 + threadIdx.x) * ca.ng + gq, acc_a);
+    if (j0 + (int)threadIdx.x + TPB < j_hi) __stcg(ca.zpart + (size_t)(j0 + threadIdx.x + TPB) * ca.ng + gq, acc_b);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ca.ctr + 1) : "memory");
+  }
+  if (stamp) ts[14] = gtimer();
 }
 
 // Grid barrier on a monotonically increasing 64-bit arrival counter: barrier k of the
@@ -1957,7 +2145,7 @@ __device__ __forceinline__ void block_reduce_parts(const double2* __restrict__ p
 // dynamic smem: w_sh[THREADS] | h1[hcap] | h2[hcap] | Givens staging[640]
 // (A one-reduction Gram-matrix CGS2 variant measured 180 vs 188 solves/s; not kept.)
 // dynamic smem: w_sh | hs1 | hs2 | gs | Givens staging
-template <int THREADS, int NCM, int MINB>
+template <int THREADS, int NCM, int MINB, bool ASIDE>
 __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs a) {
   constexpr int WARPS = THREADS / 32, LPR = THREADS / 32;
   extern __shared__ double2 tail_sh[];
@@ -1966,6 +2154,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   double2* hs2 = hs1 + a.hcap;
   double2* gs = hs2 + a.hcap;
   double2* stage = gs + a.hcap;
+  double2* z_sh = stage + 640;  // [nc], aside path only (host sizes the dynamic smem)
   __shared__ double2 cred[WARPS];
   __shared__ double inv_sh;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1992,37 +2181,58 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
       }
     }
   }
-  // warm L1 with the coarse phase's constant operands: the corner-slot lists and this
-  // block's first round of C^-1 rows (the L2-persisting inverse)
-  // corner-slot lists of this thread's first two coarse rows in registers (the rest, for
-  // large coarse spaces, warmed into L1)
+  // ASIDE (the coarse solve ran beside the dual GEMV, k_sym_gemv_aside): 4 threads per corner
+  // of the block's list sum its aside_nx partials; the coarse phase below is only the path
+  // taken when that launch gave up.  Otherwise: warm L1 with the coarse phase's constant
+  // operands -- the corner-slot lists of this thread's first two coarse rows in registers
+  // (the rest, for large coarse spaces, warmed into L1) and this block's first round of
+  // C^-1 rows.
+  static_assert(!ASIDE || kTailCorners * 4 == THREADS, "one pass over the block's corner list");
+  constexpr int PB = 10;  // partials per thread in one batch (aside_nx <= 40 groups)
   int csl[2][4];
+  int bc = -1;
+  if constexpr (!ASIDE) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int k = threadIdx.x + h * THREADS;
+    for (int h = 0; h < 2; ++h) {
+      const int k = threadIdx.x + h * THREADS;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) csl[h][q] = k < a.nc ? a.corner_slots[k * 4 + q] : -1;
-  }
-  for (int k = threadIdx.x + 2 * THREADS; k < a.nc; k += THREADS) prefetch_l1(a.corner_slots + k * 4);
-  {
+      for (int q = 0; q < 4; ++q) csl[h][q] = k < a.nc ? a.corner_slots[k * 4 + q] : -1;
+    }
+    for (int k = threadIdx.x + 2 * THREADS; k < a.nc; k += THREADS) prefetch_l1(a.corner_slots + k * 4);
     const int row = blockIdx.x * (WARPS / 2) + (warp >> 1);
     if (row < a.nc) {
       const double2* cr = a.Cinv + (size_t)row * a.nc;
       for (int k0 = (warp & 1) * 32 + lane; k0 < a.nc; k0 += 64) prefetch_l1(cr + k0);
     }
+  } else {
+    bc = a.blk_corners[(size_t)blockIdx.x * kTailCorners + threadIdx.x / 4];
   }
   pdl_wait();
-  // the dual GEMV's coarse partials, loaded together with the cycle state (one latency)
+  // requested together (one latency): the cycle state, the coarse CTAs' done count (ASIDE) or
+  // the dual GEMV's coarse partials, and the dual-tail operands that do not depend on z
+  unsigned int aside_done = 0;
   double2 gv[2][4];
+  if constexpr (ASIDE) {
+    aside_done = __ldcg(a.aside_ctr + 1);
+  } else {
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) gv[h][q] = csl[h][q] >= 0 ? a.gcp[csl[h][q]] : cz();
+      for (int q = 0; q < 4; ++q) gv[h][q] = csl[h][q] >= 0 ? a.gcp[csl[h][q]] : cz();
+  }
+  double2 u[2] = {cz(), cz()};
+  if (act) {
+    u[0] = a.u1b[slots[0]];
+    u[1] = a.u1b[slots[1]];
+  }
   if (a.st->cont == 0) {  // unrolled WHILE body: the cycle already stopped (or never started:
     // zero rhs) -- make sure the WHILE node exits
     if (a.ga.in_graph && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.ga.handle, 0u);
     return;
   }
+  // z already there?  (the same answer in every block: the count was final when the dual
+  // GEMV's launch ended and is reset only after this kernel's last barrier)
+  const bool aside = ASIDE && aside_done == 4u * a.aside_nx;
   const int nv = a.st->j + 1, nout = nv + 1, G = gridDim.x;
   const int it = a.st->iterations;
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 0] = gtimer();
@@ -2031,28 +2241,44 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   if (!a.split_givens && blockIdx.x == 0 && warp == 0)
     givens_prefetch(a.ga, &gpre, reinterpret_cast<double*>(stage), stage + 128);
   span_mark(a.span, &it, 2, 0);
-  // dual-tail operand that does not depend on z (loaded before the barrier)
-  double2 u[2] = {cz(), cz()};
-  if (act) {
-    u[0] = a.u1b[slots[0]];
-    u[1] = a.u1b[slots[1]];
+  if constexpr (ASIDE) {
+    if (aside) {
+      // z at the block's corners = sum of the coarse groups' partials, fixed order: each of the
+      // corner's 4 threads sums partials sub, sub + 4, ..., then a xor tree over the 4 lanes
+      // (loading the partials before the count is known costs registers across the prologue:
+      // measured slower)
+      const int sub = threadIdx.x & 3;
+      double2 zp[PB];
+#pragma unroll
+      for (int q = 0; q < PB; ++q)
+        zp[q] = (bc >= 0 && sub + 4 * q < (int)a.aside_nx) ? __ldcg(a.zpart + (size_t)bc * a.aside_nx + sub + 4 * q) : cz();
+      double2 t = cz();
+#pragma unroll
+      for (int q = 0; q < PB; ++q) t = cadd(t, zp[q]);
+      t = cadd(t, shfl_xor2(t, 2));
+      t = cadd(t, shfl_xor2(t, 1));
+      if ((threadIdx.x & 3) == 0 && bc >= 0) z_sh[bc] = t;
+      __syncthreads();
+    }
   }
   // ---- phase 0: z = C^-1 g.  g staged in smem (reusing the w buffer); each warp takes one
   // coarse row at a time with all of its lane's loads in one batch (clamped addresses) ----
-  {
+  if (!aside) {
     double2* g_sh = w_sh;  // nc <= hcap + THREADS is checked on the host
     // coarse rhs g = -sum_s gcp over the (up to 4) subdomains of each corner, assembled
     // redundantly by every block (same order as k_coarse_rhs)
+    if constexpr (!ASIDE) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int k = threadIdx.x + h * THREADS;
-      double2 acc = cz();
+      for (int h = 0; h < 2; ++h) {
+        const int k = threadIdx.x + h * THREADS;
+        double2 acc = cz();
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (csl[h][q] >= 0) acc = csub(acc, gv[h][q]);
-      if (k < a.nc) g_sh[k] = acc;
+        for (int q = 0; q < 4; ++q)
+          if (csl[h][q] >= 0) acc = csub(acc, gv[h][q]);
+        if (k < a.nc) g_sh[k] = acc;
+      }
     }
-    for (int k = threadIdx.x + 2 * THREADS; k < a.nc; k += THREADS) {
+    for (int k = threadIdx.x + (ASIDE ? 0 : 2 * THREADS); k < a.nc; k += THREADS) {
       double2 acc = cz();
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -2088,7 +2314,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
     }
   }
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 1] = gtimer();
-  grid_sync_plain(a.bar);
+  if (!aside) grid_sync_plain(a.bar);
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 2] = gtimer();
   // block partials of conj(V_i) w (i < nv) and |w|^2 (i = nv), one warp per vector
   // pass-1 and pass-2 partials live in separate halves of `part`: every block reduces the
@@ -2137,7 +2363,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
       double2 cz_ = cz();
 #pragma unroll
       for (int c = 0; c < NCM; ++c)
-        if (cgv[q][c] >= 0) cz_ = cfma(cpv[q][c], __ldcg(a.z + cgv[q][c]), cz_);
+        if (cgv[q][c] >= 0) cz_ = cfma(cpv[q][c], (ASIDE && aside) ? z_sh[cgv[q][c]] : __ldcg(a.z + cgv[q][c]), cz_);
       ud[q] = csub(u[q], cz_);
     }
     const double2 d = csub(ud[0], ud[1]);
@@ -2171,6 +2397,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 8] = gtimer();
   // block 0: Givens, stopping tests, WHILE-node condition; h1/h2 published for the host side
   if (blockIdx.x == 0) {
+    if (ASIDE && threadIdx.x == 0) a.aside_ctr[1] = 0u;  // (every block read it before the barriers above)
     for (int i = threadIdx.x; i < nout; i += THREADS) {
       a.h1[i] = hs1[i];
       a.h2[i] = hs2[i];
@@ -2181,6 +2408,12 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
       givens_warp<true>(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384, hs1, hs2, &gpre);
     }
     if (a.tstamp && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 9] = gtimer();
+  }
+  // coarse partials back to the all-ones sentinel for the next step's k_sym_gemv_aside
+  if constexpr (ASIDE) {
+    const double ones = __longlong_as_double(-1LL);
+    for (int i = blockIdx.x * THREADS + threadIdx.x; i < a.n_gcp; i += G * THREADS)
+      __stcg(const_cast<double2*>(a.gcp) + i, make_double2(ones, ones));
   }
   if (a.span != nullptr) {
     __syncthreads();
