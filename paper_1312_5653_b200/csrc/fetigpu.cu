@@ -177,6 +177,7 @@ struct Ctx {
   int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_rows = 512;
   // coarse solve beside the dual GEMV (k_sym_gemv_aside): coarse groups of 4 CTAs per launch (0 = off)
   int aside_nx = 0;
+  bool tail_pf = false;  // the tail prefetches the head of the preconditioner operator into L2
   bool aside_giveup = false;  // test hook FETIGPU_ASIDE_GIVEUP: the coarse CTAs never see their arrivals
   unsigned int* d_aside_ctr = nullptr;
   double2* d_zpart = nullptr;  // [nc][aside_nx] partial coarse solutions
@@ -606,6 +607,7 @@ struct Ctx {
     d_bar = alloc<unsigned int>(2);
     CU(cudaMemsetAsync(d_bar, 0, 2 * sizeof(unsigned int), stream));
     setup_coarse_aside(sms);
+    tail_pf = !std::getenv("FETIGPU_NO_TAIL_PF");
     if (std::getenv("FETIGPU_TAIL_TIMES")) {
       d_tstamp = alloc<unsigned long long>((size_t)16 * (vcap_hint() + 2));
       CU(cudaMemsetAsync(d_tstamp, 0, (size_t)16 * (vcap_hint() + 2) * sizeof(unsigned long long), stream));
@@ -1679,6 +1681,12 @@ struct Ctx {
       t.aside_ctr = aside_nx > 0 ? d_aside_ctr : nullptr;
       t.aside_nx = (unsigned int)aside_nx;
       t.n_gcp = H.n_sub * H.NC;
+      if (tail_pf) {  // head of every subdomain's S_bb (first off-diagonal tile) into L2
+        t.pf_base = reinterpret_cast<const char*>(d_Sbb_p + NT * 17 * 32);
+        t.pf_stride = sizeof(double2) * sym_tile_entries(NT);
+        t.pf_bytes = NT > 1 ? 16384u : 0u;
+        t.pf_count = H.n_sub;
+      }
       t.zpart = d_zpart;
       t.blk_corners = d_blk_corners;
       launch(FETIGPU_K_ORTHO, [&] {
