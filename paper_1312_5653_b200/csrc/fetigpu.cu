@@ -180,6 +180,8 @@ struct Ctx {
   bool tail_pf = false;  // the tail prefetches the head of the preconditioner operator into L2
   bool aside_giveup = false;  // test hook FETIGPU_ASIDE_GIVEUP: the coarse CTAs never see their arrivals
   unsigned int* d_aside_ctr = nullptr;
+  double2* d_hbuf = nullptr;   // [tail_grid][2][vcap + 2] dot vectors of long cycles
+  int tail_hcs = kTailHcs;     // (test hook FETIGPU_TAIL_HCS: a smaller shared-memory capacity)
   double2* d_zpart = nullptr;  // [nc][aside_nx] partial coarse solutions
   int* d_blk_corners = nullptr;  // [tail_grid][kTailCorners]
   static constexpr int kBodyUnroll = 4;  // steps per WHILE-body execution (measured at config 2: 4 205.6, 8 204.9, 12 203.1 solves/s; earlier code 4: 182.8, 8: 183.5)
@@ -578,11 +580,10 @@ struct Ctx {
   // measured 152 vs 203 solves/s (spills, and the tail's CTAs packed two per SM).
   static constexpr int kTailMinBlocks = 1;
   size_t tail_smem() const {
-    return sizeof(double2) * ((size_t)kTailThreads + 3 * (size_t)(vcap_hint() + 2) + 640 + (size_t)std::max(nc, 0));
+    return sizeof(double2) * ((size_t)std::max(kTailThreads, nc) + 2 * (size_t)kTailHcs + 640 + (size_t)std::max(nc, 0));
   }
   void setup_fused_tail() {
-    if (dist() || H.NC > 4 || H.n_aug > 0 || nc > kTailThreads + 2 * (vcap_hint() + 2) ||
-        std::getenv("FETIGPU_NO_FUSED_TAIL"))
+    if (dist() || H.NC > 4 || H.n_aug > 0 || std::getenv("FETIGPU_NO_FUSED_TAIL"))
       return;
     const size_t smem = tail_smem();
     if (smem > 200 * 1024) return;
@@ -606,6 +607,8 @@ struct Ctx {
     tail_rb = rows <= 1 ? 1 : rows <= 2 ? 2 : rows <= 4 ? 4 : rows <= 8 ? 8 : 16;
     d_bar = alloc<unsigned int>(2);
     CU(cudaMemsetAsync(d_bar, 0, 2 * sizeof(unsigned int), stream));
+    d_hbuf = alloc<double2>((size_t)tail_grid * 2 * (vcap_hint() + 2));
+    if (const char* e = std::getenv("FETIGPU_TAIL_HCS")) tail_hcs = std::max(0, std::min(kTailHcs, std::atoi(e)));
     setup_coarse_aside(sms);
     tail_pf = !std::getenv("FETIGPU_NO_TAIL_PF");
     if (std::getenv("FETIGPU_TAIL_TIMES")) {
@@ -1687,6 +1690,9 @@ struct Ctx {
         t.pf_bytes = NT > 1 ? 16384u : 0u;
         t.pf_count = H.n_sub;
       }
+      t.wg = std::max(kTailThreads, nc);
+      t.hbuf = d_hbuf;
+      t.hcs = tail_hcs;
       t.zpart = d_zpart;
       t.blk_corners = d_blk_corners;
       launch(FETIGPU_K_ORTHO, [&] {

@@ -1948,9 +1948,13 @@ struct ArnoldiTailArgs {
   size_t pf_stride;
   unsigned int pf_bytes;
   int pf_count;
+  int wg;                   // entries of the w / g staging region: max(THREADS, nc)
+  int hcs;                  // dot-vector entries that use shared memory (<= kTailHcs; test hook: smaller)
+  double2* hbuf;            // [grid][2][hcap] dot vectors of long cycles (nv + 1 > kTailHcs)
   const double2* zpart;     // [nc][aside_nx] partial coarse solutions
   const int* blk_corners;   // [grid][kTailCorners] corners the block's rows touch (-1 pad)
 };
+constexpr int kTailHcs = 128;      // dot-vector entries kept in shared memory
 constexpr int kTailCorners = 128;  // corners a tail block's rows may touch (4 threads each)
 
 
@@ -2150,18 +2154,20 @@ __device__ __forceinline__ void block_reduce_parts(const double2* __restrict__ p
 }
 
 // Fused tail, one multiplier row per thread, THREADS rows per block, one block per SM.
-// dynamic smem: w_sh[THREADS] | h1[hcap] | h2[hcap] | Givens staging[640]
-// (A one-reduction Gram-matrix CGS2 variant measured 180 vs 188 solves/s; not kept.)
-// dynamic smem: w_sh | hs1 | hs2 | gs | Givens staging
+// dynamic smem: w_sh / g_sh [wg = max(THREADS, nc)] | h1[kTailHcs] | h2[kTailHcs] | Givens
+// staging[640] | z_sh[nc] (ASIDE).  The dot vectors h1 / h2 (nv + 1 entries) live in shared
+// memory while they fit kTailHcs entries and in a per-block global scratch beyond (long
+// cycles): the tail's footprint does not grow with max_iter, so it stays within the shared-
+// memory carve-out of the GEMVs around it (a 129 KB tail between 90 KB GEMVs measured +2 %
+// step time).
 template <int THREADS, int NCM, int MINB, bool ASIDE>
 __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs a) {
   constexpr int WARPS = THREADS / 32, LPR = THREADS / 32;
   extern __shared__ double2 tail_sh[];
   double2* w_sh = tail_sh;
-  double2* hs1 = w_sh + THREADS;
-  double2* hs2 = hs1 + a.hcap;
-  double2* gs = hs2 + a.hcap;
-  double2* stage = gs + a.hcap;
+  double2* hs1s = w_sh + a.wg;
+  double2* hs2s = hs1s + kTailHcs;
+  double2* stage = hs2s + kTailHcs;
   double2* z_sh = stage + 640;  // [nc], aside path only (host sizes the dynamic smem)
   __shared__ double2 cred[WARPS];
   __shared__ double inv_sh;
@@ -2248,6 +2254,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   const bool aside = ASIDE && aside_done == 4u * a.aside_nx;
   const int nv = a.st->j + 1, nout = nv + 1, G = gridDim.x;
   const int it = a.st->iterations;
+  double2* hs1 = nout <= a.hcs ? hs1s : a.hbuf + (size_t)blockIdx.x * 2 * a.hcap;
+  double2* hs2 = nout <= a.hcs ? hs2s : hs1 + a.hcap;
   if (a.tstamp && blockIdx.x == 0 && threadIdx.x == 0) a.tstamp[(size_t)it * 16 + 0] = gtimer();
   // Givens operands known now (block 0): loaded during the coarse phase, off the critical path
   __shared__ GivensPre gpre;
@@ -2277,7 +2285,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
   // ---- phase 0: z = C^-1 g.  g staged in smem (reusing the w buffer); each warp takes one
   // coarse row at a time with all of its lane's loads in one batch (clamped addresses) ----
   if (!aside) {
-    double2* g_sh = w_sh;  // nc <= hcap + THREADS is checked on the host
+    double2* g_sh = w_sh;  // (wg >= nc entries)
     // coarse rhs g = -sum_s gcp over the (up to 4) subdomains of each corner, assembled
     // redundantly by every block (same order as k_coarse_rhs)
     if constexpr (!ASIDE) {

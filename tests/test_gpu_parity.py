@@ -310,7 +310,7 @@ def test_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
                                     "FETIGPU_NO_DEFER", "FETIGPU_NO_SPLIT", "FETIGPU_NO_FDM",
                                     "FETIGPU_COOP_REJECT", "FETIGPU_NO_FUSED_TAIL", "FETIGPU_NO_PDL",
                                     "FETIGPU_EAGER", "FETIGPU_NO_AIC", "FETIGPU_NO_STENCIL", "FETIGPU_NO_BT",
-                                    "FETIGPU_NO_ASIDE", "FETIGPU_ASIDE_GIVEUP", "FETIGPU_NO_TAIL_PF"])
+                                    "FETIGPU_NO_ASIDE", "FETIGPU_ASIDE_GIVEUP", "FETIGPU_NO_TAIL_PF", "FETIGPU_TAIL_HCS"])
 def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
     """Each reuse/fusion of the solve path (preconditioned basis Z, compact interior rhs,
     GEMV-free final elimination, deferred GMRES completion, Givens folded into the next
@@ -324,7 +324,7 @@ def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
     solver = fetigpu.SchurSolver(p, 8, 8, tol=1e-10)
     a = solver.solve()
     solver.close()
-    monkeypatch.setenv(switch, "1")
+    monkeypatch.setenv(switch, "4" if switch == "FETIGPU_TAIL_HCS" else "1")  # HCS: dot vectors beyond 4 entries in global scratch
     solver = fetigpu.SchurSolver(p, 8, 8, tol=1e-10)
     b = solver.solve()
     solver.close()
