@@ -1044,7 +1044,7 @@ struct Ctx {
     reuse_elim = !dist() && H.n_aug == 0 && !std::getenv("FETIGPU_NO_ELIM_REUSE");
     if (reuse_elim) {
       d_u1b0 = alloc<double2>((size_t)n_slot_ext);
-      d_gcp0 = alloc<double2>((size_t)S * NC);
+      d_z0 = alloc<double2>(std::max(nc, 1));
     }
     d_fc = alloc<double2>(std::max(nc, 1));
     zero(d_fc, std::max(nc, 1));  // augmentation rows of f_c stay zero (feti.cpp:521-522)
@@ -1072,7 +1072,7 @@ struct Ctx {
     }
     // tail: 2 halves; also the per-block partials of the primal-residual stencil reduction
     d_part = alloc<double2>(std::max((size_t)(vcap + 2) * std::max(mdot_blocks, 2 * tail_grid),
-                                     (size_t)cdiv(std::max(P.nx - 1, 1), 256) * std::max(P.ny - 1, 1) + 64));
+                                     2 * (size_t)cdiv(std::max(P.nx - 1, 1), 256) * std::max(P.ny - 1, 1) + 1024));
     d_red = alloc<double2>(3 * (vcap + 2));
     d_y = alloc<double2>(vcap + 2);
     d_gst = alloc<GmresState>(1);
@@ -1450,7 +1450,7 @@ struct Ctx {
   // first elimination's S^-1 (t_b - A_bi y_i) and coarse terms, kept for the final one
   // (reuse_elim: one GPU, no augmentation); last_dual_of_x: GMRES's last dual application was
   // on the returned multipliers (its u1_b / gcp are S^-1(-B^T lam) and cpl_b^T(-B^T lam))
-  double2 *d_u1b0 = nullptr, *d_gcp0 = nullptr;
+  double2 *d_u1b0 = nullptr, *d_z0 = nullptr;
   bool reuse_elim = false, last_dual_of_x = false;
   void eliminate_boundary(const double2* ti, const double2* tb, const double2* fc, bool new_yi) {
     const int S = H.n_sub, NI = H.NI, NB = H.NB;
@@ -1480,9 +1480,10 @@ struct Ctx {
       launch(FETIGPU_K_OTHER, [&] { k_gcp_full<<<S, 256, 0, stream>>>(L, d_cpl_i, d_cpl_b, ti, tb, d_gcp); });
     if (new_yi && reuse_elim) {
       CU(cudaMemcpyAsync(d_u1b0, d_u1b, (size_t)n_slot_ext * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
-      CU(cudaMemcpyAsync(d_gcp0, d_gcp, (size_t)S * H.NC * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
     }
     coarse_solve(fc);
+    if (new_yi && reuse_elim && nc > 0)  // z of the first elimination, for the final one (linearity)
+      CU(cudaMemcpyAsync(d_z0, d_z, (size_t)nc * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
     launch(FETIGPU_K_OTHER, [&] {
       k_ub_correct<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(L, d_cglob, d_z, d_cpl_b, d_u1b);
     });
@@ -1593,6 +1594,21 @@ struct Ctx {
     }
     launch(FETIGPU_K_ORTHO, [&] { k_add_inplace<<<cdiv(nown, 256), 256, 0, stream>>>(nown, x + own0, d_zl + own0); });
   }
+  // the Arnoldi step's dual GEMV: with the coarse solve beside it (k_sym_gemv_aside) when set up
+  void dual_gemv_step(SymGemvArgs g) {
+    if (tail_rpt > 0 && aside_nx > 0) {
+      g.alpha = -1.0;
+      g.out = d_u1b;
+      g.cpl_b = d_cpl_b;
+      g.gcp = d_gcp;
+      const CoarseAsideArgs ca{H.n_sub, aside_nx, nc, aside_giveup ? 1 : 0, d_Cinv, d_corner_slots,
+                               d_zpart, d_aside_ctr, d_tstamp, &d_gst->iterations};
+      launch(FETIGPU_K_DUAL_GEMV,
+             [&] { kx(k_sym_gemv_aside<8, 4>, H.n_sub + 4 * aside_nx, 128, sym_smem(), g, ca); });
+    } else {
+      dual_gemv(g, tail_rpt > 0);
+    }
+  }
   static constexpr int kLagSteps = 4;  // sharded cycle: steps per host check of the state
   void arnoldi_step(bool in_graph, int u = 0, int j_host = -1) {
     const bool split = in_graph && split_givens && tail_rpt > 0;
@@ -1635,18 +1651,7 @@ struct Ctx {
         g.jsel = split ? &d_gst->jcol : &d_gst->j;
         g.jstride = ldv;
       }
-      if (tail_rpt > 0 && aside_nx > 0) {
-        g.alpha = -1.0;
-        g.out = d_u1b;
-        g.cpl_b = d_cpl_b;
-        g.gcp = d_gcp;
-        const CoarseAsideArgs ca{H.n_sub, aside_nx, nc, aside_giveup ? 1 : 0, d_Cinv, d_corner_slots,
-                                 d_zpart, d_aside_ctr, d_tstamp, &d_gst->iterations};
-        launch(FETIGPU_K_DUAL_GEMV,
-               [&] { kx(k_sym_gemv_aside<8, 4>, H.n_sub + 4 * aside_nx, 128, sym_smem(), g, ca); });
-      } else {
-        dual_gemv(g, tail_rpt > 0);
-      }
+      dual_gemv_step(g);
     }
     span_on = false;
     in_arnoldi = false;
@@ -1989,7 +1994,10 @@ struct Ctx {
     st.coarse_dim = nc;
     st.setup_seconds = setup_seconds;
     phase("start");
-    norm_async(rhs, n, sb);
+    // |rhs|^2 (the primal residual's scale): summed by the residual kernel of the statistics
+    // below when that is the stencil form, else here
+    const bool rhs_norm_late = stencil_ok && !dist();
+    if (!rhs_norm_late) norm_async(rhs, n, sb);
     const int S = H.n_sub, NI = H.NI, NB = H.NB;
     launch(FETIGPU_K_OTHER, [&] {
       k_split_rhs<<<cdiv((long long)S * (NI + NB), 256), 256, 0, stream>>>(L, d_idof, d_bdof, rhs, d_fi, d_fb);
@@ -2014,15 +2022,12 @@ struct Ctx {
     if (reuse_elim && last_dual_of_x) {
       // S^-1 and the coarse terms are linear in t = [f_i ; f_b - B^T lam]: the first
       // elimination plus GMRES's true-residual dual application give them without a GEMV
+      // (z = C^-1 (f_c - sum gcp) likewise: z0 of the first elimination + the z of that dual
+      // application, so no coarse rhs / coarse GEMV either)
+      if (nc > 0)
+        launch(FETIGPU_K_OTHER, [&] { k_add_inplace<<<cdiv(nc, 256), 256, 0, stream>>>(nc, d_z, d_z0); });
       launch(FETIGPU_K_OTHER, [&] {
-        k_add_inplace<<<cdiv((long long)n_slot_ext, 256), 256, 0, stream>>>(n_slot_ext, d_u1b, d_u1b0);
-      });
-      launch(FETIGPU_K_OTHER, [&] {
-        k_add_inplace<<<cdiv((long long)S * H.NC, 256), 256, 0, stream>>>(S * H.NC, d_gcp, d_gcp0);
-      });
-      coarse_solve(d_fc);
-      launch(FETIGPU_K_OTHER, [&] {
-        k_ub_correct<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(L, d_cglob, d_z, d_cpl_b, d_u1b);
+        k_ub_correct<<<cdiv((long long)S * NB, 256), 256, 0, stream>>>(L, d_cglob, d_z, d_cpl_b, d_u1b, d_u1b0);
       });
     } else {
       launch(FETIGPU_K_OTHER, [&] {
@@ -2066,7 +2071,10 @@ struct Ctx {
         k_stencil_residual_part<<<grid, 256, 0, stream>>>(P.nx - 1, P.ny - 1, S9, x, rhs, d_part);
       });
       launch(FETIGPU_K_OTHER, [&] {
-        k_norm_max_final_big<<<1, 1024, 0, stream>>>((int)(grid.x * grid.y), d_part, d_stat + sb + 2);
+        if (rhs_norm_late)
+          k_norm_max_final_big<<<2, 1024, 0, stream>>>((int)(grid.x * grid.y), d_part, d_stat + sb + 2, d_stat + sb);
+        else
+          k_norm_max_final_big<<<1, 1024, 0, stream>>>((int)(grid.x * grid.y), d_part, d_stat + sb + 2);
       });
     } else {
       apply_global<double2>(x, nullptr, 1.0, mc, d_ax);
@@ -2148,8 +2156,10 @@ struct Ctx {
     launch(FETIGPU_K_OTHER, [&] { k_conj<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x, d_x2); });
     apply_global<double2>(d_x2, nullptr, 0.0, 1.0, d_rhs);
     fetigpu_feti_stats sm = feti_solve(d_rhs, d_x, 4);
-    // lambda = Re t = Re t', u = lambda / phi; imag leak = max |Im t'|
-    launch(FETIGPU_K_GLOBAL, [&] { k_realify_u<<<cdiv(n, 256), 256, 0, stream>>>(n, d_x, 1.0 / phi, lam, u); });
+    // lambda = Re t = Re t', u = lambda / phi; imag leak = max |Im t'| and |lambda|_inf (the leak
+    // warning's scale) from the same pass: statistics slots 8 and 9
+    const int blocks = std::max(1, std::min(592, cdiv(n, 256)));
+    launch(FETIGPU_K_GLOBAL, [&] { k_realify_stats<<<blocks, 256, 0, stream>>>(n, d_x, 1.0 / phi, lam, u, d_part); });
     const size_t nbytes = sizeof(double) * n;
     if (host_lam != nullptr) {
       if (!copy_stream) {
@@ -2161,21 +2171,12 @@ struct Ctx {
       CU(cudaMemcpyAsync(host_lam, lam, nbytes, cudaMemcpyDeviceToHost, copy_stream));
       CU(cudaMemcpyAsync(host_u, u, nbytes, cudaMemcpyDeviceToHost, copy_stream));
     }
-    const int blocks = std::max(1, std::min(296, cdiv(n, 256)));
-    launch(FETIGPU_K_GLOBAL, [&] {
-      k_imag_max_part<<<blocks, 256, 0, stream>>>(n, d_x, reinterpret_cast<double*>(d_part));
-    });
-    launch(FETIGPU_K_GLOBAL, [&] {
-      k_max_final<<<1, 32, 0, stream>>>(blocks, reinterpret_cast<const double*>(d_part), d_stat + 8);
-    });
+    launch(FETIGPU_K_GLOBAL, [&] { k_max2_final<<<1, 32, 0, stream>>>(blocks, d_part, d_stat + 8); });
     // y = ybar - V^-1 K lambda ; u = lambda / phi  (control.cpp:323-325)
     apply_global<double>(lam, nullptr, 1.0, 0.0, d_real1);
     mass_solve(d_real1);
     launch(FETIGPU_K_GLOBAL, [&] { k_recover_y<<<cdiv(n, 256), 256, 0, stream>>>(n, ybar, d_real1, y); });
     if (host_y != nullptr) CU(cudaMemcpyAsync(host_y, y, nbytes, cudaMemcpyDeviceToHost, stream));
-    // |lambda|_inf for the leak warning
-    launch(FETIGPU_K_GLOBAL, [&] { k_real_to_complex<<<cdiv(n, 256), 256, 0, stream>>>(n, lam, d_ax); });
-    norm_async(d_ax, n, 9);
     phase("recovery");
     stats_to_host();
     sync();  // the call's one final synchronisation
@@ -2222,13 +2223,14 @@ struct Ctx {
       SymGemvArgs a = sym_args(d_Sinv_p);
       a.mode = 1;
       a.wb = d_wb;
-      dual_gemv(a, tail_rpt > 0);
+      dual_gemv_step(a);  // the step's own launch (coarse CTAs included when set up)
     }
     CU(cudaEventRecordWithFlags(ev[2], stream, cudaEventRecordExternal));
     CU(cudaStreamEndCapture(stream, &g));
     prof = was_prof;
     CU(cudaGraphInstantiate(&ge, g, 0));
     CU(cudaGraphLaunch(ge, stream));
+    if (d_aside_ctr) CU(cudaMemsetAsync(d_aside_ctr, 0, 2 * sizeof(unsigned int), stream));
     sync();
     float a = 0, b = 0;
     CU(cudaEventElapsedTime(&a, ev[0], ev[1]));

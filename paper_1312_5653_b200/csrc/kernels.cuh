@@ -1308,8 +1308,11 @@ __global__ void k_gcp_full(SubLayout L, const double2* __restrict__ cpl_i, const
   }
 }
 // u_b = u1_b - cpl_b z_loc  (feti.cpp:542-555, boundary rows)
+// u_b = (u1_b [+ add]) - cpl_b z   (feti.cpp:542-548; `add`: the first elimination's part of u1_b
+// when the final elimination is assembled by linearity)
 __global__ void k_ub_correct(SubLayout L, const int* __restrict__ cglob, const double2* __restrict__ z,
-                             const double2* __restrict__ cpl_b, double2* __restrict__ ub) {
+                             const double2* __restrict__ cpl_b, double2* __restrict__ ub,
+                             const double2* __restrict__ add = nullptr) {
   const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (long long)L.S * L.NB) return;
   const int s = (int)(k / L.NB);
@@ -1318,7 +1321,8 @@ __global__ void k_ub_correct(SubLayout L, const int* __restrict__ cglob, const d
     const int cg = cglob[(size_t)s * L.NC + c];
     if (cg >= 0) acc = cfma(cpl_b[k * L.NC + c], z[cg], acc);
   }
-  ub[k] = csub(ub[k], acc);
+  const double2 u = add != nullptr ? cadd(ub[k], add[k]) : ub[k];
+  ub[k] = csub(u, acc);
 }
 // r_i = A_ib u_b + A_ic z_loc  (rhs of the interior harmonic extension)
 __global__ void k_ri_rhs(SubLayout L, const int* __restrict__ ib_idx, const double2* __restrict__ ib_val,
@@ -2494,9 +2498,14 @@ __global__ void k_norm_max_final(int nblk, const double2* __restrict__ part, dou
 
 // the same over many partials (the stencil residual's one-per-row-segment blocks): 1024
 // threads, each summing partials t, t + 1024, ... in order, then a fixed-order block reduce
+// out = (sum part.x, max part.y) over nblk partials; out_q (optional) likewise over the next nblk
 __global__ void __launch_bounds__(1024) k_norm_max_final_big(int nblk, const double2* __restrict__ part,
-                                                             double2* __restrict__ out) {
+                                                             double2* __restrict__ out, double2* __restrict__ out_q = nullptr) {
   __shared__ double ws[32], wm[32];
+  if (out_q != nullptr && blockIdx.x == 1) {
+    part += nblk;
+    out = out_q;
+  }
   double s = 0.0, m = 0.0;
   for (int b0 = threadIdx.x; b0 < nblk; b0 += 1024 * 4) {
     double2 v[4];
@@ -2679,9 +2688,27 @@ __global__ void k_jump_norm_part(int nl, const int* __restrict__ lo, const int* 
   }
   block_sum_max(s, m, part);
 }
+// as block_sum_max, plus a second sum q -> part_q[blockIdx.x] = (q, 0)
+__device__ __forceinline__ void block_sum_max_q(double s, double m, double q, double2* part, double2* part_q) {
+  __shared__ double ss[32], sm_[32], sq[32];
+  s = warp_sum(s);
+  m = warp_max(m);
+  q = warp_sum(q);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) ss[warp] = s, sm_[warp] = m, sq[warp] = q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ts = 0.0, tm = 0.0, tq = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) ts += ss[w], tm = fmax(tm, sm_[w]), tq += sq[w];
+    part[blockIdx.x] = make_double2(ts, tm);
+    part_q[blockIdx.x] = make_double2(tq, 0.0);
+  }
+}
+// primal residual |A x - rhs|^2 / max (feti.cpp:711-713) by the 9-point stencil, per block; the
+// same pass sums |rhs|^2 (the residual's scale) into part[nblk + blk]
 __global__ void k_stencil_residual_part(int fx, int fy, Stencil9 S, const double2* __restrict__ x,
                                         const double2* __restrict__ rhs, double2* __restrict__ part) {
-  double s = 0.0, m = 0.0;
+  double s = 0.0, m = 0.0, q = 0.0;
   // one row per blockIdx.y, one column per thread: every load of the launch in flight at once
   const int J = blockIdx.y, I = blockIdx.x * blockDim.x + threadIdx.x;
   if (I < fx) {
@@ -2698,11 +2725,14 @@ __global__ void k_stencil_residual_part(int fx, int fy, Stencil9 S, const double
         acc = cfma(S.c[(dy + 1) * 3 + dx + 1], x[(size_t)jj * fx + ii], acc);
       }
     }
-    const double a2 = cabs2(csub(acc, rhs[f]));
+    const double2 b = rhs[f];
+    const double a2 = cabs2(csub(acc, b));
     s += a2;
     m = fmax(m, sqrt(a2));
+    q += cabs2(b);
   }
-  block_sum_max(s, m, part + (size_t)blockIdx.y * gridDim.x);
+  const size_t nblk = (size_t)gridDim.x * gridDim.y;
+  block_sum_max_q(s, m, q, part + (size_t)blockIdx.y * gridDim.x, part + nblk + (size_t)blockIdx.y * gridDim.x);
 }
 
 // Kronecker mass solve V^-1 = (M_y ⊗ M_x ⊗ I_dpn)^-1: batches of identical SPD tridiagonal
@@ -3082,6 +3112,45 @@ __global__ void k_real_to_complex(int n, const double* __restrict__ x, double2* 
   if (k < n) y[k] = make_double2(x[k], 0.0);
 }
 // max |Im t| partials
+// lambda = Re t, u = lambda / phi (control.cpp:318-325) and, in the same pass, the block maxima
+// of |Im t| (imag_leak) and |Re t| (|lambda|_inf of the leak warning): part[blk] = (max|Im|, max|Re|)
+__global__ void __launch_bounds__(256) k_realify_stats(int n, const double2* __restrict__ t, double inv_phi,
+                                                       double* __restrict__ lam, double* __restrict__ u,
+                                                       double2* __restrict__ part) {
+  __shared__ double2 sm[8];
+  double mi = 0.0, mr = 0.0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const double2 v = t[k];
+    lam[k] = v.x;
+    u[k] = v.x * inv_phi;
+    mi = fmax(mi, fabs(v.y));
+    mr = fmax(mr, fabs(v.x));
+  }
+  mi = warp_max(mi);
+  mr = warp_max(mr);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = make_double2(mi, mr);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 m = sm[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = make_double2(fmax(m.x, sm[w].x), fmax(m.y, sm[w].y));
+    part[blockIdx.x] = m;
+  }
+}
+// out[0] = (0, max_b part[b].x), out[1] = (0, max_b part[b].y); one warp
+__global__ void __launch_bounds__(32) k_max2_final(int nblk, const double2* __restrict__ part, double2* __restrict__ out) {
+  double a = 0.0, b = 0.0;
+  for (int k = threadIdx.x; k < nblk; k += 32) {
+    const double2 v = part[k];
+    a = fmax(a, v.x);
+    b = fmax(b, v.y);
+  }
+  a = warp_max(a);
+  b = warp_max(b);
+  if (threadIdx.x == 0) {
+    out[0] = make_double2(0.0, a);
+    out[1] = make_double2(0.0, b);
+  }
+}
 __global__ void k_imag_max_part(int n, const double2* __restrict__ t, double* __restrict__ part) {
   __shared__ double sm[32];
   double m = 0.0;

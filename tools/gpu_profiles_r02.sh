@@ -11,7 +11,7 @@ timeout 1500 python bench.py --config 5 --steps 3 > gpurun_out/f_bench_c5.json 2
 # launch list of the bench command (eager: ncu cannot profile conditional-graph kernel nodes)
 FETIGPU_EAGER=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/f_launches_c2.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-sweep > gpurun_out/f_ncu1.log 2>&1
 # full capture of the per-step kernels (GEMVs, tail) and the setup / elimination kernels
-FETIGPU_EAGER=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sym_gemv|k_arnoldi_tail" --launch-skip 200 -c 3 -o gpurun_out/f_full_c2 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-sweep > gpurun_out/f_ncu2.log 2>&1
+FETIGPU_EAGER=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sym_gemv|k_arnoldi_tail" --launch-skip 200 -c 4 -o gpurun_out/f_full_c2 python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-sweep > gpurun_out/f_ncu2.log 2>&1
 M=gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_tensor_subpipe_dmma.sum,sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum,dram__bytes_read.sum,dram__bytes_write.sum
 timeout 900 ncu --metrics $M --clock-control none -k regex:"k_assemble|k_fdm_solve|k_sym_sweep_inverse|k_schur_bb|k_coupling|k_band_ldlt|k_coarse|k_gauss_jordan|k_pack_sym" -c 16 --csv --log-file gpurun_out/f_fp64_setup_c2.csv python -c "import paper_1312_5653_b200 as F; p=F.make_seeded_problem(1024,1e-4); s=F.SchurSolver(p,32,32,tol=1e-10,max_iter=2000); s.close()" > gpurun_out/f_ncu3.log 2>&1
 # plane strain (no separable solve: banded LDL^T, multi-RHS band solve, Gauss-Jordan in global memory)
