@@ -1805,7 +1805,6 @@ struct Ctx {
     last_dual_of_x = false;
     const double tol = desc.tol;
     const int max_iter = desc.max_iter;
-    zero(x, nl);
     const bool graph = use_graph && !prof && !dist();
     // with the fused step (each kernel returns once the cycle stopped) the first cycle starts
     // from a device-side |b| (statistics slot bslot): no host round trip before the graph
@@ -1813,6 +1812,7 @@ struct Ctx {
     const bool deferred = dev_start && async_ok;
     const int bslot = deferred ? 10 + sb / 4 : 14;
     double bnorm = 0.0;
+    if (!dev_start) zero(x, nl);  // (else by k_gmres_start below)
     if (dev_start) {
       const int blocks = std::max(1, std::min(296, cdiv(std::max(nown, 1), 256)));
       launch(FETIGPU_K_ORTHO, [&] { k_norm_max_part<<<blocks, 256, 0, stream>>>(nown, b + own0, d_part); });
@@ -1824,7 +1824,7 @@ struct Ctx {
         return st;
       }
     }
-    if (d_aside_ctr) {  // coarse beside the dual GEMV: done-counter cleared, partials at the sentinel
+    if (d_aside_ctr && !dev_start) {  // coarse beside the dual GEMV: done-counter cleared, partials at the sentinel
       CU(cudaMemsetAsync(d_aside_ctr, 0, 2 * sizeof(unsigned int), stream));
       CU(cudaMemsetAsync(d_gcp, 0xFF, (size_t)H.n_sub * H.NC * sizeof(double2), stream));
     }
@@ -1834,9 +1834,26 @@ struct Ctx {
       ++launches;
     }
     if (graph && !arnoldi_exec) build_arnoldi_graph();
-    CU(cudaMemcpyAsync(d_r, b, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
     double best_res = 1.0;  // |b - F 0| / |b|
-    CU(cudaMemcpyAsync(d_best, x, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+    if (dev_start) {
+      // x = 0, r = b, best = x, V_0 = b / |b|, the cycle state and the aside resets in one launch
+      GmresState init{};
+      init.j = 0;
+      init.iterations = 0;
+      init.cont = 1;
+      init.max_iter = max_iter;
+      init.m = std::max(1, std::min(max_iter, vcap - 1));
+      init.tol = tol;
+      const int ncnt = std::max(nl, d_aside_ctr ? H.n_sub * H.NC : 0);
+      launch(FETIGPU_K_ORTHO, [&] {
+        k_gmres_start<<<cdiv(std::max(ncnt, 1), 256), 256, 0, stream>>>(nl, b, d_stat + bslot, x, d_r, d_best, d_V, init, d_gst,
+                                                                        d_gvec, d_aside_ctr ? d_gcp : nullptr,
+                                                                        H.n_sub * H.NC, d_aside_ctr);
+      });
+    } else {
+      CU(cudaMemcpyAsync(d_r, b, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+      CU(cudaMemcpyAsync(d_best, x, nl * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+    }
     int iterations = 0;
     double relres = 0;
     bool first = true;
@@ -1854,11 +1871,8 @@ struct Ctx {
         break;
       }
       if (iterations >= max_iter) break;
-      // new cycle: V_0 = r / |r|, g = |r| e_0
-      if (dev_cycle)
-        launch(FETIGPU_K_ORTHO, [&] { k_scale_by_norm<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, d_stat + bslot, d_V); });
-      else
-        launch(FETIGPU_K_ORTHO, [&] { k_scale_copy<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, 1.0 / rnorm, d_V); });
+      // new cycle: V_0 = r / |r|, g = |r| e_0  (the device-driven first cycle: k_gmres_start above)
+      if (!dev_cycle) launch(FETIGPU_K_ORTHO, [&] { k_scale_copy<<<cdiv(nl, 256), 256, 0, stream>>>(nl, d_r, 1.0 / rnorm, d_V); });
       ghost_refresh(d_V);
       // (deferred: a pinned staging slot of its own, the copy may run after the host moved on)
       GmresState* init = deferred ? h_gst_async + 2 + sb / 4 : h_gst;
@@ -1871,10 +1885,8 @@ struct Ctx {
       init->tol = tol;
       init->bnorm = bnorm;
       if (!deferred) *h_gst = *init;
-      CU(cudaMemcpyAsync(d_gst, init, sizeof(GmresState), cudaMemcpyHostToDevice, stream));
-      if (dev_cycle) {
-        launch(FETIGPU_K_ORTHO, [&] { k_gmres_init<<<1, 32, 0, stream>>>(d_gst, d_stat + bslot, d_gvec); });
-      } else {
+      if (!dev_cycle) {
+        CU(cudaMemcpyAsync(d_gst, init, sizeof(GmresState), cudaMemcpyHostToDevice, stream));
         h_pin[0] = make_double2(rnorm, 0.0);
         CU(cudaMemcpyAsync(d_gvec, h_pin, sizeof(double2), cudaMemcpyHostToDevice, stream));
       }
@@ -1887,8 +1899,13 @@ struct Ctx {
         apply_dual(x, d_w);
         last_dual_of_x = true;
         project_aug(d_w);
-        launch(FETIGPU_K_ORTHO, [&] { k_sub<<<cdiv(nown, 256), 256, 0, stream>>>(nown, b + own0, d_w + own0, d_r + own0); });
-        norm_async(d_r + own0, nown, 12 + sb / 4);
+        {  // r = b - F x and its norm partials in one pass
+          const int blocks = std::max(1, std::min(296, cdiv(std::max(nown, 1), 256)));
+          launch(FETIGPU_K_ORTHO, [&] {
+            k_sub_norm_part<<<blocks, 256, 0, stream>>>(nown, b + own0, d_w + own0, d_r + own0, d_part);
+          });
+          launch(FETIGPU_K_OTHER, [&] { k_norm_max_final<<<1, 32, 0, stream>>>(blocks, d_part, d_stat + 12 + sb / 4); });
+        }
         CU(cudaMemcpyAsync(h_gst_async + sb / 4, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
         pending[sb / 4].active = true;
         pending[sb / 4].max_iter = max_iter;

@@ -1883,6 +1883,37 @@ __global__ void k_scale_by_norm(int n, const double2* __restrict__ x, const doub
   const double s2 = nrm2->x;
   if (k < n) y[k] = s2 > 0.0 ? cscale(x[k], 1.0 / sqrt(s2)) : cz();
 }
+// Start of a device-driven first GMRES cycle in ONE launch: x = 0, r = b, best iterate = 0,
+// V_0 = b / |b| (|b|^2 in *nrm2, the expression of k_scale_by_norm), the cycle state (init with
+// bnorm and cont from |b|, as k_gmres_init), g_0 = |b|, and -- with the coarse solve beside the
+// dual GEMV -- its done-counter cleared and the coarse partials at the all-ones sentinel.
+__global__ void k_gmres_start(int n, const double2* __restrict__ b, const double2* __restrict__ nrm2,
+                              double2* __restrict__ x, double2* __restrict__ r, double2* __restrict__ best,
+                              double2* __restrict__ V0, GmresState init, GmresState* __restrict__ st,
+                              double2* __restrict__ g, double2* __restrict__ gcp, int n_gcp,
+                              unsigned int* __restrict__ aside_ctr) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  const double s2 = nrm2->x;
+  if (k < n) {
+    const double2 bb = b[k];
+    x[k] = cz();
+    best[k] = cz();
+    r[k] = bb;
+    V0[k] = s2 > 0.0 ? cscale(bb, 1.0 / sqrt(s2)) : cz();
+  }
+  if (gcp != nullptr && k < n_gcp) {
+    const double ones = __longlong_as_double(-1LL);
+    gcp[k] = make_double2(ones, ones);
+  }
+  if (k == 0) {
+    const double bn = sqrt(s2);
+    init.bnorm = bn;
+    init.cont = bn > 0.0 ? 1 : 0;  // zero rhs: the (fused) step kernels all return at once
+    *st = init;
+    g[0] = make_double2(bn, 0.0);
+    if (aside_ctr != nullptr) aside_ctr[0] = aside_ctr[1] = 0u;
+  }
+}
 __global__ void k_gmres_init(GmresState* __restrict__ st, const double2* __restrict__ nrm2, double2* __restrict__ g) {
   if (threadIdx.x != 0) return;
   const double bn = sqrt(nrm2->x);
@@ -2460,6 +2491,30 @@ __global__ void k_conj(int n, const double2* x, double2* y) {
   if (k < n) y[k] = cconj(x[k]);
 }
 // block-partial |x|^2 and max|x| (abs) -> part2[blk] = (sum, max)
+// y = a - b and, in the same pass, the block partials (sum |y|^2, max |y|) of k_norm_max_part
+// (same grid-stride order: the sums are bit-identical to k_sub followed by k_norm_max_part)
+__global__ void k_sub_norm_part(int n, const double2* __restrict__ a, const double2* __restrict__ b,
+                                double2* __restrict__ y, double2* __restrict__ part) {
+  __shared__ double ssum[32], smax[32];
+  double s = 0.0, m = 0.0;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const double2 v = csub(a[k], b[k]);
+    y[k] = v;
+    const double a2 = cabs2(v);
+    s += a2;
+    m = fmax(m, sqrt(a2));
+  }
+  s = warp_sum(s);
+  m = warp_max(m);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) ssum[warp] = s, smax[warp] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ts = 0.0, tm = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) ts += ssum[w], tm = fmax(tm, smax[w]);
+    part[blockIdx.x] = make_double2(ts, tm);
+  }
+}
 __global__ void k_norm_max_part(int n, const double2* __restrict__ x, double2* __restrict__ part) {
   __shared__ double ssum[32], smax[32];
   double s = 0.0, m = 0.0;
