@@ -219,6 +219,8 @@ struct Ctx {
     if (copy_stream) cudaStreamDestroy(copy_stream);
 
     if (ev_out) cudaEventDestroy(ev_out);
+    for (auto& e : ev_in)
+      if (e) cudaEventDestroy(e);
   }
 
   template <typename T>
@@ -2146,27 +2148,65 @@ struct Ctx {
   // solve_range_space (control.cpp:297-334) on device buffers.
   // host_y/u/lam (host API): results are copied out inside the call — lambda and u on the
   // copy stream as soon as they are final, overlapping the recovery of y
+  // host_ybar (host API): the target is still in host memory; ybar is its device buffer
   void schur_solve(const double* ybar, const double* yc, double* y, double* u, double* lam,
                    fetigpu_schur_stats* out, double* host_y = nullptr, double* host_u = nullptr,
-                   double* host_lam = nullptr) {
+                   double* host_lam = nullptr, const double* host_ybar = nullptr) {
     async_ok = !std::getenv("FETIGPU_NO_DEFER");
     bool ok = false;
     try {
-      ok = schur_solve_once(ybar, yc, y, u, lam, out, host_y, host_u, host_lam);
+      ok = schur_solve_once(ybar, yc, y, u, lam, out, host_y, host_u, host_lam, host_ybar);
     } catch (...) {
       async_ok = false;
       pending[0].active = pending[1].active = false;
       throw;
     }
     async_ok = false;
-    if (!ok) schur_solve_once(ybar, yc, y, u, lam, out, host_y, host_u, host_lam);  // synchronous re-run
+    if (!ok) schur_solve_once(ybar, yc, y, u, lam, out, host_y, host_u, host_lam, nullptr);  // synchronous re-run
+  }
+  static constexpr int kInChunks = 4;  // row blocks of the host target's upload
+  cudaEvent_t ev_in[kInChunks] = {};
+  void ensure_copy_stream() {
+    if (copy_stream) return;
+    CU(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
+    for (auto& e : ev_in) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   bool schur_solve_once(const double* ybar, const double* yc, double* y, double* u, double* lam,
-                        fetigpu_schur_stats* out, double* host_y, double* host_u, double* host_lam) {
+                        fetigpu_schur_stats* out, double* host_y, double* host_u, double* host_lam,
+                        const double* host_ybar) {
     auto t0 = std::chrono::steady_clock::now();
     // rhs = K ybar + Kc yc  (control.cpp:15)
-    apply_global<double>(ybar, (yc && m > 0) ? yc : nullptr, 1.0, 0.0, d_real0);
-    launch(FETIGPU_K_GLOBAL, [&] { k_real_to_complex<<<cdiv(n, 256), 256, 0, stream>>>(n, d_real0, d_rhs); });
+    const bool has_yc = yc && m > 0;
+    if (stencil_ok && !has_yc) {
+      // 9-point stencil straight to the complex rhs.  Host target: uploaded in row blocks on
+      // the copy stream, the stencil of a block starts when the block after it has arrived
+      Stencil9 S9;
+      for (int q = 0; q < 9; ++q) S9.c[q] = d2(cd(1.0) * st_k[q]);
+      const int fx = P.nx - 1, fy = P.ny - 1;
+      const int chunks = host_ybar != nullptr ? std::min(kInChunks, std::max(1, fy / 64)) : 1;
+      if (host_ybar != nullptr) {
+        ensure_copy_stream();
+        for (int c = 0; c < chunks; ++c) {
+          const size_t r0 = (size_t)fy * c / chunks, r1 = (size_t)fy * (c + 1) / chunks;
+          CU(cudaMemcpyAsync(const_cast<double*>(ybar) + r0 * fx, host_ybar + r0 * fx, (r1 - r0) * fx * sizeof(double),
+                             cudaMemcpyHostToDevice, copy_stream));
+          CU(cudaEventRecord(ev_in[c], copy_stream));
+        }
+      }
+      for (int c = 0; c < chunks; ++c) {
+        const int r0 = (int)((size_t)fy * c / chunks), r1 = (int)((size_t)fy * (c + 1) / chunks);
+        if (host_ybar != nullptr) CU(cudaStreamWaitEvent(stream, ev_in[std::min(c + 1, chunks - 1)], 0));
+        launch(FETIGPU_K_GLOBAL, [&] {
+          k_apply_stencil9_rc<<<dim3(cdiv(fx, 128), r1 - r0), 128, 0, stream>>>(fx, fy, r0, S9, ybar, d_rhs);
+        });
+      }
+    } else {
+      if (host_ybar != nullptr)
+        CU(cudaMemcpyAsync(const_cast<double*>(ybar), host_ybar, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+      apply_global<double>(ybar, has_yc ? yc : nullptr, 1.0, 0.0, d_real0);
+      launch(FETIGPU_K_GLOBAL, [&] { k_real_to_complex<<<cdiv(n, 256), 256, 0, stream>>>(n, d_real0, d_rhs); });
+    }
     // a = (K + cV)^-1 rhs
     fetigpu_feti_stats sp = feti_solve(d_rhs, d_x, 0);
     // second factor: (K - cV) t = V a  <=>  t = conj((K + cV)^-1 conj(V a)) = conj(FETI(V conj(a)))
@@ -2179,10 +2219,7 @@ struct Ctx {
     launch(FETIGPU_K_GLOBAL, [&] { k_realify_stats<<<blocks, 256, 0, stream>>>(n, d_x, 1.0 / phi, lam, u, d_part); });
     const size_t nbytes = sizeof(double) * n;
     if (host_lam != nullptr) {
-      if (!copy_stream) {
-        CU(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
-        CU(cudaEventCreateWithFlags(&ev_out, cudaEventDisableTiming));
-      }
+      ensure_copy_stream();
       CU(cudaEventRecord(ev_out, stream));
       CU(cudaStreamWaitEvent(copy_stream, ev_out, 0));
       CU(cudaMemcpyAsync(host_lam, lam, nbytes, cudaMemcpyDeviceToHost, copy_stream));
@@ -2668,8 +2705,6 @@ int fetigpu_schur_solve(fetigpu_ctx* ctx, const double* ybar, const double* yc, 
     if (!ctx) throw ContractError("fetigpu: null context");
     Ctx& c = *ctx->c;
     if (!(c.phi > 0.0)) throw ContractError("build_complex_factors: phi must be positive");
-    const size_t nb = sizeof(double) * c.n;
-    CU(cudaMemcpyAsync(c.d_in_ybar, ybar, nb, cudaMemcpyHostToDevice, c.stream));
     const double* dyc = nullptr;
     if (yc && c.m > 0) {
       CU(cudaMemcpyAsync(c.d_in_yc, yc, sizeof(double) * c.m, cudaMemcpyHostToDevice, c.stream));
@@ -2678,7 +2713,8 @@ int fetigpu_schur_solve(fetigpu_ctx* ctx, const double* ybar, const double* yc, 
     double* dy = c.d_out_y;
     double* du = c.d_out_u;
     double* dl = c.d_out_l;
-    c.schur_solve(c.d_in_ybar, dyc, dy, du, dl, stats, y, u, lambda);  // copies y, u, lambda out
+    // uploads ybar (in row blocks, overlapped with the rhs stencil) and copies y, u, lambda out
+    c.schur_solve(c.d_in_ybar, dyc, dy, du, dl, stats, y, u, lambda, ybar);
     c.prof_collect();
   });
 }

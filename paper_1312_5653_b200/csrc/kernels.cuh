@@ -2698,6 +2698,26 @@ __global__ void k_apply_global(MeshLayout M, ElemKM KM, int n, const int* __rest
 struct Stencil9 {
   double2 c[9];
 };
+// rows [j0, j0 + gridDim.y) of y = stencil x for a REAL x, written as complex (the Schur rhs
+// K ybar, control.cpp:15, row block by row block as ybar arrives from the host)
+__global__ void k_apply_stencil9_rc(int fx, int fy, int j0, Stencil9 S, const double* __restrict__ x,
+                                    double2* __restrict__ y) {
+  const int I = blockIdx.x * blockDim.x + threadIdx.x, J = j0 + blockIdx.y;
+  if (I >= fx) return;
+  double2 acc = cz();
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+    const int jj = J + dy;
+    if (jj < 0 || jj >= fy) continue;
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int ii = I + dx;
+      if (ii < 0 || ii >= fx) continue;
+      acc = cfma(S.c[(dy + 1) * 3 + dx + 1], as_c<double>(x[(size_t)jj * fx + ii]), acc);
+    }
+  }
+  y[(size_t)J * fx + I] = acc;
+}
 template <typename T>
 __global__ void k_apply_stencil9(int fx, int fy, Stencil9 S, const T* __restrict__ x, T* __restrict__ y) {
   const int I = blockIdx.x * blockDim.x + threadIdx.x, J = blockIdx.y;

@@ -16,4 +16,7 @@ M=gpu__time_duration.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_a
 timeout 900 ncu --metrics $M --clock-control none -k regex:"k_assemble|k_fdm_solve|k_sym_sweep_inverse|k_schur_bb|k_coupling|k_band_ldlt|k_coarse|k_gauss_jordan|k_pack_sym" -c 16 --csv --log-file gpurun_out/f_fp64_setup_c2.csv python -c "import paper_1312_5653_b200 as F; p=F.make_seeded_problem(1024,1e-4); s=F.SchurSolver(p,32,32,tol=1e-10,max_iter=2000); s.close()" > gpurun_out/f_ncu3.log 2>&1
 # plane strain (no separable solve: banded LDL^T, multi-RHS band solve, Gauss-Jordan in global memory)
 timeout 900 ncu --metrics $M --clock-control none -k regex:"k_band_ldlt|k_band_solve|k_bt_factor|k_gauss_jordan|k_sym_sweep_inverse" -c 12 --csv --log-file gpurun_out/f_fp64_setup_ps.csv python -c "import paper_1312_5653_b200 as F; p=F.make_cantilever_problem(64,1e-4); s=F.SchurSolver(p,12,4,tol=1e-10,max_iter=2000); s.close()" > gpurun_out/f_ncu4.log 2>&1
+# phase timings: tail phases + the coarse CTAs of the dual GEMV's launch; Schur-solve phases
+FETIGPU_TAIL_TIMES=1 timeout 300 python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-sweep 2>&1 >/dev/null | grep fetigpu | tail -2 > gpurun_out/f_tail_times.txt
+FETIGPU_PHASE_TIMES=1 timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-sweep 2>&1 >/dev/null | grep fetigpu | tail -3 >> gpurun_out/f_tail_times.txt
 echo done > gpurun_out/f_done.txt
