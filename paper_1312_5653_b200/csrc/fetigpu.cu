@@ -1457,8 +1457,14 @@ struct Ctx {
   void eliminate_boundary(const double2* ti, const double2* tb, const double2* fc, bool new_yi) {
     const int S = H.n_sub, NI = H.NI, NB = H.NB;
     if (new_yi) {
-      CU(cudaMemcpyAsync(d_yi, ti, (size_t)S * NI * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
-      interior_solve(d_yi);
+      if (use_fdm) {  // y_i = A_ii^-1 t_i, out of place
+        launch(FETIGPU_K_BAND, [&] {
+          k_fdm_solve<<<H.n_sub, 256, 0, stream>>>(d_yi, (size_t)H.NI, fdm_mx, fdm_my, d_fdm_sx, d_fdm_sy, d_fdm_invd, ti);
+        });
+      } else {
+        CU(cudaMemcpyAsync(d_yi, ti, (size_t)S * NI * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+        interior_solve(d_yi);
+      }
     }
     {
       SymGemvArgs g = sym_args(d_Sinv_p);

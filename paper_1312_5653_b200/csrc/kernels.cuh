@@ -3066,10 +3066,12 @@ constexpr int FDM_LD = 36;  // padded row of a 32 x 32 plane in shared memory
 #endif
 __global__ void __launch_bounds__(256, FETIGPU_FDM_MINB) k_fdm_solve(double2* __restrict__ X, size_t ldx, int mx, int my,
                                                    const double* __restrict__ Sx, const double* __restrict__ Sy,
-                                                   const double2* __restrict__ invD) {
+                                                   const double2* __restrict__ invD,
+                                                   const double2* __restrict__ Xin = nullptr) {
   __shared__ double pre[32 * FDM_LD], pim[32 * FDM_LD], qre[32 * FDM_LD], qim[32 * FDM_LD];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double2* x = X + (size_t)blockIdx.x * ldx;
+  const double2* xin = Xin != nullptr ? Xin + (size_t)blockIdx.x * ldx : x;  // out of place when given
   const int n = mx * my;
   pdl_trigger();
   pdl_wait();
@@ -3078,7 +3080,7 @@ __global__ void __launch_bounds__(256, FETIGPU_FDM_MINB) k_fdm_solve(double2* __
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int e = threadIdx.x + 256 * u, j = e >> 5, i = e & 31;
-      v[u] = (j < my && i < mx) ? x[j * mx + i] : make_double2(0.0, 0.0);
+      v[u] = (j < my && i < mx) ? xin[j * mx + i] : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
