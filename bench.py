@@ -290,6 +290,10 @@ def run_gpu(args):
         return F.make_problem(n_x, n_y, phi, len_x=len_x, len_y=len_y, target="sine", seed=seed)
 
     p = problem(0)
+    # one-time process costs (CUDA module load of the library, stream / event pools) are not
+    # part of the solver's setup: create and drop a small context first
+    if world == 1:
+        F.SchurSolver(F.make_seeded_problem(64, phi, seed=0), 4, 4, tol=TOL, max_iter=50, device=local).close()
     t0 = time.perf_counter()
     if world > 1:  # subdomain-sharded over NCCL; rank 0 makes the NCCL id
         import torch.distributed as dist
