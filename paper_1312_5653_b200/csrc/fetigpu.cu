@@ -163,8 +163,6 @@ struct Ctx {
   const int* span_it = nullptr;  // split path: the preconditioner GEMV's span slot is st->jcol
   bool debug_sync = false;
   bool pdl = true;                      // FETIGPU_NO_PDL=1: plain stream serialisation
-  // FETIGPU_L2PF_KB / FETIGPU_L2PF_AT: per-subdomain bytes of the Dirichlet operator pulled
-  // into L2 by a latency-bound Arnoldi kernel (0 coarse GEMV, 1 CGS pass 1, 2 pass 2, 3 update)
   bool arnoldi_phase = false;
   size_t l2_persist_bytes = 0;
   bool watchdog = false;
