@@ -173,6 +173,10 @@ struct Ctx {
   static constexpr int kCgsThreads = 512, kCgsRows = 256;  // k_cgs_pass block shape
   // fused Arnoldi tail (k_arnoldi_tail): rows per thread (0 = off), grid, barrier words
   int tail_rpt = 0, tail_grid = 0, tail_rb = 1, tail_rows = 512;
+  // multi-row tail (k_arnoldi_tail_mr): more multiplier rows than one per thread of a
+  // co-resident grid; the step's coarse solve then stays in the coarse kernels
+  bool tail_mr = false;
+  static constexpr int kTailRpt = 4;
   // coarse solve beside the dual GEMV (k_sym_gemv_aside): coarse groups of 4 CTAs per launch (0 = off)
   int aside_nx = 0;
   bool tail_pf = false;  // the tail prefetches the head of the preconditioner operator into L2
@@ -579,6 +583,9 @@ struct Ctx {
   // file.  2 (64 registers, so the next GEMV's CTAs could be resident during the tail)
   // measured 152 vs 203 solves/s (spills, and the tail's CTAs packed two per SM).
   static constexpr int kTailMinBlocks = 1;
+  size_t tail_mr_smem() const {
+    return sizeof(double2) * ((size_t)kTailThreads * kTailRpt + 2 * (size_t)kTailHcs + 640);
+  }
   size_t tail_smem() const {
     return sizeof(double2) * ((size_t)std::max(kTailThreads, nc) + 2 * (size_t)kTailHcs + 640 + (size_t)std::max(nc, 0));
   }
@@ -598,8 +605,30 @@ struct Ctx {
     CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kTailThreads, smem));
     // rows per block: spread the rows over every SM (multiple of 32, at most one per thread)
     tail_rows = std::min(kTailThreads, 32 * cdiv(cdiv(std::max(nown, 1), sms), 32));
-    const int grid = std::max(1, cdiv(nown, tail_rows));
-    if (per_sm <= 0 || grid > per_sm * sms) return;
+    int grid = std::max(1, cdiv(nown, tail_rows));
+    if (per_sm <= 0) return;
+    const bool force_mr = std::getenv("FETIGPU_TAIL_MR") != nullptr;  // test hook: few blocks, several rows per thread
+    if (grid > per_sm * sms || force_mr) {
+      // one row per thread does not fit a co-resident grid: up to kTailRpt rows per thread
+      auto kmr = k_arnoldi_tail_mr<kTailThreads, kTailRpt>;
+      const size_t smem_mr = tail_mr_smem();
+      CU(cudaFuncSetAttribute(kmr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mr));
+      int per_sm_mr = 0;
+      CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_mr, kmr, kTailThreads, smem_mr));
+      const int cap = kTailThreads * kTailRpt;
+      tail_rows = force_mr ? cap : std::min(cap, 32 * cdiv(cdiv(std::max(nown, 1), sms), 32));
+      grid = std::max(1, cdiv(nown, tail_rows));
+      if (per_sm_mr <= 0 || grid > per_sm_mr * sms) return;
+      if (!probe_coop_tail(kmr, grid, smem_mr)) return;
+      tail_mr = true;
+      tail_rpt = kTailRpt;
+      tail_grid = grid;
+      d_bar = alloc<unsigned int>(2);
+      CU(cudaMemsetAsync(d_bar, 0, 2 * sizeof(unsigned int), stream));
+      d_hbuf = alloc<double2>((size_t)tail_grid * 2 * (vcap_hint() + 2));
+      if (const char* e = std::getenv("FETIGPU_TAIL_HCS")) tail_hcs = std::max(0, std::min(kTailHcs, std::atoi(e)));
+      return;  // (an L2 prefetch of the next GEMV's head from this tail measured no gain at config 3)
+    }
     if (!probe_coop_tail(kfn, grid, smem)) return;
     tail_rpt = 1;
     tail_grid = grid;
@@ -1367,7 +1396,8 @@ struct Ctx {
     launch(FETIGPU_K_DUAL_GEMV, [&] { launch_sym(g); });
     if (nc > 0 && !fused_tail && !last_cta)
       launch(FETIGPU_K_COARSE, [&] {
-        k_coarse_rhs<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_slots, d_gcp, nullptr, d_g);
+        k_coarse_rhs<<<cdiv(nc, 128), 128, 0, stream>>>(nc, d_corner_slots, d_gcp, nullptr, d_g,
+                                                       (in_arnoldi && tail_mr) ? &d_gst->cont : nullptr);
       });
     allreduce(d_g, nc);
   }
@@ -1389,20 +1419,23 @@ struct Ctx {
   }
   void coarse_gemv() {
     if (nc == 0) return;
+    // in the graph-captured step (multi-row tail) a launch after the cycle stopped returns at once
+    const int* cont = (arnoldi_phase && tail_mr) ? &d_gst->cont : nullptr;
     if (d_Cinv_p != nullptr) {
       const int items = NTc * (NTc - 1) / 2 + NTc;
       launch(FETIGPU_K_COARSE, [&] {
         kx(k_big_sym_gemv, cdiv(items, 4), 128, 0, nc, NTc, (const double2*)d_Cinv_p, (const double2*)d_g,
-           d_cpart_row, d_cpart_col);
+           d_cpart_row, d_cpart_col, cont);
       });
       launch(FETIGPU_K_COARSE, [&] {
-        kx(k_big_sym_reduce, NTc, 256, 0, nc, NTc, (const double2*)d_cpart_row, (const double2*)d_cpart_col, d_z);
+        kx(k_big_sym_reduce, NTc, 256, 0, nc, NTc, (const double2*)d_cpart_row, (const double2*)d_cpart_col, d_z,
+           cont);
       });
       return;
     }
     launch(FETIGPU_K_COARSE, [&] {
       kx(k_coarse_gemv<256>, d_crows ? n_crows : nc, 256, 0, nc, (const double2*)d_Cinv, (const double2*)d_g, d_z,
-         (const int*)d_crows);
+         (const int*)d_crows, cont);
     });
   }
   // u_b = u1_b - cpl_b z gathered onto the owned multiplier rows: out = -B u  (feti.cpp:593)
@@ -1612,7 +1645,12 @@ struct Ctx {
       launch(FETIGPU_K_DUAL_GEMV,
              [&] { kx(k_sym_gemv_aside<8, 4>, H.n_sub + 4 * aside_nx, 128, sym_smem(), g, ca); });
     } else {
-      dual_gemv(g, tail_rpt > 0);
+      dual_gemv(g, tail_rpt > 0 && !tail_mr);  // (the one-row fused tail assembles g itself)
+      if (tail_mr) {  // multi-row tail: z from the coarse kernels
+        arnoldi_phase = true;
+        coarse_gemv();
+        arnoldi_phase = false;
+      }
     }
   }
   static constexpr int kLagSteps = 4;  // sharded cycle: steps per host check of the state
@@ -1707,7 +1745,9 @@ struct Ctx {
       t.zpart = d_zpart;
       t.blk_corners = d_blk_corners;
       launch(FETIGPU_K_ORTHO, [&] {
-        if (aside_nx > 0)
+        if (tail_mr)
+          kx_coop(k_arnoldi_tail_mr<kTailThreads, kTailRpt>, tail_grid, kTailThreads, tail_mr_smem(), t);
+        else if (aside_nx > 0)
           kx_coop(k_arnoldi_tail<kTailThreads, 4, kTailMinBlocks, true>, tail_grid, kTailThreads, tail_smem(), t);
         else
           kx_coop(k_arnoldi_tail<kTailThreads, 4, kTailMinBlocks, false>, tail_grid, kTailThreads, tail_smem(), t);

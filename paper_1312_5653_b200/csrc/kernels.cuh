@@ -953,9 +953,11 @@ __global__ void k_lam_gather_pre(int nl, const int* __restrict__ lo, const int* 
 
 // g[c] = fc[c] - sum_slots gcp[slot]   (feti.cpp:523-538, subdomains ascending)
 __global__ void k_coarse_rhs(int nc, const int* __restrict__ corner_slots, const double2* __restrict__ gcp,
-                             const double2* __restrict__ fc, double2* __restrict__ g) {
+                             const double2* __restrict__ fc, double2* __restrict__ g,
+                             const int* __restrict__ cont_ptr = nullptr) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nc) return;
+  if (cont_ptr != nullptr && *cont_ptr == 0) return;  // a step after the cycle stopped
   double2 acc = fc ? fc[c] : cz();
   for (int q = 0; q < 4; ++q) {
     const int slot = corner_slots[c * 4 + q];
@@ -973,12 +975,13 @@ __global__ void k_coarse_rhs(int nc, const int* __restrict__ corner_slots, const
 template <int THREADS>
 __global__ void __launch_bounds__(THREADS)
     k_coarse_gemv(int nc, const double2* __restrict__ Cinv, const double2* __restrict__ g, double2* __restrict__ z,
-                  const int* __restrict__ rows = nullptr) {
+                  const int* __restrict__ rows = nullptr, const int* __restrict__ cont_ptr = nullptr) {
   constexpr int WARPS = THREADS / 32;
   __shared__ double2 red[WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   pdl_trigger();
   pdl_wait();
+  if (cont_ptr != nullptr && *cont_ptr == 0) return;  // a step after the cycle stopped
   const int row = blockIdx.x;
   const double2* cr = Cinv + (size_t)row * nc;
   double2 a = cz();
@@ -1000,13 +1003,15 @@ __global__ void __launch_bounds__(THREADS)
 // partials, as k_sym_gemv); kernel 2: fixed-order combination per 32-row block.
 __global__ void __launch_bounds__(128) k_big_sym_gemv(int nc, int NT, const double2* __restrict__ pack,
                                                       const double2* __restrict__ x, double2* __restrict__ part_row,
-                                                      double2* __restrict__ part_col) {
+                                                      double2* __restrict__ part_col,
+                                                      const int* __restrict__ cont_ptr = nullptr) {
   __shared__ double2 xs[4][2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int noff = NT * (NT - 1) / 2, items = noff + NT;
   const int t = blockIdx.x * 4 + warp;
   pdl_trigger();
   pdl_wait();
+  if (cont_ptr != nullptr && *cont_ptr == 0) return;  // a step after the cycle stopped
   if (t >= items) return;
   double2* xI = xs[warp][0];
   double2* xJ = xs[warp][1];
@@ -1067,12 +1072,14 @@ __global__ void __launch_bounds__(128) k_big_sym_gemv(int nc, int NT, const doub
 // y_I = diag(I) + sum_{J<I} rows(I,J) + sum_{I'>I} cols(I',I): one CTA per row block I, 8
 // warps over the partial tiles (fixed assignment and order), then the 8 sums in order
 __global__ void __launch_bounds__(256) k_big_sym_reduce(int nc, int NT, const double2* __restrict__ part_row,
-                                                        const double2* __restrict__ part_col, double2* __restrict__ z) {
+                                                        const double2* __restrict__ part_col, double2* __restrict__ z,
+                                                        const int* __restrict__ cont_ptr = nullptr) {
   __shared__ double2 red[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, I = blockIdx.x;
   const int noff = NT * (NT - 1) / 2;
   pdl_trigger();
   pdl_wait();
+  if (cont_ptr != nullptr && *cont_ptr == 0) return;  // a step after the cycle stopped
   double2 acc = cz();
   for (int J = warp; J < I; J += 8) acc = cadd(acc, part_row[((size_t)I * (I - 1) / 2 + J) * 32 + lane]);
   for (int I2 = I + 1 + warp; I2 < NT; I2 += 8) acc = cadd(acc, part_col[((size_t)I2 * (I2 - 1) / 2 + I) * 32 + lane]);
@@ -2470,6 +2477,127 @@ __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs 
     const double ones = __longlong_as_double(-1LL);
     for (int i = blockIdx.x * THREADS + threadIdx.x; i < a.n_gcp; i += G * THREADS)
       __stcg(const_cast<double2*>(a.gcp) + i, make_double2(ones, ones));
+  }
+  if (a.span != nullptr) {
+    __syncthreads();
+    span_mark(a.span, &it, 2, 1);
+  }
+}
+
+// Multi-row form of the fused tail for interfaces with more multiplier rows than one row per
+// thread of a co-resident grid (n > SMs x THREADS; BASELINE config 3: 250k rows): every thread
+// carries up to RPT rows (row0 + threadIdx.x + q THREADS), the coarse solve z = C^-1 g has
+// already been computed by the coarse kernels of the step (large coarse spaces use the packed
+// symmetric inverse), and the launch is CGS2 pass 1 (+ dual-tail gather), pass 2 and the
+// normalisation with two grid barriers.  dynamic smem: w_sh[THREADS RPT] | h1[kTailHcs] |
+// h2[kTailHcs] | Givens staging[640].  Same reduction order as k_arnoldi_tail (block partials
+// in block order), same Givens / split-Givens protocol.
+template <int THREADS, int RPT>
+__global__ void __launch_bounds__(THREADS, 1) k_arnoldi_tail_mr(ArnoldiTailArgs a) {
+  constexpr int WARPS = THREADS / 32, ROWS = THREADS * RPT, DB = 16;
+  extern __shared__ double2 tail_sh[];
+  double2* w_sh = tail_sh;
+  double2* hs1s = w_sh + ROWS;
+  double2* hs2s = hs1s + kTailHcs;
+  double2* stage = hs2s + kTailHcs;
+  __shared__ double inv_sh;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = blockIdx.x * a.rows_pb;
+  const int row_end = min(a.n, row0 + a.rows_pb);  // exclusive
+  const int nrows = max(row_end - row0, 0);
+  pdl_trigger();
+  pdl_wait();
+  if (a.st->cont == 0) {
+    if (a.ga.in_graph && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.ga.handle, 0u);
+    return;
+  }
+  const int nv = a.st->j + 1, nout = nv + 1, G = gridDim.x;
+  const int it = a.st->iterations;
+  double2* hs1 = nout <= a.hcs ? hs1s : a.hbuf + (size_t)blockIdx.x * 2 * a.hcap;
+  double2* hs2 = nout <= a.hcs ? hs2s : hs1 + a.hcap;
+  span_mark(a.span, &it, 2, 0);
+  auto dots = [&](const double2* w, double2* part) {
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) w_sh[threadIdx.x + q * THREADS] = w[q];  // (zero beyond the block's rows)
+    __syncthreads();
+    for (int i = warp; i < nout; i += WARPS) {
+      double2 acc = cz();
+      if (i < nv) {
+        const double2* v = a.V + (size_t)i * a.ldv + row0;
+        for (int k0 = lane; k0 < nrows; k0 += 32 * DB) {
+          double2 x[DB];
+#pragma unroll
+          for (int u = 0; u < DB; ++u) x[u] = v[min(k0 + 32 * u, nrows - 1)];
+#pragma unroll
+          for (int u = 0; u < DB; ++u)
+            if (k0 + 32 * u < nrows) acc = cfma_conj(x[u], w_sh[k0 + 32 * u], acc);
+        }
+      } else {
+        for (int k0 = lane; k0 < nrows; k0 += 32) acc.x += cabs2(w_sh[k0]);
+      }
+      acc = warp_sum2(acc);
+      if (lane == 0) part[(size_t)i * G + blockIdx.x] = acc;
+    }
+  };
+  auto sub_vh = [&](double2 w, int r, const double2* h) {  // w - sum_i h_i V_i[r]
+    double2 acc = cz();
+    int i = 0;
+    for (; i + 8 <= nv; i += 8) {
+      double2 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = a.V[(size_t)(i + u) * a.ldv + r];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = cfma(h[i + u], v[u], acc);
+    }
+    for (; i < nv; ++i) acc = cfma(h[i], a.V[(size_t)i * a.ldv + r], acc);
+    return csub(w, acc);
+  };
+  // ---- phase 1: w = F z (dual tail), h1 = V^H w, |w|^2 ----
+  double2 w[RPT];
+  bool act[RPT];
+#pragma unroll
+  for (int q = 0; q < RPT; ++q) {
+    const int lr = threadIdx.x + q * THREADS;
+    act[q] = lr < nrows;
+    w[q] = act[q] ? dual_tail_row(a, row0 + lr, true) : cz();
+  }
+  dots(w, a.part);
+  grid_sync_plain(a.bar);
+  block_reduce_parts<THREADS>(a.part, G, nout, hs1);
+  // ---- phase 2: w -= V h1, h2 = V^H w, |w|^2 ----
+#pragma unroll
+  for (int q = 0; q < RPT; ++q)
+    if (act[q]) w[q] = sub_vh(w[q], row0 + threadIdx.x + q * THREADS, hs1);
+  __syncthreads();  // w_sh reuse
+  double2* part2 = a.part + (size_t)a.hcap * G;
+  dots(w, part2);
+  grid_sync_plain(a.bar);
+  block_reduce_parts<THREADS>(part2, G, nout, hs2);
+  if (warp == 0) {
+    bool finite;
+    const double hn = warp_hnext<true>(hs1, hs2, nv - 1, finite);
+    if (lane == 0) inv_sh = 1.0 / hn;
+  }
+  __syncthreads();
+  // ---- phase 3: V_{j+1} = (w - V h2) / h_{j+1,j} ----
+  if (nv < a.vcap) {
+#pragma unroll
+    for (int q = 0; q < RPT; ++q)
+      if (act[q]) {
+        const int r = row0 + threadIdx.x + q * THREADS;
+        a.V[(size_t)nv * a.ldv + r] = cscale(sub_vh(w[q], r, hs2), inv_sh);
+      }
+  }
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < nout; i += THREADS) {
+      a.h1[i] = hs1[i];
+      a.h2[i] = hs2[i];
+    }
+    if (a.split_givens) {
+      if (threadIdx.x == 0) a.st->jcol = nv;
+    } else if (warp == 0) {
+      givens_warp<true>(a.ga, reinterpret_cast<double*>(stage), stage + 128, stage + 384, hs1, hs2);
+    }
   }
   if (a.span != nullptr) {
     __syncthreads();

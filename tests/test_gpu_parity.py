@@ -310,7 +310,7 @@ def test_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
                                     "FETIGPU_NO_DEFER", "FETIGPU_NO_SPLIT", "FETIGPU_NO_FDM",
                                     "FETIGPU_COOP_REJECT", "FETIGPU_NO_FUSED_TAIL", "FETIGPU_NO_PDL",
                                     "FETIGPU_EAGER", "FETIGPU_NO_AIC", "FETIGPU_NO_STENCIL", "FETIGPU_NO_BT",
-                                    "FETIGPU_NO_ASIDE", "FETIGPU_ASIDE_GIVEUP", "FETIGPU_NO_TAIL_PF", "FETIGPU_TAIL_HCS"])
+                                    "FETIGPU_NO_ASIDE", "FETIGPU_ASIDE_GIVEUP", "FETIGPU_NO_TAIL_PF", "FETIGPU_TAIL_HCS", "FETIGPU_TAIL_MR"])
 def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
     """Each reuse/fusion of the solve path (preconditioned basis Z, compact interior rhs,
     GEMV-free final elimination, deferred GMRES completion, Givens folded into the next
@@ -318,8 +318,9 @@ def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
     cooperative-launch probe act as rejected, as under an MPS SM limit, so the step falls
     back to the multi-launch tail; the coarse solve beside the dual GEMV -- FETIGPU_NO_ASIDE
     keeps it in the tail, FETIGPU_ASIDE_GIVEUP makes the coarse CTAs miss their arrivals and
-    give up, so the tail computes z itself) against the plain path it replaces: same
-    iterations, results equal to rounding."""
+    give up, so the tail computes z itself; FETIGPU_TAIL_MR forces the multi-row tail that
+    large interfaces use) against the plain path it replaces: same iterations, results equal
+    to rounding."""
     p = fetigpu.make_seeded_problem(128, 1e-4, seed=3)
     solver = fetigpu.SchurSolver(p, 8, 8, tol=1e-10)
     a = solver.solve()
