@@ -1942,17 +1942,18 @@ __global__ void __launch_bounds__(ROWS* GROUPS) k_combine(int n, const double2* 
   if (combine_rows<ROWS, GROUPS>(y, V, ldv, n, st->k, r, sum)) t[r] = sum;
 }
 // ---------------------------------------------------------------------------------------
-// Fused Arnoldi tail (one GPU): coarse solve z = C^-1 g, CGS pass 1 (dual-operator tail
-// gathered per row, h1 = V^H w, |w|^2), CGS pass 2 (w -= V h1, h2 = V^H w, |w|^2), Givens
-// and V_{j+1} = (w - V h2) / h_{j+1,j}, in ONE launch.  The three data dependences are grid
-// barriers whose last arriving block performs the reduction (fixed order: deterministic)
-// before releasing the others.  Each thread keeps its RPT multiplier rows of w in
-// registers across the phases and re-reads its V rows from L1.  All blocks must be
-// co-resident (the host sizes RPT from the occupancy API); a barrier that does not complete
-// within ~2 s traps instead of hanging.
+// Fused Arnoldi tail (one GPU): coarse solve z = C^-1 g (unless it ran beside the dual GEMV:
+// ASIDE), CGS pass 1 (dual-operator tail gathered per row, h1 = V^H w, |w|^2), CGS pass 2
+// (w -= V h1, h2 = V^H w, |w|^2), Givens and V_{j+1} = (w - V h2) / h_{j+1,j}, in ONE launch.
+// The data dependences are grid barriers (grid_sync_plain) after which every block reduces
+// the block partials in block order (deterministic, identical in all blocks).  Each thread
+// keeps its multiplier row(s) of w in registers across the phases and re-reads its V rows from
+// L1.  All blocks are co-resident by construction (cooperative launch, probed at setup); a
+// barrier that does not complete within ~2 s traps instead of hanging.
+// k_arnoldi_tail: one row per thread; k_arnoldi_tail_mr: up to RPT rows per thread.
 struct ArnoldiTailArgs {
   int n;        // multiplier rows
-  int rows_pb;  // rows per block (<= THREADS)
+  int rows_pb;  // rows per block (<= THREADS; k_arnoldi_tail_mr: <= THREADS RPT)
   double2* V;
   size_t ldv;
   GmresState* st;
@@ -2199,9 +2200,8 @@ __device__ __forceinline__ void block_reduce_parts(const double2* __restrict__ p
 // dynamic smem: w_sh / g_sh [wg = max(THREADS, nc)] | h1[kTailHcs] | h2[kTailHcs] | Givens
 // staging[640] | z_sh[nc] (ASIDE).  The dot vectors h1 / h2 (nv + 1 entries) live in shared
 // memory while they fit kTailHcs entries and in a per-block global scratch beyond (long
-// cycles): the tail's footprint does not grow with max_iter, so it stays within the shared-
-// memory carve-out of the GEMVs around it (a 129 KB tail between 90 KB GEMVs measured +2 %
-// step time).
+// cycles): the tail's footprint does not grow with max_iter (it used to: the fused tail was
+// then unavailable for small and for very large max_iter).
 template <int THREADS, int NCM, int MINB, bool ASIDE>
 __global__ void __launch_bounds__(THREADS, MINB) k_arnoldi_tail(ArnoldiTailArgs a) {
   constexpr int WARPS = THREADS / 32, LPR = THREADS / 32;
