@@ -444,7 +444,11 @@ def run_gpu(args):
                                 "launches of the kernel (average launch duration incl. the PDL gaps)" if graph_ms else
                                 "CUDA events around each eager launch of the profiling pass"),
                      "eager_avg_launch_ms": eager_ms, "eager_frac": kb / (eager_ms / 1000.0) / 1e9 / hbm_peak,
-                     "in_graph": in_graph},
+                     "in_graph": in_graph,
+                     "note": ("bytes_per_launch = the GEMV's operands only; at config 2 the dual GEMV's launch "
+                              "(k_sym_gemv_aside) also holds the coarse CTAs of the step's coarse solve, whose "
+                              "14.8 MB read of C^-1 (L2-resident in the solve, cold under ncu) is part of `traffic` "
+                              "but not of bytes_per_launch (DESIGN.md section 4)") if kclass == "dual_gemv" else None},
         "clocks": clk.summary(),
     }
     line["solve_roofline"] = solve_roofline(solver, prof, steps, t_max / steps * 1000.0, hbm_peak)
