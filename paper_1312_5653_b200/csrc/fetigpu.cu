@@ -137,7 +137,9 @@ struct Ctx {
   static constexpr int kStatSlots = 16;
   double2 *d_stat = nullptr, *h_stat = nullptr;
   size_t ldv = 0;
-  int vcap = 0;  // basis vectors allocated
+  int vcap = 0;  // Krylov capacity (max_iter + 1): Hessenberg, rotations, dot vectors
+  int bcap = 0;  // basis vectors allocated in V / Z (<= vcap; grows on demand, grow_basis)
+  static constexpr int kBasis0 = 128;  // initial basis capacity (one GPU)
   GmresState* d_gst = nullptr;
   GmresState* h_gst = nullptr;
   // deferred completion (schur_solve on the one-GPU graph path): each FETI solve's GMRES
@@ -1082,9 +1084,18 @@ struct Ctx {
     zero(d_z, std::max(nc, 1));
     ldv = ((size_t)nl + 63) / 64 * 64;
     vcap = std::max(2, desc.max_iter + 1);
-    d_V = alloc<double2>(ldv * vcap);
+    // The bases start at kBasis0 vectors (FETI-DP cycles are tens of steps; max_iter = 2000
+    // would be 2 x 2 GB at config 2) and grow when a cycle reaches the capacity: the cycle is
+    // then CONTINUED on the larger basis, not restarted (feti.cpp:684: unrestarted GMRES).
+    bcap = vcap;
+    if (!dist()) {
+      int b0 = kBasis0;
+      if (const char* e = std::getenv("FETIGPU_BASIS0")) b0 = std::max(2, std::atoi(e));  // test hook
+      bcap = std::min(vcap, b0);
+    }
+    d_V = alloc<double2>(ldv * bcap);
     // preconditioned basis (one GPU: every row's +1 slot is local) — FGMRES-form update
-    if (!dist() && !std::getenv("FETIGPU_NO_ZBASIS")) d_Z = alloc<double2>(ldv * vcap);
+    if (!dist() && !std::getenv("FETIGPU_NO_ZBASIS")) d_Z = alloc<double2>(ldv * bcap);
     d_w = alloc<double2>(ldv);
     d_zl = alloc<double2>(ldv);
     d_t = alloc<double2>(ldv);
@@ -1729,7 +1740,7 @@ struct Ctx {
       t.tstamp = d_tstamp;
       t.span = d_span;
       t.hcap = vcap + 2;
-      t.vcap = vcap;
+      t.vcap = bcap;
       t.aside_ctr = aside_nx > 0 ? d_aside_ctr : nullptr;
       t.aside_nx = (unsigned int)aside_nx;
       t.n_gcp = H.n_sub * H.NC;
@@ -1819,6 +1830,29 @@ struct Ctx {
          (const double2*)(d_w + own0), d_V + own0, ldv);
     });
   }
+  // Larger Krylov bases (the first `keep` vectors carried over); the Arnoldi graph holds the
+  // basis pointers, so it is rebuilt.
+  void grow_basis(int keep) {
+    const int ncap = std::min(vcap, std::max(4 * bcap, keep + 2));
+    auto regrow = [&](double2*& p) {
+      double2* q = alloc<double2>(ldv * ncap);
+      CU(cudaMemcpyAsync(q, p, ldv * (size_t)std::min(keep, bcap) * sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+      sync();
+      cudaFree(p);
+      allocs.erase(std::find(allocs.begin(), allocs.end(), (void*)p));
+      p = q;
+    };
+    regrow(d_V);
+    if (d_Z != nullptr) regrow(d_Z);
+    bcap = ncap;
+    if (arnoldi_exec) {
+      cudaGraphExecDestroy(arnoldi_exec);
+      arnoldi_exec = nullptr;
+      cudaGraphDestroy(arnoldi_graph);
+      arnoldi_graph = nullptr;
+      build_arnoldi_graph();
+    }
+  }
   void build_arnoldi_graph() {
     CU(cudaGraphCreate(&arnoldi_graph, 0));
     CU(cudaGraphConditionalHandleCreate(&arnoldi_handle, arnoldi_graph, 1, cudaGraphCondAssignDefault));
@@ -1888,7 +1922,7 @@ struct Ctx {
       init.iterations = 0;
       init.cont = 1;
       init.max_iter = max_iter;
-      init.m = std::max(1, std::min(max_iter, vcap - 1));
+      init.m = std::max(1, std::min(max_iter, bcap - 1));
       init.tol = tol;
       const int ncnt = std::max(nl, d_aside_ctr ? H.n_sub * H.NC : 0);
       launch(FETIGPU_K_ORTHO, [&] {
@@ -1927,7 +1961,7 @@ struct Ctx {
       init->iterations = iterations;
       init->cont = 1;
       init->max_iter = max_iter;
-      init->m = std::max(1, std::min(max_iter, vcap - 1));
+      init->m = std::max(1, std::min(max_iter, bcap - 1));
       init->tol = tol;
       init->bnorm = bnorm;
       if (!deferred) *h_gst = *init;
@@ -1958,6 +1992,7 @@ struct Ctx {
         pending[sb / 4].tol = tol;
         return st;  // iterations / residual filled in by finish_deferred
       }
+      for (;;) {  // (repeats only when the cycle is continued on a larger basis, below)
       if (graph) {
         CU(cudaGraphLaunch(arnoldi_exec, stream));
         CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
@@ -2015,6 +2050,20 @@ struct Ctx {
           CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
           sync();
         } while (h_gst->cont);
+      }
+      // The cycle stopped because the basis is full (not converged by the Arnoldi estimate, no
+      // breakdown, iterations left): allocate a larger basis and CONTINUE the same cycle at
+      // column k -- the reference's GMRES is unrestarted (feti.cpp:684), a restart here would
+      // change the iteration.
+      const bool full = !dist() && bcap < vcap && h_gst->status == 0 && h_gst->cont == 0 && h_gst->k >= h_gst->m &&
+                        h_gst->m < max_iter && h_gst->iterations < max_iter && h_gst->est > tol * h_gst->bnorm;
+      if (!full) break;
+      grow_basis(h_gst->k + 1);
+      h_gst->m = std::max(1, std::min(max_iter, bcap - 1));
+      h_gst->j = h_gst->k;
+      h_gst->jcol = h_gst->k;
+      h_gst->cont = 1;
+      CU(cudaMemcpyAsync(d_gst, h_gst, sizeof(GmresState), cudaMemcpyHostToDevice, stream));
       }
       phase("cycle");
       if (h_gst->status) throw NumericalError("gmres: breakdown (NaN/Inf in Arnoldi)");

@@ -310,7 +310,8 @@ def test_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
                                     "FETIGPU_NO_DEFER", "FETIGPU_NO_SPLIT", "FETIGPU_NO_FDM",
                                     "FETIGPU_COOP_REJECT", "FETIGPU_NO_FUSED_TAIL", "FETIGPU_NO_PDL",
                                     "FETIGPU_EAGER", "FETIGPU_NO_AIC", "FETIGPU_NO_STENCIL", "FETIGPU_NO_BT",
-                                    "FETIGPU_NO_ASIDE", "FETIGPU_ASIDE_GIVEUP", "FETIGPU_NO_TAIL_PF", "FETIGPU_TAIL_HCS", "FETIGPU_TAIL_MR"])
+                                    "FETIGPU_NO_ASIDE", "FETIGPU_ASIDE_GIVEUP", "FETIGPU_NO_TAIL_PF", "FETIGPU_TAIL_HCS", "FETIGPU_TAIL_MR", "FETIGPU_BASIS0",
+                                    "FETIGPU_BASIS0+FETIGPU_EAGER", "FETIGPU_BASIS0+FETIGPU_NO_DEFER"])
 def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
     """Each reuse/fusion of the solve path (preconditioned basis Z, compact interior rhs,
     GEMV-free final elimination, deferred GMRES completion, Givens folded into the next
@@ -319,13 +320,15 @@ def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
     back to the multi-launch tail; the coarse solve beside the dual GEMV -- FETIGPU_NO_ASIDE
     keeps it in the tail, FETIGPU_ASIDE_GIVEUP makes the coarse CTAs miss their arrivals and
     give up, so the tail computes z itself; FETIGPU_TAIL_MR forces the multi-row tail that
-    large interfaces use) against the plain path it replaces: same iterations, results equal
-    to rounding."""
+    large interfaces use; FETIGPU_BASIS0 starts with a Krylov basis of 4 vectors, so every cycle
+    is continued several times on a larger basis -- bitwise the same iteration) against the
+    plain path it replaces: same iterations, results equal to rounding."""
     p = fetigpu.make_seeded_problem(128, 1e-4, seed=3)
     solver = fetigpu.SchurSolver(p, 8, 8, tol=1e-10)
     a = solver.solve()
     solver.close()
-    monkeypatch.setenv(switch, "4" if switch == "FETIGPU_TAIL_HCS" else "1")  # HCS: dot vectors beyond 4 entries in global scratch
+    for sw in switch.split("+"):  # HCS: dot vectors beyond 4 entries in global scratch; BASIS0: 4 basis vectors
+        monkeypatch.setenv(sw, "4" if sw in ("FETIGPU_TAIL_HCS", "FETIGPU_BASIS0") else "1")
     solver = fetigpu.SchurSolver(p, 8, 8, tol=1e-10)
     b = solver.solve()
     solver.close()
@@ -333,6 +336,8 @@ def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
         assert a[side]["iterations"] == b[side]["iterations"]
     for k in ("y", "u", "lambda"):
         assert rel(a[k], b[k]) <= 1e-11, k
+        if switch == "FETIGPU_BASIS0":  # the continued cycle is the same arithmetic
+            assert np.array_equal(a[k], b[k]), k
 
 
 @pytest.mark.parametrize("n,s", [(36, 4), (40, 4), (66, 3)])
