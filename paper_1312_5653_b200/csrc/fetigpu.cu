@@ -592,8 +592,10 @@ struct Ctx {
     return sizeof(double2) * ((size_t)std::max(kTailThreads, nc) + 2 * (size_t)kTailHcs + 640 + (size_t)std::max(nc, 0));
   }
   void setup_fused_tail() {
-    if (dist() || H.NC > 4 || H.n_aug > 0 || std::getenv("FETIGPU_NO_FUSED_TAIL"))
-      return;
+    // edge-RBM augmentation (more than 4 local coarse unknowns, projected dual problem): the
+    // multi-row tail on an already projected w, when the per-edge gather / projection applies
+    const bool aug = H.n_aug > 0;
+    if (dist() || std::getenv("FETIGPU_NO_FUSED_TAIL") || (aug ? !edge_gather_ok : H.NC > 4)) return;
     const size_t smem = tail_smem();
     if (smem > 200 * 1024) return;
     int sms = 0, per_sm = 0, coop = 0;
@@ -610,7 +612,7 @@ struct Ctx {
     int grid = std::max(1, cdiv(nown, tail_rows));
     if (per_sm <= 0) return;
     const bool force_mr = std::getenv("FETIGPU_TAIL_MR") != nullptr;  // test hook: few blocks, several rows per thread
-    if (grid > per_sm * sms || force_mr) {
+    if (grid > per_sm * sms || force_mr || aug) {
       // one row per thread does not fit a co-resident grid: up to kTailRpt rows per thread
       auto kmr = k_arnoldi_tail_mr<kTailThreads, kTailRpt>;
       const size_t smem_mr = tail_mr_smem();
@@ -1741,6 +1743,12 @@ struct Ctx {
       t.span = d_span;
       t.hcap = vcap + 2;
       t.vcap = bcap;
+      if (tail_mr && H.n_aug > 0) {  // augmented: w = P F z, gathered and projected per edge
+        EdgeGatherArgs ea{H.n_edges, H.NB, H.NC, d_col_ptr, d_col_rows, d_col_vals, d_lam_lo, d_lam_hi,
+                          d_cglob, d_u1b, d_cpl_b, d_z, d_w, &d_gst->cont};
+        launch(FETIGPU_K_LAMBDA, [&] { k_gather_project_edges<<<cdiv(H.n_edges, 8), 256, 0, stream>>>(ea); });
+        t.w_in = d_w;
+      }
       t.aside_ctr = aside_nx > 0 ? d_aside_ctr : nullptr;
       t.aside_nx = (unsigned int)aside_nx;
       t.n_gcp = H.n_sub * H.NC;
@@ -1790,7 +1798,7 @@ struct Ctx {
     if (H.n_aug > 0) {  // augmented: w = P F z, gathered and projected before the dots
       if (edge_gather_ok) {
         EdgeGatherArgs ea{H.n_edges, H.NB, H.NC, d_col_ptr, d_col_rows, d_col_vals, d_lam_lo, d_lam_hi,
-                          d_cglob, d_u1b, d_cpl_b, d_z, d_w};
+                          d_cglob, d_u1b, d_cpl_b, d_z, d_w, nullptr};
         launch(FETIGPU_K_LAMBDA, [&] { k_gather_project_edges<<<cdiv(H.n_edges, 8), 256, 0, stream>>>(ea); });
       } else {
         launch(FETIGPU_K_LAMBDA, [&] {

@@ -1783,11 +1783,13 @@ struct EdgeGatherArgs {
   const int *lam_lo, *lam_hi, *cglob;
   const double2 *u1b, *cpl_b, *z;
   double2* w;
+  const int* cont_ptr;  // graph-captured step: a launch after the cycle stopped returns at once
 };
 __global__ void k_gather_project_edges(EdgeGatherArgs a) {
   constexpr int MAXR = 4;  // up to 128 rows per edge
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (e >= a.n_edges) return;
+  if (a.cont_ptr != nullptr && *a.cont_ptr == 0) return;
   const int q0 = a.col_ptr[e], len = a.col_ptr[e + 1] - q0;
   double2 w[MAXR];
   double qv[MAXR];
@@ -1994,6 +1996,7 @@ struct ArnoldiTailArgs {
   int wg;                   // entries of the w / g staging region: max(THREADS, nc)
   int hcs;                  // dot-vector entries that use shared memory (<= kTailHcs; test hook: smaller)
   double2* hbuf;            // [grid][2][hcap] dot vectors of long cycles (nv + 1 > kTailHcs)
+  const double2* w_in;      // k_arnoldi_tail_mr, optional: w already formed (augmented: projected)
   const double2* zpart;     // [nc][aside_nx] partial coarse solutions
   const int* blk_corners;   // [grid][kTailCorners] corners the block's rows touch (-1 pad)
 };
@@ -2559,7 +2562,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_arnoldi_tail_mr(ArnoldiTailArgs 
   for (int q = 0; q < RPT; ++q) {
     const int lr = threadIdx.x + q * THREADS;
     act[q] = lr < nrows;
-    w[q] = act[q] ? dual_tail_row(a, row0 + lr, true) : cz();
+    // augmented dual problem: w = P F z was gathered and projected per edge (k_gather_project_edges)
+    w[q] = !act[q] ? cz() : a.w_in != nullptr ? a.w_in[row0 + lr] : dual_tail_row(a, row0 + lr, true);
   }
   dots(w, a.part);
   grid_sync_plain(a.bar);
