@@ -595,7 +595,9 @@ struct Ctx {
     // edge-RBM augmentation (more than 4 local coarse unknowns, projected dual problem): the
     // multi-row tail on an already projected w, when the per-edge gather / projection applies
     const bool aug = H.n_aug > 0;
-    if (dist() || std::getenv("FETIGPU_NO_FUSED_TAIL") || (aug ? !edge_gather_ok : H.NC > 4)) return;
+    // (more than 4 local coarse unknowns without augmentation -- plane strain: 2 dofs per corner --
+    // also take the multi-row tail, whose dual-tail gather loops over any NC)
+    if (dist() || std::getenv("FETIGPU_NO_FUSED_TAIL") || (aug && !edge_gather_ok)) return;
     const size_t smem = tail_smem();
     if (smem > 200 * 1024) return;
     int sms = 0, per_sm = 0, coop = 0;
@@ -612,7 +614,7 @@ struct Ctx {
     int grid = std::max(1, cdiv(nown, tail_rows));
     if (per_sm <= 0) return;
     const bool force_mr = std::getenv("FETIGPU_TAIL_MR") != nullptr;  // test hook: few blocks, several rows per thread
-    if (grid > per_sm * sms || force_mr || aug) {
+    if (grid > per_sm * sms || force_mr || aug || H.NC > 4) {
       // one row per thread does not fit a co-resident grid: up to kTailRpt rows per thread
       auto kmr = k_arnoldi_tail_mr<kTailThreads, kTailRpt>;
       const size_t smem_mr = tail_mr_smem();
