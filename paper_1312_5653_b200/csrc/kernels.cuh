@@ -923,6 +923,9 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv(S
 #ifndef FETIGPU_GEMV_PF_MODES
 #define FETIGPU_GEMV_PF_MODES 3
 #endif
+#ifndef FETIGPU_GEMV_PF_ROWS_ASIDE
+#define FETIGPU_GEMV_PF_ROWS_ASIDE 8
+#endif
   if ((FETIGPU_GEMV_PF_MODES >> MODE) & 1) {
     // the operator is solve-constant: warm L1 with the first rows of this warp's first
     // off-diagonal tile while the producer kernel drains (CTAs that become resident early)
@@ -2058,7 +2061,7 @@ __global__ void __launch_bounds__(WARPS * 32, (WARPS == 8 ? 4 : 8)) k_sym_gemv_a
     if (warp < noff) {
       const double2* O = a.pack + (size_t)blockIdx.x * sym_tile_entries(NT) + NT * 17 * 32 + (size_t)warp * 1024;
 #pragma unroll
-      for (int u = 0; u < FETIGPU_GEMV_PF_ROWS; ++u) prefetch_l1(O + u * 32 + lane);
+      for (int u = 0; u < FETIGPU_GEMV_PF_ROWS_ASIDE; ++u) prefetch_l1(O + u * 32 + lane);
     }
     // solve-constant coupling entries of this warp's corner (NB <= 128: four rows per lane)
     double2 cp[4];
