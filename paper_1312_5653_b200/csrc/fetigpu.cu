@@ -22,6 +22,7 @@
 #include <memory>
 #include <string>
 #include <thread>
+#include <map>
 #include <vector>
 
 #include "band.cuh"
@@ -169,8 +170,20 @@ struct Ctx {
   size_t l2_persist_bytes = 0;
   bool watchdog = false;
   cudaGraph_t arnoldi_graph = nullptr;
-  cudaGraphExec_t arnoldi_exec = nullptr;
+  cudaGraphExec_t arnoldi_exec = nullptr;  // WHILE-node graph (prefix 0)
   cudaGraphConditionalHandle arnoldi_handle{};
+  // Graphs with a prefix of U unconditional steps in front of the WHILE node, keyed by U: a
+  // context's solves need about the same number of steps, so the next cycle runs U = (last
+  // count + 1) steps without a conditional-node round trip every kBodyUnroll steps (steps past
+  // the end return at once) and the WHILE node only serves what is left.
+  struct PrefixGraph {
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+  };
+  std::map<int, PrefixGraph> prefix_graphs;
+  int iter_hist[2] = {0, 0};  // iterations of the last solve per factor slot (plus / minus)
+  bool use_prefix = true;     // FETIGPU_NO_PREFIX=1: WHILE node only
+  static constexpr int kMaxPrefix = 96;
   int arnoldi_body_kernels = 0;
   static constexpr int kCgsThreads = 512, kCgsRows = 256;  // k_cgs_pass block shape
   // fused Arnoldi tail (k_arnoldi_tail): rows per thread (0 = off), grid, barrier words
@@ -219,6 +232,7 @@ struct Ctx {
     if (h_gst_async) cudaFreeHost(h_gst_async);
     if (arnoldi_exec) cudaGraphExecDestroy(arnoldi_exec);
     if (arnoldi_graph) cudaGraphDestroy(arnoldi_graph);
+    drop_prefix_graphs();
     if (stream) cudaStreamDestroy(stream);
     if (copy_stream) cudaStreamDestroy(copy_stream);
 
@@ -799,6 +813,7 @@ struct Ctx {
     // FETIGPU_EAGER=1: launch the Arnoldi steps one by one instead of through the
     // conditional-node graph (ncu cannot profile kernel nodes of such graphs)
     if (const char* e = std::getenv("FETIGPU_EAGER")) use_graph = !(e[0] == '1');
+    use_prefix = !std::getenv("FETIGPU_NO_PREFIX");
     if (const char* e = std::getenv("FETIGPU_DEBUG_SYNC")) debug_sync = e[0] == '1';
     if (debug_sync) use_graph = false;
     if (const char* e = std::getenv("FETIGPU_NO_PDL")) pdl = !(e[0] == '1');
@@ -1855,6 +1870,7 @@ struct Ctx {
     regrow(d_V);
     if (d_Z != nullptr) regrow(d_Z);
     bcap = ncap;
+    drop_prefix_graphs();
     if (arnoldi_exec) {
       cudaGraphExecDestroy(arnoldi_exec);
       arnoldi_exec = nullptr;
@@ -1863,31 +1879,68 @@ struct Ctx {
       build_arnoldi_graph();
     }
   }
-  void build_arnoldi_graph() {
-    CU(cudaGraphCreate(&arnoldi_graph, 0));
-    CU(cudaGraphConditionalHandleCreate(&arnoldi_handle, arnoldi_graph, 1, cudaGraphCondAssignDefault));
+  void drop_prefix_graphs() {
+    for (auto& kv : prefix_graphs) {
+      cudaGraphExecDestroy(kv.second.exec);
+      cudaGraphDestroy(kv.second.graph);
+    }
+    prefix_graphs.clear();
+  }
+  // [prefix unconditional steps ->] WHILE node whose body holds kBodyUnroll steps
+  void build_graph(int prefix, cudaGraph_t& graph, cudaGraphExec_t& exec) {
+    CU(cudaGraphCreate(&graph, 0));
+    CU(cudaGraphConditionalHandleCreate(&arnoldi_handle, graph, 1, cudaGraphCondAssignDefault));
+    const long long before = launches;
+    const bool was_prof = prof;
+    prof = false;
+    split_givens = tail_rpt > 0 && !std::getenv("FETIGPU_NO_SPLIT");
+    std::vector<cudaGraphNode_t> deps;
+    if (prefix > 0) {
+      // the prefix's last step ends with k_givens_step, which sets the WHILE condition
+      body_unroll = prefix;
+      CU(cudaStreamBeginCaptureToGraph(stream, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+      for (int u = 0; u < prefix; ++u) arnoldi_step(true, u);
+      cudaStreamCaptureStatus status;
+      const cudaGraphNode_t* dn = nullptr;
+      size_t nd = 0;
+      CU(cudaStreamGetCaptureInfo_v2(stream, &status, nullptr, nullptr, &dn, &nd));
+      deps.assign(dn, dn + nd);
+      cudaGraph_t same = nullptr;
+      CU(cudaStreamEndCapture(stream, &same));
+    }
     cudaGraphNodeParams cp{};
     cp.type = cudaGraphNodeTypeConditional;
     cp.conditional.handle = arnoldi_handle;
     cp.conditional.type = cudaGraphCondTypeWhile;
     cp.conditional.size = 1;
     cudaGraphNode_t node;
-    CU(cudaGraphAddNode(&node, arnoldi_graph, nullptr, 0, &cp));
+    CU(cudaGraphAddNode(&node, graph, deps.empty() ? nullptr : deps.data(), deps.size(), &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
-    const long long before = launches;
-    const bool was_prof = prof;
-    prof = false;
     // the fused-tail step is three kernels that each return at once when the cycle has
     // stopped, so the body holds `body_unroll` steps (fewer WHILE-node round trips)
     body_unroll = tail_rpt > 0 ? kBodyUnroll : 1;
+    const long long before_body = launches;
     CU(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    split_givens = tail_rpt > 0 && !std::getenv("FETIGPU_NO_SPLIT");
     for (int u = 0; u < body_unroll; ++u) arnoldi_step(true, u);
     CU(cudaStreamEndCapture(stream, &body));
     prof = was_prof;
-    arnoldi_body_kernels = (int)(launches - before) / body_unroll;
+    arnoldi_body_kernels = (int)(launches - before_body) / body_unroll;
     launches = before;
-    CU(cudaGraphInstantiate(&arnoldi_exec, arnoldi_graph, 0));
+    CU(cudaGraphInstantiate(&exec, graph, 0));
+  }
+  void build_arnoldi_graph() { build_graph(0, arnoldi_graph, arnoldi_exec); }
+  // the graph for a cycle expected to need about `expect` steps (0: unknown)
+  cudaGraphExec_t cycle_graph(int expect) {
+    // (last count + 1: measured best against + 0 / 2 / 3 on targets whose counts vary by +-1)
+    const int prefix = (use_prefix && tail_rpt > 0 && expect > 0) ? std::min({expect + 1, kMaxPrefix, bcap - 1}) : 0;
+    if (prefix < 2 * kBodyUnroll) return arnoldi_exec;
+    auto it = prefix_graphs.find(prefix);
+    if (it == prefix_graphs.end()) {
+      PrefixGraph pg{};
+      build_graph(prefix, pg.graph, pg.exec);
+      it = prefix_graphs.emplace(prefix, pg).first;
+    }
+    return it->second.exec;
   }
 
   fetigpu_feti_stats gmres(const double2* b, double2* x, int sb = 0) {
@@ -1983,7 +2036,7 @@ struct Ctx {
       if (deferred) {
         // the whole first cycle, the update x += P^-1 (Q y) and the true residual are only
         // enqueued; finish_deferred() reads them after the caller's final synchronisation
-        CU(cudaGraphLaunch(arnoldi_exec, stream));
+        CU(cudaGraphLaunch(cycle_graph(iter_hist[sb / 4]), stream));
         launch(FETIGPU_K_ORTHO, [&] { k_backsub<<<1, 32, 0, stream>>>(d_gst, d_R, d_gvec, d_y); });
         cycle_update(x);
         apply_dual(x, d_w);
@@ -2004,7 +2057,7 @@ struct Ctx {
       }
       for (;;) {  // (repeats only when the cycle is continued on a larger basis, below)
       if (graph) {
-        CU(cudaGraphLaunch(arnoldi_exec, stream));
+        CU(cudaGraphLaunch(dev_cycle ? cycle_graph(iter_hist[sb / 4]) : arnoldi_exec, stream));
         CU(cudaMemcpyAsync(h_gst, d_gst, sizeof(GmresState), cudaMemcpyDeviceToHost, stream));
         if (dev_cycle) CU(cudaMemcpyAsync(h_pin + 1, d_stat + bslot, sizeof(double2), cudaMemcpyDeviceToHost, stream));
         if (watchdog) {  // debugging aid: report a stuck Arnoldi graph
@@ -2100,6 +2153,7 @@ struct Ctx {
     st.relative_residual = relres;
     st.converged = relres <= tol;
     last_gmres_steps = iterations;
+    iter_hist[sb / 4] = iterations;
     return st;
   }
 
@@ -2243,6 +2297,7 @@ struct Ctx {
     st.relative_residual = rel;
     st.converged = rel <= pd.tol;
     last_gmres_steps = g.iterations;
+    iter_hist[sb / 4] = g.iterations;
     launches += (long long)arnoldi_body_kernels * body_unroll * std::max(1, (g.iterations + body_unroll - 1) / body_unroll);
     return true;
   }

@@ -311,7 +311,8 @@ def test_nonconvergence_is_not_an_error(fetigpu, oracle_mod):
                                     "FETIGPU_COOP_REJECT", "FETIGPU_NO_FUSED_TAIL", "FETIGPU_NO_PDL",
                                     "FETIGPU_EAGER", "FETIGPU_NO_AIC", "FETIGPU_NO_STENCIL", "FETIGPU_NO_BT",
                                     "FETIGPU_NO_ASIDE", "FETIGPU_ASIDE_GIVEUP", "FETIGPU_NO_TAIL_PF", "FETIGPU_TAIL_HCS", "FETIGPU_TAIL_MR", "FETIGPU_BASIS0",
-                                    "FETIGPU_BASIS0+FETIGPU_EAGER", "FETIGPU_BASIS0+FETIGPU_NO_DEFER"])
+                                    "FETIGPU_BASIS0+FETIGPU_EAGER", "FETIGPU_BASIS0+FETIGPU_NO_DEFER", "FETIGPU_NO_PREFIX",
+                                    "FETIGPU_NO_PREFIX+FETIGPU_NO_SPLIT"])
 def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
     """Each reuse/fusion of the solve path (preconditioned basis Z, compact interior rhs,
     GEMV-free final elimination, deferred GMRES completion, Givens folded into the next
@@ -338,6 +339,33 @@ def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
         assert rel(a[k], b[k]) <= 1e-11, k
         if switch == "FETIGPU_BASIS0":  # the continued cycle is the same arithmetic
             assert np.array_equal(a[k], b[k]), k
+
+
+def test_prefix_graphs_reproduce_the_while_loop(fetigpu, monkeypatch):
+    """From its second solve on a context runs each GMRES cycle on a graph with (last iteration
+    count + 1) unconditional Arnoldi steps in front of the WHILE node.  Targets with different
+    iteration counts (phi-scaled copies and other seeds), solved in sequence on one context,
+    must equal the WHILE-only path (FETIGPU_NO_PREFIX) bit for bit."""
+    n, s, phi = 96, 6, 1e-4
+    p = fetigpu.make_seeded_problem(n, phi, seed=0)
+    targets = [fetigpu.make_seeded_problem(n, phi, seed=k).target_state for k in range(5)]
+    targets.append(np.zeros_like(targets[0]))  # zero target: 0 iterations, then a normal one again
+    targets.append(targets[1])
+
+    def run():
+        solver = fetigpu.SchurSolver(p, s, s, tol=1e-10)
+        outs = [solver.solve(t) for t in targets]
+        solver.close()
+        return outs
+
+    a = run()
+    monkeypatch.setenv("FETIGPU_NO_PREFIX", "1")
+    b = run()
+    for x, y in zip(a, b):
+        assert x["plus_stats"]["iterations"] == y["plus_stats"]["iterations"]
+        assert x["minus_stats"]["iterations"] == y["minus_stats"]["iterations"]
+        for k in ("y", "u", "lambda"):
+            assert np.array_equal(x[k], y[k]), k
 
 
 @pytest.mark.parametrize("n,s", [(36, 4), (40, 4), (66, 3)])
