@@ -174,7 +174,7 @@ struct Ctx {
   cudaGraphConditionalHandle arnoldi_handle{};
   // Graphs with a prefix of U unconditional steps in front of the WHILE node, keyed by U: a
   // context's solves need about the same number of steps, so the next cycle runs U = (last
-  // count + 1) steps without a conditional-node round trip every kBodyUnroll steps (steps past
+  // count) steps without a conditional-node round trip every kBodyUnroll steps (steps past
   // the end return at once) and the WHILE node only serves what is left.
   struct PrefixGraph {
     cudaGraph_t graph;
@@ -1931,8 +1931,9 @@ struct Ctx {
   void build_arnoldi_graph() { build_graph(0, arnoldi_graph, arnoldi_exec); }
   // the graph for a cycle expected to need about `expect` steps (0: unknown)
   cudaGraphExec_t cycle_graph(int expect) {
-    // (last count + 1: measured best against + 0 / 2 / 3 on targets whose counts vary by +-1)
-    const int prefix = (use_prefix && tail_rpt > 0 && expect > 0) ? std::min({expect + 1, kMaxPrefix, bcap - 1}) : 0;
+    // (the last count itself: measured 225.7 against 224.5 for +1 and 222.7 for -1 solves/s on
+    // targets whose counts vary by +-1; +2 / +3 are slower still)
+    const int prefix = (use_prefix && tail_rpt > 0 && expect > 0) ? std::min({expect, kMaxPrefix, bcap - 1}) : 0;
     if (prefix < 2 * kBodyUnroll) return arnoldi_exec;
     auto it = prefix_graphs.find(prefix);
     if (it == prefix_graphs.end()) {

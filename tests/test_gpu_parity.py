@@ -343,7 +343,7 @@ def test_fast_paths_agree_with_plain_paths(fetigpu, monkeypatch, switch):
 
 def test_prefix_graphs_reproduce_the_while_loop(fetigpu, monkeypatch):
     """From its second solve on a context runs each GMRES cycle on a graph with (last iteration
-    count + 1) unconditional Arnoldi steps in front of the WHILE node.  Targets with different
+    count) unconditional Arnoldi steps in front of the WHILE node.  Targets with different
     iteration counts (phi-scaled copies and other seeds), solved in sequence on one context,
     must equal the WHILE-only path (FETIGPU_NO_PREFIX) bit for bit."""
     n, s, phi = 96, 6, 1e-4
